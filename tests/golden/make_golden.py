@@ -1,0 +1,155 @@
+"""Generate the golden fixtures by running the REFERENCE itself.
+
+Run in the build container (the only place /root/reference exists):
+
+    python tests/golden/make_golden.py
+
+It imports the reference `picluster` package from /root/reference/pkg/src,
+runs it on seeded inputs and writes small .npz fixtures next to this file.
+The tests (tests/test_oracle_golden.py on CPU, tests/test_gpu_*.py on the
+B200) read only these fixtures — nothing at test time touches
+/root/reference.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import json
+import pathlib
+import sys
+
+import numpy as np
+
+HERE = pathlib.Path(__file__).resolve().parent
+REPO = HERE.parent.parent
+sys.path.insert(0, "/root/reference/pkg/src")
+sys.path.insert(0, str(REPO))
+
+import picluster as ref  # noqa: E402
+from picluster import errors as ref_errors  # noqa: E402
+from picluster import parallel as ref_parallel  # noqa: E402
+
+from paper_1604_02700_b200.datasets import gaussian_blobs  # noqa: E402
+
+TINY_EPS = 5e-324  # test_serial.py:23 — disables the stop rule
+
+
+def sha(a: np.ndarray) -> str:
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def pipeline_case(d, sigma, k, seed, forced=()):
+    labels, v, trace = ref.cluster(d, ref.GaussianRbf(sigma), ref.PicParams(k=k), seed=seed)
+    a = ref.build_affinity(d, ref.GaussianRbf(sigma))
+    deg = ref.degree(a)
+    out = dict(
+        X=d.points, truth=d.labels, sigma=sigma, k=k, seed=seed, labels=labels, v=v,
+        deltas=trace.delta_history, iterations=trace.iterations_run,
+        converged=trace.converged, deg=deg, x_sha=sha(d.points),
+    )
+    w = ref.normalize(a, deg)
+    v0 = ref.initial_vector(deg, "degree")
+    for t in forced:
+        vt, tr = ref.power_iterate(w, ref.PicParams(k=k, epsilon=TINY_EPS, max_iterations=t), v0)
+        out[f"v_T{t}"] = vt
+        out[f"deltas_T{t}"] = tr.delta_history
+    rows = np.r_[0:4, d.n // 2: d.n // 2 + 4, d.n - 4: d.n]
+    out["a_rows_idx"] = rows
+    out["a_rows"] = a[rows]
+    # the parallel backend must agree (test_parallel.py:227-237)
+    pl, pv, pt = ref_parallel.cluster(d, ref.GaussianRbf(sigma), ref.PicParams(k=k),
+                                      ref.KernelConfig(p=4), seed=seed)
+    assert np.array_equal(pl, labels) and np.max(np.abs(pv - v)) <= 1e-12
+    return out
+
+
+def main():
+    # ---- config 1: the reference's own 2-D blobs
+    d1 = ref.generate(ref.GeneratorSpec("blobs", n=1000, noise=0.3, seed=0, components=3))
+    c1 = pipeline_case(d1, 1.0, 3, 0, forced=(1, 3, 10))
+    np.savez_compressed(HERE / "config1.npz", **c1)
+
+    # ---- a small App-B d-dim case (configs 2-5 shape, CPU-sized)
+    d2 = gaussian_blobs(1500, 16, 4, seed=7)
+    c2 = pipeline_case(ref.DataSet(d2.points, d2.labels), 2.0, 4, 3, forced=(8,))
+    c2.pop("X")  # regenerated from the seed at test time; x_sha pins it
+    c2.update(gen=json.dumps(dict(n=1500, d=16, k=4, seed=7)))
+    np.savez_compressed(HERE / "gblobs_small.npz", **c2)
+
+    # ---- balanced App-B variant (H7 stress: close levels)
+    d3 = gaussian_blobs(1200, 8, 3, seed=11, sizes="balanced")
+    c3 = pipeline_case(ref.DataSet(d3.points, d3.labels), 1.4142135623730951, 3, 1, forced=(5,))
+    c3.pop("X")
+    c3.update(gen=json.dumps(dict(n=1200, d=8, k=3, seed=11, sizes="balanced")))
+    np.savez_compressed(HERE / "gblobs_balanced.npz", **c3)
+
+    # ---- 1-D k-means cases (kmeans.py:178-196)
+    rng = np.random.default_rng(2024)
+    vals, ks, seeds, offs, labs = [], [], [], [0], []
+    cases = []
+    for t in range(40):
+        n = int(rng.integers(4, 25))
+        cases.append((rng.uniform(0, 1, n), min(int(rng.integers(2, 6)), n), t))
+    for t in range(6):
+        n = int(rng.integers(100, 400))
+        cases.append((rng.uniform(-1, 1, n), int(rng.integers(2, 8)), 100 + t))
+    grp = np.concatenate([rng.normal(0, 0.05, 2500), rng.normal(1, 0.05, 2600)])
+    cases.append((grp, 2, 2))                       # > POLISH_LIMIT: no polish
+    lev = np.repeat(np.array([1e-5, 1.3e-5, 2.2e-5, 2.9e-5]), [1500, 1700, 1600, 1400])
+    lev = lev * (1 + 1e-4 * rng.standard_normal(lev.size))
+    cases.append((lev, 4, 0))                        # PIC-like levels, n > 4096
+    cases.append((np.full(6, 0.25), 2, 3))           # all equal (test_kmeans.py:19-22)
+    cases.append((np.array([0.0, 0.0, 0.0, 10.0]), 3, 1))  # excess k (test_kmeans.py:73-79)
+    cases.append((np.array([0.05, 0.05, 0.45, 0.45]), 2, 0))
+    cases.append((np.array([0.0, 0.1, 5.0, 5.1, 10.0, 10.1]), 3, 5))
+    for v, k, s in cases:
+        lab = ref.kmeans_1d(v, ref.KMeansParams(k=k, seed=s))
+        vals.append(v)
+        ks.append(k)
+        seeds.append(s)
+        labs.append(lab)
+        offs.append(offs[-1] + v.size)
+    np.savez_compressed(HERE / "kmeans.npz", values=np.concatenate(vals), labels=np.concatenate(labs),
+                        k=np.array(ks), seed=np.array(seeds), offsets=np.array(offs))
+
+    # ---- tree reduction (parallel.py:161-178) and power-iteration KATs
+    rv = [rng.uniform(-1, 1, int(m)) for m in (1, 2, 3, 7, 8, 9, 777, 1000, 4097)]
+    sums = [ref.k_reduce(v, ref.KernelConfig()) for v in rv]
+    w8 = np.random.default_rng(6).uniform(0.1, 1.0, (8, 8))
+    w8 /= w8.sum(axis=1, keepdims=True)
+    v8, t8 = ref.power_iterate(w8, ref.PicParams(k=2, epsilon=1e-6, max_iterations=30), np.full(8, 1 / 8))
+    ident_v, ident_t = ref.power_iterate(np.eye(3), ref.PicParams(k=2, epsilon=1e-8), np.full(3, 1 / 3))
+    wb = np.random.default_rng(9).uniform(0.0, 1.0, (40, 40))
+    vb = np.random.default_rng(10).uniform(0.0, 1.0, 40)
+    np.savez_compressed(
+        HERE / "kernels.npz",
+        reduce_vals=np.concatenate(rv), reduce_lens=np.array([v.size for v in rv]),
+        reduce_sums=np.array(sums),
+        w8=w8, v8=v8, d8=t8.delta_history, it8=t8.iterations_run,
+        ident_v=ident_v, ident_it=ident_t.iterations_run,
+        mul_w=wb, mul_v=vb, mul_out=ref.k_multiply(wb, vb, ref.KernelConfig(p=4)),
+    )
+
+    # ---- error behaviour (errors.py) the GPU path must reproduce
+    errs = {}
+    try:
+        ref.cluster(ref.DataSet(np.array([[0.0], [0.05], [100.0]])), ref.GaussianRbf(1.0), ref.PicParams(k=2))
+    except ref_errors.ZeroDegree as e:
+        errs["zero_degree"] = dict(points=[[0.0], [0.05], [100.0]], sigma=1.0, index=e.index)
+    bad = np.ones((5, 3))
+    bad[3, 1] = np.nan
+    bad[4, 0] = np.inf
+    try:
+        ref.cluster(ref.DataSet(bad), ref.GaussianRbf(1.0), ref.PicParams(k=2))
+    except ref_errors.NonFiniteEntry as e:
+        errs["non_finite"] = dict(row=e.row, col=e.col)
+    try:
+        ref.kmeans_1d(np.array([0.5, 0.5]), ref.KMeansParams(k=3))
+    except ref_errors.KTooLarge:
+        errs["k_too_large"] = True
+    (HERE / "errors.json").write_text(json.dumps(errs, indent=1) + "\n")
+    print("golden fixtures written to", HERE)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,114 @@
+"""Pin the CPU oracle to the reference's own outputs (tests/golden/*.npz).
+
+The fixtures were produced by tests/golden/make_golden.py running the
+reference package; these tests show the numpy restatement in oracle/
+reproduces them, so GPU-vs-oracle parity is GPU-vs-reference parity.
+"""
+
+import hashlib
+import json
+
+import numpy as np
+import pytest
+
+from oracle import pic_oracle as po
+from paper_1604_02700_b200.datasets import blobs_2d, gaussian_blobs
+
+from conftest import GOLDEN
+
+
+def _sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def _points(z):
+    if "X" in z:
+        return z["X"]
+    g = json.loads(str(z["gen"]))
+    d = gaussian_blobs(g["n"], g["d"], g["k"], seed=g["seed"], sizes=g.get("sizes", "graded"))
+    assert _sha(d.points) == str(z["x_sha"]), "App-B generator drifted from the fixture"
+    return d.points
+
+
+@pytest.mark.parametrize("case", ["config1", "gblobs_small", "gblobs_balanced"])
+def test_pipeline_matches_reference(golden, case):
+    z = golden(case)
+    x = _points(z)
+    labels, v, deltas, conv = po.pic_cluster(x, float(z["sigma"]), int(z["k"]), seed=int(z["seed"]))
+    assert np.array_equal(labels, z["labels"])
+    assert np.max(np.abs(v - z["v"])) <= 1e-12 * np.abs(z["v"]).max()
+    assert len(deltas) == int(z["iterations"]) and bool(conv) == bool(z["converged"])
+    assert np.allclose(deltas, z["deltas"], rtol=1e-9, atol=0)
+
+
+@pytest.mark.parametrize("case", ["config1", "gblobs_small"])
+def test_affinity_rows_and_degree_bitwise(golden, case):
+    z = golden(case)
+    x = _points(z)
+    idx = z["a_rows_idx"]
+    for r, row in zip(idx, z["a_rows"]):
+        assert np.array_equal(po.rbf_rows(x, int(r), int(r) + 1, float(z["sigma"]))[0], row)
+    a = po.affinity(x, float(z["sigma"]))
+    assert np.allclose(po.degree(a), z["deg"], rtol=1e-14, atol=0)
+
+
+def test_forced_iterations(golden):
+    z = golden("config1")
+    a = po.affinity(z["X"], 1.0)
+    d = po.degree(a)
+    w = po.normalize(a, d)
+    for t in (1, 3, 10):
+        v, deltas, conv = po.power_iteration(w, po.start_vector(d), 5e-324, t)
+        assert len(deltas) == t and not conv
+        assert np.max(np.abs(v - z[f"v_T{t}"])) <= 1e-15
+
+
+def test_config1_generator_matches_reference(golden):
+    z = golden("config1")
+    d = blobs_2d(1000, components=3, noise=0.3, seed=0)
+    assert np.array_equal(d.points, z["X"])
+    assert np.array_equal(d.labels, z["truth"])
+
+
+def test_kmeans_cases(golden):
+    z = golden("kmeans")
+    off = z["offsets"]
+    for i, (k, s) in enumerate(zip(z["k"], z["seed"])):
+        v = z["values"][off[i]: off[i + 1]]
+        got = po.kmeans_1d(v, int(k), int(s))
+        assert np.array_equal(got, z["labels"][off[i]: off[i + 1]]), f"case {i}"
+
+
+def test_tree_sum_and_power_kats(golden):
+    z = golden("kernels")
+    pos = 0
+    for ln, s in zip(z["reduce_lens"], z["reduce_sums"]):
+        assert po.tree_sum(z["reduce_vals"][pos: pos + ln]) == s
+        pos += ln
+    v, deltas, conv = po.power_iteration(z["w8"], np.full(8, 1 / 8), 1e-6, 30)
+    assert len(deltas) == int(z["it8"])
+    assert np.max(np.abs(v - z["v8"])) <= 1e-15
+    v, deltas, conv = po.power_iteration(np.eye(3), np.full(3, 1 / 3), 1e-8, 50)
+    assert conv and len(deltas) == int(z["ident_it"]) == 2
+    assert np.max(np.abs(po.matvec_threaded(z["mul_w"], z["mul_v"], 4) - z["mul_out"])) <= 1e-15
+
+
+def test_error_cases():
+    e = json.loads((GOLDEN / "errors.json").read_text())
+    with pytest.raises(po.OracleError) as info:
+        po.pic_cluster(np.array(e["zero_degree"]["points"]), e["zero_degree"]["sigma"], 2)
+    assert info.value.kind == "ZeroDegree" and info.value.index == e["zero_degree"]["index"]
+    bad = np.ones((5, 3))
+    bad[3, 1] = np.nan
+    bad[4, 0] = np.inf
+    with pytest.raises(po.OracleError) as info:
+        po.pic_cluster(bad, 1.0, 2)
+    assert info.value.index == (e["non_finite"]["row"], e["non_finite"]["col"])
+    with pytest.raises(po.OracleError):
+        po.kmeans_1d(np.array([0.5, 0.5]), 3)
+
+
+def test_threaded_affinity_port_is_bitwise(golden):
+    z = golden("config1")
+    rows = po.affinity_rows_threaded(z["X"], 100, 300, 1.0, p=4)
+    assert np.array_equal(rows, po.rbf_rows(z["X"], 100, 300, 1.0))
