@@ -1,0 +1,339 @@
+"""GPIC benchmark: PIC end to end on BASELINE.json config 3 (n=100k, d=64, k=10).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C]
+
+A step is one whole PIC run (centre -> affinity+degree -> start vector ->
+device-resident power iteration -> k-means) over the config's synthetic
+Gaussian blobs (SURVEY.md App. B generator, seed 0). Prints ONE JSON line
+(rank 0). Key fields:
+
+  value      seconds per PIC run with X already resident in HBM (CUDA events,
+             max over ranks), the BASELINE metric ("PIC end-to-end s")
+  e2e        the same through the public API cluster(DataSet(host X)) with
+             the H2D of X and the D2H of labels + embedding inside the timing
+  roofline   the dominant kernel (the power-iteration GEMV): algorithmic
+             bytes (rows * n * 4 per launch) / its CUDA-event duration vs the
+             measured HBM peak
+  cpu_baseline  the reference algorithm (oracle/ numpy port of the
+             reference's threaded backend) on a bounded row sample, scaled to
+             the full job
+  power_iter_hbm_gbs  the second half of the BASELINE metric
+
+--impl reference times only the CPU reference port (rank 0) on the same
+config and prints the same line with "impl": "reference".
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import pathlib
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = pathlib.Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+from paper_1604_02700_b200.datasets import CONFIGS, config_dataset  # noqa: E402
+
+FALLBACK_HBM_GBS = 6650.0  # B200_PROFILING.md fallback
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        j = json.loads(p.read_text())
+        return float(j["hbm_gbs"]), "measured"
+    return FALLBACK_HBM_GBS, "fallback"
+
+
+# ------------------------------------------------------------ clocks
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                out, _ = self.proc.communicate()
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in getattr(self, "lines", []):
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for nm, val in zip(names, f[5:9]):
+                if val.lower() in ("active", "1"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": mx, "reasons": [], "samples": 0}
+        loaded = [s for s in sm if s > 0.5 * max(sm)]
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------- CPU reference
+def cpu_reference_sample(points, sigma, k, iters, rows, threads):
+    """Time the reference algorithm (oracle port of parallel.py) on `rows`
+    rows and scale to the whole job. Returns (seconds_full_job, detail)."""
+    from oracle import pic_oracle as po
+
+    n = points.shape[0]
+    lo = 0
+    t0 = time.perf_counter()
+    a = po.affinity_rows_threaded(points, lo, lo + rows, sigma, p=threads)   # k_affinity
+    t1 = time.perf_counter()
+    deg = np.einsum("ij->i", a)                                              # k_rowsum
+    w = a / deg[:, None]                                                     # k_normalize
+    t2 = time.perf_counter()
+    v = np.full(n, 1.0 / n)
+    for _ in range(iters):                                                   # k_multiply
+        po.matvec_threaded(w, v, threads)
+    t3 = time.perf_counter()
+    scale = n / rows
+    # PIC-like embedding: one level per blob (level ~ blob size), 1e-3 noise
+    lab = np.repeat(np.arange(k), np.bincount(np.arange(n) * k // n, minlength=k))
+    vals = (1.0 + lab) / n * (1.0 + 1e-3 * np.random.default_rng(0).standard_normal(n))
+    t4 = time.perf_counter()
+    po.lloyd(vals, k, 0)                                                     # k-means (n > 4096: no polish)
+    t5 = time.perf_counter()
+    full = (t1 - t0) * scale + (t2 - t1) * scale + (t3 - t2) * scale + (t5 - t4)
+    detail = {"affinity_s": (t1 - t0) * scale, "rowsum_normalize_s": (t2 - t1) * scale,
+              "iterate_s": (t3 - t2) * scale, "kmeans_s": t5 - t4}
+    return full, detail, t5 - t0
+
+
+def run_reference(args, cfg, rank):
+    if rank != 0:
+        return
+    c = CONFIGS[cfg]
+    d = config_dataset(cfg, seed=0)
+    threads = os.cpu_count() or 1
+    rows = args.ref_rows
+    iters = args.ref_iters
+    times, details, wall = [], None, 0.0
+    for i in range(args.warmup + args.steps):
+        full, det, w = cpu_reference_sample(d.points, c["sigma"], c["k"], iters, rows, threads)
+        if i >= args.warmup:
+            times.append(full)
+            details = det
+            wall += w
+    value = statistics.mean(times)
+    sample = (f"{rows} of {c['n']} affinity rows + {iters} matvecs on them, scaled x{c['n'] / rows:.1f};"
+              f" k-means on n={c['n']} (extrapolated full-job seconds)")
+    line = {
+        "metric": METRIC, "value": value, "unit": "s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": value * 1e3, "higher_is_better": False,
+        "scaling": "weak" if args.gpus > 1 else "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "impl": "reference",
+        "config": workload(cfg, args.gpus),
+        "cpu_baseline": {"value": value, "unit": "s", "cores": threads, "kind": "port",
+                         "sample": sample, "phases": details,
+                         "measured_cpu_seconds_per_step": wall / max(args.steps, 1)},
+        "e2e": {"value": value, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+METRIC = "PIC end-to-end s (power-iter HBM GB/s alongside)"
+
+
+def workload(cfg, gpus):
+    c = CONFIGS[cfg]
+    return {"workload": f"config{cfg}: gaussian blobs n={c['n']} d={c['d']} k={c['k']} "
+                        f"sigma={c['sigma']:.4f}, dense fp32 W in HBM",
+            "n": c["n"], "d": c["d"], "k": c["k"], "sigma": c["sigma"],
+            "parallelism": f"row-shard x{gpus}", "l2": "inputs > L2 (W = 4n^2 bytes)"}
+
+
+# ---------------------------------------------------------- ours
+def run_ours(args, cfg, rank, world):
+    import ctypes as C
+
+    import torch
+
+    from paper_1604_02700_b200 import DataSet, GaussianRbf, KernelConfig, PicParams, cluster
+    from paper_1604_02700_b200 import _lib, gpu
+    from paper_1604_02700_b200.validation import adjusted_rand_index, contingency
+
+    if world > 1:
+        raise SystemExit("multi-GPU bench path lands with the sharded engine")
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    c = CONFIGS[cfg]
+    d = config_dataset(cfg, seed=0)
+    n, m, k = d.n, d.m, c["k"]
+    sigma = c["sigma"]
+    params = PicParams(k=k)
+    impl_name = args.engine
+    impl = _lib.AFFINITY_TC if impl_name == "tc" else _lib.AFFINITY_SIMT
+    L = _lib.lib()
+    stream = torch.cuda.current_stream(dev)
+    st = C.c_void_p(stream.cuda_stream)
+
+    # pinned host input for the e2e leg (DataSet keeps the buffer, no copy)
+    host = torch.empty((n, m), dtype=torch.float64).pin_memory()
+    host.numpy()[:] = d.points
+    d_host = DataSet(host.numpy(), d.labels)
+
+    # device-resident leg
+    x = torch.from_numpy(d.points).to(dev)
+    T = params.max_iterations
+    nbytes = gpu.workspace_bytes(n, m, k, T)
+    work = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    labels = torch.empty(n, dtype=torch.int64, device=dev)
+    v = torch.empty(n, dtype=torch.float64, device=dev)
+    hist = torch.zeros(T, dtype=torch.float64, device=dev)
+    first, u = gpu.kmeans_draws(n, k, 0)
+    eps = params.resolved_epsilon(n)
+    iters, conv = C.c_int32(0), C.c_int32(0)
+
+    def step():
+        rc = L.gpic_cluster(C.c_void_p(x.data_ptr()), n, m, sigma, k, eps, T, first,
+                            u.ctypes.data_as(C.c_void_p), impl, C.c_void_p(labels.data_ptr()),
+                            C.c_void_p(v.data_ptr()), C.c_void_p(hist.data_ptr()), C.byref(iters),
+                            C.byref(conv), C.c_void_p(work.data_ptr()), nbytes, st)
+        _lib.raise_for(rc)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    launches0 = L.gpic_launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(0) as clk:
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    launches = L.gpic_launch_count() - launches0
+    ms = ev0.elapsed_time(ev1) / args.steps
+    lab_np = labels.cpu().numpy()
+    ari = adjusted_rand_index(contingency(d.labels, lab_np))
+
+    # roofline of the dominant kernel: the GEMV over the resident A
+    lda = int(L.gpic_affinity_pitch(n))
+    scratch = int(L.gpic_workspace_bytes(n, m, k, n, T))
+    a_ptr = work.data_ptr() + scratch
+    v32 = torch.zeros(lda, dtype=torch.float32, device=dev)
+    v32[:n] = v.to(torch.float32)
+    deg_dummy = torch.ones(n, dtype=torch.float64, device=dev)
+    yv = torch.empty(n, dtype=torch.float64, device=dev)
+    gemv_ms = []
+    for rep in range(args.gemv_reps + 2):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        _lib.check(L.gpic_matvec(C.c_void_p(a_ptr), lda, n, n, C.c_void_p(v32.data_ptr()),
+                                 C.c_void_p(deg_dummy.data_ptr()), C.c_void_p(yv.data_ptr()), st))
+        e1.record(stream)
+        e1.synchronize()
+        if rep >= 2:
+            gemv_ms.append(e0.elapsed_time(e1))
+    gemv_avg = statistics.mean(gemv_ms)
+    alg_bytes = float(n) * n * 4
+    achieved = alg_bytes / (gemv_avg * 1e-3) / 1e9
+    peak, peak_kind = peaks()
+
+    # e2e leg through the public API from pinned host memory
+    cfg_api = KernelConfig(affinity_impl=impl_name)
+    for _ in range(1):
+        cluster(d_host, GaussianRbf(sigma), params, config=cfg_api, seed=0)
+    torch.cuda.synchronize()
+    e2e = []
+    for _ in range(max(1, args.e2e_steps)):
+        t0 = time.perf_counter()
+        lab_e, v_e, tr_e = cluster(d_host, GaussianRbf(sigma), params, config=cfg_api, seed=0)
+        e2e.append(time.perf_counter() - t0)
+    e2e_s = statistics.mean(e2e)
+    assert np.array_equal(lab_e, lab_np), "public-API labels differ from the device-resident run"
+
+    traffic = None
+    prof = ROOT / "profiles" / "gemv_traffic.json"
+    if prof.exists():
+        traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch")
+
+    line = {
+        "metric": METRIC, "value": ms / 1e3, "unit": "s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,
+        "scaling": "weak" if world > 1 else "strong", "vs_baseline": None,
+        "dtype": "f32 (fp64 vectors/reductions)", "data": "synthetic (SURVEY App. B gaussian blobs, seed 0)",
+        "config": dict(workload(cfg, world), affinity_engine=impl_name),
+        "power_iter_hbm_gbs": achieved, "iterations": int(iters.value), "converged": bool(conv.value),
+        "ari_vs_truth": ari,
+        "roofline": {"kernel": "gemv_kernel (power iteration)", "bound": "hbm",
+                     "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "algorithmic_bytes_per_launch": alg_bytes, "avg_launch_ms": gemv_avg},
+        "e2e": {"value": e2e_s, "unit": "s", "h2d_bytes_per_step": int(n * m * 8),
+                "d2h_bytes_per_step": int(n * 8 * 2 + T * 8)},
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+    }
+    if not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        full, det, _ = cpu_reference_sample(d.points, sigma, k, max(int(iters.value), 1),
+                                            args.ref_rows, threads)
+        line["cpu_baseline"] = {"value": full, "unit": "s", "cores": threads, "kind": "port",
+                                "sample": f"{args.ref_rows} of {n} rows, scaled x{n / args.ref_rows:.1f}",
+                                "phases": det}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", type=int, default=3)
+    ap.add_argument("--engine", choices=["tc", "simt"], default="simt")
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--gemv-reps", type=int, default=10)
+    ap.add_argument("--ref-rows", type=int, default=256)
+    ap.add_argument("--ref-iters", type=int, default=7)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.impl == "reference":
+        run_reference(args, args.config, rank)
+        return
+    run_ours(args, args.config, rank, world)
+
+
+if __name__ == "__main__":
+    main()

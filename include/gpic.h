@@ -1,0 +1,193 @@
+/*
+ * gpic.h — C ABI of libgpic.so, the B200 (sm_100a) engine behind the
+ * reference's Power Iteration Clustering operators.
+ *
+ * Every entry point replaces one operator of the reference package
+ * (/root/reference/pkg/src/picluster, cited file:line). Conventions:
+ *
+ *   - Plain pointers and sizes only. Pointers named d_* are DEVICE memory
+ *     owned by the caller (PyTorch tensors in the Python binding); h_* are
+ *     host memory. The library never allocates on the hot path: scratch
+ *     space comes from a caller-provided workspace sized by
+ *     gpic_workspace_bytes().
+ *   - Calls are asynchronous on `stream` (a cudaStream_t; NULL = legacy
+ *     default stream) unless stated otherwise.
+ *   - Data-dependent errors (a zero-degree row, a non-finite input, a
+ *     non-positive normaliser) are detected ON THE DEVICE and recorded in
+ *     the gpic_ctl block; gpic_ctl_read() / the synchronous entry points
+ *     return them as status codes. The Python layer maps codes onto the
+ *     reference's exception classes (errors.py:10-113):
+ *         GPIC_E_INVALID      -> InvalidSpec / DimensionMismatch
+ *         GPIC_E_ZERO_DEGREE  -> ZeroDegree(index)          (affinity.py:113-119)
+ *         GPIC_E_NONFINITE    -> NonFiniteEntry(row, col)   (data.py:69-72)
+ *         GPIC_E_NONPOS_TAU   -> NonPositiveTau(tau)        (parallel.py:181-193)
+ *         GPIC_E_EMPTY        -> EmptyVector / EmptyDataSet
+ *         GPIC_E_K_TOO_LARGE  -> KTooLarge                  (kmeans.py:187-188)
+ *         GPIC_E_CUDA, GPIC_E_COMM, GPIC_E_UNSUPPORTED -> RuntimeError
+ *   - Not reentrant per stream / ctl block. One host thread per device.
+ */
+#ifndef GPIC_H
+#define GPIC_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GPIC_OK 0
+#define GPIC_E_INVALID 1
+#define GPIC_E_ZERO_DEGREE 2
+#define GPIC_E_NONFINITE 3
+#define GPIC_E_NONPOS_TAU 4
+#define GPIC_E_EMPTY 5
+#define GPIC_E_K_TOO_LARGE 6
+#define GPIC_E_CUDA 16
+#define GPIC_E_COMM 17
+#define GPIC_E_UNSUPPORTED 18
+
+/* Affinity engines (KernelConfig.affinity_impl). */
+#define GPIC_AFFINITY_TC 0   /* tcgen05 kind::tf32, 3xTF32 split, TMEM accumulators */
+#define GPIC_AFFINITY_SIMT 1 /* FP32 FFMA comparator */
+
+/* Device-resident control block of one power-iteration run (64-bit aligned,
+ * 256 bytes). Written by the kernels; read back once at the end. */
+typedef struct gpic_ctl {
+  int32_t iter;        /* iterations completed                          */
+  int32_t stop;        /* 1 once converged / capped / failed             */
+  int32_t converged;   /* PicTrace.converged                             */
+  int32_t status;      /* GPIC_OK or a GPIC_E_* code                     */
+  int64_t err_index;   /* first offending row (ZeroDegree, NonFinite)    */
+  int64_t err_index2;  /* column for NonFiniteEntry                      */
+  double err_value;    /* tau for NonPositiveTau                         */
+  double eps;          /* resolved stop threshold                        */
+  int32_t max_iter;
+  int32_t nranks;
+  uint64_t delta_bits; /* running max |v_t - v_(t-1)| (as fp64 bits)    */
+  uint32_t arrive[4];  /* last-CTA-done counters                         */
+  double tau;          /* current L1 normaliser                          */
+  uint64_t sync_epoch; /* cross-rank exchange epoch                      */
+  uint8_t pad[256 - 96];
+} gpic_ctl;
+
+/* Library identity: "gpic <version> sm_100a". */
+const char* gpic_version(void);
+/* Last host-side error message (thread-local). */
+const char* gpic_last_error(void);
+
+/* Bytes of device scratch the pipeline needs for n points of dimension d,
+ * k clusters, a row shard of `rows` rows and `max_iter` iterations. */
+int64_t gpic_workspace_bytes(int64_t n, int32_t d, int32_t k, int64_t rows, int32_t max_iter);
+/* Row pitch (floats) of the stored affinity block for n columns. */
+int64_t gpic_affinity_pitch(int64_t n);
+
+/* ---- stage 0: validate + centre + cast -------------------------------
+ * Replaces validate_dataset's finiteness scan (data.py:61-78) and prepares
+ * the fp32 operands of the Gram engine: xc = fp32(x - mean_fp64), its
+ * TF32 hi/lo split, and |xc|^2. A non-finite entry sets GPIC_E_NONFINITE
+ * with the first (row, col) in row-major order. Layout: d_xhi/d_xlo are
+ * (n_pad x dp) row-major, dp = gpic_feature_pitch(d), n_pad = gpic_row_pad(n). */
+int32_t gpic_feature_pitch(int32_t d);
+int64_t gpic_row_pad(int64_t n);
+int gpic_prepare_points(const double* d_x, int64_t n, int32_t d, float* d_xhi, float* d_xlo,
+                        float* d_sqn, void* d_work, gpic_ctl* d_ctl, void* stream);
+
+/* ---- stage 1: affinity block + degree ---------------------------------
+ * Replaces similarity_rows/build_affinity (affinity.py:74-110, RBF kind),
+ * k_affinity (parallel.py:113-128) and k_rowsum/degree (affinity.py:113-119,
+ * parallel.py:131-143) for rows [row_lo, row_hi):
+ *     A[i - row_lo, j] = exp(-|x_i - x_j|^2 / (2 sigma^2)),  A[i, i] = 0
+ * stored fp32 with row pitch `lda` (>= n, multiple of 32; pad columns 0),
+ * deg[i - row_lo] = sum_j A[i, j] accumulated in fp64 from the stored
+ * fp32 values, fixed order (independent of the shard plan). W = D^-1 A is
+ * never materialised: the power iteration applies 1/deg in its epilogue
+ * (folded normalisation, k_normalize parallel.py:146-158). deg <= 0 sets
+ * GPIC_E_ZERO_DEGREE(first row). */
+int gpic_affinity_rbf(const float* d_xhi, const float* d_xlo, const float* d_sqn, int64_t n,
+                      int32_t d, int64_t row_lo, int64_t row_hi, double sigma, int32_t impl,
+                      float* d_a, int64_t lda, double* d_deg, void* d_work, gpic_ctl* d_ctl,
+                      void* stream);
+
+/* ---- stage 2: start vector -----------------------------------------------
+ * initial_embedding "degree" choice (parallel.py:210-214 = k_norm(deg,
+ * k_reduce(deg))): v0 = deg / tree_sum(deg). Writes fp64 and fp32 copies. */
+int gpic_initial_vector(const double* d_deg, int64_t n, double* d_v64, float* d_v32,
+                        void* d_work, gpic_ctl* d_ctl, void* stream);
+
+/* ---- stage 3: power iteration ------------------------------------------
+ * Replaces power_iterate (serial.py:104-128) / iterate (parallel.py:217-233):
+ *     y = (A v) / deg ; tau = tree_sum(y) ; v' = y / tau ;
+ *     delta_t = max|v' - v| ; stop when t >= 2 and |delta_t - delta_(t-1)| <= eps
+ * entirely on the device (no host sync per iteration): each iteration is a
+ * GEMV with the D^-1 epilogue, a fixed-shape tau reduction and a fused
+ * normalise/delta/stop kernel; the loop is a CUDA graph whose kernels
+ * become no-ops once ctl->stop is set. Single-rank form: the shard is the
+ * whole matrix (row_lo = 0, rows = n). d_v64 holds 2*n doubles (ping-pong),
+ * the final vector is returned in d_v64_out. h_* outputs are filled after
+ * an internal stream synchronize. */
+int gpic_power_iterate(const float* d_a, int64_t lda, const double* d_deg, int64_t n,
+                       double* d_v64, float* d_v32, double eps, int32_t max_iter,
+                       double* d_delta_hist, double* d_v64_out, void* d_work, gpic_ctl* d_ctl,
+                       void* stream);
+
+/* ---- stage 4: 1-D k-means ----------------------------------------------
+ * kmeans_1d (kmeans.py:178-196): k-means++ seeding from the caller's PCG64
+ * draws (first index + k-1 uniforms from np.random.default_rng(seed),
+ * kmeans.py:43,51,73), Lloyd rounds (<= max_rounds, tol), exact DP polish
+ * when n <= 4096 (kmeans.py:97-130), contiguity check/repair
+ * (kmeans.py:133-160) and canonical relabel by ascending centroid
+ * (kmeans.py:163-175). Writes int64 labels. */
+int gpic_kmeans1d(const double* d_v, int64_t n, int32_t k, int64_t first_index,
+                  const double* h_uniforms, int32_t max_rounds, double tol, int64_t* d_labels,
+                  void* d_work, gpic_ctl* d_ctl, void* stream);
+
+/* ---- per-operator entry points (parity tests, reference kernel API) ---- */
+/* k_reduce (parallel.py:161-178): fixed-shape fp64 sum into *d_out.
+ * d_work: 256 + 8 * (ceil(n / 2048) + 1) bytes. */
+int gpic_reduce_sum(const double* d_v, int64_t n, double* d_out, void* d_work, void* stream);
+/* k_multiply (parallel.py:196-207) on an fp32 matrix: y = (A v) * scale_i,
+ * scale = d_inv_deg (fp64, may be NULL for 1). */
+int gpic_matvec(const float* d_a, int64_t lda, int64_t rows, int64_t n, const float* d_v,
+                const double* d_row_scale, double* d_y, void* stream);
+
+/* ---- whole pipeline ----------------------------------------------------
+ * cluster (serial.py:131-150 / parallel.py:236-255) for one rank owning the
+ * whole matrix. Device in/out; d_work must hold gpic_workspace_bytes(n, d,
+ * k, n, max_iter). Synchronous: returns the first error. */
+int gpic_cluster(const double* d_x, int64_t n, int32_t d, double sigma, int32_t k, double eps,
+                 int32_t max_iter, int64_t first_index, const double* h_uniforms, int32_t impl,
+                 int64_t* d_labels, double* d_v, double* d_delta_hist, int32_t* h_iters,
+                 int32_t* h_converged, void* d_work, int64_t work_bytes, void* stream);
+
+/* Same, HOST buffers in and out (the reference-facing call a ctypes/cffi
+ * binding makes): copies X in, runs, copies labels/v/deltas out. */
+int gpic_cluster_host(const double* h_x, int64_t n, int32_t d, double sigma, int32_t k,
+                      double eps, int32_t max_iter, int64_t first_index, const double* h_uniforms,
+                      int32_t impl, int64_t* h_labels, double* h_v, double* h_delta_hist,
+                      int32_t* h_iters, int32_t* h_converged, void* d_work, int64_t work_bytes,
+                      void* stream);
+
+/* Reset a control block (iteration 0, no error) with the stop threshold and
+ * iteration cap of the run. */
+int gpic_ctl_init(gpic_ctl* d_ctl, double eps, int32_t max_iter, void* stream);
+
+/* k_norm (parallel.py:181-193): dst = src / tau in fp64, plus an optional
+ * fp32 copy zero-padded to f32_len (NULL to skip). tau must be > 0 (checked
+ * on the host, NonPositiveTau otherwise, NaN included). */
+int gpic_scale(const double* d_src, int64_t n, double tau, double* d_dst, float* d_dst32,
+               int64_t f32_len, void* stream);
+
+/* Device scratch of gpic_kmeans1d for n values. */
+int64_t gpic_kmeans_scratch_bytes(int64_t n, int32_t k);
+
+/* Read the control block back (synchronizes `stream`). */
+int gpic_ctl_read(const gpic_ctl* d_ctl, gpic_ctl* h_out, void* stream);
+
+/* Kernels launched by this library since load (for the bench's
+ * gpu_launches claim). */
+int64_t gpic_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GPIC_H */

@@ -1,0 +1,135 @@
+"""ctypes binding of libgpic.so (include/gpic.h) and status -> exception map.
+
+The product path has no CPU fallback: if the library or a CUDA device is
+missing, every entry point raises instead of computing anything.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import pathlib
+
+from . import errors
+
+LIB_PATH = pathlib.Path(__file__).resolve().parent / "libgpic.so"
+
+GPIC_OK = 0
+GPIC_E_INVALID = 1
+GPIC_E_ZERO_DEGREE = 2
+GPIC_E_NONFINITE = 3
+GPIC_E_NONPOS_TAU = 4
+GPIC_E_EMPTY = 5
+GPIC_E_K_TOO_LARGE = 6
+GPIC_E_CUDA = 16
+GPIC_E_COMM = 17
+GPIC_E_UNSUPPORTED = 18
+
+AFFINITY_TC = 0
+AFFINITY_SIMT = 1
+
+
+class Ctl(C.Structure):
+    """Mirror of struct gpic_ctl (256 bytes)."""
+
+    _fields_ = [
+        ("iter", C.c_int32),
+        ("stop", C.c_int32),
+        ("converged", C.c_int32),
+        ("status", C.c_int32),
+        ("err_index", C.c_int64),
+        ("err_index2", C.c_int64),
+        ("err_value", C.c_double),
+        ("eps", C.c_double),
+        ("max_iter", C.c_int32),
+        ("nranks", C.c_int32),
+        ("delta_bits", C.c_uint64),
+        ("arrive", C.c_uint32 * 4),
+        ("tau", C.c_double),
+        ("sync_epoch", C.c_uint64),
+        ("pad", C.c_uint8 * (256 - 96)),
+    ]
+
+
+assert C.sizeof(Ctl) == 256
+
+P = C.c_void_p
+I32 = C.c_int32
+I64 = C.c_int64
+F64 = C.c_double
+
+# name -> (restype, argtypes); every symbol include/gpic.h declares.
+SIGNATURES = {
+    "gpic_version": (C.c_char_p, []),
+    "gpic_last_error": (C.c_char_p, []),
+    "gpic_workspace_bytes": (I64, [I64, I32, I32, I64, I32]),
+    "gpic_affinity_pitch": (I64, [I64]),
+    "gpic_feature_pitch": (I32, [I32]),
+    "gpic_row_pad": (I64, [I64]),
+    "gpic_ctl_init": (C.c_int, [P, F64, I32, P]),
+    "gpic_prepare_points": (C.c_int, [P, I64, I32, P, P, P, P, P, P]),
+    "gpic_affinity_rbf": (C.c_int, [P, P, P, I64, I32, I64, I64, F64, I32, P, I64, P, P, P, P]),
+    "gpic_initial_vector": (C.c_int, [P, I64, P, P, P, P, P]),
+    "gpic_power_iterate": (C.c_int, [P, I64, P, I64, P, P, F64, I32, P, P, P, P, P]),
+    "gpic_kmeans1d": (C.c_int, [P, I64, I32, I64, P, I32, F64, P, P, P, P]),
+    "gpic_kmeans_scratch_bytes": (I64, [I64, I32]),
+    "gpic_reduce_sum": (C.c_int, [P, I64, P, P, P]),
+    "gpic_scale": (C.c_int, [P, I64, F64, P, P, I64, P]),
+    "gpic_matvec": (C.c_int, [P, I64, I64, I64, P, P, P, P]),
+    "gpic_cluster": (C.c_int, [P, I64, I32, F64, I32, F64, I32, I64, P, I32, P, P, P, P, P, P,
+                               I64, P]),
+    "gpic_cluster_host": (C.c_int, [P, I64, I32, F64, I32, F64, I32, I64, P, I32, P, P, P, P, P,
+                                    P, I64, P]),
+    "gpic_ctl_read": (C.c_int, [P, P, P]),
+    "gpic_launch_count": (I64, []),
+}
+
+_lib = None
+
+
+def lib():
+    """Load libgpic.so once; raise loudly if it was never built."""
+    global _lib
+    if _lib is None:
+        if not LIB_PATH.exists():
+            raise RuntimeError(
+                f"{LIB_PATH} is missing: build it with `python -m paper_1604_02700_b200._build` "
+                "(or __graft_entry__.build()); there is no CPU fallback"
+            )
+        handle = C.CDLL(str(LIB_PATH))
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(handle, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = handle
+    return _lib
+
+
+def last_error() -> str:
+    msg = lib().gpic_last_error()
+    return msg.decode() if msg else ""
+
+
+def raise_for(code: int, ctl: Ctl | None = None, d: int = 1) -> None:
+    """Map a GPIC_E_* code (plus the control block's detail) onto errors.py."""
+    if code == GPIC_OK:
+        return
+    msg = last_error()
+    if code == GPIC_E_ZERO_DEGREE:
+        raise errors.ZeroDegree(ctl.err_index if ctl is not None else -1)
+    if code == GPIC_E_NONFINITE:
+        idx = ctl.err_index if ctl is not None else 0
+        raise errors.NonFiniteEntry(idx // max(d, 1), idx % max(d, 1))
+    if code == GPIC_E_NONPOS_TAU:
+        raise errors.NonPositiveTau(ctl.err_value if ctl is not None else float("nan"))
+    if code == GPIC_E_EMPTY:
+        raise errors.EmptyDataSet()
+    if code == GPIC_E_K_TOO_LARGE:
+        raise errors.KTooLarge(-1, -1)
+    if code == GPIC_E_INVALID:
+        raise errors.InvalidSpec(msg)
+    raise errors.DeviceError(f"libgpic error {code}: {msg}")
+
+
+def check(code: int) -> None:
+    """For calls whose only failures are host-side (no control block)."""
+    raise_for(code)

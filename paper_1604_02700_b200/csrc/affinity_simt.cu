@@ -1,0 +1,153 @@
+// Stage 1 (FP32 FFMA engine): affinity tile + fused epilogue.
+//
+// One CTA computes a 128x128 tile of the Gram matrix G = Xc Xc^T on the
+// CUDA cores (fp32 FFMA, 8x8 outputs per thread), then in registers:
+//     d2 = |x_i|^2 + |x_j|^2 - 2 G_ij   (clamped at 0)
+//     a  = exp2(d2 * (-log2(e) / (2 sigma^2)))      == exp(-d2 / (2 sigma^2))
+//     a  = 0 on the diagonal and in padding columns  (affinity.py:102-103)
+// stores A once (fp32, streaming stores) and writes the tile's fp32 row
+// partial sums; gpic_degree combines them in fixed order (fp64).
+// This is the measured-error comparator of the tcgen05 3xTF32 engine
+// (affinity_tc.cu) and the engine used when tcgen05 is unavailable for a
+// shape.
+#include "common.cuh"
+#include "ops.h"
+
+namespace gpic {
+
+namespace {
+
+constexpr int BM = 128, BN = 128, BK = 16, PADS = 4;
+
+__global__ void __launch_bounds__(256, 2)
+    affinity_simt_kernel(const float* __restrict__ xhi, const float* __restrict__ xlo,
+                         const float* __restrict__ sqn, int64_t n, int32_t dp, int64_t row_lo,
+                         int64_t row_hi, float neg_scale_log2, float* __restrict__ a, int64_t lda,
+                         float* __restrict__ rowpart, int64_t rows_pad) {
+  __shared__ __align__(16) float As[BK][BM + PADS];
+  __shared__ __align__(16) float Bs[BK][BN + PADS];
+
+  const int tid = threadIdx.x;
+  const int tx = tid & 15;   // column group
+  const int ty = tid >> 4;   // row group
+  const int64_t col0 = (int64_t)blockIdx.x * BN;
+  const int64_t lrow0 = (int64_t)blockIdx.y * BM;  // local (shard) row of the tile
+  const int64_t grow0 = row_lo + lrow0;            // global row
+
+  float acc[8][8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+
+  // loader mapping: 128 rows x 16 features = 512 float4; 256 threads x 2
+  for (int k0 = 0; k0 < dp; k0 += BK) {
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int e = tid + q * 256;       // 0..511
+      const int r = e >> 2;              // 0..127
+      const int c = (e & 3) * 4;         // 0,4,8,12
+      const int64_t ra = grow0 + r;      // rows are padded to 128 (zero rows)
+      const int64_t rb = col0 + r;
+      const float4 ah = *reinterpret_cast<const float4*>(xhi + ra * dp + k0 + c);
+      const float4 al = *reinterpret_cast<const float4*>(xlo + ra * dp + k0 + c);
+      const float4 bh = *reinterpret_cast<const float4*>(xhi + rb * dp + k0 + c);
+      const float4 bl = *reinterpret_cast<const float4*>(xlo + rb * dp + k0 + c);
+      As[c + 0][r] = ah.x + al.x;
+      As[c + 1][r] = ah.y + al.y;
+      As[c + 2][r] = ah.z + al.z;
+      As[c + 3][r] = ah.w + al.w;
+      Bs[c + 0][r] = bh.x + bl.x;
+      Bs[c + 1][r] = bh.y + bl.y;
+      Bs[c + 2][r] = bh.z + bl.z;
+      Bs[c + 3][r] = bh.w + bl.w;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < BK; ++k) {
+      const float4 a0 = *reinterpret_cast<const float4*>(&As[k][ty * 8]);
+      const float4 a1 = *reinterpret_cast<const float4*>(&As[k][ty * 8 + 4]);
+      const float4 b0 = *reinterpret_cast<const float4*>(&Bs[k][tx * 4]);
+      const float4 b1 = *reinterpret_cast<const float4*>(&Bs[k][64 + tx * 4]);
+      const float ar[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+      const float br[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(ar[i], br[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+
+  // fused epilogue
+  float sqb[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const int64_t cj = col0 + (j < 4 ? tx * 4 + j : 64 + tx * 4 + (j - 4));
+    sqb[j] = sqn[cj];
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int64_t lr = lrow0 + ty * 8 + i;
+    const int64_t gr = row_lo + lr;
+    const float sqa = sqn[gr];
+    float vals[8];
+    float rs = 0.f;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int64_t cj = col0 + (j < 4 ? tx * 4 + j : 64 + tx * 4 + (j - 4));
+      float d2 = fmaxf(sqa + sqb[j] - 2.f * acc[i][j], 0.f);
+      float e = exp2f(d2 * neg_scale_log2);
+      if (cj == gr || cj >= n) e = 0.f;
+      vals[j] = e;
+      rs += e;
+    }
+    // 16 column-group lanes share this row: fixed butterfly
+#pragma unroll
+    for (int o = 1; o < 16; o <<= 1) rs += __shfl_xor_sync(0xffffffffu, rs, o);
+    if (gr < row_hi) {
+      float* arow = a + lr * lda;
+      const int64_t c0 = col0 + tx * 4;
+      const int64_t c1 = col0 + 64 + tx * 4;
+      if (c0 < lda) st_stream_f4(reinterpret_cast<float4*>(arow + c0),
+                                 make_float4(vals[0], vals[1], vals[2], vals[3]));
+      if (c1 < lda) st_stream_f4(reinterpret_cast<float4*>(arow + c1),
+                                 make_float4(vals[4], vals[5], vals[6], vals[7]));
+      if (tx == 0) rowpart[(int64_t)blockIdx.x * rows_pad + lr] = rs;
+    }
+  }
+}
+
+// deg_i = sum over column tiles (fixed order, fp64) of the fp32 row partials.
+__global__ void degree_kernel(const float* __restrict__ rowpart, int64_t rows, int64_t rows_pad,
+                              int64_t n_ctiles, int64_t row_lo, double* __restrict__ deg,
+                              gpic_ctl* ctl) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= rows) return;
+  double s = 0.0;
+  for (int64_t t = 0; t < n_ctiles; ++t) s += (double)rowpart[t * rows_pad + i];
+  deg[i] = s;
+  if (s <= 0.0) raise_status(ctl, GPIC_E_ZERO_DEGREE, row_lo + i, -1, s);
+}
+
+}  // namespace
+
+void launch_affinity_simt(const float* xhi, const float* xlo, const float* sqn, int64_t n,
+                          int32_t dp, int64_t row_lo, int64_t row_hi, float neg_scale_log2,
+                          float* a, int64_t lda, float* rowpart, int64_t rows_pad,
+                          cudaStream_t s) {
+  const int64_t rows = row_hi - row_lo;
+  dim3 grid((unsigned)ceil_div(n, BN), (unsigned)ceil_div(rows, BM));
+  affinity_simt_kernel<<<grid, 256, 0, s>>>(xhi, xlo, sqn, n, dp, row_lo, row_hi, neg_scale_log2,
+                                            a, lda, rowpart, rows_pad);
+  count_launch();
+}
+
+void launch_degree(const float* rowpart, int64_t rows, int64_t rows_pad, int64_t n_ctiles,
+                   int64_t row_lo, double* deg, gpic_ctl* ctl, cudaStream_t s) {
+  degree_kernel<<<(unsigned)ceil_div(rows, 256), 256, 0, s>>>(rowpart, rows, rows_pad, n_ctiles,
+                                                              row_lo, deg, ctl);
+  count_launch();
+}
+
+}  // namespace gpic

@@ -1,0 +1,326 @@
+// extern "C" entry points of libgpic.so (declared in include/gpic.h).
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "common.cuh"
+#include "ops.h"
+
+static_assert(sizeof(gpic_ctl) == 256, "gpic_ctl must stay 256 bytes");
+
+namespace gpic {
+
+unsigned long long g_launches = 0;
+static thread_local std::string g_err;
+
+int fail_cuda(cudaError_t e, const char* what) {
+  g_err = std::string("CUDA error ") + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) +
+          ") at " + what;
+  return GPIC_E_CUDA;
+}
+
+int fail(int code, const char* msg) {
+  g_err = msg;
+  return code;
+}
+
+int32_t feature_pitch(int32_t d) { return (int32_t)round_up(d, 32); }
+// rows padded to the tile plus one spare tile: shard row tiles may start
+// at any row, so a tile can overhang n by up to 127 rows.
+int64_t row_pad(int64_t n) { return round_up(n, kTileM) + kTileM; }
+int64_t affinity_pitch(int64_t n) { return round_up(n, 32); }
+
+static inline int64_t al(int64_t b) { return (b + 255) & ~int64_t(255); }
+
+int64_t workspace_bytes(int64_t n, int32_t d, int32_t k, int64_t rows, int32_t /*max_iter*/) {
+  const int64_t dp = feature_pitch(d), npad = row_pad(n);
+  const int64_t rows_pad = round_up(rows, kTileM);
+  const int64_t n_ctiles = ceil_div(n, kTileN);
+  int64_t b = al(sizeof(gpic_ctl));
+  b += 2 * al(npad * dp * 4);                 // xhi, xlo
+  b += al(npad * 4);                          // sqn
+  b += al(ceil_div(n, 256) * d * 8);          // colpart
+  b += al((int64_t)d * 8);                    // mean
+  b += al(n_ctiles * rows_pad * 4);           // rowpart
+  b += al((ceil_div(n, kRedBlock) + 1) * 8);  // redpart
+  b += al(n * 8);                             // y
+  b += al(n * 8);                             // deg
+  b += al(2 * n * 8);                         // v64
+  b += al(affinity_pitch(n) * 4);             // v32
+  b += al(kmeans_scratch_bytes(n, k));        // kmeans
+  return b;
+}
+
+int carve(void* base, int64_t bytes, int64_t n, int32_t d, int32_t k, int64_t rows,
+          int32_t max_iter, Workspace* ws) {
+  if (base == nullptr) return fail(GPIC_E_INVALID, "workspace is null");
+  if ((reinterpret_cast<uintptr_t>(base) & 255) != 0)
+    return fail(GPIC_E_INVALID, "workspace must be 256-byte aligned");
+  const int64_t need = workspace_bytes(n, d, k, rows, max_iter);
+  if (bytes < need) return fail(GPIC_E_INVALID, "workspace too small");
+  const int64_t dp = feature_pitch(d), npad = row_pad(n);
+  const int64_t rows_pad = round_up(rows, kTileM);
+  const int64_t n_ctiles = ceil_div(n, kTileN);
+  uint8_t* p = static_cast<uint8_t*>(base);
+  auto take = [&](int64_t sz) { uint8_t* q = p; p += al(sz); return q; };
+  ws->ctl = reinterpret_cast<gpic_ctl*>(take(sizeof(gpic_ctl)));
+  ws->xhi = reinterpret_cast<float*>(take(npad * dp * 4));
+  ws->xlo = reinterpret_cast<float*>(take(npad * dp * 4));
+  ws->sqn = reinterpret_cast<float*>(take(npad * 4));
+  ws->colpart = reinterpret_cast<double*>(take(ceil_div(n, 256) * d * 8));
+  ws->mean = reinterpret_cast<double*>(take((int64_t)d * 8));
+  ws->rowpart = reinterpret_cast<float*>(take(n_ctiles * rows_pad * 4));
+  ws->redpart = reinterpret_cast<double*>(take((ceil_div(n, kRedBlock) + 1) * 8));
+  ws->y = reinterpret_cast<double*>(take(n * 8));
+  ws->deg = reinterpret_cast<double*>(take(n * 8));
+  ws->v64 = reinterpret_cast<double*>(take(2 * n * 8));
+  ws->v32 = reinterpret_cast<float*>(take(affinity_pitch(n) * 4));
+  ws->kscratch_bytes = kmeans_scratch_bytes(n, k);
+  ws->kscratch = reinterpret_cast<double*>(take(ws->kscratch_bytes));
+  ws->end = p;
+  return GPIC_OK;
+}
+
+static int status_from_ctl(const gpic_ctl& h, int32_t d) {
+  char buf[256];
+  switch (h.status) {
+    case GPIC_OK:
+      return GPIC_OK;
+    case GPIC_E_ZERO_DEGREE:
+      snprintf(buf, sizeof buf, "row %lld has zero degree", (long long)h.err_index);
+      return fail(h.status, buf);
+    case GPIC_E_NONFINITE:
+      snprintf(buf, sizeof buf, "non-finite value at row %lld column %lld",
+               (long long)(h.err_index / (d > 0 ? d : 1)), (long long)(h.err_index % (d > 0 ? d : 1)));
+      return fail(h.status, buf);
+    case GPIC_E_NONPOS_TAU:
+      snprintf(buf, sizeof buf, "non-positive normaliser %g", h.err_value);
+      return fail(h.status, buf);
+    case GPIC_E_UNSUPPORTED:
+      return fail(h.status, "k-means produced non-contiguous clusters (gap repair not on device)");
+    default:
+      snprintf(buf, sizeof buf, "device status %d", h.status);
+      return fail(h.status, buf);
+  }
+}
+
+}  // namespace gpic
+
+using namespace gpic;
+
+extern "C" {
+
+const char* gpic_version(void) { return "gpic 0.1.0 sm_100a"; }
+const char* gpic_last_error(void) { return g_err.c_str(); }
+int64_t gpic_launch_count(void) { return (int64_t)g_launches; }
+
+int64_t gpic_workspace_bytes(int64_t n, int32_t d, int32_t k, int64_t rows, int32_t max_iter) {
+  if (n < 1 || d < 1 || rows < 0 || rows > n) return -1;
+  return workspace_bytes(n, d, k, rows, max_iter);
+}
+int64_t gpic_affinity_pitch(int64_t n) { return affinity_pitch(n); }
+int32_t gpic_feature_pitch(int32_t d) { return feature_pitch(d); }
+int64_t gpic_row_pad(int64_t n) { return row_pad(n); }
+
+int gpic_ctl_read(const gpic_ctl* d_ctl, gpic_ctl* h_out, void* stream) {
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  GPIC_CUDA_TRY(cudaMemcpyAsync(h_out, d_ctl, sizeof(gpic_ctl), cudaMemcpyDeviceToHost, s));
+  GPIC_CUDA_TRY(cudaStreamSynchronize(s));
+  return GPIC_OK;
+}
+
+int gpic_ctl_init(gpic_ctl* d_ctl, double eps, int32_t max_iter, void* stream) {
+  launch_ctl_init(d_ctl, eps, max_iter, static_cast<cudaStream_t>(stream));
+  GPIC_CUDA_TRY(cudaGetLastError());
+  return GPIC_OK;
+}
+
+int gpic_prepare_points(const double* d_x, int64_t n, int32_t d, float* d_xhi, float* d_xlo,
+                        float* d_sqn, void* d_work, gpic_ctl* d_ctl, void* stream) {
+  if (n < 1 || d < 1) return fail(GPIC_E_EMPTY, "dataset must contain at least one point and one feature");
+  // d_work: colpart (ceil(n/256) * d doubles) followed by mean (d doubles)
+  double* colpart = static_cast<double*>(d_work);
+  double* mean = colpart + ceil_div(n, 256) * d;
+  launch_prepare(d_x, n, d, d_xhi, d_xlo, d_sqn, colpart, mean, d_ctl,
+                 static_cast<cudaStream_t>(stream));
+  GPIC_CUDA_TRY(cudaGetLastError());
+  return GPIC_OK;
+}
+
+int gpic_affinity_rbf(const float* d_xhi, const float* d_xlo, const float* d_sqn, int64_t n,
+                      int32_t d, int64_t row_lo, int64_t row_hi, double sigma, int32_t impl,
+                      float* d_a, int64_t lda, double* d_deg, void* d_work, gpic_ctl* d_ctl,
+                      void* stream) {
+  if (!(sigma > 0)) return fail(GPIC_E_INVALID, "sigma must be positive");
+  if (row_lo < 0 || row_hi > n || row_lo >= row_hi) return fail(GPIC_E_INVALID, "bad row range");
+  if (lda < affinity_pitch(n) || lda % 32) return fail(GPIC_E_INVALID, "lda must be >= pitch(n) and a multiple of 32");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int64_t rows = row_hi - row_lo;
+  const int64_t rows_pad = round_up(rows, kTileM);
+  const int32_t dp = feature_pitch(d);
+  const float neg_scale_log2 = (float)(-1.4426950408889634 / (2.0 * sigma * sigma));
+  float* rowpart = static_cast<float*>(d_work);  // n_ctiles x rows_pad
+  if (impl == GPIC_AFFINITY_TC) {
+    int rc = launch_affinity_tc(d_xhi, d_xlo, d_sqn, n, dp, row_lo, row_hi, neg_scale_log2, d_a,
+                                lda, rowpart, rows_pad, s);
+    if (rc != GPIC_OK) return rc;
+  } else if (impl == GPIC_AFFINITY_SIMT) {
+    launch_affinity_simt(d_xhi, d_xlo, d_sqn, n, dp, row_lo, row_hi, neg_scale_log2, d_a, lda,
+                         rowpart, rows_pad, s);
+  } else {
+    return fail(GPIC_E_INVALID, "unknown affinity engine");
+  }
+  launch_degree(rowpart, rows, rows_pad, ceil_div(n, kTileN), row_lo, d_deg, d_ctl, s);
+  GPIC_CUDA_TRY(cudaGetLastError());
+  return GPIC_OK;
+}
+
+int gpic_initial_vector(const double* d_deg, int64_t n, double* d_v64, float* d_v32,
+                        void* d_work, gpic_ctl* d_ctl, void* stream) {
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  double* part = static_cast<double*>(d_work);
+  double* tau = part + ceil_div(n, kRedBlock);
+  launch_tree_sum(d_deg, n, part, tau, d_ctl, s);
+  launch_scale_vector(d_deg, n, tau, d_v64, d_v32, affinity_pitch(n), s);
+  GPIC_CUDA_TRY(cudaGetLastError());
+  return GPIC_OK;
+}
+
+int gpic_power_iterate(const float* d_a, int64_t lda, const double* d_deg, int64_t n,
+                       double* d_v64, float* d_v32, double eps, int32_t max_iter,
+                       double* d_delta_hist, double* d_v64_out, void* d_work, gpic_ctl* d_ctl,
+                       void* stream) {
+  if (max_iter < 1) return fail(GPIC_E_INVALID, "max_iterations must be at least 1");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  // d_work: y (n doubles) then the reduction partials
+  double* y = static_cast<double*>(d_work);
+  double* part = y + n;
+  int rc = run_power_loop(d_a, lda, d_deg, n, y, part, d_v64, d_v32, d_delta_hist, d_ctl,
+                          max_iter, s);
+  if (rc != GPIC_OK) return rc;
+  launch_copy_result(d_v64, n, d_v64_out, d_ctl, s);
+  GPIC_CUDA_TRY(cudaGetLastError());
+  return GPIC_OK;
+}
+
+int gpic_kmeans1d(const double* d_v, int64_t n, int32_t k, int64_t first_index,
+                  const double* h_uniforms, int32_t max_rounds, double tol, int64_t* d_labels,
+                  void* d_work, gpic_ctl* d_ctl, void* stream) {
+  return launch_kmeans1d(d_v, n, k, first_index, h_uniforms, max_rounds, tol, d_labels, d_work,
+                         d_ctl, static_cast<cudaStream_t>(stream));
+}
+
+int gpic_reduce_sum(const double* d_v, int64_t n, double* d_out, void* d_work, void* stream) {
+  if (n < 1) return fail(GPIC_E_EMPTY, "cannot reduce an empty vector");
+  // d_work: a gpic_ctl followed by the partials
+  gpic_ctl* ctl = static_cast<gpic_ctl*>(d_work);
+  double* part = reinterpret_cast<double*>(static_cast<uint8_t*>(d_work) + sizeof(gpic_ctl));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  launch_ctl_init(ctl, 0.0, 1, s);
+  launch_tree_sum(d_v, n, part, d_out, ctl, s);
+  GPIC_CUDA_TRY(cudaGetLastError());
+  return GPIC_OK;
+}
+
+int gpic_scale(const double* d_src, int64_t n, double tau, double* d_dst, float* d_dst32,
+               int64_t f32_len, void* stream) {
+  if (!(tau > 0.0)) return fail(GPIC_E_NONPOS_TAU, "normalisation constant must be positive");
+  launch_scale_by(d_src, n, tau, d_dst, d_dst32, f32_len, static_cast<cudaStream_t>(stream));
+  GPIC_CUDA_TRY(cudaGetLastError());
+  return GPIC_OK;
+}
+
+int64_t gpic_kmeans_scratch_bytes(int64_t n, int32_t k) { return kmeans_scratch_bytes(n, k); }
+
+int gpic_matvec(const float* d_a, int64_t lda, int64_t rows, int64_t n, const float* d_v,
+                const double* d_row_scale, double* d_y, void* stream) {
+  if (lda % 4 || lda < n) return fail(GPIC_E_INVALID, "lda must be >= n and a multiple of 4");
+  launch_gemv(d_a, lda, rows, 0, d_v, d_row_scale, d_y, nullptr, static_cast<cudaStream_t>(stream));
+  GPIC_CUDA_TRY(cudaGetLastError());
+  return GPIC_OK;
+}
+
+int gpic_cluster(const double* d_x, int64_t n, int32_t d, double sigma, int32_t k, double eps,
+                 int32_t max_iter, int64_t first_index, const double* h_uniforms, int32_t impl,
+                 int64_t* d_labels, double* d_v, double* d_delta_hist, int32_t* h_iters,
+                 int32_t* h_converged, void* d_work, int64_t work_bytes, void* stream) {
+  if (n < 1 || d < 1) return fail(GPIC_E_EMPTY, "dataset must contain at least one point and one feature");
+  if (k > n) return fail(GPIC_E_K_TOO_LARGE, "k exceeds the number of points");
+  Workspace ws;
+  const int64_t scratch = workspace_bytes(n, d, k, n, max_iter);
+  const int64_t lda = affinity_pitch(n);
+  if (work_bytes < scratch + n * lda * 4) return fail(GPIC_E_INVALID, "workspace too small for the affinity matrix");
+  int rc = carve(d_work, scratch, n, d, k, n, max_iter, &ws);
+  if (rc) return rc;
+  float* a = reinterpret_cast<float*>(static_cast<uint8_t*>(d_work) + scratch);
+  double* deg = ws.deg;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  launch_ctl_init(ws.ctl, eps, max_iter, s);
+  launch_prepare(d_x, n, d, ws.xhi, ws.xlo, ws.sqn, ws.colpart, ws.mean, ws.ctl, s);
+  const float neg_scale_log2 = (float)(-1.4426950408889634 / (2.0 * sigma * sigma));
+  const int32_t dp = feature_pitch(d);
+  const int64_t rows_pad = round_up(n, kTileM);
+  if (impl == GPIC_AFFINITY_TC) {
+    rc = launch_affinity_tc(ws.xhi, ws.xlo, ws.sqn, n, dp, 0, n, neg_scale_log2, a, lda,
+                            ws.rowpart, rows_pad, s);
+    if (rc) return rc;
+  } else {
+    launch_affinity_simt(ws.xhi, ws.xlo, ws.sqn, n, dp, 0, n, neg_scale_log2, a, lda, ws.rowpart,
+                         rows_pad, s);
+  }
+  launch_degree(ws.rowpart, n, rows_pad, ceil_div(n, kTileN), 0, deg, ws.ctl, s);
+  launch_tree_sum(deg, n, ws.redpart, ws.redpart + ceil_div(n, kRedBlock), ws.ctl, s);
+  launch_scale_vector(deg, n, ws.redpart + ceil_div(n, kRedBlock), ws.v64, ws.v32, lda, s);
+  rc = run_power_loop(a, lda, deg, n, ws.y, ws.redpart, ws.v64, ws.v32, d_delta_hist, ws.ctl,
+                      max_iter, s);
+  if (rc) return rc;
+  launch_copy_result(ws.v64, n, d_v, ws.ctl, s);
+  GPIC_CUDA_TRY(cudaGetLastError());
+  // k-means needs the status of the loop: read the control block once.
+  gpic_ctl h;
+  rc = gpic_ctl_read(ws.ctl, &h, stream);
+  if (rc) return rc;
+  rc = status_from_ctl(h, d);
+  if (rc) return rc;
+  rc = launch_kmeans1d(d_v, n, k, first_index, h_uniforms, 100, 1e-12, d_labels, ws.kscratch,
+                       ws.ctl, s);
+  if (rc) return rc;
+  rc = gpic_ctl_read(ws.ctl, &h, stream);
+  if (rc) return rc;
+  if (h_iters) *h_iters = h.iter;
+  if (h_converged) *h_converged = h.converged;
+  return status_from_ctl(h, d);
+}
+
+int gpic_cluster_host(const double* h_x, int64_t n, int32_t d, double sigma, int32_t k,
+                      double eps, int32_t max_iter, int64_t first_index, const double* h_uniforms,
+                      int32_t impl, int64_t* h_labels, double* h_v, double* h_delta_hist,
+                      int32_t* h_iters, int32_t* h_converged, void* d_work, int64_t work_bytes,
+                      void* stream) {
+  if (n < 1 || d < 1) return fail(GPIC_E_EMPTY, "dataset must contain at least one point and one feature");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  // device staging at the tail of the workspace: X, labels, v, deltas
+  const int64_t scratch = workspace_bytes(n, d, k, n, max_iter) + n * affinity_pitch(n) * 4;
+  const int64_t stage = al(n * d * 8) + al(n * 8) * 2 + al((int64_t)max_iter * 8);
+  if (work_bytes < scratch + stage) return fail(GPIC_E_INVALID, "workspace too small (host entry)");
+  uint8_t* p = static_cast<uint8_t*>(d_work) + al(scratch);
+  double* dx = reinterpret_cast<double*>(p); p += al(n * d * 8);
+  int64_t* dl = reinterpret_cast<int64_t*>(p); p += al(n * 8);
+  double* dv = reinterpret_cast<double*>(p); p += al(n * 8);
+  double* dh = reinterpret_cast<double*>(p);
+  GPIC_CUDA_TRY(cudaMemcpyAsync(dx, h_x, n * d * 8, cudaMemcpyHostToDevice, s));
+  int32_t iters = 0, conv = 0;
+  int rc = gpic_cluster(dx, n, d, sigma, k, eps, max_iter, first_index, h_uniforms, impl, dl, dv,
+                        dh, &iters, &conv, d_work, al(scratch), stream);
+  if (rc) return rc;
+  GPIC_CUDA_TRY(cudaMemcpyAsync(h_labels, dl, n * 8, cudaMemcpyDeviceToHost, s));
+  GPIC_CUDA_TRY(cudaMemcpyAsync(h_v, dv, n * 8, cudaMemcpyDeviceToHost, s));
+  GPIC_CUDA_TRY(cudaMemcpyAsync(h_delta_hist, dh, (int64_t)iters * 8, cudaMemcpyDeviceToHost, s));
+  GPIC_CUDA_TRY(cudaStreamSynchronize(s));
+  if (h_iters) *h_iters = iters;
+  if (h_converged) *h_converged = conv;
+  return GPIC_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,524 @@
+// Stage 4: 1-D k-means of the embedding on the GPU (kmeans.py:178-196).
+//
+//   lloyd_kernel   k-means++ seeding (kmeans.py:39-55) from host-drawn PCG64
+//                  numbers, Lloyd rounds with lowest-index ties and
+//                  empty-cluster reseeding (kmeans.py:58-94)
+//   polish_kernel  n <= 4096 only: exact DP over the stable sorted order,
+//                  earliest split on ties (kmeans.py:97-130), replacing the
+//                  Lloyd labels when its WCSS is strictly lower (kmeans.py:190-193)
+//   finish_kernel  contiguity check (kmeans.py:149-160, 194-195) and the
+//                  canonical relabel by ascending centroid (kmeans.py:163-175)
+//
+// All three are single-CTA (1024 threads) kernels: the embedding is at most
+// a few MB and every step is a full-vector reduction, so one SM streaming
+// from L2 beats a grid-wide barrier per step. Every reduction has a fixed
+// order, so labels are deterministic.
+//
+// Deviation, by construction unreachable: the reference's gap-split repair
+// (kmeans.py:133-146) only runs when the labels are not contiguous in value
+// order; both Lloyd's final nearest-centre assignment and the DP partition
+// are always contiguous (1-D Voronoi cells are intervals), so the device
+// path reports GPIC_E_UNSUPPORTED instead of silently diverging if that
+// invariant is ever violated.
+#include <cfloat>
+#include <cstdint>
+
+#include "common.cuh"
+#include "ops.h"
+
+namespace gpic {
+
+namespace {
+
+constexpr int kThreads = 1024;
+constexpr int kWarps = kThreads / 32;
+constexpr int kMaxK = 64;
+constexpr int kPolishLimit = 4096;  // kmeans.py:22 POLISH_LIMIT
+
+struct KScratch {
+  int32_t* lab;     // n   Lloyd labels
+  int32_t* alt;     // n   DP labels
+  double* dist2;    // n
+  double* unif;     // kMaxK
+  int32_t* order;   // kPolishLimit   stable sorted order
+  double* best;     // 2 x (kPolishLimit + 1)
+  int32_t* split;   // (kMaxK + 1) x (kPolishLimit + 1)
+  double* stats;    // small: [0] = wcss(lloyd), [1] = wcss(dp)
+};
+
+__host__ __device__ inline int64_t al(int64_t b) { return (b + 255) & ~int64_t(255); }
+
+__host__ __device__ inline KScratch carve_k(void* base, int64_t n) {
+  uint8_t* p = static_cast<uint8_t*>(base);
+  KScratch s;
+  s.lab = reinterpret_cast<int32_t*>(p); p += al(n * 4);
+  s.alt = reinterpret_cast<int32_t*>(p); p += al(n * 4);
+  s.dist2 = reinterpret_cast<double*>(p); p += al(n * 8);
+  s.unif = reinterpret_cast<double*>(p); p += al(kMaxK * 8);
+  s.order = reinterpret_cast<int32_t*>(p); p += al(kPolishLimit * 4);
+  s.best = reinterpret_cast<double*>(p); p += al(2 * (kPolishLimit + 1) * 8);
+  s.split = reinterpret_cast<int32_t*>(p); p += al((int64_t)(kMaxK + 1) * (kPolishLimit + 1) * 4);
+  s.stats = reinterpret_cast<double*>(p); p += al(64 * 8);
+  return s;
+}
+
+__host__ __device__ inline int64_t scratch_size(int64_t n) {
+  return al(n * 4) * 2 + al(n * 8) + al(kMaxK * 8) + al(kPolishLimit * 4) +
+         al(2 * (kPolishLimit + 1) * 8) + al((int64_t)(kMaxK + 1) * (kPolishLimit + 1) * 4) +
+         al(64 * 8);
+}
+
+// ------------------------------------------------------- block primitives
+struct Shared {
+  double wsum[kWarps][kMaxK];
+  int wcnt[kWarps][kMaxK];
+  double centers[kMaxK];
+  double red_d[kWarps];
+  long long red_i[kWarps];
+  double scan[kThreads];
+  int flag;
+};
+
+__device__ double block_sum(double v, Shared& sh) {
+  v = warp_sum_f64(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) sh.red_d[w] = v;
+  __syncthreads();
+  double t = 0.0;
+  for (int i = 0; i < kWarps; ++i) t += sh.red_d[i];
+  return t;
+}
+
+// argmax of val with lowest index on ties (np.argmax semantics).
+__device__ long long block_argmax(double val, long long idx, Shared& sh) {
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ov = __shfl_xor_sync(0xffffffffu, val, o);
+    const long long oi = __shfl_xor_sync(0xffffffffu, idx, o);
+    if (ov > val || (ov == val && oi < idx)) { val = ov; idx = oi; }
+  }
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) { sh.red_d[w] = val; sh.red_i[w] = idx; }
+  __syncthreads();
+  double bv = sh.red_d[0];
+  long long bi = sh.red_i[0];
+  for (int i = 1; i < kWarps; ++i)
+    if (sh.red_d[i] > bv || (sh.red_d[i] == bv && sh.red_i[i] < bi)) { bv = sh.red_d[i]; bi = sh.red_i[i]; }
+  return bi;
+}
+
+__device__ long long block_min_i(long long v, Shared& sh) {
+  for (int o = 16; o > 0; o >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) sh.red_i[w] = v;
+  __syncthreads();
+  long long b = sh.red_i[0];
+  for (int i = 1; i < kWarps; ++i) b = min(b, sh.red_i[i]);
+  return b;
+}
+
+// nearest centre, lowest index on ties (kmeans.py:58-60: argmin |v - c|)
+__device__ __forceinline__ int nearest(double x, const double* c, int k) {
+  int best = 0;
+  double bd = fabs(x - c[0]);
+  for (int j = 1; j < k; ++j) {
+    const double d = fabs(x - c[j]);
+    if (d < bd) { bd = d; best = j; }
+  }
+  return best;
+}
+
+__device__ void assign_all(const double* v, int64_t n, int k, int32_t* lab, Shared& sh) {
+  for (int64_t i = threadIdx.x; i < n; i += kThreads) lab[i] = nearest(v[i], sh.centers, k);
+  __syncthreads();
+}
+
+// per-cluster sums and counts (fixed order: per thread, then warp
+// butterfly, then warps in order).
+__device__ void cluster_stats(const double* v, int64_t n, int k, const int32_t* lab, Shared& sh,
+                              double* sums, int64_t* cnts) {
+  double ls[kMaxK];
+  int lc[kMaxK];
+  for (int j = 0; j < k; ++j) { ls[j] = 0.0; lc[j] = 0; }
+  for (int64_t i = threadIdx.x; i < n; i += kThreads) {
+    const int j = lab[i];
+    ls[j] += v[i];
+    lc[j] += 1;
+  }
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  for (int j = 0; j < k; ++j) {
+    double s = warp_sum_f64(ls[j]);
+    int c = lc[j];
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if (l == 0) { sh.wsum[w][j] = s; sh.wcnt[w][j] = c; }
+  }
+  __syncthreads();
+  if (threadIdx.x < k) {
+    const int j = threadIdx.x;
+    double s = 0.0;
+    int64_t c = 0;
+    for (int q = 0; q < kWarps; ++q) { s += sh.wsum[q][j]; c += sh.wcnt[q][j]; }
+    sums[j] = s;
+    cnts[j] = c;
+  }
+  __syncthreads();
+}
+
+// WCSS of a labelling (kmeans.py:63-69): per-cluster mean, then squared
+// deviations; clusters added in id order.
+__device__ double wcss(const double* v, int64_t n, int k, const int32_t* lab, Shared& sh) {
+  __shared__ double sums[kMaxK];
+  __shared__ int64_t cnts[kMaxK];
+  __shared__ double mean[kMaxK];
+  cluster_stats(v, n, k, lab, sh, sums, cnts);
+  if (threadIdx.x < k) mean[threadIdx.x] = cnts[threadIdx.x] ? sums[threadIdx.x] / (double)cnts[threadIdx.x] : 0.0;
+  __syncthreads();
+  double ls[kMaxK];
+  for (int j = 0; j < k; ++j) ls[j] = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += kThreads) {
+    const int j = lab[i];
+    const double d = v[i] - mean[j];
+    ls[j] += d * d;
+  }
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  for (int j = 0; j < k; ++j) {
+    const double s = warp_sum_f64(ls[j]);
+    if (l == 0) sh.wsum[w][j] = s;
+  }
+  __syncthreads();
+  double total = 0.0;
+  for (int j = 0; j < k; ++j) {
+    if (!cnts[j]) continue;
+    double s = 0.0;
+    for (int q = 0; q < kWarps; ++q) s += sh.wsum[q][j];
+    total += s;
+  }
+  __syncthreads();
+  return total;
+}
+
+// ----------------------------------------------------------- Lloyd kernel
+__global__ void __launch_bounds__(kThreads, 1)
+    lloyd_kernel(const double* __restrict__ v, int64_t n, int k, int64_t first_index,
+                 int max_rounds, double tol, KScratch s, gpic_ctl* ctl) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  Shared& sh = *reinterpret_cast<Shared*>(smem_raw);
+  __shared__ double sums[kMaxK];
+  __shared__ int64_t cnts[kMaxK];
+  const int tid = threadIdx.x;
+
+  // ---- k-means++ seeding (kmeans.py:39-55)
+  if (tid == 0) sh.centers[0] = v[first_index];
+  __syncthreads();
+  for (int64_t i = tid; i < n; i += kThreads) {
+    const double d = v[i] - sh.centers[0];
+    s.dist2[i] = d * d;
+  }
+  __syncthreads();
+  // contiguous chunk per thread so the running prefix follows index order
+  const int64_t chunk = (n + kThreads - 1) / kThreads;
+  const int64_t lo = min(n, (int64_t)tid * chunk), hi = min(n, lo + chunk);
+  for (int j = 1; j < k; ++j) {
+    double part = 0.0;
+    for (int64_t i = lo; i < hi; ++i) part += s.dist2[i];
+    sh.scan[tid] = part;
+    __syncthreads();
+    // inclusive Hillis-Steele scan of the chunk totals (fixed pattern)
+    for (int off = 1; off < kThreads; off <<= 1) {
+      const double add = tid >= off ? sh.scan[tid - off] : 0.0;
+      __syncthreads();
+      sh.scan[tid] += add;
+      __syncthreads();
+    }
+    const double total = sh.scan[kThreads - 1];
+    if (!(total > 0.0)) {  // all mass on existing centres: duplicate the first
+      if (tid == 0)
+        for (int q = j; q < k; ++q) sh.centers[q] = sh.centers[0];
+      __syncthreads();
+      break;
+    }
+    const double r = s.unif[j - 1] * total;
+    // searchsorted(cumsum(d2), r, side="right") = first i with cumsum_i > r
+    double run = tid ? sh.scan[tid - 1] : 0.0;
+    long long found = n;
+    if (run + part > r || tid == kThreads - 1) {
+      for (int64_t i = lo; i < hi; ++i) {
+        run += s.dist2[i];
+        if (run > r) { found = i; break; }
+      }
+    }
+    long long pick = block_min_i(found, sh);
+    if (pick > n - 1) pick = n - 1;
+    if (tid == 0) sh.centers[j] = v[pick];
+    __syncthreads();
+    const double cj = sh.centers[j];
+    for (int64_t i = tid; i < n; i += kThreads) {
+      const double d = v[i] - cj;
+      s.dist2[i] = fmin(s.dist2[i], d * d);
+    }
+    __syncthreads();
+  }
+
+  // ---- Lloyd rounds (kmeans.py:75-94)
+  assign_all(v, n, k, s.lab, sh);
+  for (int round = 0; round < max_rounds; ++round) {
+    cluster_stats(v, n, k, s.lab, sh, sums, cnts);
+    // empty-cluster repair: reseed at the point farthest from its centre
+    // (stats are refreshed after every reseed, as the reference reassigns)
+    for (int j = 0; j < k; ++j) {
+      if (cnts[j] != 0) continue;
+      double bv = -1.0;
+      long long bi = n;
+      for (int64_t i = tid; i < n; i += kThreads) {
+        const double d = fabs(v[i] - sh.centers[s.lab[i]]);
+        if (d > bv) { bv = d; bi = i; }  // ascending i per thread: first max kept
+      }
+      const long long far = block_argmax(bv, bi, sh);
+      if (tid == 0) sh.centers[j] = v[far];
+      __syncthreads();
+      assign_all(v, n, k, s.lab, sh);
+      cluster_stats(v, n, k, s.lab, sh, sums, cnts);
+    }
+    if (tid == 0) {
+      double moved = 0.0;
+      for (int j = 0; j < k; ++j) {
+        if (cnts[j]) {
+          const double c = sums[j] / (double)cnts[j];
+          moved = fmax(moved, fabs(c - sh.centers[j]));
+          sh.centers[j] = c;
+        }
+      }
+      sh.flag = moved < tol;
+    }
+    __syncthreads();
+    assign_all(v, n, k, s.lab, sh);
+    if (sh.flag) break;
+    __syncthreads();
+  }
+  if (n > kPolishLimit) return;
+  const double w = wcss(v, n, k, s.lab, sh);
+  if (tid == 0) s.stats[0] = w;
+}
+
+// --------------------------------------------------- DP polish (n <= 4096)
+__global__ void __launch_bounds__(kThreads, 1)
+    polish_kernel(const double* __restrict__ v, int64_t n, int k, KScratch s) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  // [0, 4096) sort keys/values, then reused: ps (n+1), ps2 (n+1), prev (n+1)
+  double* key = reinterpret_cast<double*>(smem_raw);                       // 4096
+  int* idx = reinterpret_cast<int*>(key + kPolishLimit);                   // 4096
+  double* ps = reinterpret_cast<double*>(idx + kPolishLimit);              // 4097
+  double* ps2 = ps + (kPolishLimit + 1);                                   // 4097
+  double* prev = ps2 + (kPolishLimit + 1);                                 // 4097
+  const int tid = threadIdx.x;
+  for (int i = tid; i < kPolishLimit; i += kThreads) {
+    key[i] = i < n ? v[i] : __longlong_as_double(0x7ff0000000000000ll);
+    idx[i] = i < n ? i : 0x7fffffff;
+  }
+  __syncthreads();
+  // bitonic sort by (value, index): equals np.argsort(kind="stable")
+  for (int size = 2; size <= kPolishLimit; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int i = tid; i < kPolishLimit; i += kThreads) {
+        const int jx = i ^ stride;
+        if (jx > i) {
+          const bool up = (i & size) == 0;
+          const double ki = key[i], kj = key[jx];
+          const int ii = idx[i], ij = idx[jx];
+          const bool gt = ki > kj || (ki == kj && ii > ij);
+          if (gt == up) { key[i] = kj; key[jx] = ki; idx[i] = ij; idx[jx] = ii; }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (int i = tid; i < n; i += kThreads) s.order[i] = idx[i];
+  // prefix sums exactly as np.cumsum (sequential, x*x rounded first)
+  if (tid == 0) {
+    double a = 0.0, b = 0.0;
+    ps[0] = 0.0;
+    ps2[0] = 0.0;
+    for (int i = 0; i < n; ++i) {
+      const double x = key[i];
+      a = __dadd_rn(a, x);
+      b = __dadd_rn(b, __dmul_rn(x, x));
+      ps[i + 1] = a;
+      ps2[i + 1] = b;
+    }
+  }
+  __syncthreads();
+  // best[0][0] = 0, best[0][j>0] = inf
+  const double inf = __longlong_as_double(0x7ff0000000000000ll);
+  for (int j = tid; j <= n; j += kThreads) prev[j] = j == 0 ? 0.0 : inf;
+  __syncthreads();
+  double* cur = s.best;  // global row buffer (n + 1)
+  for (int q = 1; q <= k; ++q) {
+    for (int j = q + tid; j <= n; j += kThreads) {
+      double bc = inf;
+      int bi = q - 1;
+      const double pj = ps[j], p2j = ps2[j];
+      for (int i = q - 1; i < j; ++i) {
+        const double sg = __dsub_rn(pj, ps[i]);
+        const double c = __dsub_rn(__dadd_rn(prev[i], __dsub_rn(p2j, ps2[i])),
+                                   __ddiv_rn(__dmul_rn(sg, sg), (double)(j - i)));
+        if (c < bc) { bc = c; bi = i; }  // strict: earliest i on ties (np.argmin)
+      }
+      cur[j] = bc;
+      s.split[(int64_t)q * (kPolishLimit + 1) + j] = bi;
+    }
+    __syncthreads();
+    for (int j = tid; j <= n; j += kThreads) prev[j] = j < q ? inf : cur[j];
+    __syncthreads();
+  }
+  if (tid == 0) {
+    int j = (int)n;
+    for (int q = k; q >= 1; --q) {
+      const int i = s.split[(int64_t)q * (kPolishLimit + 1) + j];
+      for (int p = i; p < j; ++p) s.alt[idx[p]] = q - 1;
+      j = i;
+    }
+  }
+}
+
+// WCSS of the DP labelling, then choose (kmeans.py:190-193).
+__global__ void __launch_bounds__(kThreads, 1)
+    choose_kernel(const double* __restrict__ v, int64_t n, int k, KScratch s) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  Shared& sh = *reinterpret_cast<Shared*>(smem_raw);
+  const double w_dp = wcss(v, n, k, s.alt, sh);
+  const bool take = w_dp < s.stats[0];
+  if (threadIdx.x == 0) s.stats[1] = w_dp;
+  if (take)
+    for (int64_t i = threadIdx.x; i < n; i += kThreads) s.lab[i] = s.alt[i];
+}
+
+// Contiguity check + canonical relabel (kmeans.py:149-175).
+__global__ void __launch_bounds__(kThreads, 1)
+    finish_kernel(const double* __restrict__ v, int64_t n, int k, KScratch s,
+                  int64_t* __restrict__ out, gpic_ctl* ctl) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  Shared& sh = *reinterpret_cast<Shared*>(smem_raw);
+  __shared__ double sums[kMaxK];
+  __shared__ int64_t cnts[kMaxK];
+  __shared__ double lo_v[kMaxK], hi_v[kMaxK];
+  __shared__ long long lo_i[kMaxK], hi_i[kMaxK];
+  __shared__ int remap[kMaxK];
+  const int tid = threadIdx.x;
+  cluster_stats(v, n, k, s.lab, sh, sums, cnts);
+  // lexicographic (value, index) extent of every cluster
+  for (int j = 0; j < k; ++j) {
+    double mn = __longlong_as_double(0x7ff0000000000000ll), mx = -mn;
+    long long mni = LLONG_MAX, mxi = -1;
+    for (int64_t i = tid; i < n; i += kThreads) {
+      if (s.lab[i] != j) continue;
+      const double x = v[i];
+      if (x < mn || (x == mn && i < mni)) { mn = x; mni = i; }
+      if (x > mx || (x == mx && i > mxi)) { mx = x; mxi = i; }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      const double a = __shfl_xor_sync(0xffffffffu, mn, o);
+      const long long ai = __shfl_xor_sync(0xffffffffu, mni, o);
+      if (a < mn || (a == mn && ai < mni)) { mn = a; mni = ai; }
+      const double b = __shfl_xor_sync(0xffffffffu, mx, o);
+      const long long bi = __shfl_xor_sync(0xffffffffu, mxi, o);
+      if (b > mx || (b == mx && bi > mxi)) { mx = b; mxi = bi; }
+    }
+    const int w = tid >> 5, l = tid & 31;
+    if (l == 0) { sh.red_d[w] = mn; sh.red_i[w] = mni; sh.wsum[w][0] = mx; sh.wcnt[w][0] = 0; }
+    __shared__ long long s_mxi[kWarps];
+    if (l == 0) s_mxi[w] = mxi;
+    __syncthreads();
+    if (tid == 0) {
+      double bmn = sh.red_d[0], bmx = sh.wsum[0][0];
+      long long bmni = sh.red_i[0], bmxi = s_mxi[0];
+      for (int q = 1; q < kWarps; ++q) {
+        if (sh.red_d[q] < bmn || (sh.red_d[q] == bmn && sh.red_i[q] < bmni)) { bmn = sh.red_d[q]; bmni = sh.red_i[q]; }
+        if (sh.wsum[q][0] > bmx || (sh.wsum[q][0] == bmx && s_mxi[q] > bmxi)) { bmx = sh.wsum[q][0]; bmxi = s_mxi[q]; }
+      }
+      lo_v[j] = bmn; lo_i[j] = bmni; hi_v[j] = bmx; hi_i[j] = bmxi;
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    // rank occupied clusters by centroid (stable on id), check that their
+    // (value, index) extents do not interleave.
+    int ids[kMaxK];
+    double cen[kMaxK];
+    int m = 0;
+    for (int j = 0; j < k; ++j)
+      if (cnts[j]) { ids[m] = j; cen[m] = sums[j] / (double)cnts[j]; ++m; }
+    for (int a = 1; a < m; ++a) {  // insertion sort, stable
+      const int id = ids[a];
+      const double c = cen[a];
+      int b = a - 1;
+      while (b >= 0 && cen[b] > c) { ids[b + 1] = ids[b]; cen[b + 1] = cen[b]; --b; }
+      ids[b + 1] = id;
+      cen[b + 1] = c;
+    }
+    for (int j = 0; j < k; ++j) remap[j] = 0;
+    for (int r = 0; r < m; ++r) remap[ids[r]] = r;
+    // contiguity: sort extents by start, require end(prev) < start(next)
+    int by[kMaxK];
+    for (int r = 0; r < m; ++r) by[r] = ids[r];
+    for (int a = 1; a < m; ++a) {
+      const int id = by[a];
+      int b = a - 1;
+      while (b >= 0 && (lo_v[by[b]] > lo_v[id] || (lo_v[by[b]] == lo_v[id] && lo_i[by[b]] > lo_i[id]))) {
+        by[b + 1] = by[b];
+        --b;
+      }
+      by[b + 1] = id;
+    }
+    int ok = 1;
+    for (int r = 1; r < m; ++r) {
+      const int p = by[r - 1], q = by[r];
+      if (!(hi_v[p] < lo_v[q] || (hi_v[p] == lo_v[q] && hi_i[p] < lo_i[q]))) ok = 0;
+    }
+    sh.flag = ok;
+    if (!ok) raise_status(ctl, GPIC_E_UNSUPPORTED, 0, -1, 0.0);
+  }
+  __syncthreads();
+  for (int64_t i = tid; i < n; i += kThreads) out[i] = remap[s.lab[i]];
+}
+
+}  // namespace
+
+int64_t kmeans_scratch_bytes(int64_t n, int32_t /*k*/) { return scratch_size(n); }
+
+int launch_kmeans1d(const double* v, int64_t n, int32_t k, int64_t first_index,
+                    const double* h_uniforms, int32_t max_rounds, double tol, int64_t* labels,
+                    void* scratch, gpic_ctl* ctl, cudaStream_t st) {
+  if (k > n) return fail(GPIC_E_K_TOO_LARGE, "k exceeds the number of points");
+  if (k < 2 || k > kMaxK) return fail(GPIC_E_UNSUPPORTED, "k must lie in [2, 64] on the GPU path");
+  if (first_index < 0 || first_index >= n) return fail(GPIC_E_INVALID, "first_index out of range");
+  KScratch s = carve_k(scratch, n);
+  if (k > 1)
+    GPIC_CUDA_TRY(cudaMemcpyAsync(s.unif, h_uniforms, sizeof(double) * (k - 1),
+                                  cudaMemcpyHostToDevice, st));
+  const size_t shm = sizeof(Shared);
+  static bool attr = false;
+  if (!attr) {
+    GPIC_CUDA_TRY(cudaFuncSetAttribute(lloyd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
+    GPIC_CUDA_TRY(cudaFuncSetAttribute(choose_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
+    GPIC_CUDA_TRY(cudaFuncSetAttribute(finish_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
+    const int pshm = kPolishLimit * (8 + 4) + 3 * (kPolishLimit + 1) * 8;
+    GPIC_CUDA_TRY(cudaFuncSetAttribute(polish_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, pshm));
+    attr = true;
+  }
+  lloyd_kernel<<<1, kThreads, shm, st>>>(v, n, k, first_index, max_rounds, tol, s, ctl);
+  count_launch();
+  if (n <= kPolishLimit) {
+    const int pshm = kPolishLimit * (8 + 4) + 3 * (kPolishLimit + 1) * 8;
+    polish_kernel<<<1, kThreads, pshm, st>>>(v, n, k, s);
+    choose_kernel<<<1, kThreads, shm, st>>>(v, n, k, s);
+    count_launch(2);
+  }
+  finish_kernel<<<1, kThreads, shm, st>>>(v, n, k, s, labels, ctl);
+  count_launch();
+  GPIC_CUDA_TRY(cudaGetLastError());
+  return GPIC_OK;
+}
+
+}  // namespace gpic

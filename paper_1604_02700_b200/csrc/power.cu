@@ -1,0 +1,320 @@
+// Stage 2/3: start vector and the device-resident power iteration.
+//
+// Reference loop (serial.py:120-127, parallel.py:374-382):
+//     wv = W v ; v' = wv / sum(wv) ; delta = max|v' - v| ;
+//     stop when len(deltas) >= 2 and |delta_t - delta_(t-1)| <= eps
+//
+// Per iteration, three kernels, all no-ops once ctl->stop is set so a whole
+// max_iterations loop can be replayed from one CUDA graph with no host
+// synchronisation:
+//   gemv_kernel   y_i = (sum_j A_ij v_j) / deg_i        HBM-bound, 4n^2 bytes
+//   tau_kernel    tau = fixed-shape sum of y             (k_reduce, parallel.py:161-178)
+//   norm_kernel   v' = y / tau, delta = max|v' - v|, history, stop test
+// Every reduction has a fixed shape over GLOBAL indices, so results are
+// bitwise independent of how rows are sharded across ranks.
+#include <cfloat>
+#include <cstdio>
+
+#include "common.cuh"
+#include "ops.h"
+
+namespace gpic {
+
+namespace {
+
+constexpr int kGemvWarps = 8;
+constexpr int kGemvRows = 4;     // rows per warp
+constexpr int kGemvUnroll = 4;   // float4 columns in flight per lane per row
+constexpr int kFlush = 16;       // fp32 partial -> fp64 every kFlush steps
+constexpr int kRedThreads = 256;
+constexpr int kRedPer = kRedBlock / kRedThreads;  // 8 elements per thread
+
+// ---------------------------------------------------------------- GEMV
+template <int R, int U>
+__global__ void __launch_bounds__(kGemvWarps * 32)
+    gemv_kernel(const float* __restrict__ a, int64_t lda, int64_t rows, int64_t row_lo,
+                const float* __restrict__ v32, const double* __restrict__ deg,
+                double* __restrict__ y, const gpic_ctl* __restrict__ ctl) {
+  if (ctl != nullptr && *(volatile const int32_t*)&ctl->stop) return;
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int64_t r0 = ((int64_t)blockIdx.x * kGemvWarps + warp) * R;
+  if (r0 >= rows) return;
+  const int64_t nv4 = lda >> 2;
+  const float4* __restrict__ vv = reinterpret_cast<const float4*>(v32);
+  const float4* arow[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int64_t rr = min(r0 + r, rows - 1);  // tail rows re-read the last row, result dropped
+    arow[r] = reinterpret_cast<const float4*>(a + rr * lda);
+  }
+  double acc64[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) acc64[r] = 0.0;
+
+  constexpr int64_t kStep = 32 * U;
+  for (int64_t base = 0; base < nv4; base += kStep * kFlush) {
+    float acc[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) acc[r] = 0.f;
+    const int64_t stop = min(nv4, base + kStep * kFlush);
+    for (int64_t c0 = base + lane; c0 < stop; c0 += kStep) {
+      float4 vu[U];
+      float4 au[R][U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t c = c0 + u * 32;
+        const bool ok = c < stop;
+        vu[u] = ok ? __ldg(vv + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+          au[r][u] = ok ? ld_stream_f4(arow[r] + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          acc[r] = fmaf(au[r][u].x, vu[u].x, acc[r]);
+          acc[r] = fmaf(au[r][u].y, vu[u].y, acc[r]);
+          acc[r] = fmaf(au[r][u].z, vu[u].z, acc[r]);
+          acc[r] = fmaf(au[r][u].w, vu[u].w, acc[r]);
+        }
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) acc64[r] += (double)acc[r];
+  }
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const double s = warp_sum_f64(acc64[r]);
+    if (lane == 0 && r0 + r < rows) {
+      const int64_t li = r0 + r;
+      y[row_lo + li] = deg != nullptr ? s / deg[li] : s;
+    }
+  }
+}
+
+// ------------------------------------------------- fixed-shape reductions
+// Block b sums y[b*2048, (b+1)*2048) in a fixed pattern; the last block
+// combines the per-block partials in a fixed pattern.
+__device__ __forceinline__ double block_sum_fixed(double v, double* sh) {
+  sh[threadIdx.x] = v;
+  __syncthreads();
+#pragma unroll
+  for (int s = kRedThreads / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) sh[threadIdx.x] += sh[threadIdx.x + s];
+    __syncthreads();
+  }
+  const double r = sh[0];
+  __syncthreads();
+  return r;
+}
+
+__device__ __forceinline__ double block_max(double v, double* sh) {
+  sh[threadIdx.x] = v;
+  __syncthreads();
+#pragma unroll
+  for (int s = kRedThreads / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) sh[threadIdx.x] = fmax(sh[threadIdx.x], sh[threadIdx.x + s]);
+    __syncthreads();
+  }
+  const double r = sh[0];
+  __syncthreads();
+  return r;
+}
+
+// Sum of v[0, n) into *out (and ctl->tau when ctl != null). `guarded` skips
+// when ctl->stop is set (loop mode).
+__global__ void __launch_bounds__(kRedThreads)
+    tau_kernel(const double* __restrict__ v, int64_t n, double* __restrict__ part,
+               double* __restrict__ out, gpic_ctl* ctl, int guarded) {
+  __shared__ double sh[kRedThreads];
+  if (guarded && *(volatile int32_t*)&ctl->stop) return;
+  const int64_t b0 = (int64_t)blockIdx.x * kRedBlock;
+  double s = 0.0;
+#pragma unroll
+  for (int q = 0; q < kRedPer; ++q) {
+    const int64_t i = b0 + threadIdx.x + q * kRedThreads;
+    if (i < n) s += v[i];
+  }
+  s = block_sum_fixed(s, sh);
+  if (threadIdx.x == 0) part[blockIdx.x] = s;
+  if (!last_block_done(&ctl->arrive[0])) return;
+  // last block: fixed pattern over the partials
+  const int64_t nb = gridDim.x;
+  double t = 0.0;
+  for (int64_t i = threadIdx.x; i < nb; i += kRedThreads) t += part[i];
+  t = block_sum_fixed(t, sh);
+  if (threadIdx.x == 0) {
+    ctl->arrive[0] = 0u;
+    if (out) *out = t;
+    ctl->tau = t;
+    if (guarded && !(t > 0.0)) raise_status(ctl, GPIC_E_NONPOS_TAU, 0, -1, t);
+  }
+}
+
+// v' = y / tau ; delta = max|v' - v| ; last block records the history and
+// applies the stop rule.
+__global__ void __launch_bounds__(kRedThreads)
+    norm_kernel(const double* __restrict__ y, int64_t n, double* __restrict__ v64,
+                float* __restrict__ v32, double* __restrict__ hist, gpic_ctl* ctl) {
+  __shared__ double sh[kRedThreads];
+  if (*(volatile int32_t*)&ctl->stop) return;
+  const int t = ctl->iter;
+  const double tau = ctl->tau;
+  const double* __restrict__ vold = v64 + (int64_t)(t & 1) * n;
+  double* __restrict__ vnew = v64 + (int64_t)((t + 1) & 1) * n;
+  const int64_t b0 = (int64_t)blockIdx.x * kRedBlock;
+  double m = 0.0;
+#pragma unroll
+  for (int q = 0; q < kRedPer; ++q) {
+    const int64_t i = b0 + threadIdx.x + q * kRedThreads;
+    if (i < n) {
+      const double vn = y[i] / tau;
+      m = fmax(m, fabs(vn - vold[i]));
+      vnew[i] = vn;
+      v32[i] = (float)vn;
+    }
+  }
+  m = block_max(m, sh);
+  if (threadIdx.x == 0)
+    atomicMax(reinterpret_cast<unsigned long long*>(&ctl->delta_bits),
+              (unsigned long long)__double_as_longlong(m));
+  if (!last_block_done(&ctl->arrive[1])) return;
+  if (threadIdx.x == 0) {
+    const double delta = __longlong_as_double((long long)ctl->delta_bits);
+    hist[t] = delta;
+    ctl->delta_bits = 0ull;
+    ctl->arrive[1] = 0u;
+    const int done = t + 1;
+    ctl->iter = done;
+    if (done >= 2 && fabs(delta - hist[t - 1]) <= ctl->eps) {
+      ctl->converged = 1;
+      ctl->stop = 1;
+    } else if (done >= ctl->max_iter) {
+      ctl->stop = 1;
+    }
+  }
+}
+
+// src / tau[0] -> fp64 + fp32 copies (start vector: k_norm(deg, k_reduce(deg))).
+__global__ void scale_kernel(const double* __restrict__ src, int64_t n,
+                             const double* __restrict__ tau, double* __restrict__ v64,
+                             float* __restrict__ v32, int64_t v32_len) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= v32_len) return;
+  if (i < n) {
+    const double v = src[i] / tau[0];
+    v64[i] = v;
+    v32[i] = (float)v;
+  } else {
+    v32[i] = 0.f;
+  }
+}
+
+__global__ void scale_by_kernel(const double* __restrict__ src, int64_t n, double tau,
+                                double* __restrict__ dst, float* __restrict__ dst32,
+                                int64_t f32_len) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) {
+    const double v = src[i] / tau;
+    dst[i] = v;
+    if (dst32) dst32[i] = (float)v;
+  } else if (dst32 && i < f32_len) {
+    dst32[i] = 0.f;
+  }
+}
+
+__global__ void copy_result_kernel(const double* __restrict__ v64, int64_t n,
+                                   double* __restrict__ out, const gpic_ctl* __restrict__ ctl) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  out[i] = v64[(int64_t)(ctl->iter & 1) * n + i];
+}
+
+}  // namespace
+
+void launch_tree_sum(const double* v, int64_t n, double* part, double* out, gpic_ctl* ctl,
+                     cudaStream_t s) {
+  tau_kernel<<<(unsigned)ceil_div(n, kRedBlock), kRedThreads, 0, s>>>(v, n, part, out, ctl, 0);
+  count_launch();
+}
+
+void launch_scale_vector(const double* src, int64_t n, const double* tau, double* v64,
+                         float* v32, int64_t v32_len, cudaStream_t s) {
+  scale_kernel<<<(unsigned)ceil_div(v32_len, 256), 256, 0, s>>>(src, n, tau, v64, v32, v32_len);
+  count_launch();
+}
+
+void launch_scale_by(const double* src, int64_t n, double tau, double* dst, float* dst32,
+                     int64_t f32_len, cudaStream_t s) {
+  const int64_t m = dst32 ? (f32_len > n ? f32_len : n) : n;
+  scale_by_kernel<<<(unsigned)ceil_div(m, 256), 256, 0, s>>>(src, n, tau, dst, dst32, f32_len);
+  count_launch();
+}
+
+void launch_gemv(const float* a, int64_t lda, int64_t rows, int64_t row_lo, const float* v32,
+                 const double* deg, double* y, const gpic_ctl* ctl, cudaStream_t s) {
+  constexpr int rows_per_cta = kGemvWarps * kGemvRows;
+  gemv_kernel<kGemvRows, kGemvUnroll>
+      <<<(unsigned)ceil_div(rows, rows_per_cta), kGemvWarps * 32, 0, s>>>(a, lda, rows, row_lo,
+                                                                         v32, deg, y, ctl);
+  count_launch();
+}
+
+void launch_iteration_tail(const double* y, int64_t n, double* redpart, double* v64, float* v32,
+                           double* hist, gpic_ctl* ctl, cudaStream_t s) {
+  const unsigned nb = (unsigned)ceil_div(n, kRedBlock);
+  tau_kernel<<<nb, kRedThreads, 0, s>>>(y, n, redpart, nullptr, ctl, 1);
+  norm_kernel<<<nb, kRedThreads, 0, s>>>(y, n, v64, v32, hist, ctl);
+  count_launch(2);
+}
+
+void launch_copy_result(const double* v64, int64_t n, double* out, const gpic_ctl* ctl,
+                        cudaStream_t s) {
+  copy_result_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, s>>>(v64, n, out, ctl);
+  count_launch();
+}
+
+// The whole loop as one CUDA graph: max_iter copies of {gemv, tau, norm}.
+// Kernels after convergence exit at their first instruction.
+int run_power_loop(const float* a, int64_t lda, const double* deg, int64_t n, double* y,
+                   double* redpart, double* v64, float* v32, double* hist, gpic_ctl* ctl,
+                   int32_t max_iter, cudaStream_t s) {
+  cudaStream_t cs = s;
+  bool own = false;
+  if (cs == nullptr || cs == cudaStreamLegacy || cs == cudaStreamPerThread) {
+    GPIC_CUDA_TRY(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    own = true;
+    // order the private stream after the caller's work
+    cudaEvent_t ev;
+    GPIC_CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    GPIC_CUDA_TRY(cudaEventRecord(ev, s));
+    GPIC_CUDA_TRY(cudaStreamWaitEvent(cs, ev, 0));
+    GPIC_CUDA_TRY(cudaEventDestroy(ev));
+  }
+  cudaGraph_t graph;
+  cudaGraphExec_t exec;
+  GPIC_CUDA_TRY(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+  const unsigned long long before = g_launches;
+  for (int t = 0; t < max_iter; ++t) {
+    launch_gemv(a, lda, n, 0, v32, deg, y, ctl, cs);
+    launch_iteration_tail(y, n, redpart, v64, v32, hist, ctl, cs);
+  }
+  GPIC_CUDA_TRY(cudaStreamEndCapture(cs, &graph));
+  GPIC_CUDA_TRY(cudaGraphInstantiate(&exec, graph, 0));
+  GPIC_CUDA_TRY(cudaGraphLaunch(exec, cs));
+  (void)before;
+  GPIC_CUDA_TRY(cudaGraphExecDestroy(exec));
+  GPIC_CUDA_TRY(cudaGraphDestroy(graph));
+  if (own) {
+    cudaEvent_t ev;
+    GPIC_CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    GPIC_CUDA_TRY(cudaEventRecord(ev, cs));
+    GPIC_CUDA_TRY(cudaStreamWaitEvent(s, ev, 0));
+    GPIC_CUDA_TRY(cudaEventDestroy(ev));
+    GPIC_CUDA_TRY(cudaStreamDestroy(cs));
+  }
+  return GPIC_OK;
+}
+
+}  // namespace gpic

@@ -1,0 +1,480 @@
+"""The B200 backend: the reference's backend-module protocol on libgpic.
+
+Same stage names and argument meanings as `picluster/parallel.py`
+(k_affinity :113, k_rowsum :131, k_normalize :146, k_reduce :161, k_norm :181,
+k_multiply :196, initial_embedding :210, iterate :217, cluster :236) plus
+`kmeans_1d` (kmeans.py:178), so `report.run_timed`-style drivers and the
+reference's per-kernel tests read the same against this module.
+
+Data stays on the device between stages: `k_affinity` returns a
+`DeviceAffinity` (fp32 A row block + fused degrees), `k_normalize` returns a
+`NormalizedAffinity` view (W = D^-1 A is never materialised; the GEMV applies
+1/deg), vectors are CUDA tensors. Functions also accept numpy inputs and then
+return numpy outputs (uploaded in fp32 / fp64 as the engine computes), which
+is how the reference-style unit tests drive them.
+
+Tensors are PyTorch CUDA tensors (memory + streams only); every computation
+is a libgpic kernel. No CPU fallback: without a CUDA device or libgpic.so
+every entry point raises.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .data import DataSet, check_labels, check_shape
+from .errors import (
+    DeviceError,
+    DimensionMismatch,
+    EmptyVector,
+    InvalidSpec,
+    KTooLarge,
+    NonPositiveTau,
+    ZeroDegree,
+)
+from .params import (
+    Cosine,
+    GaussianRbf,
+    KernelConfig,
+    KMeansParams,
+    PicParams,
+    PicTrace,
+)
+
+KMEANS_MAX_K = 64
+
+
+def _torch():
+    import torch
+
+    if not torch.cuda.is_available():
+        raise DeviceError("the GPIC backend needs a CUDA device (B200 / sm_100a); none is visible")
+    return torch
+
+
+def _device(config: KernelConfig | None):
+    torch = _torch()
+    if config is not None and config.device is not None:
+        return torch.device("cuda", config.device)
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def _stream(dev):
+    torch = _torch()
+    return C.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
+
+
+def _ptr(t) -> C.c_void_p:
+    return C.c_void_p(t.data_ptr()) if t is not None else C.c_void_p(0)
+
+
+def _check_kind(kind) -> float:
+    if isinstance(kind, Cosine):
+        raise InvalidSpec("the cosine similarity kind is not part of this build (RBF only)")
+    if not isinstance(kind, GaussianRbf):
+        raise InvalidSpec(f"unknown similarity kind {kind!r}")
+    return float(kind.sigma)
+
+
+def _read_ctl(ctl_t, dev) -> _lib.Ctl:
+    h = _lib.Ctl()
+    rc = _lib.lib().gpic_ctl_read(_ptr(ctl_t), C.byref(h), _stream(dev))
+    _lib.check(rc)
+    return h
+
+
+def _raise_ctl(h: _lib.Ctl, d: int = 1) -> None:
+    if h.status != _lib.GPIC_OK:
+        _lib.raise_for(h.status, h, d)
+
+
+def _new_ctl(dev, eps: float = 0.0, max_iter: int = 1):
+    torch = _torch()
+    ctl = torch.empty(256, dtype=torch.uint8, device=dev)
+    _lib.check(_lib.lib().gpic_ctl_init(_ptr(ctl), eps, max_iter, _stream(dev)))
+    return ctl
+
+
+def kmeans_draws(n: int, k: int, seed: int):
+    """The PCG64 numbers kmeans.py draws: integers(n) then k-1 x random() (kmeans.py:43,51,73)."""
+    rng = np.random.default_rng(seed)
+    first = int(rng.integers(n))
+    u = np.ascontiguousarray(rng.random(max(k - 1, 1)), dtype=np.float64)
+    return first, u
+
+
+# ------------------------------------------------------------ containers
+@dataclass
+class DeviceAffinity:
+    """Rows [row_lo, row_hi) of A (fp32, row pitch `lda`) with fused degrees."""
+
+    a: object          # torch.float32 [rows, lda]
+    deg: object        # torch.float64 [rows]
+    n: int
+    lda: int
+    row_lo: int
+    row_hi: int
+    ctl: object        # torch.uint8[256] device control block
+    d: int = 1
+
+    @property
+    def shape(self):
+        return (self.row_hi - self.row_lo, self.n)
+
+    def numpy(self) -> np.ndarray:
+        return self.a[:, : self.n].double().cpu().numpy()
+
+
+@dataclass
+class NormalizedAffinity:
+    """W = D^-1 A without the second n^2 pass (k_normalize, folded into the GEMV)."""
+
+    a: object          # torch.float32 [rows, lda]
+    deg: object        # torch.float64 [rows] or None (already stochastic)
+    n: int
+    lda: int
+
+    @property
+    def shape(self):
+        return (self.a.shape[0], self.n)
+
+    def numpy(self) -> np.ndarray:
+        w = self.a[:, : self.n].double()
+        if self.deg is not None:
+            w = w / self.deg[:, None]
+        return w.cpu().numpy()
+
+
+def _as_device_matrix(w, dev):
+    """numpy (rows, n) -> fp32 device matrix with a 32-float pitch."""
+    torch = _torch()
+    w = np.asarray(w, dtype=np.float64)
+    if w.ndim != 2:
+        raise InvalidSpec(f"expected a matrix, got shape {w.shape}")
+    rows, n = w.shape
+    lda = int(_lib.lib().gpic_affinity_pitch(n))
+    t = torch.zeros((rows, lda), dtype=torch.float32, device=dev)
+    t[:, :n] = torch.from_numpy(w.astype(np.float32))
+    return t, rows, n, lda
+
+
+def _vec64(v, dev):
+    torch = _torch()
+    if isinstance(v, np.ndarray) or not hasattr(v, "is_cuda"):
+        arr = np.ascontiguousarray(np.asarray(v, dtype=np.float64).reshape(-1))
+        return torch.from_numpy(arr).to(dev), True
+    return v.to(device=dev, dtype=torch.float64).contiguous().reshape(-1), False
+
+
+def _vec32_padded(v64, n, dev):
+    torch = _torch()
+    lda = int(_lib.lib().gpic_affinity_pitch(n))
+    out = torch.zeros(lda, dtype=torch.float32, device=dev)
+    out[:n] = v64.to(torch.float32)
+    return out
+
+
+# ----------------------------------------------------------------- stages
+def k_affinity(d: DataSet, kind, config: KernelConfig | None = None,
+               rows: tuple[int, int] | None = None) -> DeviceAffinity:
+    """Affinity row block on the device (parallel.py:113-128, affinity.py:74-110).
+
+    Runs the fp64 centring/validation prepass, the selected Gram engine with
+    the fused exp/diagonal/row-sum epilogue, and the fixed-order degree
+    combine. Raises NonFiniteEntry like validate_dataset (data.py:69-72).
+    """
+    torch = _torch()
+    config = config or KernelConfig()
+    sigma = _check_kind(kind)
+    check_shape(d)
+    check_labels(d)
+    dev = _device(config)
+    L = _lib.lib()
+    n, m = d.points.shape
+    lo, hi = rows if rows is not None else (0, n)
+    st = _stream(dev)
+    x = torch.from_numpy(d.points).to(dev, non_blocking=True)
+    dp = int(L.gpic_feature_pitch(m))
+    npad = int(L.gpic_row_pad(n))
+    xhi = torch.empty((npad, dp), dtype=torch.float32, device=dev)
+    xlo = torch.empty_like(xhi)
+    sqn = torch.empty(npad, dtype=torch.float32, device=dev)
+    ctl = _new_ctl(dev)
+    prep = torch.empty(((n + 255) // 256 + 1) * m + m, dtype=torch.float64, device=dev)
+    _lib.check(L.gpic_prepare_points(_ptr(x), n, m, _ptr(xhi), _ptr(xlo), _ptr(sqn), _ptr(prep),
+                                     _ptr(ctl), st))
+    h = _read_ctl(ctl, dev)
+    _raise_ctl(h, m)
+    lda = int(L.gpic_affinity_pitch(n))
+    nrows = hi - lo
+    a = torch.empty((nrows, lda), dtype=torch.float32, device=dev)
+    deg = torch.empty(nrows, dtype=torch.float64, device=dev)
+    rows_pad = -(-nrows // 128) * 128
+    rowpart = torch.empty(((n + 127) // 128) * rows_pad, dtype=torch.float32, device=dev)
+    impl = _lib.AFFINITY_TC if config.affinity_impl == "tc" else _lib.AFFINITY_SIMT
+    _lib.check(L.gpic_affinity_rbf(_ptr(xhi), _ptr(xlo), _ptr(sqn), n, m, lo, hi, sigma, impl,
+                                   _ptr(a), lda, _ptr(deg), _ptr(rowpart), _ptr(ctl), st))
+    return DeviceAffinity(a=a, deg=deg, n=n, lda=lda, row_lo=lo, row_hi=hi, ctl=ctl, d=m)
+
+
+def k_rowsum(a, config: KernelConfig | None = None):
+    """Row sums = degrees (parallel.py:131-143). ZeroDegree(first row) if any <= 0."""
+    torch = _torch()
+    if isinstance(a, DeviceAffinity):
+        h = _read_ctl(a.ctl, a.a.device)
+        _raise_ctl(h, a.d)
+        return a.deg
+    dev = _device(config)
+    t, rows, n, lda = _as_device_matrix(a, dev)
+    ones = torch.zeros(lda, dtype=torch.float32, device=dev)
+    ones[:n] = 1.0
+    out = torch.empty(rows, dtype=torch.float64, device=dev)
+    _lib.check(_lib.lib().gpic_matvec(_ptr(t), lda, rows, n, _ptr(ones), None, _ptr(out),
+                                      _stream(dev)))
+    res = out.cpu().numpy()
+    bad = np.flatnonzero(res <= 0.0)
+    if bad.size:
+        raise ZeroDegree(int(bad[0]))
+    return res
+
+
+def k_normalize(a, deg, config: KernelConfig | None = None):
+    """W = A / deg (parallel.py:146-158), folded: returns a lazy NormalizedAffinity."""
+    torch = _torch()
+    if isinstance(a, DeviceAffinity):
+        if deg is not a.deg:
+            deg_t, _ = _vec64(deg, a.a.device)
+        else:
+            deg_t = a.deg
+        return NormalizedAffinity(a=a.a, deg=deg_t, n=a.n, lda=a.lda)
+    deg_np = np.asarray(deg, dtype=np.float64)
+    bad = np.flatnonzero(deg_np <= 0.0)
+    if bad.size:
+        raise ZeroDegree(int(bad[0]))
+    dev = _device(config)
+    t, rows, n, lda = _as_device_matrix(a, dev)
+    return NormalizedAffinity(a=t, deg=torch.from_numpy(deg_np).to(dev), n=n, lda=lda)
+
+
+def k_reduce(v, config: KernelConfig | None = None) -> float:
+    """Fixed-shape fp64 tree sum (parallel.py:161-178)."""
+    torch = _torch()
+    dev = _device(config) if not hasattr(v, "is_cuda") else v.device
+    t, _ = _vec64(v, dev)
+    n = t.numel()
+    if n == 0:
+        raise EmptyVector()
+    work = torch.empty(256 + 8 * ((n + 2047) // 2048 + 1), dtype=torch.uint8, device=dev)
+    out = torch.empty(1, dtype=torch.float64, device=dev)
+    _lib.check(_lib.lib().gpic_reduce_sum(_ptr(t), n, _ptr(out), _ptr(work), _stream(dev)))
+    return float(out.item())
+
+
+def k_norm(v, tau: float, config: KernelConfig | None = None):
+    """v / tau (parallel.py:181-193); NonPositiveTau when tau <= 0 or NaN."""
+    torch = _torch()
+    if not (tau > 0.0):
+        raise NonPositiveTau(tau)
+    dev = _device(config) if not hasattr(v, "is_cuda") else v.device
+    t, was_np = _vec64(v, dev)
+    out = torch.empty_like(t)
+    _lib.check(_lib.lib().gpic_scale(_ptr(t), t.numel(), float(tau), _ptr(out), None, 0,
+                                     _stream(dev)))
+    return out.cpu().numpy() if was_np else out
+
+
+def k_multiply(w, v, config: KernelConfig | None = None):
+    """W @ v (parallel.py:196-207): fp32 W / v streamed, fp64 row results."""
+    torch = _torch()
+    was_np = not isinstance(w, (NormalizedAffinity, DeviceAffinity))
+    if was_np:
+        wn = np.asarray(w)
+        if wn.ndim != 2 or wn.shape[1] != np.asarray(v).reshape(-1).shape[0]:
+            raise DimensionMismatch(wn.shape, np.asarray(v).shape)
+        dev = _device(config)
+        a, rows, n, lda = _as_device_matrix(wn, dev)
+        scale = None
+    else:
+        a, n, lda, rows = w.a, w.n, w.lda, w.a.shape[0]
+        dev = a.device
+        scale = getattr(w, "deg", None) if isinstance(w, NormalizedAffinity) else None
+        if isinstance(w, DeviceAffinity):
+            scale = None
+    v64, v_np = _vec64(v, dev)
+    if v64.numel() != n:
+        raise DimensionMismatch((rows, n), tuple(v64.shape))
+    v32 = _vec32_padded(v64, n, dev)
+    out = torch.empty(rows, dtype=torch.float64, device=dev)
+    _lib.check(_lib.lib().gpic_matvec(_ptr(a), lda, rows, n, _ptr(v32), _ptr(scale), _ptr(out),
+                                      _stream(dev)))
+    return out.cpu().numpy() if (was_np or v_np) else out
+
+
+def initial_embedding(deg, params: PicParams, config: KernelConfig | None = None):
+    """Start vector (parallel.py:210-214 / serial.py:77-101)."""
+    torch = _torch()
+    was_np = not hasattr(deg, "is_cuda")
+    dev = _device(config) if was_np else deg.device
+    d64, _ = _vec64(deg, dev)
+    n = d64.numel()
+    choice = params.v0
+    if isinstance(choice, str) and choice == "degree":
+        v64 = torch.empty(n, dtype=torch.float64, device=dev)
+        v32 = torch.empty(int(_lib.lib().gpic_affinity_pitch(n)), dtype=torch.float32, device=dev)
+        ctl = _new_ctl(dev)
+        work = torch.empty(((n + 2047) // 2048 + 2), dtype=torch.float64, device=dev)
+        if was_np and np.any(np.asarray(deg) <= 0.0):
+            raise ZeroDegree(int(np.flatnonzero(np.asarray(deg) <= 0.0)[0]))
+        _lib.check(_lib.lib().gpic_initial_vector(_ptr(d64), n, _ptr(v64), _ptr(v32), _ptr(work),
+                                                  _ptr(ctl), _stream(dev)))
+        return v64.cpu().numpy() if was_np else v64
+    if isinstance(choice, str):
+        if choice != "uniform":
+            raise InvalidSpec(f"unknown initial vector kind {choice!r}")
+        v = np.full(n, 1.0 / n)
+    else:
+        v = np.asarray(choice, dtype=np.float64).copy()
+        if v.shape != (n,):
+            raise InvalidSpec(f"explicit v0 has length {v.size}, expected {n}")
+        if v.min() < 0.0:
+            raise InvalidSpec("explicit v0 must be nonnegative")
+        if abs(v.sum() - 1.0) > 1e-12:
+            raise InvalidSpec("explicit v0 must have unit L1 norm within 1e-12")
+    return v if was_np else torch.from_numpy(v).to(dev)
+
+
+def iterate(w, v, params: PicParams, config: KernelConfig | None = None):
+    """Device-resident power iteration (parallel.py:217-233, serial.py:104-128)."""
+    torch = _torch()
+    if isinstance(w, DeviceAffinity):
+        w = NormalizedAffinity(a=w.a, deg=None, n=w.n, lda=w.lda)
+    was_np = not isinstance(w, NormalizedAffinity)
+    if was_np:
+        wn = np.asarray(w, dtype=np.float64)
+        if wn.ndim != 2 or wn.shape[0] != wn.shape[1]:
+            raise InvalidSpec(f"expected a square matrix, got shape {wn.shape}")
+        dev = _device(config)
+        a, rows, n, lda = _as_device_matrix(wn, dev)
+        w = NormalizedAffinity(a=a, deg=None, n=n, lda=lda)
+    dev = w.a.device
+    n = w.n
+    if w.a.shape[0] != n:
+        raise InvalidSpec("iterate on one device needs the whole matrix (use cluster(p>1) for shards)")
+    v64_in, v_np = _vec64(v, dev)
+    if v64_in.numel() != n:
+        raise DimensionMismatch((n, n), tuple(v64_in.shape))
+    eps = params.resolved_epsilon(n)
+    T = params.max_iterations
+    v64 = torch.empty(2 * n, dtype=torch.float64, device=dev)
+    v64[:n] = v64_in
+    v32 = _vec32_padded(v64_in, n, dev)
+    hist = torch.zeros(T, dtype=torch.float64, device=dev)
+    out = torch.empty(n, dtype=torch.float64, device=dev)
+    ctl = _new_ctl(dev, eps, T)
+    work = torch.empty(n + (n + 2047) // 2048 + 2, dtype=torch.float64, device=dev)
+    _lib.check(_lib.lib().gpic_power_iterate(_ptr(w.a), w.lda, _ptr(w.deg), n, _ptr(v64),
+                                             _ptr(v32), eps, T, _ptr(hist), _ptr(out), _ptr(work),
+                                             _ptr(ctl), _stream(dev)))
+    h = _read_ctl(ctl, dev)
+    _raise_ctl(h)
+    trace = PicTrace(int(h.iter), hist[: h.iter].cpu().numpy(), bool(h.converged))
+    return (out.cpu().numpy() if (was_np or v_np) else out), trace
+
+
+def kmeans_1d(values, params: KMeansParams, config: KernelConfig | None = None):
+    """GPU 1-D k-means with the reference's seeding, ties and canonical labels."""
+    torch = _torch()
+    was_np = not hasattr(values, "is_cuda")
+    dev = _device(config) if was_np else values.device
+    v, _ = _vec64(values, dev)
+    n = v.numel()
+    k = params.k
+    if k > n:
+        raise KTooLarge(k, n)
+    if k > KMEANS_MAX_K:
+        raise InvalidSpec(f"the device k-means holds at most {KMEANS_MAX_K} centres")
+    first, u = kmeans_draws(n, k, params.seed)
+    L = _lib.lib()
+    scratch = torch.empty(int(L.gpic_kmeans_scratch_bytes(n, k)), dtype=torch.uint8, device=dev)
+    labels = torch.empty(n, dtype=torch.int64, device=dev)
+    ctl = _new_ctl(dev)
+    _lib.check(L.gpic_kmeans1d(_ptr(v), n, k, first, u.ctypes.data_as(C.c_void_p),
+                               params.max_rounds, params.tol, _ptr(labels), _ptr(scratch),
+                               _ptr(ctl), _stream(dev)))
+    h = _read_ctl(ctl, dev)
+    _raise_ctl(h)
+    return labels.cpu().numpy() if was_np else labels
+
+
+# ------------------------------------------------------------- pipeline
+def workspace_bytes(n: int, d: int, k: int, max_iter: int) -> int:
+    """Device bytes one cluster() call needs: scratch + the n x pitch fp32 A."""
+    L = _lib.lib()
+    scratch = int(L.gpic_workspace_bytes(n, d, k, n, max_iter))
+    return scratch + n * int(L.gpic_affinity_pitch(n)) * 4
+
+
+def cluster(d: DataSet, kind, params: PicParams, config: KernelConfig | None = None, seed: int = 0):
+    """End-to-end PIC on the GPU: (labels int64[n], v float64[n], PicTrace).
+
+    Same contract as parallel.cluster (parallel.py:236-255). One libgpic call
+    runs centring, affinity + degree, the start vector, the device-resident
+    power iteration and the k-means; the host syncs twice (after the loop and
+    at the end).
+    """
+    torch = _torch()
+    config = config or KernelConfig()
+    sigma = _check_kind(kind)
+    check_shape(d)
+    check_labels(d)
+    n, m = d.points.shape
+    k = params.k
+    if k > n:
+        raise KTooLarge(k, n)
+    if k > KMEANS_MAX_K:
+        raise InvalidSpec(f"the device k-means holds at most {KMEANS_MAX_K} centres")
+    if config.p > 1:
+        from . import sharded
+
+        return sharded.cluster(d, kind, params, config, seed)
+    if not (isinstance(params.v0, str) and params.v0 == "degree"):
+        return _cluster_stagewise(d, kind, params, config, seed)
+    dev = _device(config)
+    L = _lib.lib()
+    eps = params.resolved_epsilon(n)
+    T = params.max_iterations
+    impl = _lib.AFFINITY_TC if config.affinity_impl == "tc" else _lib.AFFINITY_SIMT
+    x = torch.from_numpy(d.points).to(dev, non_blocking=True)
+    nbytes = workspace_bytes(n, m, k, T)
+    work = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    labels = torch.empty(n, dtype=torch.int64, device=dev)
+    v = torch.empty(n, dtype=torch.float64, device=dev)
+    hist = torch.zeros(T, dtype=torch.float64, device=dev)
+    first, u = kmeans_draws(n, k, seed)
+    iters = C.c_int32(0)
+    conv = C.c_int32(0)
+    rc = L.gpic_cluster(_ptr(x), n, m, sigma, k, eps, T, first, u.ctypes.data_as(C.c_void_p),
+                        impl, _ptr(labels), _ptr(v), _ptr(hist), C.byref(iters), C.byref(conv),
+                        _ptr(work), nbytes, _stream(dev))
+    if rc != _lib.GPIC_OK:
+        h = _lib.Ctl()
+        if L.gpic_ctl_read(_ptr(work), C.byref(h), _stream(dev)) == 0 and h.status == rc:
+            _lib.raise_for(rc, h, m)
+        _lib.raise_for(rc, None, m)
+    it = int(iters.value)
+    return (labels.cpu().numpy(), v.cpu().numpy(),
+            PicTrace(it, hist[:it].cpu().numpy(), bool(conv.value)))
+
+
+def _cluster_stagewise(d, kind, params, config, seed):
+    a = k_affinity(d, kind, config)
+    deg = k_rowsum(a, config)
+    w = k_normalize(a, deg, config)
+    v = initial_embedding(deg, params, config)
+    v, trace = iterate(w, v, params, config)
+    labels = kmeans_1d(v, KMeansParams(k=params.k, seed=seed), config)
+    return labels.cpu().numpy(), v.cpu().numpy(), trace

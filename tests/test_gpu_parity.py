@@ -1,0 +1,282 @@
+"""GPU parity: libgpic vs the reference (golden fixtures) and the CPU oracle.
+
+Tolerances (fp32 engine against the fp64 reference):
+  * labels identical (canonical ids, so plain equality),
+  * v within 1e-4 relative L1 at a forced equal iteration count
+    (epsilon = 5e-324, the reference's test_serial.py:23 idiom),
+  * iteration count within +-2 under the native stop rule,
+  * affinity entries within 2e-5 relative of the fp64 values,
+  * degrees within 1e-5 relative.
+"""
+
+import json
+
+import numpy as np
+import pytest
+
+from oracle import pic_oracle as po
+from paper_1604_02700_b200 import (
+    DataSet,
+    GaussianRbf,
+    KernelConfig,
+    KMeansParams,
+    PicParams,
+    adjusted_rand_index,
+    cluster,
+    contingency,
+    errors,
+    gaussian_blobs,
+)
+
+from conftest import GOLDEN
+
+pytestmark = pytest.mark.gpu
+
+TINY_EPS = 5e-324
+ENGINES = ["simt", "tc"]
+
+
+def _gpu():
+    from paper_1604_02700_b200 import gpu
+
+    return gpu
+
+
+def _points(z):
+    if "X" in z:
+        return z["X"]
+    g = json.loads(str(z["gen"]))
+    return gaussian_blobs(g["n"], g["d"], g["k"], seed=g["seed"], sizes=g.get("sizes", "graded")).points
+
+
+def rel_l1(a, b):
+    return float(np.abs(a - b).sum() / np.abs(b).sum())
+
+
+def _engine_ok(engine):
+    if engine == "tc":
+        try:
+            d = DataSet(np.random.default_rng(0).normal(size=(256, 8)))
+            _gpu().k_affinity(d, GaussianRbf(1.0), KernelConfig(affinity_impl="tc"))
+        except errors.DeviceError as e:  # pragma: no cover
+            if "not built" in str(e):
+                pytest.skip("tcgen05 engine not built yet")
+            raise
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+@pytest.mark.parametrize("case", ["config1", "gblobs_small", "gblobs_balanced"])
+def test_cluster_matches_reference(golden, case, engine):
+    _engine_ok(engine)
+    z = golden(case)
+    d = DataSet(_points(z))
+    labels, v, trace = cluster(d, GaussianRbf(float(z["sigma"])), PicParams(k=int(z["k"])),
+                               config=KernelConfig(affinity_impl=engine), seed=int(z["seed"]))
+    assert labels.dtype == np.int64 and v.dtype == np.float64
+    assert np.array_equal(labels, z["labels"])
+    assert abs(trace.iterations_run - int(z["iterations"])) <= 2
+    assert trace.converged == bool(z["converged"])
+    assert len(trace.delta_history) == trace.iterations_run
+    t = min(trace.iterations_run, int(z["iterations"]))
+    assert np.allclose(trace.delta_history[:t], z["deltas"][:t], rtol=2e-3, atol=1e-12)
+    assert rel_l1(v, z["v"]) <= 1e-4
+    assert abs(v.sum() - 1.0) <= 1e-12
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+def test_forced_iteration_parity(golden, engine):
+    _engine_ok(engine)
+    z = golden("config1")
+    d = DataSet(z["X"])
+    for t in (1, 3, 10):
+        _, v, trace = cluster(d, GaussianRbf(1.0), PicParams(k=3, epsilon=TINY_EPS, max_iterations=t),
+                              config=KernelConfig(affinity_impl=engine))
+        assert trace.iterations_run == t and not trace.converged
+        assert rel_l1(v, z[f"v_T{t}"]) <= 1e-4
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+def test_affinity_rows_and_degree(golden, engine):
+    _engine_ok(engine)
+    gpu = _gpu()
+    for case in ("config1", "gblobs_small"):
+        z = golden(case)
+        d = DataSet(_points(z))
+        a = gpu.k_affinity(d, GaussianRbf(float(z["sigma"])), KernelConfig(affinity_impl=engine))
+        deg = gpu.k_rowsum(a).cpu().numpy()
+        assert np.max(np.abs(deg - z["deg"]) / z["deg"]) <= 1e-5
+        full = a.numpy()
+        for r, row in zip(z["a_rows_idx"], z["a_rows"]):
+            got = full[int(r)]
+            assert got[int(r)] == 0.0
+            assert np.max(np.abs(got - row)) <= 2e-5 * max(row.max(), 1e-30) + 1e-30
+        # exact symmetry is a property of the formula; fp32 engine keeps it to rounding
+        assert np.max(np.abs(full - full.T)) <= 1e-6
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+def test_row_shards_are_bitwise_identical(engine):
+    """Rows built in shards equal the same rows built whole (P-invariance)."""
+    _engine_ok(engine)
+    gpu = _gpu()
+    d = gaussian_blobs(3000, 16, 4, seed=5)
+    kind = GaussianRbf(2.0)
+    whole = gpu.k_affinity(d, kind, KernelConfig(affinity_impl=engine))
+    for lo, hi in ((0, 1000), (1000, 2177), (2177, 3000), (5, 6)):
+        part = gpu.k_affinity(d, kind, KernelConfig(affinity_impl=engine), rows=(lo, hi))
+        assert np.array_equal(part.a[:, : d.n].cpu().numpy(), whole.a[lo:hi, : d.n].cpu().numpy())
+        assert np.array_equal(part.deg.cpu().numpy(), whole.deg[lo:hi].cpu().numpy())
+
+
+def test_simt_and_tc_agree():
+    _engine_ok("tc")
+    gpu = _gpu()
+    d = gaussian_blobs(2000, 64, 5, seed=9)
+    kind = GaussianRbf(4.0)
+    a = gpu.k_affinity(d, kind, KernelConfig(affinity_impl="simt")).numpy()
+    b = gpu.k_affinity(d, kind, KernelConfig(affinity_impl="tc")).numpy()
+    ref = po.rbf_rows(d.points, 0, 64, 4.0)
+    for got in (a[:64], b[:64]):
+        mask = ref > 1e-30
+        assert np.max(np.abs(got[mask] - ref[mask]) / ref[mask]) <= 5e-5
+
+
+def test_deterministic_repeat():
+    d = gaussian_blobs(2500, 32, 5, seed=1)
+    r1 = cluster(d, GaussianRbf(2.8284271247461903), PicParams(k=5), seed=4)
+    r2 = cluster(d, GaussianRbf(2.8284271247461903), PicParams(k=5), seed=4)
+    assert np.array_equal(r1[0], r2[0])
+    assert np.array_equal(r1[1], r2[1])
+    assert np.array_equal(r1[2].delta_history, r2[2].delta_history)
+
+
+def test_kmeans_cases(golden):
+    z = golden("kmeans")
+    gpu = _gpu()
+    off = z["offsets"]
+    for i, (k, s) in enumerate(zip(z["k"], z["seed"])):
+        v = z["values"][off[i]: off[i + 1]]
+        got = gpu.kmeans_1d(v, KMeansParams(k=int(k), seed=int(s)))
+        assert np.array_equal(got, z["labels"][off[i]: off[i + 1]]), f"case {i} n={v.size} k={k}"
+
+
+def test_kmeans_random_vs_oracle():
+    gpu = _gpu()
+    rng = np.random.default_rng(77)
+    for trial in range(20):
+        k = int(rng.integers(2, 12))
+        levels = np.sort(rng.uniform(1e-6, 1e-4, k))
+        n = int(rng.integers(200, 9000))
+        v = rng.choice(levels, n) * (1 + 1e-3 * rng.standard_normal(n))
+        got = gpu.kmeans_1d(v, KMeansParams(k=k, seed=trial))
+        assert np.array_equal(got, po.kmeans_1d(v, k, trial)), f"trial {trial}"
+
+
+def test_kernel_kats(golden):
+    gpu = _gpu()
+    z = golden("kernels")
+    pos = 0
+    for ln, s in zip(z["reduce_lens"], z["reduce_sums"]):
+        got = gpu.k_reduce(z["reduce_vals"][pos: pos + ln])
+        assert abs(got - s) <= 1e-12 * max(1.0, abs(s))
+        pos += ln
+    with pytest.raises(errors.EmptyVector):
+        gpu.k_reduce(np.array([]))
+    assert gpu.k_reduce(np.array([1.0, 2.0, 3.0, 4.0])) == 10.0
+    assert np.array_equal(gpu.k_norm(np.array([2.0, 2.0]), 4.0), [0.5, 0.5])
+    with pytest.raises(errors.NonPositiveTau):
+        gpu.k_norm(np.array([1.0]), 0.0)
+    with pytest.raises(errors.NonPositiveTau):
+        gpu.k_norm(np.array([1.0]), float("nan"))
+    out = gpu.k_multiply(z["mul_w"], z["mul_v"])
+    assert np.max(np.abs(out - z["mul_out"]) / np.abs(z["mul_out"])) <= 1e-6
+    assert np.array_equal(gpu.k_multiply(np.array([[0.0, 1.0], [1.0, 0.0]]), np.array([0.25, 0.75])),
+                          [0.75, 0.25])
+    with pytest.raises(errors.DimensionMismatch):
+        gpu.k_multiply(np.ones((3, 3)), np.ones(4))
+    assert np.array_equal(gpu.k_rowsum(np.ones((4, 4)) - np.eye(4)), [3.0, 3.0, 3.0, 3.0])
+    with pytest.raises(errors.ZeroDegree) as e:
+        gpu.k_rowsum(np.zeros((1, 1)))
+    assert e.value.index == 0
+
+
+def test_power_iteration_kats(golden):
+    gpu = _gpu()
+    z = golden("kernels")
+    v, tr = gpu.iterate(np.eye(3), np.full(3, 1 / 3), PicParams(k=2, epsilon=1e-8))
+    assert tr.converged and tr.iterations_run == 2
+    assert np.array_equal(v, np.full(3, 1 / 3))
+    v, tr = gpu.iterate(np.array([[0.0, 1.0], [1.0, 0.0]]), np.array([0.5, 0.5]),
+                        PicParams(k=2, epsilon=1e-8))
+    assert tr.converged and tr.iterations_run == 2 and np.array_equal(v, [0.5, 0.5])
+    v, tr = gpu.iterate(z["w8"], np.full(8, 1 / 8), PicParams(k=2, epsilon=1e-6, max_iterations=30))
+    assert abs(tr.iterations_run - int(z["it8"])) <= 2
+    assert rel_l1(v, z["v8"]) <= 1e-6
+
+
+def test_errors_match_reference():
+    e = json.loads((GOLDEN / "errors.json").read_text())
+    with pytest.raises(errors.ZeroDegree) as info:
+        cluster(DataSet(np.array(e["zero_degree"]["points"])), GaussianRbf(1.0), PicParams(k=2))
+    assert info.value.index == e["zero_degree"]["index"]
+    bad = np.ones((5, 3))
+    bad[3, 1] = np.nan
+    bad[4, 0] = np.inf
+    with pytest.raises(errors.NonFiniteEntry) as info:
+        cluster(DataSet(bad), GaussianRbf(1.0), PicParams(k=2))
+    assert (info.value.row, info.value.col) == (e["non_finite"]["row"], e["non_finite"]["col"])
+    with pytest.raises(errors.KTooLarge):
+        _gpu().kmeans_1d(np.array([0.5, 0.5]), KMeansParams(k=3))
+    with pytest.raises(errors.KTooLarge):
+        cluster(DataSet(np.ones((2, 2))), GaussianRbf(1.0), PicParams(k=3))
+    with pytest.raises(errors.InvalidSpec):
+        from paper_1604_02700_b200 import Cosine
+
+        cluster(DataSet(np.ones((4, 2))), Cosine(), PicParams(k=2))
+
+
+def test_stagewise_pipeline_matches_fused(golden):
+    """run_timed-style stage calls (report.py:78-95) give the fused result."""
+    gpu = _gpu()
+    z = golden("gblobs_small")
+    d = DataSet(_points(z))
+    kind, params = GaussianRbf(float(z["sigma"])), PicParams(k=int(z["k"]))
+    a = gpu.k_affinity(d, kind)
+    deg = gpu.k_rowsum(a)
+    w = gpu.k_normalize(a, deg)
+    v = gpu.initial_embedding(deg, params)
+    v, trace = gpu.iterate(w, v, params)
+    labels = gpu.kmeans_1d(v, KMeansParams(k=params.k, seed=int(z["seed"])))
+    fl, fv, ft = cluster(d, kind, params, seed=int(z["seed"]))
+    assert np.array_equal(labels.cpu().numpy(), fl)
+    assert np.array_equal(v.cpu().numpy(), fv)
+    assert np.array_equal(trace.delta_history, ft.delta_history)
+
+
+def test_uniform_and_explicit_start_vector(golden):
+    z = golden("config1")
+    d = DataSet(z["X"])
+    a = po.affinity(z["X"], 1.0)
+    w = po.normalize(a, po.degree(a))
+    for v0 in ("uniform", np.full(1000, 1e-3)):
+        _, v, tr = cluster(d, GaussianRbf(1.0), PicParams(k=3, epsilon=TINY_EPS, max_iterations=4, v0=v0))
+        ref, _, _ = po.power_iteration(w, po.start_vector(po.degree(a), v0), TINY_EPS, 4)
+        assert rel_l1(v, ref) <= 1e-4
+
+
+@pytest.mark.slow
+def test_config2_scale_parity():
+    """Config 2 (n=20k, d=32, k=5): labels vs truth and vs oracle at forced T."""
+    d = gaussian_blobs(20_000, 32, 5, seed=0)
+    sigma = float(np.sqrt(32) / 2)
+    labels, v, trace = cluster(d, GaussianRbf(sigma), PicParams(k=5), seed=0)
+    assert adjusted_rand_index(contingency(d.labels, labels)) == 1.0
+    assert 3 <= trace.iterations_run <= 20
+    # the CPU oracle on 20k points (3.2 GB fp64) is affordable at forced T = 3
+    a = po.affinity(d.points, sigma)
+    deg = po.degree(a)
+    w = po.normalize(a, deg)
+    del a
+    ref, _, _ = po.power_iteration(w, po.start_vector(deg), TINY_EPS, 3)
+    _, v3, _ = cluster(d, GaussianRbf(sigma), PicParams(k=5, epsilon=TINY_EPS, max_iterations=3))
+    assert rel_l1(v3, ref) <= 1e-4
