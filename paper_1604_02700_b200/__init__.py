@@ -31,9 +31,9 @@ BACKENDS = ("gpu",)
 
 
 def _gpu():
-    from . import gpu
+    import importlib
 
-    return gpu
+    return importlib.import_module(".gpu", __name__)
 
 
 def cluster(dataset, kind, params, backend="gpu", config=None, seed=0):

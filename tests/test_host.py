@@ -116,6 +116,19 @@ class TestParams:
         for (a0, a1), (b0, b1) in zip(ranges, ranges[1:]):
             assert a1 == b0 and a0 < a1
 
+    def test_no_cpu_fallback(self):
+        import torch
+
+        import paper_1604_02700_b200 as pkg
+
+        assert pkg.gpu.cluster is pkg.k_affinity.__globals__["cluster"]
+        if torch.cuda.is_available():
+            pytest.skip("checks the no-device behaviour")
+        with pytest.raises(errors.DeviceError):
+            cluster(DataSet(np.ones((4, 2))), GaussianRbf(1.0), PicParams(k=2))
+        with pytest.raises(errors.DeviceError):
+            pkg.kmeans_1d(np.ones(5), KMeansParams(k=2))
+
     def test_unknown_backend(self):
         d = DataSet(np.ones((3, 2)))
         with pytest.raises(errors.InvalidSpec):
