@@ -1,9 +1,469 @@
-// placeholder until the tcgen05 engine lands
+// Stage 1 (tensor-core engine): affinity row block on tcgen05 with a fused
+// exp / diagonal / row-sum epilogue.
+//
+//   G = Xc_I Xc_J^T via 3xTF32: G ~= hi_I.lo_J + lo_I.hi_J + hi_I.hi_J, where
+//   xc = hi + lo exactly (hi = TF32(xc), prepare.cu), each term a
+//   tcgen05.mma.kind::tf32 (M=128, N=128, K=8) accumulating in TMEM (fp32).
+//   a_ij = exp2(min(ns*(|x_i|^2 + |x_j|^2 - 2 G_ij), 0)),  ns = -log2(e)/(2 sigma^2)
+//   a_ii = 0, a_ij = 0 for padding columns                  (affinity.py:96-103)
+//
+// Persistent warp-specialised kernel, one CTA per SM (320 threads):
+//   warp 0      TMA producer: the CTA's row block (MB x 128 rows, hi + lo,
+//               all K) stays resident in smem while the CTA walks its
+//               contiguous range of column tiles; B tiles (128 columns,
+//               hi + lo, one 32-wide K block per stage) stream through a
+//               ring of smem stages.
+//   warp 1      TMEM owner + single-thread MMA issuer: 3 x 4 x KB MMAs per
+//               M block into one of two TMEM accumulators (double buffer,
+//               so the next tile's MMAs overlap this tile's epilogue).
+//   warps 2-9   epilogue: tcgen05.ld 32 columns at a time, exp2 + masks +
+//               row sums in registers, swizzled st.shared, TMA bulk-tensor
+//               store of 32x32 fp32 boxes (the kernel is bound by this
+//               4n^2-byte store stream), fp32 row partials per 128-column
+//               tile for the fixed-order degree combine (degree_kernel).
+//
+// The row block stays resident, so operand traffic per output byte is
+// 2*d/(128*MB) for B only (0.5x at d=64, MB=2).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "common.cuh"
 #include "ops.h"
+
 namespace gpic {
-int launch_affinity_tc(const float*, const float*, const float*, int64_t, int32_t, int64_t,
-                       int64_t, float, float*, int64_t, float*, int64_t, cudaStream_t) {
-  return fail(GPIC_E_UNSUPPORTED, "tcgen05 affinity engine not built");
+
+namespace {
+
+constexpr int kBN = 128;           // columns per tile (one MMA N)
+constexpr int kKBlk = 32;          // fp32 per 128-byte swizzle row
+constexpr int kTileBytes = 128 * kKBlk * 4;  // 16 KB: 128 rows x 32 fp32
+constexpr int kEpiWarps = 8;
+constexpr int kThreads = 64 + kEpiWarps * 32;
+constexpr int kStageOutBytes = 32 * 128;     // 32 rows x 32 fp32 per epilogue warp
+constexpr int kSmemBudget = 224 * 1024;
+
+__host__ __device__ constexpr int mblocks(int KB) { return KB <= 2 ? 2 : 1; }
+__host__ __device__ constexpr int a_bytes(int KB) { return 2 * mblocks(KB) * KB * kTileBytes; }
+__host__ __device__ constexpr int stages(int KB) {
+  return (kSmemBudget - a_bytes(KB) - kEpiWarps * kStageOutBytes) / (2 * kTileBytes) > 4
+             ? 4
+             : (kSmemBudget - a_bytes(KB) - kEpiWarps * kStageOutBytes) / (2 * kTileBytes);
 }
+__host__ __device__ constexpr int smem_bytes(int KB) {
+  return a_bytes(KB) + stages(KB) * 2 * kTileBytes + kEpiWarps * kStageOutBytes + 256 + 1024;
+}
+
+// ------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ uint32_t su32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
+      "@!P bra WAIT_%=;\n}" ::"r"(su32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+      "%3}], [%4];" ::"r"(su32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(su32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, int x, int y, const void* src) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(x), "r"(y), "r"(su32(src))
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void tma_store_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void tma_store_wait_all() {
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+__device__ __forceinline__ void fence_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_commit(uint64_t* b) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   su32(b))
+               : "memory");
+}
+__device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc,
+                                         uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+// K-major, 128-byte swizzle smem matrix descriptor (8-row groups 1024 B apart).
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+  uint64_t d = (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)1u << 16;            // leading byte offset (unused for SW128 K-major)
+  d |= (uint64_t)(1024u >> 4) << 32;  // stride byte offset: 8 rows x 128 B
+  d |= (uint64_t)1u << 46;            // sm_100 descriptor version
+  d |= (uint64_t)2u << 61;            // SWIZZLE_128B
+  return d;
+}
+// kind::tf32, fp32 accumulate, K-major A and B, M=128, N=128.
+constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(kBN >> 3) << 17) |
+                            ((uint32_t)(128 >> 4) << 24);
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%"
+      "15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+struct TcArgs {
+  const float* sqn;
+  int64_t n;
+  int64_t row_lo;
+  int64_t rows;
+  float ns;  // -log2(e) / (2 sigma^2)
+  float* rowpart;
+  int64_t rows_pad;
+  int64_t n_rtiles;  // row blocks of 128*MB rows
+  int64_t n_ctiles;  // column tiles of 128
+};
+
+template <int KB>
+__global__ void __launch_bounds__(kThreads, 1)
+    affinity_tc_kernel(const __grid_constant__ CUtensorMap map_hi,
+                       const __grid_constant__ CUtensorMap map_lo,
+                       const __grid_constant__ CUtensorMap map_out, const TcArgs args) {
+  constexpr int MB = mblocks(KB);
+  constexpr int ST = stages(KB);
+  constexpr int kTmemCols = 2 * MB * kBN;  // 2 accumulators
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* sA = base;                                     // [hl][m][kb] 16 KB tiles
+  uint8_t* sB = sA + a_bytes(KB);                         // [stage][hl] 16 KB tiles
+  uint8_t* sOut = sB + ST * 2 * kTileBytes;               // [epi warp] 4 KB
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sOut + kEpiWarps * kStageOutBytes);
+  uint64_t* full = bars;                 // [ST]
+  uint64_t* empty = bars + ST;           // [ST]
+  uint64_t* a_full = bars + 2 * ST;
+  uint64_t* a_empty = a_full + 1;
+  uint64_t* t_full = a_full + 2;         // [2]
+  uint64_t* t_empty = a_full + 4;        // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(a_full + 6);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int64_t total = args.n_rtiles * args.n_ctiles;
+  const int64_t t_begin = total * blockIdx.x / gridDim.x;
+  const int64_t t_end = total * (blockIdx.x + 1) / gridDim.x;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < ST; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(a_full, 1);
+    mbar_init(a_empty, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&t_full[b], 1);
+      mbar_init(&t_empty[b], kEpiWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_hi)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_lo)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_out)) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     su32(tmem_slot)),
+                 "r"(kTmemCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      int64_t cur_rb = -1;
+      uint32_t a_par = 1;
+      int s = 0;
+      uint32_t ph = 0;
+      for (int64_t t = t_begin; t < t_end; ++t) {
+        const int64_t rb = t / args.n_ctiles, cb = t % args.n_ctiles;
+        if (rb != cur_rb) {
+          mbar_wait(a_empty, a_par);
+          a_par ^= 1;
+          mbar_expect_tx(a_full, a_bytes(KB));
+          for (int hl = 0; hl < 2; ++hl)
+            for (int m = 0; m < MB; ++m)
+              for (int kb = 0; kb < KB; ++kb)
+                tma_load_2d(sA + ((hl * MB + m) * KB + kb) * kTileBytes, hl ? &map_lo : &map_hi,
+                            kb * kKBlk, (int)(args.row_lo + (rb * MB + m) * 128), a_full);
+          cur_rb = rb;
+        }
+        for (int kb = 0; kb < KB; ++kb) {
+          mbar_wait(&empty[s], ph ^ 1);
+          mbar_expect_tx(&full[s], 2 * kTileBytes);
+          tma_load_2d(sB + (s * 2 + 0) * kTileBytes, &map_hi, kb * kKBlk, (int)(cb * kBN), &full[s]);
+          tma_load_2d(sB + (s * 2 + 1) * kTileBytes, &map_lo, kb * kKBlk, (int)(cb * kBN), &full[s]);
+          if (++s == ST) { s = 0; ph ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------- MMA issuer
+    if (lane == 0) {
+      int64_t cur_rb = -1;
+      uint32_t a_par = 0;
+      uint32_t te_par[2] = {1, 1};
+      int s = 0;
+      uint32_t ph = 0;
+      int i = 0;
+      for (int64_t t = t_begin; t < t_end; ++t, ++i) {
+        const int64_t rb = t / args.n_ctiles;
+        if (rb != cur_rb) {
+          mbar_wait(a_full, a_par);
+          a_par ^= 1;
+          cur_rb = rb;
+        }
+        const int buf = i & 1;
+        mbar_wait(&t_empty[buf], te_par[buf]);
+        te_par[buf] ^= 1;
+        tc_fence_after();
+        for (int kb = 0; kb < KB; ++kb) {
+          mbar_wait(&full[s], ph);
+          tc_fence_after();
+          const uint64_t bh = sw128_desc(su32(sB + (s * 2 + 0) * kTileBytes));
+          const uint64_t bl = sw128_desc(su32(sB + (s * 2 + 1) * kTileBytes));
+#pragma unroll
+          for (int m = 0; m < MB; ++m) {
+            const uint32_t d = tmem_base + (uint32_t)((buf * MB + m) * kBN);
+            const uint64_t ah = sw128_desc(su32(sA + ((0 * MB + m) * KB + kb) * kTileBytes));
+            const uint64_t al = sw128_desc(su32(sA + ((1 * MB + m) * KB + kb) * kTileBytes));
+#pragma unroll
+            for (int k = 0; k < kKBlk / 8; ++k) {
+              const uint64_t off = (uint64_t)(k * 8 * 4 >> 4);  // 32 bytes along K
+              mma_tf32(d, ah + off, bl + off, kIdesc, (kb | k) != 0);
+              mma_tf32(d, al + off, bh + off, kIdesc, 1u);
+              mma_tf32(d, ah + off, bh + off, kIdesc, 1u);
+            }
+          }
+          tc_commit(&empty[s]);  // frees the B stage once these MMAs retire
+          if (++s == ST) { s = 0; ph ^= 1; }
+        }
+        tc_commit(&t_full[buf]);
+        const bool last_of_block = (t + 1 == t_end) || ((t + 1) / args.n_ctiles != rb);
+        if (last_of_block) tc_commit(a_empty);
+      }
+    }
+  } else {
+    // --------------------------------------------------------- epilogue
+    const int e = warp - 2;
+    const int q = warp & 3;          // TMEM lane quadrant this warp may access
+    const int g = e >> 2;            // group: M block (MB=2) or column half (MB=1)
+    const int m = MB == 2 ? g : 0;
+    const int c_lo = MB == 2 ? 0 : 2 * g;
+    const int c_hi = MB == 2 ? 4 : 2 * g + 2;
+    uint8_t* stage = sOut + e * kStageOutBytes;
+    const float ns = args.ns;
+    const float m2ns = -2.f * ns;
+    uint32_t tf_par[2] = {0, 0};
+    int i = 0;
+    bool pending = false;
+    for (int64_t t = t_begin; t < t_end; ++t, ++i) {
+      const int64_t rb = t / args.n_ctiles, cb = t % args.n_ctiles;
+      const int buf = i & 1;
+      const int64_t lr0 = (rb * MB + m) * 128 + q * 32;  // shard-local first row of this warp
+      const int64_t lr = lr0 + lane;
+      const int64_t gr = args.row_lo + lr;
+      const float ra = gr < args.n ? ns * __ldg(args.sqn + gr) : 0.f;
+      mbar_wait(&t_full[buf], tf_par[buf]);
+      tf_par[buf] ^= 1;
+      tc_fence_after();
+      float rsum = 0.f;
+      for (int c = c_lo; c < c_hi; ++c) {
+        uint32_t r[32];
+        tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)((buf * MB + m) * kBN + c * 32),
+                  r);
+        if (c == c_hi - 1) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&t_empty[buf]);
+        }
+        const int64_t col0 = cb * kBN + c * 32;
+        const float cb_lane = ns * __ldg(args.sqn + col0 + lane);
+        const bool diag = (col0 < args.row_lo + lr0 + 32) && (args.row_lo + lr0 < col0 + 32);
+        const bool pad = col0 + 32 > args.n;
+        float vals[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const float cj = __shfl_sync(0xffffffffu, cb_lane, j);
+          float arg = fmaf(__uint_as_float(r[j]), m2ns, ra + cj);
+          vals[j] = ex2(fminf(arg, 0.f));
+        }
+        if (diag || pad) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (col0 + j == gr || col0 + j >= args.n) vals[j] = 0.f;
+        }
+#pragma unroll
+        for (int j = 0; j < 32; ++j) rsum += vals[j];
+        // previous TMA store must have finished reading the staging buffer
+        if (pending) {
+          if (lane == 0) tma_store_wait_read();
+          __syncwarp();
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int chunk = j ^ (lane & 7);
+          *reinterpret_cast<float4*>(stage + lane * 128 + chunk * 16) =
+              make_float4(vals[4 * j], vals[4 * j + 1], vals[4 * j + 2], vals[4 * j + 3]);
+        }
+        fence_async_smem();
+        __syncwarp();
+        if (lane == 0) tma_store_2d(&map_out, (int)col0, (int)lr0, stage);
+        pending = true;
+      }
+      if constexpr (MB == 2) {
+        if (lr < args.rows) args.rowpart[cb * args.rows_pad + lr] = rsum;
+      } else {
+        // two warps (column halves) share each row: half 1 parks its sum in
+        // smem, half 0 adds it (fixed order) after a 64-thread named barrier.
+        __shared__ float half1[4][32];
+        if (g == 1) half1[q][lane] = rsum;
+        asm volatile("bar.sync %0, %1;" ::"r"(1 + q), "r"(64) : "memory");
+        if (g == 0 && lr < args.rows) args.rowpart[cb * args.rows_pad + lr] = rsum + half1[q][lane];
+        asm volatile("bar.sync %0, %1;" ::"r"(1 + q), "r"(64) : "memory");
+      }
+    }
+    if (lane == 0) tma_store_wait_all();
+    __syncwarp();
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"(kTmemCols)
+                 : "memory");
+  }
+}
+
+// ---------------------------------------------------------- host side
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+bool make_map(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t outer,
+              uint64_t row_bytes, uint32_t box_inner, uint32_t box_outer) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {row_bytes};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(ptr), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+template <int KB>
+int launch_kb(const CUtensorMap& mh, const CUtensorMap& ml, const CUtensorMap& mo,
+              const TcArgs& a0, cudaStream_t s) {
+  constexpr int MB = mblocks(KB);
+  TcArgs a = a0;
+  a.n_rtiles = ceil_div(a.rows, 128 * MB);
+  static int num_sms = 0;
+  static bool attr = false;
+  if (!attr) {
+    GPIC_CUDA_TRY(cudaFuncSetAttribute(affinity_tc_kernel<KB>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       smem_bytes(KB)));
+    int dev;
+    GPIC_CUDA_TRY(cudaGetDevice(&dev));
+    GPIC_CUDA_TRY(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev));
+    attr = true;
+  }
+  const int64_t total = a.n_rtiles * a.n_ctiles;
+  const int grid = (int)(total < num_sms ? total : num_sms);
+  affinity_tc_kernel<KB><<<grid, kThreads, smem_bytes(KB), s>>>(mh, ml, mo, a);
+  count_launch();
+  GPIC_CUDA_TRY(cudaGetLastError());
+  return GPIC_OK;
+}
+
+}  // namespace
+
+int launch_affinity_tc(const float* xhi, const float* xlo, const float* sqn, int64_t n,
+                       int32_t dp, int64_t row_lo, int64_t row_hi, float neg_scale_log2, float* a,
+                       int64_t lda, float* rowpart, int64_t rows_pad, cudaStream_t s) {
+  const int KB = dp / kKBlk;
+  if (dp % kKBlk || KB < 1 || KB > 4)
+    return fail(GPIC_E_UNSUPPORTED, "tcgen05 affinity engine supports d <= 128");
+  const int64_t npad = row_pad(n);
+  const int64_t rows = row_hi - row_lo;
+  CUtensorMap mh, ml, mo;
+  if (!make_map(&mh, xhi, (uint64_t)dp, (uint64_t)npad, (uint64_t)dp * 4, kKBlk, 128) ||
+      !make_map(&ml, xlo, (uint64_t)dp, (uint64_t)npad, (uint64_t)dp * 4, kKBlk, 128) ||
+      !make_map(&mo, a, (uint64_t)lda, (uint64_t)rows, (uint64_t)lda * 4, 32, 32))
+    return fail(GPIC_E_CUDA, "cuTensorMapEncodeTiled failed");
+  TcArgs args{sqn, n, row_lo, rows, neg_scale_log2, rowpart, rows_pad, 0, ceil_div(n, kBN)};
+  switch (KB) {
+    case 1: return launch_kb<1>(mh, ml, mo, args, s);
+    case 2: return launch_kb<2>(mh, ml, mo, args, s);
+    case 3: return launch_kb<3>(mh, ml, mo, args, s);
+    default: return launch_kb<4>(mh, ml, mo, args, s);
+  }
+}
+
 }  // namespace gpic
