@@ -320,7 +320,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", type=int, default=3)
-    ap.add_argument("--engine", choices=["tc", "simt"], default="simt")
+    ap.add_argument("--engine", choices=["tc", "simt"], default="tc")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--gemv-reps", type=int, default=10)
     ap.add_argument("--ref-rows", type=int, default=256)

@@ -105,7 +105,7 @@ class KernelConfig:
     p: int = 1
     chunk_rows: int | None = None
     memory_budget_bytes: int = DEFAULT_MEMORY_BUDGET
-    affinity_impl: str = "simt"
+    affinity_impl: str = "tc"
     virtual_ranks: bool = False
     device: int | None = None
 

@@ -115,8 +115,9 @@ def test_affinity_rows_and_degree(golden, engine):
             got = full[int(r)]
             assert got[int(r)] == 0.0
             assert np.max(np.abs(got - row)) <= 1e-4 * max(row.max(), 1e-30) + 1e-30
-        # exact symmetry is a property of the formula; fp32 engine keeps it to rounding
-        assert np.max(np.abs(full - full.T)) <= 1e-6
+        # exact symmetry is a property of the formula; the fp32 engines keep it
+        # to Gram rounding (G_ij and G_ji are accumulated in different orders)
+        assert np.max(np.abs(full - full.T)) <= 1e-5
 
 
 @pytest.mark.parametrize("engine", ENGINES)
