@@ -29,6 +29,7 @@
 
 #include "common.cuh"
 #include "ops.h"
+#include "sm100.cuh"
 
 namespace gpic {
 
@@ -44,112 +45,19 @@ constexpr int kSmemBudget = 224 * 1024;
 
 __host__ __device__ constexpr int mblocks(int KB) { return KB <= 2 ? 2 : 1; }
 __host__ __device__ constexpr int a_bytes(int KB) { return 2 * mblocks(KB) * KB * kTileBytes; }
+// output staging buffers per epilogue warp (double-buffered where smem allows)
+__host__ __device__ constexpr int out_bufs(int KB) { return (KB == 1 || KB == 3) ? 2 : 1; }
+__host__ __device__ constexpr int out_bytes(int KB) { return kEpiWarps * out_bufs(KB) * kStageOutBytes; }
 __host__ __device__ constexpr int stages(int KB) {
-  return (kSmemBudget - a_bytes(KB) - kEpiWarps * kStageOutBytes) / (2 * kTileBytes) > 4
+  return (kSmemBudget - a_bytes(KB) - out_bytes(KB)) / (2 * kTileBytes) > 4
              ? 4
-             : (kSmemBudget - a_bytes(KB) - kEpiWarps * kStageOutBytes) / (2 * kTileBytes);
+             : (kSmemBudget - a_bytes(KB) - out_bytes(KB)) / (2 * kTileBytes);
 }
 __host__ __device__ constexpr int smem_bytes(int KB) {
-  return a_bytes(KB) + stages(KB) * 2 * kTileBytes + kEpiWarps * kStageOutBytes + 256 + 1024;
+  return a_bytes(KB) + stages(KB) * 2 * kTileBytes + out_bytes(KB) + 256 + 1024;
 }
 
-// ------------------------------------------------------------ PTX helpers
-__device__ __forceinline__ uint32_t su32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred P;\n"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
-      "@!P bra WAIT_%=;\n}" ::"r"(su32(b)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y,
-                                            uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
-      "%3}], [%4];" ::"r"(su32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(su32(bar))
-      : "memory");
-}
-__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, int x, int y, const void* src) {
-  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
-                   reinterpret_cast<uint64_t>(map)),
-               "r"(x), "r"(y), "r"(su32(src))
-               : "memory");
-  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-}
-__device__ __forceinline__ void tma_store_wait_read() {
-  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-}
-__device__ __forceinline__ void tma_store_wait_all() {
-  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-}
-__device__ __forceinline__ void fence_async_smem() {
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
-__device__ __forceinline__ void tc_fence_before() {
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-}
-__device__ __forceinline__ void tc_fence_after() {
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-}
-__device__ __forceinline__ void tc_commit(uint64_t* b) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                   su32(b))
-               : "memory");
-}
-__device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc,
-                                         uint32_t acc) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}" ::"r"(d_tmem),
-      "l"(a), "l"(b), "r"(idesc), "r"(acc)
-      : "memory");
-}
-// K-major, 128-byte swizzle smem matrix descriptor (8-row groups 1024 B apart).
-__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
-  uint64_t d = (uint64_t)((saddr >> 4) & 0x3FFFu);
-  d |= (uint64_t)1u << 16;            // leading byte offset (unused for SW128 K-major)
-  d |= (uint64_t)(1024u >> 4) << 32;  // stride byte offset: 8 rows x 128 B
-  d |= (uint64_t)1u << 46;            // sm_100 descriptor version
-  d |= (uint64_t)2u << 61;            // SWIZZLE_128B
-  return d;
-}
-// kind::tf32, fp32 accumulate, K-major A and B, M=128, N=128.
-constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(kBN >> 3) << 17) |
-                            ((uint32_t)(128 >> 4) << 24);
-
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%"
-      "15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
-        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
-        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
-        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
-        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-      : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-}
-__device__ __forceinline__ float ex2(float x) {
-  float y;
-  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
-}
+constexpr uint32_t kIdesc = idesc_tf32(128, kBN);
 
 struct TcArgs {
   const float* sqn;
@@ -177,7 +85,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* sA = base;                                     // [hl][m][kb] 16 KB tiles
   uint8_t* sB = sA + a_bytes(KB);                         // [stage][hl] 16 KB tiles
   uint8_t* sOut = sB + ST * 2 * kTileBytes;               // [epi warp] 4 KB
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sOut + kEpiWarps * kStageOutBytes);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sOut + out_bytes(KB));
   uint64_t* full = bars;                 // [ST]
   uint64_t* empty = bars + ST;           // [ST]
   uint64_t* a_full = bars + 2 * ST;
@@ -297,47 +205,65 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else {
     // --------------------------------------------------------- epilogue
+    constexpr int NC = MB == 2 ? 4 : 2;  // 32-column chunks per warp per tile
+    constexpr int NBUF = out_bufs(KB);   // staging buffers per warp
     const int e = warp - 2;
     const int q = warp & 3;          // TMEM lane quadrant this warp may access
     const int g = e >> 2;            // group: M block (MB=2) or column half (MB=1)
     const int m = MB == 2 ? g : 0;
     const int c_lo = MB == 2 ? 0 : 2 * g;
-    const int c_hi = MB == 2 ? 4 : 2 * g + 2;
-    uint8_t* stage = sOut + e * kStageOutBytes;
+    uint8_t* stage0 = sOut + e * NBUF * kStageOutBytes;
     const float ns = args.ns;
     const float m2ns = -2.f * ns;
     uint32_t tf_par[2] = {0, 0};
     int i = 0;
-    bool pending = false;
+    int stores = 0;
+    // column / row norms of the next tile are fetched one tile ahead so the
+    // L2 latency hides behind the TMEM-full wait
+    float nx_cb[NC], nx_ra = 0.f;
+    auto prefetch = [&](int64_t t) {
+      const int64_t rb = t / args.n_ctiles, cb = t % args.n_ctiles;
+#pragma unroll
+      for (int cc = 0; cc < NC; ++cc)
+        nx_cb[cc] = ns * __ldg(args.sqn + cb * kBN + (c_lo + cc) * 32 + lane);
+      const int64_t gr = args.row_lo + (rb * MB + m) * 128 + q * 32 + lane;
+      nx_ra = gr < args.n ? ns * __ldg(args.sqn + gr) : 0.f;
+    };
+    if (t_begin < t_end) prefetch(t_begin);
     for (int64_t t = t_begin; t < t_end; ++t, ++i) {
       const int64_t rb = t / args.n_ctiles, cb = t % args.n_ctiles;
       const int buf = i & 1;
       const int64_t lr0 = (rb * MB + m) * 128 + q * 32;  // shard-local first row of this warp
       const int64_t lr = lr0 + lane;
       const int64_t gr = args.row_lo + lr;
-      const float ra = gr < args.n ? ns * __ldg(args.sqn + gr) : 0.f;
+      float cbv[NC];
+#pragma unroll
+      for (int cc = 0; cc < NC; ++cc) cbv[cc] = nx_cb[cc];
+      const float ra = nx_ra;
+      if (t + 1 < t_end) prefetch(t + 1);
       mbar_wait(&t_full[buf], tf_par[buf]);
       tf_par[buf] ^= 1;
       tc_fence_after();
       float rsum = 0.f;
-      for (int c = c_lo; c < c_hi; ++c) {
+#pragma unroll
+      for (int cc = 0; cc < NC; ++cc) {
+        const int c = c_lo + cc;
         uint32_t r[32];
         tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)((buf * MB + m) * kBN + c * 32),
                   r);
-        if (c == c_hi - 1) {
+        if (cc == NC - 1) {  // accumulator fully read: hand it back to the MMA warp
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&t_empty[buf]);
         }
         const int64_t col0 = cb * kBN + c * 32;
-        const float cb_lane = ns * __ldg(args.sqn + col0 + lane);
         const bool diag = (col0 < args.row_lo + lr0 + 32) && (args.row_lo + lr0 < col0 + 32);
         const bool pad = col0 + 32 > args.n;
         float vals[32];
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
-          const float cj = __shfl_sync(0xffffffffu, cb_lane, j);
-          float arg = fmaf(__uint_as_float(r[j]), m2ns, ra + cj);
+          const float cj = __shfl_sync(0xffffffffu, cbv[cc], j);
+          const float arg = fmaf(__uint_as_float(r[j]), m2ns, ra + cj);
           vals[j] = ex2(fminf(arg, 0.f));
         }
         if (diag || pad) {
@@ -347,21 +273,24 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
 #pragma unroll
         for (int j = 0; j < 32; ++j) rsum += vals[j];
-        // previous TMA store must have finished reading the staging buffer
-        if (pending) {
-          if (lane == 0) tma_store_wait_read();
+        // the store issued NBUF chunks ago must have finished reading this buffer
+        uint8_t* stage = stage0 + (stores % NBUF) * kStageOutBytes;
+        if (stores >= NBUF) {
+          if (lane == 0) tma_store_wait_read<NBUF - 1>();
           __syncwarp();
         }
+        const uint32_t srow = su32(stage) + lane * 128;
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-          const int chunk = j ^ (lane & 7);
-          *reinterpret_cast<float4*>(stage + lane * 128 + chunk * 16) =
-              make_float4(vals[4 * j], vals[4 * j + 1], vals[4 * j + 2], vals[4 * j + 3]);
+          const uint32_t addr = srow + ((j ^ (lane & 7)) << 4);
+          asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(vals[4 * j]),
+                       "f"(vals[4 * j + 1]), "f"(vals[4 * j + 2]), "f"(vals[4 * j + 3])
+                       : "memory");
         }
         fence_async_smem();
         __syncwarp();
         if (lane == 0) tma_store_2d(&map_out, (int)col0, (int)lr0, stage);
-        pending = true;
+        ++stores;
       }
       if constexpr (MB == 2) {
         if (lr < args.rows) args.rowpart[cb * args.rows_pad + lr] = rsum;

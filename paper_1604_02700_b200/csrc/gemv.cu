@@ -1,0 +1,141 @@
+// Power-iteration GEMV: y_i = (sum_j A_ij v_j) / deg_i  (k_multiply,
+// parallel.py:196-207, with k_normalize's D^-1 folded into the epilogue).
+//
+// HBM-bound: every iteration streams the whole fp32 A block (4 * rows * n
+// bytes) once. Persistent CTAs (one per SM); a producer lane feeds a 3-stage
+// smem ring with 1-D bulk copies (cp.async.bulk, completion on mbarriers):
+// per stage, a 1024-column chunk of 16 rows plus the matching chunk of v
+// (68 KB). ~200 KB per SM are in flight without tying up registers, which is
+// what keeps HBM saturated; 8 consumer warps (2 rows each) read the stage
+// with conflict-free 128-bit shared loads. Per-row sums are accumulated in
+// fp32 within a chunk and in fp64 across chunks, then reduced across lanes
+// by a fixed butterfly: the result for a row depends only on that row, not
+// on the shard plan.
+#include "common.cuh"
+#include "ops.h"
+#include "sm100.cuh"
+
+namespace gpic {
+
+namespace {
+
+constexpr int kRG = 16;          // rows per group
+constexpr int kCW = 1024;        // columns per chunk
+constexpr int kStages = 3;
+constexpr int kConsumers = 8;    // warps, kRG / kConsumers rows each
+constexpr int kRowsPerWarp = kRG / kConsumers;
+constexpr int kThreads = (kConsumers + 1) * 32;
+constexpr int kStageFloats = (kRG + 1) * kCW;
+constexpr int kSmem = kStages * kStageFloats * 4 + 64 + 128;
+
+__global__ void __launch_bounds__(kThreads, 1)
+    gemv_bulk_kernel(const float* __restrict__ a, int64_t lda, int64_t rows, int64_t row_lo,
+                     const float* __restrict__ v32, const double* __restrict__ deg,
+                     double* __restrict__ y, const gpic_ctl* __restrict__ ctl) {
+  if (ctl != nullptr && *(volatile const int32_t*)&ctl->stop) return;
+  extern __shared__ uint8_t smem_raw[];
+  float* st = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+  uint64_t* full = reinterpret_cast<uint64_t*>(st + kStages * kStageFloats);
+  uint64_t* empty = full + kStages;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kConsumers);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int64_t groups = (rows + kRG - 1) / kRG;
+  const int64_t nchunks = (lda + kCW - 1) / kCW;
+
+  if (warp == kConsumers) {
+    if (lane != 0) return;
+    int s = 0;
+    uint32_t ph = 0;
+    for (int64_t g = blockIdx.x; g < groups; g += gridDim.x) {
+      const int64_t r0 = g * kRG;
+      const int nr = (int)min((int64_t)kRG, rows - r0);
+      for (int64_t ch = 0; ch < nchunks; ++ch) {
+        const int64_t c0 = ch * kCW;
+        const uint32_t cw = (uint32_t)min((int64_t)kCW, lda - c0);
+        mbar_wait(&empty[s], ph ^ 1);
+        mbar_expect_tx(&full[s], (uint32_t)(nr + 1) * cw * 4u);
+        float* dst = st + s * kStageFloats;
+        bulk_load(dst + kRG * kCW, v32 + c0, cw * 4u, &full[s]);
+        for (int r = 0; r < nr; ++r)
+          bulk_load(dst + r * kCW, a + (r0 + r) * lda + c0, cw * 4u, &full[s]);
+        if (++s == kStages) { s = 0; ph ^= 1; }
+      }
+    }
+    return;
+  }
+
+  int s = 0;
+  uint32_t ph = 0;
+  for (int64_t g = blockIdx.x; g < groups; g += gridDim.x) {
+    const int64_t r0 = g * kRG;
+    double acc64[kRowsPerWarp];
+#pragma unroll
+    for (int r = 0; r < kRowsPerWarp; ++r) acc64[r] = 0.0;
+    for (int64_t ch = 0; ch < nchunks; ++ch) {
+      const int cw4 = (int)(min((int64_t)kCW, lda - ch * kCW) >> 2);
+      mbar_wait(&full[s], ph);
+      const float* base = st + s * kStageFloats;
+      const float4* vv = reinterpret_cast<const float4*>(base + kRG * kCW);
+      float acc[kRowsPerWarp];
+#pragma unroll
+      for (int r = 0; r < kRowsPerWarp; ++r) acc[r] = 0.f;
+#pragma unroll 4
+      for (int f = lane; f < cw4; f += 32) {
+        const float4 x = vv[f];
+#pragma unroll
+        for (int r = 0; r < kRowsPerWarp; ++r) {
+          const float4 w =
+              reinterpret_cast<const float4*>(base + (warp * kRowsPerWarp + r) * kCW)[f];
+          acc[r] = fmaf(w.x, x.x, acc[r]);
+          acc[r] = fmaf(w.y, x.y, acc[r]);
+          acc[r] = fmaf(w.z, x.z, acc[r]);
+          acc[r] = fmaf(w.w, x.w, acc[r]);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+      if (++s == kStages) { s = 0; ph ^= 1; }
+#pragma unroll
+      for (int r = 0; r < kRowsPerWarp; ++r) acc64[r] += (double)acc[r];
+    }
+#pragma unroll
+    for (int r = 0; r < kRowsPerWarp; ++r) {
+      const double sum = warp_sum_f64(acc64[r]);
+      const int64_t li = r0 + warp * kRowsPerWarp + r;
+      if (lane == 0 && li < rows) y[row_lo + li] = deg != nullptr ? sum / deg[li] : sum;
+    }
+  }
+}
+
+}  // namespace
+
+static int g_num_sms = 0;
+
+// One-time attribute setup; called before any stream capture.
+void gemv_prepare() {
+  if (g_num_sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaFuncSetAttribute(gemv_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+  }
+}
+
+void launch_gemv(const float* a, int64_t lda, int64_t rows, int64_t row_lo, const float* v32,
+                 const double* deg, double* y, const gpic_ctl* ctl, cudaStream_t s) {
+  gemv_prepare();
+  const int num_sms = g_num_sms;
+  const int64_t groups = (rows + kRG - 1) / kRG;
+  const int grid = (int)(groups < num_sms ? groups : num_sms);
+  gemv_bulk_kernel<<<grid, kThreads, kSmem, s>>>(a, lda, rows, row_lo, v32, deg, y, ctl);
+  count_launch();
+}
+
+}  // namespace gpic

@@ -66,6 +66,7 @@ void launch_scale_vector(const double* src, int64_t n, const double* tau, double
                          float* v32, int64_t v32_len, cudaStream_t s);
 void launch_scale_by(const double* src, int64_t n, double tau, double* dst, float* dst32,
                      int64_t f32_len, cudaStream_t s);
+void gemv_prepare();
 void launch_gemv(const float* a, int64_t lda, int64_t rows, int64_t row_lo, const float* v32,
                  const double* deg, double* y, const gpic_ctl* ctl, cudaStream_t s);
 void launch_iteration_tail(const double* y, int64_t n, double* redpart, double* v64,

@@ -7,7 +7,7 @@
 // Per iteration, three kernels, all no-ops once ctl->stop is set so a whole
 // max_iterations loop can be replayed from one CUDA graph with no host
 // synchronisation:
-//   gemv_kernel   y_i = (sum_j A_ij v_j) / deg_i        HBM-bound, 4n^2 bytes
+//   gemv (gemv.cu) y_i = (sum_j A_ij v_j) / deg_i       HBM-bound, 4n^2 bytes
 //   tau_kernel    tau = fixed-shape sum of y             (k_reduce, parallel.py:161-178)
 //   norm_kernel   v' = y / tau, delta = max|v' - v|, history, stop test
 // Every reduction has a fixed shape over GLOBAL indices, so results are
@@ -22,76 +22,8 @@ namespace gpic {
 
 namespace {
 
-constexpr int kGemvWarps = 8;
-constexpr int kGemvRows = 4;     // rows per warp
-constexpr int kGemvUnroll = 4;   // float4 columns in flight per lane per row
-constexpr int kFlush = 16;       // fp32 partial -> fp64 every kFlush steps
 constexpr int kRedThreads = 256;
 constexpr int kRedPer = kRedBlock / kRedThreads;  // 8 elements per thread
-
-// ---------------------------------------------------------------- GEMV
-template <int R, int U>
-__global__ void __launch_bounds__(kGemvWarps * 32)
-    gemv_kernel(const float* __restrict__ a, int64_t lda, int64_t rows, int64_t row_lo,
-                const float* __restrict__ v32, const double* __restrict__ deg,
-                double* __restrict__ y, const gpic_ctl* __restrict__ ctl) {
-  if (ctl != nullptr && *(volatile const int32_t*)&ctl->stop) return;
-  const int lane = threadIdx.x & 31;
-  const int warp = threadIdx.x >> 5;
-  const int64_t r0 = ((int64_t)blockIdx.x * kGemvWarps + warp) * R;
-  if (r0 >= rows) return;
-  const int64_t nv4 = lda >> 2;
-  const float4* __restrict__ vv = reinterpret_cast<const float4*>(v32);
-  const float4* arow[R];
-#pragma unroll
-  for (int r = 0; r < R; ++r) {
-    const int64_t rr = min(r0 + r, rows - 1);  // tail rows re-read the last row, result dropped
-    arow[r] = reinterpret_cast<const float4*>(a + rr * lda);
-  }
-  double acc64[R];
-#pragma unroll
-  for (int r = 0; r < R; ++r) acc64[r] = 0.0;
-
-  constexpr int64_t kStep = 32 * U;
-  for (int64_t base = 0; base < nv4; base += kStep * kFlush) {
-    float acc[R];
-#pragma unroll
-    for (int r = 0; r < R; ++r) acc[r] = 0.f;
-    const int64_t stop = min(nv4, base + kStep * kFlush);
-    for (int64_t c0 = base + lane; c0 < stop; c0 += kStep) {
-      float4 vu[U];
-      float4 au[R][U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int64_t c = c0 + u * 32;
-        const bool ok = c < stop;
-        vu[u] = ok ? __ldg(vv + c) : make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-        for (int r = 0; r < R; ++r)
-          au[r][u] = ok ? ld_stream_f4(arow[r] + c) : make_float4(0.f, 0.f, 0.f, 0.f);
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u)
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-          acc[r] = fmaf(au[r][u].x, vu[u].x, acc[r]);
-          acc[r] = fmaf(au[r][u].y, vu[u].y, acc[r]);
-          acc[r] = fmaf(au[r][u].z, vu[u].z, acc[r]);
-          acc[r] = fmaf(au[r][u].w, vu[u].w, acc[r]);
-        }
-    }
-#pragma unroll
-    for (int r = 0; r < R; ++r) acc64[r] += (double)acc[r];
-  }
-#pragma unroll
-  for (int r = 0; r < R; ++r) {
-    const double s = warp_sum_f64(acc64[r]);
-    if (lane == 0 && r0 + r < rows) {
-      const int64_t li = r0 + r;
-      y[row_lo + li] = deg != nullptr ? s / deg[li] : s;
-    }
-  }
-}
 
 // ------------------------------------------------- fixed-shape reductions
 // Block b sums y[b*2048, (b+1)*2048) in a fixed pattern; the last block
@@ -252,15 +184,6 @@ void launch_scale_by(const double* src, int64_t n, double tau, double* dst, floa
   count_launch();
 }
 
-void launch_gemv(const float* a, int64_t lda, int64_t rows, int64_t row_lo, const float* v32,
-                 const double* deg, double* y, const gpic_ctl* ctl, cudaStream_t s) {
-  constexpr int rows_per_cta = kGemvWarps * kGemvRows;
-  gemv_kernel<kGemvRows, kGemvUnroll>
-      <<<(unsigned)ceil_div(rows, rows_per_cta), kGemvWarps * 32, 0, s>>>(a, lda, rows, row_lo,
-                                                                         v32, deg, y, ctl);
-  count_launch();
-}
-
 void launch_iteration_tail(const double* y, int64_t n, double* redpart, double* v64, float* v32,
                            double* hist, gpic_ctl* ctl, cudaStream_t s) {
   const unsigned nb = (unsigned)ceil_div(n, kRedBlock);
@@ -292,6 +215,7 @@ int run_power_loop(const float* a, int64_t lda, const double* deg, int64_t n, do
     GPIC_CUDA_TRY(cudaStreamWaitEvent(cs, ev, 0));
     GPIC_CUDA_TRY(cudaEventDestroy(ev));
   }
+  gemv_prepare();
   cudaGraph_t graph;
   cudaGraphExec_t exec;
   GPIC_CUDA_TRY(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
