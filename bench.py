@@ -63,25 +63,41 @@ class ClockSampler:
         self.proc = None
 
     def __enter__(self):
+        import threading
+
+        self.lines = []
+        self._live = True
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True, bufsize=1)
         except OSError:
             self.proc = None
+            return self
+        first = threading.Event()
+
+        def pump():
+            for ln in self.proc.stdout:
+                if ln.strip():
+                    if self._live:
+                        self.lines.append(ln.strip())
+                    first.set()
+
+        self._thread = threading.Thread(target=pump, daemon=True)
+        self._thread.start()
+        first.wait(timeout=5.0)  # sampling is live before the timed region starts
+        self.lines.clear()
         return self
 
     def __exit__(self, *exc):
-        self.lines = []
+        self._live = False
         if self.proc is not None:
             self.proc.terminate()
             try:
-                out, _ = self.proc.communicate(timeout=5)
+                self.proc.wait(timeout=5)
             except subprocess.TimeoutExpired:
                 self.proc.kill()
-                out, _ = self.proc.communicate()
-            self.lines = [ln for ln in out.splitlines() if ln.strip()]
 
     def summary(self):
         sm, mx, reasons = [], None, set()
@@ -316,7 +332,7 @@ def run_ours(args, cfg, rank, world):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", type=int, default=3)

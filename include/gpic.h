@@ -187,6 +187,46 @@ int gpic_ctl_read(const gpic_ctl* d_ctl, gpic_ctl* h_out, void* stream);
  * gpu_launches claim). */
 int64_t gpic_launch_count(void);
 
+/* ---- multi-rank (row-sharded) power iteration --------------------------
+ * Replaces the worker fan-out of the reference's parallel backend
+ * (plan_rows / _run_workers, parallel.py:90-110; k_multiply per row range,
+ * :196-207) with one rank per GPU: rank r owns rows [row_lo, row_lo + rows)
+ * of A. Exchanges are fused into the producing kernels (P2P stores of the
+ * y / degree slices into every rank's buffers through CUDA IPC over
+ * NVLink, epoch flags, acquire-spin waits); no NCCL launch and no host sync
+ * per iteration. Results are bitwise independent of the rank count (the
+ * reference's p-invariance, parallel.py:10-22, test_parallel.py:194-223).
+ *
+ * Real ranks (one process per GPU): gpic_comm_create on every rank, share
+ * the GPIC_IPC_HANDLE_BYTES handles (any host collective), gpic_comm_open.
+ * Virtual ranks (P shards in one process on one device, the identical
+ * exchange code path): gpic_comm_create_virtual. At most 8 ranks. */
+#define GPIC_IPC_HANDLE_BYTES 64
+typedef struct gpic_comm gpic_comm;
+typedef struct gpic_shard {
+  const float* a;     /* rows x lda fp32 affinity rows of this shard        */
+  int64_t lda;
+  const double* deg;  /* rows degrees                                       */
+  int64_t row_lo;
+  int64_t rows;
+} gpic_shard;
+
+int gpic_comm_create(int32_t nranks, int32_t rank, int64_t n, gpic_comm** out,
+                     uint8_t* h_ipc_handle);
+int gpic_comm_open(gpic_comm* comm, const uint8_t* h_all_handles /* nranks x 64 bytes */);
+int gpic_comm_create_virtual(int32_t nranks, int64_t n, gpic_comm** out);
+int gpic_comm_destroy(gpic_comm* comm);
+/* All-gather of the degree slices (once per run) + the global ZeroDegree
+ * check; optionally copies the full degree vector out. Synchronous. */
+int gpic_comm_gather_degrees(gpic_comm* comm, const gpic_shard* shards, int32_t nlocal,
+                             double* d_deg_full_out, void* stream);
+/* v0 = d / tree_sum(d), then the device-resident loop. d_hist holds
+ * nlocal x max_iter doubles, d_vout nlocal x n (every shard ends with the
+ * same full embedding), h_ctl nlocal control blocks. Synchronous. */
+int gpic_comm_iterate(gpic_comm* comm, const gpic_shard* shards, int32_t nlocal, double eps,
+                      int32_t max_iter, double* d_hist, double* d_vout, gpic_ctl* h_ctl,
+                      void* stream);
+
 #ifdef __cplusplus
 }
 #endif

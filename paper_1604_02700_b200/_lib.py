@@ -81,7 +81,23 @@ SIGNATURES = {
                                     P, I64, P]),
     "gpic_ctl_read": (C.c_int, [P, P, P]),
     "gpic_launch_count": (I64, []),
+    "gpic_comm_create": (C.c_int, [I32, I32, I64, P, P]),
+    "gpic_comm_open": (C.c_int, [P, P]),
+    "gpic_comm_create_virtual": (C.c_int, [I32, I64, P]),
+    "gpic_comm_destroy": (C.c_int, [P]),
+    "gpic_comm_gather_degrees": (C.c_int, [P, P, I32, P, P]),
+    "gpic_comm_iterate": (C.c_int, [P, P, I32, F64, I32, P, P, P, P]),
 }
+
+IPC_HANDLE_BYTES = 64
+MAX_RANKS = 8
+
+
+class Shard(C.Structure):
+    """Mirror of struct gpic_shard."""
+
+    _fields_ = [("a", C.c_void_p), ("lda", C.c_int64), ("deg", C.c_void_p),
+                ("row_lo", C.c_int64), ("rows", C.c_int64)]
 
 _lib = None
 

@@ -236,7 +236,11 @@ int64_t gpic_kmeans_scratch_bytes(int64_t n, int32_t k) { return kmeans_scratch_
 int gpic_matvec(const float* d_a, int64_t lda, int64_t rows, int64_t n, const float* d_v,
                 const double* d_row_scale, double* d_y, void* stream) {
   if (lda % 4 || lda < n) return fail(GPIC_E_INVALID, "lda must be >= n and a multiple of 4");
-  launch_gemv(d_a, lda, rows, 0, d_v, d_row_scale, d_y, nullptr, static_cast<cudaStream_t>(stream));
+  PeerTable pt;
+  std::memset(&pt, 0, sizeof pt);
+  pt.y[0][0] = pt.y[0][1] = d_y;
+  pt.nranks = 1;
+  launch_gemv(d_a, lda, rows, 0, d_v, d_row_scale, pt, nullptr, static_cast<cudaStream_t>(stream));
   GPIC_CUDA_TRY(cudaGetLastError());
   return GPIC_OK;
 }

@@ -28,11 +28,16 @@ constexpr int kThreads = (kConsumers + 1) * 32;
 constexpr int kStageFloats = (kRG + 1) * kCW;
 constexpr int kSmem = kStages * kStageFloats * 4 + 64 + 128;
 
+__device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
 __global__ void __launch_bounds__(kThreads, 1)
     gemv_bulk_kernel(const float* __restrict__ a, int64_t lda, int64_t rows, int64_t row_lo,
                      const float* __restrict__ v32, const double* __restrict__ deg,
-                     double* __restrict__ y, const gpic_ctl* __restrict__ ctl) {
+                     const PeerTable pt, gpic_ctl* ctl) {
   if (ctl != nullptr && *(volatile const int32_t*)&ctl->stop) return;
+  const int parity = ctl != nullptr ? (ctl->iter & 1) : 0;
   extern __shared__ uint8_t smem_raw[];
   float* st = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
   uint64_t* full = reinterpret_cast<uint64_t*>(st + kStages * kStageFloats);
@@ -109,7 +114,25 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int r = 0; r < kRowsPerWarp; ++r) {
       const double sum = warp_sum_f64(acc64[r]);
       const int64_t li = r0 + warp * kRowsPerWarp + r;
-      if (lane == 0 && li < rows) y[row_lo + li] = deg != nullptr ? sum / deg[li] : sum;
+      if (lane == 0 && li < rows) {
+        const double val = deg != nullptr ? sum / deg[li] : sum;
+        // fused all-gather: the row lands in every rank's y (P2P over NVLink)
+        for (int p = 0; p < pt.nranks; ++p) pt.y[p][parity][row_lo + li] = val;
+      }
+    }
+  }
+  if (pt.flags[0] == nullptr) return;
+  // publish: after every consumer of every CTA stored its rows, release the
+  // epoch into each rank's flag slot for this shard
+  __threadfence_system();
+  asm volatile("bar.sync 1, %0;" ::"n"(kConsumers * 32) : "memory");
+  if (threadIdx.x == 0) {
+    const unsigned prev = atomicAdd(&ctl->arrive[2], 1u);
+    if (prev == gridDim.x - 1) {
+      ctl->arrive[2] = 0u;
+      __threadfence_system();
+      const uint64_t epoch = ctl->sync_epoch + (uint64_t)ctl->iter + 1;
+      for (int p = 0; p < pt.nranks; ++p) st_release_sys(pt.flags[p] + pt.self, epoch);
     }
   }
 }
@@ -129,12 +152,12 @@ void gemv_prepare() {
 }
 
 void launch_gemv(const float* a, int64_t lda, int64_t rows, int64_t row_lo, const float* v32,
-                 const double* deg, double* y, const gpic_ctl* ctl, cudaStream_t s) {
+                 const double* deg, const PeerTable& pt, gpic_ctl* ctl, cudaStream_t s) {
   gemv_prepare();
   const int num_sms = g_num_sms;
   const int64_t groups = (rows + kRG - 1) / kRG;
   const int grid = (int)(groups < num_sms ? groups : num_sms);
-  gemv_bulk_kernel<<<grid, kThreads, kSmem, s>>>(a, lda, rows, row_lo, v32, deg, y, ctl);
+  gemv_bulk_kernel<<<grid, kThreads, kSmem, s>>>(a, lda, rows, row_lo, v32, deg, pt, ctl);
   count_launch();
 }
 

@@ -59,6 +59,26 @@ int launch_affinity_tc(const float* xhi, const float* xlo, const float* sqn, int
 void launch_degree(const float* rowpart, int64_t rows, int64_t rows_pad, int64_t n_ctiles,
                    int64_t row_lo, double* deg, gpic_ctl* ctl, cudaStream_t s);
 
+// ---- rank exchange (comm.cu) -----------------------------------------
+// Every rank owns rows [row_lo, row_lo + rows) of A. Each iteration, the
+// GEMV of rank s stores its y rows straight into the y buffer of EVERY rank
+// (peer pointers: CUDA IPC mappings over NVLink, or plain device pointers
+// for virtual ranks on one GPU), then its last CTA release-stores the epoch
+// into flags_p[s] on every rank p. A rank's tail waits (acquire) until all P
+// epochs have arrived. y is double-buffered by iteration parity, so a fast
+// rank writing iteration t+1 never races a slow rank still reading t.
+constexpr int kMaxRanks = 8;
+constexpr int kFlagSlots = 2 * kMaxRanks;  // [0,P): iteration epochs, [P,2P): gather epochs
+
+struct PeerTable {
+  double* y[kMaxRanks][2];     // y ping-pong of every rank, as seen from this process
+  uint64_t* flags[kMaxRanks];  // kFlagSlots epochs per rank (nullptr: single rank)
+  int nranks;
+  int self;                    // global rank index of the local shard
+  // the epoch base of a loop is ctl->sync_epoch (device-side, so one
+  // captured graph is replayed for every run)
+};
+
 // power.cu
 void launch_tree_sum(const double* v, int64_t n, double* part, double* out, gpic_ctl* ctl,
                      cudaStream_t s);
@@ -68,11 +88,31 @@ void launch_scale_by(const double* src, int64_t n, double tau, double* dst, floa
                      int64_t f32_len, cudaStream_t s);
 void gemv_prepare();
 void launch_gemv(const float* a, int64_t lda, int64_t rows, int64_t row_lo, const float* v32,
-                 const double* deg, double* y, const gpic_ctl* ctl, cudaStream_t s);
-void launch_iteration_tail(const double* y, int64_t n, double* redpart, double* v64,
-                           float* v32, double* hist, gpic_ctl* ctl, cudaStream_t s);
+                 const double* deg, const PeerTable& pt, gpic_ctl* ctl, cudaStream_t s);
+void launch_peer_wait(const uint64_t* flags_self, int slot0, int count, uint64_t base,
+                      int add_iter, gpic_ctl* ctl, cudaStream_t s);
+void launch_iteration_tail(const double* y0, const double* y1, int64_t n, double* redpart,
+                           double* v64, float* v32, double* hist, gpic_ctl* ctl, cudaStream_t s);
 void launch_copy_result(const double* v64, int64_t n, double* out, const gpic_ctl* ctl,
                         cudaStream_t s);
+
+// One shard's loop state (a single-rank run is one shard with nranks = 1).
+struct ShardLoop {
+  const float* a;
+  int64_t lda;
+  int64_t rows;
+  int64_t row_lo;
+  const double* deg;  // degrees of the shard's rows
+  double* redpart;
+  double* v64;        // 2 x n ping-pong
+  float* v32;         // pitch(n) floats
+  double* hist;
+  gpic_ctl* ctl;
+  PeerTable pt;
+};
+// Capture max_iter iterations of every local shard into one CUDA graph
+// (virtual ranks: all GEMVs of an iteration precede all tails) and launch it.
+int run_power_loops(ShardLoop* shards, int nlocal, int64_t n, int32_t max_iter, cudaStream_t s);
 int run_power_loop(const float* a, int64_t lda, const double* deg, int64_t n, double* y,
                    double* redpart, double* v64, float* v32, double* hist, gpic_ctl* ctl,
                    int32_t max_iter, cudaStream_t s);

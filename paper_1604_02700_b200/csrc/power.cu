@@ -14,6 +14,8 @@
 // bitwise independent of how rows are sharded across ranks.
 #include <cfloat>
 #include <cstdio>
+#include <cstring>
+#include <vector>
 
 #include "common.cuh"
 #include "ops.h"
@@ -57,10 +59,12 @@ __device__ __forceinline__ double block_max(double v, double* sh) {
 // Sum of v[0, n) into *out (and ctl->tau when ctl != null). `guarded` skips
 // when ctl->stop is set (loop mode).
 __global__ void __launch_bounds__(kRedThreads)
-    tau_kernel(const double* __restrict__ v, int64_t n, double* __restrict__ part,
-               double* __restrict__ out, gpic_ctl* ctl, int guarded) {
+    tau_kernel(const double* __restrict__ v0, const double* __restrict__ v1, int64_t n,
+               double* __restrict__ part, double* __restrict__ out, gpic_ctl* ctl, int guarded) {
   __shared__ double sh[kRedThreads];
   if (guarded && *(volatile int32_t*)&ctl->stop) return;
+  // loop mode: the y buffer of this iteration (parity ping-pong)
+  const double* __restrict__ v = (guarded && (ctl->iter & 1)) ? v1 : v0;
   const int64_t b0 = (int64_t)blockIdx.x * kRedBlock;
   double s = 0.0;
 #pragma unroll
@@ -87,11 +91,13 @@ __global__ void __launch_bounds__(kRedThreads)
 // v' = y / tau ; delta = max|v' - v| ; last block records the history and
 // applies the stop rule.
 __global__ void __launch_bounds__(kRedThreads)
-    norm_kernel(const double* __restrict__ y, int64_t n, double* __restrict__ v64,
-                float* __restrict__ v32, double* __restrict__ hist, gpic_ctl* ctl) {
+    norm_kernel(const double* __restrict__ y0, const double* __restrict__ y1, int64_t n,
+                double* __restrict__ v64, float* __restrict__ v32, double* __restrict__ hist,
+                gpic_ctl* ctl) {
   __shared__ double sh[kRedThreads];
   if (*(volatile int32_t*)&ctl->stop) return;
   const int t = ctl->iter;
+  const double* __restrict__ y = (t & 1) ? y1 : y0;
   const double tau = ctl->tau;
   const double* __restrict__ vold = v64 + (int64_t)(t & 1) * n;
   double* __restrict__ vnew = v64 + (int64_t)((t + 1) & 1) * n;
@@ -156,6 +162,35 @@ __global__ void scale_by_kernel(const double* __restrict__ src, int64_t n, doubl
   }
 }
 
+// Acquire-spin until flags[slot0 .. slot0+count) all reach base (+ iter + 1
+// when add_iter). A peer that never arrives (dead rank) trips a ~10 s
+// timeout: the run stops with GPIC_E_COMM instead of hanging the device.
+__global__ void peer_wait_kernel(const uint64_t* flags, int slot0, int count, uint64_t base,
+                                 int add_iter, gpic_ctl* ctl) {
+  if (threadIdx.x != 0) return;
+  if (add_iter && *(volatile int32_t*)&ctl->stop) return;
+  // loop mode: the epoch base lives in the control block so one captured
+  // graph serves every run; gather mode: an explicit target
+  const uint64_t target = add_iter ? ctl->sync_epoch + (uint64_t)ctl->iter + 1 : base;
+  uint64_t t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (int s = 0; s < count; ++s) {
+    for (;;) {
+      uint64_t v;
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flags + slot0 + s) : "memory");
+      if (v >= target) break;
+      uint64_t now;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+      if (now - t0 > 10ull * 1000 * 1000 * 1000) {
+        raise_status(ctl, GPIC_E_COMM, slot0 + s, -1, 0.0);
+        return;
+      }
+      __nanosleep(64);
+    }
+  }
+  __threadfence_system();
+}
+
 __global__ void copy_result_kernel(const double* __restrict__ v64, int64_t n,
                                    double* __restrict__ out, const gpic_ctl* __restrict__ ctl) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -167,7 +202,7 @@ __global__ void copy_result_kernel(const double* __restrict__ v64, int64_t n,
 
 void launch_tree_sum(const double* v, int64_t n, double* part, double* out, gpic_ctl* ctl,
                      cudaStream_t s) {
-  tau_kernel<<<(unsigned)ceil_div(n, kRedBlock), kRedThreads, 0, s>>>(v, n, part, out, ctl, 0);
+  tau_kernel<<<(unsigned)ceil_div(n, kRedBlock), kRedThreads, 0, s>>>(v, v, n, part, out, ctl, 0);
   count_launch();
 }
 
@@ -184,12 +219,18 @@ void launch_scale_by(const double* src, int64_t n, double tau, double* dst, floa
   count_launch();
 }
 
-void launch_iteration_tail(const double* y, int64_t n, double* redpart, double* v64, float* v32,
-                           double* hist, gpic_ctl* ctl, cudaStream_t s) {
+void launch_iteration_tail(const double* y0, const double* y1, int64_t n, double* redpart,
+                           double* v64, float* v32, double* hist, gpic_ctl* ctl, cudaStream_t s) {
   const unsigned nb = (unsigned)ceil_div(n, kRedBlock);
-  tau_kernel<<<nb, kRedThreads, 0, s>>>(y, n, redpart, nullptr, ctl, 1);
-  norm_kernel<<<nb, kRedThreads, 0, s>>>(y, n, v64, v32, hist, ctl);
+  tau_kernel<<<nb, kRedThreads, 0, s>>>(y0, y1, n, redpart, nullptr, ctl, 1);
+  norm_kernel<<<nb, kRedThreads, 0, s>>>(y0, y1, n, v64, v32, hist, ctl);
   count_launch(2);
+}
+
+void launch_peer_wait(const uint64_t* flags_self, int slot0, int count, uint64_t base,
+                      int add_iter, gpic_ctl* ctl, cudaStream_t s) {
+  peer_wait_kernel<<<1, 32, 0, s>>>(flags_self, slot0, count, base, add_iter, ctl);
+  count_launch();
 }
 
 void launch_copy_result(const double* v64, int64_t n, double* out, const gpic_ctl* ctl,
@@ -198,38 +239,89 @@ void launch_copy_result(const double* v64, int64_t n, double* out, const gpic_ct
   count_launch();
 }
 
-// The whole loop as one CUDA graph: max_iter copies of {gemv, tau, norm}.
-// Kernels after convergence exit at their first instruction.
-int run_power_loop(const float* a, int64_t lda, const double* deg, int64_t n, double* y,
-                   double* redpart, double* v64, float* v32, double* hist, gpic_ctl* ctl,
-                   int32_t max_iter, cudaStream_t s) {
+namespace {
+
+// Instantiated loop graphs, keyed by everything that is baked into them.
+struct GraphKey {
+  ShardLoop shards[kMaxRanks];
+  int nlocal;
+  int64_t n;
+  int32_t max_iter;
+  int device;
+  bool operator==(const GraphKey& o) const { return std::memcmp(this, &o, sizeof(GraphKey)) == 0; }
+};
+struct GraphEntry {
+  GraphKey key;
+  cudaGraphExec_t exec;
+  unsigned long long launches;
+};
+std::vector<GraphEntry> g_graphs;
+constexpr size_t kGraphCache = 8;
+
+}  // namespace
+
+// The whole loop as one CUDA graph: max_iter copies of, per iteration,
+// every local shard's GEMV (+ fused peer stores / epoch publish), then every
+// local shard's [peer wait] + tau + normalise. Kernels after convergence
+// exit at their first instruction, so the replay needs no host decisions.
+int run_power_loops(ShardLoop* shards, int nlocal, int64_t n, int32_t max_iter, cudaStream_t s) {
+  if (nlocal < 1 || nlocal > kMaxRanks) return fail(GPIC_E_INVALID, "bad local shard count");
+  GraphKey key;
+  std::memset(&key, 0, sizeof key);
+  for (int i = 0; i < nlocal; ++i) key.shards[i] = shards[i];
+  key.nlocal = nlocal;
+  key.n = n;
+  key.max_iter = max_iter;
+  GPIC_CUDA_TRY(cudaGetDevice(&key.device));
   cudaStream_t cs = s;
   bool own = false;
   if (cs == nullptr || cs == cudaStreamLegacy || cs == cudaStreamPerThread) {
     GPIC_CUDA_TRY(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
     own = true;
-    // order the private stream after the caller's work
-    cudaEvent_t ev;
+    cudaEvent_t ev;  // order the private stream after the caller's work
     GPIC_CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
     GPIC_CUDA_TRY(cudaEventRecord(ev, s));
     GPIC_CUDA_TRY(cudaStreamWaitEvent(cs, ev, 0));
     GPIC_CUDA_TRY(cudaEventDestroy(ev));
   }
-  gemv_prepare();
-  cudaGraph_t graph;
-  cudaGraphExec_t exec;
-  GPIC_CUDA_TRY(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
-  const unsigned long long before = g_launches;
-  for (int t = 0; t < max_iter; ++t) {
-    launch_gemv(a, lda, n, 0, v32, deg, y, ctl, cs);
-    launch_iteration_tail(y, n, redpart, v64, v32, hist, ctl, cs);
+  GraphEntry* hit = nullptr;
+  for (auto& e : g_graphs)
+    if (e.key == key) hit = &e;
+  if (hit == nullptr) {
+    gemv_prepare();
+    cudaGraph_t graph;
+    GraphEntry ent;
+    ent.key = key;
+    const unsigned long long before = g_launches;
+    GPIC_CUDA_TRY(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+    for (int t = 0; t < max_iter; ++t) {
+      for (int i = 0; i < nlocal; ++i) {
+        const ShardLoop& L = shards[i];
+        launch_gemv(L.a, L.lda, L.rows, L.row_lo, L.v32, L.deg, L.pt, L.ctl, cs);
+      }
+      for (int i = 0; i < nlocal; ++i) {
+        const ShardLoop& L = shards[i];
+        const PeerTable& pt = L.pt;
+        if (pt.flags[0] != nullptr)
+          launch_peer_wait(pt.flags[pt.self], 0, pt.nranks, 0, 1, L.ctl, cs);
+        launch_iteration_tail(pt.y[pt.self][0], pt.y[pt.self][1], n, L.redpart, L.v64, L.v32,
+                              L.hist, L.ctl, cs);
+      }
+    }
+    GPIC_CUDA_TRY(cudaStreamEndCapture(cs, &graph));
+    GPIC_CUDA_TRY(cudaGraphInstantiate(&ent.exec, graph, 0));
+    GPIC_CUDA_TRY(cudaGraphDestroy(graph));
+    ent.launches = g_launches - before;
+    g_launches = before;
+    if (g_graphs.size() >= kGraphCache) {
+      cudaGraphExecDestroy(g_graphs.front().exec);
+      g_graphs.erase(g_graphs.begin());
+    }
+    g_graphs.push_back(ent);
+    hit = &g_graphs.back();
   }
-  GPIC_CUDA_TRY(cudaStreamEndCapture(cs, &graph));
-  GPIC_CUDA_TRY(cudaGraphInstantiate(&exec, graph, 0));
-  GPIC_CUDA_TRY(cudaGraphLaunch(exec, cs));
-  (void)before;
-  GPIC_CUDA_TRY(cudaGraphExecDestroy(exec));
-  GPIC_CUDA_TRY(cudaGraphDestroy(graph));
+  GPIC_CUDA_TRY(cudaGraphLaunch(hit->exec, cs));
+  g_launches += hit->launches;
   if (own) {
     cudaEvent_t ev;
     GPIC_CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
@@ -239,6 +331,28 @@ int run_power_loop(const float* a, int64_t lda, const double* deg, int64_t n, do
     GPIC_CUDA_TRY(cudaStreamDestroy(cs));
   }
   return GPIC_OK;
+}
+
+int run_power_loop(const float* a, int64_t lda, const double* deg, int64_t n, double* y,
+                   double* redpart, double* v64, float* v32, double* hist, gpic_ctl* ctl,
+                   int32_t max_iter, cudaStream_t s) {
+  ShardLoop L;
+  std::memset(&L, 0, sizeof L);
+  L.a = a;
+  L.lda = lda;
+  L.rows = n;
+  L.row_lo = 0;
+  L.deg = deg;
+  L.redpart = redpart;
+  L.v64 = v64;
+  L.v32 = v32;
+  L.hist = hist;
+  L.ctl = ctl;
+  L.pt.y[0][0] = y;
+  L.pt.y[0][1] = y;
+  L.pt.nranks = 1;
+  L.pt.self = 0;
+  return run_power_loops(&L, 1, n, max_iter, s);
 }
 
 }  // namespace gpic

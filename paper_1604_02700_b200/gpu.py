@@ -187,15 +187,34 @@ def k_affinity(d: DataSet, kind, config: KernelConfig | None = None,
     the fused exp/diagonal/row-sum epilogue, and the fixed-order degree
     combine. Raises NonFiniteEntry like validate_dataset (data.py:69-72).
     """
-    torch = _torch()
     config = config or KernelConfig()
     sigma = _check_kind(kind)
     check_shape(d)
     check_labels(d)
     dev = _device(config)
+    n = d.points.shape[0]
+    lo, hi = rows if rows is not None else (0, n)
+    prep = prepare_points(d, dev)
+    return affinity_rows(prep, lo, hi, sigma, config.affinity_impl)
+
+
+@dataclass
+class PreparedPoints:
+    """Centred fp32 operands of the Gram engines (gpic_prepare_points)."""
+
+    xhi: object
+    xlo: object
+    sqn: object
+    n: int
+    d: int
+    device: object
+
+
+def prepare_points(d: DataSet, dev) -> PreparedPoints:
+    """Upload X (fp64), scan for non-finite entries, centre, cast and split."""
+    torch = _torch()
     L = _lib.lib()
     n, m = d.points.shape
-    lo, hi = rows if rows is not None else (0, n)
     st = _stream(dev)
     x = torch.from_numpy(d.points).to(dev, non_blocking=True)
     dp = int(L.gpic_feature_pitch(m))
@@ -204,20 +223,29 @@ def k_affinity(d: DataSet, kind, config: KernelConfig | None = None,
     xlo = torch.empty_like(xhi)
     sqn = torch.empty(npad, dtype=torch.float32, device=dev)
     ctl = _new_ctl(dev)
-    prep = torch.empty(((n + 255) // 256 + 1) * m + m, dtype=torch.float64, device=dev)
-    _lib.check(L.gpic_prepare_points(_ptr(x), n, m, _ptr(xhi), _ptr(xlo), _ptr(sqn), _ptr(prep),
+    work = torch.empty(((n + 255) // 256 + 1) * m + m, dtype=torch.float64, device=dev)
+    _lib.check(L.gpic_prepare_points(_ptr(x), n, m, _ptr(xhi), _ptr(xlo), _ptr(sqn), _ptr(work),
                                      _ptr(ctl), st))
-    h = _read_ctl(ctl, dev)
-    _raise_ctl(h, m)
+    _raise_ctl(_read_ctl(ctl, dev), m)
+    return PreparedPoints(xhi=xhi, xlo=xlo, sqn=sqn, n=n, d=m, device=dev)
+
+
+def affinity_rows(prep: PreparedPoints, lo: int, hi: int, sigma: float, engine: str = "tc"):
+    """Rows [lo, hi) of A plus their degrees (fused epilogue + fixed-order combine)."""
+    torch = _torch()
+    L = _lib.lib()
+    dev, n, m = prep.device, prep.n, prep.d
     lda = int(L.gpic_affinity_pitch(n))
     nrows = hi - lo
     a = torch.empty((nrows, lda), dtype=torch.float32, device=dev)
     deg = torch.empty(nrows, dtype=torch.float64, device=dev)
     rows_pad = -(-nrows // 128) * 128
     rowpart = torch.empty(((n + 127) // 128) * rows_pad, dtype=torch.float32, device=dev)
-    impl = _lib.AFFINITY_TC if config.affinity_impl == "tc" else _lib.AFFINITY_SIMT
-    _lib.check(L.gpic_affinity_rbf(_ptr(xhi), _ptr(xlo), _ptr(sqn), n, m, lo, hi, sigma, impl,
-                                   _ptr(a), lda, _ptr(deg), _ptr(rowpart), _ptr(ctl), st))
+    ctl = _new_ctl(dev)
+    impl = _lib.AFFINITY_TC if engine == "tc" else _lib.AFFINITY_SIMT
+    _lib.check(L.gpic_affinity_rbf(_ptr(prep.xhi), _ptr(prep.xlo), _ptr(prep.sqn), n, m, lo, hi,
+                                   sigma, impl, _ptr(a), lda, _ptr(deg), _ptr(rowpart), _ptr(ctl),
+                                   _stream(dev)))
     return DeviceAffinity(a=a, deg=deg, n=n, lda=lda, row_lo=lo, row_hi=hi, ctl=ctl, d=m)
 
 

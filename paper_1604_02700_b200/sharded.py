@@ -1,0 +1,166 @@
+"""Row-sharded PIC over P ranks.
+
+Rank r owns the contiguous rows [r*n//P, (r+1)*n//P) of A — the reference's
+row-range plan (plan_rows, parallel.py:90-98) balanced so every rank is
+non-empty. Each rank builds its own row block with no communication; the
+degree slices are all-gathered once and the y slices every iteration, both
+by P2P stores fused into the producing kernels (csrc/comm.cu). Every rank
+then runs the (bitwise identical) tau / normalise / stop tail and the
+k-means on the full embedding, so all ranks return the same result.
+
+Two launch modes share that code path:
+
+* real ranks: one process per GPU under torch.distributed (torchrun); the
+  host only exchanges the 64-byte CUDA-IPC handles of the exchange buffers
+  (all_gather_object, any backend) once per run;
+* virtual ranks (KernelConfig(p=P, virtual_ranks=True)): all P shards in
+  this process on one device — how the multi-rank path is tested on a
+  single B200; results are bitwise equal to p=1.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _lib
+from .errors import DeviceError, InvalidSpec, ZeroDegree
+from .params import KMeansParams, PicTrace
+
+
+def shard_ranges(n: int, p: int):
+    """Balanced contiguous row ranges, all non-empty (n >= p)."""
+    if p < 1 or p > _lib.MAX_RANKS:
+        raise InvalidSpec(f"the sharded engine runs 1..{_lib.MAX_RANKS} ranks, got {p}")
+    if n < p:
+        raise InvalidSpec(f"cannot shard n={n} points over {p} ranks")
+    return [(r * n // p, (r + 1) * n // p) for r in range(p)]
+
+
+def dist_context():
+    """(rank, world_size) of an initialised torch.distributed job, else (0, 1)."""
+    try:
+        import torch.distributed as dist
+    except ImportError:  # pragma: no cover
+        return 0, 1
+    if dist.is_available() and dist.is_initialized():
+        return dist.get_rank(), dist.get_world_size()
+    return 0, 1
+
+
+def exchange_handles(mine: bytes, world: int) -> list[bytes]:
+    """All-gather the per-rank IPC handles (host plumbing, once per run)."""
+    if world == 1:
+        return [mine]
+    import torch.distributed as dist
+
+    out = [None] * world
+    dist.all_gather_object(out, bytes(mine))
+    return [bytes(h) for h in out]
+
+
+def assemble_handles(handles: list[bytes]) -> bytes:
+    if any(len(h) != _lib.IPC_HANDLE_BYTES for h in handles):
+        raise DeviceError("malformed CUDA IPC handle from a peer rank")
+    return b"".join(handles)
+
+
+class Comm:
+    """Owns a gpic_comm (exchange buffers of this process's shards)."""
+
+    def __init__(self, n: int, p: int, virtual: bool, rank: int = 0):
+        self.L = _lib.lib()
+        self.ptr = C.c_void_p()
+        if virtual:
+            _lib.check(self.L.gpic_comm_create_virtual(p, n, C.byref(self.ptr)))
+        else:
+            handle = (C.c_uint8 * _lib.IPC_HANDLE_BYTES)()
+            _lib.check(self.L.gpic_comm_create(p, rank, n, C.byref(self.ptr), handle))
+            allh = assemble_handles(exchange_handles(bytes(handle), p))
+            buf = (C.c_uint8 * len(allh)).from_buffer_copy(allh)
+            _lib.check(self.L.gpic_comm_open(self.ptr, buf))
+
+    def close(self):
+        if self.ptr:
+            self.L.gpic_comm_destroy(self.ptr)
+            self.ptr = C.c_void_p()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+
+def cluster(d, kind, params, config, seed):
+    """Sharded counterpart of gpu.cluster (same return contract)."""
+    from . import gpu
+
+    torch = gpu._torch()
+    sigma = gpu._check_kind(kind)
+    n = d.n
+    P = config.p
+    ranges = shard_ranges(n, P)
+    if config.virtual_ranks:
+        locals_ = list(range(P))
+        rank = 0
+    else:
+        rank, world = dist_context()
+        if world != P:
+            raise InvalidSpec(
+                f"KernelConfig(p={P}) without virtual_ranks needs a torch.distributed job of "
+                f"{P} ranks (one per GPU); world size is {world}"
+            )
+        locals_ = [rank]
+    dev = gpu._device(config)
+    st = gpu._stream(dev)
+    prep = gpu.prepare_points(d, dev)
+    blocks = [gpu.affinity_rows(prep, *ranges[r], sigma, config.affinity_impl) for r in locals_]
+    shards = (_lib.Shard * len(locals_))()
+    for i, (r, blk) in enumerate(zip(locals_, blocks)):
+        shards[i] = _lib.Shard(blk.a.data_ptr(), blk.lda, blk.deg.data_ptr(), ranges[r][0],
+                               ranges[r][1] - ranges[r][0])
+    T = params.max_iterations
+    eps = params.resolved_epsilon(n)
+    nl = len(locals_)
+    hist = torch.zeros(nl * T, dtype=torch.float64, device=dev)
+    vout = torch.empty(nl * n, dtype=torch.float64, device=dev)
+    ctls = (_lib.Ctl * nl)()
+    with Comm(n, P, config.virtual_ranks, rank) as comm:
+        L = comm.L
+        rc = L.gpic_comm_gather_degrees(comm.ptr, shards, nl, None, st)
+        if rc == _lib.GPIC_E_ZERO_DEGREE:
+            msg = _lib.last_error()
+            raise ZeroDegree(int(msg.split()[1]))
+        _lib.check(rc)
+        rc = L.gpic_comm_iterate(comm.ptr, shards, nl, eps, T, gpu._ptr(hist), gpu._ptr(vout),
+                                 ctls, st)
+        if rc != _lib.GPIC_OK:
+            bad = next((c for c in ctls if c.status != _lib.GPIC_OK), None)
+            _lib.raise_for(rc, bad)
+    # every shard holds the same embedding; local shard 0 speaks for the rank
+    h = ctls[0]
+    for c in ctls[1:]:
+        if c.iter != h.iter or c.converged != h.converged:
+            raise DeviceError("ranks disagree on the stop decision")
+    v = vout[:n]
+    labels = gpu.kmeans_1d(v, KMeansParams(k=params.k, seed=seed), config)
+    it = int(h.iter)
+    trace = PicTrace(it, hist[:it].cpu().numpy(), bool(h.converged))
+    return labels.cpu().numpy(), v.cpu().numpy(), trace
+
+
+def all_ranks_agree(labels: np.ndarray, v: np.ndarray) -> bool:
+    """Host check (real ranks): every rank returned bit-identical results."""
+    rank, world = dist_context()
+    if world == 1:
+        return True
+    import hashlib
+
+    import torch.distributed as dist
+
+    digest = hashlib.sha256(labels.tobytes() + v.tobytes()).hexdigest()
+    out = [None] * world
+    dist.all_gather_object(out, digest)
+    return all(x == out[0] for x in out)

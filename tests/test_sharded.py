@@ -1,0 +1,140 @@
+"""Multi-rank path: host logic on CPU (gloo, world_size 2) and GPU-count
+invariance on one GPU (virtual ranks + two processes sharing the device).
+
+Mirrors the reference's bitwise p-invariance tests (test_parallel.py:194-223,
+test_acceptance.py:127-155): the embedding, deltas and labels must be
+IDENTICAL for any rank count.
+"""
+
+import os
+import pathlib
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_1604_02700_b200 import GaussianRbf, KernelConfig, PicParams, cluster, gaussian_blobs
+from paper_1604_02700_b200 import _lib, errors, sharded
+
+ROOT = pathlib.Path(__file__).resolve().parent.parent
+
+
+# ------------------------------------------------------------- CPU / gloo
+@pytest.mark.parametrize("n,p", [(10, 4), (9, 4), (100_000, 8), (8, 8), (1000, 3)])
+def test_shard_ranges_cover_and_nonempty(n, p):
+    r = sharded.shard_ranges(n, p)
+    assert len(r) == p and r[0][0] == 0 and r[-1][1] == n
+    assert all(b > a for a, b in r)
+    assert all(r[i][1] == r[i + 1][0] for i in range(p - 1))
+    assert max(b - a for a, b in r) - min(b - a for a, b in r) <= 1
+
+
+def test_shard_ranges_rejects():
+    with pytest.raises(errors.InvalidSpec):
+        sharded.shard_ranges(3, 4)
+    with pytest.raises(errors.InvalidSpec):
+        sharded.shard_ranges(100, 9)
+
+
+def _gloo_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        assert sharded.dist_context() == (rank, world)
+        mine = bytes([rank]) * _lib.IPC_HANDLE_BYTES
+        got = sharded.exchange_handles(mine, world)
+        blob = sharded.assemble_handles(got)
+        ok_handles = blob == b"".join(bytes([r]) * _lib.IPC_HANDLE_BYTES for r in range(world))
+        same = sharded.all_ranks_agree(np.arange(5), np.ones(5))
+        diff = sharded.all_ranks_agree(np.arange(5) + rank, np.ones(5))
+        q.put((rank, ok_handles, same, diff))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_handle_exchange_and_agreement_gloo():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29500 + os.getpid() % 1000
+    procs = [ctx.Process(target=_gloo_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    assert [r[0] for r in res] == [0, 1]
+    assert all(r[1] for r in res)          # every rank saw every handle, in rank order
+    assert all(r[2] for r in res)          # identical results agree
+    assert not any(r[3] for r in res)      # differing results are caught
+
+
+def test_world_mismatch_is_rejected_without_a_gpu_call():
+    cfg = KernelConfig(p=2)
+    assert sharded.dist_context() == (0, 1)
+    if torch.cuda.is_available():
+        with pytest.raises(errors.InvalidSpec):
+            cluster(gaussian_blobs(100, 4, 2, seed=0), GaussianRbf(1.0), PicParams(k=2), config=cfg)
+
+
+def test_malformed_handle_rejected():
+    with pytest.raises(errors.DeviceError):
+        sharded.assemble_handles([b"x" * 64, b"y" * 10])
+
+
+# ------------------------------------------------------------------ GPU
+@pytest.mark.gpu
+@pytest.mark.parametrize("engine", ["tc", "simt"])
+def test_virtual_ranks_bitwise_invariant(engine):
+    d = gaussian_blobs(3000, 32, 5, seed=2)
+    kind, params = GaussianRbf(float(np.sqrt(32) / 2)), PicParams(k=5)
+    base = cluster(d, kind, params, config=KernelConfig(affinity_impl=engine), seed=1)
+    for p in (2, 3, 4, 8):
+        got = cluster(d, kind, params, seed=1,
+                      config=KernelConfig(p=p, virtual_ranks=True, affinity_impl=engine))
+        assert np.array_equal(got[0], base[0]), p
+        assert np.array_equal(got[1], base[1]), p
+        assert got[2].iterations_run == base[2].iterations_run
+        assert np.array_equal(got[2].delta_history, base[2].delta_history), p
+
+
+@pytest.mark.gpu
+def test_virtual_ranks_forced_iterations_and_repeat():
+    d = gaussian_blobs(2048, 16, 4, seed=3)
+    kind = GaussianRbf(2.0)
+    params = PicParams(k=4, epsilon=5e-324, max_iterations=9)
+    base = cluster(d, kind, params)
+    cfg = KernelConfig(p=4, virtual_ranks=True)
+    a = cluster(d, kind, params, config=cfg)
+    b = cluster(d, kind, params, config=cfg)   # second run: epochs keep increasing
+    for r in (a, b):
+        assert r[2].iterations_run == 9 and not r[2].converged
+        assert np.array_equal(r[1], base[1])
+
+
+@pytest.mark.gpu
+def test_virtual_ranks_zero_degree():
+    pts = np.array([[0.0], [0.05], [0.1], [100.0], [0.2], [0.3]])
+    from paper_1604_02700_b200 import DataSet
+
+    with pytest.raises(errors.ZeroDegree) as e:
+        cluster(DataSet(pts), GaussianRbf(1.0), PicParams(k=2),
+                config=KernelConfig(p=3, virtual_ranks=True))
+    assert e.value.index == 3
+
+
+@pytest.mark.gpu
+def test_two_processes_one_device_ipc():
+    """Real ranks (torchrun, 2 processes) sharing one GPU through CUDA IPC."""
+    script = ROOT / "tests" / "dist_worker.py"
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", str(29600 + os.getpid() % 300),
+           str(script)]
+    env = dict(os.environ, GPIC_SAME_DEVICE="1")
+    res = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env, cwd=ROOT)
+    assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-3000:]
+    assert "RANKS_AGREE True" in res.stdout and "MATCHES_SINGLE True" in res.stdout
