@@ -196,6 +196,51 @@ def workload(cfg, gpus):
 
 
 # ---------------------------------------------------------- ours
+def _gemv_roofline(args, L, C, torch, stream, st, n, m, k, T, work, v, storage):
+    """Time the dominant kernel (the power-iteration GEMV) on the resident
+    affinity storage, CUDA events on the launching stream."""
+    scratch = int(L.gpic_workspace_bytes(n, m, k, n, T))
+    base = work.data_ptr() + scratch
+    dev = work.device
+    vp = int(L.gpic_vector_pitch(n))
+    v32 = torch.zeros(vp, dtype=torch.float32, device=dev)
+    v32[:n] = v.to(torch.float32)
+    yv = torch.empty(n, dtype=torch.float64, device=dev)
+    deg1 = torch.ones(n, dtype=torch.float64, device=dev)
+    if storage == 1:
+        ntiles = int(L.gpic_packed_tiles(n))
+        tile_bytes = ntiles * 128 * 128 * 4
+        rowp = base + tile_bytes
+        colp = rowp + ((ntiles * 128 * 4 + 255) // 256) * 256
+
+        def launch():
+            return L.gpic_sym_matvec(C.c_void_p(base), n, C.c_void_p(v32.data_ptr()),
+                                     C.c_void_p(rowp), C.c_void_p(colp),
+                                     C.c_void_p(deg1.data_ptr()), C.c_void_p(yv.data_ptr()), st)
+        alg = float(tile_bytes)
+        name = "sym_gemv_kernel + sym_reduce_kernel (packed symmetric tiles)"
+    else:
+        lda = int(L.gpic_affinity_pitch(n))
+
+        def launch():
+            return L.gpic_matvec(C.c_void_p(base), lda, n, n, C.c_void_p(v32.data_ptr()),
+                                 C.c_void_p(deg1.data_ptr()), C.c_void_p(yv.data_ptr()), st)
+        alg = float(n) * n * 4
+        name = "gemv_bulk_kernel (dense rows)"
+    times = []
+    for rep in range(args.gemv_reps + 2):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        rc = launch()
+        e1.record(stream)
+        e1.synchronize()
+        if rc:
+            raise RuntimeError(f"GEMV launch failed: {rc}")
+        if rep >= 2:
+            times.append(e0.elapsed_time(e1))
+    return name, alg, statistics.mean(times)
+
+
 def run_ours(args, cfg, rank, world):
     import ctypes as C
 
@@ -206,7 +251,7 @@ def run_ours(args, cfg, rank, world):
     from paper_1604_02700_b200.validation import adjusted_rand_index, contingency
 
     if world > 1:
-        raise SystemExit("multi-GPU bench path lands with the sharded engine")
+        return run_ours_sharded(args, cfg, rank, world)
     dev = torch.device("cuda", 0)
     torch.cuda.set_device(dev)
     c = CONFIGS[cfg]
@@ -215,7 +260,9 @@ def run_ours(args, cfg, rank, world):
     sigma = c["sigma"]
     params = PicParams(k=k)
     impl_name = args.engine
+    cfg_api = KernelConfig(affinity_impl=impl_name, storage=args.storage)
     impl = _lib.AFFINITY_TC if impl_name == "tc" else _lib.AFFINITY_SIMT
+    storage = cfg_api.storage_code()
     L = _lib.lib()
     stream = torch.cuda.current_stream(dev)
     st = C.c_void_p(stream.cuda_stream)
@@ -225,10 +272,10 @@ def run_ours(args, cfg, rank, world):
     host.numpy()[:] = d.points
     d_host = DataSet(host.numpy(), d.labels)
 
-    # device-resident leg
+    # device-resident leg: one libgpic call per step on X already in HBM
     x = torch.from_numpy(d.points).to(dev)
     T = params.max_iterations
-    nbytes = gpu.workspace_bytes(n, m, k, T)
+    nbytes = gpu.workspace_bytes(n, m, k, T, storage)
     work = torch.empty(nbytes, dtype=torch.uint8, device=dev)
     labels = torch.empty(n, dtype=torch.int64, device=dev)
     v = torch.empty(n, dtype=torch.float64, device=dev)
@@ -239,9 +286,10 @@ def run_ours(args, cfg, rank, world):
 
     def step():
         rc = L.gpic_cluster(C.c_void_p(x.data_ptr()), n, m, sigma, k, eps, T, first,
-                            u.ctypes.data_as(C.c_void_p), impl, C.c_void_p(labels.data_ptr()),
-                            C.c_void_p(v.data_ptr()), C.c_void_p(hist.data_ptr()), C.byref(iters),
-                            C.byref(conv), C.c_void_p(work.data_ptr()), nbytes, st)
+                            u.ctypes.data_as(C.c_void_p), impl, storage,
+                            C.c_void_p(labels.data_ptr()), C.c_void_p(v.data_ptr()),
+                            C.c_void_p(hist.data_ptr()), C.byref(iters), C.byref(conv),
+                            C.c_void_p(work.data_ptr()), nbytes, st)
         _lib.raise_for(rc)
 
     for _ in range(args.warmup):
@@ -256,38 +304,19 @@ def run_ours(args, cfg, rank, world):
             step()
         ev1.record(stream)
         torch.cuda.synchronize()
-    launches = L.gpic_launch_count() - launches0
+    launches = (L.gpic_launch_count() - launches0) // args.steps
     ms = ev0.elapsed_time(ev1) / args.steps
     lab_np = labels.cpu().numpy()
     ari = adjusted_rand_index(contingency(d.labels, lab_np))
 
-    # roofline of the dominant kernel: the GEMV over the resident A
-    lda = int(L.gpic_affinity_pitch(n))
-    scratch = int(L.gpic_workspace_bytes(n, m, k, n, T))
-    a_ptr = work.data_ptr() + scratch
-    v32 = torch.zeros(lda, dtype=torch.float32, device=dev)
-    v32[:n] = v.to(torch.float32)
-    deg_dummy = torch.ones(n, dtype=torch.float64, device=dev)
-    yv = torch.empty(n, dtype=torch.float64, device=dev)
-    gemv_ms = []
-    for rep in range(args.gemv_reps + 2):
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        _lib.check(L.gpic_matvec(C.c_void_p(a_ptr), lda, n, n, C.c_void_p(v32.data_ptr()),
-                                 C.c_void_p(deg_dummy.data_ptr()), C.c_void_p(yv.data_ptr()), st))
-        e1.record(stream)
-        e1.synchronize()
-        if rep >= 2:
-            gemv_ms.append(e0.elapsed_time(e1))
-    gemv_avg = statistics.mean(gemv_ms)
-    alg_bytes = float(n) * n * 4
-    achieved = alg_bytes / (gemv_avg * 1e-3) / 1e9
+    kname, alg_bytes, gemv_ms = _gemv_roofline(args, L, C, torch, stream, st, n, m, k, T, work,
+                                               v, storage)
+    achieved = alg_bytes / (gemv_ms * 1e-3) / 1e9
+    dense_equiv = float(n) * n * 4 / (gemv_ms * 1e-3) / 1e9
     peak, peak_kind = peaks()
 
     # e2e leg through the public API from pinned host memory
-    cfg_api = KernelConfig(affinity_impl=impl_name)
-    for _ in range(1):
-        cluster(d_host, GaussianRbf(sigma), params, config=cfg_api, seed=0)
+    cluster(d_host, GaussianRbf(sigma), params, config=cfg_api, seed=0)
     torch.cuda.synchronize()
     e2e = []
     for _ in range(max(1, args.e2e_steps)):
@@ -300,20 +329,23 @@ def run_ours(args, cfg, rank, world):
     traffic = None
     prof = ROOT / "profiles" / "gemv_traffic.json"
     if prof.exists():
-        traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch")
+        j = json.loads(prof.read_text())
+        if j.get("storage", "packed") == args.storage and j.get("n") == n:
+            traffic = j.get("dram_bytes_per_launch")
 
     line = {
         "metric": METRIC, "value": ms / 1e3, "unit": "s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,
-        "scaling": "weak" if world > 1 else "strong", "vs_baseline": None,
-        "dtype": "f32 (fp64 vectors/reductions)", "data": "synthetic (SURVEY App. B gaussian blobs, seed 0)",
-        "config": dict(workload(cfg, world), affinity_engine=impl_name),
-        "power_iter_hbm_gbs": achieved, "iterations": int(iters.value), "converged": bool(conv.value),
-        "ari_vs_truth": ari,
-        "roofline": {"kernel": "gemv_kernel (power iteration)", "bound": "hbm",
-                     "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": traffic,
-                     "algorithmic_bytes_per_launch": alg_bytes, "avg_launch_ms": gemv_avg},
+        "scaling": "strong", "vs_baseline": None,
+        "dtype": "f32 (tf32x3 Gram, fp64 vectors/reductions)",
+        "data": "synthetic (SURVEY App. B gaussian blobs, seed 0)",
+        "config": dict(workload(cfg, world), affinity_engine=impl_name, storage=args.storage),
+        "power_iter_hbm_gbs": achieved, "power_iter_dense_equiv_gbs": dense_equiv,
+        "iterations": int(iters.value), "converged": bool(conv.value), "ari_vs_truth": ari,
+        "roofline": {"kernel": kname, "bound": "hbm", "achieved": achieved, "peak": peak,
+                     "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": traffic, "algorithmic_bytes_per_launch": alg_bytes,
+                     "avg_launch_ms": gemv_ms},
         "e2e": {"value": e2e_s, "unit": "s", "h2d_bytes_per_step": int(n * m * 8),
                 "d2h_bytes_per_step": int(n * 8 * 2 + T * 8)},
         "gpu_launches": int(launches),
@@ -324,9 +356,88 @@ def run_ours(args, cfg, rank, world):
         full, det, _ = cpu_reference_sample(d.points, sigma, k, max(int(iters.value), 1),
                                             args.ref_rows, threads)
         line["cpu_baseline"] = {"value": full, "unit": "s", "cores": threads, "kind": "port",
-                                "sample": f"{args.ref_rows} of {n} rows, scaled x{n / args.ref_rows:.1f}",
+                                "sample": f"{args.ref_rows} of {n} affinity rows + matvecs, "
+                                          f"scaled x{n / args.ref_rows:.1f}; k-means on full n",
                                 "phases": det}
     print(json.dumps(line), flush=True)
+
+
+def run_ours_sharded(args, cfg, rank, world):
+    """N > 1: one rank per GPU, row-sharded dense A, fused P2P y exchange."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1604_02700_b200 import DataSet, GaussianRbf, KernelConfig, PicParams
+    from paper_1604_02700_b200 import _lib, sharded
+    from paper_1604_02700_b200.validation import adjusted_rand_index, contingency
+
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    c = CONFIGS[cfg]
+    d = config_dataset(cfg, seed=0)
+    n, m, k, sigma = d.n, d.m, c["k"], c["sigma"]
+    params = PicParams(k=k)
+    config = KernelConfig(p=world, device=local, affinity_impl=args.engine, storage="dense")
+    runner = sharded.ShardedRunner(n, config)
+    x = torch.from_numpy(d.points).to(dev)
+    stream = torch.cuda.current_stream(dev)
+    L = _lib.lib()
+    for _ in range(args.warmup):
+        runner.run(x, sigma, params, 0)
+    torch.cuda.synchronize()
+    dist.barrier()
+    launches0 = L.gpic_launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        dist.barrier()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            labels, v, trace = runner.run(x, sigma, params, 0)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    dist.barrier()
+    ms_local = ev0.elapsed_time(ev1) / args.steps
+    t = torch.tensor([ms_local], device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    launches = (L.gpic_launch_count() - launches0) // args.steps
+    lab_np = labels.cpu().numpy()
+    agree = sharded.all_ranks_agree(lab_np, v.cpu().numpy())
+    # e2e: host X in, host labels / v out, through the public runner
+    host = torch.empty((n, m), dtype=torch.float64).pin_memory()
+    host.numpy()[:] = d.points
+    d_host = DataSet(host.numpy(), d.labels)
+    e2e = []
+    for _ in range(max(1, args.e2e_steps)):
+        dist.barrier()
+        t0 = time.perf_counter()
+        lab_e, v_e, _ = runner.run(d_host, sigma, params, 0)
+        lab_e, v_e = lab_e.cpu().numpy(), v_e.cpu().numpy()
+        e2e.append(time.perf_counter() - t0)
+    te = torch.tensor([statistics.mean(e2e)], device=dev)
+    dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    runner.close()
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": ms / 1e3, "unit": "s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f32 (tf32x3 Gram, fp64 vectors/reductions)",
+            "data": "synthetic (SURVEY App. B gaussian blobs, seed 0)",
+            "config": dict(workload(cfg, world), affinity_engine=args.engine, storage="dense",
+                           parallelism=f"row-shard x{world}, fused P2P y all-gather"),
+            "iterations": trace.iterations_run, "converged": trace.converged,
+            "ari_vs_truth": adjusted_rand_index(contingency(d.labels, lab_np)),
+            "ranks_agree_bitwise": agree,
+            "e2e": {"value": float(te.item()), "unit": "s", "h2d_bytes_per_step": int(n * m * 8),
+                    "d2h_bytes_per_step": int(n * 8 * 2)},
+            "gpu_launches": int(launches), "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
 
 
 def main():
@@ -337,6 +448,7 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", type=int, default=3)
     ap.add_argument("--engine", choices=["tc", "simt"], default="tc")
+    ap.add_argument("--storage", choices=["packed", "dense"], default="packed")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--gemv-reps", type=int, default=10)
     ap.add_argument("--ref-rows", type=int, default=256)

@@ -149,23 +149,45 @@ int gpic_reduce_sum(const double* d_v, int64_t n, double* d_out, void* d_work, v
  * scale = d_inv_deg (fp64, may be NULL for 1). */
 int gpic_matvec(const float* d_a, int64_t lda, int64_t rows, int64_t n, const float* d_v,
                 const double* d_row_scale, double* d_y, void* stream);
+/* k_multiply on PACKED symmetric tiles (gpic_packed_tiles(n) tiles of
+ * 128 x 128 fp32, upper triangle): y = (A v) * scale_i. d_v holds
+ * gpic_vector_pitch(n) floats (zero padded); d_rowp / d_colp hold
+ * gpic_packed_tiles(n) * 128 floats each (per-tile partials). */
+int gpic_sym_matvec(const float* d_tiles, int64_t n, const float* d_v, float* d_rowp,
+                    float* d_colp, const double* d_row_scale, double* d_y, void* stream);
+int64_t gpic_vector_pitch(int64_t n);
 
 /* ---- whole pipeline ----------------------------------------------------
  * cluster (serial.py:131-150 / parallel.py:236-255) for one rank owning the
- * whole matrix. Device in/out; d_work must hold gpic_workspace_bytes(n, d,
- * k, n, max_iter). Synchronous: returns the first error. */
+ * whole matrix. Device in/out; d_work must hold
+ * gpic_cluster_workspace_bytes(n, d, k, max_iter, storage). Synchronous:
+ * returns the first error.
+ *
+ * storage: GPIC_STORAGE_DENSE keeps A as n x pitch(n) fp32 rows (4n^2 bytes
+ * per power iteration); GPIC_STORAGE_PACKED keeps only the upper triangle
+ * of 128 x 128 tiles (A is exactly symmetric, test_affinity.py:81-87): half
+ * the bytes for the affinity store and for every iteration's GEMV
+ * (tcgen05 engine only). */
+#define GPIC_STORAGE_DENSE 0
+#define GPIC_STORAGE_PACKED 1
+int64_t gpic_packed_tiles(int64_t n);
+int64_t gpic_cluster_workspace_bytes(int64_t n, int32_t d, int32_t k, int32_t max_iter,
+                                     int32_t storage);
 int gpic_cluster(const double* d_x, int64_t n, int32_t d, double sigma, int32_t k, double eps,
                  int32_t max_iter, int64_t first_index, const double* h_uniforms, int32_t impl,
-                 int64_t* d_labels, double* d_v, double* d_delta_hist, int32_t* h_iters,
-                 int32_t* h_converged, void* d_work, int64_t work_bytes, void* stream);
+                 int32_t storage, int64_t* d_labels, double* d_v, double* d_delta_hist,
+                 int32_t* h_iters, int32_t* h_converged, void* d_work, int64_t work_bytes,
+                 void* stream);
 
 /* Same, HOST buffers in and out (the reference-facing call a ctypes/cffi
- * binding makes): copies X in, runs, copies labels/v/deltas out. */
+ * binding makes): copies X in, runs, copies labels/v/deltas out. d_work
+ * must hold gpic_cluster_workspace_bytes(...) (256-aligned) + the staging
+ * of X (n*d*8), labels and v (n*8 each) and the deltas (max_iter*8). */
 int gpic_cluster_host(const double* h_x, int64_t n, int32_t d, double sigma, int32_t k,
                       double eps, int32_t max_iter, int64_t first_index, const double* h_uniforms,
-                      int32_t impl, int64_t* h_labels, double* h_v, double* h_delta_hist,
-                      int32_t* h_iters, int32_t* h_converged, void* d_work, int64_t work_bytes,
-                      void* stream);
+                      int32_t impl, int32_t storage, int64_t* h_labels, double* h_v,
+                      double* h_delta_hist, int32_t* h_iters, int32_t* h_converged, void* d_work,
+                      int64_t work_bytes, void* stream);
 
 /* Reset a control block (iteration 0, no error) with the stop threshold and
  * iteration cap of the run. */

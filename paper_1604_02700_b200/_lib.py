@@ -27,6 +27,9 @@ GPIC_E_UNSUPPORTED = 18
 AFFINITY_TC = 0
 AFFINITY_SIMT = 1
 
+STORAGE_DENSE = 0
+STORAGE_PACKED = 1
+
 
 class Ctl(C.Structure):
     """Mirror of struct gpic_ctl (256 bytes)."""
@@ -75,10 +78,14 @@ SIGNATURES = {
     "gpic_reduce_sum": (C.c_int, [P, I64, P, P, P]),
     "gpic_scale": (C.c_int, [P, I64, F64, P, P, I64, P]),
     "gpic_matvec": (C.c_int, [P, I64, I64, I64, P, P, P, P]),
-    "gpic_cluster": (C.c_int, [P, I64, I32, F64, I32, F64, I32, I64, P, I32, P, P, P, P, P, P,
-                               I64, P]),
-    "gpic_cluster_host": (C.c_int, [P, I64, I32, F64, I32, F64, I32, I64, P, I32, P, P, P, P, P,
-                                    P, I64, P]),
+    "gpic_packed_tiles": (I64, [I64]),
+    "gpic_vector_pitch": (I64, [I64]),
+    "gpic_sym_matvec": (C.c_int, [P, I64, P, P, P, P, P, P]),
+    "gpic_cluster_workspace_bytes": (I64, [I64, I32, I32, I32, I32]),
+    "gpic_cluster": (C.c_int, [P, I64, I32, F64, I32, F64, I32, I64, P, I32, I32, P, P, P, P, P,
+                               P, I64, P]),
+    "gpic_cluster_host": (C.c_int, [P, I64, I32, F64, I32, F64, I32, I64, P, I32, I32, P, P, P,
+                                    P, P, P, I64, P]),
     "gpic_ctl_read": (C.c_int, [P, P, P]),
     "gpic_launch_count": (I64, []),
     "gpic_comm_create": (C.c_int, [I32, I32, I64, P, P]),

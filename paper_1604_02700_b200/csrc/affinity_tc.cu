@@ -69,7 +69,38 @@ struct TcArgs {
   int64_t rows_pad;
   int64_t n_rtiles;  // row blocks of 128*MB rows
   int64_t n_ctiles;  // column tiles of 128
+  int packed;        // 1: symmetric packed output (tiles J >= I only, no row partials)
 };
+
+// Work item t -> (row block, column tile). Dense: all column tiles of every
+// row block. Packed (symmetric): column tiles cb >= rb*MB only, so the
+// upper triangle of 128x128 tiles is computed once.
+template <int MB>
+__device__ __forceinline__ void decode(int64_t t, const TcArgs& a, int64_t& rb, int64_t& cb) {
+  if (!a.packed) {
+    rb = t / a.n_ctiles;
+    cb = t % a.n_ctiles;
+    return;
+  }
+  // S(r) = r*NC - MB*r*(r-1)/2 items precede row block r
+  int64_t lo = 0, hi = a.n_rtiles - 1;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi + 1) >> 1;
+    const int64_t s = mid * a.n_ctiles - (int64_t)MB * mid * (mid - 1) / 2;
+    if (s <= t) lo = mid; else hi = mid - 1;
+  }
+  rb = lo;
+  cb = rb * MB + (t - (lo * a.n_ctiles - (int64_t)MB * lo * (lo - 1) / 2));
+}
+
+__host__ __device__ inline int64_t packed_items(int64_t nrt, int64_t nct, int mb) {
+  return nrt * nct - (int64_t)mb * nrt * (nrt - 1) / 2;
+}
+
+// Packed index of tile (I, J), J >= I, row-major over the upper triangle.
+__host__ __device__ inline int64_t tile_index(int64_t I, int64_t J, int64_t nt) {
+  return I * nt - I * (I - 1) / 2 + (J - I);
+}
 
 template <int KB>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -96,7 +127,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int64_t total = args.n_rtiles * args.n_ctiles;
+  const int64_t total = args.packed ? packed_items(args.n_rtiles, args.n_ctiles, MB)
+                                    : args.n_rtiles * args.n_ctiles;
   const int64_t t_begin = total * blockIdx.x / gridDim.x;
   const int64_t t_end = total * (blockIdx.x + 1) / gridDim.x;
 
@@ -136,7 +168,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       int s = 0;
       uint32_t ph = 0;
       for (int64_t t = t_begin; t < t_end; ++t) {
-        const int64_t rb = t / args.n_ctiles, cb = t % args.n_ctiles;
+        int64_t rb, cb;
+        decode<MB>(t, args, rb, cb);
         if (rb != cur_rb) {
           mbar_wait(a_empty, a_par);
           a_par ^= 1;
@@ -167,7 +200,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t ph = 0;
       int i = 0;
       for (int64_t t = t_begin; t < t_end; ++t, ++i) {
-        const int64_t rb = t / args.n_ctiles;
+        int64_t rb, cb;
+        decode<MB>(t, args, rb, cb);
         if (rb != cur_rb) {
           mbar_wait(a_full, a_par);
           a_par ^= 1;
@@ -199,7 +233,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (++s == ST) { s = 0; ph ^= 1; }
         }
         tc_commit(&t_full[buf]);
-        const bool last_of_block = (t + 1 == t_end) || ((t + 1) / args.n_ctiles != rb);
+        int64_t nrb = -1, ncb;
+        if (t + 1 < t_end) decode<MB>(t + 1, args, nrb, ncb);
+        const bool last_of_block = (t + 1 == t_end) || (nrb != rb);
         if (last_of_block) tc_commit(a_empty);
       }
     }
@@ -222,7 +258,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     // L2 latency hides behind the TMEM-full wait
     float nx_cb[NC], nx_ra = 0.f;
     auto prefetch = [&](int64_t t) {
-      const int64_t rb = t / args.n_ctiles, cb = t % args.n_ctiles;
+      int64_t rb, cb;
+      decode<MB>(t, args, rb, cb);
 #pragma unroll
       for (int cc = 0; cc < NC; ++cc)
         nx_cb[cc] = ns * __ldg(args.sqn + cb * kBN + (c_lo + cc) * 32 + lane);
@@ -231,8 +268,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     };
     if (t_begin < t_end) prefetch(t_begin);
     for (int64_t t = t_begin; t < t_end; ++t, ++i) {
-      const int64_t rb = t / args.n_ctiles, cb = t % args.n_ctiles;
+      int64_t rb, cb;
+      decode<MB>(t, args, rb, cb);
       const int buf = i & 1;
+      const int64_t tI = rb * MB + m;  // tile row of this warp's rows
+      // packed: the lower-triangle half of a diagonal row block is not stored
+      const bool store_ok = !args.packed || tI <= cb;
+      const int64_t out_row0 = args.packed ? tile_index(tI, cb, args.n_ctiles) * 128 + q * 32
+                                           : (rb * MB + m) * 128 + q * 32;
       const int64_t lr0 = (rb * MB + m) * 128 + q * 32;  // shard-local first row of this warp
       const int64_t lr = lr0 + lane;
       const int64_t gr = args.row_lo + lr;
@@ -258,7 +301,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         const int64_t col0 = cb * kBN + c * 32;
         const bool diag = (col0 < args.row_lo + lr0 + 32) && (args.row_lo + lr0 < col0 + 32);
-        const bool pad = col0 + 32 > args.n;
+        const bool pad = col0 + 32 > args.n || args.row_lo + lr0 + 32 > args.n;
         float vals[32];
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
@@ -269,7 +312,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (diag || pad) {
 #pragma unroll
           for (int j = 0; j < 32; ++j)
-            if (col0 + j == gr || col0 + j >= args.n) vals[j] = 0.f;
+            if (col0 + j == gr || col0 + j >= args.n || gr >= args.n) vals[j] = 0.f;
         }
 #pragma unroll
         for (int j = 0; j < 32; ++j) rsum += vals[j];
@@ -289,9 +332,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         fence_async_smem();
         __syncwarp();
-        if (lane == 0) tma_store_2d(&map_out, (int)col0, (int)lr0, stage);
+        if (lane == 0 && store_ok)
+          tma_store_2d(&map_out, args.packed ? c * 32 : (int)col0, (int)out_row0, stage);
         ++stores;
       }
+      if (args.packed) continue;  // degrees come from the symmetric GEMV
       if constexpr (MB == 2) {
         if (lr < args.rows) args.rowpart[cb * args.rows_pad + lr] = rsum;
       } else {
@@ -363,7 +408,8 @@ int launch_kb(const CUtensorMap& mh, const CUtensorMap& ml, const CUtensorMap& m
     GPIC_CUDA_TRY(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev));
     attr = true;
   }
-  const int64_t total = a.n_rtiles * a.n_ctiles;
+  const int64_t total =
+      a.packed ? packed_items(a.n_rtiles, a.n_ctiles, MB) : a.n_rtiles * a.n_ctiles;
   const int grid = (int)(total < num_sms ? total : num_sms);
   affinity_tc_kernel<KB><<<grid, kThreads, smem_bytes(KB), s>>>(mh, ml, mo, a);
   count_launch();
@@ -372,6 +418,40 @@ int launch_kb(const CUtensorMap& mh, const CUtensorMap& ml, const CUtensorMap& m
 }
 
 }  // namespace
+
+namespace {
+int dispatch_kb(int KB, const CUtensorMap& mh, const CUtensorMap& ml, const CUtensorMap& mo,
+                const TcArgs& args, cudaStream_t s) {
+  switch (KB) {
+    case 1: return launch_kb<1>(mh, ml, mo, args, s);
+    case 2: return launch_kb<2>(mh, ml, mo, args, s);
+    case 3: return launch_kb<3>(mh, ml, mo, args, s);
+    default: return launch_kb<4>(mh, ml, mo, args, s);
+  }
+}
+}  // namespace
+
+int64_t packed_tiles(int64_t n) {
+  const int64_t nt = ceil_div(n, kBN);
+  return nt * (nt + 1) / 2;
+}
+
+// Symmetric packed output: tile (I, J), J >= I, stored as a contiguous
+// 128 x 128 fp32 block at tile_index(I, J) (row-major over the triangle).
+int launch_affinity_tc_packed(const float* xhi, const float* xlo, const float* sqn, int64_t n,
+                              int32_t dp, float neg_scale_log2, float* a_packed, cudaStream_t s) {
+  const int KB = dp / kKBlk;
+  if (dp % kKBlk || KB < 1 || KB > 4)
+    return fail(GPIC_E_UNSUPPORTED, "tcgen05 affinity engine supports d <= 128");
+  const int64_t npad = row_pad(n);
+  CUtensorMap mh, ml, mo;
+  if (!make_map(&mh, xhi, (uint64_t)dp, (uint64_t)npad, (uint64_t)dp * 4, kKBlk, 128) ||
+      !make_map(&ml, xlo, (uint64_t)dp, (uint64_t)npad, (uint64_t)dp * 4, kKBlk, 128) ||
+      !make_map(&mo, a_packed, 128, (uint64_t)packed_tiles(n) * 128, 512, 32, 32))
+    return fail(GPIC_E_CUDA, "cuTensorMapEncodeTiled failed");
+  TcArgs args{sqn, n, 0, n, neg_scale_log2, nullptr, 0, 0, ceil_div(n, kBN), 1};
+  return dispatch_kb(KB, mh, ml, mo, args, s);
+}
 
 int launch_affinity_tc(const float* xhi, const float* xlo, const float* sqn, int64_t n,
                        int32_t dp, int64_t row_lo, int64_t row_hi, float neg_scale_log2, float* a,
@@ -386,13 +466,8 @@ int launch_affinity_tc(const float* xhi, const float* xlo, const float* sqn, int
       !make_map(&ml, xlo, (uint64_t)dp, (uint64_t)npad, (uint64_t)dp * 4, kKBlk, 128) ||
       !make_map(&mo, a, (uint64_t)lda, (uint64_t)rows, (uint64_t)lda * 4, 32, 32))
     return fail(GPIC_E_CUDA, "cuTensorMapEncodeTiled failed");
-  TcArgs args{sqn, n, row_lo, rows, neg_scale_log2, rowpart, rows_pad, 0, ceil_div(n, kBN)};
-  switch (KB) {
-    case 1: return launch_kb<1>(mh, ml, mo, args, s);
-    case 2: return launch_kb<2>(mh, ml, mo, args, s);
-    case 3: return launch_kb<3>(mh, ml, mo, args, s);
-    default: return launch_kb<4>(mh, ml, mo, args, s);
-  }
+  TcArgs args{sqn, n, row_lo, rows, neg_scale_log2, rowpart, rows_pad, 0, ceil_div(n, kBN), 0};
+  return dispatch_kb(KB, mh, ml, mo, args, s);
 }
 
 }  // namespace gpic

@@ -47,7 +47,7 @@ int64_t workspace_bytes(int64_t n, int32_t d, int32_t k, int64_t rows, int32_t /
   b += al(n * 8);                             // y
   b += al(n * 8);                             // deg
   b += al(2 * n * 8);                         // v64
-  b += al(affinity_pitch(n) * 4);             // v32
+  b += al(vector_pitch(n) * 4);               // v32
   b += al(kmeans_scratch_bytes(n, k));        // kmeans
   return b;
 }
@@ -75,7 +75,7 @@ int carve(void* base, int64_t bytes, int64_t n, int32_t d, int32_t k, int64_t ro
   ws->y = reinterpret_cast<double*>(take(n * 8));
   ws->deg = reinterpret_cast<double*>(take(n * 8));
   ws->v64 = reinterpret_cast<double*>(take(2 * n * 8));
-  ws->v32 = reinterpret_cast<float*>(take(affinity_pitch(n) * 4));
+  ws->v32 = reinterpret_cast<float*>(take(vector_pitch(n) * 4));
   ws->kscratch_bytes = kmeans_scratch_bytes(n, k);
   ws->kscratch = reinterpret_cast<double*>(take(ws->kscratch_bytes));
   ws->end = p;
@@ -182,7 +182,7 @@ int gpic_initial_vector(const double* d_deg, int64_t n, double* d_v64, float* d_
   double* part = static_cast<double*>(d_work);
   double* tau = part + ceil_div(n, kRedBlock);
   launch_tree_sum(d_deg, n, part, tau, d_ctl, s);
-  launch_scale_vector(d_deg, n, tau, d_v64, d_v32, affinity_pitch(n), s);
+  launch_scale_vector(d_deg, n, tau, d_v64, d_v32, vector_pitch(n), s);
   GPIC_CUDA_TRY(cudaGetLastError());
   return GPIC_OK;
 }
@@ -233,6 +233,21 @@ int gpic_scale(const double* d_src, int64_t n, double tau, double* d_dst, float*
 
 int64_t gpic_kmeans_scratch_bytes(int64_t n, int32_t k) { return kmeans_scratch_bytes(n, k); }
 
+int gpic_sym_matvec(const float* d_tiles, int64_t n, const float* d_v, float* d_rowp,
+                    float* d_colp, const double* d_row_scale, double* d_y, void* stream) {
+  if (n < 1) return fail(GPIC_E_EMPTY, "empty matrix");
+  PeerTable pt;
+  std::memset(&pt, 0, sizeof pt);
+  pt.y[0][0] = pt.y[0][1] = d_y;
+  pt.nranks = 1;
+  launch_sym_gemv(d_tiles, n, d_v, d_rowp, d_colp, d_row_scale, pt, nullptr,
+                  static_cast<cudaStream_t>(stream));
+  GPIC_CUDA_TRY(cudaGetLastError());
+  return GPIC_OK;
+}
+
+int64_t gpic_vector_pitch(int64_t n) { return vector_pitch(n); }
+
 int gpic_matvec(const float* d_a, int64_t lda, int64_t rows, int64_t n, const float* d_v,
                 const double* d_row_scale, double* d_y, void* stream) {
   if (lda % 4 || lda < n) return fail(GPIC_E_INVALID, "lda must be >= n and a multiple of 4");
@@ -245,16 +260,41 @@ int gpic_matvec(const float* d_a, int64_t lda, int64_t rows, int64_t n, const fl
   return GPIC_OK;
 }
 
+int64_t gpic_packed_tiles(int64_t n) { return n < 1 ? -1 : packed_tiles(n); }
+
+int64_t gpic_cluster_workspace_bytes(int64_t n, int32_t d, int32_t k, int32_t max_iter,
+                                     int32_t storage) {
+  if (n < 1 || d < 1) return -1;
+  const int64_t scratch = workspace_bytes(n, d, k, n, max_iter);
+  if (storage == GPIC_STORAGE_PACKED)
+    return scratch + packed_tiles(n) * 128 * 128 * 4 + 2 * al(sym_partial_floats(n) * 4);
+  return scratch + n * affinity_pitch(n) * 4;
+}
+
+namespace {
+__global__ void fill_ones_kernel(float* v, int64_t n, int64_t len) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < len) v[i] = i < n ? 1.f : 0.f;
+}
+__global__ void zero_check_kernel(const double* __restrict__ deg, int64_t n, gpic_ctl* ctl) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n && deg[i] <= 0.0) raise_status(ctl, GPIC_E_ZERO_DEGREE, i, -1, deg[i]);
+}
+}  // namespace
+
 int gpic_cluster(const double* d_x, int64_t n, int32_t d, double sigma, int32_t k, double eps,
                  int32_t max_iter, int64_t first_index, const double* h_uniforms, int32_t impl,
-                 int64_t* d_labels, double* d_v, double* d_delta_hist, int32_t* h_iters,
-                 int32_t* h_converged, void* d_work, int64_t work_bytes, void* stream) {
+                 int32_t storage, int64_t* d_labels, double* d_v, double* d_delta_hist,
+                 int32_t* h_iters, int32_t* h_converged, void* d_work, int64_t work_bytes,
+                 void* stream) {
   if (n < 1 || d < 1) return fail(GPIC_E_EMPTY, "dataset must contain at least one point and one feature");
   if (k > n) return fail(GPIC_E_K_TOO_LARGE, "k exceeds the number of points");
+  if (storage == GPIC_STORAGE_PACKED && impl != GPIC_AFFINITY_TC)
+    return fail(GPIC_E_UNSUPPORTED, "packed symmetric storage is built by the tcgen05 engine");
   Workspace ws;
   const int64_t scratch = workspace_bytes(n, d, k, n, max_iter);
-  const int64_t lda = affinity_pitch(n);
-  if (work_bytes < scratch + n * lda * 4) return fail(GPIC_E_INVALID, "workspace too small for the affinity matrix");
+  const int64_t need = gpic_cluster_workspace_bytes(n, d, k, max_iter, storage);
+  if (work_bytes < need) return fail(GPIC_E_INVALID, "workspace too small for the affinity matrix");
   int rc = carve(d_work, scratch, n, d, k, n, max_iter, &ws);
   if (rc) return rc;
   float* a = reinterpret_cast<float*>(static_cast<uint8_t*>(d_work) + scratch);
@@ -264,20 +304,53 @@ int gpic_cluster(const double* d_x, int64_t n, int32_t d, double sigma, int32_t 
   launch_prepare(d_x, n, d, ws.xhi, ws.xlo, ws.sqn, ws.colpart, ws.mean, ws.ctl, s);
   const float neg_scale_log2 = (float)(-1.4426950408889634 / (2.0 * sigma * sigma));
   const int32_t dp = feature_pitch(d);
-  const int64_t rows_pad = round_up(n, kTileM);
-  if (impl == GPIC_AFFINITY_TC) {
-    rc = launch_affinity_tc(ws.xhi, ws.xlo, ws.sqn, n, dp, 0, n, neg_scale_log2, a, lda,
-                            ws.rowpart, rows_pad, s);
+  const int64_t lda = affinity_pitch(n);
+  ShardLoop L;
+  std::memset(&L, 0, sizeof L);
+  if (storage == GPIC_STORAGE_PACKED) {
+    float* rowp = a + packed_tiles(n) * 128 * 128;
+    float* colp = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(rowp) + al(sym_partial_floats(n) * 4));
+    rc = launch_affinity_tc_packed(ws.xhi, ws.xlo, ws.sqn, n, dp, neg_scale_log2, a, s);
     if (rc) return rc;
+    // degrees = A 1 through the same symmetric GEMV (consistent with the stored values)
+    fill_ones_kernel<<<(unsigned)ceil_div(vector_pitch(n), 256), 256, 0, s>>>(ws.v32, n, vector_pitch(n));
+    PeerTable pt;
+    std::memset(&pt, 0, sizeof pt);
+    pt.y[0][0] = pt.y[0][1] = deg;
+    pt.nranks = 1;
+    launch_sym_gemv(a, n, ws.v32, rowp, colp, nullptr, pt, nullptr, s);
+    zero_check_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, s>>>(deg, n, ws.ctl);
+    count_launch(2);
+    L.packed = 1;
+    L.rowp = rowp;
+    L.colp = colp;
   } else {
-    launch_affinity_simt(ws.xhi, ws.xlo, ws.sqn, n, dp, 0, n, neg_scale_log2, a, lda, ws.rowpart,
-                         rows_pad, s);
+    const int64_t rows_pad = round_up(n, kTileM);
+    if (impl == GPIC_AFFINITY_TC) {
+      rc = launch_affinity_tc(ws.xhi, ws.xlo, ws.sqn, n, dp, 0, n, neg_scale_log2, a, lda,
+                              ws.rowpart, rows_pad, s);
+      if (rc) return rc;
+    } else {
+      launch_affinity_simt(ws.xhi, ws.xlo, ws.sqn, n, dp, 0, n, neg_scale_log2, a, lda,
+                           ws.rowpart, rows_pad, s);
+    }
+    launch_degree(ws.rowpart, n, rows_pad, ceil_div(n, kTileN), 0, deg, ws.ctl, s);
   }
-  launch_degree(ws.rowpart, n, rows_pad, ceil_div(n, kTileN), 0, deg, ws.ctl, s);
   launch_tree_sum(deg, n, ws.redpart, ws.redpart + ceil_div(n, kRedBlock), ws.ctl, s);
-  launch_scale_vector(deg, n, ws.redpart + ceil_div(n, kRedBlock), ws.v64, ws.v32, lda, s);
-  rc = run_power_loop(a, lda, deg, n, ws.y, ws.redpart, ws.v64, ws.v32, d_delta_hist, ws.ctl,
-                      max_iter, s);
+  launch_scale_vector(deg, n, ws.redpart + ceil_div(n, kRedBlock), ws.v64, ws.v32,
+                      vector_pitch(n), s);
+  L.a = a;
+  L.lda = lda;
+  L.rows = n;
+  L.deg = deg;
+  L.redpart = ws.redpart;
+  L.v64 = ws.v64;
+  L.v32 = ws.v32;
+  L.hist = d_delta_hist;
+  L.ctl = ws.ctl;
+  L.pt.y[0][0] = L.pt.y[0][1] = ws.y;
+  L.pt.nranks = 1;
+  rc = run_power_loops(&L, 1, n, max_iter, s);
   if (rc) return rc;
   launch_copy_result(ws.v64, n, d_v, ws.ctl, s);
   GPIC_CUDA_TRY(cudaGetLastError());
@@ -299,24 +372,24 @@ int gpic_cluster(const double* d_x, int64_t n, int32_t d, double sigma, int32_t 
 
 int gpic_cluster_host(const double* h_x, int64_t n, int32_t d, double sigma, int32_t k,
                       double eps, int32_t max_iter, int64_t first_index, const double* h_uniforms,
-                      int32_t impl, int64_t* h_labels, double* h_v, double* h_delta_hist,
-                      int32_t* h_iters, int32_t* h_converged, void* d_work, int64_t work_bytes,
-                      void* stream) {
+                      int32_t impl, int32_t storage, int64_t* h_labels, double* h_v,
+                      double* h_delta_hist, int32_t* h_iters, int32_t* h_converged, void* d_work,
+                      int64_t work_bytes, void* stream) {
   if (n < 1 || d < 1) return fail(GPIC_E_EMPTY, "dataset must contain at least one point and one feature");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  // device staging at the tail of the workspace: X, labels, v, deltas
-  const int64_t scratch = workspace_bytes(n, d, k, n, max_iter) + n * affinity_pitch(n) * 4;
+  // device staging after the pipeline workspace: X, labels, v, deltas
+  const int64_t scratch = al(gpic_cluster_workspace_bytes(n, d, k, max_iter, storage));
   const int64_t stage = al(n * d * 8) + al(n * 8) * 2 + al((int64_t)max_iter * 8);
   if (work_bytes < scratch + stage) return fail(GPIC_E_INVALID, "workspace too small (host entry)");
-  uint8_t* p = static_cast<uint8_t*>(d_work) + al(scratch);
+  uint8_t* p = static_cast<uint8_t*>(d_work) + scratch;
   double* dx = reinterpret_cast<double*>(p); p += al(n * d * 8);
   int64_t* dl = reinterpret_cast<int64_t*>(p); p += al(n * 8);
   double* dv = reinterpret_cast<double*>(p); p += al(n * 8);
   double* dh = reinterpret_cast<double*>(p);
   GPIC_CUDA_TRY(cudaMemcpyAsync(dx, h_x, n * d * 8, cudaMemcpyHostToDevice, s));
   int32_t iters = 0, conv = 0;
-  int rc = gpic_cluster(dx, n, d, sigma, k, eps, max_iter, first_index, h_uniforms, impl, dl, dv,
-                        dh, &iters, &conv, d_work, al(scratch), stream);
+  int rc = gpic_cluster(dx, n, d, sigma, k, eps, max_iter, first_index, h_uniforms, impl, storage,
+                        dl, dv, dh, &iters, &conv, d_work, scratch, stream);
   if (rc) return rc;
   GPIC_CUDA_TRY(cudaMemcpyAsync(h_labels, dl, n * 8, cudaMemcpyDeviceToHost, s));
   GPIC_CUDA_TRY(cudaMemcpyAsync(h_v, dv, n * 8, cudaMemcpyDeviceToHost, s));

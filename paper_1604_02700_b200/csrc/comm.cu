@@ -58,7 +58,7 @@ inline uint64_t* r_flags(uint8_t* r, int64_t n) {
   return reinterpret_cast<uint64_t*>(r + 3 * al(n * 8));
 }
 inline int64_t local_bytes(int64_t n) {
-  return al(sizeof(gpic_ctl)) + al(2 * n * 8) + al(affinity_pitch(n) * 4) +
+  return al(sizeof(gpic_ctl)) + al(2 * n * 8) + al(vector_pitch(n) * 4) +
          al((ceil_div(n, kRedBlock) + 1) * 8);
 }
 
@@ -174,7 +174,7 @@ int alloc_locals(gpic_comm* c) {
     c->loc[li].v64 = reinterpret_cast<double*>(p);
     p += al(2 * c->n * 8);
     c->loc[li].v32 = reinterpret_cast<float*>(p);
-    p += al(affinity_pitch(c->n) * 4);
+    p += al(vector_pitch(c->n) * 4);
     c->loc[li].redpart = reinterpret_cast<double*>(p);
   }
   return GPIC_OK;
@@ -313,7 +313,7 @@ int gpic_comm_iterate(gpic_comm* c, const gpic_shard* shards, int32_t nlocal, do
     const double* degf = r_deg(c->region[self], n);
     double* tau = L.redpart + ceil_div(n, kRedBlock);
     launch_tree_sum(degf, n, L.redpart, tau, L.ctl, s);
-    launch_scale_vector(degf, n, tau, L.v64, L.v32, affinity_pitch(n), s);
+    launch_scale_vector(degf, n, tau, L.v64, L.v32, vector_pitch(n), s);
     ShardLoop& S = loops[li];
     std::memset(&S, 0, sizeof S);
     S.a = shards[li].a;

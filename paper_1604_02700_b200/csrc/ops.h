@@ -19,6 +19,15 @@ inline int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }
 int32_t feature_pitch(int32_t d);
 int64_t row_pad(int64_t n);
 int64_t affinity_pitch(int64_t n);
+// fp32 vector copies of v are zero-padded to whole 128-element tiles
+inline int64_t vector_pitch(int64_t n) { return round_up(n, 128); }
+
+// ---- symmetric packed storage (affinity_tc.cu, sym.cu) -------------------
+int64_t packed_tiles(int64_t n);        // nt (nt + 1) / 2, nt = ceil(n / 128)
+int64_t sym_partial_floats(int64_t n);  // packed_tiles(n) * 128
+int launch_affinity_tc_packed(const float* xhi, const float* xlo, const float* sqn, int64_t n,
+                              int32_t dp, float neg_scale_log2, float* a_packed, cudaStream_t s);
+void sym_prepare();
 
 // Workspace carve-up (see capi.cu).
 struct Workspace {
@@ -96,9 +105,16 @@ void launch_iteration_tail(const double* y0, const double* y1, int64_t n, double
 void launch_copy_result(const double* v64, int64_t n, double* out, const gpic_ctl* ctl,
                         cudaStream_t s);
 
+struct PeerTable;
+void launch_sym_gemv(const float* tiles, int64_t n, const float* v32, float* rowp, float* colp,
+                     const double* deg, const PeerTable& pt, gpic_ctl* ctl, cudaStream_t s);
+
 // One shard's loop state (a single-rank run is one shard with nranks = 1).
 struct ShardLoop {
-  const float* a;
+  const float* a;     // dense row block, or the packed tiles when packed
+  int packed;         // 1: symmetric packed tiles (whole matrix, one shard)
+  float* rowp;        // packed: per-tile row / column partials
+  float* colp;
   int64_t lda;
   int64_t rows;
   int64_t row_lo;

@@ -289,6 +289,7 @@ int run_power_loops(ShardLoop* shards, int nlocal, int64_t n, int32_t max_iter, 
     if (e.key == key) hit = &e;
   if (hit == nullptr) {
     gemv_prepare();
+    sym_prepare();
     cudaGraph_t graph;
     GraphEntry ent;
     ent.key = key;
@@ -297,7 +298,10 @@ int run_power_loops(ShardLoop* shards, int nlocal, int64_t n, int32_t max_iter, 
     for (int t = 0; t < max_iter; ++t) {
       for (int i = 0; i < nlocal; ++i) {
         const ShardLoop& L = shards[i];
-        launch_gemv(L.a, L.lda, L.rows, L.row_lo, L.v32, L.deg, L.pt, L.ctl, cs);
+        if (L.packed)
+          launch_sym_gemv(L.a, n, L.v32, L.rowp, L.colp, L.deg, L.pt, L.ctl, cs);
+        else
+          launch_gemv(L.a, L.lda, L.rows, L.row_lo, L.v32, L.deg, L.pt, L.ctl, cs);
       }
       for (int i = 0; i < nlocal; ++i) {
         const ShardLoop& L = shards[i];

@@ -1,0 +1,225 @@
+// Symmetric packed storage: A is exactly symmetric (affinity.py:96-103;
+// test_affinity.py:81-87), so only the upper triangle of 128 x 128 tiles is
+// stored (tile (I, J), J >= I, contiguous 64 KB at tile_index(I, J)). That
+// halves the bytes of the two HBM-bound stages: the affinity store and the
+// per-iteration GEMV read (2n^2 instead of 4n^2 bytes).
+//
+//   sym_gemv_kernel   streams every stored tile once (1-D bulk copies into a
+//                     3-stage smem ring) and produces, per tile, the 128 row
+//                     partials  sum_j T[i][j] v_J[j]   (for y_I) and, off the
+//                     diagonal, the 128 column partials  sum_i T[i][j] v_I[i]
+//                     (for y_J = (T^T v_I)_J). fp32 within a tile.
+//   sym_reduce_kernel y_i = sum over the row's tiles in column order (fp64):
+//                     column partials of tiles (J', R), J' < R, then row
+//                     partials of tiles (R, J), J >= R; / deg_i; stored into
+//                     every rank's y (same epilogue as the dense GEMV).
+// Degrees are the same GEMV with v = 1 (exactly consistent with the stored
+// fp32 values). Every sum has a fixed order, so results are deterministic.
+#include "common.cuh"
+#include "ops.h"
+#include "sm100.cuh"
+
+namespace gpic {
+
+namespace {
+
+constexpr int kTS = 128;
+constexpr int kTileFloats = kTS * kTS;
+constexpr int kStages = 3;
+constexpr int kWarps = 8;                   // consumers; 16 rows each
+constexpr int kRowsPerWarp = kTS / kWarps;  // 16
+constexpr int kThreads = (kWarps + 1) * 32;
+constexpr int kSmem = kStages * kTileFloats * 4 + 2 * kWarps * kTS * 4 + 64 + 128;
+
+__host__ __device__ inline int64_t tile_index(int64_t I, int64_t J, int64_t nt) {
+  return I * nt - I * (I - 1) / 2 + (J - I);
+}
+
+// tile index -> (I, J) by the row prefix P(I) = I*nt - I*(I-1)/2
+__device__ inline void tile_coords(int64_t t, int64_t nt, int64_t& I, int64_t& J) {
+  int64_t lo = 0, hi = nt - 1;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi + 1) >> 1;
+    if (mid * nt - mid * (mid - 1) / 2 <= t) lo = mid; else hi = mid - 1;
+  }
+  I = lo;
+  J = I + (t - (I * nt - I * (I - 1) / 2));
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    sym_gemv_kernel(const float* __restrict__ tiles, int64_t nt, const float* __restrict__ v32,
+                    float* __restrict__ rowp, float* __restrict__ colp,
+                    const gpic_ctl* __restrict__ ctl) {
+  if (ctl != nullptr && *(volatile const int32_t*)&ctl->stop) return;
+  extern __shared__ uint8_t smem_raw[];
+  float* st = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+  float* red = st + kStages * kTileFloats;  // [2][kWarps][128] column partials
+  uint64_t* full = reinterpret_cast<uint64_t*>(red + 2 * kWarps * kTS);
+  uint64_t* empty = full + kStages;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int64_t total = nt * (nt + 1) / 2;
+  const int64_t t0 = total * blockIdx.x / gridDim.x;
+  const int64_t t1 = total * (blockIdx.x + 1) / gridDim.x;
+
+  if (warp == kWarps) {  // producer
+    if (lane != 0) return;
+    int s = 0;
+    uint32_t ph = 0;
+    for (int64_t t = t0; t < t1; ++t) {
+      mbar_wait(&empty[s], ph ^ 1);
+      mbar_expect_tx(&full[s], kTileFloats * 4);
+      bulk_load(st + s * kTileFloats, tiles + t * kTileFloats, kTileFloats * 4, &full[s]);
+      if (++s == kStages) { s = 0; ph ^= 1; }
+    }
+    return;
+  }
+
+  int s = 0;
+  uint32_t ph = 0;
+  int rb = 0;
+  int64_t I = 0, J = 0;
+  if (t0 < t1) tile_coords(t0, nt, I, J);
+  for (int64_t t = t0; t < t1; ++t) {
+    const float4 vj = __ldg(reinterpret_cast<const float4*>(v32 + J * kTS) + lane);
+    const float vi_l = lane < kRowsPerWarp ? __ldg(v32 + I * kTS + warp * kRowsPerWarp + lane) : 0.f;
+    mbar_wait(&full[s], ph);
+    const float* tile = st + s * kTileFloats + warp * kRowsPerWarp * kTS;
+    float acc[kRowsPerWarp];
+    float4 cp = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int i = 0; i < kRowsPerWarp; ++i) {
+      const float4 a = reinterpret_cast<const float4*>(tile + i * kTS)[lane];
+      const float vi = __shfl_sync(0xffffffffu, vi_l, i);
+      float r = a.x * vj.x;
+      r = fmaf(a.y, vj.y, r);
+      r = fmaf(a.z, vj.z, r);
+      acc[i] = fmaf(a.w, vj.w, r);
+      cp.x = fmaf(a.x, vi, cp.x);
+      cp.y = fmaf(a.y, vi, cp.y);
+      cp.z = fmaf(a.z, vi, cp.z);
+      cp.w = fmaf(a.w, vi, cp.w);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+    if (++s == kStages) { s = 0; ph ^= 1; }
+    // transpose-reduce the 16 row partials across the 32 lanes (fixed
+    // pattern): after 4 halving steps lane l holds row f(l) over 16 lanes,
+    // the last xor-1 step completes it.
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const bool up = lane & 16;
+      const float send = up ? acc[k] : acc[k + 8];
+      const float keep = up ? acc[k + 8] : acc[k];
+      acc[k] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const bool up = lane & 8;
+      const float send = up ? acc[k] : acc[k + 4];
+      const float keep = up ? acc[k + 4] : acc[k];
+      acc[k] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+    }
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const bool up = lane & 4;
+      const float send = up ? acc[k] : acc[k + 2];
+      const float keep = up ? acc[k + 2] : acc[k];
+      acc[k] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+    }
+    {
+      const bool up = lane & 2;
+      const float send = up ? acc[0] : acc[1];
+      const float keep = up ? acc[1] : acc[0];
+      acc[0] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+    }
+    acc[0] += __shfl_xor_sync(0xffffffffu, acc[0], 1);
+    const int row = ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 +
+                    ((lane >> 1) & 1);
+    if ((lane & 1) == 0) rowp[t * kTS + warp * kRowsPerWarp + row] = acc[0];
+    // column partials: combine the 8 warps in order
+    float* rw = red + rb * kWarps * kTS;
+    reinterpret_cast<float4*>(rw + warp * kTS)[lane] = cp;
+    asm volatile("bar.sync 1, %0;" ::"n"(kWarps * 32) : "memory");
+    if (I != J && threadIdx.x < kTS) {
+      float c = 0.f;
+#pragma unroll
+      for (int w = 0; w < kWarps; ++w) c += rw[w * kTS + threadIdx.x];
+      colp[t * kTS + threadIdx.x] = c;
+    }
+    rb ^= 1;  // double-buffered: the next tile writes the other half
+    if (++J == nt) { ++I; J = I; }
+  }
+}
+
+__device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__global__ void __launch_bounds__(256)
+    sym_reduce_kernel(const float* __restrict__ rowp, const float* __restrict__ colp, int64_t n,
+                      int64_t nt, const double* __restrict__ deg, const PeerTable pt,
+                      gpic_ctl* ctl) {
+  if (ctl != nullptr && *(volatile const int32_t*)&ctl->stop) return;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) {
+    const int64_t R = i / kTS, o = i % kTS;
+    double s = 0.0;
+    for (int64_t Jp = 0; Jp < R; ++Jp) s += (double)colp[tile_index(Jp, R, nt) * kTS + o];
+    const int64_t base = tile_index(R, R, nt);
+    for (int64_t J = R; J < nt; ++J) s += (double)rowp[(base + (J - R)) * kTS + o];
+    const double val = deg != nullptr ? s / deg[i] : s;
+    const int parity = ctl != nullptr ? (ctl->iter & 1) : 0;
+    for (int p = 0; p < pt.nranks; ++p) pt.y[p][parity][i] = val;
+  }
+  if (pt.flags[0] == nullptr) return;
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned prev = atomicAdd(&ctl->arrive[2], 1u);
+    if (prev == gridDim.x - 1) {
+      ctl->arrive[2] = 0u;
+      __threadfence_system();
+      const uint64_t epoch = ctl->sync_epoch + (uint64_t)ctl->iter + 1;
+      for (int p = 0; p < pt.nranks; ++p) st_release_sys(pt.flags[p] + pt.self, epoch);
+    }
+  }
+}
+
+int g_sms = 0;
+
+}  // namespace
+
+void sym_prepare() {
+  if (g_sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaFuncSetAttribute(sym_gemv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+  }
+}
+
+int64_t sym_partial_floats(int64_t n) {
+  const int64_t nt = ceil_div(n, kTS);
+  return nt * (nt + 1) / 2 * kTS;
+}
+
+void launch_sym_gemv(const float* tiles, int64_t n, const float* v32, float* rowp, float* colp,
+                     const double* deg, const PeerTable& pt, gpic_ctl* ctl, cudaStream_t s) {
+  sym_prepare();
+  const int64_t nt = ceil_div(n, kTS);
+  const int64_t total = nt * (nt + 1) / 2;
+  const int grid = (int)(total < g_sms ? total : g_sms);
+  sym_gemv_kernel<<<grid, kThreads, kSmem, s>>>(tiles, nt, v32, rowp, colp, ctl);
+  sym_reduce_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, s>>>(rowp, colp, n, nt, deg, pt, ctl);
+  count_launch(2);
+}
+
+}  // namespace gpic

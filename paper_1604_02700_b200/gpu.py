@@ -210,13 +210,20 @@ class PreparedPoints:
     device: object
 
 
-def prepare_points(d: DataSet, dev) -> PreparedPoints:
-    """Upload X (fp64), scan for non-finite entries, centre, cast and split."""
+def prepare_points(d, dev) -> PreparedPoints:
+    """Upload X (fp64), scan for non-finite entries, centre, cast and split.
+
+    ``d`` is a DataSet (host points, uploaded here) or an (n, m) float64
+    CUDA tensor already resident on ``dev``.
+    """
     torch = _torch()
     L = _lib.lib()
-    n, m = d.points.shape
+    if isinstance(d, DataSet):
+        x = torch.from_numpy(d.points).to(dev, non_blocking=True)
+    else:
+        x = d.to(device=dev, dtype=torch.float64).contiguous()
+    n, m = x.shape
     st = _stream(dev)
-    x = torch.from_numpy(d.points).to(dev, non_blocking=True)
     dp = int(L.gpic_feature_pitch(m))
     npad = int(L.gpic_row_pad(n))
     xhi = torch.empty((npad, dp), dtype=torch.float32, device=dev)
@@ -439,11 +446,9 @@ def kmeans_1d(values, params: KMeansParams, config: KernelConfig | None = None):
 
 
 # ------------------------------------------------------------- pipeline
-def workspace_bytes(n: int, d: int, k: int, max_iter: int) -> int:
-    """Device bytes one cluster() call needs: scratch + the n x pitch fp32 A."""
-    L = _lib.lib()
-    scratch = int(L.gpic_workspace_bytes(n, d, k, n, max_iter))
-    return scratch + n * int(L.gpic_affinity_pitch(n)) * 4
+def workspace_bytes(n: int, d: int, k: int, max_iter: int, storage: int = 1) -> int:
+    """Device bytes one cluster() call needs: scratch + the fp32 affinity storage."""
+    return int(_lib.lib().gpic_cluster_workspace_bytes(n, d, k, max_iter, storage))
 
 
 def cluster(d: DataSet, kind, params: PicParams, config: KernelConfig | None = None, seed: int = 0):
@@ -476,8 +481,9 @@ def cluster(d: DataSet, kind, params: PicParams, config: KernelConfig | None = N
     eps = params.resolved_epsilon(n)
     T = params.max_iterations
     impl = _lib.AFFINITY_TC if config.affinity_impl == "tc" else _lib.AFFINITY_SIMT
+    storage = config.storage_code()
     x = torch.from_numpy(d.points).to(dev, non_blocking=True)
-    nbytes = workspace_bytes(n, m, k, T)
+    nbytes = workspace_bytes(n, m, k, T, storage)
     work = torch.empty(nbytes, dtype=torch.uint8, device=dev)
     labels = torch.empty(n, dtype=torch.int64, device=dev)
     v = torch.empty(n, dtype=torch.float64, device=dev)
@@ -486,8 +492,8 @@ def cluster(d: DataSet, kind, params: PicParams, config: KernelConfig | None = N
     iters = C.c_int32(0)
     conv = C.c_int32(0)
     rc = L.gpic_cluster(_ptr(x), n, m, sigma, k, eps, T, first, u.ctypes.data_as(C.c_void_p),
-                        impl, _ptr(labels), _ptr(v), _ptr(hist), C.byref(iters), C.byref(conv),
-                        _ptr(work), nbytes, _stream(dev))
+                        impl, storage, _ptr(labels), _ptr(v), _ptr(hist), C.byref(iters),
+                        C.byref(conv), _ptr(work), nbytes, _stream(dev))
     if rc != _lib.GPIC_OK:
         h = _lib.Ctl()
         if L.gpic_ctl_read(_ptr(work), C.byref(h), _stream(dev)) == 0 and h.status == rc:

@@ -85,6 +85,7 @@ class KMeansParams:
 DEFAULT_MEMORY_BUDGET = 256 * 1024 * 1024
 
 AFFINITY_IMPLS = ("tc", "simt")
+STORAGES = ("packed", "dense")
 
 
 @dataclass(frozen=True)
@@ -100,6 +101,10 @@ class KernelConfig:
     keep their reference meaning for the host port; the GPU builds whole
     row shards in one launch. ``affinity_impl`` picks the Gram engine:
     "tc" (tcgen05 3xTF32, default) or "simt" (FP32 FFMA, the comparator).
+    ``storage`` = "packed" keeps only the upper triangle of 128x128 tiles
+    of the (exactly symmetric) affinity matrix — half the HBM bytes of the
+    affinity store and of every power iteration; "dense" keeps full rows
+    (used by the SIMT engine and by row-sharded multi-rank runs).
     """
 
     p: int = 1
@@ -108,6 +113,7 @@ class KernelConfig:
     affinity_impl: str = "tc"
     virtual_ranks: bool = False
     device: int | None = None
+    storage: str = "packed"
 
     def __post_init__(self) -> None:
         if self.p < 1:
@@ -118,6 +124,14 @@ class KernelConfig:
             raise InvalidSpec("memory budget must be positive")
         if self.affinity_impl not in AFFINITY_IMPLS:
             raise InvalidSpec(f"affinity_impl must be one of {AFFINITY_IMPLS}")
+        if self.storage not in STORAGES:
+            raise InvalidSpec(f"storage must be one of {STORAGES}")
+
+    def storage_code(self) -> int:
+        """Packed symmetric tiles need the tcgen05 engine and a single rank."""
+        if self.storage == "packed" and self.affinity_impl == "tc" and self.p == 1:
+            return 1
+        return 0
 
     def resolved_chunk_rows(self, n: int) -> int:
         if self.chunk_rows is not None:

@@ -93,62 +93,90 @@ class Comm:
         self.close()
 
 
+class ShardedRunner:
+    """The sharded pipeline for a fixed (n, P): exchange buffers live across runs.
+
+    ``run(dataset_or_device_points, sigma, params, seed)`` returns device
+    tensors (labels, v) and the PicTrace; the comm (CUDA-IPC mappings of the
+    peers' exchange buffers) is set up once in the constructor, outside any
+    timed region.
+    """
+
+    def __init__(self, n: int, config):
+        from . import gpu
+
+        self.gpu = gpu
+        self.n = n
+        self.config = config
+        P = config.p
+        self.ranges = shard_ranges(n, P)
+        if config.virtual_ranks:
+            self.locals = list(range(P))
+            self.rank = 0
+        else:
+            self.rank, world = dist_context()
+            if world != P:
+                raise InvalidSpec(
+                    f"KernelConfig(p={P}) without virtual_ranks needs a torch.distributed job of "
+                    f"{P} ranks (one per GPU); world size is {world}"
+                )
+            self.locals = [self.rank]
+        self.dev = gpu._device(config)
+        self.comm = Comm(n, P, config.virtual_ranks, self.rank)
+
+    def close(self):
+        self.comm.close()
+
+    def run(self, points, sigma: float, params, seed: int = 0):
+        gpu = self.gpu
+        torch = gpu._torch()
+        n, dev, cfg = self.n, self.dev, self.config
+        st = gpu._stream(dev)
+        prep = gpu.prepare_points(points, dev)
+        blocks = [gpu.affinity_rows(prep, *self.ranges[r], sigma, cfg.affinity_impl)
+                  for r in self.locals]
+        nl = len(self.locals)
+        shards = (_lib.Shard * nl)()
+        for i, (r, blk) in enumerate(zip(self.locals, blocks)):
+            lo, hi = self.ranges[r]
+            shards[i] = _lib.Shard(blk.a.data_ptr(), blk.lda, blk.deg.data_ptr(), lo, hi - lo)
+        T = params.max_iterations
+        eps = params.resolved_epsilon(n)
+        hist = torch.zeros(nl * T, dtype=torch.float64, device=dev)
+        vout = torch.empty(nl * n, dtype=torch.float64, device=dev)
+        ctls = (_lib.Ctl * nl)()
+        L = self.comm.L
+        rc = L.gpic_comm_gather_degrees(self.comm.ptr, shards, nl, None, st)
+        if rc == _lib.GPIC_E_ZERO_DEGREE:
+            raise ZeroDegree(int(_lib.last_error().split()[1]))
+        _lib.check(rc)
+        rc = L.gpic_comm_iterate(self.comm.ptr, shards, nl, eps, T, gpu._ptr(hist),
+                                 gpu._ptr(vout), ctls, st)
+        if rc != _lib.GPIC_OK:
+            bad = next((c for c in ctls if c.status != _lib.GPIC_OK), None)
+            _lib.raise_for(rc, bad)
+        # every shard holds the same embedding; local shard 0 speaks for the rank
+        h = ctls[0]
+        for c in ctls[1:]:
+            if c.iter != h.iter or c.converged != h.converged:
+                raise DeviceError("ranks disagree on the stop decision")
+        v = vout[:n]
+        labels = gpu.kmeans_1d(v, KMeansParams(k=params.k, seed=seed), cfg)
+        it = int(h.iter)
+        return labels, v, PicTrace(it, hist[:it].cpu().numpy(), bool(h.converged))
+
+
 def cluster(d, kind, params, config, seed):
     """Sharded counterpart of gpu.cluster (same return contract)."""
     from . import gpu
 
-    torch = gpu._torch()
     sigma = gpu._check_kind(kind)
-    n = d.n
-    P = config.p
-    ranges = shard_ranges(n, P)
-    if config.virtual_ranks:
-        locals_ = list(range(P))
-        rank = 0
-    else:
-        rank, world = dist_context()
-        if world != P:
-            raise InvalidSpec(
-                f"KernelConfig(p={P}) without virtual_ranks needs a torch.distributed job of "
-                f"{P} ranks (one per GPU); world size is {world}"
-            )
-        locals_ = [rank]
-    dev = gpu._device(config)
-    st = gpu._stream(dev)
-    prep = gpu.prepare_points(d, dev)
-    blocks = [gpu.affinity_rows(prep, *ranges[r], sigma, config.affinity_impl) for r in locals_]
-    shards = (_lib.Shard * len(locals_))()
-    for i, (r, blk) in enumerate(zip(locals_, blocks)):
-        shards[i] = _lib.Shard(blk.a.data_ptr(), blk.lda, blk.deg.data_ptr(), ranges[r][0],
-                               ranges[r][1] - ranges[r][0])
-    T = params.max_iterations
-    eps = params.resolved_epsilon(n)
-    nl = len(locals_)
-    hist = torch.zeros(nl * T, dtype=torch.float64, device=dev)
-    vout = torch.empty(nl * n, dtype=torch.float64, device=dev)
-    ctls = (_lib.Ctl * nl)()
-    with Comm(n, P, config.virtual_ranks, rank) as comm:
-        L = comm.L
-        rc = L.gpic_comm_gather_degrees(comm.ptr, shards, nl, None, st)
-        if rc == _lib.GPIC_E_ZERO_DEGREE:
-            msg = _lib.last_error()
-            raise ZeroDegree(int(msg.split()[1]))
-        _lib.check(rc)
-        rc = L.gpic_comm_iterate(comm.ptr, shards, nl, eps, T, gpu._ptr(hist), gpu._ptr(vout),
-                                 ctls, st)
-        if rc != _lib.GPIC_OK:
-            bad = next((c for c in ctls if c.status != _lib.GPIC_OK), None)
-            _lib.raise_for(rc, bad)
-    # every shard holds the same embedding; local shard 0 speaks for the rank
-    h = ctls[0]
-    for c in ctls[1:]:
-        if c.iter != h.iter or c.converged != h.converged:
-            raise DeviceError("ranks disagree on the stop decision")
-    v = vout[:n]
-    labels = gpu.kmeans_1d(v, KMeansParams(k=params.k, seed=seed), config)
-    it = int(h.iter)
-    trace = PicTrace(it, hist[:it].cpu().numpy(), bool(h.converged))
-    return labels.cpu().numpy(), v.cpu().numpy(), trace
+    runner = ShardedRunner(d.n, config)
+    try:
+        labels, v, trace = runner.run(d, sigma, params, seed)
+        return labels.cpu().numpy(), v.cpu().numpy(), trace
+    finally:
+        runner.close()
 
 
 def all_ranks_agree(labels: np.ndarray, v: np.ndarray) -> bool:

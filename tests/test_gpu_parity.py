@@ -287,3 +287,53 @@ def test_config2_scale_parity():
     ref, _, _ = po.power_iteration(w, po.start_vector(deg), TINY_EPS, 3)
     _, v3, _ = cluster(d, GaussianRbf(sigma), PicParams(k=5, epsilon=TINY_EPS, max_iterations=3))
     assert rel_l1(v3, ref) <= 1e-4
+
+
+@pytest.mark.parametrize("case", ["config1", "gblobs_small", "gblobs_balanced"])
+def test_packed_and_dense_storage_agree(golden, case):
+    z = golden(case)
+    d = DataSet(_points(z))
+    kind, params = GaussianRbf(float(z["sigma"])), PicParams(k=int(z["k"]))
+    lp, vp, tp = cluster(d, kind, params, config=KernelConfig(storage="packed"), seed=int(z["seed"]))
+    ld, vd, td = cluster(d, kind, params, config=KernelConfig(storage="dense"), seed=int(z["seed"]))
+    assert np.array_equal(lp, ld) and np.array_equal(lp, z["labels"])
+    assert rel_l1(vp, vd) <= 1e-5
+    assert rel_l1(vp, z["v"]) <= 1e-4
+
+
+def test_sym_matvec_against_numpy():
+    """Packed-tile GEMV (row + column partials) equals the dense product."""
+    import ctypes as C
+
+    import torch
+
+    from paper_1604_02700_b200 import _lib
+
+    L = _lib.lib()
+    rng = np.random.default_rng(5)
+    for n in (1, 127, 128, 300, 1000):
+        a = rng.uniform(0, 1, (n, n))
+        a = (a + a.T) / 2
+        nt = -(-n // 128)
+        full = np.zeros((nt * 128, nt * 128), dtype=np.float32)
+        full[:n, :n] = a
+        tiles = []
+        for i in range(nt):
+            for j in range(i, nt):
+                tiles.append(full[i * 128:(i + 1) * 128, j * 128:(j + 1) * 128])
+        assert len(tiles) == L.gpic_packed_tiles(n)
+        dev = torch.device("cuda")
+        t_dev = torch.from_numpy(np.stack(tiles)).to(dev)
+        v = rng.uniform(0, 1, n)
+        v32 = torch.zeros(int(L.gpic_vector_pitch(n)), dtype=torch.float32, device=dev)
+        v32[:n] = torch.from_numpy(v.astype(np.float32)).to(dev)
+        rowp = torch.empty(len(tiles) * 128, dtype=torch.float32, device=dev)
+        colp = torch.empty_like(rowp)
+        y = torch.empty(n, dtype=torch.float64, device=dev)
+        rc = L.gpic_sym_matvec(C.c_void_p(t_dev.data_ptr()), n, C.c_void_p(v32.data_ptr()),
+                               C.c_void_p(rowp.data_ptr()), C.c_void_p(colp.data_ptr()), None,
+                               C.c_void_p(y.data_ptr()),
+                               C.c_void_p(torch.cuda.current_stream().cuda_stream))
+        assert rc == 0
+        ref = a.astype(np.float32).astype(np.float64) @ v.astype(np.float32).astype(np.float64)
+        assert np.max(np.abs(y.cpu().numpy() - ref) / np.abs(ref)) <= 1e-5, n
