@@ -29,7 +29,7 @@ def main():
     labels, v, trace = cluster(d, kind, params, config=KernelConfig(p=world, device=dev), seed=2)
     agree = sharded.all_ranks_agree(labels, v)
     if rank == 0:
-        single = cluster(d, kind, params, config=KernelConfig(device=dev), seed=2)
+        single = cluster(d, kind, params, config=KernelConfig(device=dev, storage="dense"), seed=2)
         same = (np.array_equal(single[0], labels) and np.array_equal(single[1], v)
                 and np.array_equal(single[2].delta_history, trace.delta_history))
         print("RANKS_AGREE", agree, flush=True)

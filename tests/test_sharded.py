@@ -92,7 +92,9 @@ def test_malformed_handle_rejected():
 def test_virtual_ranks_bitwise_invariant(engine):
     d = gaussian_blobs(3000, 32, 5, seed=2)
     kind, params = GaussianRbf(float(np.sqrt(32) / 2)), PicParams(k=5)
-    base = cluster(d, kind, params, config=KernelConfig(affinity_impl=engine), seed=1)
+    # ranks hold dense row shards: the single-rank reference is dense too
+    base = cluster(d, kind, params, config=KernelConfig(affinity_impl=engine, storage="dense"),
+                   seed=1)
     for p in (2, 3, 4, 8):
         got = cluster(d, kind, params, seed=1,
                       config=KernelConfig(p=p, virtual_ranks=True, affinity_impl=engine))
@@ -107,7 +109,7 @@ def test_virtual_ranks_forced_iterations_and_repeat():
     d = gaussian_blobs(2048, 16, 4, seed=3)
     kind = GaussianRbf(2.0)
     params = PicParams(k=4, epsilon=5e-324, max_iterations=9)
-    base = cluster(d, kind, params)
+    base = cluster(d, kind, params, config=KernelConfig(storage="dense"))
     cfg = KernelConfig(p=4, virtual_ranks=True)
     a = cluster(d, kind, params, config=cfg)
     b = cluster(d, kind, params, config=cfg)   # second run: epochs keep increasing
