@@ -170,6 +170,10 @@ int64_t gpic_vector_pitch(int64_t n);
  * (tcgen05 engine only). */
 #define GPIC_STORAGE_DENSE 0
 #define GPIC_STORAGE_PACKED 1
+/* matrix-free (n^2 beyond HBM): A is never stored; every A v is
+ * recomputed from X by the tcgen05 engine with the multiply-by-v fused into
+ * the exp epilogue (compute-bound instead of HBM-bound). */
+#define GPIC_STORAGE_NONE 2
 int64_t gpic_packed_tiles(int64_t n);
 int64_t gpic_cluster_workspace_bytes(int64_t n, int32_t d, int32_t k, int32_t max_iter,
                                      int32_t storage);
@@ -231,7 +235,24 @@ typedef struct gpic_shard {
   const double* deg;  /* rows degrees                                       */
   int64_t row_lo;
   int64_t rows;
+  /* matrix-free shards (storage == GPIC_STORAGE_NONE): a is unused and the
+   * rows are recomputed from the prepared points every iteration */
+  int32_t storage;
+  int32_t d;
+  const float* xhi;
+  const float* xlo;
+  const float* sqn;
+  double sigma;
+  double* ypart;      /* gpic_mf_ypart_doubles(n, d, rows) doubles          */
 } gpic_shard;
+
+/* Matrix-free degrees of rows [row_lo, row_hi): deg = A 1 recomputed from the
+ * prepared points (gpic_prepare_points). d_ones: gpic_vector_pitch(n) floats
+ * of scratch; d_ypart: gpic_mf_ypart_doubles(n, d, rows) doubles. */
+int64_t gpic_mf_ypart_doubles(int64_t n, int32_t d, int64_t rows);
+int gpic_mf_degrees(const float* d_xhi, const float* d_xlo, const float* d_sqn, int64_t n,
+                    int32_t d, int64_t row_lo, int64_t row_hi, double sigma, float* d_ones,
+                    double* d_ypart, double* d_deg, void* stream);
 
 int gpic_comm_create(int32_t nranks, int32_t rank, int64_t n, gpic_comm** out,
                      uint8_t* h_ipc_handle);

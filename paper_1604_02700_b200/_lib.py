@@ -29,6 +29,7 @@ AFFINITY_SIMT = 1
 
 STORAGE_DENSE = 0
 STORAGE_PACKED = 1
+STORAGE_NONE = 2
 
 
 class Ctl(C.Structure):
@@ -80,6 +81,8 @@ SIGNATURES = {
     "gpic_matvec": (C.c_int, [P, I64, I64, I64, P, P, P, P]),
     "gpic_packed_tiles": (I64, [I64]),
     "gpic_vector_pitch": (I64, [I64]),
+    "gpic_mf_ypart_doubles": (I64, [I64, I32, I64]),
+    "gpic_mf_degrees": (C.c_int, [P, P, P, I64, I32, I64, I64, F64, P, P, P, P]),
     "gpic_sym_matvec": (C.c_int, [P, I64, P, P, P, P, P, P]),
     "gpic_cluster_workspace_bytes": (I64, [I64, I32, I32, I32, I32]),
     "gpic_cluster": (C.c_int, [P, I64, I32, F64, I32, F64, I32, I64, P, I32, I32, P, P, P, P, P,
@@ -104,7 +107,9 @@ class Shard(C.Structure):
     """Mirror of struct gpic_shard."""
 
     _fields_ = [("a", C.c_void_p), ("lda", C.c_int64), ("deg", C.c_void_p),
-                ("row_lo", C.c_int64), ("rows", C.c_int64)]
+                ("row_lo", C.c_int64), ("rows", C.c_int64), ("storage", C.c_int32),
+                ("d", C.c_int32), ("xhi", C.c_void_p), ("xlo", C.c_void_p), ("sqn", C.c_void_p),
+                ("sigma", C.c_double), ("ypart", C.c_void_p)]
 
 _lib = None
 

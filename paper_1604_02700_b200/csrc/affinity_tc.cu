@@ -1,11 +1,21 @@
-// Stage 1 (tensor-core engine): affinity row block on tcgen05 with a fused
-// exp / diagonal / row-sum epilogue.
+// Stage 1 (tensor-core engine): affinity tiles on tcgen05 with a fused
+// exp / diagonal / row-sum epilogue, in three output modes.
 //
 //   G = Xc_I Xc_J^T via 3xTF32: G ~= hi_I.lo_J + lo_I.hi_J + hi_I.hi_J, where
 //   xc = hi + lo exactly (hi = TF32(xc), prepare.cu), each term a
 //   tcgen05.mma.kind::tf32 (M=128, N=128, K=8) accumulating in TMEM (fp32).
 //   a_ij = exp2(min(ns*(|x_i|^2 + |x_j|^2 - 2 G_ij), 0)),  ns = -log2(e)/(2 sigma^2)
-//   a_ii = 0, a_ij = 0 for padding columns                  (affinity.py:96-103)
+//   a_ii = 0, a_ij = 0 for padding rows / columns          (affinity.py:96-103)
+//
+// Modes (epilogue):
+//   dense   store rows [row_lo, row_hi) x all columns, fp32 pitch lda, plus
+//           fp32 row partials per 128-column tile for the degree combine
+//   packed  store only tiles J >= I of the (exactly symmetric) matrix, each
+//           128x128 tile contiguous (sym.cu streams them)
+//   matvec  matrix-free: nothing is stored; each element is
+//           multiplied by v_j in registers and row sums are accumulated per
+//           32-tile column chunk (fp64) -> ypart; A v is recomputed every
+//           iteration when n^2 does not fit HBM
 //
 // Persistent warp-specialised kernel, one CTA per SM (320 threads):
 //   warp 0      TMA producer: the CTA's row block (MB x 128 rows, hi + lo,
@@ -17,13 +27,8 @@
 //               M block into one of two TMEM accumulators (double buffer,
 //               so the next tile's MMAs overlap this tile's epilogue).
 //   warps 2-9   epilogue: tcgen05.ld 32 columns at a time, exp2 + masks +
-//               row sums in registers, swizzled st.shared, TMA bulk-tensor
-//               store of 32x32 fp32 boxes (the kernel is bound by this
-//               4n^2-byte store stream), fp32 row partials per 128-column
-//               tile for the fixed-order degree combine (degree_kernel).
-//
-// The row block stays resident, so operand traffic per output byte is
-// 2*d/(128*MB) for B only (0.5x at d=64, MB=2).
+//               row sums in registers; store modes go through swizzled
+//               st.shared and TMA bulk-tensor stores of 32x32 fp32 boxes.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -35,6 +40,8 @@ namespace gpic {
 
 namespace {
 
+enum { kModeDense = 0, kModePacked = 1, kModeMatvec = 2 };
+
 constexpr int kBN = 128;           // columns per tile (one MMA N)
 constexpr int kKBlk = 32;          // fp32 per 128-byte swizzle row
 constexpr int kTileBytes = 128 * kKBlk * 4;  // 16 KB: 128 rows x 32 fp32
@@ -42,19 +49,24 @@ constexpr int kEpiWarps = 8;
 constexpr int kThreads = 64 + kEpiWarps * 32;
 constexpr int kStageOutBytes = 32 * 128;     // 32 rows x 32 fp32 per epilogue warp
 constexpr int kSmemBudget = 224 * 1024;
+constexpr int kChunkTiles = 32;              // matvec: column tiles per work item
 
 __host__ __device__ constexpr int mblocks(int KB) { return KB <= 2 ? 2 : 1; }
 __host__ __device__ constexpr int a_bytes(int KB) { return 2 * mblocks(KB) * KB * kTileBytes; }
 // output staging buffers per epilogue warp (double-buffered where smem allows)
-__host__ __device__ constexpr int out_bufs(int KB) { return (KB == 1 || KB == 3) ? 2 : 1; }
-__host__ __device__ constexpr int out_bytes(int KB) { return kEpiWarps * out_bufs(KB) * kStageOutBytes; }
-__host__ __device__ constexpr int stages(int KB) {
-  return (kSmemBudget - a_bytes(KB) - out_bytes(KB)) / (2 * kTileBytes) > 4
-             ? 4
-             : (kSmemBudget - a_bytes(KB) - out_bytes(KB)) / (2 * kTileBytes);
+__host__ __device__ constexpr int out_bufs(int KB, int MODE) {
+  return MODE == kModeMatvec ? 0 : ((KB == 1 || KB == 3) ? 2 : 1);
 }
-__host__ __device__ constexpr int smem_bytes(int KB) {
-  return a_bytes(KB) + stages(KB) * 2 * kTileBytes + out_bytes(KB) + 256 + 1024;
+__host__ __device__ constexpr int out_bytes(int KB, int MODE) {
+  return kEpiWarps * out_bufs(KB, MODE) * kStageOutBytes;
+}
+__host__ __device__ constexpr int stages(int KB, int MODE) {
+  return (kSmemBudget - a_bytes(KB) - out_bytes(KB, MODE)) / (2 * kTileBytes) > 4
+             ? 4
+             : (kSmemBudget - a_bytes(KB) - out_bytes(KB, MODE)) / (2 * kTileBytes);
+}
+__host__ __device__ constexpr int smem_bytes(int KB, int MODE) {
+  return a_bytes(KB) + stages(KB, MODE) * 2 * kTileBytes + out_bytes(KB, MODE) + 256 + 1024;
 }
 
 constexpr uint32_t kIdesc = idesc_tf32(128, kBN);
@@ -65,33 +77,15 @@ struct TcArgs {
   int64_t row_lo;
   int64_t rows;
   float ns;  // -log2(e) / (2 sigma^2)
-  float* rowpart;
+  float* rowpart;    // dense: [n_ctiles][rows_pad] fp32 row partials
   int64_t rows_pad;
   int64_t n_rtiles;  // row blocks of 128*MB rows
   int64_t n_ctiles;  // column tiles of 128
-  int packed;        // 1: symmetric packed output (tiles J >= I only, no row partials)
+  const float* v32;  // matvec: vector_pitch(n) floats
+  double* ypart;     // matvec: [n_chunks * parts][rows_pad] fp64 row partials
+  int64_t n_chunks;  // matvec: column chunks (kChunkTiles tiles) per row block
+  const gpic_ctl* ctl;  // matvec in a loop: exit at once when ctl->stop is set
 };
-
-// Work item t -> (row block, column tile). Dense: all column tiles of every
-// row block. Packed (symmetric): column tiles cb >= rb*MB only, so the
-// upper triangle of 128x128 tiles is computed once.
-template <int MB>
-__device__ __forceinline__ void decode(int64_t t, const TcArgs& a, int64_t& rb, int64_t& cb) {
-  if (!a.packed) {
-    rb = t / a.n_ctiles;
-    cb = t % a.n_ctiles;
-    return;
-  }
-  // S(r) = r*NC - MB*r*(r-1)/2 items precede row block r
-  int64_t lo = 0, hi = a.n_rtiles - 1;
-  while (lo < hi) {
-    const int64_t mid = (lo + hi + 1) >> 1;
-    const int64_t s = mid * a.n_ctiles - (int64_t)MB * mid * (mid - 1) / 2;
-    if (s <= t) lo = mid; else hi = mid - 1;
-  }
-  rb = lo;
-  cb = rb * MB + (t - (lo * a.n_ctiles - (int64_t)MB * lo * (lo - 1) / 2));
-}
 
 __host__ __device__ inline int64_t packed_items(int64_t nrt, int64_t nct, int mb) {
   return nrt * nct - (int64_t)mb * nrt * (nrt - 1) / 2;
@@ -102,21 +96,78 @@ __host__ __device__ inline int64_t tile_index(int64_t I, int64_t J, int64_t nt) 
   return I * nt - I * (I - 1) / 2 + (J - I);
 }
 
-template <int KB>
+// Work sequence of one CTA, identical for all three roles.
+//   dense / packed: units are tiles (rb, cb); packed keeps cb >= rb*MB only
+//   matvec: units are items (rb, chunk) of up to kChunkTiles column tiles, so
+//           a chunk's row partial is always produced by one CTA (fixed shape)
+template <int MB, int MODE>
+struct Cursor {
+  int64_t u, u_end;    // unit counter
+  int64_t rb, cb;      // current tile
+  int64_t cb_end;      // matvec: end of the current item's columns
+  int64_t chunk;       // matvec: chunk index of the current item
+
+  __device__ void decode_unit(const TcArgs& a) {
+    if (MODE == kModeDense) {
+      rb = u / a.n_ctiles;
+      cb = u % a.n_ctiles;
+    } else if (MODE == kModePacked) {
+      int64_t lo = 0, hi = a.n_rtiles - 1;
+      while (lo < hi) {
+        const int64_t mid = (lo + hi + 1) >> 1;
+        const int64_t s = mid * a.n_ctiles - (int64_t)MB * mid * (mid - 1) / 2;
+        if (s <= u) lo = mid; else hi = mid - 1;
+      }
+      rb = lo;
+      cb = rb * MB + (u - (lo * a.n_ctiles - (int64_t)MB * lo * (lo - 1) / 2));
+    } else {
+      rb = u / a.n_chunks;
+      chunk = u % a.n_chunks;
+      cb = chunk * kChunkTiles;
+      cb_end = min(cb + kChunkTiles, a.n_ctiles);
+    }
+  }
+  __device__ void begin(const TcArgs& a, int64_t u0, int64_t u1) {
+    u = u0;
+    u_end = u1;
+    if (u < u_end) decode_unit(a);
+  }
+  __device__ bool valid() const { return u < u_end; }
+  __device__ bool item_last() const { return MODE != kModeMatvec || cb + 1 == cb_end; }
+  __device__ void next(const TcArgs& a) {
+    if (MODE == kModeMatvec && cb + 1 < cb_end) {
+      ++cb;
+      return;
+    }
+    ++u;
+    if (u < u_end) decode_unit(a);
+  }
+};
+
+template <int MB, int MODE>
+__host__ __device__ inline int64_t total_units(const TcArgs& a) {
+  if (MODE == kModePacked) return packed_items(a.n_rtiles, a.n_ctiles, MB);
+  if (MODE == kModeMatvec) return a.n_rtiles * a.n_chunks;
+  return a.n_rtiles * a.n_ctiles;
+}
+
+template <int KB, int MODE>
 __global__ void __launch_bounds__(kThreads, 1)
     affinity_tc_kernel(const __grid_constant__ CUtensorMap map_hi,
                        const __grid_constant__ CUtensorMap map_lo,
                        const __grid_constant__ CUtensorMap map_out, const TcArgs args) {
   constexpr int MB = mblocks(KB);
-  constexpr int ST = stages(KB);
+  constexpr int ST = stages(KB, MODE);
   constexpr int kTmemCols = 2 * MB * kBN;  // 2 accumulators
+  if (MODE == kModeMatvec && args.ctl != nullptr && *(volatile const int32_t*)&args.ctl->stop)
+    return;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   uint8_t* sA = base;                                     // [hl][m][kb] 16 KB tiles
   uint8_t* sB = sA + a_bytes(KB);                         // [stage][hl] 16 KB tiles
-  uint8_t* sOut = sB + ST * 2 * kTileBytes;               // [epi warp] 4 KB
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sOut + out_bytes(KB));
+  uint8_t* sOut = sB + ST * 2 * kTileBytes;               // [epi warp][buf] 4 KB
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sOut + out_bytes(KB, MODE));
   uint64_t* full = bars;                 // [ST]
   uint64_t* empty = bars + ST;           // [ST]
   uint64_t* a_full = bars + 2 * ST;
@@ -127,10 +178,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int64_t total = args.packed ? packed_items(args.n_rtiles, args.n_ctiles, MB)
-                                    : args.n_rtiles * args.n_ctiles;
-  const int64_t t_begin = total * blockIdx.x / gridDim.x;
-  const int64_t t_end = total * (blockIdx.x + 1) / gridDim.x;
+  const int64_t total = total_units<MB, MODE>(args);
+  const int64_t u_begin = total * blockIdx.x / gridDim.x;
+  const int64_t u_end = total * (blockIdx.x + 1) / gridDim.x;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < ST; ++s) {
@@ -146,7 +196,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_hi)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_lo)) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_out)) : "memory");
+    if (MODE != kModeMatvec)
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_out)) : "memory");
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
@@ -167,10 +218,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t a_par = 1;
       int s = 0;
       uint32_t ph = 0;
-      for (int64_t t = t_begin; t < t_end; ++t) {
-        int64_t rb, cb;
-        decode<MB>(t, args, rb, cb);
-        if (rb != cur_rb) {
+      Cursor<MB, MODE> c;
+      for (c.begin(args, u_begin, u_end); c.valid(); c.next(args)) {
+        if (c.rb != cur_rb) {
           mbar_wait(a_empty, a_par);
           a_par ^= 1;
           mbar_expect_tx(a_full, a_bytes(KB));
@@ -178,14 +228,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int m = 0; m < MB; ++m)
               for (int kb = 0; kb < KB; ++kb)
                 tma_load_2d(sA + ((hl * MB + m) * KB + kb) * kTileBytes, hl ? &map_lo : &map_hi,
-                            kb * kKBlk, (int)(args.row_lo + (rb * MB + m) * 128), a_full);
-          cur_rb = rb;
+                            kb * kKBlk, (int)(args.row_lo + (c.rb * MB + m) * 128), a_full);
+          cur_rb = c.rb;
         }
         for (int kb = 0; kb < KB; ++kb) {
           mbar_wait(&empty[s], ph ^ 1);
           mbar_expect_tx(&full[s], 2 * kTileBytes);
-          tma_load_2d(sB + (s * 2 + 0) * kTileBytes, &map_hi, kb * kKBlk, (int)(cb * kBN), &full[s]);
-          tma_load_2d(sB + (s * 2 + 1) * kTileBytes, &map_lo, kb * kKBlk, (int)(cb * kBN), &full[s]);
+          tma_load_2d(sB + (s * 2 + 0) * kTileBytes, &map_hi, kb * kKBlk, (int)(c.cb * kBN), &full[s]);
+          tma_load_2d(sB + (s * 2 + 1) * kTileBytes, &map_lo, kb * kKBlk, (int)(c.cb * kBN), &full[s]);
           if (++s == ST) { s = 0; ph ^= 1; }
         }
       }
@@ -199,9 +249,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       int s = 0;
       uint32_t ph = 0;
       int i = 0;
-      for (int64_t t = t_begin; t < t_end; ++t, ++i) {
-        int64_t rb, cb;
-        decode<MB>(t, args, rb, cb);
+      Cursor<MB, MODE> c;
+      for (c.begin(args, u_begin, u_end); c.valid(); ++i) {
+        const int64_t rb = c.rb;
         if (rb != cur_rb) {
           mbar_wait(a_full, a_par);
           a_par ^= 1;
@@ -233,73 +283,80 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (++s == ST) { s = 0; ph ^= 1; }
         }
         tc_commit(&t_full[buf]);
-        int64_t nrb = -1, ncb;
-        if (t + 1 < t_end) decode<MB>(t + 1, args, nrb, ncb);
-        const bool last_of_block = (t + 1 == t_end) || (nrb != rb);
-        if (last_of_block) tc_commit(a_empty);
+        c.next(args);
+        if (!c.valid() || c.rb != rb) tc_commit(a_empty);  // last tile of this row block
       }
     }
   } else {
     // --------------------------------------------------------- epilogue
     constexpr int NC = MB == 2 ? 4 : 2;  // 32-column chunks per warp per tile
-    constexpr int NBUF = out_bufs(KB);   // staging buffers per warp
+    constexpr int NBUF = out_bufs(KB, MODE);
     const int e = warp - 2;
     const int q = warp & 3;          // TMEM lane quadrant this warp may access
     const int g = e >> 2;            // group: M block (MB=2) or column half (MB=1)
     const int m = MB == 2 ? g : 0;
     const int c_lo = MB == 2 ? 0 : 2 * g;
-    uint8_t* stage0 = sOut + e * NBUF * kStageOutBytes;
+    uint8_t* stage0 = sOut + e * (NBUF > 0 ? NBUF : 1) * kStageOutBytes;
     const float ns = args.ns;
     const float m2ns = -2.f * ns;
     uint32_t tf_par[2] = {0, 0};
     int i = 0;
     int stores = 0;
-    // column / row norms of the next tile are fetched one tile ahead so the
-    // L2 latency hides behind the TMEM-full wait
-    float nx_cb[NC], nx_ra = 0.f;
-    auto prefetch = [&](int64_t t) {
-      int64_t rb, cb;
-      decode<MB>(t, args, rb, cb);
+    double acc64 = 0.0;  // matvec: row partial over the current item
+    // column norms (and matvec v) of the next tile are fetched one tile ahead
+    // so the L2 latency hides behind the TMEM-full wait
+    float nx_cb[NC], nx_v[NC], nx_ra = 0.f;
+    auto prefetch = [&](const Cursor<MB, MODE>& c) {
 #pragma unroll
-      for (int cc = 0; cc < NC; ++cc)
-        nx_cb[cc] = ns * __ldg(args.sqn + cb * kBN + (c_lo + cc) * 32 + lane);
-      const int64_t gr = args.row_lo + (rb * MB + m) * 128 + q * 32 + lane;
+      for (int cc = 0; cc < NC; ++cc) {
+        const int64_t col = c.cb * kBN + (c_lo + cc) * 32 + lane;
+        nx_cb[cc] = ns * __ldg(args.sqn + col);
+        if (MODE == kModeMatvec) nx_v[cc] = __ldg(args.v32 + col);
+      }
+      const int64_t gr = args.row_lo + (c.rb * MB + m) * 128 + q * 32 + lane;
       nx_ra = gr < args.n ? ns * __ldg(args.sqn + gr) : 0.f;
     };
-    if (t_begin < t_end) prefetch(t_begin);
-    for (int64_t t = t_begin; t < t_end; ++t, ++i) {
-      int64_t rb, cb;
-      decode<MB>(t, args, rb, cb);
+    Cursor<MB, MODE> c;
+    c.begin(args, u_begin, u_end);
+    if (c.valid()) prefetch(c);
+    for (; c.valid(); ++i) {
+      const int64_t rb = c.rb, cb = c.cb;
+      const bool item_last = c.item_last();
+      const int64_t chunk = c.chunk;
       const int buf = i & 1;
       const int64_t tI = rb * MB + m;  // tile row of this warp's rows
       // packed: the lower-triangle half of a diagonal row block is not stored
-      const bool store_ok = !args.packed || tI <= cb;
-      const int64_t out_row0 = args.packed ? tile_index(tI, cb, args.n_ctiles) * 128 + q * 32
-                                           : (rb * MB + m) * 128 + q * 32;
+      const bool store_ok = MODE != kModePacked || tI <= cb;
+      const int64_t out_row0 = MODE == kModePacked ? tile_index(tI, cb, args.n_ctiles) * 128 + q * 32
+                                                   : (rb * MB + m) * 128 + q * 32;
       const int64_t lr0 = (rb * MB + m) * 128 + q * 32;  // shard-local first row of this warp
       const int64_t lr = lr0 + lane;
       const int64_t gr = args.row_lo + lr;
-      float cbv[NC];
+      float cbv[NC], vv[NC];
 #pragma unroll
-      for (int cc = 0; cc < NC; ++cc) cbv[cc] = nx_cb[cc];
+      for (int cc = 0; cc < NC; ++cc) {
+        cbv[cc] = nx_cb[cc];
+        vv[cc] = nx_v[cc];
+      }
       const float ra = nx_ra;
-      if (t + 1 < t_end) prefetch(t + 1);
+      c.next(args);
+      if (c.valid()) prefetch(c);
       mbar_wait(&t_full[buf], tf_par[buf]);
       tf_par[buf] ^= 1;
       tc_fence_after();
       float rsum = 0.f;
 #pragma unroll
       for (int cc = 0; cc < NC; ++cc) {
-        const int c = c_lo + cc;
+        const int ch = c_lo + cc;
         uint32_t r[32];
-        tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)((buf * MB + m) * kBN + c * 32),
+        tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)((buf * MB + m) * kBN + ch * 32),
                   r);
         if (cc == NC - 1) {  // accumulator fully read: hand it back to the MMA warp
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&t_empty[buf]);
         }
-        const int64_t col0 = cb * kBN + c * 32;
+        const int64_t col0 = cb * kBN + ch * 32;
         const bool diag = (col0 < args.row_lo + lr0 + 32) && (args.row_lo + lr0 < col0 + 32);
         const bool pad = col0 + 32 > args.n || args.row_lo + lr0 + 32 > args.n;
         float vals[32];
@@ -314,42 +371,56 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int j = 0; j < 32; ++j)
             if (col0 + j == gr || col0 + j >= args.n || gr >= args.n) vals[j] = 0.f;
         }
+        if constexpr (MODE == kModeMatvec) {
 #pragma unroll
-        for (int j = 0; j < 32; ++j) rsum += vals[j];
-        // the store issued NBUF chunks ago must have finished reading this buffer
-        uint8_t* stage = stage0 + (stores % NBUF) * kStageOutBytes;
-        if (stores >= NBUF) {
-          if (lane == 0) tma_store_wait_read<NBUF - 1>();
+          for (int j = 0; j < 32; ++j) rsum = fmaf(vals[j], __shfl_sync(0xffffffffu, vv[cc], j), rsum);
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) rsum += vals[j];
+          // the store issued NBUF chunks ago must have finished reading this buffer
+          uint8_t* stage = stage0 + (stores % NBUF) * kStageOutBytes;
+          if (stores >= NBUF) {
+            if (lane == 0) tma_store_wait_read<NBUF - 1>();
+            __syncwarp();
+          }
+          const uint32_t srow = su32(stage) + lane * 128;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const uint32_t addr = srow + ((j ^ (lane & 7)) << 4);
+            asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(vals[4 * j]),
+                         "f"(vals[4 * j + 1]), "f"(vals[4 * j + 2]), "f"(vals[4 * j + 3])
+                         : "memory");
+          }
+          fence_async_smem();
           __syncwarp();
+          if (lane == 0 && store_ok)
+            tma_store_2d(&map_out, MODE == kModePacked ? ch * 32 : (int)col0, (int)out_row0, stage);
+          ++stores;
         }
-        const uint32_t srow = su32(stage) + lane * 128;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const uint32_t addr = srow + ((j ^ (lane & 7)) << 4);
-          asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(vals[4 * j]),
-                       "f"(vals[4 * j + 1]), "f"(vals[4 * j + 2]), "f"(vals[4 * j + 3])
-                       : "memory");
-        }
-        fence_async_smem();
-        __syncwarp();
-        if (lane == 0 && store_ok)
-          tma_store_2d(&map_out, args.packed ? c * 32 : (int)col0, (int)out_row0, stage);
-        ++stores;
       }
-      if (args.packed) continue;  // degrees come from the symmetric GEMV
-      if constexpr (MB == 2) {
-        if (lr < args.rows) args.rowpart[cb * args.rows_pad + lr] = rsum;
-      } else {
-        // two warps (column halves) share each row: half 1 parks its sum in
-        // smem, half 0 adds it (fixed order) after a 64-thread named barrier.
-        __shared__ float half1[4][32];
-        if (g == 1) half1[q][lane] = rsum;
-        asm volatile("bar.sync %0, %1;" ::"r"(1 + q), "r"(64) : "memory");
-        if (g == 0 && lr < args.rows) args.rowpart[cb * args.rows_pad + lr] = rsum + half1[q][lane];
-        asm volatile("bar.sync %0, %1;" ::"r"(1 + q), "r"(64) : "memory");
+      if constexpr (MODE == kModeMatvec) {
+        acc64 += (double)rsum;
+        if (item_last) {
+          // MB=2: one partial per (chunk, row); MB=1: one per (chunk, half, row)
+          const int64_t slot = MB == 2 ? chunk : chunk * 2 + g;
+          if (lr < args.rows) args.ypart[slot * args.rows_pad + lr] = acc64;
+          acc64 = 0.0;
+        }
+      } else if constexpr (MODE == kModeDense) {
+        if constexpr (MB == 2) {
+          if (lr < args.rows) args.rowpart[cb * args.rows_pad + lr] = rsum;
+        } else {
+          // two warps (column halves) share each row: half 1 parks its sum in
+          // smem, half 0 adds it (fixed order) after a 64-thread named barrier.
+          __shared__ float half1[4][32];
+          if (g == 1) half1[q][lane] = rsum;
+          asm volatile("bar.sync %0, %1;" ::"r"(1 + q), "r"(64) : "memory");
+          if (g == 0 && lr < args.rows) args.rowpart[cb * args.rows_pad + lr] = rsum + half1[q][lane];
+          asm volatile("bar.sync %0, %1;" ::"r"(1 + q), "r"(64) : "memory");
+        }
       }
     }
-    if (lane == 0) tma_store_wait_all();
+    if (MODE != kModeMatvec && lane == 0) tma_store_wait_all();
     __syncwarp();
   }
 
@@ -391,44 +462,59 @@ bool make_map(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t outer,
   return r == CUDA_SUCCESS;
 }
 
-template <int KB>
+int g_num_sms = 0;
+
+template <int KB, int MODE>
 int launch_kb(const CUtensorMap& mh, const CUtensorMap& ml, const CUtensorMap& mo,
               const TcArgs& a0, cudaStream_t s) {
   constexpr int MB = mblocks(KB);
   TcArgs a = a0;
   a.n_rtiles = ceil_div(a.rows, 128 * MB);
-  static int num_sms = 0;
+  a.n_chunks = ceil_div(a.n_ctiles, kChunkTiles);
   static bool attr = false;
   if (!attr) {
-    GPIC_CUDA_TRY(cudaFuncSetAttribute(affinity_tc_kernel<KB>,
+    GPIC_CUDA_TRY(cudaFuncSetAttribute(affinity_tc_kernel<KB, MODE>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       smem_bytes(KB)));
-    int dev;
-    GPIC_CUDA_TRY(cudaGetDevice(&dev));
-    GPIC_CUDA_TRY(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev));
+                                       smem_bytes(KB, MODE)));
     attr = true;
   }
-  const int64_t total =
-      a.packed ? packed_items(a.n_rtiles, a.n_ctiles, MB) : a.n_rtiles * a.n_ctiles;
-  const int grid = (int)(total < num_sms ? total : num_sms);
-  affinity_tc_kernel<KB><<<grid, kThreads, smem_bytes(KB), s>>>(mh, ml, mo, a);
+  if (g_num_sms == 0) {
+    int dev;
+    GPIC_CUDA_TRY(cudaGetDevice(&dev));
+    GPIC_CUDA_TRY(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev));
+  }
+  const int64_t total = total_units<MB, MODE>(a);
+  const int grid = (int)(total < g_num_sms ? total : g_num_sms);
+  if (grid < 1) return GPIC_OK;
+  affinity_tc_kernel<KB, MODE><<<grid, kThreads, smem_bytes(KB, MODE), s>>>(mh, ml, mo, a);
   count_launch();
   GPIC_CUDA_TRY(cudaGetLastError());
   return GPIC_OK;
 }
 
-}  // namespace
-
-namespace {
+template <int MODE>
 int dispatch_kb(int KB, const CUtensorMap& mh, const CUtensorMap& ml, const CUtensorMap& mo,
                 const TcArgs& args, cudaStream_t s) {
   switch (KB) {
-    case 1: return launch_kb<1>(mh, ml, mo, args, s);
-    case 2: return launch_kb<2>(mh, ml, mo, args, s);
-    case 3: return launch_kb<3>(mh, ml, mo, args, s);
-    default: return launch_kb<4>(mh, ml, mo, args, s);
+    case 1: return launch_kb<1, MODE>(mh, ml, mo, args, s);
+    case 2: return launch_kb<2, MODE>(mh, ml, mo, args, s);
+    case 3: return launch_kb<3, MODE>(mh, ml, mo, args, s);
+    default: return launch_kb<4, MODE>(mh, ml, mo, args, s);
   }
 }
+
+int operand_maps(const float* xhi, const float* xlo, int64_t n, int32_t dp, CUtensorMap* mh,
+                 CUtensorMap* ml) {
+  const int KB = dp / kKBlk;
+  if (dp % kKBlk || KB < 1 || KB > 4)
+    return fail(GPIC_E_UNSUPPORTED, "tcgen05 affinity engine supports d <= 128");
+  const int64_t npad = row_pad(n);
+  if (!make_map(mh, xhi, (uint64_t)dp, (uint64_t)npad, (uint64_t)dp * 4, kKBlk, 128) ||
+      !make_map(ml, xlo, (uint64_t)dp, (uint64_t)npad, (uint64_t)dp * 4, kKBlk, 128))
+    return fail(GPIC_E_CUDA, "cuTensorMapEncodeTiled failed");
+  return GPIC_OK;
+}
+
 }  // namespace
 
 int64_t packed_tiles(int64_t n) {
@@ -440,34 +526,67 @@ int64_t packed_tiles(int64_t n) {
 // 128 x 128 fp32 block at tile_index(I, J) (row-major over the triangle).
 int launch_affinity_tc_packed(const float* xhi, const float* xlo, const float* sqn, int64_t n,
                               int32_t dp, float neg_scale_log2, float* a_packed, cudaStream_t s) {
-  const int KB = dp / kKBlk;
-  if (dp % kKBlk || KB < 1 || KB > 4)
-    return fail(GPIC_E_UNSUPPORTED, "tcgen05 affinity engine supports d <= 128");
-  const int64_t npad = row_pad(n);
   CUtensorMap mh, ml, mo;
-  if (!make_map(&mh, xhi, (uint64_t)dp, (uint64_t)npad, (uint64_t)dp * 4, kKBlk, 128) ||
-      !make_map(&ml, xlo, (uint64_t)dp, (uint64_t)npad, (uint64_t)dp * 4, kKBlk, 128) ||
-      !make_map(&mo, a_packed, 128, (uint64_t)packed_tiles(n) * 128, 512, 32, 32))
+  int rc = operand_maps(xhi, xlo, n, dp, &mh, &ml);
+  if (rc) return rc;
+  if (!make_map(&mo, a_packed, 128, (uint64_t)packed_tiles(n) * 128, 512, 32, 32))
     return fail(GPIC_E_CUDA, "cuTensorMapEncodeTiled failed");
-  TcArgs args{sqn, n, 0, n, neg_scale_log2, nullptr, 0, 0, ceil_div(n, kBN), 1};
-  return dispatch_kb(KB, mh, ml, mo, args, s);
+  TcArgs args{};
+  args.sqn = sqn;
+  args.n = n;
+  args.rows = n;
+  args.ns = neg_scale_log2;
+  args.n_ctiles = ceil_div(n, kBN);
+  return dispatch_kb<kModePacked>(dp / kKBlk, mh, ml, mo, args, s);
 }
 
 int launch_affinity_tc(const float* xhi, const float* xlo, const float* sqn, int64_t n,
                        int32_t dp, int64_t row_lo, int64_t row_hi, float neg_scale_log2, float* a,
                        int64_t lda, float* rowpart, int64_t rows_pad, cudaStream_t s) {
-  const int KB = dp / kKBlk;
-  if (dp % kKBlk || KB < 1 || KB > 4)
-    return fail(GPIC_E_UNSUPPORTED, "tcgen05 affinity engine supports d <= 128");
-  const int64_t npad = row_pad(n);
   const int64_t rows = row_hi - row_lo;
   CUtensorMap mh, ml, mo;
-  if (!make_map(&mh, xhi, (uint64_t)dp, (uint64_t)npad, (uint64_t)dp * 4, kKBlk, 128) ||
-      !make_map(&ml, xlo, (uint64_t)dp, (uint64_t)npad, (uint64_t)dp * 4, kKBlk, 128) ||
-      !make_map(&mo, a, (uint64_t)lda, (uint64_t)rows, (uint64_t)lda * 4, 32, 32))
+  int rc = operand_maps(xhi, xlo, n, dp, &mh, &ml);
+  if (rc) return rc;
+  if (!make_map(&mo, a, (uint64_t)lda, (uint64_t)rows, (uint64_t)lda * 4, 32, 32))
     return fail(GPIC_E_CUDA, "cuTensorMapEncodeTiled failed");
-  TcArgs args{sqn, n, row_lo, rows, neg_scale_log2, rowpart, rows_pad, 0, ceil_div(n, kBN), 0};
-  return dispatch_kb(KB, mh, ml, mo, args, s);
+  TcArgs args{};
+  args.sqn = sqn;
+  args.n = n;
+  args.row_lo = row_lo;
+  args.rows = rows;
+  args.ns = neg_scale_log2;
+  args.rowpart = rowpart;
+  args.rows_pad = rows_pad;
+  args.n_ctiles = ceil_div(n, kBN);
+  return dispatch_kb<kModeDense>(dp / kKBlk, mh, ml, mo, args, s);
+}
+
+int64_t mf_parts(int64_t n, int32_t dp) {
+  const int64_t chunks = ceil_div(ceil_div(n, kBN), kChunkTiles);
+  return mblocks(dp / kKBlk) == 2 ? chunks : 2 * chunks;
+}
+
+// Matrix-free row block: ypart[p][i - row_lo] = sum over chunk p of
+// a_ij v_j (fp64 across tiles); gpic's mf_reduce combines the parts.
+int launch_affinity_tc_matvec(const float* xhi, const float* xlo, const float* sqn, int64_t n,
+                              int32_t dp, int64_t row_lo, int64_t row_hi, float neg_scale_log2,
+                              const float* v32, double* ypart, int64_t rows_pad,
+                              const gpic_ctl* ctl, cudaStream_t s) {
+  CUtensorMap mh, ml;
+  int rc = operand_maps(xhi, xlo, n, dp, &mh, &ml);
+  if (rc) return rc;
+  TcArgs args{};
+  args.sqn = sqn;
+  args.n = n;
+  args.row_lo = row_lo;
+  args.rows = row_hi - row_lo;
+  args.ns = neg_scale_log2;
+  args.rows_pad = rows_pad;
+  args.n_ctiles = ceil_div(n, kBN);
+  args.v32 = v32;
+  args.ypart = ypart;
+  args.ctl = ctl;
+  return dispatch_kb<kModeMatvec>(dp / kKBlk, mh, ml, mh, args, s);
 }
 
 }  // namespace gpic

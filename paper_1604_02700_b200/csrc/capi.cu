@@ -248,6 +248,22 @@ int gpic_sym_matvec(const float* d_tiles, int64_t n, const float* d_v, float* d_
 
 int64_t gpic_vector_pitch(int64_t n) { return vector_pitch(n); }
 
+int64_t gpic_mf_ypart_doubles(int64_t n, int32_t d, int64_t rows) {
+  if (n < 1 || d < 1 || rows < 1) return -1;
+  return mf_ypart_doubles(n, feature_pitch(d), rows);
+}
+
+int gpic_mf_degrees(const float* d_xhi, const float* d_xlo, const float* d_sqn, int64_t n,
+                    int32_t d, int64_t row_lo, int64_t row_hi, double sigma, float* d_ones,
+                    double* d_ypart, double* d_deg, void* stream) {
+  if (!(sigma > 0)) return fail(GPIC_E_INVALID, "sigma must be positive");
+  if (row_lo < 0 || row_hi > n || row_lo >= row_hi) return fail(GPIC_E_INVALID, "bad row range");
+  const MfOperands op{d_xhi, d_xlo, d_sqn, n, feature_pitch(d),
+                      (float)(-1.4426950408889634 / (2.0 * sigma * sigma))};
+  return launch_mf_degrees(op, row_lo, row_hi - row_lo, d_ones, d_ypart, d_deg,
+                           static_cast<cudaStream_t>(stream));
+}
+
 int gpic_matvec(const float* d_a, int64_t lda, int64_t rows, int64_t n, const float* d_v,
                 const double* d_row_scale, double* d_y, void* stream) {
   if (lda % 4 || lda < n) return fail(GPIC_E_INVALID, "lda must be >= n and a multiple of 4");
@@ -268,6 +284,8 @@ int64_t gpic_cluster_workspace_bytes(int64_t n, int32_t d, int32_t k, int32_t ma
   const int64_t scratch = workspace_bytes(n, d, k, n, max_iter);
   if (storage == GPIC_STORAGE_PACKED)
     return scratch + packed_tiles(n) * 128 * 128 * 4 + 2 * al(sym_partial_floats(n) * 4);
+  if (storage == GPIC_STORAGE_NONE)
+    return scratch + al(mf_ypart_doubles(n, feature_pitch(d), n) * 8);
   return scratch + n * affinity_pitch(n) * 4;
 }
 
@@ -289,8 +307,10 @@ int gpic_cluster(const double* d_x, int64_t n, int32_t d, double sigma, int32_t 
                  void* stream) {
   if (n < 1 || d < 1) return fail(GPIC_E_EMPTY, "dataset must contain at least one point and one feature");
   if (k > n) return fail(GPIC_E_K_TOO_LARGE, "k exceeds the number of points");
-  if (storage == GPIC_STORAGE_PACKED && impl != GPIC_AFFINITY_TC)
-    return fail(GPIC_E_UNSUPPORTED, "packed symmetric storage is built by the tcgen05 engine");
+  if (storage != GPIC_STORAGE_DENSE && impl != GPIC_AFFINITY_TC)
+    return fail(GPIC_E_UNSUPPORTED, "packed / matrix-free storage runs on the tcgen05 engine");
+  if (storage < GPIC_STORAGE_DENSE || storage > GPIC_STORAGE_NONE)
+    return fail(GPIC_E_INVALID, "unknown storage mode");
   Workspace ws;
   const int64_t scratch = workspace_bytes(n, d, k, n, max_iter);
   const int64_t need = gpic_cluster_workspace_bytes(n, d, k, max_iter, storage);
@@ -321,9 +341,19 @@ int gpic_cluster(const double* d_x, int64_t n, int32_t d, double sigma, int32_t 
     launch_sym_gemv(a, n, ws.v32, rowp, colp, nullptr, pt, nullptr, s);
     zero_check_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, s>>>(deg, n, ws.ctl);
     count_launch(2);
-    L.packed = 1;
+    L.mode = kLoopPacked;
     L.rowp = rowp;
     L.colp = colp;
+  } else if (storage == GPIC_STORAGE_NONE) {
+    // matrix-free: A is recomputed from X for the degrees and every iteration
+    double* ypart = reinterpret_cast<double*>(a);
+    L.mode = kLoopMatrixFree;
+    L.mf = MfOperands{ws.xhi, ws.xlo, ws.sqn, n, dp, neg_scale_log2};
+    L.ypart = ypart;
+    rc = launch_mf_degrees(L.mf, 0, n, ws.v32, ypart, deg, s);
+    if (rc) return rc;
+    zero_check_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, s>>>(deg, n, ws.ctl);
+    count_launch();
   } else {
     const int64_t rows_pad = round_up(n, kTileM);
     if (impl == GPIC_AFFINITY_TC) {

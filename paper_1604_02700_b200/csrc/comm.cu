@@ -318,6 +318,13 @@ int gpic_comm_iterate(gpic_comm* c, const gpic_shard* shards, int32_t nlocal, do
     std::memset(&S, 0, sizeof S);
     S.a = shards[li].a;
     S.lda = shards[li].lda;
+    if (shards[li].storage == GPIC_STORAGE_NONE) {
+      const gpic_shard& sh = shards[li];
+      S.mode = kLoopMatrixFree;
+      S.mf = MfOperands{sh.xhi, sh.xlo, sh.sqn, n, feature_pitch(sh.d),
+                        (float)(-1.4426950408889634 / (2.0 * sh.sigma * sh.sigma))};
+      S.ypart = sh.ypart;
+    }
     S.rows = shards[li].rows;
     S.row_lo = shards[li].row_lo;
     S.deg = shards[li].deg;

@@ -109,12 +109,37 @@ struct PeerTable;
 void launch_sym_gemv(const float* tiles, int64_t n, const float* v32, float* rowp, float* colp,
                      const double* deg, const PeerTable& pt, gpic_ctl* ctl, cudaStream_t s);
 
+// ---- matrix-free (affinity_tc.cu matvec mode + mf.cu) --------------------
+struct MfOperands {
+  const float* xhi;
+  const float* xlo;
+  const float* sqn;
+  int64_t n;
+  int32_t dp;
+  float ns;  // -log2(e) / (2 sigma^2)
+};
+int64_t mf_parts(int64_t n, int32_t dp);
+int64_t mf_ypart_doubles(int64_t n, int32_t dp, int64_t rows);
+int launch_affinity_tc_matvec(const float* xhi, const float* xlo, const float* sqn, int64_t n,
+                              int32_t dp, int64_t row_lo, int64_t row_hi, float neg_scale_log2,
+                              const float* v32, double* ypart, int64_t rows_pad,
+                              const gpic_ctl* ctl, cudaStream_t s);
+int launch_mf_matvec(const MfOperands& op, int64_t row_lo, int64_t rows, const float* v32,
+                     double* ypart, const double* deg, const PeerTable& pt, gpic_ctl* ctl,
+                     cudaStream_t s);
+int launch_mf_degrees(const MfOperands& op, int64_t row_lo, int64_t rows, float* ones,
+                      double* ypart, double* deg, cudaStream_t s);
+
+enum { kLoopDense = 0, kLoopPacked = 1, kLoopMatrixFree = 2 };
+
 // One shard's loop state (a single-rank run is one shard with nranks = 1).
 struct ShardLoop {
   const float* a;     // dense row block, or the packed tiles when packed
-  int packed;         // 1: symmetric packed tiles (whole matrix, one shard)
+  int mode;           // kLoopDense / kLoopPacked (whole matrix) / kLoopMatrixFree
   float* rowp;        // packed: per-tile row / column partials
   float* colp;
+  MfOperands mf;      // matrix-free operands
+  double* ypart;      // matrix-free row partials
   int64_t lda;
   int64_t rows;
   int64_t row_lo;

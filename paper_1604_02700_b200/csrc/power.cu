@@ -298,10 +298,20 @@ int run_power_loops(ShardLoop* shards, int nlocal, int64_t n, int32_t max_iter, 
     for (int t = 0; t < max_iter; ++t) {
       for (int i = 0; i < nlocal; ++i) {
         const ShardLoop& L = shards[i];
-        if (L.packed)
+        if (L.mode == kLoopPacked) {
           launch_sym_gemv(L.a, n, L.v32, L.rowp, L.colp, L.deg, L.pt, L.ctl, cs);
-        else
+        } else if (L.mode == kLoopMatrixFree) {
+          const int rc = launch_mf_matvec(L.mf, L.row_lo, L.rows, L.v32, L.ypart, L.deg, L.pt,
+                                          L.ctl, cs);
+          if (rc) {
+            cudaGraph_t junk;
+            cudaStreamEndCapture(cs, &junk);
+            if (junk) cudaGraphDestroy(junk);
+            return rc;
+          }
+        } else {
           launch_gemv(L.a, L.lda, L.rows, L.row_lo, L.v32, L.deg, L.pt, L.ctl, cs);
+        }
       }
       for (int i = 0; i < nlocal; ++i) {
         const ShardLoop& L = shards[i];

@@ -163,19 +163,36 @@ __device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
   asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
-__global__ void __launch_bounds__(256)
+// One CTA per tile row R (128 rows), 8 segments of the row's NT tiles per
+// row: segment s sums its contiguous column-tile range in order (column
+// partials of tiles (p, R) for p < R, row partials of (R, p) for p >= R),
+// then the 8 segment sums are added in order. The shape depends on NT only.
+constexpr int kSeg = 8;
+
+__global__ void __launch_bounds__(kTS * kSeg)
     sym_reduce_kernel(const float* __restrict__ rowp, const float* __restrict__ colp, int64_t n,
                       int64_t nt, const double* __restrict__ deg, const PeerTable pt,
                       gpic_ctl* ctl) {
   if (ctl != nullptr && *(volatile const int32_t*)&ctl->stop) return;
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) {
-    const int64_t R = i / kTS, o = i % kTS;
-    double s = 0.0;
-    for (int64_t Jp = 0; Jp < R; ++Jp) s += (double)colp[tile_index(Jp, R, nt) * kTS + o];
-    const int64_t base = tile_index(R, R, nt);
-    for (int64_t J = R; J < nt; ++J) s += (double)rowp[(base + (J - R)) * kTS + o];
-    const double val = deg != nullptr ? s / deg[i] : s;
+  __shared__ double part[kSeg][kTS];
+  const int64_t R = blockIdx.x;
+  const int o = threadIdx.x % kTS, sg = threadIdx.x / kTS;
+  const int64_t p0 = nt * sg / kSeg, p1 = nt * (sg + 1) / kSeg;
+  double s = 0.0;
+  const int64_t diag = tile_index(R, R, nt);
+#pragma unroll 4
+  for (int64_t p = p0; p < p1; ++p) {
+    const float x = p < R ? colp[tile_index(p, R, nt) * kTS + o] : rowp[(diag + (p - R)) * kTS + o];
+    s += (double)x;
+  }
+  part[sg][o] = s;
+  __syncthreads();
+  const int64_t i = R * kTS + o;
+  if (sg == 0 && i < n) {
+    double t = 0.0;
+#pragma unroll
+    for (int q = 0; q < kSeg; ++q) t += part[q][o];
+    const double val = deg != nullptr ? t / deg[i] : t;
     const int parity = ctl != nullptr ? (ctl->iter & 1) : 0;
     for (int p = 0; p < pt.nranks; ++p) pt.y[p][parity][i] = val;
   }
@@ -218,7 +235,7 @@ void launch_sym_gemv(const float* tiles, int64_t n, const float* v32, float* row
   const int64_t total = nt * (nt + 1) / 2;
   const int grid = (int)(total < g_sms ? total : g_sms);
   sym_gemv_kernel<<<grid, kThreads, kSmem, s>>>(tiles, nt, v32, rowp, colp, ctl);
-  sym_reduce_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, s>>>(rowp, colp, n, nt, deg, pt, ctl);
+  sym_reduce_kernel<<<(unsigned)nt, kTS * kSeg, 0, s>>>(rowp, colp, n, nt, deg, pt, ctl);
   count_launch(2);
 }
 

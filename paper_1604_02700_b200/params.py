@@ -85,7 +85,7 @@ class KMeansParams:
 DEFAULT_MEMORY_BUDGET = 256 * 1024 * 1024
 
 AFFINITY_IMPLS = ("tc", "simt")
-STORAGES = ("packed", "dense")
+STORAGES = ("packed", "dense", "none")
 
 
 @dataclass(frozen=True)
@@ -104,7 +104,8 @@ class KernelConfig:
     ``storage`` = "packed" keeps only the upper triangle of 128x128 tiles
     of the (exactly symmetric) affinity matrix — half the HBM bytes of the
     affinity store and of every power iteration; "dense" keeps full rows
-    (used by the SIMT engine and by row-sharded multi-rank runs).
+    (used by the SIMT engine and by row-sharded multi-rank runs); "none" is
+    matrix-free: A is recomputed from X for every product (n^2 > HBM).
     """
 
     p: int = 1
@@ -128,7 +129,12 @@ class KernelConfig:
             raise InvalidSpec(f"storage must be one of {STORAGES}")
 
     def storage_code(self) -> int:
-        """Packed symmetric tiles need the tcgen05 engine and a single rank."""
+        """GPIC_STORAGE_*: packed symmetric tiles need the tcgen05 engine and a
+        single rank; matrix-free ("none") needs the tcgen05 engine."""
+        if self.storage == "none":
+            if self.affinity_impl != "tc":
+                raise InvalidSpec("matrix-free storage runs on the tcgen05 engine")
+            return 2
         if self.storage == "packed" and self.affinity_impl == "tc" and self.p == 1:
             return 1
         return 0

@@ -133,13 +133,33 @@ class ShardedRunner:
         n, dev, cfg = self.n, self.dev, self.config
         st = gpu._stream(dev)
         prep = gpu.prepare_points(points, dev)
-        blocks = [gpu.affinity_rows(prep, *self.ranges[r], sigma, cfg.affinity_impl)
-                  for r in self.locals]
         nl = len(self.locals)
         shards = (_lib.Shard * nl)()
-        for i, (r, blk) in enumerate(zip(self.locals, blocks)):
-            lo, hi = self.ranges[r]
-            shards[i] = _lib.Shard(blk.a.data_ptr(), blk.lda, blk.deg.data_ptr(), lo, hi - lo)
+        keep = []  # device buffers referenced by the shard structs
+        L = _lib.lib()
+        if cfg.storage == "none":
+            if cfg.affinity_impl != "tc":
+                raise InvalidSpec("matrix-free storage runs on the tcgen05 engine")
+            ones = torch.empty(int(L.gpic_vector_pitch(n)), dtype=torch.float32, device=dev)
+            for i, r in enumerate(self.locals):
+                lo, hi = self.ranges[r]
+                deg = torch.empty(hi - lo, dtype=torch.float64, device=dev)
+                ypart = torch.empty(int(L.gpic_mf_ypart_doubles(n, prep.d, hi - lo)),
+                                    dtype=torch.float64, device=dev)
+                _lib.check(L.gpic_mf_degrees(gpu._ptr(prep.xhi), gpu._ptr(prep.xlo),
+                                             gpu._ptr(prep.sqn), n, prep.d, lo, hi, sigma,
+                                             gpu._ptr(ones), gpu._ptr(ypart), gpu._ptr(deg), st))
+                keep += [deg, ypart]
+                shards[i] = _lib.Shard(None, 0, deg.data_ptr(), lo, hi - lo, _lib.STORAGE_NONE,
+                                       prep.d, prep.xhi.data_ptr(), prep.xlo.data_ptr(),
+                                       prep.sqn.data_ptr(), sigma, ypart.data_ptr())
+        else:
+            for i, r in enumerate(self.locals):
+                lo, hi = self.ranges[r]
+                blk = gpu.affinity_rows(prep, lo, hi, sigma, cfg.affinity_impl)
+                keep.append(blk)
+                shards[i] = _lib.Shard(blk.a.data_ptr(), blk.lda, blk.deg.data_ptr(), lo, hi - lo,
+                                       _lib.STORAGE_DENSE, prep.d, None, None, None, sigma, None)
         T = params.max_iterations
         eps = params.resolved_epsilon(n)
         hist = torch.zeros(nl * T, dtype=torch.float64, device=dev)

@@ -338,3 +338,24 @@ def test_sym_matvec_against_numpy():
         assert rc == 0
         ref = a.astype(np.float32).astype(np.float64) @ v.astype(np.float32).astype(np.float64)
         assert np.max(np.abs(y.cpu().numpy() - ref) / np.abs(ref)) <= 1e-5, n
+
+
+@pytest.mark.parametrize("case", ["config1", "gblobs_small"])
+def test_matrix_free_matches_stored(golden, case):
+    """K4: recomputing A every iteration gives the stored-matrix result."""
+    z = golden(case)
+    d = DataSet(_points(z))
+    kind, params = GaussianRbf(float(z["sigma"])), PicParams(k=int(z["k"]))
+    lm, vm, tm = cluster(d, kind, params, config=KernelConfig(storage="none"), seed=int(z["seed"]))
+    lp, vp, tp = cluster(d, kind, params, config=KernelConfig(storage="packed"), seed=int(z["seed"]))
+    assert np.array_equal(lm, z["labels"]) and np.array_equal(lm, lp)
+    assert tm.iterations_run == tp.iterations_run
+    assert rel_l1(vm, vp) <= 1e-5
+    assert rel_l1(vm, z["v"]) <= 1e-4
+    # forced iterations against the reference
+    _, vT, _ = cluster(d, kind, PicParams(k=int(z["k"]), epsilon=TINY_EPS, max_iterations=3),
+                       config=KernelConfig(storage="none"))
+    a = po.affinity(d.points, float(z["sigma"]))
+    dd = po.degree(a)
+    ref, _, _ = po.power_iteration(po.normalize(a, dd), po.start_vector(dd), TINY_EPS, 3)
+    assert rel_l1(vT, ref) <= 1e-4

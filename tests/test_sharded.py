@@ -140,3 +140,15 @@ def test_two_processes_one_device_ipc():
     res = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env, cwd=ROOT)
     assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-3000:]
     assert "RANKS_AGREE True" in res.stdout and "MATCHES_SINGLE True" in res.stdout
+
+
+@pytest.mark.gpu
+def test_matrix_free_virtual_ranks_bitwise():
+    d = gaussian_blobs(2600, 64, 4, seed=8)
+    kind, params = GaussianRbf(4.0), PicParams(k=4)
+    base = cluster(d, kind, params, config=KernelConfig(storage="none"), seed=3)
+    for p in (2, 5):
+        got = cluster(d, kind, params, seed=3,
+                      config=KernelConfig(p=p, virtual_ranks=True, storage="none"))
+        assert np.array_equal(got[0], base[0]) and np.array_equal(got[1], base[1]), p
+        assert np.array_equal(got[2].delta_history, base[2].delta_history)
