@@ -52,6 +52,17 @@ def peaks():
     return FALLBACK_HBM_GBS, "fallback"
 
 
+def tf32_peak():
+    """TF32 dense = half the bf16 rate (measured cuBLAS bf16 burst / 2)."""
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        return float(json.loads(p.read_text())["bf16_tflops"]) / 2.0, "measured bf16 / 2"
+    return 1590.0 / 2.0, "fallback bf16 / 2"
+
+
+CONFIGS_SIGMA = {c["n"]: c["sigma"] for c in CONFIGS.values()}
+
+
 # ------------------------------------------------------------ clocks
 class ClockSampler:
     FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
@@ -190,7 +201,7 @@ METRIC = "PIC end-to-end s (power-iter HBM GB/s alongside)"
 def workload(cfg, gpus):
     c = CONFIGS[cfg]
     return {"workload": f"config{cfg}: gaussian blobs n={c['n']} d={c['d']} k={c['k']} "
-                        f"sigma={c['sigma']:.4f}, dense fp32 W in HBM",
+                        f"sigma={c['sigma']:.4f}",
             "n": c["n"], "d": c["d"], "k": c["k"], "sigma": c["sigma"],
             "parallelism": f"row-shard x{gpus}", "l2": "inputs > L2 (W = 4n^2 bytes)"}
 
@@ -207,7 +218,28 @@ def _gemv_roofline(args, L, C, torch, stream, st, n, m, k, T, work, v, storage):
     v32[:n] = v.to(torch.float32)
     yv = torch.empty(n, dtype=torch.float64, device=dev)
     deg1 = torch.ones(n, dtype=torch.float64, device=dev)
-    if storage == 1:
+    if storage == 2:
+        # matrix-free: one recompute pass A v (tcgen05 3xTF32 Gram + exp + v),
+        # timed through the degree entry (v = 1); work = 3 x 2 n^2 dp flops
+        scr = ((int(L.gpic_workspace_bytes(n, m, k, n, T)) + 255) // 256) * 256
+        dp = int(L.gpic_feature_pitch(m))
+        npad = int(L.gpic_row_pad(n))
+        # xhi / xlo / sqn live at the head of the workspace (after the ctl)
+        xhi = work.data_ptr() + 256
+        xlo = xhi + ((npad * dp * 4 + 255) // 256) * 256
+        sqn = xlo + ((npad * dp * 4 + 255) // 256) * 256
+        ypart = torch.empty(int(L.gpic_mf_ypart_doubles(n, m, n)), dtype=torch.float64, device=dev)
+        ones = torch.empty(vp, dtype=torch.float32, device=dev)
+        sigma = CONFIGS_SIGMA[n]
+
+        def launch():
+            return L.gpic_mf_degrees(C.c_void_p(xhi), C.c_void_p(xlo), C.c_void_p(sqn), n, m, 0, n,
+                                     sigma, C.c_void_p(ones.data_ptr()),
+                                     C.c_void_p(ypart.data_ptr()), C.c_void_p(yv.data_ptr()), st)
+        alg = 3.0 * 2.0 * n * n * dp
+        name = "affinity_tc_kernel<matvec> (matrix-free A v: 3xTF32 Gram + exp + v)"
+        del scr
+    elif storage == 1:
         ntiles = int(L.gpic_packed_tiles(n))
         tile_bytes = ntiles * 128 * 128 * 4
         rowp = base + tile_bytes
@@ -314,6 +346,12 @@ def run_ours(args, cfg, rank, world):
     achieved = alg_bytes / (gemv_ms * 1e-3) / 1e9
     dense_equiv = float(n) * n * 4 / (gemv_ms * 1e-3) / 1e9
     peak, peak_kind = peaks()
+    bound, unit = "hbm", "GB/s"
+    if storage == 2:
+        # tensor-bound: TF32 dense rate = half the measured bf16 cuBLAS rate
+        achieved = alg_bytes / (gemv_ms * 1e-3) / 1e12
+        peak, peak_kind = tf32_peak()
+        bound, unit = "tensor", "TFLOP/s"
 
     # e2e leg through the public API from pinned host memory
     cluster(d_host, GaussianRbf(sigma), params, config=cfg_api, seed=0)
@@ -342,9 +380,11 @@ def run_ours(args, cfg, rank, world):
         "config": dict(workload(cfg, world), affinity_engine=impl_name, storage=args.storage),
         "power_iter_hbm_gbs": achieved, "power_iter_dense_equiv_gbs": dense_equiv,
         "iterations": int(iters.value), "converged": bool(conv.value), "ari_vs_truth": ari,
-        "roofline": {"kernel": kname, "bound": "hbm", "achieved": achieved, "peak": peak,
-                     "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "algorithmic_bytes_per_launch": alg_bytes,
+        "roofline": {"kernel": kname, "bound": bound, "achieved": achieved, "peak": peak,
+                     "peak_kind": peak_kind, "unit": unit, "frac": achieved / peak,
+                     "traffic": traffic,
+                     ("algorithmic_flops_per_launch" if storage == 2
+                      else "algorithmic_bytes_per_launch"): alg_bytes,
                      "avg_launch_ms": gemv_ms},
         "e2e": {"value": e2e_s, "unit": "s", "h2d_bytes_per_step": int(n * m * 8),
                 "d2h_bytes_per_step": int(n * 8 * 2 + T * 8)},
@@ -448,7 +488,7 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", type=int, default=3)
     ap.add_argument("--engine", choices=["tc", "simt"], default="tc")
-    ap.add_argument("--storage", choices=["packed", "dense"], default="packed")
+    ap.add_argument("--storage", choices=["packed", "dense", "none"], default="packed")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--gemv-reps", type=int, default=10)
     ap.add_argument("--ref-rows", type=int, default=256)
