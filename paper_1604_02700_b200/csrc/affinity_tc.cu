@@ -32,6 +32,8 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
+
 #include "common.cuh"
 #include "ops.h"
 #include "sm100.cuh"
@@ -54,19 +56,21 @@ constexpr int kChunkTiles = 32;              // matvec: column tiles per work it
 __host__ __device__ constexpr int mblocks(int KB) { return KB <= 2 ? 2 : 1; }
 __host__ __device__ constexpr int a_bytes(int KB) { return 2 * mblocks(KB) * KB * kTileBytes; }
 // output staging buffers per epilogue warp (double-buffered where smem allows)
-__host__ __device__ constexpr int out_bufs(int KB, int MODE) {
-  return MODE == kModeMatvec ? 0 : ((KB == 1 || KB == 3) ? 2 : 1);
+// DIRECT: the epilogue stores straight from registers (no smem staging)
+__host__ __device__ constexpr int out_bufs(int KB, int MODE, bool DIRECT) {
+  return (MODE == kModeMatvec || DIRECT) ? 0 : ((KB == 1 || KB == 3) ? 2 : 1);
 }
-__host__ __device__ constexpr int out_bytes(int KB, int MODE) {
-  return kEpiWarps * out_bufs(KB, MODE) * kStageOutBytes;
+__host__ __device__ constexpr int out_bytes(int KB, int MODE, bool DIRECT) {
+  return kEpiWarps * out_bufs(KB, MODE, DIRECT) * kStageOutBytes;
 }
-__host__ __device__ constexpr int stages(int KB, int MODE) {
-  return (kSmemBudget - a_bytes(KB) - out_bytes(KB, MODE)) / (2 * kTileBytes) > 4
+__host__ __device__ constexpr int stages(int KB, int MODE, bool DIRECT) {
+  return (kSmemBudget - a_bytes(KB) - out_bytes(KB, MODE, DIRECT)) / (2 * kTileBytes) > 4
              ? 4
-             : (kSmemBudget - a_bytes(KB) - out_bytes(KB, MODE)) / (2 * kTileBytes);
+             : (kSmemBudget - a_bytes(KB) - out_bytes(KB, MODE, DIRECT)) / (2 * kTileBytes);
 }
-__host__ __device__ constexpr int smem_bytes(int KB, int MODE) {
-  return a_bytes(KB) + stages(KB, MODE) * 2 * kTileBytes + out_bytes(KB, MODE) + 256 + 1024;
+__host__ __device__ constexpr int smem_bytes(int KB, int MODE, bool DIRECT) {
+  return a_bytes(KB) + stages(KB, MODE, DIRECT) * 2 * kTileBytes + out_bytes(KB, MODE, DIRECT) +
+         256 + 1024;
 }
 
 constexpr uint32_t kIdesc = idesc_tf32(128, kBN);
@@ -85,6 +89,8 @@ struct TcArgs {
   double* ypart;     // matvec: [n_chunks * parts][rows_pad] fp64 row partials
   int64_t n_chunks;  // matvec: column chunks (kChunkTiles tiles) per row block
   const gpic_ctl* ctl;  // matvec in a loop: exit at once when ctl->stop is set
+  float* out;        // DIRECT stores: dense A rows (pitch lda) or packed tiles
+  int64_t lda;
 };
 
 __host__ __device__ inline int64_t packed_items(int64_t nrt, int64_t nct, int mb) {
@@ -151,13 +157,13 @@ __host__ __device__ inline int64_t total_units(const TcArgs& a) {
   return a.n_rtiles * a.n_ctiles;
 }
 
-template <int KB, int MODE>
+template <int KB, int MODE, bool DIRECT>
 __global__ void __launch_bounds__(kThreads, 1)
     affinity_tc_kernel(const __grid_constant__ CUtensorMap map_hi,
                        const __grid_constant__ CUtensorMap map_lo,
                        const __grid_constant__ CUtensorMap map_out, const TcArgs args) {
   constexpr int MB = mblocks(KB);
-  constexpr int ST = stages(KB, MODE);
+  constexpr int ST = stages(KB, MODE, DIRECT);
   constexpr int kTmemCols = 2 * MB * kBN;  // 2 accumulators
   if (MODE == kModeMatvec && args.ctl != nullptr && *(volatile const int32_t*)&args.ctl->stop)
     return;
@@ -167,7 +173,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* sA = base;                                     // [hl][m][kb] 16 KB tiles
   uint8_t* sB = sA + a_bytes(KB);                         // [stage][hl] 16 KB tiles
   uint8_t* sOut = sB + ST * 2 * kTileBytes;               // [epi warp][buf] 4 KB
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sOut + out_bytes(KB, MODE));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sOut + out_bytes(KB, MODE, DIRECT));
   uint64_t* full = bars;                 // [ST]
   uint64_t* empty = bars + ST;           // [ST]
   uint64_t* a_full = bars + 2 * ST;
@@ -196,7 +202,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_hi)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_lo)) : "memory");
-    if (MODE != kModeMatvec)
+    if (MODE != kModeMatvec && !DIRECT)
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_out)) : "memory");
   }
   if (warp == 1) {
@@ -245,7 +251,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       int64_t cur_rb = -1;
       uint32_t a_par = 0;
-      uint32_t te_par[2] = {1, 1};
+      uint32_t te_bits = 3u;  // TMEM-empty parity per accumulator buffer
       int s = 0;
       uint32_t ph = 0;
       int i = 0;
@@ -258,8 +264,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           cur_rb = rb;
         }
         const int buf = i & 1;
-        mbar_wait(&t_empty[buf], te_par[buf]);
-        te_par[buf] ^= 1;
+        mbar_wait(&t_empty[buf], (te_bits >> buf) & 1u);
+        te_bits ^= 1u << buf;
         tc_fence_after();
         for (int kb = 0; kb < KB; ++kb) {
           mbar_wait(&full[s], ph);
@@ -290,7 +296,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else {
     // --------------------------------------------------------- epilogue
     constexpr int NC = MB == 2 ? 4 : 2;  // 32-column chunks per warp per tile
-    constexpr int NBUF = out_bufs(KB, MODE);
+    constexpr int NBUF = out_bufs(KB, MODE, DIRECT);
     const int e = warp - 2;
     const int q = warp & 3;          // TMEM lane quadrant this warp may access
     const int g = e >> 2;            // group: M block (MB=2) or column half (MB=1)
@@ -299,7 +305,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint8_t* stage0 = sOut + e * (NBUF > 0 ? NBUF : 1) * kStageOutBytes;
     const float ns = args.ns;
     const float m2ns = -2.f * ns;
-    uint32_t tf_par[2] = {0, 0};
+    uint32_t tf_bits = 0;  // TMEM-full parity per accumulator buffer
     int i = 0;
     int stores = 0;
     double acc64 = 0.0;  // matvec: row partial over the current item
@@ -341,8 +347,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       const float ra = nx_ra;
       c.next(args);
       if (c.valid()) prefetch(c);
-      mbar_wait(&t_full[buf], tf_par[buf]);
-      tf_par[buf] ^= 1;
+      mbar_wait(&t_full[buf], (tf_bits >> buf) & 1u);
+      tf_bits ^= 1u << buf;
       tc_fence_after();
       float rsum = 0.f;
 #pragma unroll
@@ -374,6 +380,23 @@ __global__ void __launch_bounds__(kThreads, 1)
         if constexpr (MODE == kModeMatvec) {
 #pragma unroll
           for (int j = 0; j < 32; ++j) rsum = fmaf(vals[j], __shfl_sync(0xffffffffu, vv[cc], j), rsum);
+        } else if constexpr (DIRECT) {
+          // direct 128-bit stores: each lane writes its row's 32 consecutive
+          // floats (one full 128-byte line per row and chunk)
+#pragma unroll
+          for (int j = 0; j < 32; ++j) rsum += vals[j];
+          float* dst = nullptr;
+          if (MODE == kModePacked) {
+            if (store_ok) dst = args.out + (out_row0 + lane) * 128 + ch * 32;
+          } else if (lr < args.rows && col0 < args.lda) {
+            dst = args.out + lr * args.lda + col0;
+          }
+          if (dst != nullptr) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              *reinterpret_cast<float4*>(dst + 4 * j) =
+                  make_float4(vals[4 * j], vals[4 * j + 1], vals[4 * j + 2], vals[4 * j + 3]);
+          }
         } else {
 #pragma unroll
           for (int j = 0; j < 32; ++j) rsum += vals[j];
@@ -420,7 +443,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
-    if (MODE != kModeMatvec && lane == 0) tma_store_wait_all();
+    if (MODE != kModeMatvec && !DIRECT && lane == 0) tma_store_wait_all();
     __syncwarp();
   }
 
@@ -464,7 +487,7 @@ bool make_map(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t outer,
 
 int g_num_sms = 0;
 
-template <int KB, int MODE>
+template <int KB, int MODE, bool DIRECT>
 int launch_kb(const CUtensorMap& mh, const CUtensorMap& ml, const CUtensorMap& mo,
               const TcArgs& a0, cudaStream_t s) {
   constexpr int MB = mblocks(KB);
@@ -473,9 +496,9 @@ int launch_kb(const CUtensorMap& mh, const CUtensorMap& ml, const CUtensorMap& m
   a.n_chunks = ceil_div(a.n_ctiles, kChunkTiles);
   static bool attr = false;
   if (!attr) {
-    GPIC_CUDA_TRY(cudaFuncSetAttribute(affinity_tc_kernel<KB, MODE>,
+    GPIC_CUDA_TRY(cudaFuncSetAttribute(affinity_tc_kernel<KB, MODE, DIRECT>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       smem_bytes(KB, MODE)));
+                                       smem_bytes(KB, MODE, DIRECT)));
     attr = true;
   }
   if (g_num_sms == 0) {
@@ -486,20 +509,37 @@ int launch_kb(const CUtensorMap& mh, const CUtensorMap& ml, const CUtensorMap& m
   const int64_t total = total_units<MB, MODE>(a);
   const int grid = (int)(total < g_num_sms ? total : g_num_sms);
   if (grid < 1) return GPIC_OK;
-  affinity_tc_kernel<KB, MODE><<<grid, kThreads, smem_bytes(KB, MODE), s>>>(mh, ml, mo, a);
+  affinity_tc_kernel<KB, MODE, DIRECT><<<grid, kThreads, smem_bytes(KB, MODE, DIRECT), s>>>(
+      mh, ml, mo, a);
   count_launch();
   GPIC_CUDA_TRY(cudaGetLastError());
   return GPIC_OK;
 }
 
+// Epilogue store path: TMA bulk-tensor stores from swizzled smem staging
+// (default) or direct 128-bit st.global from registers (GPIC_TC_DIRECT=1).
+bool direct_stores() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("GPIC_TC_DIRECT");
+    v = (e != nullptr && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+
 template <int MODE>
 int dispatch_kb(int KB, const CUtensorMap& mh, const CUtensorMap& ml, const CUtensorMap& mo,
                 const TcArgs& args, cudaStream_t s) {
+  const bool direct = MODE != kModeMatvec && direct_stores();
   switch (KB) {
-    case 1: return launch_kb<1, MODE>(mh, ml, mo, args, s);
-    case 2: return launch_kb<2, MODE>(mh, ml, mo, args, s);
-    case 3: return launch_kb<3, MODE>(mh, ml, mo, args, s);
-    default: return launch_kb<4, MODE>(mh, ml, mo, args, s);
+    case 1: return direct ? launch_kb<1, MODE, true>(mh, ml, mo, args, s)
+                          : launch_kb<1, MODE, false>(mh, ml, mo, args, s);
+    case 2: return direct ? launch_kb<2, MODE, true>(mh, ml, mo, args, s)
+                          : launch_kb<2, MODE, false>(mh, ml, mo, args, s);
+    case 3: return direct ? launch_kb<3, MODE, true>(mh, ml, mo, args, s)
+                          : launch_kb<3, MODE, false>(mh, ml, mo, args, s);
+    default: return direct ? launch_kb<4, MODE, true>(mh, ml, mo, args, s)
+                           : launch_kb<4, MODE, false>(mh, ml, mo, args, s);
   }
 }
 
@@ -537,6 +577,7 @@ int launch_affinity_tc_packed(const float* xhi, const float* xlo, const float* s
   args.rows = n;
   args.ns = neg_scale_log2;
   args.n_ctiles = ceil_div(n, kBN);
+  args.out = a_packed;
   return dispatch_kb<kModePacked>(dp / kKBlk, mh, ml, mo, args, s);
 }
 
@@ -558,6 +599,8 @@ int launch_affinity_tc(const float* xhi, const float* xlo, const float* sqn, int
   args.rowpart = rowpart;
   args.rows_pad = rows_pad;
   args.n_ctiles = ceil_div(n, kBN);
+  args.out = a;
+  args.lda = lda;
   return dispatch_kb<kModeDense>(dp / kKBlk, mh, ml, mo, args, s);
 }
 
