@@ -91,6 +91,8 @@ struct TcArgs {
   const gpic_ctl* ctl;  // matvec in a loop: exit at once when ctl->stop is set
   float* out;        // DIRECT stores: dense A rows (pitch lda) or packed tiles
   int64_t lda;
+  float* degrow;     // packed: [tile][halves][128] row partials of each stored tile
+  float* degcol;     // packed: [tile][4 row quadrants][128] column partials
 };
 
 __host__ __device__ inline int64_t packed_items(int64_t nrt, int64_t nct, int mb) {
@@ -224,6 +226,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t a_par = 1;
       int s = 0;
       uint32_t ph = 0;
+      // the operands (MBs) are re-read by every CTA: keep them in L2 against
+      // the GB-scale output stream
+      const uint64_t keep = policy_evict_last();
       Cursor<MB, MODE> c;
       for (c.begin(args, u_begin, u_end); c.valid(); c.next(args)) {
         if (c.rb != cur_rb) {
@@ -234,14 +239,16 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int m = 0; m < MB; ++m)
               for (int kb = 0; kb < KB; ++kb)
                 tma_load_2d(sA + ((hl * MB + m) * KB + kb) * kTileBytes, hl ? &map_lo : &map_hi,
-                            kb * kKBlk, (int)(args.row_lo + (c.rb * MB + m) * 128), a_full);
+                            kb * kKBlk, (int)(args.row_lo + (c.rb * MB + m) * 128), a_full, keep);
           cur_rb = c.rb;
         }
         for (int kb = 0; kb < KB; ++kb) {
           mbar_wait(&empty[s], ph ^ 1);
           mbar_expect_tx(&full[s], 2 * kTileBytes);
-          tma_load_2d(sB + (s * 2 + 0) * kTileBytes, &map_hi, kb * kKBlk, (int)(c.cb * kBN), &full[s]);
-          tma_load_2d(sB + (s * 2 + 1) * kTileBytes, &map_lo, kb * kKBlk, (int)(c.cb * kBN), &full[s]);
+          tma_load_2d(sB + (s * 2 + 0) * kTileBytes, &map_hi, kb * kKBlk, (int)(c.cb * kBN), &full[s],
+                      keep);
+          tma_load_2d(sB + (s * 2 + 1) * kTileBytes, &map_lo, kb * kKBlk, (int)(c.cb * kBN), &full[s],
+                      keep);
           if (++s == ST) { s = 0; ph ^= 1; }
         }
       }
@@ -305,6 +312,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint8_t* stage0 = sOut + e * (NBUF > 0 ? NBUF : 1) * kStageOutBytes;
     const float ns = args.ns;
     const float m2ns = -2.f * ns;
+    const uint64_t stream_pol = policy_evict_first();  // A is written once here
     uint32_t tf_bits = 0;  // TMEM-full parity per accumulator buffer
     int i = 0;
     int stores = 0;
@@ -417,11 +425,35 @@ __global__ void __launch_bounds__(kThreads, 1)
           fence_async_smem();
           __syncwarp();
           if (lane == 0 && store_ok)
-            tma_store_2d(&map_out, MODE == kModePacked ? ch * 32 : (int)col0, (int)out_row0, stage);
+            tma_store_2d(&map_out, MODE == kModePacked ? ch * 32 : (int)col0, (int)out_row0, stage,
+                         stream_pol);
           ++stores;
+          if (MODE == kModePacked && store_ok && tI != cb) {
+            // degrees of the tile's COLUMN rows (A is symmetric): lane l sums
+            // column l of the staged 32x32 chunk over this warp's 32 rows
+            // (row r of the swizzled stage: chunk (l/4) ^ (r & 7)), fixed order
+            const uint32_t sb = su32(stage) + (lane & 3) * 4;
+            float cs = 0.f;
+#pragma unroll
+            for (int r2 = 0; r2 < 32; ++r2) {
+              float x;
+              asm volatile("ld.shared.f32 %0, [%1];"
+                           : "=f"(x)
+                           : "r"(sb + r2 * 128 + ((((lane >> 2) ^ (r2 & 7))) << 4)));
+              cs += x;
+            }
+            args.degcol[(tile_index(tI, cb, args.n_ctiles) * 4 + q) * 128 + ch * 32 + lane] = cs;
+          }
         }
       }
-      if constexpr (MODE == kModeMatvec) {
+      if constexpr (MODE == kModePacked) {
+        // degrees of the tile's ROW rows: this warp's partial over its chunks
+        if (store_ok) {
+          constexpr int NH = MB == 2 ? 1 : 2;  // column halves per row
+          args.degrow[(tile_index(tI, cb, args.n_ctiles) * NH + (MB == 2 ? 0 : g)) * 128 + q * 32 +
+                      lane] = rsum;
+        }
+      } else if constexpr (MODE == kModeMatvec) {
         acc64 += (double)rsum;
         if (item_last) {
           // MB=2: one partial per (chunk, row); MB=1: one per (chunk, half, row)
@@ -530,7 +562,8 @@ bool direct_stores() {
 template <int MODE>
 int dispatch_kb(int KB, const CUtensorMap& mh, const CUtensorMap& ml, const CUtensorMap& mo,
                 const TcArgs& args, cudaStream_t s) {
-  const bool direct = MODE != kModeMatvec && direct_stores();
+  // (packed mode derives the column degrees from the smem stage: staging only)
+  const bool direct = MODE == kModeDense && direct_stores();
   switch (KB) {
     case 1: return direct ? launch_kb<1, MODE, true>(mh, ml, mo, args, s)
                           : launch_kb<1, MODE, false>(mh, ml, mo, args, s);
@@ -564,8 +597,11 @@ int64_t packed_tiles(int64_t n) {
 
 // Symmetric packed output: tile (I, J), J >= I, stored as a contiguous
 // 128 x 128 fp32 block at tile_index(I, J) (row-major over the triangle).
+int packed_row_halves(int32_t dp) { return mblocks(dp / kKBlk) == 2 ? 1 : 2; }
+
 int launch_affinity_tc_packed(const float* xhi, const float* xlo, const float* sqn, int64_t n,
-                              int32_t dp, float neg_scale_log2, float* a_packed, cudaStream_t s) {
+                              int32_t dp, float neg_scale_log2, float* a_packed, float* degrow,
+                              float* degcol, cudaStream_t s) {
   CUtensorMap mh, ml, mo;
   int rc = operand_maps(xhi, xlo, n, dp, &mh, &ml);
   if (rc) return rc;
@@ -578,6 +614,8 @@ int launch_affinity_tc_packed(const float* xhi, const float* xlo, const float* s
   args.ns = neg_scale_log2;
   args.n_ctiles = ceil_div(n, kBN);
   args.out = a_packed;
+  args.degrow = degrow;
+  args.degcol = degcol;
   return dispatch_kb<kModePacked>(dp / kKBlk, mh, ml, mo, args, s);
 }
 

@@ -282,8 +282,8 @@ int64_t gpic_cluster_workspace_bytes(int64_t n, int32_t d, int32_t k, int32_t ma
                                      int32_t storage) {
   if (n < 1 || d < 1) return -1;
   const int64_t scratch = workspace_bytes(n, d, k, n, max_iter);
-  if (storage == GPIC_STORAGE_PACKED)
-    return scratch + packed_tiles(n) * 128 * 128 * 4 + 2 * al(sym_partial_floats(n) * 4);
+  if (storage == GPIC_STORAGE_PACKED)  // tiles + GEMV partials (2) + degree partials (<= 2 + 4)
+    return scratch + packed_tiles(n) * 128 * 128 * 4 + 8 * al(sym_partial_floats(n) * 4);
   if (storage == GPIC_STORAGE_NONE)
     return scratch + al(mf_ypart_doubles(n, feature_pitch(d), n) * 8);
   return scratch + n * affinity_pitch(n) * 4;
@@ -330,17 +330,15 @@ int gpic_cluster(const double* d_x, int64_t n, int32_t d, double sigma, int32_t 
   if (storage == GPIC_STORAGE_PACKED) {
     float* rowp = a + packed_tiles(n) * 128 * 128;
     float* colp = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(rowp) + al(sym_partial_floats(n) * 4));
-    rc = launch_affinity_tc_packed(ws.xhi, ws.xlo, ws.sqn, n, dp, neg_scale_log2, a, s);
+    // degree partials from the affinity epilogue (row sums + column sums of
+    // every stored tile, consistent with the stored fp32 values)
+    const int64_t pf = al(sym_partial_floats(n) * 4) / 4;
+    float* degrow = colp + pf;
+    float* degcol = degrow + 2 * pf;
+    rc = launch_affinity_tc_packed(ws.xhi, ws.xlo, ws.sqn, n, dp, neg_scale_log2, a, degrow,
+                                   degcol, s);
     if (rc) return rc;
-    // degrees = A 1 through the same symmetric GEMV (consistent with the stored values)
-    fill_ones_kernel<<<(unsigned)ceil_div(vector_pitch(n), 256), 256, 0, s>>>(ws.v32, n, vector_pitch(n));
-    PeerTable pt;
-    std::memset(&pt, 0, sizeof pt);
-    pt.y[0][0] = pt.y[0][1] = deg;
-    pt.nranks = 1;
-    launch_sym_gemv(a, n, ws.v32, rowp, colp, nullptr, pt, nullptr, s);
-    zero_check_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, s>>>(deg, n, ws.ctl);
-    count_launch(2);
+    launch_sym_degree(degrow, degcol, n, packed_row_halves(dp), deg, ws.ctl, s);
     L.mode = kLoopPacked;
     L.rowp = rowp;
     L.colp = colp;

@@ -58,6 +58,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane != 0) return;
     int s = 0;
     uint32_t ph = 0;
+    const uint64_t once = policy_evict_first(), keep = policy_evict_last();
     for (int64_t g = blockIdx.x; g < groups; g += gridDim.x) {
       const int64_t r0 = g * kRG;
       const int nr = (int)min((int64_t)kRG, rows - r0);
@@ -67,9 +68,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&empty[s], ph ^ 1);
         mbar_expect_tx(&full[s], (uint32_t)(nr + 1) * cw * 4u);
         float* dst = st + s * kStageFloats;
-        bulk_load(dst + kRG * kCW, v32 + c0, cw * 4u, &full[s]);
+        bulk_load(dst + kRG * kCW, v32 + c0, cw * 4u, &full[s], keep);
         for (int r = 0; r < nr; ++r)
-          bulk_load(dst + r * kCW, a + (r0 + r) * lda + c0, cw * 4u, &full[s]);
+          bulk_load(dst + r * kCW, a + (r0 + r) * lda + c0, cw * 4u, &full[s], once);
         if (++s == kStages) { s = 0; ph ^= 1; }
       }
     }

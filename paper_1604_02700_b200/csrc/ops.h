@@ -25,8 +25,16 @@ inline int64_t vector_pitch(int64_t n) { return round_up(n, 128); }
 // ---- symmetric packed storage (affinity_tc.cu, sym.cu) -------------------
 int64_t packed_tiles(int64_t n);        // nt (nt + 1) / 2, nt = ceil(n / 128)
 int64_t sym_partial_floats(int64_t n);  // packed_tiles(n) * 128
+// Packed affinity; the epilogue also leaves per-tile degree partials:
+// degrow [tile][packed_row_halves(dp)][128] (row sums of the stored tile)
+// and degcol [tile][4][128] (column sums per 32-row quadrant, off-diagonal
+// tiles), combined by launch_sym_degree.
+int packed_row_halves(int32_t dp);
 int launch_affinity_tc_packed(const float* xhi, const float* xlo, const float* sqn, int64_t n,
-                              int32_t dp, float neg_scale_log2, float* a_packed, cudaStream_t s);
+                              int32_t dp, float neg_scale_log2, float* a_packed, float* degrow,
+                              float* degcol, cudaStream_t s);
+void launch_sym_degree(const float* degrow, const float* degcol, int64_t n, int nhalf,
+                       double* deg, gpic_ctl* ctl, cudaStream_t s);
 void sym_prepare();
 
 // Workspace carve-up (see capi.cu).

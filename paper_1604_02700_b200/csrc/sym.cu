@@ -73,10 +73,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane != 0) return;
     int s = 0;
     uint32_t ph = 0;
+    const uint64_t once = policy_evict_first();  // every tile is read once per pass
     for (int64_t t = t0; t < t1; ++t) {
       mbar_wait(&empty[s], ph ^ 1);
       mbar_expect_tx(&full[s], kTileFloats * 4);
-      bulk_load(st + s * kTileFloats, tiles + t * kTileFloats, kTileFloats * 4, &full[s]);
+      bulk_load(st + s * kTileFloats, tiles + t * kTileFloats, kTileFloats * 4, &full[s], once);
       if (++s == kStages) { s = 0; ph ^= 1; }
     }
     return;
@@ -210,9 +211,49 @@ __global__ void __launch_bounds__(kTS * kSeg)
   }
 }
 
+// deg_i from the affinity epilogue's partials (same segmented fixed shape as
+// sym_reduce): column partials (4 row quadrants) of tiles (p, R), p < R,
+// then row partials (nhalf column halves) of tiles (R, p), p >= R.
+__global__ void __launch_bounds__(kTS * kSeg)
+    sym_degree_kernel(const float* __restrict__ degrow, const float* __restrict__ degcol,
+                      int64_t n, int64_t nt, int nhalf, double* __restrict__ deg, gpic_ctl* ctl) {
+  __shared__ double part[kSeg][kTS];
+  const int64_t R = blockIdx.x;
+  const int o = threadIdx.x % kTS, sg = threadIdx.x / kTS;
+  const int64_t p0 = nt * sg / kSeg, p1 = nt * (sg + 1) / kSeg;
+  double s = 0.0;
+  for (int64_t p = p0; p < p1; ++p) {
+    if (p < R) {
+      const float* c = degcol + tile_index(p, R, nt) * 4 * kTS + o;
+      s += (double)c[0] + (double)c[kTS] + (double)c[2 * kTS] + (double)c[3 * kTS];
+    } else {
+      const float* r = degrow + tile_index(R, p, nt) * nhalf * kTS + o;
+      s += (double)r[0];
+      if (nhalf == 2) s += (double)r[kTS];
+    }
+  }
+  part[sg][o] = s;
+  __syncthreads();
+  const int64_t i = R * kTS + o;
+  if (sg == 0 && i < n) {
+    double t = 0.0;
+#pragma unroll
+    for (int q = 0; q < kSeg; ++q) t += part[q][o];
+    deg[i] = t;
+    if (t <= 0.0) raise_status(ctl, GPIC_E_ZERO_DEGREE, i, -1, t);
+  }
+}
+
 int g_sms = 0;
 
 }  // namespace
+
+void launch_sym_degree(const float* degrow, const float* degcol, int64_t n, int nhalf,
+                       double* deg, gpic_ctl* ctl, cudaStream_t s) {
+  const int64_t nt = ceil_div(n, kTS);
+  sym_degree_kernel<<<(unsigned)nt, kTS * kSeg, 0, s>>>(degrow, degcol, n, nt, nhalf, deg, ctl);
+  count_launch();
+}
 
 void sym_prepare() {
   if (g_sms == 0) {
