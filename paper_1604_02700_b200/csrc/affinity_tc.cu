@@ -433,16 +433,17 @@ __global__ void __launch_bounds__(kThreads, 1)
             // column l of the staged 32x32 chunk over this warp's 32 rows
             // (row r of the swizzled stage: chunk (l/4) ^ (r & 7)), fixed order
             const uint32_t sb = su32(stage) + (lane & 3) * 4;
-            float cs = 0.f;
+            float cs[4] = {0.f, 0.f, 0.f, 0.f};  // 4 chains: rows r2 = 4u + w
 #pragma unroll
             for (int r2 = 0; r2 < 32; ++r2) {
               float x;
               asm volatile("ld.shared.f32 %0, [%1];"
                            : "=f"(x)
                            : "r"(sb + r2 * 128 + ((((lane >> 2) ^ (r2 & 7))) << 4)));
-              cs += x;
+              cs[r2 & 3] += x;
             }
-            args.degcol[(tile_index(tI, cb, args.n_ctiles) * 4 + q) * 128 + ch * 32 + lane] = cs;
+            args.degcol[(tile_index(tI, cb, args.n_ctiles) * 4 + q) * 128 + ch * 32 + lane] =
+                (cs[0] + cs[1]) + (cs[2] + cs[3]);
           }
         }
       }
