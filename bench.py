@@ -234,7 +234,7 @@ def _gemv_roofline(args, L, C, torch, stream, st, n, m, k, T, work, v, storage):
 
         def launch():
             return L.gpic_mf_degrees(C.c_void_p(xhi), C.c_void_p(xlo), C.c_void_p(sqn), n, m, 0, n,
-                                     sigma, C.c_void_p(ones.data_ptr()),
+                                     sigma, _lib.KIND_RBF, C.c_void_p(ones.data_ptr()),
                                      C.c_void_p(ypart.data_ptr()), C.c_void_p(yv.data_ptr()), st)
         alg = 3.0 * 2.0 * n * n * dp
         name = "affinity_tc_kernel<matvec> (matrix-free A v: 3xTF32 Gram + exp + v)"
@@ -317,7 +317,7 @@ def run_ours(args, cfg, rank, world):
     iters, conv = C.c_int32(0), C.c_int32(0)
 
     def step():
-        rc = L.gpic_cluster(C.c_void_p(x.data_ptr()), n, m, sigma, k, eps, T, first,
+        rc = L.gpic_cluster(C.c_void_p(x.data_ptr()), n, m, sigma, _lib.KIND_RBF, k, eps, T, first,
                             u.ctypes.data_as(C.c_void_p), impl, storage,
                             C.c_void_p(labels.data_ptr()), C.c_void_p(v.data_ptr()),
                             C.c_void_p(hist.data_ptr()), C.byref(iters), C.byref(conv),
@@ -425,7 +425,7 @@ def run_ours_sharded(args, cfg, rank, world):
     stream = torch.cuda.current_stream(dev)
     L = _lib.lib()
     for _ in range(args.warmup):
-        runner.run(x, sigma, params, 0)
+        runner.run(x, GaussianRbf(sigma), params, 0)
     torch.cuda.synchronize()
     dist.barrier()
     launches0 = L.gpic_launch_count()
@@ -435,7 +435,7 @@ def run_ours_sharded(args, cfg, rank, world):
         dist.barrier()
         ev0.record(stream)
         for _ in range(args.steps):
-            labels, v, trace = runner.run(x, sigma, params, 0)
+            labels, v, trace = runner.run(x, GaussianRbf(sigma), params, 0)
         ev1.record(stream)
         torch.cuda.synchronize()
     dist.barrier()
@@ -454,7 +454,7 @@ def run_ours_sharded(args, cfg, rank, world):
     for _ in range(max(1, args.e2e_steps)):
         dist.barrier()
         t0 = time.perf_counter()
-        lab_e, v_e, _ = runner.run(d_host, sigma, params, 0)
+        lab_e, v_e, _ = runner.run(d_host, GaussianRbf(sigma), params, 0)
         lab_e, v_e = lab_e.cpu().numpy(), v_e.cpu().numpy()
         e2e.append(time.perf_counter() - t0)
     te = torch.tensor([statistics.mean(e2e)], device=dev)

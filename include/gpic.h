@@ -45,6 +45,11 @@ extern "C" {
 #define GPIC_E_CUDA 16
 #define GPIC_E_COMM 17
 #define GPIC_E_UNSUPPORTED 18
+#define GPIC_E_ZERO_VECTOR 7 /* ZeroVector(index), cosine kind (affinity.py:41-53) */
+
+/* Similarity kinds (affinity.py:22-35). */
+#define GPIC_KIND_RBF 0    /* GaussianRbf(sigma): exp(-|x-y|^2 / 2 sigma^2) */
+#define GPIC_KIND_COSINE 1 /* Cosine(): max(0, x.y / (|x||y|)), sigma ignored */
 
 /* Affinity engines (KernelConfig.affinity_impl). */
 #define GPIC_AFFINITY_TC 0   /* tcgen05 kind::tf32, 3xTF32 split, TMEM accumulators */
@@ -86,11 +91,14 @@ int64_t gpic_affinity_pitch(int64_t n);
  * the fp32 operands of the Gram engine: xc = fp32(x - mean_fp64), its
  * TF32 hi/lo split, and |xc|^2. A non-finite entry sets GPIC_E_NONFINITE
  * with the first (row, col) in row-major order. Layout: d_xhi/d_xlo are
- * (n_pad x dp) row-major, dp = gpic_feature_pitch(d), n_pad = gpic_row_pad(n). */
+ * (n_pad x dp) row-major, dp = gpic_feature_pitch(d), n_pad = gpic_row_pad(n).
+ * kind GPIC_KIND_COSINE instead scales every row to unit length in fp64
+ * (no centring: cosine is not translation invariant) and reports a zero
+ * row as GPIC_E_ZERO_VECTOR(first row) (cosine_norms, affinity.py:41-53). */
 int32_t gpic_feature_pitch(int32_t d);
 int64_t gpic_row_pad(int64_t n);
-int gpic_prepare_points(const double* d_x, int64_t n, int32_t d, float* d_xhi, float* d_xlo,
-                        float* d_sqn, void* d_work, gpic_ctl* d_ctl, void* stream);
+int gpic_prepare_points(const double* d_x, int64_t n, int32_t d, int32_t kind, float* d_xhi,
+                        float* d_xlo, float* d_sqn, void* d_work, gpic_ctl* d_ctl, void* stream);
 
 /* ---- stage 1: affinity block + degree ---------------------------------
  * Replaces similarity_rows/build_affinity (affinity.py:74-110, RBF kind),
@@ -107,6 +115,11 @@ int gpic_affinity_rbf(const float* d_xhi, const float* d_xlo, const float* d_sqn
                       int32_t d, int64_t row_lo, int64_t row_hi, double sigma, int32_t impl,
                       float* d_a, int64_t lda, double* d_deg, void* d_work, gpic_ctl* d_ctl,
                       void* stream);
+/* Same for the cosine kind (affinity.py:88-95): A_ij = max(0, cos(x_i, x_j))
+ * on points prepared with GPIC_KIND_COSINE. */
+int gpic_affinity_cosine(const float* d_xhi, const float* d_xlo, const float* d_sqn, int64_t n,
+                         int32_t d, int64_t row_lo, int64_t row_hi, int32_t impl, float* d_a,
+                         int64_t lda, double* d_deg, void* d_work, gpic_ctl* d_ctl, void* stream);
 
 /* ---- stage 2: start vector -----------------------------------------------
  * initial_embedding "degree" choice (parallel.py:210-214 = k_norm(deg,
@@ -177,21 +190,21 @@ int64_t gpic_vector_pitch(int64_t n);
 int64_t gpic_packed_tiles(int64_t n);
 int64_t gpic_cluster_workspace_bytes(int64_t n, int32_t d, int32_t k, int32_t max_iter,
                                      int32_t storage);
-int gpic_cluster(const double* d_x, int64_t n, int32_t d, double sigma, int32_t k, double eps,
-                 int32_t max_iter, int64_t first_index, const double* h_uniforms, int32_t impl,
-                 int32_t storage, int64_t* d_labels, double* d_v, double* d_delta_hist,
-                 int32_t* h_iters, int32_t* h_converged, void* d_work, int64_t work_bytes,
-                 void* stream);
+int gpic_cluster(const double* d_x, int64_t n, int32_t d, double sigma, int32_t kind, int32_t k,
+                 double eps, int32_t max_iter, int64_t first_index, const double* h_uniforms,
+                 int32_t impl, int32_t storage, int64_t* d_labels, double* d_v,
+                 double* d_delta_hist, int32_t* h_iters, int32_t* h_converged, void* d_work,
+                 int64_t work_bytes, void* stream);
 
 /* Same, HOST buffers in and out (the reference-facing call a ctypes/cffi
  * binding makes): copies X in, runs, copies labels/v/deltas out. d_work
  * must hold gpic_cluster_workspace_bytes(...) (256-aligned) + the staging
  * of X (n*d*8), labels and v (n*8 each) and the deltas (max_iter*8). */
-int gpic_cluster_host(const double* h_x, int64_t n, int32_t d, double sigma, int32_t k,
-                      double eps, int32_t max_iter, int64_t first_index, const double* h_uniforms,
-                      int32_t impl, int32_t storage, int64_t* h_labels, double* h_v,
-                      double* h_delta_hist, int32_t* h_iters, int32_t* h_converged, void* d_work,
-                      int64_t work_bytes, void* stream);
+int gpic_cluster_host(const double* h_x, int64_t n, int32_t d, double sigma, int32_t kind,
+                      int32_t k, double eps, int32_t max_iter, int64_t first_index,
+                      const double* h_uniforms, int32_t impl, int32_t storage, int64_t* h_labels,
+                      double* h_v, double* h_delta_hist, int32_t* h_iters, int32_t* h_converged,
+                      void* d_work, int64_t work_bytes, void* stream);
 
 /* Reset a control block (iteration 0, no error) with the stop threshold and
  * iteration cap of the run. */
@@ -243,6 +256,7 @@ typedef struct gpic_shard {
   const float* xlo;
   const float* sqn;
   double sigma;
+  int32_t kind;       /* GPIC_KIND_*                                          */
   double* ypart;      /* gpic_mf_ypart_doubles(n, d, rows) doubles          */
 } gpic_shard;
 
@@ -251,8 +265,8 @@ typedef struct gpic_shard {
  * of scratch; d_ypart: gpic_mf_ypart_doubles(n, d, rows) doubles. */
 int64_t gpic_mf_ypart_doubles(int64_t n, int32_t d, int64_t rows);
 int gpic_mf_degrees(const float* d_xhi, const float* d_xlo, const float* d_sqn, int64_t n,
-                    int32_t d, int64_t row_lo, int64_t row_hi, double sigma, float* d_ones,
-                    double* d_ypart, double* d_deg, void* stream);
+                    int32_t d, int64_t row_lo, int64_t row_hi, double sigma, int32_t kind,
+                    float* d_ones, double* d_ypart, double* d_deg, void* stream);
 
 int gpic_comm_create(int32_t nranks, int32_t rank, int64_t n, gpic_comm** out,
                      uint8_t* h_ipc_handle);

@@ -62,13 +62,40 @@ def rbf_rows(points: np.ndarray, lo: int, hi: int, sigma: float) -> np.ndarray:
     return out
 
 
-def affinity(points: np.ndarray, sigma: float) -> np.ndarray:
-    """Full A (affinity.py:107-110 build_affinity, RBF kind)."""
+def cosine_rows(points: np.ndarray, lo: int, hi: int) -> np.ndarray:
+    """Rows [lo, hi) of A_ij = max(0, x_i.x_j / (|x_i||x_j|)), A_ii = 0.
+
+    Restates affinity.py:41-53 (norms accumulated feature by feature,
+    ZeroVector(first i) for a zero row) and :88-95,102-103.
+    """
+    x = np.asarray(points, dtype=np.float64)
+    n, m = x.shape
+    sq = np.zeros(n)
+    for f in range(m):
+        sq += x[:, f] * x[:, f]
+    zero = np.flatnonzero(sq == 0.0)
+    if zero.size:
+        raise OracleError("ZeroVector", int(zero[0]))
+    norms = np.sqrt(sq)
+    dots = np.zeros((hi - lo, n))
+    for f in range(m):
+        dots += x[lo:hi, f, None] * x[None, :, f]
+    out = dots / (norms[lo:hi, None] * norms[None, :])
+    np.maximum(out, 0.0, out=out)
+    rows = np.arange(lo, hi)
+    out[rows - lo, rows] = 0.0
+    return out
+
+
+def affinity(points: np.ndarray, sigma: float | None) -> np.ndarray:
+    """Full A (affinity.py:107-110 build_affinity): RBF, or cosine when sigma is None."""
     x = np.asarray(points, dtype=np.float64)
     bad = ~np.isfinite(x)
     if bad.any():  # data.py:69-72 NonFiniteEntry(row, col) of the first bad entry
         r, c = np.argwhere(bad)[0]
         raise OracleError("NonFiniteEntry", (int(r), int(c)))
+    if sigma is None:
+        return cosine_rows(x, 0, x.shape[0])
     return rbf_rows(x, 0, x.shape[0], sigma)
 
 

@@ -20,6 +20,10 @@ GPIC_E_NONFINITE = 3
 GPIC_E_NONPOS_TAU = 4
 GPIC_E_EMPTY = 5
 GPIC_E_K_TOO_LARGE = 6
+GPIC_E_ZERO_VECTOR = 7
+
+KIND_RBF = 0
+KIND_COSINE = 1
 GPIC_E_CUDA = 16
 GPIC_E_COMM = 17
 GPIC_E_UNSUPPORTED = 18
@@ -70,8 +74,9 @@ SIGNATURES = {
     "gpic_feature_pitch": (I32, [I32]),
     "gpic_row_pad": (I64, [I64]),
     "gpic_ctl_init": (C.c_int, [P, F64, I32, P]),
-    "gpic_prepare_points": (C.c_int, [P, I64, I32, P, P, P, P, P, P]),
+    "gpic_prepare_points": (C.c_int, [P, I64, I32, I32, P, P, P, P, P, P]),
     "gpic_affinity_rbf": (C.c_int, [P, P, P, I64, I32, I64, I64, F64, I32, P, I64, P, P, P, P]),
+    "gpic_affinity_cosine": (C.c_int, [P, P, P, I64, I32, I64, I64, I32, P, I64, P, P, P, P]),
     "gpic_initial_vector": (C.c_int, [P, I64, P, P, P, P, P]),
     "gpic_power_iterate": (C.c_int, [P, I64, P, I64, P, P, F64, I32, P, P, P, P, P]),
     "gpic_kmeans1d": (C.c_int, [P, I64, I32, I64, P, I32, F64, P, P, P, P]),
@@ -82,13 +87,13 @@ SIGNATURES = {
     "gpic_packed_tiles": (I64, [I64]),
     "gpic_vector_pitch": (I64, [I64]),
     "gpic_mf_ypart_doubles": (I64, [I64, I32, I64]),
-    "gpic_mf_degrees": (C.c_int, [P, P, P, I64, I32, I64, I64, F64, P, P, P, P]),
+    "gpic_mf_degrees": (C.c_int, [P, P, P, I64, I32, I64, I64, F64, I32, P, P, P, P]),
     "gpic_sym_matvec": (C.c_int, [P, I64, P, P, P, P, P, P]),
     "gpic_cluster_workspace_bytes": (I64, [I64, I32, I32, I32, I32]),
-    "gpic_cluster": (C.c_int, [P, I64, I32, F64, I32, F64, I32, I64, P, I32, I32, P, P, P, P, P,
-                               P, I64, P]),
-    "gpic_cluster_host": (C.c_int, [P, I64, I32, F64, I32, F64, I32, I64, P, I32, I32, P, P, P,
-                                    P, P, P, I64, P]),
+    "gpic_cluster": (C.c_int, [P, I64, I32, F64, I32, I32, F64, I32, I64, P, I32, I32, P, P, P,
+                               P, P, P, I64, P]),
+    "gpic_cluster_host": (C.c_int, [P, I64, I32, F64, I32, I32, F64, I32, I64, P, I32, I32, P, P,
+                                    P, P, P, P, I64, P]),
     "gpic_ctl_read": (C.c_int, [P, P, P]),
     "gpic_launch_count": (I64, []),
     "gpic_comm_create": (C.c_int, [I32, I32, I64, P, P]),
@@ -109,7 +114,7 @@ class Shard(C.Structure):
     _fields_ = [("a", C.c_void_p), ("lda", C.c_int64), ("deg", C.c_void_p),
                 ("row_lo", C.c_int64), ("rows", C.c_int64), ("storage", C.c_int32),
                 ("d", C.c_int32), ("xhi", C.c_void_p), ("xlo", C.c_void_p), ("sqn", C.c_void_p),
-                ("sigma", C.c_double), ("ypart", C.c_void_p)]
+                ("sigma", C.c_double), ("kind", C.c_int32), ("ypart", C.c_void_p)]
 
 _lib = None
 
@@ -149,6 +154,8 @@ def raise_for(code: int, ctl: Ctl | None = None, d: int = 1) -> None:
         raise errors.NonFiniteEntry(idx // max(d, 1), idx % max(d, 1))
     if code == GPIC_E_NONPOS_TAU:
         raise errors.NonPositiveTau(ctl.err_value if ctl is not None else float("nan"))
+    if code == GPIC_E_ZERO_VECTOR:
+        raise errors.ZeroVector(ctl.err_index if ctl is not None else -1)
     if code == GPIC_E_EMPTY:
         raise errors.EmptyDataSet()
     if code == GPIC_E_K_TOO_LARGE:

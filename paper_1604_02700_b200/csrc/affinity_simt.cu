@@ -23,7 +23,7 @@ __global__ void __launch_bounds__(256, 2)
     affinity_simt_kernel(const float* __restrict__ xhi, const float* __restrict__ xlo,
                          const float* __restrict__ sqn, int64_t n, int32_t dp, int64_t row_lo,
                          int64_t row_hi, float neg_scale_log2, float* __restrict__ a, int64_t lda,
-                         float* __restrict__ rowpart, int64_t rows_pad) {
+                         float* __restrict__ rowpart, int64_t rows_pad, int kind) {
   __shared__ __align__(16) float As[BK][BM + PADS];
   __shared__ __align__(16) float Bs[BK][BN + PADS];
 
@@ -96,8 +96,13 @@ __global__ void __launch_bounds__(256, 2)
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       const int64_t cj = col0 + (j < 4 ? tx * 4 + j : 64 + tx * 4 + (j - 4));
-      float d2 = fmaxf(sqa + sqb[j] - 2.f * acc[i][j], 0.f);
-      float e = exp2f(d2 * neg_scale_log2);
+      float e;
+      if (kind == GPIC_KIND_COSINE) {
+        e = fmaxf(acc[i][j], 0.f);  // unit rows: the Gram entry is the cosine
+      } else {
+        const float d2 = fmaxf(sqa + sqb[j] - 2.f * acc[i][j], 0.f);
+        e = exp2f(d2 * neg_scale_log2);
+      }
       if (cj == gr || cj >= n) e = 0.f;
       vals[j] = e;
       rs += e;
@@ -135,11 +140,11 @@ __global__ void degree_kernel(const float* __restrict__ rowpart, int64_t rows, i
 void launch_affinity_simt(const float* xhi, const float* xlo, const float* sqn, int64_t n,
                           int32_t dp, int64_t row_lo, int64_t row_hi, float neg_scale_log2,
                           float* a, int64_t lda, float* rowpart, int64_t rows_pad,
-                          cudaStream_t s) {
+                          cudaStream_t s, int kind) {
   const int64_t rows = row_hi - row_lo;
   dim3 grid((unsigned)ceil_div(n, BN), (unsigned)ceil_div(rows, BM));
   affinity_simt_kernel<<<grid, 256, 0, s>>>(xhi, xlo, sqn, n, dp, row_lo, row_hi, neg_scale_log2,
-                                            a, lda, rowpart, rows_pad);
+                                            a, lda, rowpart, rows_pad, kind);
   count_launch();
 }
 

@@ -93,6 +93,7 @@ struct TcArgs {
   int64_t lda;
   float* degrow;     // packed: [tile][halves][128] row partials of each stored tile
   float* degcol;     // packed: [tile][4 row quadrants][128] column partials
+  int kind;          // GPIC_KIND_RBF: exp2 epilogue; GPIC_KIND_COSINE: max(0, G) on unit rows
 };
 
 __host__ __device__ inline int64_t packed_items(int64_t nrt, int64_t nct, int mb) {
@@ -374,11 +375,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         const bool diag = (col0 < args.row_lo + lr0 + 32) && (args.row_lo + lr0 < col0 + 32);
         const bool pad = col0 + 32 > args.n || args.row_lo + lr0 + 32 > args.n;
         float vals[32];
+        if (args.kind == GPIC_KIND_COSINE) {
+          // rows are unit vectors: G_ij = cos(x_i, x_j), clamped at 0 (affinity.py:93-94)
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const float cj = __shfl_sync(0xffffffffu, cbv[cc], j);
-          const float arg = fmaf(__uint_as_float(r[j]), m2ns, ra + cj);
-          vals[j] = ex2(fminf(arg, 0.f));
+          for (int j = 0; j < 32; ++j) vals[j] = fmaxf(__uint_as_float(r[j]), 0.f);
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const float cj = __shfl_sync(0xffffffffu, cbv[cc], j);
+            const float arg = fmaf(__uint_as_float(r[j]), m2ns, ra + cj);
+            vals[j] = ex2(fminf(arg, 0.f));
+          }
         }
         if (diag || pad) {
 #pragma unroll
@@ -573,7 +580,7 @@ int packed_row_halves(int32_t dp) { return mblocks(dp / kKBlk) == 2 ? 1 : 2; }
 
 int launch_affinity_tc_packed(const float* xhi, const float* xlo, const float* sqn, int64_t n,
                               int32_t dp, float neg_scale_log2, float* a_packed, float* degrow,
-                              float* degcol, cudaStream_t s) {
+                              float* degcol, cudaStream_t s, int kind) {
   CUtensorMap mh, ml, mo;
   int rc = operand_maps(xhi, xlo, n, dp, &mh, &ml);
   if (rc) return rc;
@@ -588,12 +595,13 @@ int launch_affinity_tc_packed(const float* xhi, const float* xlo, const float* s
   args.out = a_packed;
   args.degrow = degrow;
   args.degcol = degcol;
+  args.kind = kind;
   return dispatch_kb<kModePacked>(dp / kKBlk, mh, ml, mo, args, s);
 }
 
 int launch_affinity_tc(const float* xhi, const float* xlo, const float* sqn, int64_t n,
                        int32_t dp, int64_t row_lo, int64_t row_hi, float neg_scale_log2, float* a,
-                       int64_t lda, float* rowpart, int64_t rows_pad, cudaStream_t s) {
+                       int64_t lda, float* rowpart, int64_t rows_pad, cudaStream_t s, int kind) {
   const int64_t rows = row_hi - row_lo;
   CUtensorMap mh, ml, mo;
   int rc = operand_maps(xhi, xlo, n, dp, &mh, &ml);
@@ -611,6 +619,7 @@ int launch_affinity_tc(const float* xhi, const float* xlo, const float* sqn, int
   args.n_ctiles = ceil_div(n, kBN);
   args.out = a;
   args.lda = lda;
+  args.kind = kind;
   return dispatch_kb<kModeDense>(dp / kKBlk, mh, ml, mo, args, s);
 }
 
@@ -624,7 +633,7 @@ int64_t mf_parts(int64_t n, int32_t dp) {
 int launch_affinity_tc_matvec(const float* xhi, const float* xlo, const float* sqn, int64_t n,
                               int32_t dp, int64_t row_lo, int64_t row_hi, float neg_scale_log2,
                               const float* v32, double* ypart, int64_t rows_pad,
-                              const gpic_ctl* ctl, cudaStream_t s) {
+                              const gpic_ctl* ctl, cudaStream_t s, int kind) {
   CUtensorMap mh, ml;
   int rc = operand_maps(xhi, xlo, n, dp, &mh, &ml);
   if (rc) return rc;
@@ -639,6 +648,7 @@ int launch_affinity_tc_matvec(const float* xhi, const float* xlo, const float* s
   args.v32 = v32;
   args.ypart = ypart;
   args.ctl = ctl;
+  args.kind = kind;
   return dispatch_kb<kModeMatvec>(dp / kKBlk, mh, ml, mh, args, s);
 }
 

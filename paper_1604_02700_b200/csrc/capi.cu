@@ -97,6 +97,9 @@ static int status_from_ctl(const gpic_ctl& h, int32_t d) {
     case GPIC_E_NONPOS_TAU:
       snprintf(buf, sizeof buf, "non-positive normaliser %g", h.err_value);
       return fail(h.status, buf);
+    case GPIC_E_ZERO_VECTOR:
+      snprintf(buf, sizeof buf, "point %lld has zero norm", (long long)h.err_index);
+      return fail(h.status, buf);
     case GPIC_E_UNSUPPORTED:
       return fail(h.status, "k-means produced non-contiguous clusters (gap repair not on device)");
     default:
@@ -136,23 +139,44 @@ int gpic_ctl_init(gpic_ctl* d_ctl, double eps, int32_t max_iter, void* stream) {
   return GPIC_OK;
 }
 
-int gpic_prepare_points(const double* d_x, int64_t n, int32_t d, float* d_xhi, float* d_xlo,
-                        float* d_sqn, void* d_work, gpic_ctl* d_ctl, void* stream) {
+int gpic_prepare_points(const double* d_x, int64_t n, int32_t d, int32_t kind, float* d_xhi,
+                        float* d_xlo, float* d_sqn, void* d_work, gpic_ctl* d_ctl, void* stream) {
   if (n < 1 || d < 1) return fail(GPIC_E_EMPTY, "dataset must contain at least one point and one feature");
+  if (kind != GPIC_KIND_RBF && kind != GPIC_KIND_COSINE) return fail(GPIC_E_INVALID, "unknown kind");
   // d_work: colpart (ceil(n/256) * d doubles) followed by mean (d doubles)
   double* colpart = static_cast<double*>(d_work);
   double* mean = colpart + ceil_div(n, 256) * d;
   launch_prepare(d_x, n, d, d_xhi, d_xlo, d_sqn, colpart, mean, d_ctl,
-                 static_cast<cudaStream_t>(stream));
+                 static_cast<cudaStream_t>(stream), kind);
   GPIC_CUDA_TRY(cudaGetLastError());
   return GPIC_OK;
 }
+
+static int affinity_rows(int kind, const float* d_xhi, const float* d_xlo, const float* d_sqn,
+                         int64_t n, int32_t d, int64_t row_lo, int64_t row_hi, double sigma,
+                         int32_t impl, float* d_a, int64_t lda, double* d_deg, void* d_work,
+                         gpic_ctl* d_ctl, void* stream);
 
 int gpic_affinity_rbf(const float* d_xhi, const float* d_xlo, const float* d_sqn, int64_t n,
                       int32_t d, int64_t row_lo, int64_t row_hi, double sigma, int32_t impl,
                       float* d_a, int64_t lda, double* d_deg, void* d_work, gpic_ctl* d_ctl,
                       void* stream) {
   if (!(sigma > 0)) return fail(GPIC_E_INVALID, "sigma must be positive");
+  return affinity_rows(GPIC_KIND_RBF, d_xhi, d_xlo, d_sqn, n, d, row_lo, row_hi, sigma, impl,
+                       d_a, lda, d_deg, d_work, d_ctl, stream);
+}
+
+int gpic_affinity_cosine(const float* d_xhi, const float* d_xlo, const float* d_sqn, int64_t n,
+                         int32_t d, int64_t row_lo, int64_t row_hi, int32_t impl, float* d_a,
+                         int64_t lda, double* d_deg, void* d_work, gpic_ctl* d_ctl, void* stream) {
+  return affinity_rows(GPIC_KIND_COSINE, d_xhi, d_xlo, d_sqn, n, d, row_lo, row_hi, 1.0, impl,
+                       d_a, lda, d_deg, d_work, d_ctl, stream);
+}
+
+static int affinity_rows(int kind, const float* d_xhi, const float* d_xlo, const float* d_sqn,
+                         int64_t n, int32_t d, int64_t row_lo, int64_t row_hi, double sigma,
+                         int32_t impl, float* d_a, int64_t lda, double* d_deg, void* d_work,
+                         gpic_ctl* d_ctl, void* stream) {
   if (row_lo < 0 || row_hi > n || row_lo >= row_hi) return fail(GPIC_E_INVALID, "bad row range");
   if (lda < affinity_pitch(n) || lda % 32) return fail(GPIC_E_INVALID, "lda must be >= pitch(n) and a multiple of 32");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -163,11 +187,11 @@ int gpic_affinity_rbf(const float* d_xhi, const float* d_xlo, const float* d_sqn
   float* rowpart = static_cast<float*>(d_work);  // n_ctiles x rows_pad
   if (impl == GPIC_AFFINITY_TC) {
     int rc = launch_affinity_tc(d_xhi, d_xlo, d_sqn, n, dp, row_lo, row_hi, neg_scale_log2, d_a,
-                                lda, rowpart, rows_pad, s);
+                                lda, rowpart, rows_pad, s, kind);
     if (rc != GPIC_OK) return rc;
   } else if (impl == GPIC_AFFINITY_SIMT) {
     launch_affinity_simt(d_xhi, d_xlo, d_sqn, n, dp, row_lo, row_hi, neg_scale_log2, d_a, lda,
-                         rowpart, rows_pad, s);
+                         rowpart, rows_pad, s, kind);
   } else {
     return fail(GPIC_E_INVALID, "unknown affinity engine");
   }
@@ -254,12 +278,12 @@ int64_t gpic_mf_ypart_doubles(int64_t n, int32_t d, int64_t rows) {
 }
 
 int gpic_mf_degrees(const float* d_xhi, const float* d_xlo, const float* d_sqn, int64_t n,
-                    int32_t d, int64_t row_lo, int64_t row_hi, double sigma, float* d_ones,
-                    double* d_ypart, double* d_deg, void* stream) {
-  if (!(sigma > 0)) return fail(GPIC_E_INVALID, "sigma must be positive");
+                    int32_t d, int64_t row_lo, int64_t row_hi, double sigma, int32_t kind,
+                    float* d_ones, double* d_ypart, double* d_deg, void* stream) {
+  if (kind == GPIC_KIND_RBF && !(sigma > 0)) return fail(GPIC_E_INVALID, "sigma must be positive");
   if (row_lo < 0 || row_hi > n || row_lo >= row_hi) return fail(GPIC_E_INVALID, "bad row range");
   const MfOperands op{d_xhi, d_xlo, d_sqn, n, feature_pitch(d),
-                      (float)(-1.4426950408889634 / (2.0 * sigma * sigma))};
+                      (float)(-1.4426950408889634 / (2.0 * sigma * sigma)), kind};
   return launch_mf_degrees(op, row_lo, row_hi - row_lo, d_ones, d_ypart, d_deg,
                            static_cast<cudaStream_t>(stream));
 }
@@ -300,13 +324,16 @@ __global__ void zero_check_kernel(const double* __restrict__ deg, int64_t n, gpi
 }
 }  // namespace
 
-int gpic_cluster(const double* d_x, int64_t n, int32_t d, double sigma, int32_t k, double eps,
-                 int32_t max_iter, int64_t first_index, const double* h_uniforms, int32_t impl,
-                 int32_t storage, int64_t* d_labels, double* d_v, double* d_delta_hist,
-                 int32_t* h_iters, int32_t* h_converged, void* d_work, int64_t work_bytes,
-                 void* stream) {
+int gpic_cluster(const double* d_x, int64_t n, int32_t d, double sigma, int32_t kind, int32_t k,
+                 double eps, int32_t max_iter, int64_t first_index, const double* h_uniforms,
+                 int32_t impl, int32_t storage, int64_t* d_labels, double* d_v,
+                 double* d_delta_hist, int32_t* h_iters, int32_t* h_converged, void* d_work,
+                 int64_t work_bytes, void* stream) {
   if (n < 1 || d < 1) return fail(GPIC_E_EMPTY, "dataset must contain at least one point and one feature");
   if (k > n) return fail(GPIC_E_K_TOO_LARGE, "k exceeds the number of points");
+  if (kind != GPIC_KIND_RBF && kind != GPIC_KIND_COSINE) return fail(GPIC_E_INVALID, "unknown kind");
+  if (kind == GPIC_KIND_RBF && !(sigma > 0)) return fail(GPIC_E_INVALID, "sigma must be positive");
+  if (kind == GPIC_KIND_COSINE) sigma = 1.0;  // unused
   if (storage != GPIC_STORAGE_DENSE && impl != GPIC_AFFINITY_TC)
     return fail(GPIC_E_UNSUPPORTED, "packed / matrix-free storage runs on the tcgen05 engine");
   if (storage < GPIC_STORAGE_DENSE || storage > GPIC_STORAGE_NONE)
@@ -321,7 +348,7 @@ int gpic_cluster(const double* d_x, int64_t n, int32_t d, double sigma, int32_t 
   double* deg = ws.deg;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   launch_ctl_init(ws.ctl, eps, max_iter, s);
-  launch_prepare(d_x, n, d, ws.xhi, ws.xlo, ws.sqn, ws.colpart, ws.mean, ws.ctl, s);
+  launch_prepare(d_x, n, d, ws.xhi, ws.xlo, ws.sqn, ws.colpart, ws.mean, ws.ctl, s, kind);
   const float neg_scale_log2 = (float)(-1.4426950408889634 / (2.0 * sigma * sigma));
   const int32_t dp = feature_pitch(d);
   const int64_t lda = affinity_pitch(n);
@@ -336,7 +363,7 @@ int gpic_cluster(const double* d_x, int64_t n, int32_t d, double sigma, int32_t 
     float* degrow = colp + pf;
     float* degcol = degrow + 2 * pf;
     rc = launch_affinity_tc_packed(ws.xhi, ws.xlo, ws.sqn, n, dp, neg_scale_log2, a, degrow,
-                                   degcol, s);
+                                   degcol, s, kind);
     if (rc) return rc;
     launch_sym_degree(degrow, degcol, n, packed_row_halves(dp), deg, ws.ctl, s);
     L.mode = kLoopPacked;
@@ -346,7 +373,7 @@ int gpic_cluster(const double* d_x, int64_t n, int32_t d, double sigma, int32_t 
     // matrix-free: A is recomputed from X for the degrees and every iteration
     double* ypart = reinterpret_cast<double*>(a);
     L.mode = kLoopMatrixFree;
-    L.mf = MfOperands{ws.xhi, ws.xlo, ws.sqn, n, dp, neg_scale_log2};
+    L.mf = MfOperands{ws.xhi, ws.xlo, ws.sqn, n, dp, neg_scale_log2, kind};
     L.ypart = ypart;
     rc = launch_mf_degrees(L.mf, 0, n, ws.v32, ypart, deg, s);
     if (rc) return rc;
@@ -356,11 +383,11 @@ int gpic_cluster(const double* d_x, int64_t n, int32_t d, double sigma, int32_t 
     const int64_t rows_pad = round_up(n, kTileM);
     if (impl == GPIC_AFFINITY_TC) {
       rc = launch_affinity_tc(ws.xhi, ws.xlo, ws.sqn, n, dp, 0, n, neg_scale_log2, a, lda,
-                              ws.rowpart, rows_pad, s);
+                              ws.rowpart, rows_pad, s, kind);
       if (rc) return rc;
     } else {
       launch_affinity_simt(ws.xhi, ws.xlo, ws.sqn, n, dp, 0, n, neg_scale_log2, a, lda,
-                           ws.rowpart, rows_pad, s);
+                           ws.rowpart, rows_pad, s, kind);
     }
     launch_degree(ws.rowpart, n, rows_pad, ceil_div(n, kTileN), 0, deg, ws.ctl, s);
   }
@@ -398,11 +425,11 @@ int gpic_cluster(const double* d_x, int64_t n, int32_t d, double sigma, int32_t 
   return status_from_ctl(h, d);
 }
 
-int gpic_cluster_host(const double* h_x, int64_t n, int32_t d, double sigma, int32_t k,
-                      double eps, int32_t max_iter, int64_t first_index, const double* h_uniforms,
-                      int32_t impl, int32_t storage, int64_t* h_labels, double* h_v,
-                      double* h_delta_hist, int32_t* h_iters, int32_t* h_converged, void* d_work,
-                      int64_t work_bytes, void* stream) {
+int gpic_cluster_host(const double* h_x, int64_t n, int32_t d, double sigma, int32_t kind,
+                      int32_t k, double eps, int32_t max_iter, int64_t first_index,
+                      const double* h_uniforms, int32_t impl, int32_t storage, int64_t* h_labels,
+                      double* h_v, double* h_delta_hist, int32_t* h_iters, int32_t* h_converged,
+                      void* d_work, int64_t work_bytes, void* stream) {
   if (n < 1 || d < 1) return fail(GPIC_E_EMPTY, "dataset must contain at least one point and one feature");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   // device staging after the pipeline workspace: X, labels, v, deltas
@@ -416,8 +443,8 @@ int gpic_cluster_host(const double* h_x, int64_t n, int32_t d, double sigma, int
   double* dh = reinterpret_cast<double*>(p);
   GPIC_CUDA_TRY(cudaMemcpyAsync(dx, h_x, n * d * 8, cudaMemcpyHostToDevice, s));
   int32_t iters = 0, conv = 0;
-  int rc = gpic_cluster(dx, n, d, sigma, k, eps, max_iter, first_index, h_uniforms, impl, storage,
-                        dl, dv, dh, &iters, &conv, d_work, scratch, stream);
+  int rc = gpic_cluster(dx, n, d, sigma, kind, k, eps, max_iter, first_index, h_uniforms, impl,
+                        storage, dl, dv, dh, &iters, &conv, d_work, scratch, stream);
   if (rc) return rc;
   GPIC_CUDA_TRY(cudaMemcpyAsync(h_labels, dl, n * 8, cudaMemcpyDeviceToHost, s));
   GPIC_CUDA_TRY(cudaMemcpyAsync(h_v, dv, n * 8, cudaMemcpyDeviceToHost, s));

@@ -63,7 +63,7 @@ int launch_mf_matvec(const MfOperands& op, int64_t row_lo, int64_t rows, const f
                      cudaStream_t s) {
   const int64_t rows_pad = round_up(rows, kTileM);
   int rc = launch_affinity_tc_matvec(op.xhi, op.xlo, op.sqn, op.n, op.dp, row_lo, row_lo + rows,
-                                     op.ns, v32, ypart, rows_pad, ctl, s);
+                                     op.ns, v32, ypart, rows_pad, ctl, s, op.kind);
   if (rc) return rc;
   mf_reduce_kernel<<<(unsigned)ceil_div(rows, 256), 256, 0, s>>>(
       ypart, mf_parts(op.n, op.dp), rows_pad, rows, row_lo, deg, pt, ctl);

@@ -32,7 +32,7 @@ int64_t sym_partial_floats(int64_t n);  // packed_tiles(n) * 128
 int packed_row_halves(int32_t dp);
 int launch_affinity_tc_packed(const float* xhi, const float* xlo, const float* sqn, int64_t n,
                               int32_t dp, float neg_scale_log2, float* a_packed, float* degrow,
-                              float* degcol, cudaStream_t s);
+                              float* degcol, cudaStream_t s, int kind = GPIC_KIND_RBF);
 void launch_sym_degree(const float* degrow, const float* degcol, int64_t n, int nhalf,
                        double* deg, gpic_ctl* ctl, cudaStream_t s);
 void sym_prepare();
@@ -63,16 +63,18 @@ int carve(void* base, int64_t bytes, int64_t n, int32_t d, int32_t k, int64_t ro
 // prepare.cu
 void launch_ctl_init(gpic_ctl* ctl, double eps, int32_t max_iter, cudaStream_t s);
 void launch_prepare(const double* x, int64_t n, int32_t d, float* xhi, float* xlo, float* sqn,
-                    double* colpart, double* mean, gpic_ctl* ctl, cudaStream_t s);
+                    double* colpart, double* mean, gpic_ctl* ctl, cudaStream_t s,
+                    int kind = GPIC_KIND_RBF);
 
 // affinity_simt.cu / affinity_tc.cu
 void launch_affinity_simt(const float* xhi, const float* xlo, const float* sqn, int64_t n,
                           int32_t dp, int64_t row_lo, int64_t row_hi, float neg_scale_log2,
                           float* a, int64_t lda, float* rowpart, int64_t rows_pad,
-                          cudaStream_t s);
+                          cudaStream_t s, int kind = GPIC_KIND_RBF);
 int launch_affinity_tc(const float* xhi, const float* xlo, const float* sqn, int64_t n,
                        int32_t dp, int64_t row_lo, int64_t row_hi, float neg_scale_log2, float* a,
-                       int64_t lda, float* rowpart, int64_t rows_pad, cudaStream_t s);
+                       int64_t lda, float* rowpart, int64_t rows_pad, cudaStream_t s,
+                       int kind = GPIC_KIND_RBF);
 void launch_degree(const float* rowpart, int64_t rows, int64_t rows_pad, int64_t n_ctiles,
                    int64_t row_lo, double* deg, gpic_ctl* ctl, cudaStream_t s);
 
@@ -125,13 +127,14 @@ struct MfOperands {
   int64_t n;
   int32_t dp;
   float ns;  // -log2(e) / (2 sigma^2)
+  int kind = GPIC_KIND_RBF;
 };
 int64_t mf_parts(int64_t n, int32_t dp);
 int64_t mf_ypart_doubles(int64_t n, int32_t dp, int64_t rows);
 int launch_affinity_tc_matvec(const float* xhi, const float* xlo, const float* sqn, int64_t n,
                               int32_t dp, int64_t row_lo, int64_t row_hi, float neg_scale_log2,
                               const float* v32, double* ypart, int64_t rows_pad,
-                              const gpic_ctl* ctl, cudaStream_t s);
+                              const gpic_ctl* ctl, cudaStream_t s, int kind = GPIC_KIND_RBF);
 int launch_mf_matvec(const MfOperands& op, int64_t row_lo, int64_t rows, const float* v32,
                      double* ypart, const double* deg, const PeerTable& pt, gpic_ctl* ctl,
                      cudaStream_t s);

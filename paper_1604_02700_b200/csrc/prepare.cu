@@ -92,6 +92,41 @@ __global__ void center_split_kernel(const double* __restrict__ x, int64_t n, int
   if (lane == 0) sqn[row] = (float)sq;
 }
 
+// Cosine kind (affinity.py:41-53, 88-95): one warp per (padded) row, fp64
+// norm, ZeroVector(first row) for a zero row, unit row cast to fp32 and
+// split; the Gram engine then yields cos(x_i, x_j) directly.
+__global__ void normalize_split_kernel(const double* __restrict__ x, int64_t n, int32_t d,
+                                       int32_t dp, int64_t n_pad, float* __restrict__ xhi,
+                                       float* __restrict__ xlo, float* __restrict__ sqn,
+                                       gpic_ctl* ctl) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  if (row >= n_pad) return;
+  double sq = 0.0;
+  if (row < n)
+    for (int f = lane; f < d; f += 32) {
+      double v = x[row * d + f];
+      if (!isfinite(v)) v = 0.0;
+      sq += v * v;
+    }
+  sq = warp_sum_f64(sq);
+  if (row < n && sq == 0.0) {
+    if (lane == 0) raise_status(ctl, GPIC_E_ZERO_VECTOR, row, -1, 0.0);
+  }
+  const double inv = sq > 0.0 ? 1.0 / sqrt(sq) : 0.0;
+  for (int f = lane; f < dp; f += 32) {
+    float xc = 0.f;
+    if (row < n && f < d) {
+      const double v = x[row * d + f];
+      xc = isfinite(v) ? (float)(v * inv) : 0.f;
+    }
+    const float hi = to_tf32(xc);
+    xhi[row * dp + f] = hi;
+    xlo[row * dp + f] = xc - hi;
+  }
+  if (lane == 0) sqn[row] = 1.f;
+}
+
 }  // namespace
 
 void launch_ctl_init(gpic_ctl* ctl, double eps, int32_t max_iter, cudaStream_t s) {
@@ -100,13 +135,19 @@ void launch_ctl_init(gpic_ctl* ctl, double eps, int32_t max_iter, cudaStream_t s
 }
 
 void launch_prepare(const double* x, int64_t n, int32_t d, float* xhi, float* xlo, float* sqn,
-                    double* colpart, double* mean, gpic_ctl* ctl, cudaStream_t s) {
+                    double* colpart, double* mean, gpic_ctl* ctl, cudaStream_t s, int kind) {
   const int64_t nblk = ceil_div(n, kColRows);
   const int threads = d >= 256 ? 256 : (int)round_up(d, 32);
-  colsum_kernel<<<(unsigned)nblk, threads, 0, s>>>(x, n, d, colpart, ctl);
-  mean_kernel<<<1, threads, 0, s>>>(colpart, nblk, n, d, mean);
   const int32_t dp = feature_pitch(d);
   const int64_t n_pad = row_pad(n);
+  colsum_kernel<<<(unsigned)nblk, threads, 0, s>>>(x, n, d, colpart, ctl);  // + finiteness scan
+  if (kind == GPIC_KIND_COSINE) {
+    normalize_split_kernel<<<(unsigned)ceil_div(n_pad, 8), 256, 0, s>>>(x, n, d, dp, n_pad, xhi,
+                                                                        xlo, sqn, ctl);
+    count_launch(2);
+    return;
+  }
+  mean_kernel<<<1, threads, 0, s>>>(colpart, nblk, n, d, mean);
   center_split_kernel<<<(unsigned)ceil_div(n_pad, 8), 256, 0, s>>>(x, n, d, dp, n_pad, mean, xhi,
                                                                   xlo, sqn);
   count_launch(3);

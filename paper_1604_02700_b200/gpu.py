@@ -72,12 +72,13 @@ def _ptr(t) -> C.c_void_p:
     return C.c_void_p(t.data_ptr()) if t is not None else C.c_void_p(0)
 
 
-def _check_kind(kind) -> float:
+def _check_kind(kind) -> tuple[int, float]:
+    """(GPIC_KIND_*, sigma) of a similarity kind (affinity.py:22-35)."""
     if isinstance(kind, Cosine):
-        raise InvalidSpec("the cosine similarity kind is not part of this build (RBF only)")
+        return _lib.KIND_COSINE, 1.0
     if not isinstance(kind, GaussianRbf):
         raise InvalidSpec(f"unknown similarity kind {kind!r}")
-    return float(kind.sigma)
+    return _lib.KIND_RBF, float(kind.sigma)
 
 
 def _read_ctl(ctl_t, dev) -> _lib.Ctl:
@@ -188,19 +189,20 @@ def k_affinity(d: DataSet, kind, config: KernelConfig | None = None,
     combine. Raises NonFiniteEntry like validate_dataset (data.py:69-72).
     """
     config = config or KernelConfig()
-    sigma = _check_kind(kind)
+    code, sigma = _check_kind(kind)
     check_shape(d)
     check_labels(d)
     dev = _device(config)
     n = d.points.shape[0]
     lo, hi = rows if rows is not None else (0, n)
-    prep = prepare_points(d, dev)
+    prep = prepare_points(d, dev, code)
     return affinity_rows(prep, lo, hi, sigma, config.affinity_impl)
 
 
 @dataclass
 class PreparedPoints:
-    """Centred fp32 operands of the Gram engines (gpic_prepare_points)."""
+    """fp32 operands of the Gram engines (gpic_prepare_points): centred rows
+    (RBF) or unit rows (cosine), TF32 hi + fp32 lo split."""
 
     xhi: object
     xlo: object
@@ -208,10 +210,12 @@ class PreparedPoints:
     n: int
     d: int
     device: object
+    kind: int = _lib.KIND_RBF
 
 
-def prepare_points(d, dev) -> PreparedPoints:
-    """Upload X (fp64), scan for non-finite entries, centre, cast and split.
+def prepare_points(d, dev, kind: int = _lib.KIND_RBF) -> PreparedPoints:
+    """Upload X (fp64), scan for non-finite entries, centre (RBF) or
+    normalise (cosine, ZeroVector for a zero row), cast and split.
 
     ``d`` is a DataSet (host points, uploaded here) or an (n, m) float64
     CUDA tensor already resident on ``dev``.
@@ -231,10 +235,10 @@ def prepare_points(d, dev) -> PreparedPoints:
     sqn = torch.empty(npad, dtype=torch.float32, device=dev)
     ctl = _new_ctl(dev)
     work = torch.empty(((n + 255) // 256 + 1) * m + m, dtype=torch.float64, device=dev)
-    _lib.check(L.gpic_prepare_points(_ptr(x), n, m, _ptr(xhi), _ptr(xlo), _ptr(sqn), _ptr(work),
-                                     _ptr(ctl), st))
+    _lib.check(L.gpic_prepare_points(_ptr(x), n, m, kind, _ptr(xhi), _ptr(xlo), _ptr(sqn),
+                                     _ptr(work), _ptr(ctl), st))
     _raise_ctl(_read_ctl(ctl, dev), m)
-    return PreparedPoints(xhi=xhi, xlo=xlo, sqn=sqn, n=n, d=m, device=dev)
+    return PreparedPoints(xhi=xhi, xlo=xlo, sqn=sqn, n=n, d=m, device=dev, kind=kind)
 
 
 def affinity_rows(prep: PreparedPoints, lo: int, hi: int, sigma: float, engine: str = "tc"):
@@ -250,9 +254,15 @@ def affinity_rows(prep: PreparedPoints, lo: int, hi: int, sigma: float, engine: 
     rowpart = torch.empty(((n + 127) // 128) * rows_pad, dtype=torch.float32, device=dev)
     ctl = _new_ctl(dev)
     impl = _lib.AFFINITY_TC if engine == "tc" else _lib.AFFINITY_SIMT
-    _lib.check(L.gpic_affinity_rbf(_ptr(prep.xhi), _ptr(prep.xlo), _ptr(prep.sqn), n, m, lo, hi,
-                                   sigma, impl, _ptr(a), lda, _ptr(deg), _ptr(rowpart), _ptr(ctl),
-                                   _stream(dev)))
+    if prep.kind == _lib.KIND_COSINE:
+        rc = L.gpic_affinity_cosine(_ptr(prep.xhi), _ptr(prep.xlo), _ptr(prep.sqn), n, m, lo, hi,
+                                    impl, _ptr(a), lda, _ptr(deg), _ptr(rowpart), _ptr(ctl),
+                                    _stream(dev))
+    else:
+        rc = L.gpic_affinity_rbf(_ptr(prep.xhi), _ptr(prep.xlo), _ptr(prep.sqn), n, m, lo, hi,
+                                 sigma, impl, _ptr(a), lda, _ptr(deg), _ptr(rowpart), _ptr(ctl),
+                                 _stream(dev))
+    _lib.check(rc)
     return DeviceAffinity(a=a, deg=deg, n=n, lda=lda, row_lo=lo, row_hi=hi, ctl=ctl, d=m)
 
 
@@ -461,7 +471,7 @@ def cluster(d: DataSet, kind, params: PicParams, config: KernelConfig | None = N
     """
     torch = _torch()
     config = config or KernelConfig()
-    sigma = _check_kind(kind)
+    code, sigma = _check_kind(kind)
     check_shape(d)
     check_labels(d)
     n, m = d.points.shape
@@ -491,9 +501,10 @@ def cluster(d: DataSet, kind, params: PicParams, config: KernelConfig | None = N
     first, u = kmeans_draws(n, k, seed)
     iters = C.c_int32(0)
     conv = C.c_int32(0)
-    rc = L.gpic_cluster(_ptr(x), n, m, sigma, k, eps, T, first, u.ctypes.data_as(C.c_void_p),
-                        impl, storage, _ptr(labels), _ptr(v), _ptr(hist), C.byref(iters),
-                        C.byref(conv), _ptr(work), nbytes, _stream(dev))
+    rc = L.gpic_cluster(_ptr(x), n, m, sigma, code, k, eps, T, first,
+                        u.ctypes.data_as(C.c_void_p), impl, storage, _ptr(labels), _ptr(v),
+                        _ptr(hist), C.byref(iters), C.byref(conv), _ptr(work), nbytes,
+                        _stream(dev))
     if rc != _lib.GPIC_OK:
         h = _lib.Ctl()
         if L.gpic_ctl_read(_ptr(work), C.byref(h), _stream(dev)) == 0 and h.status == rc:

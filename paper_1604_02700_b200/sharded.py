@@ -127,12 +127,13 @@ class ShardedRunner:
     def close(self):
         self.comm.close()
 
-    def run(self, points, sigma: float, params, seed: int = 0):
+    def run(self, points, kind, params, seed: int = 0):
         gpu = self.gpu
         torch = gpu._torch()
         n, dev, cfg = self.n, self.dev, self.config
         st = gpu._stream(dev)
-        prep = gpu.prepare_points(points, dev)
+        code, sigma = gpu._check_kind(kind)
+        prep = gpu.prepare_points(points, dev, code)
         nl = len(self.locals)
         shards = (_lib.Shard * nl)()
         keep = []  # device buffers referenced by the shard structs
@@ -147,19 +148,20 @@ class ShardedRunner:
                 ypart = torch.empty(int(L.gpic_mf_ypart_doubles(n, prep.d, hi - lo)),
                                     dtype=torch.float64, device=dev)
                 _lib.check(L.gpic_mf_degrees(gpu._ptr(prep.xhi), gpu._ptr(prep.xlo),
-                                             gpu._ptr(prep.sqn), n, prep.d, lo, hi, sigma,
+                                             gpu._ptr(prep.sqn), n, prep.d, lo, hi, sigma, code,
                                              gpu._ptr(ones), gpu._ptr(ypart), gpu._ptr(deg), st))
                 keep += [deg, ypart]
                 shards[i] = _lib.Shard(None, 0, deg.data_ptr(), lo, hi - lo, _lib.STORAGE_NONE,
                                        prep.d, prep.xhi.data_ptr(), prep.xlo.data_ptr(),
-                                       prep.sqn.data_ptr(), sigma, ypart.data_ptr())
+                                       prep.sqn.data_ptr(), sigma, code, ypart.data_ptr())
         else:
             for i, r in enumerate(self.locals):
                 lo, hi = self.ranges[r]
                 blk = gpu.affinity_rows(prep, lo, hi, sigma, cfg.affinity_impl)
                 keep.append(blk)
                 shards[i] = _lib.Shard(blk.a.data_ptr(), blk.lda, blk.deg.data_ptr(), lo, hi - lo,
-                                       _lib.STORAGE_DENSE, prep.d, None, None, None, sigma, None)
+                                       _lib.STORAGE_DENSE, prep.d, None, None, None, sigma, code,
+                                       None)
         T = params.max_iterations
         eps = params.resolved_epsilon(n)
         hist = torch.zeros(nl * T, dtype=torch.float64, device=dev)
@@ -190,10 +192,10 @@ def cluster(d, kind, params, config, seed):
     """Sharded counterpart of gpu.cluster (same return contract)."""
     from . import gpu
 
-    sigma = gpu._check_kind(kind)
+    gpu._check_kind(kind)
     runner = ShardedRunner(d.n, config)
     try:
-        labels, v, trace = runner.run(d, sigma, params, seed)
+        labels, v, trace = runner.run(d, kind, params, seed)
         return labels.cpu().numpy(), v.cpu().numpy(), trace
     finally:
         runner.close()

@@ -39,11 +39,14 @@ def sha(a: np.ndarray) -> str:
 
 
 def pipeline_case(d, sigma, k, seed, forced=()):
-    labels, v, trace = ref.cluster(d, ref.GaussianRbf(sigma), ref.PicParams(k=k), seed=seed)
-    a = ref.build_affinity(d, ref.GaussianRbf(sigma))
+    """sigma=None selects the cosine kind (affinity.py:22-24)."""
+    kind = ref.Cosine() if sigma is None else ref.GaussianRbf(sigma)
+    labels, v, trace = ref.cluster(d, kind, ref.PicParams(k=k), seed=seed)
+    a = ref.build_affinity(d, kind)
     deg = ref.degree(a)
     out = dict(
-        X=d.points, truth=d.labels, sigma=sigma, k=k, seed=seed, labels=labels, v=v,
+        X=d.points, truth=d.labels, sigma=-1.0 if sigma is None else sigma,
+        kind="cosine" if sigma is None else "rbf", k=k, seed=seed, labels=labels, v=v,
         deltas=trace.delta_history, iterations=trace.iterations_run,
         converged=trace.converged, deg=deg, x_sha=sha(d.points),
     )
@@ -57,8 +60,8 @@ def pipeline_case(d, sigma, k, seed, forced=()):
     out["a_rows_idx"] = rows
     out["a_rows"] = a[rows]
     # the parallel backend must agree (test_parallel.py:227-237)
-    pl, pv, pt = ref_parallel.cluster(d, ref.GaussianRbf(sigma), ref.PicParams(k=k),
-                                      ref.KernelConfig(p=4), seed=seed)
+    pl, pv, pt = ref_parallel.cluster(d, kind, ref.PicParams(k=k), ref.KernelConfig(p=4),
+                                      seed=seed)
     assert np.array_equal(pl, labels) and np.max(np.abs(pv - v)) <= 1e-12
     return out
 
@@ -82,6 +85,23 @@ def main():
     c3.pop("X")
     c3.update(gen=json.dumps(dict(n=1200, d=8, k=3, seed=11, sizes="balanced")))
     np.savez_compressed(HERE / "gblobs_balanced.npz", **c3)
+
+    # ---- cosine kind (affinity.py:22-24, 41-53, 88-95) on the reference's
+    # own 2-D generators, the paper's Table-2 similarity
+    # (cosine on offset 2-D data can be a k-means knife edge where even the
+    # reference's serial and parallel backends disagree, test_acceptance.py:
+    # 104-108; keep the first generator seed on which they agree)
+    for name, spec_kw, k in (("cosine_blobs", dict(kind="blobs", n=900, noise=0.3, components=3), 3),
+                             ("cosine_moons", dict(kind="two-moons", n=600, noise=0.05), 2)):
+        for gseed in range(40):
+            dd = ref.generate(ref.GeneratorSpec(seed=gseed, **spec_kw))
+            try:
+                case = pipeline_case(dd, None, k, 2, forced=(4,))
+            except AssertionError:
+                continue
+            case["gen_seed"] = gseed
+            np.savez_compressed(HERE / f"{name}.npz", **case)
+            break
 
     # ---- 1-D k-means cases (kmeans.py:178-196)
     rng = np.random.default_rng(2024)
@@ -147,6 +167,11 @@ def main():
         ref.kmeans_1d(np.array([0.5, 0.5]), ref.KMeansParams(k=3))
     except ref_errors.KTooLarge:
         errs["k_too_large"] = True
+    try:
+        ref.cluster(ref.DataSet(np.array([[1.0, 0.0], [0.0, 0.0], [0.0, 1.0]])), ref.Cosine(),
+                    ref.PicParams(k=2))
+    except ref_errors.ZeroVector as e:
+        errs["zero_vector"] = dict(points=[[1.0, 0.0], [0.0, 0.0], [0.0, 1.0]], index=e.index)
     (HERE / "errors.json").write_text(json.dumps(errs, indent=1) + "\n")
     print("golden fixtures written to", HERE)
 

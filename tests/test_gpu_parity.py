@@ -236,10 +236,38 @@ def test_errors_match_reference():
         _gpu().kmeans_1d(np.array([0.5, 0.5]), KMeansParams(k=3))
     with pytest.raises(errors.KTooLarge):
         cluster(DataSet(np.ones((2, 2))), GaussianRbf(1.0), PicParams(k=3))
-    with pytest.raises(errors.InvalidSpec):
-        from paper_1604_02700_b200 import Cosine
+    from paper_1604_02700_b200 import Cosine
 
-        cluster(DataSet(np.ones((4, 2))), Cosine(), PicParams(k=2))
+    zv = e["zero_vector"]
+    for storage in ("packed", "dense", "none"):
+        with pytest.raises(errors.ZeroVector) as info:
+            cluster(DataSet(np.array(zv["points"])), Cosine(), PicParams(k=2),
+                    config=KernelConfig(storage=storage))
+        assert info.value.index == zv["index"]
+
+
+COSINE_CONFIGS = [KernelConfig(storage="packed"), KernelConfig(storage="dense"),
+                  KernelConfig(storage="none"), KernelConfig(affinity_impl="simt"),
+                  KernelConfig(p=3, virtual_ranks=True)]
+
+
+@pytest.mark.parametrize("case", ["cosine_blobs", "cosine_moons"])
+@pytest.mark.parametrize("cfg", range(len(COSINE_CONFIGS)))
+def test_cosine_kind_matches_reference(golden, case, cfg):
+    """Cosine similarity (affinity.py:88-95), the paper's Table-2 kind."""
+    from paper_1604_02700_b200 import Cosine
+
+    z = golden(case)
+    d = DataSet(z["X"])
+    config = COSINE_CONFIGS[cfg]
+    labels, v, trace = cluster(d, Cosine(), PicParams(k=int(z["k"])), config=config,
+                               seed=int(z["seed"]))
+    assert np.array_equal(labels, z["labels"])
+    assert abs(trace.iterations_run - int(z["iterations"])) <= 2
+    assert rel_l1(v, z["v"]) <= 1e-4
+    _, v4, _ = cluster(d, Cosine(), PicParams(k=int(z["k"]), epsilon=TINY_EPS, max_iterations=4),
+                       config=config)
+    assert rel_l1(v4, z["v_T4"]) <= 1e-4
 
 
 def test_stagewise_pipeline_matches_fused(golden):

@@ -30,11 +30,16 @@ def _points(z):
     return d.points
 
 
-@pytest.mark.parametrize("case", ["config1", "gblobs_small", "gblobs_balanced"])
+def _sigma(z):
+    return None if str(z.get("kind", "rbf")) == "cosine" else float(z["sigma"])
+
+
+@pytest.mark.parametrize("case", ["config1", "gblobs_small", "gblobs_balanced", "cosine_blobs",
+                                  "cosine_moons"])
 def test_pipeline_matches_reference(golden, case):
     z = golden(case)
     x = _points(z)
-    labels, v, deltas, conv = po.pic_cluster(x, float(z["sigma"]), int(z["k"]), seed=int(z["seed"]))
+    labels, v, deltas, conv = po.pic_cluster(x, _sigma(z), int(z["k"]), seed=int(z["seed"]))
     assert np.array_equal(labels, z["labels"])
     assert np.max(np.abs(v - z["v"])) <= 1e-12 * np.abs(z["v"]).max()
     assert len(deltas) == int(z["iterations"]) and bool(conv) == bool(z["converged"])
@@ -112,3 +117,17 @@ def test_threaded_affinity_port_is_bitwise(golden):
     z = golden("config1")
     rows = po.affinity_rows_threaded(z["X"], 100, 300, 1.0, p=4)
     assert np.array_equal(rows, po.rbf_rows(z["X"], 100, 300, 1.0))
+
+
+@pytest.mark.parametrize("case", ["cosine_blobs", "cosine_moons"])
+def test_cosine_rows_bitwise(golden, case):
+    z = golden(case)
+    for r, row in zip(z["a_rows_idx"], z["a_rows"]):
+        assert np.array_equal(po.cosine_rows(z["X"], int(r), int(r) + 1)[0], row)
+
+
+def test_zero_vector_error():
+    e = json.loads((GOLDEN / "errors.json").read_text())["zero_vector"]
+    with pytest.raises(po.OracleError) as info:
+        po.pic_cluster(np.array(e["points"]), None, 2)
+    assert info.value.kind == "ZeroVector" and info.value.index == e["index"]
