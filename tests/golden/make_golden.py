@@ -88,6 +88,15 @@ def main():
 
     # ---- cosine kind (affinity.py:22-24, 41-53, 88-95) on the reference's
     # own 2-D generators, the paper's Table-2 similarity
+    # angular clusters (rays from the origin at 0, 120, 240 degrees) that the
+    # cosine kind separates cleanly: labels are stable, not a knife edge
+    rng = np.random.default_rng(17)
+    ang = np.repeat([0.0, 2 * np.pi / 3, 4 * np.pi / 3], [300, 250, 350])
+    ang = ang + 0.15 * rng.standard_normal(ang.size)
+    rad = rng.uniform(1.0, 5.0, ang.size)
+    rays = ref.DataSet(np.column_stack([rad * np.cos(ang), rad * np.sin(ang)]),
+                       np.repeat([0, 1, 2], [300, 250, 350]))
+    np.savez_compressed(HERE / "cosine_rays.npz", **pipeline_case(rays, None, 3, 1, forced=(4,)))
     # (cosine on offset 2-D data can be a k-means knife edge where even the
     # reference's serial and parallel backends disagree, test_acceptance.py:
     # 104-108; keep the first generator seed on which they agree)

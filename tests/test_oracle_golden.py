@@ -35,7 +35,7 @@ def _sigma(z):
 
 
 @pytest.mark.parametrize("case", ["config1", "gblobs_small", "gblobs_balanced", "cosine_blobs",
-                                  "cosine_moons"])
+                                  "cosine_moons", "cosine_rays"])
 def test_pipeline_matches_reference(golden, case):
     z = golden(case)
     x = _points(z)
