@@ -364,6 +364,15 @@ def run_ours(args, cfg, rank, world):
     e2e_s = statistics.mean(e2e)
     assert np.array_equal(lab_e, lab_np), "public-API labels differ from the device-resident run"
 
+    # phase breakdown (report.run_timed, CUDA events at the phase boundaries)
+    from paper_1604_02700_b200 import report as R
+
+    rep, _ = R.benchmark(d_host, GaussianRbf(sigma), params, backend="gpu", config=cfg_api,
+                         seed=0, repetitions=3)
+    if args.report:
+        rep.write(args.report)
+    phases_ms = {p: statistics.median(r["phases"][p] for r in rep.runs) * 1e3 for p in R.PHASES}
+
     traffic = None
     prof = ROOT / "profiles" / "gemv_traffic.json"
     if prof.exists():
@@ -388,6 +397,7 @@ def run_ours(args, cfg, rank, world):
                      "avg_launch_ms": gemv_ms},
         "e2e": {"value": e2e_s, "unit": "s", "h2d_bytes_per_step": int(n * m * 8),
                 "d2h_bytes_per_step": int(n * 8 * 2 + T * 8)},
+        "phases_ms": phases_ms,
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
     }
@@ -494,6 +504,8 @@ def main():
     ap.add_argument("--ref-rows", type=int, default=256)
     ap.add_argument("--ref-iters", type=int, default=7)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--report", default=None,
+                    help="also write a BenchReport (schema 1, report.py) of 3 timed runs here")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))

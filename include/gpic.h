@@ -196,6 +196,15 @@ int gpic_cluster(const double* d_x, int64_t n, int32_t d, double sigma, int32_t 
                  double* d_delta_hist, int32_t* h_iters, int32_t* h_converged, void* d_work,
                  int64_t work_bytes, void* stream);
 
+/* gpic_cluster plus per-phase device times (CUDA events on `stream`), the
+ * phases of report.py:28 / run_timed report.py:47-99: h_phase_ms[5] =
+ * {affinity, rowsum, normalize (0: folded into the GEMV), iterate, kmeans}. */
+int gpic_cluster_timed(const double* d_x, int64_t n, int32_t d, double sigma, int32_t kind,
+                       int32_t k, double eps, int32_t max_iter, int64_t first_index,
+                       const double* h_uniforms, int32_t impl, int32_t storage, int64_t* d_labels,
+                       double* d_v, double* d_delta_hist, int32_t* h_iters, int32_t* h_converged,
+                       void* d_work, int64_t work_bytes, void* stream, float* h_phase_ms);
+
 /* Same, HOST buffers in and out (the reference-facing call a ctypes/cffi
  * binding makes): copies X in, runs, copies labels/v/deltas out. d_work
  * must hold gpic_cluster_workspace_bytes(...) (256-aligned) + the staging

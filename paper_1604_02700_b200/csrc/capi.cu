@@ -324,11 +324,21 @@ __global__ void zero_check_kernel(const double* __restrict__ deg, int64_t n, gpi
 }
 }  // namespace
 
-int gpic_cluster(const double* d_x, int64_t n, int32_t d, double sigma, int32_t kind, int32_t k,
+}  // extern "C"
+
+namespace {
+// Phase boundaries of one cluster() run (report.py:28 PHASES): prepare +
+// affinity | degree | (normalize: folded into the GEMV) | start vector +
+// power loop | k-means. `ev` is null or 5 recorded events.
+inline void mark(cudaEvent_t* ev, int i, cudaStream_t s) {
+  if (ev) cudaEventRecord(ev[i], s);
+}
+
+int cluster_impl(const double* d_x, int64_t n, int32_t d, double sigma, int32_t kind, int32_t k,
                  double eps, int32_t max_iter, int64_t first_index, const double* h_uniforms,
                  int32_t impl, int32_t storage, int64_t* d_labels, double* d_v,
                  double* d_delta_hist, int32_t* h_iters, int32_t* h_converged, void* d_work,
-                 int64_t work_bytes, void* stream) {
+                 int64_t work_bytes, void* stream, cudaEvent_t* ev) {
   if (n < 1 || d < 1) return fail(GPIC_E_EMPTY, "dataset must contain at least one point and one feature");
   if (k > n) return fail(GPIC_E_K_TOO_LARGE, "k exceeds the number of points");
   if (kind != GPIC_KIND_RBF && kind != GPIC_KIND_COSINE) return fail(GPIC_E_INVALID, "unknown kind");
@@ -347,6 +357,7 @@ int gpic_cluster(const double* d_x, int64_t n, int32_t d, double sigma, int32_t 
   float* a = reinterpret_cast<float*>(static_cast<uint8_t*>(d_work) + scratch);
   double* deg = ws.deg;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  mark(ev, 0, s);
   launch_ctl_init(ws.ctl, eps, max_iter, s);
   launch_prepare(d_x, n, d, ws.xhi, ws.xlo, ws.sqn, ws.colpart, ws.mean, ws.ctl, s, kind);
   const float neg_scale_log2 = (float)(-1.4426950408889634 / (2.0 * sigma * sigma));
@@ -365,6 +376,7 @@ int gpic_cluster(const double* d_x, int64_t n, int32_t d, double sigma, int32_t 
     rc = launch_affinity_tc_packed(ws.xhi, ws.xlo, ws.sqn, n, dp, neg_scale_log2, a, degrow,
                                    degcol, s, kind);
     if (rc) return rc;
+    mark(ev, 1, s);
     launch_sym_degree(degrow, degcol, n, packed_row_halves(dp), deg, ws.ctl, s);
     L.mode = kLoopPacked;
     L.rowp = rowp;
@@ -375,6 +387,7 @@ int gpic_cluster(const double* d_x, int64_t n, int32_t d, double sigma, int32_t 
     L.mode = kLoopMatrixFree;
     L.mf = MfOperands{ws.xhi, ws.xlo, ws.sqn, n, dp, neg_scale_log2, kind};
     L.ypart = ypart;
+    mark(ev, 1, s);  // matrix-free: the degree pass is the first A recompute
     rc = launch_mf_degrees(L.mf, 0, n, ws.v32, ypart, deg, s);
     if (rc) return rc;
     zero_check_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, s>>>(deg, n, ws.ctl);
@@ -389,8 +402,10 @@ int gpic_cluster(const double* d_x, int64_t n, int32_t d, double sigma, int32_t 
       launch_affinity_simt(ws.xhi, ws.xlo, ws.sqn, n, dp, 0, n, neg_scale_log2, a, lda,
                            ws.rowpart, rows_pad, s, kind);
     }
+    mark(ev, 1, s);
     launch_degree(ws.rowpart, n, rows_pad, ceil_div(n, kTileN), 0, deg, ws.ctl, s);
   }
+  mark(ev, 2, s);
   launch_tree_sum(deg, n, ws.redpart, ws.redpart + ceil_div(n, kRedBlock), ws.ctl, s);
   launch_scale_vector(deg, n, ws.redpart + ceil_div(n, kRedBlock), ws.v64, ws.v32,
                       vector_pitch(n), s);
@@ -408,6 +423,7 @@ int gpic_cluster(const double* d_x, int64_t n, int32_t d, double sigma, int32_t 
   rc = run_power_loops(&L, 1, n, max_iter, s);
   if (rc) return rc;
   launch_copy_result(ws.v64, n, d_v, ws.ctl, s);
+  mark(ev, 3, s);
   GPIC_CUDA_TRY(cudaGetLastError());
   // k-means needs the status of the loop: read the control block once.
   gpic_ctl h;
@@ -418,11 +434,50 @@ int gpic_cluster(const double* d_x, int64_t n, int32_t d, double sigma, int32_t 
   rc = launch_kmeans1d(d_v, n, k, first_index, h_uniforms, 100, 1e-12, d_labels, ws.kscratch,
                        ws.ctl, s);
   if (rc) return rc;
+  mark(ev, 4, s);
   rc = gpic_ctl_read(ws.ctl, &h, stream);
   if (rc) return rc;
   if (h_iters) *h_iters = h.iter;
   if (h_converged) *h_converged = h.converged;
   return status_from_ctl(h, d);
+}
+}  // namespace
+
+extern "C" {
+
+int gpic_cluster(const double* d_x, int64_t n, int32_t d, double sigma, int32_t kind, int32_t k,
+                 double eps, int32_t max_iter, int64_t first_index, const double* h_uniforms,
+                 int32_t impl, int32_t storage, int64_t* d_labels, double* d_v,
+                 double* d_delta_hist, int32_t* h_iters, int32_t* h_converged, void* d_work,
+                 int64_t work_bytes, void* stream) {
+  return cluster_impl(d_x, n, d, sigma, kind, k, eps, max_iter, first_index, h_uniforms, impl,
+                      storage, d_labels, d_v, d_delta_hist, h_iters, h_converged, d_work,
+                      work_bytes, stream, nullptr);
+}
+
+int gpic_cluster_timed(const double* d_x, int64_t n, int32_t d, double sigma, int32_t kind,
+                       int32_t k, double eps, int32_t max_iter, int64_t first_index,
+                       const double* h_uniforms, int32_t impl, int32_t storage, int64_t* d_labels,
+                       double* d_v, double* d_delta_hist, int32_t* h_iters, int32_t* h_converged,
+                       void* d_work, int64_t work_bytes, void* stream, float* h_phase_ms) {
+  if (!h_phase_ms) return fail(GPIC_E_INVALID, "h_phase_ms must point at 5 floats");
+  cudaEvent_t ev[5];
+  for (int i = 0; i < 5; ++i) GPIC_CUDA_TRY(cudaEventCreate(&ev[i]));
+  int rc = cluster_impl(d_x, n, d, sigma, kind, k, eps, max_iter, first_index, h_uniforms, impl,
+                        storage, d_labels, d_v, d_delta_hist, h_iters, h_converged, d_work,
+                        work_bytes, stream, ev);
+  if (rc == GPIC_OK) {
+    // the final gpic_ctl_read synchronised the stream: all 5 events are complete
+    float t[4];
+    for (int i = 0; i < 4; ++i) cudaEventElapsedTime(&t[i], ev[i], ev[i + 1]);
+    h_phase_ms[0] = t[0];  // affinity (prepare + Gram + exp epilogue)
+    h_phase_ms[1] = t[1];  // rowsum (degree combine)
+    h_phase_ms[2] = 0.f;   // normalize: folded into the GEMV epilogue
+    h_phase_ms[3] = t[2];  // iterate (start vector + device-resident loop)
+    h_phase_ms[4] = t[3];  // kmeans
+  }
+  for (int i = 0; i < 5; ++i) cudaEventDestroy(ev[i]);
+  return rc;
 }
 
 int gpic_cluster_host(const double* h_x, int64_t n, int32_t d, double sigma, int32_t kind,

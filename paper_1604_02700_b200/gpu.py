@@ -469,9 +469,9 @@ def cluster(d: DataSet, kind, params: PicParams, config: KernelConfig | None = N
     power iteration and the k-means; the host syncs twice (after the loop and
     at the end).
     """
-    torch = _torch()
+    _torch()
     config = config or KernelConfig()
-    code, sigma = _check_kind(kind)
+    _check_kind(kind)
     check_shape(d)
     check_labels(d)
     n, m = d.points.shape
@@ -486,6 +486,18 @@ def cluster(d: DataSet, kind, params: PicParams, config: KernelConfig | None = N
         return sharded.cluster(d, kind, params, config, seed)
     if not (isinstance(params.v0, str) and params.v0 == "degree"):
         return _cluster_stagewise(d, kind, params, config, seed)
+    labels, v, trace, _ = cluster_fused(d, kind, params, config, seed)
+    return labels, v, trace
+
+
+def cluster_fused(d: DataSet, kind, params: PicParams, config: KernelConfig, seed: int = 0,
+                  timed: bool = False):
+    """One gpic_cluster call (p == 1, degree start). With ``timed`` the
+    per-phase device milliseconds come back as a dict (report.py:28 PHASES)."""
+    torch = _torch()
+    code, sigma = _check_kind(kind)
+    n, m = d.points.shape
+    k = params.k
     dev = _device(config)
     L = _lib.lib()
     eps = params.resolved_epsilon(n)
@@ -501,18 +513,21 @@ def cluster(d: DataSet, kind, params: PicParams, config: KernelConfig | None = N
     first, u = kmeans_draws(n, k, seed)
     iters = C.c_int32(0)
     conv = C.c_int32(0)
-    rc = L.gpic_cluster(_ptr(x), n, m, sigma, code, k, eps, T, first,
-                        u.ctypes.data_as(C.c_void_p), impl, storage, _ptr(labels), _ptr(v),
-                        _ptr(hist), C.byref(iters), C.byref(conv), _ptr(work), nbytes,
-                        _stream(dev))
+    args = (_ptr(x), n, m, sigma, code, k, eps, T, first, u.ctypes.data_as(C.c_void_p), impl,
+            storage, _ptr(labels), _ptr(v), _ptr(hist), C.byref(iters), C.byref(conv),
+            _ptr(work), nbytes, _stream(dev))
+    ms = (C.c_float * 5)()
+    rc = L.gpic_cluster_timed(*args, ms) if timed else L.gpic_cluster(*args)
     if rc != _lib.GPIC_OK:
         h = _lib.Ctl()
         if L.gpic_ctl_read(_ptr(work), C.byref(h), _stream(dev)) == 0 and h.status == rc:
             _lib.raise_for(rc, h, m)
         _lib.raise_for(rc, None, m)
     it = int(iters.value)
+    phases = dict(zip(("affinity", "rowsum", "normalize", "iterate", "kmeans"),
+                      (t / 1e3 for t in ms))) if timed else None
     return (labels.cpu().numpy(), v.cpu().numpy(),
-            PicTrace(it, hist[:it].cpu().numpy(), bool(conv.value)))
+            PicTrace(it, hist[:it].cpu().numpy(), bool(conv.value)), phases)
 
 
 def _cluster_stagewise(d, kind, params, config, seed):
