@@ -88,10 +88,14 @@ int64_t gpic_affinity_pitch(int64_t n);
 
 /* ---- stage 0: validate + centre + cast -------------------------------
  * Replaces validate_dataset's finiteness scan (data.py:61-78) and prepares
- * the fp32 operands of the Gram engine: xc = fp32(x - mean_fp64), its
- * TF32 hi/lo split, and |xc|^2. A non-finite entry sets GPIC_E_NONFINITE
- * with the first (row, col) in row-major order. Layout: d_xhi/d_xlo are
- * (n_pad x dp) row-major, dp = gpic_feature_pitch(d), n_pad = gpic_row_pad(n).
+ * the operands of the Gram engines. Both buffers hold n_pad x dp floats
+ * (dp = gpic_feature_pitch(d), n_pad = gpic_row_pad(n)):
+ *   d_xlo  xc = fp32(x - mean_fp64), row-major (the FFMA engine)
+ *   d_xhi  the tensor engine's fp16 planes: hi = fp16(xc * s) (n_pad x dp
+ *          halves) then lo = fp16(xc * s - hi); s = 2^e, max|xc * s| < 2^14
+ *   d_sqn  |xc|^2 per row; d_sqn[n_pad - 1] (a padding row) holds 1 / s^2
+ * A non-finite entry sets GPIC_E_NONFINITE with the first (row, col) in
+ * row-major order. d_work: (ceil(n / 256) + 1) * d + 1 doubles.
  * kind GPIC_KIND_COSINE instead scales every row to unit length in fp64
  * (no centring: cosine is not translation invariant) and reports a zero
  * row as GPIC_E_ZERO_VECTOR(first row) (cosine_norms, affinity.py:41-53). */
@@ -292,6 +296,24 @@ int gpic_comm_gather_degrees(gpic_comm* comm, const gpic_shard* shards, int32_t 
 int gpic_comm_iterate(gpic_comm* comm, const gpic_shard* shards, int32_t nlocal, double eps,
                       int32_t max_iter, double* d_hist, double* d_vout, gpic_ctl* h_ctl,
                       void* stream);
+
+/* ---- batched small-n PIC (Experiment II: cli.py:230-256)
+ * `count` independent problems of n_b = h_offsets[b+1] - h_offsets[b]
+ * (1..4096) points each, all with d features, concatenated row-major in
+ * d_x. One CTA runs one whole problem in fp64 (the reference's operation
+ * order) — affinity, degrees, W, v0, power iteration — then the k-means.
+ * Per problem: h_eps[b] (resolved epsilon), h_first[b] + h_uniforms[b*(k-1)
+ * ...] (its k-means PCG64 draws), outputs d_labels / d_v at its offset,
+ * d_hist[b*max_iter ...], and its control block h_ctl[b] (status, iter,
+ * converged, error index) — a failing problem does not stop the others.
+ * Synchronous. */
+int64_t gpic_batch_workspace_bytes(const int64_t* h_offsets, int32_t count, int32_t d, int32_t k,
+                                   int32_t max_iter);
+int gpic_cluster_batch(const double* d_x, const int64_t* h_offsets, int32_t count, int32_t d,
+                       double sigma, int32_t kind, int32_t k, const double* h_eps,
+                       int32_t max_iter, const int64_t* h_first, const double* h_uniforms,
+                       int64_t* d_labels, double* d_v, double* d_hist, gpic_ctl* h_ctl,
+                       void* d_work, int64_t work_bytes, void* stream);
 
 #ifdef __cplusplus
 }

@@ -94,6 +94,9 @@ SIGNATURES = {
                                P, P, P, I64, P]),
     "gpic_cluster_timed": (C.c_int, [P, I64, I32, F64, I32, I32, F64, I32, I64, P, I32, I32, P, P,
                                      P, P, P, P, I64, P, P]),
+    "gpic_batch_workspace_bytes": (I64, [P, I32, I32, I32, I32]),
+    "gpic_cluster_batch": (C.c_int, [P, P, I32, I32, F64, I32, I32, P, I32, P, P, P, P, P, P, P,
+                                     I64, P]),
     "gpic_cluster_host": (C.c_int, [P, I64, I32, F64, I32, I32, F64, I32, I64, P, I32, I32, P, P,
                                     P, P, P, P, I64, P]),
     "gpic_ctl_read": (C.c_int, [P, P, P]),

@@ -7,7 +7,8 @@
 //     a  = 0 on the diagonal and in padding columns  (affinity.py:102-103)
 // stores A once (fp32, streaming stores) and writes the tile's fp32 row
 // partial sums; gpic_degree combines them in fixed order (fp64).
-// This is the measured-error comparator of the tcgen05 3xTF32 engine
+// It reads the fp32 centred rows (the d_xlo operand of gpic_prepare_points).
+// This is the measured-error comparator of the tcgen05 3-term fp16 engine
 // (affinity_tc.cu) and the engine used when tcgen05 is unavailable for a
 // shape.
 #include "common.cuh"
@@ -20,8 +21,7 @@ namespace {
 constexpr int BM = 128, BN = 128, BK = 16, PADS = 4;
 
 __global__ void __launch_bounds__(256, 2)
-    affinity_simt_kernel(const float* __restrict__ xhi, const float* __restrict__ xlo,
-                         const float* __restrict__ sqn, int64_t n, int32_t dp, int64_t row_lo,
+    affinity_simt_kernel(const float* __restrict__ xc, const float* __restrict__ sqn, int64_t n, int32_t dp, int64_t row_lo,
                          int64_t row_hi, float neg_scale_log2, float* __restrict__ a, int64_t lda,
                          float* __restrict__ rowpart, int64_t rows_pad, int kind) {
   __shared__ __align__(16) float As[BK][BM + PADS];
@@ -49,18 +49,16 @@ __global__ void __launch_bounds__(256, 2)
       const int c = (e & 3) * 4;         // 0,4,8,12
       const int64_t ra = grow0 + r;      // rows are padded to 128 (zero rows)
       const int64_t rb = col0 + r;
-      const float4 ah = *reinterpret_cast<const float4*>(xhi + ra * dp + k0 + c);
-      const float4 al = *reinterpret_cast<const float4*>(xlo + ra * dp + k0 + c);
-      const float4 bh = *reinterpret_cast<const float4*>(xhi + rb * dp + k0 + c);
-      const float4 bl = *reinterpret_cast<const float4*>(xlo + rb * dp + k0 + c);
-      As[c + 0][r] = ah.x + al.x;
-      As[c + 1][r] = ah.y + al.y;
-      As[c + 2][r] = ah.z + al.z;
-      As[c + 3][r] = ah.w + al.w;
-      Bs[c + 0][r] = bh.x + bl.x;
-      Bs[c + 1][r] = bh.y + bl.y;
-      Bs[c + 2][r] = bh.z + bl.z;
-      Bs[c + 3][r] = bh.w + bl.w;
+      const float4 av = *reinterpret_cast<const float4*>(xc + ra * dp + k0 + c);
+      const float4 bv = *reinterpret_cast<const float4*>(xc + rb * dp + k0 + c);
+      As[c + 0][r] = av.x;
+      As[c + 1][r] = av.y;
+      As[c + 2][r] = av.z;
+      As[c + 3][r] = av.w;
+      Bs[c + 0][r] = bv.x;
+      Bs[c + 1][r] = bv.y;
+      Bs[c + 2][r] = bv.z;
+      Bs[c + 3][r] = bv.w;
     }
     __syncthreads();
 #pragma unroll
@@ -143,7 +141,7 @@ void launch_affinity_simt(const float* xhi, const float* xlo, const float* sqn, 
                           cudaStream_t s, int kind) {
   const int64_t rows = row_hi - row_lo;
   dim3 grid((unsigned)ceil_div(n, BN), (unsigned)ceil_div(rows, BM));
-  affinity_simt_kernel<<<grid, 256, 0, s>>>(xhi, xlo, sqn, n, dp, row_lo, row_hi, neg_scale_log2,
+  affinity_simt_kernel<<<grid, 256, 0, s>>>(xlo, sqn, n, dp, row_lo, row_hi, neg_scale_log2,
                                             a, lda, rowpart, rows_pad, kind);
   count_launch();
 }

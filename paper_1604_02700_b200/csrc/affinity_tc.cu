@@ -1,9 +1,12 @@
 // Stage 1 (tensor-core engine): affinity tiles on tcgen05 with a fused
 // exp / diagonal / row-sum epilogue, in three output modes.
 //
-//   G = Xc_I Xc_J^T via 3xTF32: G ~= hi_I.lo_J + lo_I.hi_J + hi_I.hi_J, where
-//   xc = hi + lo exactly (hi = TF32(xc), prepare.cu), each term a
-//   tcgen05.mma.kind::tf32 (M=128, N=128, K=8) accumulating in TMEM (fp32).
+//   G = Xc_I Xc_J^T via a 3-term fp16 split: s^2 G ~= hi_I.lo_J + lo_I.hi_J +
+//   hi_I.hi_J, where xc s ~= hi + lo (hi = fp16(xc s), lo = fp16(xc s - hi),
+//   s = 2^e from the data range, prepare.cu), each term a
+//   tcgen05.mma.kind::f16 (M=128, N=128, K=16) accumulating in TMEM (fp32).
+//   fp16 and TF32 both keep 11 significant bits, so this matches 3xTF32's
+//   accuracy at half the smem operand bytes per MMA and twice the rate.
 //   a_ij = exp2(min(ns*(|x_i|^2 + |x_j|^2 - 2 G_ij), 0)),  ns = -log2(e)/(2 sigma^2)
 //   a_ii = 0, a_ij = 0 for padding rows / columns          (affinity.py:96-103)
 //
@@ -21,7 +24,7 @@
 //   warp 0      TMA producer: the CTA's row block (MB x 128 rows, hi + lo,
 //               all K) stays resident in smem while the CTA walks its
 //               contiguous range of column tiles; B tiles (128 columns,
-//               hi + lo, one 32-wide K block per stage) stream through a
+//               hi + lo, one 64-wide K block per stage) stream through a
 //               ring of smem stages.
 //   warp 1      TMEM owner + single-thread MMA issuer: 3 x 4 x KB MMAs per
 //               M block into one of two TMEM accumulators (double buffer,
@@ -45,8 +48,8 @@ namespace {
 enum { kModeDense = 0, kModePacked = 1, kModeMatvec = 2 };
 
 constexpr int kBN = 128;           // columns per tile (one MMA N)
-constexpr int kKBlk = 32;          // fp32 per 128-byte swizzle row
-constexpr int kTileBytes = 128 * kKBlk * 4;  // 16 KB: 128 rows x 32 fp32
+constexpr int kKBlk = 64;          // fp16 per 128-byte swizzle row
+constexpr int kTileBytes = 128 * kKBlk * 2;  // 16 KB: 128 rows x 64 fp16
 constexpr int kEpiWarps = 8;
 constexpr int kThreads = 64 + kEpiWarps * 32;
 constexpr int kStageOutBytes = 32 * 128;     // 32 rows x 32 fp32 per epilogue warp
@@ -73,7 +76,7 @@ __host__ __device__ constexpr int smem_bytes(int KB, int MODE, bool DIRECT) {
          256 + 1024;
 }
 
-constexpr uint32_t kIdesc = idesc_tf32(128, kBN);
+constexpr uint32_t kIdesc = idesc_f16(128, kBN);
 
 struct TcArgs {
   const float* sqn;
@@ -94,6 +97,7 @@ struct TcArgs {
   float* degrow;     // packed: [tile][halves][128] row partials of each stored tile
   float* degcol;     // packed: [tile][4 row quadrants][128] column partials
   int kind;          // GPIC_KIND_RBF: exp2 epilogue; GPIC_KIND_COSINE: max(0, G) on unit rows
+  const float* gscale;  // 1 / s^2 of the fp16 operand planes (sqn[n_pad - 1], prepare.cu)
 };
 
 __host__ __device__ inline int64_t packed_items(int64_t nrt, int64_t nct, int mb) {
@@ -286,11 +290,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint64_t ah = sw128_desc(su32(sA + ((0 * MB + m) * KB + kb) * kTileBytes));
             const uint64_t al = sw128_desc(su32(sA + ((1 * MB + m) * KB + kb) * kTileBytes));
 #pragma unroll
-            for (int k = 0; k < kKBlk / 8; ++k) {
-              const uint64_t off = (uint64_t)(k * 8 * 4 >> 4);  // 32 bytes along K
-              mma_tf32(d, ah + off, bl + off, kIdesc, (kb | k) != 0);
-              mma_tf32(d, al + off, bh + off, kIdesc, 1u);
-              mma_tf32(d, ah + off, bh + off, kIdesc, 1u);
+            for (int k = 0; k < kKBlk / 16; ++k) {
+              const uint64_t off = (uint64_t)(k * 16 * 2 >> 4);  // 32 bytes along K
+              mma_f16(d, ah + off, bl + off, kIdesc, (kb | k) != 0);
+              mma_f16(d, al + off, bh + off, kIdesc, 1u);
+              mma_f16(d, ah + off, bh + off, kIdesc, 1u);
             }
           }
           tc_commit(&empty[s]);  // frees the B stage once these MMAs retire
@@ -312,7 +316,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int c_lo = MB == 2 ? 0 : 2 * g;
     uint8_t* stage0 = sOut + e * (NBUF > 0 ? NBUF : 1) * kStageOutBytes;
     const float ns = args.ns;
-    const float m2ns = -2.f * ns;
+    const float gs = __ldg(args.gscale);  // accumulator units -> G
+    const float m2ns = -2.f * ns * gs;
     const uint64_t stream_pol = policy_evict_first();  // A is written once here
     uint32_t tf_bits = 0;  // TMEM-full parity per accumulator buffer
     int i = 0;
@@ -378,7 +383,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (args.kind == GPIC_KIND_COSINE) {
           // rows are unit vectors: G_ij = cos(x_i, x_j), clamped at 0 (affinity.py:93-94)
 #pragma unroll
-          for (int j = 0; j < 32; ++j) vals[j] = fmaxf(__uint_as_float(r[j]), 0.f);
+          for (int j = 0; j < 32; ++j) vals[j] = fmaxf(__uint_as_float(r[j]) * gs, 0.f);
         } else {
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
@@ -495,14 +500,15 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 
 bool make_map(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t outer,
-              uint64_t row_bytes, uint32_t box_inner, uint32_t box_outer) {
+              uint64_t row_bytes, uint32_t box_inner, uint32_t box_outer,
+              CUtensorMapDataType dtype = CU_TENSOR_MAP_DATA_TYPE_FLOAT32) {
   auto fn = encode_fn();
   if (!fn) return false;
   cuuint64_t dims[2] = {inner, outer};
   cuuint64_t strides[1] = {row_bytes};
   cuuint32_t box[2] = {box_inner, box_outer};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(ptr), dims, strides,
+  CUresult r = fn(map, dtype, 2, const_cast<void*>(ptr), dims, strides,
                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
@@ -555,14 +561,18 @@ int dispatch_kb(int KB, const CUtensorMap& mh, const CUtensorMap& ml, const CUte
   }
 }
 
-int operand_maps(const float* xhi, const float* xlo, int64_t n, int32_t dp, CUtensorMap* mh,
-                 CUtensorMap* ml) {
+// The fp16 hi / lo planes live back to back in the d_xhi buffer (prepare.cu).
+int operand_maps(const float* xhi, int64_t n, int32_t dp, CUtensorMap* mh, CUtensorMap* ml) {
   const int KB = dp / kKBlk;
   if (dp % kKBlk || KB < 1 || KB > 4)
-    return fail(GPIC_E_UNSUPPORTED, "tcgen05 affinity engine supports d <= 128");
+    return fail(GPIC_E_UNSUPPORTED, "tcgen05 affinity engine supports d <= 256");
   const int64_t npad = row_pad(n);
-  if (!make_map(mh, xhi, (uint64_t)dp, (uint64_t)npad, (uint64_t)dp * 4, kKBlk, 128) ||
-      !make_map(ml, xlo, (uint64_t)dp, (uint64_t)npad, (uint64_t)dp * 4, kKBlk, 128))
+  const uint16_t* hi = reinterpret_cast<const uint16_t*>(xhi);
+  const uint16_t* lo = hi + npad * dp;
+  if (!make_map(mh, hi, (uint64_t)dp, (uint64_t)npad, (uint64_t)dp * 2, kKBlk, 128,
+                CU_TENSOR_MAP_DATA_TYPE_FLOAT16) ||
+      !make_map(ml, lo, (uint64_t)dp, (uint64_t)npad, (uint64_t)dp * 2, kKBlk, 128,
+                CU_TENSOR_MAP_DATA_TYPE_FLOAT16))
     return fail(GPIC_E_CUDA, "cuTensorMapEncodeTiled failed");
   return GPIC_OK;
 }
@@ -582,12 +592,13 @@ int launch_affinity_tc_packed(const float* xhi, const float* xlo, const float* s
                               int32_t dp, float neg_scale_log2, float* a_packed, float* degrow,
                               float* degcol, cudaStream_t s, int kind) {
   CUtensorMap mh, ml, mo;
-  int rc = operand_maps(xhi, xlo, n, dp, &mh, &ml);
+  int rc = operand_maps(xhi, n, dp, &mh, &ml);
   if (rc) return rc;
   if (!make_map(&mo, a_packed, 128, (uint64_t)packed_tiles(n) * 128, 512, 32, 32))
     return fail(GPIC_E_CUDA, "cuTensorMapEncodeTiled failed");
   TcArgs args{};
   args.sqn = sqn;
+  args.gscale = sqn + row_pad(n) - 1;
   args.n = n;
   args.rows = n;
   args.ns = neg_scale_log2;
@@ -604,12 +615,13 @@ int launch_affinity_tc(const float* xhi, const float* xlo, const float* sqn, int
                        int64_t lda, float* rowpart, int64_t rows_pad, cudaStream_t s, int kind) {
   const int64_t rows = row_hi - row_lo;
   CUtensorMap mh, ml, mo;
-  int rc = operand_maps(xhi, xlo, n, dp, &mh, &ml);
+  int rc = operand_maps(xhi, n, dp, &mh, &ml);
   if (rc) return rc;
   if (!make_map(&mo, a, (uint64_t)lda, (uint64_t)rows, (uint64_t)lda * 4, 32, 32))
     return fail(GPIC_E_CUDA, "cuTensorMapEncodeTiled failed");
   TcArgs args{};
   args.sqn = sqn;
+  args.gscale = sqn + row_pad(n) - 1;
   args.n = n;
   args.row_lo = row_lo;
   args.rows = rows;
@@ -635,10 +647,11 @@ int launch_affinity_tc_matvec(const float* xhi, const float* xlo, const float* s
                               const float* v32, double* ypart, int64_t rows_pad,
                               const gpic_ctl* ctl, cudaStream_t s, int kind) {
   CUtensorMap mh, ml;
-  int rc = operand_maps(xhi, xlo, n, dp, &mh, &ml);
+  int rc = operand_maps(xhi, n, dp, &mh, &ml);
   if (rc) return rc;
   TcArgs args{};
   args.sqn = sqn;
+  args.gscale = sqn + row_pad(n) - 1;
   args.n = n;
   args.row_lo = row_lo;
   args.rows = row_hi - row_lo;

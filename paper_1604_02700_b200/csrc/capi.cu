@@ -25,7 +25,8 @@ int fail(int code, const char* msg) {
   return code;
 }
 
-int32_t feature_pitch(int32_t d) { return (int32_t)round_up(d, 32); }
+// 64 features = one 128-byte swizzle row of the fp16 tensor operands
+int32_t feature_pitch(int32_t d) { return (int32_t)round_up(d, 64); }
 // rows padded to the tile plus one spare tile: shard row tiles may start
 // at any row, so a tile can overhang n by up to 127 rows.
 int64_t row_pad(int64_t n) { return round_up(n, kTileM) + kTileM; }
@@ -41,7 +42,7 @@ int64_t workspace_bytes(int64_t n, int32_t d, int32_t k, int64_t rows, int32_t /
   b += 2 * al(npad * dp * 4);                 // xhi, xlo
   b += al(npad * 4);                          // sqn
   b += al(ceil_div(n, 256) * d * 8);          // colpart
-  b += al((int64_t)d * 8);                    // mean
+  b += al((int64_t)(d + 1) * 8);              // mean + max|x - mean|
   b += al(n_ctiles * rows_pad * 4);           // rowpart
   b += al((ceil_div(n, kRedBlock) + 1) * 8);  // redpart
   b += al(n * 8);                             // y
@@ -69,7 +70,7 @@ int carve(void* base, int64_t bytes, int64_t n, int32_t d, int32_t k, int64_t ro
   ws->xlo = reinterpret_cast<float*>(take(npad * dp * 4));
   ws->sqn = reinterpret_cast<float*>(take(npad * 4));
   ws->colpart = reinterpret_cast<double*>(take(ceil_div(n, 256) * d * 8));
-  ws->mean = reinterpret_cast<double*>(take((int64_t)d * 8));
+  ws->mean = reinterpret_cast<double*>(take((int64_t)(d + 1) * 8));
   ws->rowpart = reinterpret_cast<float*>(take(n_ctiles * rows_pad * 4));
   ws->redpart = reinterpret_cast<double*>(take((ceil_div(n, kRedBlock) + 1) * 8));
   ws->y = reinterpret_cast<double*>(take(n * 8));
@@ -143,7 +144,7 @@ int gpic_prepare_points(const double* d_x, int64_t n, int32_t d, int32_t kind, f
                         float* d_xlo, float* d_sqn, void* d_work, gpic_ctl* d_ctl, void* stream) {
   if (n < 1 || d < 1) return fail(GPIC_E_EMPTY, "dataset must contain at least one point and one feature");
   if (kind != GPIC_KIND_RBF && kind != GPIC_KIND_COSINE) return fail(GPIC_E_INVALID, "unknown kind");
-  // d_work: colpart (ceil(n/256) * d doubles) followed by mean (d doubles)
+  // d_work: colpart (ceil(n/256) * d doubles) followed by mean (d + 1 doubles)
   double* colpart = static_cast<double*>(d_work);
   double* mean = colpart + ceil_div(n, 256) * d;
   launch_prepare(d_x, n, d, d_xhi, d_xlo, d_sqn, colpart, mean, d_ctl,

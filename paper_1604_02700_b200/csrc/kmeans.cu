@@ -40,32 +40,52 @@ struct KScratch {
   int32_t* alt;     // n   DP labels
   double* dist2;    // n
   double* unif;     // kMaxK
-  int32_t* order;   // kPolishLimit   stable sorted order
-  double* best;     // 2 x (kPolishLimit + 1)
-  int32_t* split;   // (kMaxK + 1) x (kPolishLimit + 1)
+  int32_t* order;   // m = min(n, kPolishLimit): stable sorted order
+  double* best;     // m + 1
+  int32_t* split;   // (kcap + 1) x split_ld, split_ld = m + 1
   double* stats;    // small: [0] = wcss(lloyd), [1] = wcss(dp)
+  int64_t split_ld;
+};
+
+// One k-means problem; the batched launch (Experiment II) runs one per CTA.
+struct KProblem {
+  const double* v;
+  int64_t n;
+  int64_t first;     // k-means++ first centre (host PCG64 draw)
+  KScratch s;
+  int64_t* out;      // canonical labels
+  gpic_ctl* ctl;
 };
 
 __host__ __device__ inline int64_t al(int64_t b) { return (b + 255) & ~int64_t(255); }
 
-__host__ __device__ inline KScratch carve_k(void* base, int64_t n) {
+__host__ __device__ inline int64_t polish_len(int64_t n) { return n < kPolishLimit ? n : kPolishLimit; }
+
+__host__ __device__ inline int64_t scratch_size(int64_t n, int kcap) {
+  const int64_t m = polish_len(n);
+  return al(n * 4) * 2 + al(n * 8) + al(kMaxK * 8) + al(m * 4) + al((m + 1) * 8) +
+         al((int64_t)(kcap + 1) * (m + 1) * 4) + al(64 * 8);
+}
+
+__host__ __device__ inline KScratch carve_k(void* base, int64_t n, int kcap) {
+  const int64_t m = polish_len(n);
   uint8_t* p = static_cast<uint8_t*>(base);
   KScratch s;
   s.lab = reinterpret_cast<int32_t*>(p); p += al(n * 4);
   s.alt = reinterpret_cast<int32_t*>(p); p += al(n * 4);
   s.dist2 = reinterpret_cast<double*>(p); p += al(n * 8);
   s.unif = reinterpret_cast<double*>(p); p += al(kMaxK * 8);
-  s.order = reinterpret_cast<int32_t*>(p); p += al(kPolishLimit * 4);
-  s.best = reinterpret_cast<double*>(p); p += al(2 * (kPolishLimit + 1) * 8);
-  s.split = reinterpret_cast<int32_t*>(p); p += al((int64_t)(kMaxK + 1) * (kPolishLimit + 1) * 4);
+  s.order = reinterpret_cast<int32_t*>(p); p += al(m * 4);
+  s.best = reinterpret_cast<double*>(p); p += al((m + 1) * 8);
+  s.split = reinterpret_cast<int32_t*>(p); p += al((int64_t)(kcap + 1) * (m + 1) * 4);
   s.stats = reinterpret_cast<double*>(p); p += al(64 * 8);
+  s.split_ld = m + 1;
   return s;
 }
 
-__host__ __device__ inline int64_t scratch_size(int64_t n) {
-  return al(n * 4) * 2 + al(n * 8) + al(kMaxK * 8) + al(kPolishLimit * 4) +
-         al(2 * (kPolishLimit + 1) * 8) + al((int64_t)(kMaxK + 1) * (kPolishLimit + 1) * 4) +
-         al(64 * 8);
+// the CTA's problem: `many[blockIdx.x]` in a batch, else the by-value one
+__device__ __forceinline__ KProblem problem(const KProblem& one, const KProblem* many) {
+  return many ? many[blockIdx.x] : one;
 }
 
 // ------------------------------------------------------- block primitives
@@ -201,8 +221,14 @@ __device__ double wcss(const double* v, int64_t n, int k, const int32_t* lab, Sh
 
 // ----------------------------------------------------------- Lloyd kernel
 __global__ void __launch_bounds__(kThreads, 1)
-    lloyd_kernel(const double* __restrict__ v, int64_t n, int k, int64_t first_index,
-                 int max_rounds, double tol, KScratch s, gpic_ctl* ctl) {
+    lloyd_kernel(KProblem one, const KProblem* __restrict__ many, int k, int max_rounds,
+                 double tol) {
+  const KProblem P = problem(one, many);
+  if (P.ctl->status != GPIC_OK) return;  // failed upstream (batched PIC)
+  const double* __restrict__ v = P.v;
+  const int64_t n = P.n;
+  const int64_t first_index = P.first;
+  const KScratch s = P.s;
   extern __shared__ __align__(16) uint8_t smem_raw[];
   Shared& sh = *reinterpret_cast<Shared*>(smem_raw);
   __shared__ double sums[kMaxK];
@@ -304,7 +330,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 // --------------------------------------------------- DP polish (n <= 4096)
 __global__ void __launch_bounds__(kThreads, 1)
-    polish_kernel(const double* __restrict__ v, int64_t n, int k, KScratch s) {
+    polish_kernel(KProblem one, const KProblem* __restrict__ many, int k) {
+  const KProblem P = problem(one, many);
+  if (P.ctl->status != GPIC_OK || P.n > kPolishLimit) return;
+  const double* __restrict__ v = P.v;
+  const int64_t n = P.n;
+  const KScratch s = P.s;
   extern __shared__ __align__(16) uint8_t smem_raw[];
   // [0, 4096) sort keys/values, then reused: ps (n+1), ps2 (n+1), prev (n+1)
   double* key = reinterpret_cast<double*>(smem_raw);                       // 4096
@@ -366,7 +397,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (c < bc) { bc = c; bi = i; }  // strict: earliest i on ties (np.argmin)
       }
       cur[j] = bc;
-      s.split[(int64_t)q * (kPolishLimit + 1) + j] = bi;
+      s.split[(int64_t)q * s.split_ld + j] = bi;
     }
     __syncthreads();
     for (int j = tid; j <= n; j += kThreads) prev[j] = j < q ? inf : cur[j];
@@ -375,7 +406,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (tid == 0) {
     int j = (int)n;
     for (int q = k; q >= 1; --q) {
-      const int i = s.split[(int64_t)q * (kPolishLimit + 1) + j];
+      const int i = s.split[(int64_t)q * s.split_ld + j];
       for (int p = i; p < j; ++p) s.alt[idx[p]] = q - 1;
       j = i;
     }
@@ -384,7 +415,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 // WCSS of the DP labelling, then choose (kmeans.py:190-193).
 __global__ void __launch_bounds__(kThreads, 1)
-    choose_kernel(const double* __restrict__ v, int64_t n, int k, KScratch s) {
+    choose_kernel(KProblem one, const KProblem* __restrict__ many, int k) {
+  const KProblem P = problem(one, many);
+  if (P.ctl->status != GPIC_OK || P.n > kPolishLimit) return;
+  const double* __restrict__ v = P.v;
+  const int64_t n = P.n;
+  const KScratch s = P.s;
   extern __shared__ __align__(16) uint8_t smem_raw[];
   Shared& sh = *reinterpret_cast<Shared*>(smem_raw);
   const double w_dp = wcss(v, n, k, s.alt, sh);
@@ -396,8 +432,14 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 // Contiguity check + canonical relabel (kmeans.py:149-175).
 __global__ void __launch_bounds__(kThreads, 1)
-    finish_kernel(const double* __restrict__ v, int64_t n, int k, KScratch s,
-                  int64_t* __restrict__ out, gpic_ctl* ctl) {
+    finish_kernel(KProblem one, const KProblem* __restrict__ many, int k) {
+  const KProblem P = problem(one, many);
+  if (P.ctl->status != GPIC_OK) return;
+  const double* __restrict__ v = P.v;
+  const int64_t n = P.n;
+  const KScratch s = P.s;
+  int64_t* __restrict__ out = P.out;
+  gpic_ctl* ctl = P.ctl;
   extern __shared__ __align__(16) uint8_t smem_raw[];
   Shared& sh = *reinterpret_cast<Shared*>(smem_raw);
   __shared__ double sums[kMaxK];
@@ -483,9 +525,42 @@ __global__ void __launch_bounds__(kThreads, 1)
   for (int64_t i = tid; i < n; i += kThreads) out[i] = remap[s.lab[i]];
 }
 
+int set_kmeans_attributes() {
+  static bool done = false;
+  if (done) return GPIC_OK;
+  const int shm = (int)sizeof(Shared);
+  const int pshm = kPolishLimit * (8 + 4) + 3 * (kPolishLimit + 1) * 8;
+  GPIC_CUDA_TRY(cudaFuncSetAttribute(lloyd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, shm));
+  GPIC_CUDA_TRY(cudaFuncSetAttribute(choose_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, shm));
+  GPIC_CUDA_TRY(cudaFuncSetAttribute(finish_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, shm));
+  GPIC_CUDA_TRY(cudaFuncSetAttribute(polish_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, pshm));
+  done = true;
+  return GPIC_OK;
+}
+
+// the four stages over `grid` problems (one = by-value problem when many == null)
+int launch_stages(const KProblem& one, const KProblem* many, int grid, int k, int max_rounds,
+                  double tol, bool polish, cudaStream_t st) {
+  int rc = set_kmeans_attributes();
+  if (rc) return rc;
+  const size_t shm = sizeof(Shared);
+  const int pshm = kPolishLimit * (8 + 4) + 3 * (kPolishLimit + 1) * 8;
+  lloyd_kernel<<<grid, kThreads, shm, st>>>(one, many, k, max_rounds, tol);
+  count_launch();
+  if (polish) {
+    polish_kernel<<<grid, kThreads, pshm, st>>>(one, many, k);
+    choose_kernel<<<grid, kThreads, shm, st>>>(one, many, k);
+    count_launch(2);
+  }
+  finish_kernel<<<grid, kThreads, shm, st>>>(one, many, k);
+  count_launch();
+  GPIC_CUDA_TRY(cudaGetLastError());
+  return GPIC_OK;
+}
+
 }  // namespace
 
-int64_t kmeans_scratch_bytes(int64_t n, int32_t /*k*/) { return scratch_size(n); }
+int64_t kmeans_scratch_bytes(int64_t n, int32_t /*k*/) { return scratch_size(n, kMaxK); }
 
 int launch_kmeans1d(const double* v, int64_t n, int32_t k, int64_t first_index,
                     const double* h_uniforms, int32_t max_rounds, double tol, int64_t* labels,
@@ -493,32 +568,43 @@ int launch_kmeans1d(const double* v, int64_t n, int32_t k, int64_t first_index,
   if (k > n) return fail(GPIC_E_K_TOO_LARGE, "k exceeds the number of points");
   if (k < 2 || k > kMaxK) return fail(GPIC_E_UNSUPPORTED, "k must lie in [2, 64] on the GPU path");
   if (first_index < 0 || first_index >= n) return fail(GPIC_E_INVALID, "first_index out of range");
-  KScratch s = carve_k(scratch, n);
-  if (k > 1)
-    GPIC_CUDA_TRY(cudaMemcpyAsync(s.unif, h_uniforms, sizeof(double) * (k - 1),
-                                  cudaMemcpyHostToDevice, st));
-  const size_t shm = sizeof(Shared);
-  static bool attr = false;
-  if (!attr) {
-    GPIC_CUDA_TRY(cudaFuncSetAttribute(lloyd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
-    GPIC_CUDA_TRY(cudaFuncSetAttribute(choose_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
-    GPIC_CUDA_TRY(cudaFuncSetAttribute(finish_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm));
-    const int pshm = kPolishLimit * (8 + 4) + 3 * (kPolishLimit + 1) * 8;
-    GPIC_CUDA_TRY(cudaFuncSetAttribute(polish_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, pshm));
-    attr = true;
-  }
-  lloyd_kernel<<<1, kThreads, shm, st>>>(v, n, k, first_index, max_rounds, tol, s, ctl);
-  count_launch();
-  if (n <= kPolishLimit) {
-    const int pshm = kPolishLimit * (8 + 4) + 3 * (kPolishLimit + 1) * 8;
-    polish_kernel<<<1, kThreads, pshm, st>>>(v, n, k, s);
-    choose_kernel<<<1, kThreads, shm, st>>>(v, n, k, s);
-    count_launch(2);
-  }
-  finish_kernel<<<1, kThreads, shm, st>>>(v, n, k, s, labels, ctl);
-  count_launch();
-  GPIC_CUDA_TRY(cudaGetLastError());
+  KProblem p;
+  p.v = v;
+  p.n = n;
+  p.first = first_index;
+  p.s = carve_k(scratch, n, kMaxK);
+  p.out = labels;
+  p.ctl = ctl;
+  GPIC_CUDA_TRY(cudaMemcpyAsync(p.s.unif, h_uniforms, sizeof(double) * (k - 1),
+                                cudaMemcpyHostToDevice, st));
+  return launch_stages(p, nullptr, 1, k, max_rounds, tol, n <= kPolishLimit, st);
+}
+
+// ---------------------------------------------------------------- batched
+int64_t kmeans_batch_scratch_bytes(int64_t n, int32_t k) { return scratch_size(n, k); }
+
+int64_t kmeans_problem_bytes() { return (int64_t)sizeof(KProblem); }
+
+int fill_kmeans_problem(void* host_slot, const double* v, int64_t n, int64_t first, void* scratch,
+                        int32_t k, const double* d_unif, int64_t* labels, gpic_ctl* ctl) {
+  KProblem p;
+  p.v = v;
+  p.n = n;
+  p.first = first;
+  p.s = carve_k(scratch, n, k);
+  p.s.unif = const_cast<double*>(d_unif);
+  p.out = labels;
+  p.ctl = ctl;
+  *static_cast<KProblem*>(host_slot) = p;
   return GPIC_OK;
+}
+
+int launch_kmeans1d_batch(const void* d_problems, int32_t count, int32_t k, int32_t max_rounds,
+                          double tol, bool polish, cudaStream_t st) {
+  if (k < 2 || k > kMaxK) return fail(GPIC_E_UNSUPPORTED, "k must lie in [2, 64] on the GPU path");
+  KProblem none{};
+  return launch_stages(none, static_cast<const KProblem*>(d_problems), count, k, max_rounds, tol,
+                       polish, st);
 }
 
 }  // namespace gpic

@@ -174,5 +174,13 @@ int64_t kmeans_scratch_bytes(int64_t n, int32_t k);
 int launch_kmeans1d(const double* v, int64_t n, int32_t k, int64_t first_index,
                     const double* h_uniforms, int32_t max_rounds, double tol, int64_t* labels,
                     void* scratch, gpic_ctl* ctl, cudaStream_t s);
+// batched k-means (batch.cu): one CTA per problem, problems described by
+// opaque KProblem records filled on the host and copied to the device
+int64_t kmeans_batch_scratch_bytes(int64_t n, int32_t k);
+int64_t kmeans_problem_bytes();
+int fill_kmeans_problem(void* host_slot, const double* v, int64_t n, int64_t first, void* scratch,
+                        int32_t k, const double* d_unif, int64_t* labels, gpic_ctl* ctl);
+int launch_kmeans1d_batch(const void* d_problems, int32_t count, int32_t k, int32_t max_rounds,
+                          double tol, bool polish, cudaStream_t s);
 
 }  // namespace gpic

@@ -3,9 +3,20 @@
 // Replaces the finiteness scan of validate_dataset (data.py:61-78) and
 // builds the Gram-engine operands. RBF affinities are translation
 // invariant, so X is centred in fp64 first (centring cuts
-// the fp32 Gram cancellation error by ~5x); the centred rows are cast to
-// fp32 and split into a TF32 head and an exact fp32 tail
-// (xc = hi + lo exactly) for the 3xTF32 tcgen05 engine.
+// the fp32 Gram cancellation error by ~5x). Two operand forms come out:
+//
+//   xc   (d_xlo buffer)  fp32 centred rows, pitch dp — the FFMA engine
+//   hi/lo planes (d_xhi buffer, fp16, pitch dp, hi plane then lo plane)
+//        xs = xc * s with s = 2^e chosen so max|xs| < 2^14 (exact scaling),
+//        hi = fp16(xs), lo = fp16(xs - hi): the 3-term split of the
+//        tcgen05 kind::f16 engine (hi.hi + hi.lo + lo.hi, fp32 accumulate);
+//        1/s^2 is stored in the padding slot sqn[n_pad - 1]
+//
+// fp16 and TF32 both carry 11 significant bits, so the 3-term fp16 split
+// is as accurate as 3xTF32 (the fp32 accumulation dominates both), with
+// half the operand bytes per MMA and twice the tensor-pipe rate.
+#include <cuda_fp16.h>
+
 #include <cfloat>
 
 #include "common.cuh"
@@ -63,45 +74,83 @@ __global__ void mean_kernel(const double* __restrict__ colpart, int64_t nblk, in
     for (int64_t b = 0; b < nblk; ++b) s += colpart[b * d + f];
     mean[f] = s / (double)n;
   }
+  if (threadIdx.x == 0) mean[d] = 0.0;  // max |x - mean| slot (maxabs_kernel)
 }
 
-// One warp per (padded) row: centre in fp64, cast to fp32, split into
-// TF32 hi + fp32 lo, and the fp64-accumulated squared norm of the fp32 row.
+// max |x - mean| over all finite entries -> mean[d] (non-negative doubles
+// order like their bit patterns, so an integer atomicMax is exact)
+__global__ void maxabs_kernel(const double* __restrict__ x, int64_t n, int32_t d,
+                              double* __restrict__ mean) {
+  double m = 0.0;
+  const int64_t total = n * d;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double v = x[i];
+    if (isfinite(v)) m = fmax(m, fabs(v - mean[i % d]));
+  }
+  m = warp_max_f64(m);
+  if ((threadIdx.x & 31) == 0)
+    atomicMax(reinterpret_cast<unsigned long long*>(mean + d), (unsigned long long)__double_as_longlong(m));
+}
+
+// s = 2^e with max|x| * s < 2^14 (1 when every row is the mean)
+__device__ __forceinline__ double operand_scale(double maxabs) {
+  if (!(maxabs > 0.0)) return 1.0;
+  int e;
+  frexp(maxabs, &e);  // maxabs < 2^e
+  const int sh = 14 - e;  // clamped so 1/s^2 stays a normal fp32
+  return ldexp(1.0, sh < -60 ? -60 : (sh > 60 ? 60 : sh));
+}
+
+__device__ __forceinline__ void split16(double xs, __half* hi, __half* lo, int64_t at) {
+  const float x32 = (float)xs;
+  const __half h = __float2half_rn(x32);
+  hi[at] = h;
+  lo[at] = __float2half_rn(x32 - __half2float(h));
+}
+
+// One warp per (padded) row: centre in fp64, fp32 row for the FFMA engine,
+// scaled fp16 hi/lo planes for the tensor engine, fp64-accumulated squared
+// norm of the fp32 row.
 __global__ void center_split_kernel(const double* __restrict__ x, int64_t n, int32_t d, int32_t dp,
                                     int64_t n_pad, const double* __restrict__ mean,
-                                    float* __restrict__ xhi, float* __restrict__ xlo,
+                                    __half* __restrict__ hi, float* __restrict__ xc_out,
                                     float* __restrict__ sqn) {
   const int lane = threadIdx.x & 31;
   const int64_t row = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
   if (row >= n_pad) return;
+  __half* lo = hi + n_pad * dp;
+  const double s = operand_scale(mean[d]);
   double sq = 0.0;
   for (int f = lane; f < dp; f += 32) {
-    float xc = 0.f;
+    double c = 0.0;
     if (row < n && f < d) {
       double v = x[row * d + f];
       if (!isfinite(v)) v = mean[f];
-      xc = (float)(v - mean[f]);
+      c = v - mean[f];
     }
-    const float hi = to_tf32(xc);
-    const float lo = xc - hi;
-    xhi[row * dp + f] = hi;
-    xlo[row * dp + f] = lo;
+    const float xc = (float)c;
+    xc_out[row * dp + f] = xc;
+    split16(c * s, hi, lo, row * dp + f);
     sq += (double)xc * (double)xc;
   }
   sq = warp_sum_f64(sq);
-  if (lane == 0) sqn[row] = (float)sq;
+  if (lane == 0) sqn[row] = row == n_pad - 1 ? (float)(1.0 / (s * s)) : (float)sq;
 }
 
 // Cosine kind (affinity.py:41-53, 88-95): one warp per (padded) row, fp64
 // norm, ZeroVector(first row) for a zero row, unit row cast to fp32 and
-// split; the Gram engine then yields cos(x_i, x_j) directly.
+// split (s = 2^14: unit components); the Gram engines then yield
+// cos(x_i, x_j) directly.
 __global__ void normalize_split_kernel(const double* __restrict__ x, int64_t n, int32_t d,
-                                       int32_t dp, int64_t n_pad, float* __restrict__ xhi,
-                                       float* __restrict__ xlo, float* __restrict__ sqn,
+                                       int32_t dp, int64_t n_pad, __half* __restrict__ hi,
+                                       float* __restrict__ xc_out, float* __restrict__ sqn,
                                        gpic_ctl* ctl) {
   const int lane = threadIdx.x & 31;
   const int64_t row = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
   if (row >= n_pad) return;
+  __half* lo = hi + n_pad * dp;
+  constexpr double s = 16384.0;
   double sq = 0.0;
   if (row < n)
     for (int f = lane; f < d; f += 32) {
@@ -115,16 +164,15 @@ __global__ void normalize_split_kernel(const double* __restrict__ x, int64_t n, 
   }
   const double inv = sq > 0.0 ? 1.0 / sqrt(sq) : 0.0;
   for (int f = lane; f < dp; f += 32) {
-    float xc = 0.f;
+    double u = 0.0;
     if (row < n && f < d) {
       const double v = x[row * d + f];
-      xc = isfinite(v) ? (float)(v * inv) : 0.f;
+      u = isfinite(v) ? v * inv : 0.0;
     }
-    const float hi = to_tf32(xc);
-    xhi[row * dp + f] = hi;
-    xlo[row * dp + f] = xc - hi;
+    xc_out[row * dp + f] = (float)u;
+    split16(u * s, hi, lo, row * dp + f);
   }
-  if (lane == 0) sqn[row] = 1.f;
+  if (lane == 0) sqn[row] = row == n_pad - 1 ? (float)(1.0 / (s * s)) : 1.f;
 }
 
 }  // namespace
@@ -140,17 +188,20 @@ void launch_prepare(const double* x, int64_t n, int32_t d, float* xhi, float* xl
   const int threads = d >= 256 ? 256 : (int)round_up(d, 32);
   const int32_t dp = feature_pitch(d);
   const int64_t n_pad = row_pad(n);
+  __half* planes = reinterpret_cast<__half*>(xhi);
   colsum_kernel<<<(unsigned)nblk, threads, 0, s>>>(x, n, d, colpart, ctl);  // + finiteness scan
   if (kind == GPIC_KIND_COSINE) {
-    normalize_split_kernel<<<(unsigned)ceil_div(n_pad, 8), 256, 0, s>>>(x, n, d, dp, n_pad, xhi,
+    normalize_split_kernel<<<(unsigned)ceil_div(n_pad, 8), 256, 0, s>>>(x, n, d, dp, n_pad, planes,
                                                                         xlo, sqn, ctl);
     count_launch(2);
     return;
   }
   mean_kernel<<<1, threads, 0, s>>>(colpart, nblk, n, d, mean);
-  center_split_kernel<<<(unsigned)ceil_div(n_pad, 8), 256, 0, s>>>(x, n, d, dp, n_pad, mean, xhi,
+  const int64_t mblk = ceil_div(n * d, 256);
+  maxabs_kernel<<<(unsigned)(mblk < 1184 ? mblk : 1184), 256, 0, s>>>(x, n, d, mean);
+  center_split_kernel<<<(unsigned)ceil_div(n_pad, 8), 256, 0, s>>>(x, n, d, dp, n_pad, mean, planes,
                                                                   xlo, sqn);
-  count_launch(3);
+  count_launch(4);
 }
 
 }  // namespace gpic

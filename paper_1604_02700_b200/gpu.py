@@ -538,3 +538,81 @@ def _cluster_stagewise(d, kind, params, config, seed):
     v, trace = iterate(w, v, params, config)
     labels = kmeans_1d(v, KMeansParams(k=params.k, seed=seed), config)
     return labels.cpu().numpy(), v.cpu().numpy(), trace
+
+
+# ------------------------------------------------- batched small problems
+BATCH_MAX_N = 4096
+
+
+def cluster_batch(datasets, kind, params: PicParams, seeds, config: KernelConfig | None = None):
+    """Many small independent PIC runs in one launch (Experiment II engine).
+
+    ``datasets``: DataSets with the same feature count and 1..4096 points;
+    ``seeds``: the k-means seed of each run. Returns one (labels, v, PicTrace)
+    per dataset — what ``cluster(d, kind, params, seed=s)`` returns for it.
+    Errors raise the reference's exception of the first failing problem, in
+    input order (cli.py:240-246 runs them one after another).
+    """
+    torch = _torch()
+    config = config or KernelConfig()
+    code, sigma = _check_kind(kind)
+    datasets = list(datasets)
+    seeds = list(seeds)
+    if not datasets or len(seeds) != len(datasets):
+        raise InvalidSpec("cluster_batch needs one seed per dataset and at least one dataset")
+    if not (isinstance(params.v0, str) and params.v0 == "degree"):
+        raise InvalidSpec("the batched engine starts from the degree vector (v0='degree')")
+    for d in datasets:
+        check_shape(d)
+        check_labels(d)
+    m = datasets[0].points.shape[1]
+    if any(d.points.shape[1] != m for d in datasets):
+        raise DimensionMismatch((datasets[0].n, m), next(d.points.shape for d in datasets
+                                                          if d.points.shape[1] != m))
+    k = params.k
+    for d in datasets:
+        if k > d.n:
+            raise KTooLarge(k, d.n)
+    if k > KMEANS_MAX_K:
+        raise InvalidSpec(f"the device k-means holds at most {KMEANS_MAX_K} centres")
+    if max(d.n for d in datasets) > BATCH_MAX_N:
+        raise InvalidSpec(f"batched problems hold at most {BATCH_MAX_N} points; use cluster()")
+    B = len(datasets)
+    T = params.max_iterations
+    offsets = np.zeros(B + 1, dtype=np.int64)
+    offsets[1:] = np.cumsum([d.n for d in datasets])
+    eps = np.array([params.resolved_epsilon(d.n) for d in datasets], dtype=np.float64)
+    first = np.zeros(B, dtype=np.int64)
+    unif = np.zeros(B * max(k - 1, 1), dtype=np.float64)
+    for b, (d, s) in enumerate(zip(datasets, seeds)):
+        f, u = kmeans_draws(d.n, k, s)
+        first[b] = f
+        unif[b * (k - 1):(b + 1) * (k - 1)] = u[: k - 1]
+    dev = _device(config)
+    L = _lib.lib()
+    x = torch.from_numpy(np.ascontiguousarray(np.concatenate([d.points for d in datasets]))).to(dev)
+    N = int(offsets[-1])
+    labels = torch.empty(N, dtype=torch.int64, device=dev)
+    v = torch.empty(N, dtype=torch.float64, device=dev)
+    hist = torch.zeros(B * T, dtype=torch.float64, device=dev)
+    cptr = lambda a: a.ctypes.data_as(C.c_void_p)  # noqa: E731
+    nbytes = int(L.gpic_batch_workspace_bytes(cptr(offsets), B, m, k, T))
+    if nbytes < 0:
+        raise InvalidSpec("invalid batch shape")
+    work = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    ctls = (_lib.Ctl * B)()
+    rc = L.gpic_cluster_batch(_ptr(x), cptr(offsets), B, m, sigma, code, k, cptr(eps), T,
+                              cptr(first), cptr(unif), _ptr(labels), _ptr(v), _ptr(hist), ctls,
+                              _ptr(work), nbytes, _stream(dev))
+    _lib.check(rc)
+    for c in ctls:
+        if c.status != _lib.GPIC_OK:
+            _lib.raise_for(c.status, c, m)
+    lab_np, v_np, h_np = labels.cpu().numpy(), v.cpu().numpy(), hist.cpu().numpy()
+    out = []
+    for b in range(B):
+        lo, hi = int(offsets[b]), int(offsets[b + 1])
+        it = int(ctls[b].iter)
+        out.append((lab_np[lo:hi].copy(), v_np[lo:hi].copy(),
+                    PicTrace(it, h_np[b * T: b * T + it].copy(), bool(ctls[b].converged))))
+    return out

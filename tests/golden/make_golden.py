@@ -66,6 +66,68 @@ def pipeline_case(d, sigma, k, seed, forced=()):
     return out
 
 
+def generators():
+    """sha256 of the reference's 2-D generators / subsampler outputs
+    (datasets.py:79-98,147-204) for the Table-2 and Experiment-II inputs."""
+    from picluster.datasets import SubsampleSpec, subsample_balanced
+
+    out = {"generate": [], "subsample": []}
+    for kind, n, noise, seed in (("two-moons", 15000, 0.05, 0), ("two-moons", 601, 0.1, 3),
+                                 ("three-circles", 15000, 0.05, 0), ("three-circles", 602, 0.1, 3),
+                                 ("two-moons", 45000, 0.05, 0), ("three-circles", 45000, 0.05, 0)):
+        d = ref.generate(ref.GeneratorSpec(kind, n=n, noise=noise, seed=seed))
+        out["generate"].append(dict(kind=kind, n=n, noise=noise, seed=seed,
+                                    points=sha(d.points), labels=sha(d.labels)))
+    for kind in ("cassine", "shapes", "smiley", "blobs"):
+        for n, noise, seed in ((45000, 0.05, 0), (17, 0.1, 5)):
+            d = ref.generate(ref.GeneratorSpec(kind, n=n, noise=noise, seed=seed))
+            out["generate"].append(dict(kind=kind, n=n, noise=noise, seed=seed,
+                                        points=sha(d.points), labels=sha(d.labels)))
+    base = ref.generate(ref.GeneratorSpec("three-circles", n=999, noise=0.05, seed=2))
+    for f, s in ((0.1, 0), (0.5, 7919), (1.0, 3), (0.0001, 1)):
+        sub = subsample_balanced(base, SubsampleSpec(f, seed=s))
+        out["subsample"].append(dict(base=["three-circles", 999, 0.05, 2], fraction=f, seed=s,
+                                     points=sha(sub.points), labels=sha(sub.labels),
+                                     name=sub.name))
+    (HERE / "generators.json").write_text(json.dumps(out, indent=1) + "\n")
+
+
+def experiment2():
+    """The reference's own Experiment-II driver (cli.py:230-256) on the
+    paper's n = 45k datasets with the CLI defaults (cosine,
+    noise 0.05, seed 0), a CPU-sized subset of the fractions: the rows plus
+    every run's labels / embedding / iteration count."""
+    import types
+
+    # picluster.cli imports figures -> matplotlib (absent here; not used by
+    # run_experiment2): an in-process stand-in module is enough to import it
+    mpl = types.ModuleType("matplotlib")
+    mpl.use = lambda *a, **k: None
+    sys.modules.setdefault("matplotlib", mpl)
+    sys.modules.setdefault("matplotlib.pyplot", types.ModuleType("matplotlib.pyplot"))
+    from picluster import cli as ref_cli
+    from picluster.datasets import SubsampleSpec, subsample_balanced
+
+    cases = []
+    fractions = [0.0001, 0.0005, 0.001, 0.004, 0.009]
+    for kind, k in (("smiley", 4), ("cassine", 2), ("shapes", 4), ("blobs", 3)):
+        d = ref.generate(ref.GeneratorSpec(kind, n=45000, noise=0.05, seed=0))
+        params = ref.PicParams(k=k)
+        rows = ref_cli.run_experiment2(d, ref.Cosine(), params, fractions, 3, backend="serial",
+                                       seed=0)
+        runs = []
+        for f in fractions:
+            for rep in range(3):
+                rs = 7919 * rep
+                sub = subsample_balanced(d, SubsampleSpec(f, seed=rs))
+                lab, v, tr = ref.cluster(sub, ref.Cosine(), params, seed=rs)
+                runs.append(dict(fraction=f, seed=rs, n=int(sub.n), labels=lab.tolist(),
+                                 v=v.tolist(), iterations=int(tr.iterations_run),
+                                 converged=bool(tr.converged)))
+        cases.append(dict(kind=kind, k=k, fractions=fractions, reps=3, rows=rows, runs=runs))
+    (HERE / "experiment2.json").write_text(json.dumps(cases) + "\n")
+
+
 def main():
     # ---- config 1: the reference's own 2-D blobs (SURVEY App. A)
     d1 = ref.generate(ref.GeneratorSpec("blobs", n=1000, noise=0.3, seed=0, components=3))
@@ -186,4 +248,11 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] == ["generators"]:
+        generators()
+    elif sys.argv[1:] == ["experiment2"]:
+        experiment2()
+    else:
+        main()
+        generators()
+        experiment2()

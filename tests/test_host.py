@@ -51,7 +51,8 @@ class TestABI:
         assert L.gpic_version().decode().endswith("sm_100a")
         assert L.gpic_affinity_pitch(100_000) == 100_000
         assert L.gpic_affinity_pitch(1000) == 1024
-        assert L.gpic_feature_pitch(2) == 32 and L.gpic_feature_pitch(64) == 64
+        assert L.gpic_feature_pitch(2) == 64 and L.gpic_feature_pitch(64) == 64
+        assert L.gpic_feature_pitch(65) == 128
         assert L.gpic_row_pad(1000) % 128 == 0 and L.gpic_row_pad(1000) >= 1000 + 127
         ws = L.gpic_workspace_bytes(100_000, 64, 10, 100_000, 50)
         assert 0 < ws < 2 * 1024**3  # scratch only; A (40 GB) is separate

@@ -131,3 +131,33 @@ def test_zero_vector_error():
     with pytest.raises(po.OracleError) as info:
         po.pic_cluster(np.array(e["points"]), None, 2)
     assert info.value.kind == "ZeroVector" and info.value.index == e["index"]
+
+
+def test_table2_generators_and_subsampler_match_reference():
+    from paper_1604_02700_b200.datasets import generate, subsample_balanced
+
+    g = json.loads((GOLDEN / "generators.json").read_text())
+    assert {c["kind"] for c in g["generate"]} == {"two-moons", "three-circles", "cassine", "shapes",
+                                                  "smiley", "blobs"}
+    for c in g["generate"]:
+        d = generate(c["kind"], c["n"], c["noise"], c["seed"])
+        assert _sha(d.points) == c["points"] and _sha(d.labels) == c["labels"], c
+    for c in g["subsample"]:
+        kind, n, noise, seed = c["base"]
+        sub = subsample_balanced(generate(kind, n, noise, seed), c["fraction"], c["seed"])
+        assert _sha(sub.points) == c["points"] and _sha(sub.labels) == c["labels"]
+        assert sub.name == c["name"]
+
+
+def test_oracle_reproduces_reference_experiment2_runs():
+    from paper_1604_02700_b200.datasets import generate, subsample_balanced
+
+    for case in json.loads((GOLDEN / "experiment2.json").read_text()):
+        d = generate(case["kind"], 45000, 0.05, 0)
+        for run in case["runs"]:
+            sub = subsample_balanced(d, run["fraction"], run["seed"])
+            assert sub.n == run["n"]
+            labels, v, deltas, conv = po.pic_cluster(sub.points, None, case["k"], seed=run["seed"])
+            assert np.array_equal(labels, run["labels"]), (case["kind"], run["fraction"])
+            assert np.max(np.abs(v - run["v"])) <= 1e-12 * np.max(np.abs(run["v"]))
+            assert len(deltas) == run["iterations"]
