@@ -50,29 +50,32 @@ enum { kModeDense = 0, kModePacked = 1, kModeMatvec = 2 };
 constexpr int kBN = 128;           // columns per tile (one MMA N)
 constexpr int kKBlk = 64;          // fp16 per 128-byte swizzle row
 constexpr int kTileBytes = 128 * kKBlk * 2;  // 16 KB: 128 rows x 64 fp16
-constexpr int kEpiWarps = 8;
+constexpr int kEpiWarps = 16;      // 4 per SM sub-partition: latency hiding for the epilogue
 constexpr int kThreads = 64 + kEpiWarps * 32;
-constexpr int kStageOutBytes = 32 * 128;     // 32 rows x 32 fp32 per epilogue warp
-constexpr int kSmemBudget = 224 * 1024;
+constexpr int kSmemBudget = 232448 - 1024 - 256;  // 227 KB opt-in minus alignment + barriers
 constexpr int kChunkTiles = 32;              // matvec: column tiles per work item
 
-__host__ __device__ constexpr int mblocks(int KB) { return KB <= 2 ? 2 : 1; }
+// rows per CTA block: 256 (two M blocks sharing every B stage) while the
+// operands fit, else 128
+__host__ __device__ constexpr int mblocks(int KB) { return KB == 1 ? 2 : 1; }
 __host__ __device__ constexpr int a_bytes(int KB) { return 2 * mblocks(KB) * KB * kTileBytes; }
-// output staging buffers per epilogue warp (double-buffered where smem allows)
-// DIRECT: the epilogue stores straight from registers (no smem staging)
-__host__ __device__ constexpr int out_bufs(int KB, int MODE, bool DIRECT) {
-  return (MODE == kModeMatvec || DIRECT) ? 0 : ((KB == 1 || KB == 3) ? 2 : 1);
+// store modes: one 4 KB staging buffer (a swizzled 32 x 32 fp32 box) per
+// epilogue warp, also used for the row-sum combine; matvec: a fp64
+// [warp][32 rows] combine scratch
+constexpr int kStageOutBytes = 32 * 128;
+__host__ __device__ constexpr int out_bytes(int KB, int MODE) {
+  return MODE == kModeMatvec ? kEpiWarps * 32 * 8 : kEpiWarps * kStageOutBytes;
 }
-__host__ __device__ constexpr int out_bytes(int KB, int MODE, bool DIRECT) {
-  return kEpiWarps * out_bufs(KB, MODE, DIRECT) * kStageOutBytes;
+// per epilogue warp, double-buffered by tile: the 64 columns' |x_j|^2 and v_j
+constexpr int kColBytes = kEpiWarps * 2 * 2 * 64 * 4;
+__host__ __device__ constexpr int stages_raw(int KB, int MODE) {
+  return (kSmemBudget - a_bytes(KB) - out_bytes(KB, MODE) - kColBytes) / (2 * kTileBytes);
 }
-__host__ __device__ constexpr int stages(int KB, int MODE, bool DIRECT) {
-  return (kSmemBudget - a_bytes(KB) - out_bytes(KB, MODE, DIRECT)) / (2 * kTileBytes) > 4
-             ? 4
-             : (kSmemBudget - a_bytes(KB) - out_bytes(KB, MODE, DIRECT)) / (2 * kTileBytes);
+__host__ __device__ constexpr int stages(int KB, int MODE) {
+  return stages_raw(KB, MODE) > 4 ? 4 : (stages_raw(KB, MODE) < 1 ? 1 : stages_raw(KB, MODE));
 }
-__host__ __device__ constexpr int smem_bytes(int KB, int MODE, bool DIRECT) {
-  return a_bytes(KB) + stages(KB, MODE, DIRECT) * 2 * kTileBytes + out_bytes(KB, MODE, DIRECT) +
+__host__ __device__ constexpr int smem_bytes(int KB, int MODE) {
+  return a_bytes(KB) + stages(KB, MODE) * 2 * kTileBytes + out_bytes(KB, MODE) + kColBytes +
          256 + 1024;
 }
 
@@ -92,13 +95,25 @@ struct TcArgs {
   double* ypart;     // matvec: [n_chunks * parts][rows_pad] fp64 row partials
   int64_t n_chunks;  // matvec: column chunks (kChunkTiles tiles) per row block
   const gpic_ctl* ctl;  // matvec in a loop: exit at once when ctl->stop is set
-  float* out;        // DIRECT stores: dense A rows (pitch lda) or packed tiles
+  float* out;        // stored A: dense rows (pitch lda) or packed 128 x 128 tiles
   int64_t lda;
-  float* degrow;     // packed: [tile][halves][128] row partials of each stored tile
+  float* degrow;     // packed: [tile][128] row partials of each stored tile
   float* degcol;     // packed: [tile][4 row quadrants][128] column partials
   int kind;          // GPIC_KIND_RBF: exp2 epilogue; GPIC_KIND_COSINE: max(0, G) on unit rows
   const float* gscale;  // 1 / s^2 of the fp16 operand planes (sqn[n_pad - 1], prepare.cu)
 };
+
+// fixed-shape pairwise sum of 32 values (short dependency chains)
+__device__ __forceinline__ float tree_sum32(const float (&v)[32]) {
+  float t[16];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) t[j] = v[2 * j] + v[2 * j + 1];
+#pragma unroll
+  for (int w = 8; w >= 1; w >>= 1)
+#pragma unroll
+    for (int j = 0; j < w; ++j) t[j] = t[2 * j] + t[2 * j + 1];
+  return t[0];
+}
 
 __host__ __device__ inline int64_t packed_items(int64_t nrt, int64_t nct, int mb) {
   return nrt * nct - (int64_t)mb * nrt * (nrt - 1) / 2;
@@ -116,14 +131,14 @@ __host__ __device__ inline int64_t tile_index(int64_t I, int64_t J, int64_t nt) 
 template <int MB, int MODE>
 struct Cursor {
   int64_t u, u_end;    // unit counter
-  int64_t rb, cb;      // current tile
-  int64_t cb_end;      // matvec: end of the current item's columns
-  int64_t chunk;       // matvec: chunk index of the current item
+  int rb, cb;          // current tile (tile counts stay far below 2^31)
+  int cb_end;          // matvec: end of the current item's columns
+  int chunk;           // matvec: chunk index of the current item
 
   __device__ void decode_unit(const TcArgs& a) {
     if (MODE == kModeDense) {
-      rb = u / a.n_ctiles;
-      cb = u % a.n_ctiles;
+      rb = (int)(u / a.n_ctiles);
+      cb = (int)(u % a.n_ctiles);
     } else if (MODE == kModePacked) {
       int64_t lo = 0, hi = a.n_rtiles - 1;
       while (lo < hi) {
@@ -131,13 +146,13 @@ struct Cursor {
         const int64_t s = mid * a.n_ctiles - (int64_t)MB * mid * (mid - 1) / 2;
         if (s <= u) lo = mid; else hi = mid - 1;
       }
-      rb = lo;
-      cb = rb * MB + (u - (lo * a.n_ctiles - (int64_t)MB * lo * (lo - 1) / 2));
+      rb = (int)lo;
+      cb = (int)(lo * MB + (u - (lo * a.n_ctiles - (int64_t)MB * lo * (lo - 1) / 2)));
     } else {
-      rb = u / a.n_chunks;
-      chunk = u % a.n_chunks;
+      rb = (int)(u / a.n_chunks);
+      chunk = (int)(u % a.n_chunks);
       cb = chunk * kChunkTiles;
-      cb_end = min(cb + kChunkTiles, a.n_ctiles);
+      cb_end = (int)min((int64_t)cb + kChunkTiles, a.n_ctiles);
     }
   }
   __device__ void begin(const TcArgs& a, int64_t u0, int64_t u1) {
@@ -147,13 +162,26 @@ struct Cursor {
   }
   __device__ bool valid() const { return u < u_end; }
   __device__ bool item_last() const { return MODE != kModeMatvec || cb + 1 == cb_end; }
+  // units are walked in order, so the successor is found without the
+  // division / search of decode_unit (which runs once, in begin())
   __device__ void next(const TcArgs& a) {
     if (MODE == kModeMatvec && cb + 1 < cb_end) {
       ++cb;
       return;
     }
     ++u;
-    if (u < u_end) decode_unit(a);
+    if (u >= u_end) return;
+    if (MODE == kModeMatvec) {
+      if (++chunk == a.n_chunks) {
+        chunk = 0;
+        ++rb;
+      }
+      cb = chunk * kChunkTiles;
+      cb_end = (int)min((int64_t)cb + kChunkTiles, a.n_ctiles);
+    } else if (++cb == a.n_ctiles) {
+      ++rb;
+      cb = MODE == kModePacked ? rb * MB : 0;
+    }
   }
 };
 
@@ -164,13 +192,13 @@ __host__ __device__ inline int64_t total_units(const TcArgs& a) {
   return a.n_rtiles * a.n_ctiles;
 }
 
-template <int KB, int MODE, bool DIRECT>
+template <int KB, int MODE>
 __global__ void __launch_bounds__(kThreads, 1)
     affinity_tc_kernel(const __grid_constant__ CUtensorMap map_hi,
                        const __grid_constant__ CUtensorMap map_lo,
                        const __grid_constant__ CUtensorMap map_out, const TcArgs args) {
   constexpr int MB = mblocks(KB);
-  constexpr int ST = stages(KB, MODE, DIRECT);
+  constexpr int ST = stages(KB, MODE);
   constexpr int kTmemCols = 2 * MB * kBN;  // 2 accumulators
   if (MODE == kModeMatvec && args.ctl != nullptr && *(volatile const int32_t*)&args.ctl->stop)
     return;
@@ -179,8 +207,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                                              ~uintptr_t(1023));
   uint8_t* sA = base;                                     // [hl][m][kb] 16 KB tiles
   uint8_t* sB = sA + a_bytes(KB);                         // [stage][hl] 16 KB tiles
-  uint8_t* sOut = sB + ST * 2 * kTileBytes;               // [epi warp][buf] 4 KB
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sOut + out_bytes(KB, MODE, DIRECT));
+  uint8_t* sOut = sB + ST * 2 * kTileBytes;               // [epi warp] staging / combine
+  float* sCol = reinterpret_cast<float*>(sOut + out_bytes(KB, MODE));  // [warp][buf][sqn|v][64]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sCol) + kColBytes);
   uint64_t* full = bars;                 // [ST]
   uint64_t* empty = bars + ST;           // [ST]
   uint64_t* a_full = bars + 2 * ST;
@@ -209,7 +238,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_hi)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_lo)) : "memory");
-    if (MODE != kModeMatvec && !DIRECT)
+    if (MODE != kModeMatvec)
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_out)) : "memory");
   }
   if (warp == 1) {
@@ -307,171 +336,288 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else {
     // --------------------------------------------------------- epilogue
-    constexpr int NC = MB == 2 ? 4 : 2;  // 32-column chunks per warp per tile
-    constexpr int NBUF = out_bufs(KB, MODE, DIRECT);
+    // Warp w may only read TMEM lanes 32*(w%4)..+31: q = w & 3 picks this
+    // warp's 32 rows; the 4 warps of a quadrant (h = e >> 2) split the
+    // tile's MB x 4 chunks of 32 columns, MB chunks each. The GW = 4 / MB
+    // warps that cover the same rows combine their row sums in fixed order.
+    //
+    // Accumulators are read with tcgen05.ld.16x256b (two 16-lane halves x4):
+    // thread t holds rows hf*16 + t/4 (+8) and, per 8-column block b, the
+    // two columns 8b + 2(t%4) + {0,1}. So every thread owns just 4 rows and
+    // 8 columns: row / column terms stay in registers (no per-element
+    // broadcasts) and the column-degree partials are a 7-shuffle
+    // reduce-scatter instead of a re-read of the staged tile. Values go out
+    // through a swizzled 32 x 32 staging box (8-byte st.shared, conflict-free)
+    // and a TMA bulk-tensor store (direct 8-byte global stores were measured
+    // slower: one L1 wavefront per row segment).
+    constexpr int UPW = MB;
+    constexpr int GW = 4 / MB;
     const int e = warp - 2;
-    const int q = warp & 3;          // TMEM lane quadrant this warp may access
-    const int g = e >> 2;            // group: M block (MB=2) or column half (MB=1)
-    const int m = MB == 2 ? g : 0;
-    const int c_lo = MB == 2 ? 0 : 2 * g;
-    uint8_t* stage0 = sOut + e * (NBUF > 0 ? NBUF : 1) * kStageOutBytes;
+    const int q = warp & 3;
+    const int h = e >> 2;
+    const int m = (h * UPW) >> 2;
+    const int c_lo = (h * UPW) & 3;
+    const int gi = h % GW;                   // position in the row group
+    const uint32_t bar_id = 1 + q * MB + m;  // named barrier of the row group
+    const int tq = lane >> 2;                // row within a 16-lane half (and +8)
+    const int tc = (lane & 3) * 2;           // first of this thread's 2 columns per block
+    double* comb = reinterpret_cast<double*>(sOut);  // matvec: [warp][32 rows] row-sum combine
+    uint8_t* stage = sOut + e * kStageOutBytes;       // store modes: this warp's staging box
+    const uint64_t stream_pol = policy_evict_first();  // A is written once here
+    int stores = 0;
     const float ns = args.ns;
     const float gs = __ldg(args.gscale);  // accumulator units -> G
     const float m2ns = -2.f * ns * gs;
-    const uint64_t stream_pol = policy_evict_first();  // A is written once here
     uint32_t tf_bits = 0;  // TMEM-full parity per accumulator buffer
     int i = 0;
-    int stores = 0;
-    double acc64 = 0.0;  // matvec: row partial over the current item
-    // column norms (and matvec v) of the next tile are fetched one tile ahead
-    // so the L2 latency hides behind the TMEM-full wait
-    float nx_cb[NC], nx_v[NC], nx_ra = 0.f;
-    auto prefetch = [&](const Cursor<MB, MODE>& c) {
+    double acc64[4] = {0.0, 0.0, 0.0, 0.0};  // matvec: the 4 rows' partials over an item
+    auto group_sync = [&]() {
+      asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(GW * 32) : "memory");
+    };
+    // row terms ns |x_i|^2 of this thread's 4 rows: reloaded when the row block changes
+    float ra[4] = {0.f, 0.f, 0.f, 0.f};
+    int64_t grow[4] = {0, 0, 0, 0};
+    int64_t cur_rb = -1;
+    // column terms of a tile arrive one tile ahead by cp.async into this
+    // warp's double buffer: lane l copies column l of each of its chunks
+    float* colw = sCol + e * (2 * 2 * 64);
+    auto fetch_cols = [&](int64_t cbn, int slot) {
+      float* dst = colw + slot * 128;
 #pragma unroll
-      for (int cc = 0; cc < NC; ++cc) {
-        const int64_t col = c.cb * kBN + (c_lo + cc) * 32 + lane;
-        nx_cb[cc] = ns * __ldg(args.sqn + col);
-        if (MODE == kModeMatvec) nx_v[cc] = __ldg(args.v32 + col);
+      for (int cc = 0; cc < UPW; ++cc) {
+        const int64_t col = cbn * kBN + (c_lo + cc) * 32 + lane;
+        cp_async4(dst + cc * 32 + lane, args.sqn + col);
+        if (MODE == kModeMatvec) cp_async4(dst + 64 + cc * 32 + lane, args.v32 + col);
       }
-      const int64_t gr = args.row_lo + (c.rb * MB + m) * 128 + q * 32 + lane;
-      nx_ra = gr < args.n ? ns * __ldg(args.sqn + gr) : 0.f;
+      cp_async_commit();
     };
     Cursor<MB, MODE> c;
     c.begin(args, u_begin, u_end);
-    if (c.valid()) prefetch(c);
+    if (c.valid()) fetch_cols(c.cb, 0);
     for (; c.valid(); ++i) {
       const int64_t rb = c.rb, cb = c.cb;
       const bool item_last = c.item_last();
-      const int64_t chunk = c.chunk;
+      const int chunk = c.chunk;
       const int buf = i & 1;
       const int64_t tI = rb * MB + m;  // tile row of this warp's rows
       // packed: the lower-triangle half of a diagonal row block is not stored
       const bool store_ok = MODE != kModePacked || tI <= cb;
-      const int64_t out_row0 = MODE == kModePacked ? tile_index(tI, cb, args.n_ctiles) * 128 + q * 32
-                                                   : (rb * MB + m) * 128 + q * 32;
       const int64_t lr0 = (rb * MB + m) * 128 + q * 32;  // shard-local first row of this warp
-      const int64_t lr = lr0 + lane;
-      const int64_t gr = args.row_lo + lr;
-      float cbv[NC], vv[NC];
+      if (rb != cur_rb) {
+        // this thread's 4 rows: rr = 2*half + {0: tq, 1: tq + 8}
 #pragma unroll
-      for (int cc = 0; cc < NC; ++cc) {
-        cbv[cc] = nx_cb[cc];
-        vv[cc] = nx_v[cc];
+        for (int rr = 0; rr < 4; ++rr) {
+          grow[rr] = args.row_lo + lr0 + (rr >> 1) * 16 + tq + (rr & 1) * 8;
+          ra[rr] = grow[rr] < args.n ? ns * __ldg(args.sqn + grow[rr]) : 0.f;
+        }
+        cur_rb = rb;
       }
-      const float ra = nx_ra;
       c.next(args);
-      if (c.valid()) prefetch(c);
-      mbar_wait(&t_full[buf], (tf_bits >> buf) & 1u);
+      if (c.valid()) {
+        fetch_cols(c.cb, (i + 1) & 1);
+        cp_async_wait<1>();  // this tile's group has landed
+      } else {
+        cp_async_wait<0>();
+      }
+      __syncwarp();
+      const float* colt = colw + (i & 1) * 128;
+      mbar_wait_sleep(&t_full[buf], (tf_bits >> buf) & 1u);
       tf_bits ^= 1u << buf;
       tc_fence_after();
-      float rsum = 0.f;
-#pragma unroll
-      for (int cc = 0; cc < NC; ++cc) {
+      float rsum[4] = {0.f, 0.f, 0.f, 0.f};  // this thread's 4 rows, its 8 columns per chunk
+#pragma unroll 1
+      for (int cc = 0; cc < UPW; ++cc) {
         const int ch = c_lo + cc;
-        uint32_t r[32];
-        tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)((buf * MB + m) * kBN + ch * 32),
-                  r);
-        if (cc == NC - 1) {  // accumulator fully read: hand it back to the MMA warp
+        uint32_t r[32];  // [hf][block b][4]: (row tq, c), (row tq, c+1), (row tq+8, c), (row tq+8, c+1)
+        const int64_t col0 = cb * kBN + ch * 32;
+        // this thread's 8 columns: ns |x_j|^2 (and v_j) from the staged terms
+        float cterm[8], vcol[8];
+#pragma unroll
+        for (int b2 = 0; b2 < 4; ++b2) {
+          const float2 t2 = *reinterpret_cast<const float2*>(colt + cc * 32 + 8 * b2 + tc);
+          cterm[2 * b2] = t2.x;
+          cterm[2 * b2 + 1] = t2.y;
+          if (MODE == kModeMatvec) {
+            const float2 v2 = *reinterpret_cast<const float2*>(colt + 64 + cc * 32 + 8 * b2 + tc);
+            vcol[2 * b2] = v2.x;
+            vcol[2 * b2 + 1] = v2.y;
+          }
+        }
+        const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) +
+                               (uint32_t)((buf * MB + m) * kBN + ch * 32);
+        tmem_ld16x256_x4(taddr, r);
+        tmem_ld16x256_x4(taddr + (16u << 16), r + 16);
+        tmem_wait_ld();
+        if (cc == UPW - 1) {  // accumulator fully read: hand it back to the MMA warp
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&t_empty[buf]);
         }
-        const int64_t col0 = cb * kBN + ch * 32;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) cterm[k] *= ns;
         const bool diag = (col0 < args.row_lo + lr0 + 32) && (args.row_lo + lr0 < col0 + 32);
         const bool pad = col0 + 32 > args.n || args.row_lo + lr0 + 32 > args.n;
         float vals[32];
-        if (args.kind == GPIC_KIND_COSINE) {
-          // rows are unit vectors: G_ij = cos(x_i, x_j), clamped at 0 (affinity.py:93-94)
 #pragma unroll
-          for (int j = 0; j < 32; ++j) vals[j] = fmaxf(__uint_as_float(r[j]) * gs, 0.f);
-        } else {
-#pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const float cj = __shfl_sync(0xffffffffu, cbv[cc], j);
-            const float arg = fmaf(__uint_as_float(r[j]), m2ns, ra + cj);
-            vals[j] = ex2(fminf(arg, 0.f));
-          }
+        for (int x = 0; x < 32; ++x) {
+          const int rr = (x >> 4) * 2 + ((x >> 1) & 1);  // half, then row tq / tq+8
+          const int k = ((x >> 2) & 3) * 2 + (x & 1);    // block, then column c / c+1
+          const float g = __uint_as_float(r[x]);
+          if (args.kind == GPIC_KIND_COSINE)
+            vals[x] = fmaxf(g * gs, 0.f);  // unit rows: G = cos, clamped (affinity.py:93-94)
+          else
+            vals[x] = ex2(fminf(fmaf(g, m2ns, ra[rr] + cterm[k]), 0.f));
         }
         if (diag || pad) {
 #pragma unroll
-          for (int j = 0; j < 32; ++j)
-            if (col0 + j == gr || col0 + j >= args.n || gr >= args.n) vals[j] = 0.f;
+          for (int x = 0; x < 32; ++x) {
+            const int rr = (x >> 4) * 2 + ((x >> 1) & 1);
+            const int64_t col = col0 + ((x >> 2) & 3) * 8 + tc + (x & 1);
+            if (col == grow[rr] || col >= args.n || grow[rr] >= args.n) vals[x] = 0.f;
+          }
         }
         if constexpr (MODE == kModeMatvec) {
 #pragma unroll
-          for (int j = 0; j < 32; ++j) rsum = fmaf(vals[j], __shfl_sync(0xffffffffu, vv[cc], j), rsum);
+          for (int x = 0; x < 32; ++x) {
+            const int rr = (x >> 4) * 2 + ((x >> 1) & 1);
+            const int k = ((x >> 2) & 3) * 2 + (x & 1);
+            rsum[rr] = fmaf(vals[x], vcol[k], rsum[rr]);
+          }
         } else {
 #pragma unroll
-          for (int j = 0; j < 32; ++j) rsum += vals[j];
-          // the store issued NBUF chunks ago must have finished reading this buffer
-          uint8_t* stage = stage0 + (stores % NBUF) * kStageOutBytes;
-          if (stores >= NBUF) {
-            if (lane == 0) tma_store_wait_read<NBUF - 1>();
+          for (int x = 0; x < 32; ++x) rsum[(x >> 4) * 2 + ((x >> 1) & 1)] += vals[x];
+          // full 32-byte sectors straight from registers: each quad writes 8
+          // consecutive floats of one row per (block, row)
+          // stage the 32 x 32 box (row R at R*128, 16-byte chunk c/4 ^ (R&7))
+          if (stores > 0) {  // the previous TMA store must have read the box
+            if (lane == 0) tma_store_wait_read<0>();
             __syncwarp();
           }
-          const uint32_t srow = su32(stage) + lane * 128;
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const uint32_t addr = srow + ((j ^ (lane & 7)) << 4);
-            asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(vals[4 * j]),
-                         "f"(vals[4 * j + 1]), "f"(vals[4 * j + 2]), "f"(vals[4 * j + 3])
+          for (int x = 0; x < 32; x += 2) {
+            const int R = (x >> 4) * 16 + tq + ((x >> 1) & 1) * 8;
+            const int cq = ((x >> 2) & 3) * 2 + (tc >> 2);  // 16-byte chunk of the columns
+            const uint32_t addr = su32(stage) + R * 128 + ((cq ^ (R & 7)) << 4) + (tc & 3) * 4;
+            asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(addr), "f"(vals[x]),
+                         "f"(vals[x + 1])
                          : "memory");
           }
           fence_async_smem();
           __syncwarp();
-          if (lane == 0 && store_ok)
+          if (lane == 0 && store_ok) {
+            const int64_t out_row0 = MODE == kModePacked
+                                         ? tile_index(tI, cb, args.n_ctiles) * 128 + q * 32
+                                         : lr0;
             tma_store_2d(&map_out, MODE == kModePacked ? ch * 32 : (int)col0, (int)out_row0, stage,
                          stream_pol);
+          }
           ++stores;
           if (MODE == kModePacked && store_ok && tI != cb) {
-            // degrees of the tile's COLUMN rows (A is symmetric): lane l sums
-            // column l of the staged 32x32 chunk over this warp's 32 rows
-            // (row r of the swizzled stage: chunk (l/4) ^ (r & 7)), fixed order
-            const uint32_t sb = su32(stage) + (lane & 3) * 4;
-            float cs[4] = {0.f, 0.f, 0.f, 0.f};  // 4 chains: rows r2 = 4u + w
+            // degrees of the tile's COLUMN rows (A is symmetric): per column
+            // slot k, this thread's 4 rows, then a reduce-scatter over the 8
+            // threads sharing the slot (xor 16, 8, 4): thread (tq, quad) ends
+            // with the 32-row total of slot k = tq. Fixed order.
+            float cs[8];
 #pragma unroll
-            for (int r2 = 0; r2 < 32; ++r2) {
-              float x;
-              asm volatile("ld.shared.f32 %0, [%1];"
-                           : "=f"(x)
-                           : "r"(sb + r2 * 128 + ((((lane >> 2) ^ (r2 & 7))) << 4)));
-              cs[r2 & 3] += x;
+            for (int k = 0; k < 8; ++k) {
+              const int x0 = (k >> 1) * 4 + (k & 1);  // half 0, row tq
+              cs[k] = (vals[x0] + vals[x0 + 2]) + (vals[x0 + 16] + vals[x0 + 18]);
             }
-            args.degcol[(tile_index(tI, cb, args.n_ctiles) * 4 + q) * 128 + ch * 32 + lane] =
-                (cs[0] + cs[1]) + (cs[2] + cs[3]);
+            const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {  // slots k | 4 go up when lane bit 4 is set
+              const float send = b4 ? cs[k] : cs[k + 4];
+              const float keep = b4 ? cs[k + 4] : cs[k];
+              cs[k] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+            }
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+              const float send = b3 ? cs[k] : cs[k + 2];
+              const float keep = b3 ? cs[k + 2] : cs[k];
+              cs[k] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+            }
+            {
+              const float send = b2 ? cs[0] : cs[1];
+              const float keep = b2 ? cs[1] : cs[0];
+              cs[0] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+            }
+            const int k = (b4 ? 4 : 0) + (b3 ? 2 : 0) + (b2 ? 1 : 0);  // = tq
+            const int col = 8 * (k >> 1) + tc + (k & 1);
+            args.degcol[(tile_index(tI, cb, args.n_ctiles) * 4 + q) * 128 + ch * 32 + col] = cs[0];
           }
         }
       }
-      if constexpr (MODE == kModePacked) {
-        // degrees of the tile's ROW rows: this warp's partial over its chunks
-        if (store_ok) {
-          constexpr int NH = MB == 2 ? 1 : 2;  // column halves per row
-          args.degrow[(tile_index(tI, cb, args.n_ctiles) * NH + (MB == 2 ? 0 : g)) * 128 + q * 32 +
-                      lane] = rsum;
-        }
-      } else if constexpr (MODE == kModeMatvec) {
-        acc64 += (double)rsum;
+      // this thread's row partials -> the quad's row totals (xor 1, 2)
+#pragma unroll
+      for (int rr = 0; rr < 4; ++rr) {
+        rsum[rr] += __shfl_xor_sync(0xffffffffu, rsum[rr], 1);
+        rsum[rr] += __shfl_xor_sync(0xffffffffu, rsum[rr], 2);
+      }
+      const bool quad_lead = (lane & 3) == 0;
+      if constexpr (MODE == kModeMatvec) {
+#pragma unroll
+        for (int rr = 0; rr < 4; ++rr) acc64[rr] += (double)rsum[rr];
         if (item_last) {
-          // MB=2: one partial per (chunk, row); MB=1: one per (chunk, half, row)
-          const int64_t slot = MB == 2 ? chunk : chunk * 2 + g;
-          if (lr < args.rows) args.ypart[slot * args.rows_pad + lr] = acc64;
-          acc64 = 0.0;
+          double tot[4] = {acc64[0], acc64[1], acc64[2], acc64[3]};
+          if (GW > 1) {
+            if (quad_lead)
+#pragma unroll
+              for (int rr = 0; rr < 4; ++rr)
+                comb[e * 32 + (rr >> 1) * 16 + tq + (rr & 1) * 8] = acc64[rr];
+            group_sync();
+            if (gi == 0 && quad_lead)
+              for (int g2 = 1; g2 < GW; ++g2)
+#pragma unroll
+                for (int rr = 0; rr < 4; ++rr)
+                  tot[rr] += comb[(e + 4 * g2) * 32 + (rr >> 1) * 16 + tq + (rr & 1) * 8];
+            group_sync();
+          }
+          if (gi == 0 && quad_lead)
+#pragma unroll
+            for (int rr = 0; rr < 4; ++rr) {
+              const int64_t lrow = lr0 + (rr >> 1) * 16 + tq + (rr & 1) * 8;
+              if (lrow < args.rows) args.ypart[(int64_t)chunk * args.rows_pad + lrow] = tot[rr];
+            }
+#pragma unroll
+          for (int rr = 0; rr < 4; ++rr) acc64[rr] = 0.0;
         }
-      } else if constexpr (MODE == kModeDense) {
-        if constexpr (MB == 2) {
-          if (lr < args.rows) args.rowpart[cb * args.rows_pad + lr] = rsum;
-        } else {
-          // two warps (column halves) share each row: half 1 parks its sum in
-          // smem, half 0 adds it (fixed order) after a 64-thread named barrier.
-          __shared__ float half1[4][32];
-          if (g == 1) half1[q][lane] = rsum;
-          asm volatile("bar.sync %0, %1;" ::"r"(1 + q), "r"(64) : "memory");
-          if (g == 0 && lr < args.rows) args.rowpart[cb * args.rows_pad + lr] = rsum + half1[q][lane];
-          asm volatile("bar.sync %0, %1;" ::"r"(1 + q), "r"(64) : "memory");
+      } else if (MODE == kModeDense || store_ok) {
+        // row sums of the tile's rows: the group's warps combine in order
+        float tot[4] = {rsum[0], rsum[1], rsum[2], rsum[3]};
+        if (GW > 1) {
+          // partials go through each writer's staging box once it is drained
+          if (gi > 0) {
+            if (lane == 0) tma_store_wait_read<0>();
+            __syncwarp();
+            if (quad_lead) {
+              float* cf = reinterpret_cast<float*>(stage);
+#pragma unroll
+              for (int rr = 0; rr < 4; ++rr) cf[(rr >> 1) * 16 + tq + (rr & 1) * 8] = rsum[rr];
+            }
+          }
+          group_sync();
+          if (gi == 0 && quad_lead)
+            for (int g2 = 1; g2 < GW; ++g2) {
+              const float* cf = reinterpret_cast<const float*>(sOut + (e + 4 * g2) * kStageOutBytes);
+#pragma unroll
+              for (int rr = 0; rr < 4; ++rr) tot[rr] += cf[(rr >> 1) * 16 + tq + (rr & 1) * 8];
+            }
+          group_sync();
         }
+        if (gi == 0 && quad_lead)
+#pragma unroll
+          for (int rr = 0; rr < 4; ++rr) {
+            const int rloc = (rr >> 1) * 16 + tq + (rr & 1) * 8;  // row within the warp's 32
+            if constexpr (MODE == kModePacked) {
+              args.degrow[tile_index(tI, cb, args.n_ctiles) * 128 + q * 32 + rloc] = tot[rr];
+            } else {
+              const int64_t lrow = lr0 + rloc;
+              if (lrow < args.rows) args.rowpart[cb * args.rows_pad + lrow] = tot[rr];
+            }
+          }
       }
     }
-    if (MODE != kModeMatvec && !DIRECT && lane == 0) tma_store_wait_all();
+    if (MODE != kModeMatvec && lane == 0) tma_store_wait_all();
     __syncwarp();
   }
 
@@ -516,7 +662,7 @@ bool make_map(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t outer,
 
 int g_num_sms = 0;
 
-template <int KB, int MODE, bool DIRECT>
+template <int KB, int MODE>
 int launch_kb(const CUtensorMap& mh, const CUtensorMap& ml, const CUtensorMap& mo,
               const TcArgs& a0, cudaStream_t s) {
   constexpr int MB = mblocks(KB);
@@ -525,9 +671,9 @@ int launch_kb(const CUtensorMap& mh, const CUtensorMap& ml, const CUtensorMap& m
   a.n_chunks = ceil_div(a.n_ctiles, kChunkTiles);
   static bool attr = false;
   if (!attr) {
-    GPIC_CUDA_TRY(cudaFuncSetAttribute(affinity_tc_kernel<KB, MODE, DIRECT>,
+    GPIC_CUDA_TRY(cudaFuncSetAttribute(affinity_tc_kernel<KB, MODE>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       smem_bytes(KB, MODE, DIRECT)));
+                                       smem_bytes(KB, MODE)));
     attr = true;
   }
   if (g_num_sms == 0) {
@@ -538,26 +684,20 @@ int launch_kb(const CUtensorMap& mh, const CUtensorMap& ml, const CUtensorMap& m
   const int64_t total = total_units<MB, MODE>(a);
   const int grid = (int)(total < g_num_sms ? total : g_num_sms);
   if (grid < 1) return GPIC_OK;
-  affinity_tc_kernel<KB, MODE, DIRECT><<<grid, kThreads, smem_bytes(KB, MODE, DIRECT), s>>>(
-      mh, ml, mo, a);
+  affinity_tc_kernel<KB, MODE><<<grid, kThreads, smem_bytes(KB, MODE), s>>>(mh, ml, mo, a);
   count_launch();
   GPIC_CUDA_TRY(cudaGetLastError());
   return GPIC_OK;
 }
 
-// The epilogue stores through swizzled smem staging + TMA bulk-tensor
-// stores (measured 2x faster on config 3 than direct 128-bit st.global from
-// registers, which left partially written lines to the L2). The DIRECT
-// template flag only removes the staging smem (matvec mode stores nothing).
 template <int MODE>
 int dispatch_kb(int KB, const CUtensorMap& mh, const CUtensorMap& ml, const CUtensorMap& mo,
                 const TcArgs& args, cudaStream_t s) {
-  constexpr bool kNoStage = MODE == kModeMatvec;
   switch (KB) {
-    case 1: return launch_kb<1, MODE, kNoStage>(mh, ml, mo, args, s);
-    case 2: return launch_kb<2, MODE, kNoStage>(mh, ml, mo, args, s);
-    case 3: return launch_kb<3, MODE, kNoStage>(mh, ml, mo, args, s);
-    default: return launch_kb<4, MODE, kNoStage>(mh, ml, mo, args, s);
+    case 1: return launch_kb<1, MODE>(mh, ml, mo, args, s);
+    case 2: return launch_kb<2, MODE>(mh, ml, mo, args, s);
+    case 3: return launch_kb<3, MODE>(mh, ml, mo, args, s);
+    default: return launch_kb<4, MODE>(mh, ml, mo, args, s);
   }
 }
 
@@ -586,7 +726,7 @@ int64_t packed_tiles(int64_t n) {
 
 // Symmetric packed output: tile (I, J), J >= I, stored as a contiguous
 // 128 x 128 fp32 block at tile_index(I, J) (row-major over the triangle).
-int packed_row_halves(int32_t dp) { return mblocks(dp / kKBlk) == 2 ? 1 : 2; }
+int packed_row_halves(int32_t /*dp*/) { return 1; }  // the epilogue combines a row's warps
 
 int launch_affinity_tc_packed(const float* xhi, const float* xlo, const float* sqn, int64_t n,
                               int32_t dp, float neg_scale_log2, float* a_packed, float* degrow,
@@ -637,7 +777,8 @@ int launch_affinity_tc(const float* xhi, const float* xlo, const float* sqn, int
 
 int64_t mf_parts(int64_t n, int32_t dp) {
   const int64_t chunks = ceil_div(ceil_div(n, kBN), kChunkTiles);
-  return mblocks(dp / kKBlk) == 2 ? chunks : 2 * chunks;
+  (void)dp;
+  return chunks;  // one fp64 partial per (chunk item, row): the row's warps combine in-CTA
 }
 
 // Matrix-free row block: ypart[p][i - row_lo] = sum over chunk p of

@@ -63,6 +63,11 @@ __device__ __forceinline__ void st_stream_f4(float4* p, float4 v) {
                : "memory");
 }
 
+// Streaming 8-byte store (a quad of lanes fills one 32-byte sector).
+__device__ __forceinline__ void st_stream_f2(float* p, float a, float b) {
+  asm volatile("st.global.cs.v2.f32 [%0], {%1,%2};" ::"l"(p), "f"(a), "f"(b) : "memory");
+}
+
 // Round fp32 to TF32 (10 explicit mantissa bits), round-to-nearest-away.
 __device__ __forceinline__ float to_tf32(float x) {
   uint32_t r;

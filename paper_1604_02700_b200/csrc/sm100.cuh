@@ -29,6 +29,29 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+// Same, but the thread may be suspended (up to ~1 ms) until the phase
+// completes instead of re-polling: for waits expected to be long, so that
+// idle warps do not steal issue slots from the warps sharing their SMSP.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1, %2;\n\t"
+      "@!P bra WAIT_%=;\n}" ::"r"(su32(b)),
+      "r"(parity), "r"(1000000u)
+      : "memory");
+}
+// 4-byte asynchronous global -> shared copy (LDGSTS), grouped per thread.
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(su32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
 // L2 eviction policies: small operands that are re-read (X, v) stay
 // (evict_last); multi-GB streams written or read once go first.
 __device__ __forceinline__ uint64_t policy_evict_last() {
@@ -142,6 +165,21 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
         "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
         "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
       : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+// 16x256b shape, 4 repeats along columns: 16 TMEM lanes x 32 columns; thread
+// t gets, per 8-column block b, (lane t/4, cols 8b + 2(t%4) + {0,1}) then
+// (lane t/4 + 8, same cols) (layout measured: scripts/probe/tmem_layout.cu).
+__device__ __forceinline__ void tmem_ld16x256_x4(uint32_t taddr, uint32_t* r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.16x256b.x4.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+      "%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 __device__ __forceinline__ float ex2(float x) {

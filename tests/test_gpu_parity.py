@@ -116,8 +116,10 @@ def test_affinity_rows_and_degree(golden, engine):
             assert got[int(r)] == 0.0
             assert np.max(np.abs(got - row)) <= 1e-4 * max(row.max(), 1e-30) + 1e-30
         # exact symmetry is a property of the formula; the fp32 engines keep it
-        # to Gram rounding (G_ij and G_ji are accumulated in different orders)
-        assert np.max(np.abs(full - full.T)) <= 1e-5
+        # to Gram rounding (G_ij and G_ji are accumulated in different orders):
+        # one fp32 ulp of |x|^2 in d2 is a RELATIVE error of A, so the bound is
+        # relative (App-B rows have |x|^2 ~ 1.7e3, sigma = 2: ~2e-5 observed)
+        assert np.all(np.abs(full - full.T) <= 1e-4 * np.maximum(full, full.T) + 1e-12)
 
 
 @pytest.mark.parametrize("engine", ENGINES)
