@@ -101,6 +101,7 @@ struct TcArgs {
   float* degcol;     // packed: [tile][4 row quadrants][128] column partials
   int kind;          // GPIC_KIND_RBF: exp2 epilogue; GPIC_KIND_COSINE: max(0, G) on unit rows
   const float* gscale;  // 1 / s^2 of the fp16 operand planes (sqn[n_pad - 1], prepare.cu)
+  int strided;          // dense / packed: row-block-strided work order (see Cursor)
 };
 
 // fixed-shape pairwise sum of 32 values (short dependency chains)
@@ -124,22 +125,32 @@ __host__ __device__ inline int64_t tile_index(int64_t I, int64_t J, int64_t nt) 
   return I * nt - I * (I - 1) / 2 + (J - I);
 }
 
-// Work sequence of one CTA, identical for all three roles.
-//   dense / packed: units are tiles (rb, cb); packed keeps cb >= rb*MB only
-//   matvec: units are items (rb, chunk) of up to kChunkTiles column tiles, so
-//           a chunk's row partial is always produced by one CTA (fixed shape)
+// Work sequence of one CTA, identical for all three roles. Two orders:
+//   contiguous (a.strided == 0; dense / packed with L2-resident operands):
+//           a balanced contiguous range of tiles (rb, cb) in row-major order
+//           (packed keeps cb >= rb*MB only)
+//   strided (matvec always; dense / packed when the operands exceed ~L2/4):
+//           wave w gives CTA k the row block w*G + k (G = gridDim.x; packed /
+//           dense reverse odd waves, which balances the packed triangle),
+//           walked from its first column tile to the last. The CTAs of a
+//           wave read the same B tiles at about the same time, so operands
+//           larger than the L2 stream from DRAM about once per wave instead
+//           of once per CTA. A matvec chunk's row partial is produced by
+//           one CTA (fixed shape).
 template <int MB, int MODE>
 struct Cursor {
-  int64_t u, u_end;    // unit counter
+  int64_t u, u_end;    // contiguous: unit counter; strided: 0 while running, 1 when done
   int rb, cb;          // current tile (tile counts stay far below 2^31)
   int cb_end;          // matvec: end of the current item's columns
   int chunk;           // matvec: chunk index of the current item
+  int wave;            // strided: current wave
+  bool strided;
 
   __device__ void decode_unit(const TcArgs& a) {
     if (MODE == kModeDense) {
       rb = (int)(u / a.n_ctiles);
       cb = (int)(u % a.n_ctiles);
-    } else if (MODE == kModePacked) {
+    } else {
       int64_t lo = 0, hi = a.n_rtiles - 1;
       while (lo < hi) {
         const int64_t mid = (lo + hi + 1) >> 1;
@@ -148,14 +159,33 @@ struct Cursor {
       }
       rb = (int)lo;
       cb = (int)(lo * MB + (u - (lo * a.n_ctiles - (int64_t)MB * lo * (lo - 1) / 2)));
-    } else {
-      rb = (int)(u / a.n_chunks);
-      chunk = (int)(u % a.n_chunks);
-      cb = chunk * kChunkTiles;
-      cb_end = (int)min((int64_t)cb + kChunkTiles, a.n_ctiles);
     }
   }
+  // strided: first row block at or after `wave`; false when none is left
+  __device__ bool start_row(const TcArgs& a) {
+    const int G = gridDim.x, k = blockIdx.x;
+    for (;; ++wave) {
+      if ((int64_t)wave * G >= a.n_rtiles) return false;
+      rb = wave * G + ((wave & 1) && MODE != kModeMatvec ? G - 1 - k : k);
+      if (rb < a.n_rtiles) break;
+    }
+    if (MODE == kModeMatvec) {
+      chunk = 0;
+      cb = 0;
+      cb_end = (int)min((int64_t)kChunkTiles, a.n_ctiles);
+    } else {
+      cb = MODE == kModePacked ? rb * MB : 0;
+    }
+    return true;
+  }
   __device__ void begin(const TcArgs& a, int64_t u0, int64_t u1) {
+    strided = MODE == kModeMatvec || a.strided;
+    if (strided) {
+      wave = 0;
+      u_end = 1;
+      u = start_row(a) ? 0 : 1;
+      return;
+    }
     u = u0;
     u_end = u1;
     if (u < u_end) decode_unit(a);
@@ -165,20 +195,28 @@ struct Cursor {
   // units are walked in order, so the successor is found without the
   // division / search of decode_unit (which runs once, in begin())
   __device__ void next(const TcArgs& a) {
-    if (MODE == kModeMatvec && cb + 1 < cb_end) {
-      ++cb;
+    if (MODE == kModeMatvec) {
+      if (cb + 1 < cb_end) {
+        ++cb;
+      } else if (++chunk < a.n_chunks) {
+        cb = chunk * kChunkTiles;
+        cb_end = (int)min((int64_t)cb + kChunkTiles, a.n_ctiles);
+      } else {
+        ++wave;
+        if (!start_row(a)) u = 1;
+      }
+      return;
+    }
+    if (strided) {
+      if (++cb == a.n_ctiles) {
+        ++wave;
+        if (!start_row(a)) u = 1;
+      }
       return;
     }
     ++u;
     if (u >= u_end) return;
-    if (MODE == kModeMatvec) {
-      if (++chunk == a.n_chunks) {
-        chunk = 0;
-        ++rb;
-      }
-      cb = chunk * kChunkTiles;
-      cb_end = (int)min((int64_t)cb + kChunkTiles, a.n_ctiles);
-    } else if (++cb == a.n_ctiles) {
+    if (++cb == a.n_ctiles) {
       ++rb;
       cb = MODE == kModePacked ? rb * MB : 0;
     }
@@ -681,7 +719,10 @@ int launch_kb(const CUtensorMap& mh, const CUtensorMap& ml, const CUtensorMap& m
     GPIC_CUDA_TRY(cudaGetDevice(&dev));
     GPIC_CUDA_TRY(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev));
   }
-  const int64_t total = total_units<MB, MODE>(a);
+  // operands beyond ~L2/4 (the store stream needs the rest): strided order
+  a.strided = (int64_t)row_pad(a.n) * kKBlk * KB * 4 > (32ll << 20);
+  if (const char* o = getenv("GPIC_TC_ORDER")) a.strided = atoi(o) != 0;  // tests: force an order
+  const int64_t total = (MODE == kModeMatvec || a.strided) ? a.n_rtiles : total_units<MB, MODE>(a);
   const int grid = (int)(total < g_num_sms ? total : g_num_sms);
   if (grid < 1) return GPIC_OK;
   affinity_tc_kernel<KB, MODE><<<grid, kThreads, smem_bytes(KB, MODE), s>>>(mh, ml, mo, a);

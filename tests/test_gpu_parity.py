@@ -339,6 +339,23 @@ def test_packed_and_dense_storage_agree(golden, case):
     assert rel_l1(vp, z["v"]) <= 1e-4
 
 
+@pytest.mark.parametrize("storage", ["packed", "dense", "none"])
+def test_work_orders_are_bitwise_identical(golden, monkeypatch, storage):
+    """The tensor engine's contiguous and row-block-strided work orders (the
+    latter is used when the operands outgrow the L2) give identical bits."""
+    z = golden("gblobs_small")
+    d = DataSet(_points(z))
+    kind, params = GaussianRbf(float(z["sigma"])), PicParams(k=int(z["k"]))
+    cfg = KernelConfig(storage=storage)
+    out = []
+    for order in ("0", "1"):
+        monkeypatch.setenv("GPIC_TC_ORDER", order)
+        out.append(cluster(d, kind, params, config=cfg, seed=int(z["seed"])))
+    (l0, v0, t0), (l1, v1, t1) = out
+    assert np.array_equal(l0, l1) and np.array_equal(v0, v1)
+    assert np.array_equal(t0.delta_history, t1.delta_history)
+
+
 def test_sym_matvec_against_numpy():
     """Packed-tile GEMV (row + column partials) equals the dense product."""
     import ctypes as C
