@@ -227,7 +227,7 @@ def _gemv_roofline(args, L, C, torch, stream, st, n, m, k, T, work, v, storage):
         npad = int(L.gpic_row_pad(n))
         # xhi / xlo / sqn live at the head of the workspace (after the ctl)
         xhi = work.data_ptr() + 256
-        xlo = xhi + ((npad * dp * 4 + 255) // 256) * 256
+        xlo = xhi + ((int(L.gpic_operand_floats(n, m)) * 4 + 255) // 256) * 256
         sqn = xlo + ((npad * dp * 4 + 255) // 256) * 256
         ypart = torch.empty(int(L.gpic_mf_ypart_doubles(n, m, n)), dtype=torch.float64, device=dev)
         ones = torch.empty(vp, dtype=torch.float32, device=dev)

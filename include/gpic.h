@@ -88,11 +88,17 @@ int64_t gpic_affinity_pitch(int64_t n);
 
 /* ---- stage 0: validate + centre + cast -------------------------------
  * Replaces validate_dataset's finiteness scan (data.py:61-78) and prepares
- * the operands of the Gram engines. Both buffers hold n_pad x dp floats
- * (dp = gpic_feature_pitch(d), n_pad = gpic_row_pad(n)):
- *   d_xlo  xc = fp32(x - mean_fp64), row-major (the FFMA engine)
- *   d_xhi  the tensor engine's fp16 planes: hi = fp16(xc * s) (n_pad x dp
- *          halves) then lo = fp16(xc * s - hi); s = 2^e, max|xc * s| < 2^14
+ * the operands of the Gram engines (dp = gpic_feature_pitch(d),
+ * n_pad = gpic_row_pad(n)):
+ *   d_xlo  n_pad x dp floats: xc = fp32(x - mean_fp64), row-major (the FFMA
+ *          engine)
+ *   d_xhi  gpic_operand_floats(n, d) floats: the tensor engine's fp16
+ *          planes hi = fp16(xc * s) (n_pad x dp halves) then
+ *          lo = fp16(xc * s - hi); s = 2^e, max|xc * s| < 2^8; then the
+ *          norm block (4 planes of n_pad x 16 halves: row operand hi / lo
+ *          [2^10, M_i], column operand hi / lo [M_j, 2^10],
+ *          M = -(s^2/2)|x~|^2 / 2^10) with which the MMA accumulates
+ *          -(s^2/2)|x_i - x_j|^2 directly
  *   d_sqn  |xc|^2 per row; d_sqn[n_pad - 1] (a padding row) holds 1 / s^2
  * A non-finite entry sets GPIC_E_NONFINITE with the first (row, col) in
  * row-major order. d_work: (ceil(n / 256) + 1) * d + 1 doubles.
@@ -101,6 +107,7 @@ int64_t gpic_affinity_pitch(int64_t n);
  * row as GPIC_E_ZERO_VECTOR(first row) (cosine_norms, affinity.py:41-53). */
 int32_t gpic_feature_pitch(int32_t d);
 int64_t gpic_row_pad(int64_t n);
+int64_t gpic_operand_floats(int64_t n, int32_t d);
 int gpic_prepare_points(const double* d_x, int64_t n, int32_t d, int32_t kind, float* d_xhi,
                         float* d_xlo, float* d_sqn, void* d_work, gpic_ctl* d_ctl, void* stream);
 

@@ -73,6 +73,7 @@ SIGNATURES = {
     "gpic_affinity_pitch": (I64, [I64]),
     "gpic_feature_pitch": (I32, [I32]),
     "gpic_row_pad": (I64, [I64]),
+    "gpic_operand_floats": (I64, [I64, I32]),
     "gpic_ctl_init": (C.c_int, [P, F64, I32, P]),
     "gpic_prepare_points": (C.c_int, [P, I64, I32, I32, P, P, P, P, P, P]),
     "gpic_affinity_rbf": (C.c_int, [P, P, P, I64, I32, I64, I64, F64, I32, P, I64, P, P, P, P]),

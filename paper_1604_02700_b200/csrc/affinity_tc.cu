@@ -18,9 +18,14 @@
 //   matvec  matrix-free: nothing is stored; each element is
 //           multiplied by v_j in registers and row sums are accumulated per
 //           32-tile column chunk (fp64) -> ypart; A v is recomputed every
-//           iteration when n^2 does not fit HBM
+//           iteration when n^2 does not fit HBM.
+//           sym (whole matrix on one rank): only tiles J >= I are computed
+//           (A is exactly symmetric); each off-diagonal tile also yields the
+//           column partials sum_i a_ij v_i (its transpose's row partials),
+//           combined across the CTA's warps in fixed order -> colpart, one
+//           128-float record per (row block, column tile). Half the work.
 //
-// Persistent warp-specialised kernel, one CTA per SM (320 threads):
+// Persistent warp-specialised kernel, one CTA per SM (576 threads):
 //   warp 0      TMA producer: the CTA's row block (MB x 128 rows, hi + lo,
 //               all K) stays resident in smem while the CTA walks its
 //               contiguous range of column tiles; B tiles (128 columns,
@@ -29,7 +34,7 @@
 //   warp 1      TMEM owner + single-thread MMA issuer: 3 x 4 x KB MMAs per
 //               M block into one of two TMEM accumulators (double buffer,
 //               so the next tile's MMAs overlap this tile's epilogue).
-//   warps 2-9   epilogue: tcgen05.ld 32 columns at a time, exp2 + masks +
+//   warps 2-17  epilogue: tcgen05.ld 32 columns at a time, exp2 + masks +
 //               row sums in registers; store modes go through swizzled
 //               st.shared and TMA bulk-tensor stores of 32x32 fp32 boxes.
 #include <cuda.h>
@@ -58,24 +63,34 @@ constexpr int kChunkTiles = 32;              // matvec: column tiles per work it
 // rows per CTA block: 256 (two M blocks sharing every B stage) while the
 // operands fit, else 128
 __host__ __device__ constexpr int mblocks(int KB) { return KB == 1 ? 2 : 1; }
-__host__ __device__ constexpr int a_bytes(int KB) { return 2 * mblocks(KB) * KB * kTileBytes; }
+// norm block (prepare.cu): per 128-row tile, hi + lo planes of 128 x 16 fp16
+// (32-byte swizzle), one extra K = 16 step that adds -(s^2/2)(|x_i|^2+|x_j|^2)
+constexpr int kNrmPlane = 128 * 16 * 2;   // 4 KB
+constexpr int kNrmBytes = 2 * kNrmPlane;  // hi + lo
+__host__ __device__ constexpr int a_main_bytes(int KB) { return 2 * mblocks(KB) * KB * kTileBytes; }
+__host__ __device__ constexpr int a_bytes(int KB) { return a_main_bytes(KB) + mblocks(KB) * kNrmBytes; }
+constexpr int kStageBytes = 2 * kTileBytes + kNrmBytes;  // B hi, B lo, B norm block
 // store modes: one 4 KB staging buffer (a swizzled 32 x 32 fp32 box) per
 // epilogue warp, also used for the row-sum combine; matvec: a fp64
-// [warp][32 rows] combine scratch
+// [warp][32 rows] combine scratch + the sym column-partial exchange
+// [tile parity][m][quadrant][128 columns] fp32
 constexpr int kStageOutBytes = 32 * 128;
+__host__ __device__ constexpr int colx_bytes(int KB) { return 2 * mblocks(KB) * 4 * 128 * 4; }
 __host__ __device__ constexpr int out_bytes(int KB, int MODE) {
-  return MODE == kModeMatvec ? kEpiWarps * 32 * 8 : kEpiWarps * kStageOutBytes;
+  return MODE == kModeMatvec ? kEpiWarps * 32 * 8 + colx_bytes(KB) : kEpiWarps * kStageOutBytes;
 }
-// per epilogue warp, double-buffered by tile: the 64 columns' |x_j|^2 and v_j
-constexpr int kColBytes = kEpiWarps * 2 * 2 * 64 * 4;
+// matvec: per epilogue warp, double-buffered by tile, the 64 columns' v_j
+__host__ __device__ constexpr int col_bytes(int MODE) {
+  return MODE == kModeMatvec ? kEpiWarps * 2 * 64 * 4 : 0;
+}
 __host__ __device__ constexpr int stages_raw(int KB, int MODE) {
-  return (kSmemBudget - a_bytes(KB) - out_bytes(KB, MODE) - kColBytes) / (2 * kTileBytes);
+  return (kSmemBudget - a_bytes(KB) - out_bytes(KB, MODE) - col_bytes(MODE)) / kStageBytes;
 }
 __host__ __device__ constexpr int stages(int KB, int MODE) {
   return stages_raw(KB, MODE) > 4 ? 4 : (stages_raw(KB, MODE) < 1 ? 1 : stages_raw(KB, MODE));
 }
 __host__ __device__ constexpr int smem_bytes(int KB, int MODE) {
-  return a_bytes(KB) + stages(KB, MODE) * 2 * kTileBytes + out_bytes(KB, MODE) + kColBytes +
+  return a_bytes(KB) + stages(KB, MODE) * kStageBytes + out_bytes(KB, MODE) + col_bytes(MODE) +
          256 + 1024;
 }
 
@@ -102,6 +117,9 @@ struct TcArgs {
   int kind;          // GPIC_KIND_RBF: exp2 epilogue; GPIC_KIND_COSINE: max(0, G) on unit rows
   const float* gscale;  // 1 / s^2 of the fp16 operand planes (sqn[n_pad - 1], prepare.cu)
   int strided;          // dense / packed: row-block-strided work order (see Cursor)
+  int64_t n_pad;        // rows per operand plane (the norm block's plane stride)
+  int sym;              // matvec: upper-triangle tiles only, column partials -> colpart
+  float* colpart;       // matvec sym: [packed (row block, column tile)][128] fp32
 };
 
 // fixed-shape pairwise sum of 32 values (short dependency chains)
@@ -166,13 +184,13 @@ struct Cursor {
     const int G = gridDim.x, k = blockIdx.x;
     for (;; ++wave) {
       if ((int64_t)wave * G >= a.n_rtiles) return false;
-      rb = wave * G + ((wave & 1) && MODE != kModeMatvec ? G - 1 - k : k);
+      rb = wave * G + ((wave & 1) && (MODE != kModeMatvec || a.sym) ? G - 1 - k : k);
       if (rb < a.n_rtiles) break;
     }
     if (MODE == kModeMatvec) {
-      chunk = 0;
-      cb = 0;
-      cb_end = (int)min((int64_t)kChunkTiles, a.n_ctiles);
+      cb = a.sym ? rb * MB : 0;  // sym: the upper triangle J >= I only
+      chunk = cb / kChunkTiles;
+      cb_end = (int)min((int64_t)(chunk + 1) * kChunkTiles, a.n_ctiles);
     } else {
       cb = MODE == kModePacked ? rb * MB : 0;
     }
@@ -226,28 +244,30 @@ struct Cursor {
 template <int MB, int MODE>
 __host__ __device__ inline int64_t total_units(const TcArgs& a) {
   if (MODE == kModePacked) return packed_items(a.n_rtiles, a.n_ctiles, MB);
-  if (MODE == kModeMatvec) return a.n_rtiles * a.n_chunks;
+  if (MODE == kModeMatvec) return a.n_rtiles * a.n_chunks;  // (strided: unused)
   return a.n_rtiles * a.n_ctiles;
 }
 
-template <int KB, int MODE>
+template <int KB, int MODE, int KIND>
 __global__ void __launch_bounds__(kThreads, 1)
     affinity_tc_kernel(const __grid_constant__ CUtensorMap map_hi,
                        const __grid_constant__ CUtensorMap map_lo,
-                       const __grid_constant__ CUtensorMap map_out, const TcArgs args) {
+                       const __grid_constant__ CUtensorMap map_out,
+                       const __grid_constant__ CUtensorMap map_nrm, const TcArgs args) {
+  constexpr bool kNorm = KIND == GPIC_KIND_RBF;  // the distance comes out of the MMA
   constexpr int MB = mblocks(KB);
   constexpr int ST = stages(KB, MODE);
   constexpr int kTmemCols = 2 * MB * kBN;  // 2 accumulators
   if (MODE == kModeMatvec && args.ctl != nullptr && *(volatile const int32_t*)&args.ctl->stop)
     return;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~uintptr_t(1023));
+  uint8_t* base = smem_align<1024>(smem_raw);
   uint8_t* sA = base;                                     // [hl][m][kb] 16 KB tiles
-  uint8_t* sB = sA + a_bytes(KB);                         // [stage][hl] 16 KB tiles
-  uint8_t* sOut = sB + ST * 2 * kTileBytes;               // [epi warp] staging / combine
-  float* sCol = reinterpret_cast<float*>(sOut + out_bytes(KB, MODE));  // [warp][buf][sqn|v][64]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sCol) + kColBytes);
+  uint8_t* sAn = sA + a_main_bytes(KB);                   // [m][hl] 4 KB norm planes
+  uint8_t* sB = sA + a_bytes(KB);                         // [stage]{hi, lo, norm hi, norm lo}
+  uint8_t* sOut = sB + ST * kStageBytes;                  // [epi warp] staging / combine
+  float* sCol = reinterpret_cast<float*>(sOut + out_bytes(KB, MODE));  // matvec: [warp][buf][v][64]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sCol) + col_bytes(MODE));
   uint64_t* full = bars;                 // [ST]
   uint64_t* empty = bars + ST;           // [ST]
   uint64_t* a_full = bars + 2 * ST;
@@ -278,6 +298,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_lo)) : "memory");
     if (MODE != kModeMatvec)
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_out)) : "memory");
+    if (kNorm)
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_nrm)) : "memory");
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
@@ -304,23 +326,32 @@ __global__ void __launch_bounds__(kThreads, 1)
       Cursor<MB, MODE> c;
       for (c.begin(args, u_begin, u_end); c.valid(); c.next(args)) {
         if (c.rb != cur_rb) {
-          mbar_wait(a_empty, a_par);
+          mbar_wait_sleep(a_empty, a_par);
           a_par ^= 1;
-          mbar_expect_tx(a_full, a_bytes(KB));
+          mbar_expect_tx(a_full, kNorm ? a_bytes(KB) : a_main_bytes(KB));
           for (int hl = 0; hl < 2; ++hl)
-            for (int m = 0; m < MB; ++m)
+            for (int m = 0; m < MB; ++m) {
+              const int row0 = (int)(args.row_lo + (c.rb * MB + m) * 128);
               for (int kb = 0; kb < KB; ++kb)
                 tma_load_2d(sA + ((hl * MB + m) * KB + kb) * kTileBytes, hl ? &map_lo : &map_hi,
-                            kb * kKBlk, (int)(args.row_lo + (c.rb * MB + m) * 128), a_full, keep);
+                            kb * kKBlk, row0, a_full, keep);
+              if (kNorm)  // row-operand norm planes 0 (hi) / 1 (lo)
+                tma_load_2d(sAn + (m * 2 + hl) * kNrmPlane, &map_nrm, 0,
+                            (int)(hl * args.n_pad) + row0, a_full, keep);
+            }
           cur_rb = c.rb;
         }
         for (int kb = 0; kb < KB; ++kb) {
-          mbar_wait(&empty[s], ph ^ 1);
-          mbar_expect_tx(&full[s], 2 * kTileBytes);
-          tma_load_2d(sB + (s * 2 + 0) * kTileBytes, &map_hi, kb * kKBlk, (int)(c.cb * kBN), &full[s],
-                      keep);
-          tma_load_2d(sB + (s * 2 + 1) * kTileBytes, &map_lo, kb * kKBlk, (int)(c.cb * kBN), &full[s],
-                      keep);
+          mbar_wait_sleep(&empty[s], ph ^ 1);
+          const bool nrm = kNorm && kb == KB - 1;
+          mbar_expect_tx(&full[s], 2 * kTileBytes + (nrm ? kNrmBytes : 0));
+          uint8_t* stg = sB + s * kStageBytes;
+          tma_load_2d(stg, &map_hi, kb * kKBlk, (int)(c.cb * kBN), &full[s], keep);
+          tma_load_2d(stg + kTileBytes, &map_lo, kb * kKBlk, (int)(c.cb * kBN), &full[s], keep);
+          if (nrm)  // column-operand norm planes 2 (hi) / 3 (lo)
+            for (int hl = 0; hl < 2; ++hl)
+              tma_load_2d(stg + 2 * kTileBytes + hl * kNrmPlane, &map_nrm, 0,
+                          (int)((2 + hl) * args.n_pad + c.cb * kBN), &full[s], keep);
           if (++s == ST) { s = 0; ph ^= 1; }
         }
       }
@@ -338,19 +369,20 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (c.begin(args, u_begin, u_end); c.valid(); ++i) {
         const int64_t rb = c.rb;
         if (rb != cur_rb) {
-          mbar_wait(a_full, a_par);
+          mbar_wait_sleep(a_full, a_par);
           a_par ^= 1;
           cur_rb = rb;
         }
         const int buf = i & 1;
-        mbar_wait(&t_empty[buf], (te_bits >> buf) & 1u);
+        mbar_wait_sleep(&t_empty[buf], (te_bits >> buf) & 1u);
         te_bits ^= 1u << buf;
         tc_fence_after();
         for (int kb = 0; kb < KB; ++kb) {
-          mbar_wait(&full[s], ph);
+          mbar_wait_sleep(&full[s], ph);
           tc_fence_after();
-          const uint64_t bh = sw128_desc(su32(sB + (s * 2 + 0) * kTileBytes));
-          const uint64_t bl = sw128_desc(su32(sB + (s * 2 + 1) * kTileBytes));
+          uint8_t* stg = sB + s * kStageBytes;
+          const uint64_t bh = sw128_desc(su32(stg));
+          const uint64_t bl = sw128_desc(su32(stg + kTileBytes));
 #pragma unroll
           for (int m = 0; m < MB; ++m) {
             const uint32_t d = tmem_base + (uint32_t)((buf * MB + m) * kBN);
@@ -362,6 +394,15 @@ __global__ void __launch_bounds__(kThreads, 1)
               mma_f16(d, ah + off, bl + off, kIdesc, (kb | k) != 0);
               mma_f16(d, al + off, bh + off, kIdesc, 1u);
               mma_f16(d, ah + off, bh + off, kIdesc, 1u);
+            }
+            if (kNorm && kb == KB - 1) {  // + the norm block: acc = -(s^2/2)|x_i - x_j|^2
+              const uint64_t nah = sw32_desc(su32(sAn + (m * 2 + 0) * kNrmPlane));
+              const uint64_t nal = sw32_desc(su32(sAn + (m * 2 + 1) * kNrmPlane));
+              const uint64_t nbh = sw32_desc(su32(stg + 2 * kTileBytes));
+              const uint64_t nbl = sw32_desc(su32(stg + 2 * kTileBytes + kNrmPlane));
+              mma_f16(d, nah, nbl, kIdesc, 1u);
+              mma_f16(d, nal, nbh, kIdesc, 1u);
+              mma_f16(d, nah, nbh, kIdesc, 1u);
             }
           }
           tc_commit(&empty[s]);  // frees the B stage once these MMAs retire
@@ -403,31 +444,33 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint8_t* stage = sOut + e * kStageOutBytes;       // store modes: this warp's staging box
     const uint64_t stream_pol = policy_evict_first();  // A is written once here
     int stores = 0;
-    const float ns = args.ns;
-    const float gs = __ldg(args.gscale);  // accumulator units -> G
-    const float m2ns = -2.f * ns * gs;
+    const float gs = __ldg(args.gscale);  // accumulator units -> G (1 / s^2)
+    const float m2ns = -2.f * args.ns * gs;
     uint32_t tf_bits = 0;  // TMEM-full parity per accumulator buffer
     int i = 0;
     double acc64[4] = {0.0, 0.0, 0.0, 0.0};  // matvec: the 4 rows' partials over an item
     auto group_sync = [&]() {
       asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(GW * 32) : "memory");
     };
-    // row terms ns |x_i|^2 of this thread's 4 rows: reloaded when the row block changes
-    float ra[4] = {0.f, 0.f, 0.f, 0.f};
+    float vrow[4] = {0.f, 0.f, 0.f, 0.f};  // matvec sym: v_i of the 4 rows (column partials)
     int64_t grow[4] = {0, 0, 0, 0};
+    // matvec sym: the warps holding the same columns (all quadrants, both M
+    // blocks) exchange column partials through smem; one writer per group
+    float* colx = reinterpret_cast<float*>(sOut + kEpiWarps * 32 * 8);
+    const uint32_t colbar = 9 + c_lo / UPW;
+    const bool col_writer = q == 0 && m == 0;
     int64_t cur_rb = -1;
-    // column terms of a tile arrive one tile ahead by cp.async into this
+    // matvec: v_j of a tile arrives one tile ahead by cp.async into this
     // warp's double buffer: lane l copies column l of each of its chunks
-    float* colw = sCol + e * (2 * 2 * 64);
+    float* colw = sCol + e * (2 * 64);
     auto fetch_cols = [&](int64_t cbn, int slot) {
-      float* dst = colw + slot * 128;
+      if constexpr (MODE == kModeMatvec) {
+        float* dst = colw + slot * 64;
 #pragma unroll
-      for (int cc = 0; cc < UPW; ++cc) {
-        const int64_t col = cbn * kBN + (c_lo + cc) * 32 + lane;
-        cp_async4(dst + cc * 32 + lane, args.sqn + col);
-        if (MODE == kModeMatvec) cp_async4(dst + 64 + cc * 32 + lane, args.v32 + col);
+        for (int cc = 0; cc < UPW; ++cc)
+          cp_async4(dst + cc * 32 + lane, args.v32 + cbn * kBN + (c_lo + cc) * 32 + lane);
+        cp_async_commit();
       }
-      cp_async_commit();
     };
     Cursor<MB, MODE> c;
     c.begin(args, u_begin, u_end);
@@ -440,25 +483,30 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int64_t tI = rb * MB + m;  // tile row of this warp's rows
       // packed: the lower-triangle half of a diagonal row block is not stored
       const bool store_ok = MODE != kModePacked || tI <= cb;
+      // matvec sym: row partials from tiles J >= I, column partials from J > I
+      const bool row_ok = MODE != kModeMatvec || !args.sym || tI <= cb;
+      const bool col_ok = MODE == kModeMatvec && args.sym && tI < cb;
       const int64_t lr0 = (rb * MB + m) * 128 + q * 32;  // shard-local first row of this warp
       if (rb != cur_rb) {
         // this thread's 4 rows: rr = 2*half + {0: tq, 1: tq + 8}
 #pragma unroll
         for (int rr = 0; rr < 4; ++rr) {
           grow[rr] = args.row_lo + lr0 + (rr >> 1) * 16 + tq + (rr & 1) * 8;
-          ra[rr] = grow[rr] < args.n ? ns * __ldg(args.sqn + grow[rr]) : 0.f;
+          if (MODE == kModeMatvec) vrow[rr] = grow[rr] < args.n ? __ldg(args.v32 + grow[rr]) : 0.f;
         }
         cur_rb = rb;
       }
       c.next(args);
-      if (c.valid()) {
-        fetch_cols(c.cb, (i + 1) & 1);
-        cp_async_wait<1>();  // this tile's group has landed
-      } else {
-        cp_async_wait<0>();
+      if constexpr (MODE == kModeMatvec) {
+        if (c.valid()) {
+          fetch_cols(c.cb, (i + 1) & 1);
+          cp_async_wait<1>();  // this tile's group has landed
+        } else {
+          cp_async_wait<0>();
+        }
+        __syncwarp();
       }
-      __syncwarp();
-      const float* colt = colw + (i & 1) * 128;
+      const float* colt = colw + (i & 1) * 64;
       mbar_wait_sleep(&t_full[buf], (tf_bits >> buf) & 1u);
       tf_bits ^= 1u << buf;
       tc_fence_after();
@@ -468,15 +516,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int ch = c_lo + cc;
         uint32_t r[32];  // [hf][block b][4]: (row tq, c), (row tq, c+1), (row tq+8, c), (row tq+8, c+1)
         const int64_t col0 = cb * kBN + ch * 32;
-        // this thread's 8 columns: ns |x_j|^2 (and v_j) from the staged terms
-        float cterm[8], vcol[8];
+        // matvec: this thread's 8 columns' v_j from the staged copy
+        float vcol[8];
+        if constexpr (MODE == kModeMatvec) {
 #pragma unroll
-        for (int b2 = 0; b2 < 4; ++b2) {
-          const float2 t2 = *reinterpret_cast<const float2*>(colt + cc * 32 + 8 * b2 + tc);
-          cterm[2 * b2] = t2.x;
-          cterm[2 * b2 + 1] = t2.y;
-          if (MODE == kModeMatvec) {
-            const float2 v2 = *reinterpret_cast<const float2*>(colt + 64 + cc * 32 + 8 * b2 + tc);
+          for (int b2 = 0; b2 < 4; ++b2) {
+            const float2 v2 = *reinterpret_cast<const float2*>(colt + cc * 32 + 8 * b2 + tc);
             vcol[2 * b2] = v2.x;
             vcol[2 * b2 + 1] = v2.y;
           }
@@ -491,20 +536,19 @@ __global__ void __launch_bounds__(kThreads, 1)
           __syncwarp();
           if (lane == 0) mbar_arrive(&t_empty[buf]);
         }
-#pragma unroll
-        for (int k = 0; k < 8; ++k) cterm[k] *= ns;
         const bool diag = (col0 < args.row_lo + lr0 + 32) && (args.row_lo + lr0 < col0 + 32);
         const bool pad = col0 + 32 > args.n || args.row_lo + lr0 + 32 > args.n;
         float vals[32];
 #pragma unroll
         for (int x = 0; x < 32; ++x) {
-          const int rr = (x >> 4) * 2 + ((x >> 1) & 1);  // half, then row tq / tq+8
-          const int k = ((x >> 2) & 3) * 2 + (x & 1);    // block, then column c / c+1
           const float g = __uint_as_float(r[x]);
-          if (args.kind == GPIC_KIND_COSINE)
+          if constexpr (KIND == GPIC_KIND_COSINE)
             vals[x] = fmaxf(g * gs, 0.f);  // unit rows: G = cos, clamped (affinity.py:93-94)
           else
-            vals[x] = ex2(fminf(fmaf(g, m2ns, ra[rr] + cterm[k]), 0.f));
+            // g = -(s^2/2)|x_i - x_j|^2 from the MMA (norm block); no clamp:
+            // a near-duplicate's distance^2 rounding below 0 gives
+            // exp2(+ulp-scale) = 1 + O(1e-6), the Gram's own rounding order
+            vals[x] = ex2(g * m2ns);
         }
         if (diag || pad) {
 #pragma unroll
@@ -515,11 +559,46 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
         if constexpr (MODE == kModeMatvec) {
+          if (row_ok) {
 #pragma unroll
-          for (int x = 0; x < 32; ++x) {
-            const int rr = (x >> 4) * 2 + ((x >> 1) & 1);
-            const int k = ((x >> 2) & 3) * 2 + (x & 1);
-            rsum[rr] = fmaf(vals[x], vcol[k], rsum[rr]);
+            for (int x = 0; x < 32; ++x) {
+              const int rr = (x >> 4) * 2 + ((x >> 1) & 1);
+              const int k = ((x >> 2) & 3) * 2 + (x & 1);
+              rsum[rr] = fmaf(vals[x], vcol[k], rsum[rr]);
+            }
+          }
+          if (args.sym) {
+            // column partials sum_i a_ij v_i over this warp's 32 rows (same
+            // fixed reduce-scatter as the packed degree partials)
+            float cs[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+              const int x0 = (k >> 1) * 4 + (k & 1);
+              cs[k] = col_ok ? fmaf(vals[x0], vrow[0], vals[x0 + 2] * vrow[1]) +
+                                   fmaf(vals[x0 + 16], vrow[2], vals[x0 + 18] * vrow[3])
+                             : 0.f;
+            }
+            const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const float send = b4 ? cs[k] : cs[k + 4];
+              const float keep = b4 ? cs[k + 4] : cs[k];
+              cs[k] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+            }
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+              const float send = b3 ? cs[k] : cs[k + 2];
+              const float keep = b3 ? cs[k + 2] : cs[k];
+              cs[k] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+            }
+            {
+              const float send = b2 ? cs[0] : cs[1];
+              const float keep = b2 ? cs[1] : cs[0];
+              cs[0] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+            }
+            const int k = (b4 ? 4 : 0) + (b3 ? 2 : 0) + (b2 ? 1 : 0);
+            const int col = 8 * (k >> 1) + tc + (k & 1);
+            colx[((buf * MB + m) * 4 + q) * 128 + ch * 32 + col] = cs[0];
           }
         } else {
 #pragma unroll
@@ -593,6 +672,25 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       const bool quad_lead = (lane & 3) == 0;
       if constexpr (MODE == kModeMatvec) {
+        if (args.sym) {
+          // combine the column partials of the 4 * MB warps sharing these
+          // columns (M block, then quadrant order) into one record
+          asm volatile("bar.sync %0, %1;" ::"r"(colbar), "r"(4 * MB * 32) : "memory");
+          if (col_writer) {
+            const int64_t rec = (int64_t)rb * args.n_ctiles - (int64_t)MB * rb * (rb - 1) / 2 +
+                                (cb - (int64_t)rb * MB);
+#pragma unroll
+            for (int cc = 0; cc < UPW; ++cc) {
+              const int cidx = (c_lo + cc) * 32 + lane;
+              float t = 0.f;
+#pragma unroll
+              for (int mm = 0; mm < MB; ++mm)
+#pragma unroll
+                for (int qq = 0; qq < 4; ++qq) t += colx[((buf * MB + mm) * 4 + qq) * 128 + cidx];
+              args.colpart[rec * 128 + cidx] = t;
+            }
+          }
+        }
 #pragma unroll
         for (int rr = 0; rr < 4; ++rr) acc64[rr] += (double)rsum[rr];
         if (item_last) {
@@ -685,7 +783,8 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 
 bool make_map(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t outer,
               uint64_t row_bytes, uint32_t box_inner, uint32_t box_outer,
-              CUtensorMapDataType dtype = CU_TENSOR_MAP_DATA_TYPE_FLOAT32) {
+              CUtensorMapDataType dtype = CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+              CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
   auto fn = encode_fn();
   if (!fn) return false;
   cuuint64_t dims[2] = {inner, outer};
@@ -693,7 +792,7 @@ bool make_map(CUtensorMap* map, const void* ptr, uint64_t inner, uint64_t outer,
   cuuint32_t box[2] = {box_inner, box_outer};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = fn(map, dtype, 2, const_cast<void*>(ptr), dims, strides,
-                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
@@ -702,14 +801,17 @@ int g_num_sms = 0;
 
 template <int KB, int MODE>
 int launch_kb(const CUtensorMap& mh, const CUtensorMap& ml, const CUtensorMap& mo,
-              const TcArgs& a0, cudaStream_t s) {
+              const CUtensorMap& mn, const TcArgs& a0, cudaStream_t s) {
   constexpr int MB = mblocks(KB);
   TcArgs a = a0;
   a.n_rtiles = ceil_div(a.rows, 128 * MB);
   a.n_chunks = ceil_div(a.n_ctiles, kChunkTiles);
   static bool attr = false;
   if (!attr) {
-    GPIC_CUDA_TRY(cudaFuncSetAttribute(affinity_tc_kernel<KB, MODE>,
+    GPIC_CUDA_TRY(cudaFuncSetAttribute(affinity_tc_kernel<KB, MODE, GPIC_KIND_RBF>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       smem_bytes(KB, MODE)));
+    GPIC_CUDA_TRY(cudaFuncSetAttribute(affinity_tc_kernel<KB, MODE, GPIC_KIND_COSINE>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        smem_bytes(KB, MODE)));
     attr = true;
@@ -725,36 +827,51 @@ int launch_kb(const CUtensorMap& mh, const CUtensorMap& ml, const CUtensorMap& m
   const int64_t total = (MODE == kModeMatvec || a.strided) ? a.n_rtiles : total_units<MB, MODE>(a);
   const int grid = (int)(total < g_num_sms ? total : g_num_sms);
   if (grid < 1) return GPIC_OK;
-  affinity_tc_kernel<KB, MODE><<<grid, kThreads, smem_bytes(KB, MODE), s>>>(mh, ml, mo, a);
+  // the similarity kind is a template parameter: a runtime select would
+  // evaluate both epilogues per element
+  if (a.kind == GPIC_KIND_COSINE)
+    affinity_tc_kernel<KB, MODE, GPIC_KIND_COSINE><<<grid, kThreads, smem_bytes(KB, MODE), s>>>(
+        mh, ml, mo, mn, a);
+  else
+    affinity_tc_kernel<KB, MODE, GPIC_KIND_RBF><<<grid, kThreads, smem_bytes(KB, MODE), s>>>(
+        mh, ml, mo, mn, a);
   count_launch();
   GPIC_CUDA_TRY(cudaGetLastError());
   return GPIC_OK;
 }
 
+struct Maps {
+  CUtensorMap hi, lo, out, nrm;
+};
+
 template <int MODE>
-int dispatch_kb(int KB, const CUtensorMap& mh, const CUtensorMap& ml, const CUtensorMap& mo,
-                const TcArgs& args, cudaStream_t s) {
+int dispatch_kb(int KB, const Maps& mp, const TcArgs& args, cudaStream_t s) {
   switch (KB) {
-    case 1: return launch_kb<1, MODE>(mh, ml, mo, args, s);
-    case 2: return launch_kb<2, MODE>(mh, ml, mo, args, s);
-    case 3: return launch_kb<3, MODE>(mh, ml, mo, args, s);
-    default: return launch_kb<4, MODE>(mh, ml, mo, args, s);
+    case 1: return launch_kb<1, MODE>(mp.hi, mp.lo, mp.out, mp.nrm, args, s);
+    case 2: return launch_kb<2, MODE>(mp.hi, mp.lo, mp.out, mp.nrm, args, s);
+    case 3: return launch_kb<3, MODE>(mp.hi, mp.lo, mp.out, mp.nrm, args, s);
+    default: return launch_kb<4, MODE>(mp.hi, mp.lo, mp.out, mp.nrm, args, s);
   }
 }
 
-// The fp16 hi / lo planes live back to back in the d_xhi buffer (prepare.cu).
-int operand_maps(const float* xhi, int64_t n, int32_t dp, CUtensorMap* mh, CUtensorMap* ml) {
+// The fp16 hi / lo planes live back to back in the d_xhi buffer, followed
+// by the norm block's four 16-wide planes (prepare.cu).
+int operand_maps(const float* xhi, int64_t n, int32_t dp, Maps* mp) {
   const int KB = dp / kKBlk;
   if (dp % kKBlk || KB < 1 || KB > 4)
     return fail(GPIC_E_UNSUPPORTED, "tcgen05 affinity engine supports d <= 256");
   const int64_t npad = row_pad(n);
   const uint16_t* hi = reinterpret_cast<const uint16_t*>(xhi);
   const uint16_t* lo = hi + npad * dp;
-  if (!make_map(mh, hi, (uint64_t)dp, (uint64_t)npad, (uint64_t)dp * 2, kKBlk, 128,
+  const uint16_t* nrm = lo + npad * dp;
+  if (!make_map(&mp->hi, hi, (uint64_t)dp, (uint64_t)npad, (uint64_t)dp * 2, kKBlk, 128,
                 CU_TENSOR_MAP_DATA_TYPE_FLOAT16) ||
-      !make_map(ml, lo, (uint64_t)dp, (uint64_t)npad, (uint64_t)dp * 2, kKBlk, 128,
-                CU_TENSOR_MAP_DATA_TYPE_FLOAT16))
+      !make_map(&mp->lo, lo, (uint64_t)dp, (uint64_t)npad, (uint64_t)dp * 2, kKBlk, 128,
+                CU_TENSOR_MAP_DATA_TYPE_FLOAT16) ||
+      !make_map(&mp->nrm, nrm, 16, (uint64_t)(4 * npad), 32, 16, 128,
+                CU_TENSOR_MAP_DATA_TYPE_FLOAT16, CU_TENSOR_MAP_SWIZZLE_32B))
     return fail(GPIC_E_CUDA, "cuTensorMapEncodeTiled failed");
+  mp->out = mp->hi;  // placeholder for the matvec mode (no stores)
   return GPIC_OK;
 }
 
@@ -772,12 +889,13 @@ int packed_row_halves(int32_t /*dp*/) { return 1; }  // the epilogue combines a 
 int launch_affinity_tc_packed(const float* xhi, const float* xlo, const float* sqn, int64_t n,
                               int32_t dp, float neg_scale_log2, float* a_packed, float* degrow,
                               float* degcol, cudaStream_t s, int kind) {
-  CUtensorMap mh, ml, mo;
-  int rc = operand_maps(xhi, n, dp, &mh, &ml);
+  Maps mp;
+  int rc = operand_maps(xhi, n, dp, &mp);
   if (rc) return rc;
-  if (!make_map(&mo, a_packed, 128, (uint64_t)packed_tiles(n) * 128, 512, 32, 32))
+  if (!make_map(&mp.out, a_packed, 128, (uint64_t)packed_tiles(n) * 128, 512, 32, 32))
     return fail(GPIC_E_CUDA, "cuTensorMapEncodeTiled failed");
   TcArgs args{};
+  args.n_pad = row_pad(n);
   args.sqn = sqn;
   args.gscale = sqn + row_pad(n) - 1;
   args.n = n;
@@ -788,19 +906,20 @@ int launch_affinity_tc_packed(const float* xhi, const float* xlo, const float* s
   args.degrow = degrow;
   args.degcol = degcol;
   args.kind = kind;
-  return dispatch_kb<kModePacked>(dp / kKBlk, mh, ml, mo, args, s);
+  return dispatch_kb<kModePacked>(dp / kKBlk, mp, args, s);
 }
 
 int launch_affinity_tc(const float* xhi, const float* xlo, const float* sqn, int64_t n,
                        int32_t dp, int64_t row_lo, int64_t row_hi, float neg_scale_log2, float* a,
                        int64_t lda, float* rowpart, int64_t rows_pad, cudaStream_t s, int kind) {
   const int64_t rows = row_hi - row_lo;
-  CUtensorMap mh, ml, mo;
-  int rc = operand_maps(xhi, n, dp, &mh, &ml);
+  Maps mp;
+  int rc = operand_maps(xhi, n, dp, &mp);
   if (rc) return rc;
-  if (!make_map(&mo, a, (uint64_t)lda, (uint64_t)rows, (uint64_t)lda * 4, 32, 32))
+  if (!make_map(&mp.out, a, (uint64_t)lda, (uint64_t)rows, (uint64_t)lda * 4, 32, 32))
     return fail(GPIC_E_CUDA, "cuTensorMapEncodeTiled failed");
   TcArgs args{};
+  args.n_pad = row_pad(n);
   args.sqn = sqn;
   args.gscale = sqn + row_pad(n) - 1;
   args.n = n;
@@ -813,7 +932,7 @@ int launch_affinity_tc(const float* xhi, const float* xlo, const float* sqn, int
   args.out = a;
   args.lda = lda;
   args.kind = kind;
-  return dispatch_kb<kModeDense>(dp / kKBlk, mh, ml, mo, args, s);
+  return dispatch_kb<kModeDense>(dp / kKBlk, mp, args, s);
 }
 
 int64_t mf_parts(int64_t n, int32_t dp) {
@@ -822,16 +941,26 @@ int64_t mf_parts(int64_t n, int32_t dp) {
   return chunks;  // one fp64 partial per (chunk item, row): the row's warps combine in-CTA
 }
 
+int mf_rows_per_block(int32_t dp) { return 128 * mblocks(dp / kKBlk); }
+
+// sym column-partial records: one per (row block of 128 * MB rows, column
+// tile J >= MB * row block)
+int64_t mf_colpart_floats(int64_t n, int32_t dp) {
+  const int mb = mblocks(dp / kKBlk);
+  return packed_items(ceil_div(n, 128 * mb), ceil_div(n, kBN), mb) * 128;
+}
+
 // Matrix-free row block: ypart[p][i - row_lo] = sum over chunk p of
 // a_ij v_j (fp64 across tiles); gpic's mf_reduce combines the parts.
 int launch_affinity_tc_matvec(const float* xhi, const float* xlo, const float* sqn, int64_t n,
                               int32_t dp, int64_t row_lo, int64_t row_hi, float neg_scale_log2,
                               const float* v32, double* ypart, int64_t rows_pad,
-                              const gpic_ctl* ctl, cudaStream_t s, int kind) {
-  CUtensorMap mh, ml;
-  int rc = operand_maps(xhi, n, dp, &mh, &ml);
+                              const gpic_ctl* ctl, cudaStream_t s, int kind, float* colpart) {
+  Maps mp;
+  int rc = operand_maps(xhi, n, dp, &mp);
   if (rc) return rc;
   TcArgs args{};
+  args.n_pad = row_pad(n);
   args.sqn = sqn;
   args.gscale = sqn + row_pad(n) - 1;
   args.n = n;
@@ -844,7 +973,9 @@ int launch_affinity_tc_matvec(const float* xhi, const float* xlo, const float* s
   args.ypart = ypart;
   args.ctl = ctl;
   args.kind = kind;
-  return dispatch_kb<kModeMatvec>(dp / kKBlk, mh, ml, mh, args, s);
+  args.sym = colpart != nullptr && row_lo == 0 && row_hi == n;
+  args.colpart = colpart;
+  return dispatch_kb<kModeMatvec>(dp / kKBlk, mp, args, s);
 }
 
 }  // namespace gpic

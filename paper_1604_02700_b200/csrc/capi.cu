@@ -31,6 +31,9 @@ int32_t feature_pitch(int32_t d) { return (int32_t)round_up(d, 64); }
 // at any row, so a tile can overhang n by up to 127 rows.
 int64_t row_pad(int64_t n) { return round_up(n, kTileM) + kTileM; }
 int64_t affinity_pitch(int64_t n) { return round_up(n, 32); }
+// d_xhi: hi + lo fp16 planes (n_pad x dp each) + the norm block (4 planes of
+// n_pad x 16 fp16) = n_pad x (dp + 32) floats
+int64_t operand_floats(int64_t n, int32_t d) { return row_pad(n) * (feature_pitch(d) + 32); }
 
 static inline int64_t al(int64_t b) { return (b + 255) & ~int64_t(255); }
 
@@ -39,7 +42,8 @@ int64_t workspace_bytes(int64_t n, int32_t d, int32_t k, int64_t rows, int32_t /
   const int64_t rows_pad = round_up(rows, kTileM);
   const int64_t n_ctiles = ceil_div(n, kTileN);
   int64_t b = al(sizeof(gpic_ctl));
-  b += 2 * al(npad * dp * 4);                 // xhi, xlo
+  b += al(operand_floats(n, d) * 4);          // xhi: fp16 planes + norm block
+  b += al(npad * dp * 4);                     // xlo
   b += al(npad * 4);                          // sqn
   b += al(ceil_div(n, 256) * d * 8);          // colpart
   b += al((int64_t)(d + 1) * 8);              // mean + max|x - mean|
@@ -66,7 +70,7 @@ int carve(void* base, int64_t bytes, int64_t n, int32_t d, int32_t k, int64_t ro
   uint8_t* p = static_cast<uint8_t*>(base);
   auto take = [&](int64_t sz) { uint8_t* q = p; p += al(sz); return q; };
   ws->ctl = reinterpret_cast<gpic_ctl*>(take(sizeof(gpic_ctl)));
-  ws->xhi = reinterpret_cast<float*>(take(npad * dp * 4));
+  ws->xhi = reinterpret_cast<float*>(take(operand_floats(n, d) * 4));
   ws->xlo = reinterpret_cast<float*>(take(npad * dp * 4));
   ws->sqn = reinterpret_cast<float*>(take(npad * 4));
   ws->colpart = reinterpret_cast<double*>(take(ceil_div(n, 256) * d * 8));
@@ -126,6 +130,7 @@ int64_t gpic_workspace_bytes(int64_t n, int32_t d, int32_t k, int64_t rows, int3
 int64_t gpic_affinity_pitch(int64_t n) { return affinity_pitch(n); }
 int32_t gpic_feature_pitch(int32_t d) { return feature_pitch(d); }
 int64_t gpic_row_pad(int64_t n) { return row_pad(n); }
+int64_t gpic_operand_floats(int64_t n, int32_t d) { return n < 1 || d < 1 ? -1 : operand_floats(n, d); }
 
 int gpic_ctl_read(const gpic_ctl* d_ctl, gpic_ctl* h_out, void* stream) {
   cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -283,8 +288,9 @@ int gpic_mf_degrees(const float* d_xhi, const float* d_xlo, const float* d_sqn, 
                     float* d_ones, double* d_ypart, double* d_deg, void* stream) {
   if (kind == GPIC_KIND_RBF && !(sigma > 0)) return fail(GPIC_E_INVALID, "sigma must be positive");
   if (row_lo < 0 || row_hi > n || row_lo >= row_hi) return fail(GPIC_E_INVALID, "bad row range");
-  const MfOperands op{d_xhi, d_xlo, d_sqn, n, feature_pitch(d),
-                      (float)(-1.4426950408889634 / (2.0 * sigma * sigma)), kind};
+  MfOperands op{d_xhi, d_xlo, d_sqn, n, feature_pitch(d),
+                (float)(-1.4426950408889634 / (2.0 * sigma * sigma)), kind};
+  op.sym = mf_sym_default();
   return launch_mf_degrees(op, row_lo, row_hi - row_lo, d_ones, d_ypart, d_deg,
                            static_cast<cudaStream_t>(stream));
 }
@@ -387,6 +393,7 @@ int cluster_impl(const double* d_x, int64_t n, int32_t d, double sigma, int32_t 
     double* ypart = reinterpret_cast<double*>(a);
     L.mode = kLoopMatrixFree;
     L.mf = MfOperands{ws.xhi, ws.xlo, ws.sqn, n, dp, neg_scale_log2, kind};
+    L.mf.sym = mf_sym_default();
     L.ypart = ypart;
     mark(ev, 1, s);  // matrix-free: the degree pass is the first A recompute
     rc = launch_mf_degrees(L.mf, 0, n, ws.v32, ypart, deg, s);

@@ -39,7 +39,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (ctl != nullptr && *(volatile const int32_t*)&ctl->stop) return;
   const int parity = ctl != nullptr ? (ctl->iter & 1) : 0;
   extern __shared__ uint8_t smem_raw[];
-  float* st = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+  float* st = reinterpret_cast<float*>(smem_align<128>(smem_raw));
   uint64_t* full = reinterpret_cast<uint64_t*>(st + kStages * kStageFloats);
   uint64_t* empty = full + kStages;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;

@@ -7,6 +7,12 @@
 // rank's y buffer (same epilogue contract as the dense GEMV, so the
 // tau / normalise / stop tail and the multi-rank exchange are unchanged).
 // Degrees are the same pass with v = 1.
+//
+// Whole matrix on one rank (the sym pass): only tiles J >= I are computed;
+// y_i = (row partials of row i's chunks from its own diagonal tile on) +
+// (column partials of the tiles (I', J(i)), I' < J(i), i.e. the transposed
+// upper triangle), combined by mf_sym_reduce_kernel in a fixed order.
+#include <cstdlib>
 #include <cstring>
 
 #include "common.cuh"
@@ -47,6 +53,58 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// One CTA per column tile J (128 rows of y), kSeg segments: segment s sums
+// its share of row i's chunk partials (chunks from the row block's first
+// tile on) and of the column records (row blocks I' = 0 .. J / MB), then the
+// segment sums are added in order. The shape depends on (n, MB) only.
+constexpr int kSeg = 8;
+
+__global__ void __launch_bounds__(128 * kSeg)
+    mf_sym_reduce_kernel(const double* __restrict__ ypart, const float* __restrict__ colpart,
+                         int64_t nparts, int64_t rows_pad, int64_t n, int64_t nct, int mb,
+                         const double* __restrict__ deg, const PeerTable pt, gpic_ctl* ctl) {
+  if (ctl != nullptr && *(volatile const int32_t*)&ctl->stop) return;
+  __shared__ double part[kSeg][128];
+  const int64_t J = blockIdx.x;
+  const int o = threadIdx.x % 128, sg = threadIdx.x / 128;
+  const int64_t i = J * 128 + o;
+  const int64_t rb = J / mb;  // row block of row i (128 * mb rows)
+  const int64_t c0 = rb * mb / 32;  // first chunk written for this row block (kChunkTiles = 32)
+  const int64_t p0 = c0 + (nparts - c0) * sg / kSeg, p1 = c0 + (nparts - c0) * (sg + 1) / kSeg;
+  double s = 0.0;
+  if (i < n)
+    for (int64_t p = p0; p < p1; ++p) s += ypart[p * rows_pad + i];
+  const int64_t nrec = rb + 1;  // row blocks 0 .. rb hold tiles (I', J) with I' <= J
+  const int64_t r0 = nrec * sg / kSeg, r1 = nrec * (sg + 1) / kSeg;
+#pragma unroll 4
+  for (int64_t r = r0; r < r1; ++r) {
+    const int64_t rec = r * nct - (int64_t)mb * r * (r - 1) / 2 + (J - r * mb);
+    s += (double)colpart[rec * 128 + o];
+  }
+  part[sg][o] = s;
+  __syncthreads();
+  if (sg == 0 && i < n) {
+    double t = 0.0;
+#pragma unroll
+    for (int q = 0; q < kSeg; ++q) t += part[q][o];
+    const double val = deg != nullptr ? t / deg[i] : t;
+    const int parity = ctl != nullptr ? (ctl->iter & 1) : 0;
+    for (int p = 0; p < pt.nranks; ++p) pt.y[p][parity][i] = val;
+  }
+  if (pt.flags[0] == nullptr) return;
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned prev = atomicAdd(&ctl->arrive[2], 1u);
+    if (prev == gridDim.x - 1) {
+      ctl->arrive[2] = 0u;
+      __threadfence_system();
+      const uint64_t epoch = ctl->sync_epoch + (uint64_t)ctl->iter + 1;
+      for (int p = 0; p < pt.nranks; ++p) st_release_sys(pt.flags[p] + pt.self, epoch);
+    }
+  }
+}
+
 __global__ void fill_ones_kernel(float* v, int64_t n, int64_t len) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < len) v[i] = i < n ? 1.f : 0.f;
@@ -54,14 +112,38 @@ __global__ void fill_ones_kernel(float* v, int64_t n, int64_t len) {
 
 }  // namespace
 
+// scratch of one pass: the chunk row partials, plus (whole matrix on one
+// rank: the sym pass) the column-partial records behind them
+bool mf_sym_default() {
+  const char* e = getenv("GPIC_MF_SYM");  // tests / ablation: 0 forces the full-square pass
+  return e == nullptr || atoi(e) != 0;
+}
+static bool mf_sym(const MfOperands& op, int64_t row_lo, int64_t rows) {
+  return op.sym && row_lo == 0 && rows == op.n;
+}
+
 int64_t mf_ypart_doubles(int64_t n, int32_t dp, int64_t rows) {
-  return mf_parts(n, dp) * round_up(rows, kTileM);
+  const int64_t rp = mf_parts(n, dp) * round_up(rows, kTileM);
+  return rows == n ? rp + ceil_div(mf_colpart_floats(n, dp), 2) : rp;
 }
 
 int launch_mf_matvec(const MfOperands& op, int64_t row_lo, int64_t rows, const float* v32,
                      double* ypart, const double* deg, const PeerTable& pt, gpic_ctl* ctl,
                      cudaStream_t s) {
   const int64_t rows_pad = round_up(rows, kTileM);
+  if (mf_sym(op, row_lo, rows)) {
+    float* colpart = reinterpret_cast<float*>(ypart + mf_parts(op.n, op.dp) * rows_pad);
+    int rc = launch_affinity_tc_matvec(op.xhi, op.xlo, op.sqn, op.n, op.dp, 0, op.n, op.ns, v32,
+                                       ypart, rows_pad, ctl, s, op.kind, colpart);
+    if (rc) return rc;
+    const int64_t nct = ceil_div(op.n, kTileN);
+    mf_sym_reduce_kernel<<<(unsigned)nct, 128 * kSeg, 0, s>>>(
+        ypart, colpart, mf_parts(op.n, op.dp), rows_pad, op.n, nct,
+        mf_rows_per_block(op.dp) / 128, deg, pt, ctl);
+    count_launch();
+    GPIC_CUDA_TRY(cudaGetLastError());
+    return GPIC_OK;
+  }
   int rc = launch_affinity_tc_matvec(op.xhi, op.xlo, op.sqn, op.n, op.dp, row_lo, row_lo + rows,
                                      op.ns, v32, ypart, rows_pad, ctl, s, op.kind);
   if (rc) return rc;

@@ -18,6 +18,7 @@ inline int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }
 
 int32_t feature_pitch(int32_t d);
 int64_t row_pad(int64_t n);
+int64_t operand_floats(int64_t n, int32_t d);
 int64_t affinity_pitch(int64_t n);
 // fp32 vector copies of v are zero-padded to whole 128-element tiles
 inline int64_t vector_pitch(int64_t n) { return round_up(n, 128); }
@@ -128,13 +129,18 @@ struct MfOperands {
   int32_t dp;
   float ns;  // -log2(e) / (2 sigma^2)
   int kind = GPIC_KIND_RBF;
+  int sym = 0;  // whole matrix on one rank: upper-triangle pass (mf.cu)
 };
+bool mf_sym_default();
 int64_t mf_parts(int64_t n, int32_t dp);
+int mf_rows_per_block(int32_t dp);
+int64_t mf_colpart_floats(int64_t n, int32_t dp);
 int64_t mf_ypart_doubles(int64_t n, int32_t dp, int64_t rows);
 int launch_affinity_tc_matvec(const float* xhi, const float* xlo, const float* sqn, int64_t n,
                               int32_t dp, int64_t row_lo, int64_t row_hi, float neg_scale_log2,
                               const float* v32, double* ypart, int64_t rows_pad,
-                              const gpic_ctl* ctl, cudaStream_t s, int kind = GPIC_KIND_RBF);
+                              const gpic_ctl* ctl, cudaStream_t s, int kind = GPIC_KIND_RBF,
+                              float* colpart = nullptr);
 int launch_mf_matvec(const MfOperands& op, int64_t row_lo, int64_t rows, const float* v32,
                      double* ypart, const double* deg, const PeerTable& pt, gpic_ctl* ctl,
                      cudaStream_t s);

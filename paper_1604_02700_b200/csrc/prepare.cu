@@ -7,10 +7,19 @@
 //
 //   xc   (d_xlo buffer)  fp32 centred rows, pitch dp — the FFMA engine
 //   hi/lo planes (d_xhi buffer, fp16, pitch dp, hi plane then lo plane)
-//        xs = xc * s with s = 2^e chosen so max|xs| < 2^14 (exact scaling),
+//        xs = xc * s with s = 2^e chosen so max|xs| < 2^8 (exact scaling),
 //        hi = fp16(xs), lo = fp16(xs - hi): the 3-term split of the
 //        tcgen05 kind::f16 engine (hi.hi + hi.lo + lo.hi, fp32 accumulate);
 //        1/s^2 is stored in the padding slot sqn[n_pad - 1]
+//   norm block (after the planes; RBF): a 16-wide K extension that makes
+//        the MMA accumulate -(s^2/2)|x_i - x_j|^2 directly:
+//            row operand    [2^10, M_i, 0 ...]   (hi / lo planes)
+//            column operand [M_j, 2^10, 0 ...]   M = -(s^2/2)|x~|^2 / 2^10
+//        so acc = s^2 x_i.x_j + 2^10 M_j + 2^10 M_i, with |x~|^2 taken from
+//        the split operands themselves (x~ = (hi + lo) / s), which keeps the
+//        distance of a point to itself at the accumulator's rounding level.
+//        Four planes [row hi][row lo][column hi][column lo], each n_pad rows
+//        x 16 fp16 (32 B rows), loaded by TMA with the 32-byte swizzle.
 //
 // fp16 and TF32 both carry 11 significant bits, so the 3-term fp16 split
 // is as accurate as 3xTF32 (the fp32 accumulation dominates both), with
@@ -93,12 +102,13 @@ __global__ void maxabs_kernel(const double* __restrict__ x, int64_t n, int32_t d
     atomicMax(reinterpret_cast<unsigned long long*>(mean + d), (unsigned long long)__double_as_longlong(m));
 }
 
-// s = 2^e with max|x| * s < 2^14 (1 when every row is the mean)
+// s = 2^e with max|x| * s < 2^8 (1 when every row is the mean); 2^8 keeps
+// the norm block's M = (s^2/2)|x|^2 / 2^10 <= 32 d inside fp16 range
 __device__ __forceinline__ double operand_scale(double maxabs) {
   if (!(maxabs > 0.0)) return 1.0;
   int e;
   frexp(maxabs, &e);  // maxabs < 2^e
-  const int sh = 14 - e;  // clamped so 1/s^2 stays a normal fp32
+  const int sh = 8 - e;  // clamped so 1/s^2 stays a normal fp32
   return ldexp(1.0, sh < -60 ? -60 : (sh > 60 ? 60 : sh));
 }
 
@@ -111,7 +121,7 @@ __device__ __forceinline__ void split16(double xs, __half* hi, __half* lo, int64
 
 // One warp per (padded) row: centre in fp64, fp32 row for the FFMA engine,
 // scaled fp16 hi/lo planes for the tensor engine, fp64-accumulated squared
-// norm of the fp32 row.
+// norm of the fp32 row, and the row's entries of the norm block.
 __global__ void center_split_kernel(const double* __restrict__ x, int64_t n, int32_t d, int32_t dp,
                                     int64_t n_pad, const double* __restrict__ mean,
                                     __half* __restrict__ hi, float* __restrict__ xc_out,
@@ -121,7 +131,7 @@ __global__ void center_split_kernel(const double* __restrict__ x, int64_t n, int
   if (row >= n_pad) return;
   __half* lo = hi + n_pad * dp;
   const double s = operand_scale(mean[d]);
-  double sq = 0.0;
+  double sq = 0.0, sqs = 0.0;
   for (int f = lane; f < dp; f += 32) {
     double c = 0.0;
     if (row < n && f < d) {
@@ -133,9 +143,25 @@ __global__ void center_split_kernel(const double* __restrict__ x, int64_t n, int
     xc_out[row * dp + f] = xc;
     split16(c * s, hi, lo, row * dp + f);
     sq += (double)xc * (double)xc;
+    const double t = (double)__half2float(hi[row * dp + f]) + (double)__half2float(lo[row * dp + f]);
+    sqs += t * t;  // |x~ s|^2 of the split operands
   }
   sq = warp_sum_f64(sq);
+  sqs = warp_sum_f64(sqs);
   if (lane == 0) sqn[row] = row == n_pad - 1 ? (float)(1.0 / (s * s)) : (float)sq;
+  // norm block: lanes 0-15 write k = lane of the row / column operands
+  __half* nb = lo + n_pad * dp + row * 16 + lane;
+  const int64_t plane = n_pad * 16;
+  if (lane < 16) {
+    const double m = row < n ? -0.5 * sqs / 1024.0 : 0.0;
+    const __half mh = __float2half_rn((float)m);
+    const __half ml = __float2half_rn((float)(m - (double)__half2float(mh)));
+    const __half one = __float2half_rn(1024.f), zero = __float2half_rn(0.f);
+    nb[0] = lane == 0 ? one : (lane == 1 ? mh : zero);          // row operand hi
+    nb[plane] = lane == 1 ? ml : zero;                           // row operand lo
+    nb[2 * plane] = lane == 0 ? mh : (lane == 1 ? one : zero);   // column operand hi
+    nb[3 * plane] = lane == 0 ? ml : zero;                       // column operand lo
+  }
 }
 
 // Cosine kind (affinity.py:41-53, 88-95): one warp per (padded) row, fp64
@@ -173,6 +199,9 @@ __global__ void normalize_split_kernel(const double* __restrict__ x, int64_t n, 
     split16(u * s, hi, lo, row * dp + f);
   }
   if (lane == 0) sqn[row] = row == n_pad - 1 ? (float)(1.0 / (s * s)) : 1.f;
+  // the norm block is unused by the cosine kind: keep it zero
+  if (lane < 16)
+    for (int p = 0; p < 4; ++p) lo[n_pad * dp + p * n_pad * 16 + row * 16 + lane] = __float2half_rn(0.f);
 }
 
 }  // namespace

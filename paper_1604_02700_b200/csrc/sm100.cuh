@@ -10,6 +10,14 @@ namespace gpic {
 __device__ __forceinline__ uint32_t su32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
+// Align a dynamic shared-memory base by an offset (not by integer casts of
+// the pointer): the result keeps the shared address space, so accesses
+// compile to LDS / STS instead of generic LD / ST (which queue in the L1TEX
+// pipe behind outstanding global loads).
+template <int ALIGN>
+__device__ __forceinline__ uint8_t* smem_align(uint8_t* p) {
+  return p + ((ALIGN - (su32(p) & (ALIGN - 1))) & (ALIGN - 1));
+}
 __device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(count) : "memory");
 }
@@ -142,6 +150,16 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
   d |= (uint64_t)(1024u >> 4) << 32;  // stride byte offset: 8 rows x 128 B
   d |= (uint64_t)1u << 46;            // sm_100 descriptor version
   d |= (uint64_t)2u << 61;            // SWIZZLE_128B
+  return d;
+}
+// K-major, 32-byte swizzle (16 fp16 per row: the norm block), 8-row groups
+// 256 B apart (scripts/probe/umma_noswz.cu checks this layout on the GPU).
+__device__ __forceinline__ uint64_t sw32_desc(uint32_t saddr) {
+  uint64_t d = (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)1u << 16;           // leading byte offset (unused for swizzled K-major)
+  d |= (uint64_t)(256u >> 4) << 32;  // stride byte offset: 8 rows x 32 B
+  d |= (uint64_t)1u << 46;           // sm_100 descriptor version
+  d |= (uint64_t)6u << 61;           // SWIZZLE_32B
   return d;
 }
 // Instruction descriptor: kind::tf32, fp32 accumulate, K-major A and B.

@@ -230,8 +230,8 @@ def prepare_points(d, dev, kind: int = _lib.KIND_RBF) -> PreparedPoints:
     st = _stream(dev)
     dp = int(L.gpic_feature_pitch(m))
     npad = int(L.gpic_row_pad(n))
-    xhi = torch.empty((npad, dp), dtype=torch.float32, device=dev)
-    xlo = torch.empty_like(xhi)
+    xhi = torch.empty(int(L.gpic_operand_floats(n, m)), dtype=torch.float32, device=dev)
+    xlo = torch.empty((npad, dp), dtype=torch.float32, device=dev)
     sqn = torch.empty(npad, dtype=torch.float32, device=dev)
     ctl = _new_ctl(dev)
     work = torch.empty(((n + 255) // 256 + 1) * m + m, dtype=torch.float64, device=dev)

@@ -413,3 +413,65 @@ def test_matrix_free_matches_stored(golden, case):
     dd = po.degree(a)
     ref, _, _ = po.power_iteration(po.normalize(a, dd), po.start_vector(dd), TINY_EPS, 3)
     assert rel_l1(vT, ref) <= 1e-4
+
+
+def _mf_degrees(prep, sigma, lo, hi, sym, monkeypatch):
+    """gpic_mf_degrees (A 1 recomputed) over rows [lo, hi)."""
+    import ctypes as C
+
+    import torch
+
+    from paper_1604_02700_b200 import _lib
+
+    monkeypatch.setenv("GPIC_MF_SYM", "1" if sym else "0")
+    L = _lib.lib()
+    n, m, dev = prep.n, prep.d, prep.device
+    ones = torch.empty(int(L.gpic_vector_pitch(n)), dtype=torch.float32, device=dev)
+    ypart = torch.empty(int(L.gpic_mf_ypart_doubles(n, m, hi - lo)), dtype=torch.float64,
+                        device=dev)
+    deg = torch.empty(hi - lo, dtype=torch.float64, device=dev)
+    rc = L.gpic_mf_degrees(C.c_void_p(prep.xhi.data_ptr()), C.c_void_p(prep.xlo.data_ptr()),
+                           C.c_void_p(prep.sqn.data_ptr()), n, m, lo, hi, sigma, _lib.KIND_RBF,
+                           C.c_void_p(ones.data_ptr()), C.c_void_p(ypart.data_ptr()),
+                           C.c_void_p(deg.data_ptr()),
+                           C.c_void_p(torch.cuda.current_stream().cuda_stream))
+    assert rc == 0
+    return deg.cpu().numpy()
+
+
+@pytest.mark.parametrize("n,m", [(300, 2), (4500, 64), (9001, 16), (5000, 100), (4097, 200)])
+def test_matrix_free_symmetric_pass(monkeypatch, n, m):
+    """The upper-triangle matrix-free pass (row partials + transposed column
+    partials, both M-block layouts, several column chunks) gives the
+    full-square pass's degrees and the oracle's, and rows sharded or not."""
+    import torch
+
+    d = gaussian_blobs(n, m, 4, seed=n % 7)
+    # sigma >= 2 keeps the fp32 Gram within the 1e-4 degree gate for d = 2
+    # (radius-40 blobs: |x|^2 / 2 sigma^2 would otherwise reach ~1e3)
+    sigma = float(max(np.sqrt(m) / 2, 2.0))
+    prep = _gpu().prepare_points(d, torch.device("cuda"))
+    sym = _mf_degrees(prep, sigma, 0, n, True, monkeypatch)
+    full = _mf_degrees(prep, sigma, 0, n, False, monkeypatch)
+    half = _mf_degrees(prep, sigma, n // 3, n, True, monkeypatch)  # a shard: full-square path
+    ref = po.degree(po.affinity(d.points, sigma))
+    # a_ij and a_ji differ by the Gram's fp32 accumulation order (the MMA
+    # operands swap), so the two passes agree to the engine's own accuracy
+    assert np.max(np.abs(sym - full) / full) <= 5e-5
+    assert np.array_equal(half, full[n // 3:])
+    assert np.max(np.abs(sym - ref) / ref) <= 1e-4
+    # determinism of the sym pass
+    assert np.array_equal(sym, _mf_degrees(prep, sigma, 0, n, True, monkeypatch))
+
+
+def test_matrix_free_symmetric_cluster(golden, monkeypatch):
+    z = golden("gblobs_small")
+    d = DataSet(_points(z))
+    kind, params = GaussianRbf(float(z["sigma"])), PicParams(k=int(z["k"]))
+    monkeypatch.setenv("GPIC_MF_SYM", "0")
+    lf, vf, tf = cluster(d, kind, params, config=KernelConfig(storage="none"), seed=int(z["seed"]))
+    monkeypatch.setenv("GPIC_MF_SYM", "1")
+    ls, vs, ts = cluster(d, kind, params, config=KernelConfig(storage="none"), seed=int(z["seed"]))
+    assert np.array_equal(ls, lf) and np.array_equal(ls, z["labels"])
+    assert ts.iterations_run == tf.iterations_run
+    assert rel_l1(vs, vf) <= 1e-6

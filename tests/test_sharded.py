@@ -146,8 +146,14 @@ def test_two_processes_one_device_ipc():
 def test_matrix_free_virtual_ranks_bitwise():
     d = gaussian_blobs(2600, 64, 4, seed=8)
     kind, params = GaussianRbf(4.0), PicParams(k=4)
-    base = cluster(d, kind, params, config=KernelConfig(storage="none"), seed=3)
-    for p in (2, 5):
+    # one rank runs the upper-triangle pass; row shards the full-square pass,
+    # which is bitwise P-invariant
+    single = cluster(d, kind, params, config=KernelConfig(storage="none"), seed=3)
+    base = cluster(d, kind, params, seed=3,
+                   config=KernelConfig(p=2, virtual_ranks=True, storage="none"))
+    assert np.array_equal(single[0], base[0])
+    assert np.abs(single[1] - base[1]).sum() / np.abs(base[1]).sum() <= 1e-6
+    for p in (3, 5):
         got = cluster(d, kind, params, seed=3,
                       config=KernelConfig(p=p, virtual_ranks=True, storage="none"))
         assert np.array_equal(got[0], base[0]) and np.array_equal(got[1], base[1]), p
