@@ -242,18 +242,20 @@ def _gemv_roofline(args, L, C, torch, stream, st, n, m, k, T, work, v, storage):
         alg = 3.0 * 2.0 * n * n * dp
         name = "affinity_tc_kernel<matvec> (matrix-free A v: 3-term fp16 Gram + exp + v)"
         del scr
-    elif storage == 1:
+    elif storage in (1, 3):
         ntiles = int(L.gpic_packed_tiles(n))
-        tile_bytes = ntiles * 128 * 128 * 4
+        tile_bytes = ntiles * 128 * 128 * (4 if storage == 1 else 2)
         rowp = base + tile_bytes
         colp = rowp + ((ntiles * 128 * 4 + 255) // 256) * 256
+        fn = L.gpic_sym_matvec if storage == 1 else L.gpic_sym_matvec16
 
         def launch():
-            return L.gpic_sym_matvec(C.c_void_p(base), n, C.c_void_p(v32.data_ptr()),
-                                     C.c_void_p(rowp), C.c_void_p(colp),
-                                     C.c_void_p(deg1.data_ptr()), C.c_void_p(yv.data_ptr()), st)
+            return fn(C.c_void_p(base), n, C.c_void_p(v32.data_ptr()),
+                      C.c_void_p(rowp), C.c_void_p(colp),
+                      C.c_void_p(deg1.data_ptr()), C.c_void_p(yv.data_ptr()), st)
         alg = float(tile_bytes)
-        name = "sym_gemv_kernel + sym_reduce_kernel (packed symmetric tiles)"
+        name = ("sym_gemv_kernel + sym_reduce_kernel (packed symmetric tiles, "
+                + ("fp32)" if storage == 1 else "fp16)"))
     else:
         lda = int(L.gpic_affinity_pitch(n))
 
@@ -387,7 +389,9 @@ def run_ours(args, cfg, rank, world):
         "metric": METRIC, "value": ms / 1e3, "unit": "s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,
         "scaling": "strong", "vs_baseline": None,
-        "dtype": "f32 (3-term fp16-split tensor Gram, fp32 accumulate; fp64 vectors/reductions)",
+        "dtype": ("f32 (3-term fp16-split tensor Gram, fp32 accumulate; fp64 vectors/reductions)"
+                  if storage != 3 else
+                  "f16 W storage (fp32 Gram/exp, fp32 accumulate; fp64 vectors/reductions)"),
         "data": "synthetic (SURVEY App. B gaussian blobs, seed 0)",
         "config": dict(workload(cfg, world), affinity_engine=impl_name, storage=args.storage),
         "power_iter_hbm_gbs": achieved, "power_iter_dense_equiv_gbs": dense_equiv,
@@ -501,7 +505,7 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", type=int, default=3)
     ap.add_argument("--engine", choices=["tc", "simt"], default="tc")
-    ap.add_argument("--storage", choices=["packed", "dense", "none"], default="packed")
+    ap.add_argument("--storage", choices=["packed", "dense", "none", "packed16"], default="packed")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--gemv-reps", type=int, default=10)
     ap.add_argument("--ref-rows", type=int, default=256)

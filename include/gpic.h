@@ -179,6 +179,9 @@ int gpic_matvec(const float* d_a, int64_t lda, int64_t rows, int64_t n, const fl
  * gpic_packed_tiles(n) * 128 floats each (per-tile partials). */
 int gpic_sym_matvec(const float* d_tiles, int64_t n, const float* d_v, float* d_rowp,
                     float* d_colp, const double* d_row_scale, double* d_y, void* stream);
+/* Same over fp16 tiles (GPIC_STORAGE_PACKED16 layout, 128 x 128 halves each). */
+int gpic_sym_matvec16(const void* d_tiles, int64_t n, const float* d_v, float* d_rowp,
+                      float* d_colp, const double* d_row_scale, double* d_y, void* stream);
 int64_t gpic_vector_pitch(int64_t n);
 
 /* ---- whole pipeline ----------------------------------------------------
@@ -198,6 +201,11 @@ int64_t gpic_vector_pitch(int64_t n);
  * recomputed from X by the tcgen05 engine with the multiply-by-v fused into
  * the exp epilogue (compute-bound instead of HBM-bound). */
 #define GPIC_STORAGE_NONE 2
+/* packed upper-triangle tiles stored as fp16 (A in [0, 1]; the compressed-W
+ * option of SURVEY.md §8f-2): a quarter of the dense bytes per iteration.
+ * Degrees are the sums of the stored (rounded) values, so W = D^-1 A stays
+ * row-stochastic; fp32 accumulation everywhere. Opt-in: the default is fp32. */
+#define GPIC_STORAGE_PACKED16 3
 int64_t gpic_packed_tiles(int64_t n);
 int64_t gpic_cluster_workspace_bytes(int64_t n, int32_t d, int32_t k, int32_t max_iter,
                                      int32_t storage);

@@ -40,6 +40,8 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <cuda_fp16.h>
+
 #include <cstdlib>
 
 #include "common.cuh"
@@ -50,7 +52,11 @@ namespace gpic {
 
 namespace {
 
-enum { kModeDense = 0, kModePacked = 1, kModeMatvec = 2 };
+enum { kModeDense = 0, kModePacked = 1, kModeMatvec = 2, kModePacked16 = 3 };
+// packed symmetric tiles, fp32 (kModePacked) or fp16 (kModePacked16) values
+__host__ __device__ constexpr bool is_packed(int MODE) {
+  return MODE == kModePacked || MODE == kModePacked16;
+}
 
 constexpr int kBN = 128;           // columns per tile (one MMA N)
 constexpr int kKBlk = 64;          // fp16 per 128-byte swizzle row
@@ -192,7 +198,7 @@ struct Cursor {
       chunk = cb / kChunkTiles;
       cb_end = (int)min((int64_t)(chunk + 1) * kChunkTiles, a.n_ctiles);
     } else {
-      cb = MODE == kModePacked ? rb * MB : 0;
+      cb = is_packed(MODE) ? rb * MB : 0;
     }
     return true;
   }
@@ -236,14 +242,14 @@ struct Cursor {
     if (u >= u_end) return;
     if (++cb == a.n_ctiles) {
       ++rb;
-      cb = MODE == kModePacked ? rb * MB : 0;
+      cb = is_packed(MODE) ? rb * MB : 0;
     }
   }
 };
 
 template <int MB, int MODE>
 __host__ __device__ inline int64_t total_units(const TcArgs& a) {
-  if (MODE == kModePacked) return packed_items(a.n_rtiles, a.n_ctiles, MB);
+  if (is_packed(MODE)) return packed_items(a.n_rtiles, a.n_ctiles, MB);
   if (MODE == kModeMatvec) return a.n_rtiles * a.n_chunks;  // (strided: unused)
   return a.n_rtiles * a.n_ctiles;
 }
@@ -482,7 +488,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int buf = i & 1;
       const int64_t tI = rb * MB + m;  // tile row of this warp's rows
       // packed: the lower-triangle half of a diagonal row block is not stored
-      const bool store_ok = MODE != kModePacked || tI <= cb;
+      const bool store_ok = !is_packed(MODE) || tI <= cb;
       // matvec sym: row partials from tiles J >= I, column partials from J > I
       const bool row_ok = MODE != kModeMatvec || !args.sym || tI <= cb;
       const bool col_ok = MODE == kModeMatvec && args.sym && tI < cb;
@@ -558,6 +564,16 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (col == grow[rr] || col >= args.n || grow[rr] >= args.n) vals[x] = 0.f;
           }
         }
+        if constexpr (MODE == kModePacked16) {
+          // degrees from the stored (rounded) values: W = D^-1 A stays
+          // exactly row-stochastic in the stored precision
+#pragma unroll
+          for (int x = 0; x < 32; x += 2) {
+            const float2 f = __half22float2(__floats2half2_rn(vals[x], vals[x + 1]));
+            vals[x] = f.x;
+            vals[x + 1] = f.y;
+          }
+        }
         if constexpr (MODE == kModeMatvec) {
           if (row_ok) {
 #pragma unroll
@@ -610,26 +626,41 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (lane == 0) tma_store_wait_read<0>();
             __syncwarp();
           }
+          if constexpr (MODE == kModePacked16) {
+            // fp16 box: 32 rows x 64 B, 64-byte swizzle (16-byte chunk ^
+            // (R >> 1) & 3); 4-byte stores, conflict-free
 #pragma unroll
-          for (int x = 0; x < 32; x += 2) {
-            const int R = (x >> 4) * 16 + tq + ((x >> 1) & 1) * 8;
-            const int cq = ((x >> 2) & 3) * 2 + (tc >> 2);  // 16-byte chunk of the columns
-            const uint32_t addr = su32(stage) + R * 128 + ((cq ^ (R & 7)) << 4) + (tc & 3) * 4;
-            asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(addr), "f"(vals[x]),
-                         "f"(vals[x + 1])
-                         : "memory");
+            for (int x = 0; x < 32; x += 2) {
+              const int R = (x >> 4) * 16 + tq + ((x >> 1) & 1) * 8;
+              const int blk = (x >> 2) & 3;
+              const uint32_t addr = su32(stage) + R * 64 + ((blk ^ ((R >> 1) & 3)) << 4) + tc * 2;
+              const __half2 h = __floats2half2_rn(vals[x], vals[x + 1]);
+              asm volatile("st.shared.b32 [%0], %1;" ::"r"(addr),
+                           "r"(*reinterpret_cast<const uint32_t*>(&h))
+                           : "memory");
+            }
+          } else {
+#pragma unroll
+            for (int x = 0; x < 32; x += 2) {
+              const int R = (x >> 4) * 16 + tq + ((x >> 1) & 1) * 8;
+              const int cq = ((x >> 2) & 3) * 2 + (tc >> 2);  // 16-byte chunk of the columns
+              const uint32_t addr = su32(stage) + R * 128 + ((cq ^ (R & 7)) << 4) + (tc & 3) * 4;
+              asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(addr), "f"(vals[x]),
+                           "f"(vals[x + 1])
+                           : "memory");
+            }
           }
           fence_async_smem();
           __syncwarp();
           if (lane == 0 && store_ok) {
-            const int64_t out_row0 = MODE == kModePacked
+            const int64_t out_row0 = is_packed(MODE)
                                          ? tile_index(tI, cb, args.n_ctiles) * 128 + q * 32
                                          : lr0;
-            tma_store_2d(&map_out, MODE == kModePacked ? ch * 32 : (int)col0, (int)out_row0, stage,
+            tma_store_2d(&map_out, is_packed(MODE) ? ch * 32 : (int)col0, (int)out_row0, stage,
                          stream_pol);
           }
           ++stores;
-          if (MODE == kModePacked && store_ok && tI != cb) {
+          if (is_packed(MODE) && store_ok && tI != cb) {
             // degrees of the tile's COLUMN rows (A is symmetric): per column
             // slot k, this thread's 4 rows, then a reduce-scatter over the 8
             // threads sharing the slot (xor 16, 8, 4): thread (tq, quad) ends
@@ -744,7 +775,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int rr = 0; rr < 4; ++rr) {
             const int rloc = (rr >> 1) * 16 + tq + (rr & 1) * 8;  // row within the warp's 32
-            if constexpr (MODE == kModePacked) {
+            if constexpr (is_packed(MODE)) {
               args.degrow[tile_index(tI, cb, args.n_ctiles) * 128 + q * 32 + rloc] = tot[rr];
             } else {
               const int64_t lrow = lr0 + rloc;
@@ -887,13 +918,17 @@ int64_t packed_tiles(int64_t n) {
 int packed_row_halves(int32_t /*dp*/) { return 1; }  // the epilogue combines a row's warps
 
 int launch_affinity_tc_packed(const float* xhi, const float* xlo, const float* sqn, int64_t n,
-                              int32_t dp, float neg_scale_log2, float* a_packed, float* degrow,
-                              float* degcol, cudaStream_t s, int kind) {
+                              int32_t dp, float neg_scale_log2, void* a_packed, float* degrow,
+                              float* degcol, cudaStream_t s, int kind, bool half_out) {
   Maps mp;
   int rc = operand_maps(xhi, n, dp, &mp);
   if (rc) return rc;
-  if (!make_map(&mp.out, a_packed, 128, (uint64_t)packed_tiles(n) * 128, 512, 32, 32))
-    return fail(GPIC_E_CUDA, "cuTensorMapEncodeTiled failed");
+  const bool ok = half_out ? make_map(&mp.out, a_packed, 128, (uint64_t)packed_tiles(n) * 128, 256,
+                                      32, 32, CU_TENSOR_MAP_DATA_TYPE_FLOAT16,
+                                      CU_TENSOR_MAP_SWIZZLE_64B)
+                           : make_map(&mp.out, a_packed, 128, (uint64_t)packed_tiles(n) * 128, 512,
+                                      32, 32);
+  if (!ok) return fail(GPIC_E_CUDA, "cuTensorMapEncodeTiled failed");
   TcArgs args{};
   args.n_pad = row_pad(n);
   args.sqn = sqn;
@@ -902,10 +937,11 @@ int launch_affinity_tc_packed(const float* xhi, const float* xlo, const float* s
   args.rows = n;
   args.ns = neg_scale_log2;
   args.n_ctiles = ceil_div(n, kBN);
-  args.out = a_packed;
+  args.out = static_cast<float*>(a_packed);
   args.degrow = degrow;
   args.degcol = degcol;
   args.kind = kind;
+  if (half_out) return dispatch_kb<kModePacked16>(dp / kKBlk, mp, args, s);
   return dispatch_kb<kModePacked>(dp / kKBlk, mp, args, s);
 }
 

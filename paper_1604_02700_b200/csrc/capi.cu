@@ -263,6 +263,19 @@ int gpic_scale(const double* d_src, int64_t n, double tau, double* d_dst, float*
 
 int64_t gpic_kmeans_scratch_bytes(int64_t n, int32_t k) { return kmeans_scratch_bytes(n, k); }
 
+int gpic_sym_matvec16(const void* d_tiles, int64_t n, const float* d_v, float* d_rowp,
+                      float* d_colp, const double* d_row_scale, double* d_y, void* stream) {
+  if (n < 1) return fail(GPIC_E_EMPTY, "empty matrix");
+  PeerTable pt;
+  std::memset(&pt, 0, sizeof pt);
+  pt.y[0][0] = pt.y[0][1] = d_y;
+  pt.nranks = 1;
+  launch_sym_gemv16(d_tiles, n, d_v, d_rowp, d_colp, d_row_scale, pt, nullptr,
+                    static_cast<cudaStream_t>(stream));
+  GPIC_CUDA_TRY(cudaGetLastError());
+  return GPIC_OK;
+}
+
 int gpic_sym_matvec(const float* d_tiles, int64_t n, const float* d_v, float* d_rowp,
                     float* d_colp, const double* d_row_scale, double* d_y, void* stream) {
   if (n < 1) return fail(GPIC_E_EMPTY, "empty matrix");
@@ -315,6 +328,8 @@ int64_t gpic_cluster_workspace_bytes(int64_t n, int32_t d, int32_t k, int32_t ma
   const int64_t scratch = workspace_bytes(n, d, k, n, max_iter);
   if (storage == GPIC_STORAGE_PACKED)  // tiles + GEMV partials (2) + degree partials (<= 2 + 4)
     return scratch + packed_tiles(n) * 128 * 128 * 4 + 8 * al(sym_partial_floats(n) * 4);
+  if (storage == GPIC_STORAGE_PACKED16)
+    return scratch + packed_tiles(n) * 128 * 128 * 2 + 8 * al(sym_partial_floats(n) * 4);
   if (storage == GPIC_STORAGE_NONE)
     return scratch + al(mf_ypart_doubles(n, feature_pitch(d), n) * 8);
   return scratch + n * affinity_pitch(n) * 4;
@@ -353,7 +368,7 @@ int cluster_impl(const double* d_x, int64_t n, int32_t d, double sigma, int32_t 
   if (kind == GPIC_KIND_COSINE) sigma = 1.0;  // unused
   if (storage != GPIC_STORAGE_DENSE && impl != GPIC_AFFINITY_TC)
     return fail(GPIC_E_UNSUPPORTED, "packed / matrix-free storage runs on the tcgen05 engine");
-  if (storage < GPIC_STORAGE_DENSE || storage > GPIC_STORAGE_NONE)
+  if (storage < GPIC_STORAGE_DENSE || storage > GPIC_STORAGE_PACKED16)
     return fail(GPIC_E_INVALID, "unknown storage mode");
   Workspace ws;
   const int64_t scratch = workspace_bytes(n, d, k, n, max_iter);
@@ -372,8 +387,10 @@ int cluster_impl(const double* d_x, int64_t n, int32_t d, double sigma, int32_t 
   const int64_t lda = affinity_pitch(n);
   ShardLoop L;
   std::memset(&L, 0, sizeof L);
-  if (storage == GPIC_STORAGE_PACKED) {
-    float* rowp = a + packed_tiles(n) * 128 * 128;
+  if (storage == GPIC_STORAGE_PACKED || storage == GPIC_STORAGE_PACKED16) {
+    const bool half = storage == GPIC_STORAGE_PACKED16;
+    float* rowp = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(a) +
+                                           packed_tiles(n) * 128 * 128 * (half ? 2 : 4));
     float* colp = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(rowp) + al(sym_partial_floats(n) * 4));
     // degree partials from the affinity epilogue (row sums + column sums of
     // every stored tile, consistent with the stored fp32 values)
@@ -381,11 +398,11 @@ int cluster_impl(const double* d_x, int64_t n, int32_t d, double sigma, int32_t 
     float* degrow = colp + pf;
     float* degcol = degrow + 2 * pf;
     rc = launch_affinity_tc_packed(ws.xhi, ws.xlo, ws.sqn, n, dp, neg_scale_log2, a, degrow,
-                                   degcol, s, kind);
+                                   degcol, s, kind, half);
     if (rc) return rc;
     mark(ev, 1, s);
     launch_sym_degree(degrow, degcol, n, packed_row_halves(dp), deg, ws.ctl, s);
-    L.mode = kLoopPacked;
+    L.mode = half ? kLoopPacked16 : kLoopPacked;
     L.rowp = rowp;
     L.colp = colp;
   } else if (storage == GPIC_STORAGE_NONE) {

@@ -32,8 +32,9 @@ int64_t sym_partial_floats(int64_t n);  // packed_tiles(n) * 128
 // tiles), combined by launch_sym_degree.
 int packed_row_halves(int32_t dp);
 int launch_affinity_tc_packed(const float* xhi, const float* xlo, const float* sqn, int64_t n,
-                              int32_t dp, float neg_scale_log2, float* a_packed, float* degrow,
-                              float* degcol, cudaStream_t s, int kind = GPIC_KIND_RBF);
+                              int32_t dp, float neg_scale_log2, void* a_packed, float* degrow,
+                              float* degcol, cudaStream_t s, int kind = GPIC_KIND_RBF,
+                              bool half_out = false);
 void launch_sym_degree(const float* degrow, const float* degcol, int64_t n, int nhalf,
                        double* deg, gpic_ctl* ctl, cudaStream_t s);
 void sym_prepare();
@@ -119,6 +120,9 @@ void launch_copy_result(const double* v64, int64_t n, double* out, const gpic_ct
 struct PeerTable;
 void launch_sym_gemv(const float* tiles, int64_t n, const float* v32, float* rowp, float* colp,
                      const double* deg, const PeerTable& pt, gpic_ctl* ctl, cudaStream_t s);
+// fp16 packed tiles (GPIC_STORAGE_PACKED16): same partials / reduce
+void launch_sym_gemv16(const void* tiles, int64_t n, const float* v32, float* rowp, float* colp,
+                       const double* deg, const PeerTable& pt, gpic_ctl* ctl, cudaStream_t s);
 
 // ---- matrix-free (affinity_tc.cu matvec mode + mf.cu) --------------------
 struct MfOperands {
@@ -147,7 +151,7 @@ int launch_mf_matvec(const MfOperands& op, int64_t row_lo, int64_t rows, const f
 int launch_mf_degrees(const MfOperands& op, int64_t row_lo, int64_t rows, float* ones,
                       double* ypart, double* deg, cudaStream_t s);
 
-enum { kLoopDense = 0, kLoopPacked = 1, kLoopMatrixFree = 2 };
+enum { kLoopDense = 0, kLoopPacked = 1, kLoopMatrixFree = 2, kLoopPacked16 = 3 };
 
 // One shard's loop state (a single-rank run is one shard with nranks = 1).
 struct ShardLoop {

@@ -300,6 +300,8 @@ int run_power_loops(ShardLoop* shards, int nlocal, int64_t n, int32_t max_iter, 
         const ShardLoop& L = shards[i];
         if (L.mode == kLoopPacked) {
           launch_sym_gemv(L.a, n, L.v32, L.rowp, L.colp, L.deg, L.pt, L.ctl, cs);
+        } else if (L.mode == kLoopPacked16) {
+          launch_sym_gemv16(L.a, n, L.v32, L.rowp, L.colp, L.deg, L.pt, L.ctl, cs);
         } else if (L.mode == kLoopMatrixFree) {
           const int rc = launch_mf_matvec(L.mf, L.row_lo, L.rows, L.v32, L.ypart, L.deg, L.pt,
                                           L.ctl, cs);

@@ -15,6 +15,8 @@
 //                     every rank's y (same epilogue as the dense GEMV).
 // Degrees are the same GEMV with v = 1 (exactly consistent with the stored
 // fp32 values). Every sum has a fixed order, so results are deterministic.
+#include <cuda_fp16.h>
+
 #include <cstdlib>
 
 #include "common.cuh"
@@ -27,11 +29,31 @@ namespace {
 
 constexpr int kTS = 128;
 constexpr int kTileFloats = kTS * kTS;
-constexpr int kStages = 3;
+constexpr int kStages = 3;  // fp32 tiles (64 KB); fp16 tiles (32 KB) use 2x the stages
 constexpr int kWarps = 8;                   // consumers; 16 rows each
 constexpr int kRowsPerWarp = kTS / kWarps;  // 16
 constexpr int kThreads = (kWarps + 1) * 32;
 constexpr int kSmem = kStages * kTileFloats * 4 + 2 * kWarps * kTS * 4 + 64 + 128;
+template <typename T>
+struct TileTraits;  // element type of the stored tiles
+template <>
+struct TileTraits<float> {
+  static constexpr int kStg = kStages;
+  // 4 consecutive values of row i at this lane's columns
+  __device__ static float4 load4(const uint8_t* row, int lane) {
+    return reinterpret_cast<const float4*>(row)[lane];
+  }
+};
+template <>
+struct TileTraits<__half> {
+  static constexpr int kStg = 2 * kStages;
+  __device__ static float4 load4(const uint8_t* row, int lane) {
+    const uint2 u = reinterpret_cast<const uint2*>(row)[lane];
+    const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&u.x));
+    const float2 b = __half22float2(*reinterpret_cast<const __half2*>(&u.y));
+    return make_float4(a.x, a.y, b.x, b.y);
+  }
+};
 
 __host__ __device__ inline int64_t tile_index(int64_t I, int64_t J, int64_t nt) {
   return I * nt - I * (I - 1) / 2 + (J - I);
@@ -48,14 +70,17 @@ __device__ inline void tile_coords(int64_t t, int64_t nt, int64_t& I, int64_t& J
   J = I + (t - (I * nt - I * (I - 1) / 2));
 }
 
+template <typename T>
 __global__ void __launch_bounds__(kThreads, 1)
-    sym_gemv_kernel(const float* __restrict__ tiles, int64_t nt, const float* __restrict__ v32,
+    sym_gemv_kernel(const T* __restrict__ tiles, int64_t nt, const float* __restrict__ v32,
                     float* __restrict__ rowp, float* __restrict__ colp,
-                    const gpic_ctl* __restrict__ ctl, int split, int pol) {
+                    const gpic_ctl* __restrict__ ctl, int split, int pol, int ablate) {
+  constexpr int kStages = TileTraits<T>::kStg;
+  constexpr int kTileBytes = kTileFloats * (int)sizeof(T);
   if (ctl != nullptr && *(volatile const int32_t*)&ctl->stop) return;
   extern __shared__ uint8_t smem_raw[];
-  float* st = reinterpret_cast<float*>(smem_align<128>(smem_raw));
-  float* red = st + kStages * kTileFloats;  // [2][kWarps][128] column partials
+  uint8_t* st = smem_align<128>(smem_raw);
+  float* red = reinterpret_cast<float*>(st + kStages * kTileBytes);  // [2][kWarps][128] column partials
   uint64_t* full = reinterpret_cast<uint64_t*>(red + 2 * kWarps * kTS);
   uint64_t* empty = full + kStages;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -76,15 +101,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     int s = 0;
     uint32_t ph = 0;
     const uint64_t once = policy_evict_first();  // every tile is read once per pass
-    const uint32_t piece = kTileFloats / split;
+    const uint32_t piece = kTileBytes / split;
+    const uint8_t* src0 = reinterpret_cast<const uint8_t*>(tiles);
     for (int64_t t = t0; t < t1; ++t) {
       mbar_wait(&empty[s], ph ^ 1);
-      mbar_expect_tx(&full[s], kTileFloats * 4);
+      mbar_expect_tx(&full[s], kTileBytes);
       for (int p = 0; p < split; ++p) {
-        float* dst = st + s * kTileFloats + p * piece;
-        const float* src = tiles + t * kTileFloats + p * piece;
-        if (pol) bulk_load(dst, src, piece * 4, &full[s], once);
-        else bulk_load(dst, src, piece * 4, &full[s]);
+        uint8_t* dst = st + s * kTileBytes + p * piece;
+        const uint8_t* src = src0 + t * kTileBytes + p * piece;
+        if (pol) bulk_load(dst, src, piece, &full[s], once);
+        else bulk_load(dst, src, piece, &full[s]);
       }
       if (++s == kStages) { s = 0; ph ^= 1; }
     }
@@ -117,12 +143,19 @@ __global__ void __launch_bounds__(kThreads, 1)
       vi_next = load_vi(In);
     }
     mbar_wait(&full[s], ph);
-    const float* tile = st + s * kTileFloats + warp * kRowsPerWarp * kTS;
+    if (ablate == 1) {  // measurement only (GPIC_SYM_ABLATE=1): stream without compute
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+      if (++s == kStages) { s = 0; ph ^= 1; }
+      if (++J == nt) { ++I; J = I; }
+      continue;
+    }
+    const uint8_t* tile = st + s * kTileBytes + warp * kRowsPerWarp * kTS * (int)sizeof(T);
     float acc[kRowsPerWarp];
     float4 cp = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
     for (int i = 0; i < kRowsPerWarp; ++i) {
-      const float4 a = reinterpret_cast<const float4*>(tile + i * kTS)[lane];
+      const float4 a = TileTraits<T>::load4(tile + i * kTS * (int)sizeof(T), lane);
       const float vi = __shfl_sync(0xffffffffu, vi_l, i);
       float r = a.x * vj.x;
       r = fmaf(a.y, vj.y, r);
@@ -206,11 +239,19 @@ __global__ void __launch_bounds__(kTS * kSeg)
   const int64_t p0 = nt * sg / kSeg, p1 = nt * (sg + 1) / kSeg;
   double s = 0.0;
   const int64_t diag = tile_index(R, R, nt);
-#pragma unroll 4
-  for (int64_t p = p0; p < p1; ++p) {
-    const float x = p < R ? colp[tile_index(p, R, nt) * kTS + o] : rowp[(diag + (p - R)) * kTS + o];
-    s += (double)x;
+  auto load = [&](int64_t p) {
+    return p < R ? colp[tile_index(p, R, nt) * kTS + o] : rowp[(diag + (p - R)) * kTS + o];
+  };
+  // batches of 8 independent loads in flight, then added in order
+  int64_t p = p0;
+  for (; p + 8 <= p1; p += 8) {
+    float x[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) x[u] = load(p + u);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) s += (double)x[u];
   }
+  for (; p < p1; ++p) s += (double)load(p);
   part[sg][o] = s;
   __syncthreads();
   const int64_t i = R * kTS + o;
@@ -270,7 +311,8 @@ __global__ void __launch_bounds__(kTS * kSeg)
 }
 
 int g_sms = 0;
-int g_split = 1, g_pol = 0;  // evict_first on the tile stream measured 4% slower  // GEMV copy shape (GPIC_SYM_SPLIT pieces per tile, GPIC_SYM_POL)
+int g_split = 1, g_pol = 0;  // evict_first on the tile stream measured 4% slower
+int g_ablate = 0;  // GEMV copy shape (GPIC_SYM_SPLIT pieces per tile, GPIC_SYM_POL)
 
 }  // namespace
 
@@ -286,12 +328,14 @@ void sym_prepare() {
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaFuncSetAttribute(sym_gemv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+    cudaFuncSetAttribute(sym_gemv_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+    cudaFuncSetAttribute(sym_gemv_kernel<__half>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
     if (const char* e = getenv("GPIC_SYM_SPLIT")) {
       const int v = atoi(e);
       if (v == 1 || v == 2 || v == 4 || v == 8 || v == 16) g_split = v;
     }
     if (const char* e = getenv("GPIC_SYM_POL")) g_pol = atoi(e) != 0;
+    if (const char* e = getenv("GPIC_SYM_ABLATE")) g_ablate = atoi(e);
   }
 }
 
@@ -306,7 +350,21 @@ void launch_sym_gemv(const float* tiles, int64_t n, const float* v32, float* row
   const int64_t nt = ceil_div(n, kTS);
   const int64_t total = nt * (nt + 1) / 2;
   const int grid = (int)(total < g_sms ? total : g_sms);
-  sym_gemv_kernel<<<grid, kThreads, kSmem, s>>>(tiles, nt, v32, rowp, colp, ctl, g_split, g_pol);
+  sym_gemv_kernel<float><<<grid, kThreads, kSmem, s>>>(tiles, nt, v32, rowp, colp, ctl, g_split,
+                                                           g_pol, g_ablate);
+  sym_reduce_kernel<<<(unsigned)nt, kTS * kSeg, 0, s>>>(rowp, colp, n, nt, deg, pt, ctl);
+  count_launch(2);
+}
+
+void launch_sym_gemv16(const void* tiles, int64_t n, const float* v32, float* rowp, float* colp,
+                       const double* deg, const PeerTable& pt, gpic_ctl* ctl, cudaStream_t s) {
+  sym_prepare();
+  const int64_t nt = ceil_div(n, kTS);
+  const int64_t total = nt * (nt + 1) / 2;
+  const int grid = (int)(total < g_sms ? total : g_sms);
+  sym_gemv_kernel<__half><<<grid, kThreads, kSmem, s>>>(static_cast<const __half*>(tiles), nt, v32,
+                                                            rowp, colp, ctl, g_split, g_pol,
+                                                            g_ablate);
   sym_reduce_kernel<<<(unsigned)nt, kTS * kSeg, 0, s>>>(rowp, colp, n, nt, deg, pt, ctl);
   count_launch(2);
 }

@@ -85,7 +85,7 @@ class KMeansParams:
 DEFAULT_MEMORY_BUDGET = 256 * 1024 * 1024
 
 AFFINITY_IMPLS = ("tc", "simt")
-STORAGES = ("packed", "dense", "none")
+STORAGES = ("packed", "dense", "none", "packed16")
 
 
 @dataclass(frozen=True)
@@ -100,12 +100,15 @@ class KernelConfig:
     invariance tests this way). ``chunk_rows`` / ``memory_budget_bytes``
     keep their reference meaning for the host port; the GPU builds whole
     row shards in one launch. ``affinity_impl`` picks the Gram engine:
-    "tc" (tcgen05 3xTF32, default) or "simt" (FP32 FFMA, the comparator).
+    "tc" (tcgen05, 3-term fp16 split, default) or "simt" (FP32 FFMA, the
+    comparator).
     ``storage`` = "packed" keeps only the upper triangle of 128x128 tiles
     of the (exactly symmetric) affinity matrix — half the HBM bytes of the
     affinity store and of every power iteration; "dense" keeps full rows
     (used by the SIMT engine and by row-sharded multi-rank runs); "none" is
-    matrix-free: A is recomputed from X for every product (n^2 > HBM).
+    matrix-free: A is recomputed from X for every product (n^2 > HBM);
+    "packed16" is "packed" with fp16 values (opt-in compressed W: half the
+    bytes again, degrees from the stored values, fp32 accumulation).
     """
 
     p: int = 1
@@ -135,6 +138,10 @@ class KernelConfig:
             if self.affinity_impl != "tc":
                 raise InvalidSpec("matrix-free storage runs on the tcgen05 engine")
             return 2
+        if self.storage == "packed16":
+            if self.affinity_impl != "tc" or self.p != 1:
+                raise InvalidSpec("fp16 packed storage runs on the tcgen05 engine, one rank")
+            return 3
         if self.storage == "packed" and self.affinity_impl == "tc" and self.p == 1:
             return 1
         return 0

@@ -475,3 +475,59 @@ def test_matrix_free_symmetric_cluster(golden, monkeypatch):
     assert np.array_equal(ls, lf) and np.array_equal(ls, z["labels"])
     assert ts.iterations_run == tf.iterations_run
     assert rel_l1(vs, vf) <= 1e-6
+
+
+@pytest.mark.parametrize("case", ["config1", "gblobs_small", "gblobs_balanced"])
+def test_packed16_storage_matches_reference(golden, case):
+    """fp16 packed tiles (opt-in compressed W): labels identical to the
+    reference, v within the 1e-4 gate at a forced iteration count, iteration
+    count within +-2 under the native stop rule."""
+    z = golden(case)
+    d = DataSet(_points(z))
+    kind, params = GaussianRbf(float(z["sigma"])), PicParams(k=int(z["k"]))
+    cfg = KernelConfig(storage="packed16")
+    labels, v, trace = cluster(d, kind, params, config=cfg, seed=int(z["seed"]))
+    assert np.array_equal(labels, z["labels"])
+    assert abs(trace.iterations_run - int(z["iterations"])) <= 2
+    T = 4
+    _, vT, _ = cluster(d, kind, PicParams(k=int(z["k"]), epsilon=TINY_EPS, max_iterations=T),
+                       config=cfg, seed=int(z["seed"]))
+    a = po.affinity(d.points, float(z["sigma"]))
+    dd = po.degree(a)
+    ref, _, _ = po.power_iteration(po.normalize(a, dd), po.start_vector(dd), TINY_EPS, T)
+    assert rel_l1(vT, ref) <= 1e-4
+
+
+def test_sym_matvec16_against_numpy():
+    """fp16 packed-tile GEMV equals the dense product of the rounded tiles."""
+    import ctypes as C
+
+    import torch
+
+    from paper_1604_02700_b200 import _lib
+
+    L = _lib.lib()
+    rng = np.random.default_rng(6)
+    for n in (1, 130, 1000):
+        a = rng.uniform(0, 1, (n, n))
+        a = ((a + a.T) / 2).astype(np.float16)
+        nt = -(-n // 128)
+        full = np.zeros((nt * 128, nt * 128), dtype=np.float16)
+        full[:n, :n] = a
+        tiles = [full[i * 128:(i + 1) * 128, j * 128:(j + 1) * 128]
+                 for i in range(nt) for j in range(i, nt)]
+        dev = torch.device("cuda")
+        t_dev = torch.from_numpy(np.stack(tiles)).to(dev)
+        v = rng.uniform(0, 1, n)
+        v32 = torch.zeros(int(L.gpic_vector_pitch(n)), dtype=torch.float32, device=dev)
+        v32[:n] = torch.from_numpy(v.astype(np.float32)).to(dev)
+        rowp = torch.empty(len(tiles) * 128, dtype=torch.float32, device=dev)
+        colp = torch.empty_like(rowp)
+        y = torch.empty(n, dtype=torch.float64, device=dev)
+        rc = L.gpic_sym_matvec16(C.c_void_p(t_dev.data_ptr()), n, C.c_void_p(v32.data_ptr()),
+                                 C.c_void_p(rowp.data_ptr()), C.c_void_p(colp.data_ptr()), None,
+                                 C.c_void_p(y.data_ptr()),
+                                 C.c_void_p(torch.cuda.current_stream().cuda_stream))
+        assert rc == 0
+        ref = a.astype(np.float64) @ v.astype(np.float32).astype(np.float64)
+        assert np.max(np.abs(y.cpu().numpy() - ref) / np.abs(ref)) <= 1e-5, n
