@@ -459,13 +459,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(GW * 32) : "memory");
     };
     float vrow[4] = {0.f, 0.f, 0.f, 0.f};  // matvec sym: v_i of the 4 rows (column partials)
-    int64_t grow[4] = {0, 0, 0, 0};
+    int grow[4] = {0, 0, 0, 0};  // row / column indices fit 32 bits (n < 2^31)
+    const int n32 = (int)args.n, row_lo32 = (int)args.row_lo;
     // matvec sym: the warps holding the same columns (all quadrants, both M
     // blocks) exchange column partials through smem; one writer per group
     float* colx = reinterpret_cast<float*>(sOut + kEpiWarps * 32 * 8);
     const uint32_t colbar = 9 + c_lo / UPW;
     const bool col_writer = q == 0 && m == 0;
-    int64_t cur_rb = -1;
+    int cur_rb = -1;
     // matvec: v_j of a tile arrives one tile ahead by cp.async into this
     // warp's double buffer: lane l copies column l of each of its chunks
     float* colw = sCol + e * (2 * 64);
@@ -482,23 +483,23 @@ __global__ void __launch_bounds__(kThreads, 1)
     c.begin(args, u_begin, u_end);
     if (c.valid()) fetch_cols(c.cb, 0);
     for (; c.valid(); ++i) {
-      const int64_t rb = c.rb, cb = c.cb;
+      const int rb = c.rb, cb = c.cb;
       const bool item_last = c.item_last();
       const int chunk = c.chunk;
       const int buf = i & 1;
-      const int64_t tI = rb * MB + m;  // tile row of this warp's rows
+      const int tI = rb * MB + m;  // tile row of this warp's rows
       // packed: the lower-triangle half of a diagonal row block is not stored
       const bool store_ok = !is_packed(MODE) || tI <= cb;
       // matvec sym: row partials from tiles J >= I, column partials from J > I
       const bool row_ok = MODE != kModeMatvec || !args.sym || tI <= cb;
       const bool col_ok = MODE == kModeMatvec && args.sym && tI < cb;
-      const int64_t lr0 = (rb * MB + m) * 128 + q * 32;  // shard-local first row of this warp
+      const int lr0 = (rb * MB + m) * 128 + q * 32;  // shard-local first row of this warp
       if (rb != cur_rb) {
         // this thread's 4 rows: rr = 2*half + {0: tq, 1: tq + 8}
 #pragma unroll
         for (int rr = 0; rr < 4; ++rr) {
-          grow[rr] = args.row_lo + lr0 + (rr >> 1) * 16 + tq + (rr & 1) * 8;
-          if (MODE == kModeMatvec) vrow[rr] = grow[rr] < args.n ? __ldg(args.v32 + grow[rr]) : 0.f;
+          grow[rr] = row_lo32 + lr0 + (rr >> 1) * 16 + tq + (rr & 1) * 8;
+          if (MODE == kModeMatvec) vrow[rr] = grow[rr] < n32 ? __ldg(args.v32 + grow[rr]) : 0.f;
         }
         cur_rb = rb;
       }
@@ -521,7 +522,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int cc = 0; cc < UPW; ++cc) {
         const int ch = c_lo + cc;
         uint32_t r[32];  // [hf][block b][4]: (row tq, c), (row tq, c+1), (row tq+8, c), (row tq+8, c+1)
-        const int64_t col0 = cb * kBN + ch * 32;
+        const int col0 = cb * kBN + ch * 32;
         // matvec: this thread's 8 columns' v_j from the staged copy
         float vcol[8];
         if constexpr (MODE == kModeMatvec) {
@@ -542,8 +543,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           __syncwarp();
           if (lane == 0) mbar_arrive(&t_empty[buf]);
         }
-        const bool diag = (col0 < args.row_lo + lr0 + 32) && (args.row_lo + lr0 < col0 + 32);
-        const bool pad = col0 + 32 > args.n || args.row_lo + lr0 + 32 > args.n;
+        const bool diag = (col0 < row_lo32 + lr0 + 32) && (row_lo32 + lr0 < col0 + 32);
+        const bool pad = col0 + 32 > n32 || row_lo32 + lr0 + 32 > n32;
         float vals[32];
 #pragma unroll
         for (int x = 0; x < 32; ++x) {
@@ -560,8 +561,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int x = 0; x < 32; ++x) {
             const int rr = (x >> 4) * 2 + ((x >> 1) & 1);
-            const int64_t col = col0 + ((x >> 2) & 3) * 8 + tc + (x & 1);
-            if (col == grow[rr] || col >= args.n || grow[rr] >= args.n) vals[x] = 0.f;
+            const int col = col0 + ((x >> 2) & 3) * 8 + tc + (x & 1);
+            if (col == grow[rr] || col >= n32 || grow[rr] >= n32) vals[x] = 0.f;
           }
         }
         if constexpr (MODE == kModePacked16) {
