@@ -185,7 +185,7 @@ def run_reference(args, cfg, rank):
     line = {
         "metric": METRIC, "value": value, "unit": "s", "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": value * 1e3, "higher_is_better": False,
-        "scaling": "weak" if args.gpus > 1 else "strong", "vs_baseline": None, "dtype": "f64",
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "impl": "reference",
         "config": workload(cfg, args.gpus),
         "cpu_baseline": {"value": value, "unit": "s", "cores": threads, "kind": "port",
@@ -239,8 +239,17 @@ def _gemv_roofline(args, L, C, torch, stream, st, n, m, k, T, work, v, storage):
             return L.gpic_mf_degrees(C.c_void_p(xhi), C.c_void_p(xlo), C.c_void_p(sqn), n, m, 0, n,
                                      sigma, _lib.KIND_RBF, C.c_void_p(ones.data_ptr()),
                                      C.c_void_p(ypart.data_ptr()), C.c_void_p(yv.data_ptr()), st)
-        alg = 3.0 * 2.0 * n * n * dp
-        name = "affinity_tc_kernel<matvec> (matrix-free A v: 3-term fp16 Gram + exp + v)"
+        # the whole-matrix pass computes the upper triangle of tile pairs
+        # (MB row tiles x 1 column tile each, J >= MB * I): entries actually
+        # computed x 3 terms x 2 x (dp + 16 norm-block columns)
+        mb = 2 if dp == 64 else 1
+        nrt, nct = -(-n // (128 * mb)), -(-n // 128)
+        items = nrt * nct - mb * nrt * (nrt - 1) // 2
+        if os.environ.get("GPIC_MF_SYM", "1") == "0":
+            items = nrt * nct
+        alg = 3.0 * 2.0 * (dp + 16) * float(items) * 128 * mb * 128
+        name = ("affinity_tc_kernel<matvec> (matrix-free symmetric A v pass: 3-term fp16 Gram "
+                "with the distance from the MMA, exp2, row + column products)")
         del scr
     elif storage in (1, 3):
         ntiles = int(L.gpic_packed_tiles(n))
@@ -381,9 +390,9 @@ def run_ours(args, cfg, rank, world):
     traffic = None
     prof = ROOT / "profiles" / "gemv_traffic.json"
     if prof.exists():
-        j = json.loads(prof.read_text())
-        if j.get("storage", "packed") == args.storage and j.get("n") == n:
-            traffic = j.get("dram_bytes_per_launch")
+        for ent in json.loads(prof.read_text()).get("entries", []):
+            if ent.get("storage") == args.storage and ent.get("n") == n:
+                traffic = ent.get("dram_bytes_per_launch")
 
     line = {
         "metric": METRIC, "value": ms / 1e3, "unit": "s", "n_gpus": world, "steps": args.steps,
@@ -428,10 +437,19 @@ def run_ours_sharded(args, cfg, rank, world):
     from paper_1604_02700_b200 import _lib, sharded
     from paper_1604_02700_b200.validation import adjusted_rand_index, contingency
 
-    local = int(os.environ.get("LOCAL_RANK", rank))
+    # GPIC_BENCH_SAME_DEVICE=1 (functional check on a one-GPU box only): every
+    # rank shares device 0 (CUDA IPC still carries the exchange) and the
+    # timing collectives go over gloo; the timings it prints are not N-GPU
+    # numbers
+    same = os.environ.get("GPIC_BENCH_SAME_DEVICE") == "1"
+    local = 0 if same else int(os.environ.get("LOCAL_RANK", rank))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    dist.init_process_group("nccl", device_id=dev)
+    if same:
+        dist.init_process_group("gloo")
+    else:
+        dist.init_process_group("nccl", device_id=dev)
+    cdev = torch.device("cpu") if same else dev
     c = CONFIGS[cfg]
     d = config_dataset(cfg, seed=0)
     n, m, k, sigma = d.n, d.m, c["k"], c["sigma"]
@@ -457,7 +475,7 @@ def run_ours_sharded(args, cfg, rank, world):
         torch.cuda.synchronize()
     dist.barrier()
     ms_local = ev0.elapsed_time(ev1) / args.steps
-    t = torch.tensor([ms_local], device=dev)
+    t = torch.tensor([ms_local], device=cdev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
     launches = (L.gpic_launch_count() - launches0) // args.steps
@@ -474,7 +492,7 @@ def run_ours_sharded(args, cfg, rank, world):
         lab_e, v_e, _ = runner.run(d_host, GaussianRbf(sigma), params, 0)
         lab_e, v_e = lab_e.cpu().numpy(), v_e.cpu().numpy()
         e2e.append(time.perf_counter() - t0)
-    te = torch.tensor([statistics.mean(e2e)], device=dev)
+    te = torch.tensor([statistics.mean(e2e)], device=cdev)
     dist.all_reduce(te, op=dist.ReduceOp.MAX)
     runner.close()
     if rank == 0:

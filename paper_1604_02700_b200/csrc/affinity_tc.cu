@@ -454,7 +454,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     const float m2ns = -2.f * args.ns * gs;
     uint32_t tf_bits = 0;  // TMEM-full parity per accumulator buffer
     int i = 0;
-    double acc64[4] = {0.0, 0.0, 0.0, 0.0};  // matvec: the 4 rows' partials over an item
+    // matvec: the 4 rows' partials over an item as unevaluated fp32 pairs
+    // (hi + lo, TwoSum per tile: ~46 significant bits, FMA pipe only) and
+    // converted to fp64 once per item — an fp64 add per tile waits on a
+    // f32 -> f64 conversion queued behind the saturated ex2 pipe
+    float acc_hi[4] = {0.f, 0.f, 0.f, 0.f}, acc_lo[4] = {0.f, 0.f, 0.f, 0.f};
     auto group_sync = [&]() {
       asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(GW * 32) : "memory");
     };
@@ -724,8 +728,16 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
 #pragma unroll
-        for (int rr = 0; rr < 4; ++rr) acc64[rr] += (double)rsum[rr];
+        for (int rr = 0; rr < 4; ++rr) {
+          const float t = acc_hi[rr] + rsum[rr];
+          const float bb = t - acc_hi[rr];
+          acc_lo[rr] += (acc_hi[rr] - (t - bb)) + (rsum[rr] - bb);
+          acc_hi[rr] = t;
+        }
         if (item_last) {
+          double acc64[4];
+#pragma unroll
+          for (int rr = 0; rr < 4; ++rr) acc64[rr] = (double)acc_hi[rr] + (double)acc_lo[rr];
           double tot[4] = {acc64[0], acc64[1], acc64[2], acc64[3]};
           if (GW > 1) {
             if (quad_lead)
@@ -747,7 +759,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               if (lrow < args.rows) args.ypart[(int64_t)chunk * args.rows_pad + lrow] = tot[rr];
             }
 #pragma unroll
-          for (int rr = 0; rr < 4; ++rr) acc64[rr] = 0.0;
+          for (int rr = 0; rr < 4; ++rr) acc_hi[rr] = acc_lo[rr] = 0.f;
         }
       } else if (MODE == kModeDense || store_ok) {
         // row sums of the tile's rows: the group's warps combine in order

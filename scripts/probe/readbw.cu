@@ -27,7 +27,7 @@ __global__ void ldg_kernel(const float4* __restrict__ a, size_t n4, float* out) 
 
 template <int STAGES>
 __global__ void bulk_kernel(const char* __restrict__ a, size_t bytes, uint32_t chunk, int split,
-                            float* out) {
+                            float* out, float* side = nullptr, int side_floats = 0) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* st = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
   uint64_t* full = reinterpret_cast<uint64_t*>(st + STAGES * chunk);
@@ -60,11 +60,45 @@ __global__ void bulk_kernel(const char* __restrict__ a, size_t bytes, uint32_t c
   for (size_t c = c0; c < c1; ++c) {
     mbar_wait(&full[s], ph);
     acc += reinterpret_cast<const float*>(st + s * chunk)[warp * 32 + lane];
+    // optional side stream: side_floats floats written per chunk (the GEMV's
+    // per-tile partials), spread over the consumer warps
+    for (int f = warp * 32 + lane; f < side_floats; f += nw * 32) side[c * side_floats + f] = acc;
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
     if (++s == STAGES) { s = 0; ph ^= 1; }
   }
   if (acc == 12345.f) *out = acc;
+}
+
+__global__ void stg_kernel(float4* __restrict__ a, size_t n4) {
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  const float4 z = make_float4(1.f, 2.f, 3.f, (float)threadIdx.x);
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) __stcs(a + i, z);
+}
+
+// smem -> global bulk stores (cp.async.bulk.global.shared::cta), chunk bytes
+// per store, `depth` stores in flight per CTA
+__global__ void bulk_store_kernel(char* __restrict__ a, size_t bytes, uint32_t chunk, int depth) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* st = smem_align<128>(smem_raw);
+  for (int i = threadIdx.x; i < (int)chunk; i += blockDim.x) st[i] = (uint8_t)i;
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  const size_t nchunks = bytes / chunk;
+  const size_t c0 = nchunks * blockIdx.x / gridDim.x, c1 = nchunks * (blockIdx.x + 1) / gridDim.x;
+  int inflight = 0;
+  for (size_t c = c0; c < c1; ++c) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(a + c * chunk),
+                 "r"(su32(st)), "r"(chunk)
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    if (++inflight >= depth) {
+      asm volatile("cp.async.bulk.wait_group.read 8;" ::: "memory");
+      inflight = 8;
+    }
+  }
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 int main(int argc, char** argv) {
@@ -106,13 +140,37 @@ int main(int argc, char** argv) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     char nm[64];
     snprintf(nm, sizeof nm, "bulk %dx%uKB split=%d warps=%d", stages, chunk >> 10, split, warps);
-    timeit(nm, [&] { kern<<<sms, (warps + 1) * 32, smem>>>(a, bytes, chunk, split, out); });
+    timeit(nm, [&] { kern<<<sms, (warps + 1) * 32, smem>>>(a, bytes, chunk, split, out, nullptr, 0); });
   };
   for (int split : {1, 4, 16}) bulk(bulk_kernel<3>, 3, 65536, split, 8);
   bulk(bulk_kernel<6>, 6, 32768, 1, 8);
   bulk(bulk_kernel<12>, 12, 16384, 1, 8);
   bulk(bulk_kernel<4>, 4, 49152, 1, 8);
   bulk(bulk_kernel<2>, 2, 65536, 1, 8);
+  {
+    float* side;
+    cudaMalloc(&side, (bytes / 65536) * 256 * 4 + 4096);
+    for (int sf : {128, 256}) {
+      cudaFuncSetAttribute(bulk_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 3 * 65536 + 256);
+      char nm[64];
+      snprintf(nm, sizeof nm, "bulk 3x64KB + %d B written per tile", sf * 4);
+      timeit(nm, [&] { bulk_kernel<3><<<sms, 9 * 32, 3 * 65536 + 256>>>(a, bytes, 65536, 1, out, side, sf); });
+    }
+    cudaFree(side);
+  }
+  for (int th : {256, 1024})
+    for (int bpsm : {1, 4}) {
+      char nm[64];
+      snprintf(nm, sizeof nm, "stg grid=%dx%d th=%d (write)", bpsm, sms, th);
+      timeit(nm, [&] { stg_kernel<<<bpsm * sms, th>>>((float4*)a, bytes / 16); });
+    }
+  for (uint32_t chunk : {4096u, 16384u, 65536u}) {
+    cudaFuncSetAttribute(bulk_store_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, chunk + 256);
+    char nm[64];
+    snprintf(nm, sizeof nm, "bulk store %uKB depth 16 (write)", chunk >> 10);
+    timeit(nm, [&] { bulk_store_kernel<<<sms, 128, chunk + 256>>>(a, bytes, chunk, 16); });
+  }
+  timeit("cudaMemsetAsync (write)", [&] { cudaMemsetAsync(a, 1, bytes); });
   printf("err: %s\n", cudaGetErrorString(cudaGetLastError()));
   return 0;
 }
