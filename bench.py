@@ -255,7 +255,7 @@ def _gemv_roofline(args, L, C, torch, stream, st, n, m, k, T, work, v, storage):
         ntiles = int(L.gpic_packed_tiles(n))
         tile_bytes = ntiles * 128 * 128 * (4 if storage == 1 else 2)
         rowp = base + tile_bytes
-        colp = rowp + ((ntiles * 128 * 4 + 255) // 256) * 256
+        colp = rowp + ((int(L.gpic_sym_partial_floats(n)) * 4 + 255) // 256) * 256
         fn = L.gpic_sym_matvec if storage == 1 else L.gpic_sym_matvec16
 
         def launch():

@@ -176,9 +176,11 @@ int gpic_matvec(const float* d_a, int64_t lda, int64_t rows, int64_t n, const fl
 /* k_multiply on PACKED symmetric tiles (gpic_packed_tiles(n) tiles of
  * 128 x 128 fp32, upper triangle): y = (A v) * scale_i. d_v holds
  * gpic_vector_pitch(n) floats (zero padded); d_rowp / d_colp hold
- * gpic_packed_tiles(n) * 128 floats each (per-tile partials). */
+ * gpic_sym_partial_floats(n) floats each (super-block partial records). */
 int gpic_sym_matvec(const float* d_tiles, int64_t n, const float* d_v, float* d_rowp,
                     float* d_colp, const double* d_row_scale, double* d_y, void* stream);
+/* Floats of each partial buffer (d_rowp, d_colp) of gpic_sym_matvec[16]. */
+int64_t gpic_sym_partial_floats(int64_t n);
 /* Same over fp16 tiles (GPIC_STORAGE_PACKED16 layout, 128 x 128 halves each). */
 int gpic_sym_matvec16(const void* d_tiles, int64_t n, const float* d_v, float* d_rowp,
                       float* d_colp, const double* d_row_scale, double* d_y, void* stream);

@@ -92,6 +92,7 @@ SIGNATURES = {
     "gpic_mf_degrees": (C.c_int, [P, P, P, I64, I32, I64, I64, F64, I32, P, P, P, P]),
     "gpic_sym_matvec": (C.c_int, [P, I64, P, P, P, P, P, P]),
     "gpic_sym_matvec16": (C.c_int, [P, I64, P, P, P, P, P, P]),
+    "gpic_sym_partial_floats": (I64, [I64]),
     "gpic_cluster_workspace_bytes": (I64, [I64, I32, I32, I32, I32]),
     "gpic_cluster": (C.c_int, [P, I64, I32, F64, I32, I32, F64, I32, I64, P, I32, I32, P, P, P,
                                P, P, P, I64, P]),

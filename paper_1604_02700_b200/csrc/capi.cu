@@ -321,6 +321,7 @@ int gpic_matvec(const float* d_a, int64_t lda, int64_t rows, int64_t n, const fl
 }
 
 int64_t gpic_packed_tiles(int64_t n) { return n < 1 ? -1 : packed_tiles(n); }
+int64_t gpic_sym_partial_floats(int64_t n) { return n < 1 ? -1 : sym_partial_floats(n); }
 
 int64_t gpic_cluster_workspace_bytes(int64_t n, int32_t d, int32_t k, int32_t max_iter,
                                      int32_t storage) {

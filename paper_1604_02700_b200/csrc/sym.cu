@@ -5,16 +5,18 @@
 // per-iteration GEMV read (2n^2 instead of 4n^2 bytes).
 //
 //   sym_gemv_kernel   streams every stored tile once (1-D bulk copies into a
-//                     3-stage smem ring) and produces, per tile, the 128 row
-//                     partials  sum_j T[i][j] v_J[j]   (for y_I) and, off the
-//                     diagonal, the 128 column partials  sum_i T[i][j] v_I[i]
-//                     (for y_J = (T^T v_I)_J). fp32 within a tile.
-//   sym_reduce_kernel y_i = sum over the row's tiles in column order (fp64):
-//                     column partials of tiles (J', R), J' < R, then row
-//                     partials of tiles (R, J), J >= R; / deg_i; stored into
+//                     smem ring), walking 4 x 4-tile super-blocks, and
+//                     produces per super-block the 128 row partials
+//                     sum_j T[i][j] v_J[j] of each of its tile rows (for y_I)
+//                     and, off the diagonal, the 128 column partials
+//                     sum_i T[i][j] v_I[i] of each tile column (for
+//                     y_J = (T^T v_I)_J). fp32 within a super-block.
+//   sym_reduce_kernel y_i = sum over the row's super-block records (fp64):
+//                     column records of (P', Q(i)), P' <= Q(i), then row
+//                     records of (Q(i), Q'), Q' >= Q(i); / deg_i; stored into
 //                     every rank's y (same epilogue as the dense GEMV).
-// Degrees are the same GEMV with v = 1 (exactly consistent with the stored
-// fp32 values). Every sum has a fixed order, so results are deterministic.
+// Degrees come from the affinity epilogue's per-tile partials (sums of the
+// stored values). Every sum has a fixed order, so results are deterministic.
 #include <cuda_fp16.h>
 
 #include <cstdlib>
@@ -33,7 +35,7 @@ constexpr int kStages = 3;  // fp32 tiles (64 KB); fp16 tiles (32 KB) use 2x the
 constexpr int kWarps = 8;                   // consumers; 16 rows each
 constexpr int kRowsPerWarp = kTS / kWarps;  // 16
 constexpr int kThreads = (kWarps + 1) * 32;
-constexpr int kSmem = kStages * kTileFloats * 4 + 2 * kWarps * kTS * 4 + 64 + 128;
+constexpr int kSmem = kStages * kTileFloats * 4 + 2 * kWarps * kTS * 4 + 4 * kTS * 4 + 64 + 128;
 template <typename T>
 struct TileTraits;  // element type of the stored tiles
 template <>
@@ -70,18 +72,62 @@ __device__ inline void tile_coords(int64_t t, int64_t nt, int64_t& I, int64_t& J
   J = I + (t - (I * nt - I * (I - 1) / 2));
 }
 
+// Super-blocks of kSB x kSB tiles, (P, Q >= P) row-major over the
+// NS x NS triangle (NS = ceil(NT / kSB)), same index formula as the tiles.
+constexpr int kSB = 4;
+
+// The tiles of one super-block, in the order both roles walk them: rows
+// I = kSB P .. (< NT), then columns J = max(I, kSB Q) .. (< NT).
+struct SbWalk {
+  int64_t nt, ns;
+  int64_t P, Q, I, J;
+  int64_t i_end, j_end;
+  __device__ void open(int64_t p, int64_t q) {
+    P = p;
+    Q = q;
+    I = kSB * P;
+    i_end = min(I + kSB, nt);
+    j_end = min(kSB * Q + kSB, nt);
+    J = max(I, kSB * Q);
+  }
+  // advance to the next tile of the super-block; false at its end
+  __device__ bool next() {
+    if (++J < j_end) return true;
+    if (++I >= i_end) return false;
+    J = max(I, kSB * Q);
+    return J < j_end;
+  }
+  __device__ void next_sb() {
+    if (++Q == ns) {
+      ++P;
+      Q = P;
+    }
+  }
+};
+
+// Packed GEMV with super-block aggregation. Per stored tile (I, J) the 8
+// consumer warps (16 rows each) form the row products sum_j T[i][j] v_J[j]
+// (kept per lane across the row's tiles of the super-block) and, off the
+// diagonal, the column products sum_i T[i][j] v_I[i] (combined across warps
+// in smem and accumulated per column tile in I order). One 128-float record
+// per (super-block, tile row) and per (super-block, tile column) goes to
+// HBM: ~2 KB of partials per 16 tiles (1 MB) instead of 1 KB per 64 KB tile
+// (measured: 1 KB of writes per 64 KB read costs a read stream ~7 %,
+// scripts/probe/readbw.cu). Every sum has a fixed shape independent of the
+// grid, so results are deterministic and grid-invariant.
 template <typename T>
 __global__ void __launch_bounds__(kThreads, 1)
     sym_gemv_kernel(const T* __restrict__ tiles, int64_t nt, const float* __restrict__ v32,
                     float* __restrict__ rowp, float* __restrict__ colp,
-                    const gpic_ctl* __restrict__ ctl, int split, int pol, int ablate) {
+                    const gpic_ctl* __restrict__ ctl) {
   constexpr int kStages = TileTraits<T>::kStg;
   constexpr int kTileBytes = kTileFloats * (int)sizeof(T);
   if (ctl != nullptr && *(volatile const int32_t*)&ctl->stop) return;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* st = smem_align<128>(smem_raw);
   float* red = reinterpret_cast<float*>(st + kStages * kTileBytes);  // [2][kWarps][128] column partials
-  uint64_t* full = reinterpret_cast<uint64_t*>(red + 2 * kWarps * kTS);
+  float* colacc = red + 2 * kWarps * kTS;                            // [kSB][128] per super-block
+  uint64_t* full = reinterpret_cast<uint64_t*>(colacc + kSB * kTS);
   uint64_t* empty = full + kStages;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -92,27 +138,33 @@ __global__ void __launch_bounds__(kThreads, 1)
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  const int64_t total = nt * (nt + 1) / 2;
-  const int64_t t0 = total * blockIdx.x / gridDim.x;
-  const int64_t t1 = total * (blockIdx.x + 1) / gridDim.x;
+  const int64_t ns = (nt + kSB - 1) / kSB;
+  const int64_t total = ns * (ns + 1) / 2;
+  const int64_t s0 = total * blockIdx.x / gridDim.x;
+  const int64_t s1 = total * (blockIdx.x + 1) / gridDim.x;
+  if (s0 >= s1) return;
+  SbWalk w;
+  w.nt = nt;
+  w.ns = ns;
+  int64_t P0, Q0;
+  tile_coords(s0, ns, P0, Q0);
 
   if (warp == kWarps) {  // producer
     if (lane != 0) return;
     int s = 0;
     uint32_t ph = 0;
-    const uint64_t once = policy_evict_first();  // every tile is read once per pass
-    const uint32_t piece = kTileBytes / split;
     const uint8_t* src0 = reinterpret_cast<const uint8_t*>(tiles);
-    for (int64_t t = t0; t < t1; ++t) {
-      mbar_wait(&empty[s], ph ^ 1);
-      mbar_expect_tx(&full[s], kTileBytes);
-      for (int p = 0; p < split; ++p) {
-        uint8_t* dst = st + s * kTileBytes + p * piece;
-        const uint8_t* src = src0 + t * kTileBytes + p * piece;
-        if (pol) bulk_load(dst, src, piece, &full[s], once);
-        else bulk_load(dst, src, piece, &full[s]);
-      }
-      if (++s == kStages) { s = 0; ph ^= 1; }
+    w.P = P0;
+    w.Q = Q0;
+    for (int64_t sb = s0; sb < s1; ++sb, w.next_sb()) {
+      w.open(w.P, w.Q);
+      do {
+        mbar_wait(&empty[s], ph ^ 1);
+        mbar_expect_tx(&full[s], kTileBytes);
+        bulk_load(st + s * kTileBytes, src0 + tile_index(w.I, w.J, nt) * kTileBytes, kTileBytes,
+                  &full[s]);
+        if (++s == kStages) { s = 0; ph ^= 1; }
+      } while (w.next());
     }
     return;
   }
@@ -120,101 +172,112 @@ __global__ void __launch_bounds__(kThreads, 1)
   int s = 0;
   uint32_t ph = 0;
   int rb = 0;
-  int64_t I = 0, J = 0;
-  if (t0 < t1) tile_coords(t0, nt, I, J);
-  // v slices of the next tile are loaded one tile ahead (L2 latency off the
-  // per-tile critical path)
-  auto load_vj = [&](int64_t j) { return __ldg(reinterpret_cast<const float4*>(v32 + j * kTS) + lane); };
-  auto load_vi = [&](int64_t i) {
-    return lane < kRowsPerWarp ? __ldg(v32 + i * kTS + warp * kRowsPerWarp + lane) : 0.f;
-  };
-  float4 vj_next = make_float4(0.f, 0.f, 0.f, 0.f);
-  float vi_next = 0.f;
-  if (t0 < t1) {
-    vj_next = load_vj(J);
-    vi_next = load_vi(I);
-  }
-  for (int64_t t = t0; t < t1; ++t) {
-    const float4 vj = vj_next;
-    const float vi_l = vi_next;
-    if (t + 1 < t1) {
-      const int64_t In = J + 1 == nt ? I + 1 : I, Jn = J + 1 == nt ? I + 1 : J + 1;
-      vj_next = load_vj(Jn);
-      vi_next = load_vi(In);
-    }
-    mbar_wait(&full[s], ph);
-    if (ablate == 1) {  // measurement only (GPIC_SYM_ABLATE=1): stream without compute
+  const int t = threadIdx.x;  // consumers: threads < 128 own one column of colacc
+  if (t < kTS)
+    for (int k = 0; k < kSB; ++k) colacc[k * kTS + t] = 0.f;
+  w.P = P0;
+  w.Q = Q0;
+  for (int64_t sb = s0; sb < s1; ++sb, w.next_sb()) {
+    w.open(w.P, w.Q);
+    float acc[kRowsPerWarp];
+#pragma unroll
+    for (int i = 0; i < kRowsPerWarp; ++i) acc[i] = 0.f;
+    float vi_l = lane < kRowsPerWarp ? __ldg(v32 + w.I * kTS + warp * kRowsPerWarp + lane) : 0.f;
+    float4 vj = __ldg(reinterpret_cast<const float4*>(v32 + w.J * kTS) + lane);
+    for (;;) {
+      const int64_t I = w.I, J = w.J;
+      const bool more = w.next();
+      const bool row_end = !more || w.I != I;
+      // next tile's v slices, one tile ahead
+      float4 vj_n = vj;
+      float vi_n = vi_l;
+      if (more) {
+        vj_n = __ldg(reinterpret_cast<const float4*>(v32 + w.J * kTS) + lane);
+        if (row_end && lane < kRowsPerWarp) vi_n = __ldg(v32 + w.I * kTS + warp * kRowsPerWarp + lane);
+      }
+      mbar_wait(&full[s], ph);
+      const uint8_t* tile = st + s * kTileBytes + warp * kRowsPerWarp * kTS * (int)sizeof(T);
+      float4 cp = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int i = 0; i < kRowsPerWarp; ++i) {
+        const float4 a = TileTraits<T>::load4(tile + i * kTS * (int)sizeof(T), lane);
+        const float vi = __shfl_sync(0xffffffffu, vi_l, i);
+        float r = fmaf(a.x, vj.x, acc[i]);
+        r = fmaf(a.y, vj.y, r);
+        r = fmaf(a.z, vj.z, r);
+        acc[i] = fmaf(a.w, vj.w, r);
+        cp.x = fmaf(a.x, vi, cp.x);
+        cp.y = fmaf(a.y, vi, cp.y);
+        cp.z = fmaf(a.z, vi, cp.z);
+        cp.w = fmaf(a.w, vi, cp.w);
+      }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
       if (++s == kStages) { s = 0; ph ^= 1; }
-      if (++J == nt) { ++I; J = I; }
-      continue;
-    }
-    const uint8_t* tile = st + s * kTileBytes + warp * kRowsPerWarp * kTS * (int)sizeof(T);
-    float acc[kRowsPerWarp];
-    float4 cp = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (I != J) {
+        // column products of this tile: the 8 warps combine in order, then
+        // accumulate into the super-block's record of column tile J (I order)
+        float* rw = red + rb * kWarps * kTS;
+        reinterpret_cast<float4*>(rw + warp * kTS)[lane] = cp;
+        asm volatile("bar.sync 1, %0;" ::"n"(kWarps * 32) : "memory");
+        if (t < kTS) {
+          float c = 0.f;
 #pragma unroll
-    for (int i = 0; i < kRowsPerWarp; ++i) {
-      const float4 a = TileTraits<T>::load4(tile + i * kTS * (int)sizeof(T), lane);
-      const float vi = __shfl_sync(0xffffffffu, vi_l, i);
-      float r = a.x * vj.x;
-      r = fmaf(a.y, vj.y, r);
-      r = fmaf(a.z, vj.z, r);
-      acc[i] = fmaf(a.w, vj.w, r);
-      cp.x = fmaf(a.x, vi, cp.x);
-      cp.y = fmaf(a.y, vi, cp.y);
-      cp.z = fmaf(a.z, vi, cp.z);
-      cp.w = fmaf(a.w, vi, cp.w);
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);
-    if (++s == kStages) { s = 0; ph ^= 1; }
-    // transpose-reduce the 16 row partials across the 32 lanes (fixed
-    // pattern): after 4 halving steps lane l holds row f(l) over 16 lanes,
-    // the last xor-1 step completes it.
+          for (int w8 = 0; w8 < kWarps; ++w8) c += rw[w8 * kTS + t];
+          colacc[(J - kSB * w.Q) * kTS + t] += c;
+        }
+        rb ^= 1;  // double-buffered: the next tile writes the other half
+      }
+      if (row_end) {
+        // transpose-reduce the 16 row accumulators across the 32 lanes
+        // (fixed pattern): after 4 halving steps lane l holds row f(l) over
+        // 16 lanes, the last xor-1 step completes it
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const bool up = lane & 16;
-      const float send = up ? acc[k] : acc[k + 8];
-      const float keep = up ? acc[k + 8] : acc[k];
-      acc[k] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
-    }
+        for (int k = 0; k < 8; ++k) {
+          const bool up = lane & 16;
+          const float send = up ? acc[k] : acc[k + 8];
+          const float keep = up ? acc[k + 8] : acc[k];
+          acc[k] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+        }
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const bool up = lane & 8;
-      const float send = up ? acc[k] : acc[k + 4];
-      const float keep = up ? acc[k + 4] : acc[k];
-      acc[k] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
-    }
+        for (int k = 0; k < 4; ++k) {
+          const bool up = lane & 8;
+          const float send = up ? acc[k] : acc[k + 4];
+          const float keep = up ? acc[k + 4] : acc[k];
+          acc[k] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+        }
 #pragma unroll
-    for (int k = 0; k < 2; ++k) {
-      const bool up = lane & 4;
-      const float send = up ? acc[k] : acc[k + 2];
-      const float keep = up ? acc[k + 2] : acc[k];
-      acc[k] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
-    }
-    {
-      const bool up = lane & 2;
-      const float send = up ? acc[0] : acc[1];
-      const float keep = up ? acc[1] : acc[0];
-      acc[0] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
-    }
-    acc[0] += __shfl_xor_sync(0xffffffffu, acc[0], 1);
-    const int row = ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 +
-                    ((lane >> 1) & 1);
-    if ((lane & 1) == 0) rowp[t * kTS + warp * kRowsPerWarp + row] = acc[0];
-    // column partials: combine the 8 warps in order
-    float* rw = red + rb * kWarps * kTS;
-    reinterpret_cast<float4*>(rw + warp * kTS)[lane] = cp;
-    asm volatile("bar.sync 1, %0;" ::"n"(kWarps * 32) : "memory");
-    if (I != J && threadIdx.x < kTS) {
-      float c = 0.f;
+        for (int k = 0; k < 2; ++k) {
+          const bool up = lane & 4;
+          const float send = up ? acc[k] : acc[k + 2];
+          const float keep = up ? acc[k + 2] : acc[k];
+          acc[k] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+        }
+        {
+          const bool up = lane & 2;
+          const float send = up ? acc[0] : acc[1];
+          const float keep = up ? acc[1] : acc[0];
+          acc[0] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+        }
+        acc[0] += __shfl_xor_sync(0xffffffffu, acc[0], 1);
+        const int row = ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 +
+                        ((lane >> 1) & 1);
+        if ((lane & 1) == 0)
+          rowp[(sb * kSB + (I - kSB * w.P)) * kTS + warp * kRowsPerWarp + row] = acc[0];
 #pragma unroll
-      for (int w = 0; w < kWarps; ++w) c += rw[w * kTS + threadIdx.x];
-      colp[t * kTS + threadIdx.x] = c;
+        for (int i = 0; i < kRowsPerWarp; ++i) acc[i] = 0.f;
+      }
+      vj = vj_n;
+      vi_l = vi_n;
+      if (!more) break;
     }
-    rb ^= 1;  // double-buffered: the next tile writes the other half
-    if (++J == nt) { ++I; J = I; }
+    // the super-block's column records (thread t owns column t of every
+    // record: its own adds precede these reads in program order)
+    if (t < kTS)
+      for (int k = 0; k < kSB; ++k) {
+        colp[(sb * kSB + k) * kTS + t] = colacc[k * kTS + t];
+        colacc[k * kTS + t] = 0.f;
+      }
   }
 }
 
@@ -222,10 +285,11 @@ __device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
   asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
-// One CTA per tile row R (128 rows), 8 segments of the row's NT tiles per
-// row: segment s sums its contiguous column-tile range in order (column
-// partials of tiles (p, R) for p < R, row partials of (R, p) for p >= R),
-// then the 8 segment sums are added in order. The shape depends on NT only.
+// One CTA per tile row R (128 rows of y), kSeg segments over the row's
+// ns + 1 super-block records in a fixed order: column records of the
+// super-blocks (P', Q) for P' = 0 .. Q (Q = R / kSB; tiles (I, R) with I < R),
+// then row records of (Q, Q') for Q' = Q .. ns - 1 (tiles (R, J >= R)); the
+// segment sums are added in order. The shape depends on NT only.
 constexpr int kSeg = 8;
 
 __global__ void __launch_bounds__(kTS * kSeg)
@@ -236,20 +300,22 @@ __global__ void __launch_bounds__(kTS * kSeg)
   __shared__ double part[kSeg][kTS];
   const int64_t R = blockIdx.x;
   const int o = threadIdx.x % kTS, sg = threadIdx.x / kTS;
-  const int64_t p0 = nt * sg / kSeg, p1 = nt * (sg + 1) / kSeg;
-  double s = 0.0;
-  const int64_t diag = tile_index(R, R, nt);
+  const int64_t ns = (nt + kSB - 1) / kSB;
+  const int64_t Q = R / kSB, k = R - kSB * Q;
+  const int64_t terms = ns + 1;
+  const int64_t p0 = terms * sg / kSeg, p1 = terms * (sg + 1) / kSeg;
   auto load = [&](int64_t p) {
-    return p < R ? colp[tile_index(p, R, nt) * kTS + o] : rowp[(diag + (p - R)) * kTS + o];
+    return p <= Q ? colp[(tile_index(p, Q, ns) * kSB + k) * kTS + o]
+                  : rowp[(tile_index(Q, Q + (p - Q - 1), ns) * kSB + k) * kTS + o];
   };
-  // batches of 8 independent loads in flight, then added in order
+  double s = 0.0;
   int64_t p = p0;
-  for (; p + 8 <= p1; p += 8) {
-    float x[8];
+  for (; p + 4 <= p1; p += 4) {  // independent loads in flight, added in order
+    float x[4];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) x[u] = load(p + u);
+    for (int u = 0; u < 4; ++u) x[u] = load(p + u);
 #pragma unroll
-    for (int u = 0; u < 8; ++u) s += (double)x[u];
+    for (int u = 0; u < 4; ++u) s += (double)x[u];
   }
   for (; p < p1; ++p) s += (double)load(p);
   part[sg][o] = s;
@@ -261,7 +327,7 @@ __global__ void __launch_bounds__(kTS * kSeg)
     for (int q = 0; q < kSeg; ++q) t += part[q][o];
     const double val = deg != nullptr ? t / deg[i] : t;
     const int parity = ctl != nullptr ? (ctl->iter & 1) : 0;
-    for (int p = 0; p < pt.nranks; ++p) pt.y[p][parity][i] = val;
+    for (int r = 0; r < pt.nranks; ++r) pt.y[r][parity][i] = val;
   }
   if (pt.flags[0] == nullptr) return;
   __threadfence_system();
@@ -272,7 +338,7 @@ __global__ void __launch_bounds__(kTS * kSeg)
       ctl->arrive[2] = 0u;
       __threadfence_system();
       const uint64_t epoch = ctl->sync_epoch + (uint64_t)ctl->iter + 1;
-      for (int p = 0; p < pt.nranks; ++p) st_release_sys(pt.flags[p] + pt.self, epoch);
+      for (int r = 0; r < pt.nranks; ++r) st_release_sys(pt.flags[r] + pt.self, epoch);
     }
   }
 }
@@ -330,28 +396,26 @@ void sym_prepare() {
     cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
     cudaFuncSetAttribute(sym_gemv_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
     cudaFuncSetAttribute(sym_gemv_kernel<__half>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
-    if (const char* e = getenv("GPIC_SYM_SPLIT")) {
-      const int v = atoi(e);
-      if (v == 1 || v == 2 || v == 4 || v == 8 || v == 16) g_split = v;
-    }
-    if (const char* e = getenv("GPIC_SYM_POL")) g_pol = atoi(e) != 0;
-    if (const char* e = getenv("GPIC_SYM_ABLATE")) g_ablate = atoi(e);
   }
 }
 
+// GEMV partial records (super-block rows / columns) or the affinity
+// epilogue's per-tile degree partials, whichever is larger
 int64_t sym_partial_floats(int64_t n) {
   const int64_t nt = ceil_div(n, kTS);
-  return nt * (nt + 1) / 2 * kTS;
+  const int64_t ns = ceil_div(nt, kSB);
+  const int64_t tiles = nt * (nt + 1) / 2, recs = ns * (ns + 1) / 2 * kSB;
+  return (tiles > recs ? tiles : recs) * kTS;
 }
 
 void launch_sym_gemv(const float* tiles, int64_t n, const float* v32, float* rowp, float* colp,
                      const double* deg, const PeerTable& pt, gpic_ctl* ctl, cudaStream_t s) {
   sym_prepare();
   const int64_t nt = ceil_div(n, kTS);
-  const int64_t total = nt * (nt + 1) / 2;
+  const int64_t ns = (nt + kSB - 1) / kSB;
+  const int64_t total = ns * (ns + 1) / 2;  // super-blocks
   const int grid = (int)(total < g_sms ? total : g_sms);
-  sym_gemv_kernel<float><<<grid, kThreads, kSmem, s>>>(tiles, nt, v32, rowp, colp, ctl, g_split,
-                                                           g_pol, g_ablate);
+  sym_gemv_kernel<float><<<grid, kThreads, kSmem, s>>>(tiles, nt, v32, rowp, colp, ctl);
   sym_reduce_kernel<<<(unsigned)nt, kTS * kSeg, 0, s>>>(rowp, colp, n, nt, deg, pt, ctl);
   count_launch(2);
 }
@@ -360,11 +424,11 @@ void launch_sym_gemv16(const void* tiles, int64_t n, const float* v32, float* ro
                        const double* deg, const PeerTable& pt, gpic_ctl* ctl, cudaStream_t s) {
   sym_prepare();
   const int64_t nt = ceil_div(n, kTS);
-  const int64_t total = nt * (nt + 1) / 2;
+  const int64_t ns = (nt + kSB - 1) / kSB;
+  const int64_t total = ns * (ns + 1) / 2;  // super-blocks
   const int grid = (int)(total < g_sms ? total : g_sms);
   sym_gemv_kernel<__half><<<grid, kThreads, kSmem, s>>>(static_cast<const __half*>(tiles), nt, v32,
-                                                            rowp, colp, ctl, g_split, g_pol,
-                                                            g_ablate);
+                                                            rowp, colp, ctl);
   sym_reduce_kernel<<<(unsigned)nt, kTS * kSeg, 0, s>>>(rowp, colp, n, nt, deg, pt, ctl);
   count_launch(2);
 }

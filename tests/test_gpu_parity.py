@@ -382,7 +382,7 @@ def test_sym_matvec_against_numpy():
         v = rng.uniform(0, 1, n)
         v32 = torch.zeros(int(L.gpic_vector_pitch(n)), dtype=torch.float32, device=dev)
         v32[:n] = torch.from_numpy(v.astype(np.float32)).to(dev)
-        rowp = torch.empty(len(tiles) * 128, dtype=torch.float32, device=dev)
+        rowp = torch.empty(int(L.gpic_sym_partial_floats(n)), dtype=torch.float32, device=dev)
         colp = torch.empty_like(rowp)
         y = torch.empty(n, dtype=torch.float64, device=dev)
         rc = L.gpic_sym_matvec(C.c_void_p(t_dev.data_ptr()), n, C.c_void_p(v32.data_ptr()),
@@ -521,7 +521,7 @@ def test_sym_matvec16_against_numpy():
         v = rng.uniform(0, 1, n)
         v32 = torch.zeros(int(L.gpic_vector_pitch(n)), dtype=torch.float32, device=dev)
         v32[:n] = torch.from_numpy(v.astype(np.float32)).to(dev)
-        rowp = torch.empty(len(tiles) * 128, dtype=torch.float32, device=dev)
+        rowp = torch.empty(int(L.gpic_sym_partial_floats(n)), dtype=torch.float32, device=dev)
         colp = torch.empty_like(rowp)
         y = torch.empty(n, dtype=torch.float64, device=dev)
         rc = L.gpic_sym_matvec16(C.c_void_p(t_dev.data_ptr()), n, C.c_void_p(v32.data_ptr()),
