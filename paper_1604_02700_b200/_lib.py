@@ -7,11 +7,13 @@ missing, every entry point raises instead of computing anything.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import pathlib
 
 from . import errors
 
-LIB_PATH = pathlib.Path(__file__).resolve().parent / "libgpic.so"
+LIB_PATH = pathlib.Path(os.environ.get("GPIC_LIB") or  # experiments: an alternative build
+                        pathlib.Path(__file__).resolve().parent / "libgpic.so")
 
 GPIC_OK = 0
 GPIC_E_INVALID = 1

@@ -62,7 +62,29 @@ constexpr int kBN = 128;           // columns per tile (one MMA N)
 constexpr int kKBlk = 64;          // fp16 per 128-byte swizzle row
 constexpr int kTileBytes = 128 * kKBlk * 2;  // 16 KB: 128 rows x 64 fp16
 constexpr int kEpiWarps = 16;      // 4 per SM sub-partition: latency hiding for the epilogue
-constexpr int kThreads = 64 + kEpiWarps * 32;
+// warpgroup 0: TMA producer (warp 0), MMA issuer (warp 1), two idle warps;
+// warpgroups 1-4: epilogue. setmaxnreg moves registers from warpgroup 0
+// (kCtlRegs) to the epilogue (kEpiRegs, room for the next chunk's TMEM load
+// in flight). Launch: 96 per thread; an increase is served only from what
+// warpgroup 0 releases (measured, scripts/probe/smr.cu: 56 -> 104 runs,
+// 88 -> 104 waits forever), so 128 (96 - kCtlRegs) >= 512 (kEpiRegs - 96).
+constexpr int kThreads = 128 + kEpiWarps * 32;  // with the register split (matrix-free)
+constexpr int kCtlRegs = 64;
+constexpr int kEpiRegs = 104;
+static_assert(128 * (96 - kCtlRegs) >= kEpiWarps * 32 * (kEpiRegs - 96),
+              "setmaxnreg.inc would wait for registers nobody releases");
+// Matrix-free (compute-bound): registers rebalanced and the next chunk's
+// TMEM load overlapped with this chunk's work (config 5 pass 273 -> 244 ms).
+// Store modes keep 96 each and one chunk in flight (measured faster: the
+// producer / MMA code spills at 64 registers and the stores bound them).
+template <int MODE>
+constexpr bool kSplitRegs = MODE == kModeMatvec;
+// first epilogue warp: 4 with the split (warpgroup 0 = producer, MMA, two
+// idle warps), else 2 (producer, MMA); CTA size follows
+template <int MODE>
+constexpr int kEpiBase = kSplitRegs<MODE> ? 4 : 2;
+template <int MODE>
+constexpr int kCtaThreads = 32 * kEpiBase<MODE> + kEpiWarps * 32;
 constexpr int kSmemBudget = 232448 - 1024 - 256;  // 227 KB opt-in minus alignment + barriers
 constexpr int kChunkTiles = 32;              // matvec: column tiles per work item
 
@@ -255,7 +277,7 @@ __host__ __device__ inline int64_t total_units(const TcArgs& a) {
 }
 
 template <int KB, int MODE, int KIND>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kCtaThreads<MODE>, 1)
     affinity_tc_kernel(const __grid_constant__ CUtensorMap map_hi,
                        const __grid_constant__ CUtensorMap map_lo,
                        const __grid_constant__ CUtensorMap map_out,
@@ -318,7 +340,22 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // every role ends here (no code after the role branches: the warpgroups
+  // run with different register budgets after setmaxnreg)
+  auto teardown = [&]() {
+    tc_fence_before();
+    asm volatile("bar.sync 15, %0;" ::"n"(kCtaThreads<MODE>) : "memory");
+    if (warp == 1) {
+      tc_fence_after();
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                   "r"(kTmemCols)
+                   : "memory");
+    }
+  };
 
+  if (warp < kEpiBase<MODE>) {
+  // warpgroup 0 gives registers back in one instruction all its warps share
+  if constexpr (kSplitRegs<MODE>) setmaxnreg_dec<kCtlRegs>();
   if (warp == 0) {
     // ------------------------------------------------------ TMA producer
     if (lane == 0) {
@@ -419,8 +456,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (!c.valid() || c.rb != rb) tc_commit(a_empty);  // last tile of this row block
       }
     }
+  }  // split mode: warps 2-3 are idle, they only complete warpgroup 0
+  teardown();
   } else {
     // --------------------------------------------------------- epilogue
+    if constexpr (kSplitRegs<MODE>) setmaxnreg_inc<kEpiRegs>();
     // Warp w may only read TMEM lanes 32*(w%4)..+31: q = w & 3 picks this
     // warp's 32 rows; the 4 warps of a quadrant (h = e >> 2) split the
     // tile's MB x 4 chunks of 32 columns, MB chunks each. The GW = 4 / MB
@@ -437,7 +477,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // slower: one L1 wavefront per row segment).
     constexpr int UPW = MB;
     constexpr int GW = 4 / MB;
-    const int e = warp - 2;
+    const int e = warp - kEpiBase<MODE>;
     const int q = warp & 3;
     const int h = e >> 2;
     const int m = (h * UPW) >> 2;
@@ -522,10 +562,24 @@ __global__ void __launch_bounds__(kThreads, 1)
       tf_bits ^= 1u << buf;
       tc_fence_after();
       float rsum[4] = {0.f, 0.f, 0.f, 0.f};  // this thread's 4 rows, its 8 columns per chunk
-#pragma unroll 1
-      for (int cc = 0; cc < UPW; ++cc) {
+      // chunk cc's 32 values per thread, [hf][block b][4]: (row tq, c),
+      // (row tq, c+1), (row tq+8, c), (row tq+8, c+1); the next chunk's
+      // TMEM load is in flight while this one is processed
+      uint32_t rbuf[2][32];
+      auto tmem_chunk = [&](int cc, uint32_t* r) {
+        const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) +
+                               (uint32_t)((buf * MB + m) * kBN + (c_lo + cc) * 32);
+        tmem_ld16x256_x4(taddr, r);
+        tmem_ld16x256_x4(taddr + (16u << 16), r + 16);
+      };
+      auto tmem_done = [&]() {  // accumulator fully read: hand it back to the MMA warp
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&t_empty[buf]);
+      };
+      // one 32-column chunk of this warp's rows: exp, masks, sums, stores
+      auto process_chunk = [&](const int cc, const uint32_t* r) {
         const int ch = c_lo + cc;
-        uint32_t r[32];  // [hf][block b][4]: (row tq, c), (row tq, c+1), (row tq+8, c), (row tq+8, c+1)
         const int col0 = cb * kBN + ch * 32;
         // matvec: this thread's 8 columns' v_j from the staged copy
         float vcol[8];
@@ -536,16 +590,6 @@ __global__ void __launch_bounds__(kThreads, 1)
             vcol[2 * b2] = v2.x;
             vcol[2 * b2 + 1] = v2.y;
           }
-        }
-        const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) +
-                               (uint32_t)((buf * MB + m) * kBN + ch * 32);
-        tmem_ld16x256_x4(taddr, r);
-        tmem_ld16x256_x4(taddr + (16u << 16), r + 16);
-        tmem_wait_ld();
-        if (cc == UPW - 1) {  // accumulator fully read: hand it back to the MMA warp
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&t_empty[buf]);
         }
         const bool diag = (col0 < row_lo32 + lr0 + 32) && (row_lo32 + lr0 < col0 + 32);
         const bool pad = col0 + 32 > n32 || row_lo32 + lr0 + 32 > n32;
@@ -699,6 +743,28 @@ __global__ void __launch_bounds__(kThreads, 1)
             args.degcol[(tile_index(tI, cb, args.n_ctiles) * 4 + q) * 128 + ch * 32 + col] = cs[0];
           }
         }
+      };
+      if constexpr (kSplitRegs<MODE>) {
+        tmem_chunk(0, rbuf[0]);
+        tmem_wait_ld(rbuf[0]);
+        if (UPW == 1) tmem_done();
+#pragma unroll
+        for (int cc = 0; cc < UPW; ++cc) {
+          if (cc + 1 < UPW) tmem_chunk(cc + 1, rbuf[(cc + 1) & 1]);
+          process_chunk(cc, rbuf[cc & 1]);
+          if (cc + 1 < UPW) {
+            tmem_wait_ld(rbuf[(cc + 1) & 1]);
+            if (cc + 1 == UPW - 1) tmem_done();
+          }
+        }
+      } else {
+#pragma unroll 1
+        for (int cc = 0; cc < UPW; ++cc) {
+          tmem_chunk(cc, rbuf[0]);
+          tmem_wait_ld(rbuf[0]);
+          if (cc == UPW - 1) tmem_done();
+          process_chunk(cc, rbuf[0]);
+        }
       }
       // this thread's row partials -> the quad's row totals (xor 1, 2)
 #pragma unroll
@@ -799,15 +865,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     if (MODE != kModeMatvec && lane == 0) tma_store_wait_all();
     __syncwarp();
-  }
-
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 1) {
-    tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
-                 "r"(kTmemCols)
-                 : "memory");
+    teardown();
   }
 }
 
@@ -874,10 +932,10 @@ int launch_kb(const CUtensorMap& mh, const CUtensorMap& ml, const CUtensorMap& m
   // the similarity kind is a template parameter: a runtime select would
   // evaluate both epilogues per element
   if (a.kind == GPIC_KIND_COSINE)
-    affinity_tc_kernel<KB, MODE, GPIC_KIND_COSINE><<<grid, kThreads, smem_bytes(KB, MODE), s>>>(
+    affinity_tc_kernel<KB, MODE, GPIC_KIND_COSINE><<<grid, kCtaThreads<MODE>, smem_bytes(KB, MODE), s>>>(
         mh, ml, mo, mn, a);
   else
-    affinity_tc_kernel<KB, MODE, GPIC_KIND_RBF><<<grid, kThreads, smem_bytes(KB, MODE), s>>>(
+    affinity_tc_kernel<KB, MODE, GPIC_KIND_RBF><<<grid, kCtaThreads<MODE>, smem_bytes(KB, MODE), s>>>(
         mh, ml, mo, mn, a);
   count_launch();
   GPIC_CUDA_TRY(cudaGetLastError());
