@@ -377,7 +377,6 @@ __global__ void __launch_bounds__(kTS * kSeg)
 }
 
 int g_sms = 0;
-int g_ablate = 0;  // GEMV copy shape (GPIC_SYM_SPLIT pieces per tile, GPIC_SYM_POL)
 
 }  // namespace
 
