@@ -147,6 +147,7 @@ struct TcArgs {
   int strided;          // dense / packed: row-block-strided work order (see Cursor)
   int64_t n_pad;        // rows per operand plane (the norm block's plane stride)
   int sym;              // matvec: upper-triangle tiles only, column partials -> colpart
+  int store_hint;       // store modes: L2 evict-first hint on the output stream
   float* colpart;       // matvec sym: [packed (row block, column tile)][128] fp32
 };
 
@@ -705,8 +706,11 @@ __global__ void __launch_bounds__(kCtaThreads<MODE>, 1)
             const int64_t out_row0 = is_packed(MODE)
                                          ? tile_index(tI, cb, args.n_ctiles) * 128 + q * 32
                                          : lr0;
-            tma_store_2d(&map_out, is_packed(MODE) ? ch * 32 : (int)col0, (int)out_row0, stage,
-                         stream_pol);
+            if (args.store_hint)
+              tma_store_2d(&map_out, is_packed(MODE) ? ch * 32 : (int)col0, (int)out_row0, stage,
+                           stream_pol);
+            else
+              tma_store_2d(&map_out, is_packed(MODE) ? ch * 32 : (int)col0, (int)out_row0, stage);
           }
           ++stores;
           if (is_packed(MODE) && store_ok && tI != cb) {
@@ -923,9 +927,19 @@ int launch_kb(const CUtensorMap& mh, const CUtensorMap& ml, const CUtensorMap& m
     GPIC_CUDA_TRY(cudaGetDevice(&dev));
     GPIC_CUDA_TRY(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev));
   }
-  // operands beyond ~L2/4 (the store stream needs the rest): strided order
-  a.strided = (int64_t)row_pad(a.n) * kKBlk * KB * 4 > (32ll << 20);
+  // strided order once there is at least one full wave of row blocks: the
+  // CTAs of a wave stream the same B tiles together, so operand tiles come
+  // from L2 instead of DRAM even next to a GB-scale output stream (config 3
+  // packed: 745 -> 54 MB of DRAM reads, 4.01 -> 3.55 ms); small problems
+  // keep the contiguous split, which uses every SM. The fp16 store mode is
+  // epilogue-bound rather than store-bound and prefers the contiguous split's
+  // balance (3.1 vs 3.4 ms) while its operands fit in ~L2/4.
+  a.strided = MODE == kModePacked16
+                  ? (int64_t)row_pad(a.n) * kKBlk * KB * 4 > (32ll << 20)
+                  : a.n_rtiles >= g_num_sms;
   if (const char* o = getenv("GPIC_TC_ORDER")) a.strided = atoi(o) != 0;  // tests: force an order
+  a.store_hint = 1;
+  if (const char* o = getenv("GPIC_TC_STORE_HINT")) a.store_hint = atoi(o) != 0;  // measurement
   const int64_t total = (MODE == kModeMatvec || a.strided) ? a.n_rtiles : total_units<MB, MODE>(a);
   const int grid = (int)(total < g_num_sms ? total : g_num_sms);
   if (grid < 1) return GPIC_OK;
