@@ -354,15 +354,36 @@ __global__ void __launch_bounds__(kTS * kSeg)
   const int o = threadIdx.x % kTS, sg = threadIdx.x / kTS;
   const int64_t p0 = nt * sg / kSeg, p1 = nt * (sg + 1) / kSeg;
   double s = 0.0;
-  for (int64_t p = p0; p < p1; ++p) {
+  // 4 tiles' partials in flight per step, then added in order
+  auto load4 = [&](int64_t p, float (&x)[4]) {
     if (p < R) {
       const float* c = degcol + tile_index(p, R, nt) * 4 * kTS + o;
-      s += (double)c[0] + (double)c[kTS] + (double)c[2 * kTS] + (double)c[3 * kTS];
+      x[0] = c[0]; x[1] = c[kTS]; x[2] = c[2 * kTS]; x[3] = c[3 * kTS];
     } else {
       const float* r = degrow + tile_index(R, p, nt) * nhalf * kTS + o;
-      s += (double)r[0];
-      if (nhalf == 2) s += (double)r[kTS];
+      x[0] = r[0]; x[1] = nhalf == 2 ? r[kTS] : 0.f; x[2] = x[3] = 0.f;
     }
+  };
+  auto add4 = [&](int64_t p, const float (&x)[4]) {
+    if (p < R) {
+      s += (double)x[0] + (double)x[1] + (double)x[2] + (double)x[3];
+    } else {
+      s += (double)x[0];
+      if (nhalf == 2) s += (double)x[1];
+    }
+  };
+  int64_t p = p0;
+  for (; p + 4 <= p1; p += 4) {
+    float x[4][4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) load4(p + u, x[u]);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) add4(p + u, x[u]);
+  }
+  for (; p < p1; ++p) {
+    float x[4];
+    load4(p, x);
+    add4(p, x);
   }
   part[sg][o] = s;
   __syncthreads();
