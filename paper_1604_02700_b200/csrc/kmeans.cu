@@ -247,8 +247,19 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int64_t chunk = (n + kThreads - 1) / kThreads;
   const int64_t lo = min(n, (int64_t)tid * chunk), hi = min(n, lo + chunk);
   for (int j = 1; j < k; ++j) {
+    // sequential sum of the thread's chunk, 8 loads in flight (same order)
     double part = 0.0;
-    for (int64_t i = lo; i < hi; ++i) part += s.dist2[i];
+    {
+      int64_t i = lo;
+      for (; i + 8 <= hi; i += 8) {
+        double x[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) x[u] = s.dist2[i + u];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) part += x[u];
+      }
+      for (; i < hi; ++i) part += s.dist2[i];
+    }
     sh.scan[tid] = part;
     __syncthreads();
     // inclusive Hillis-Steele scan of the chunk totals (fixed pattern)
@@ -270,9 +281,21 @@ __global__ void __launch_bounds__(kThreads, 1)
     double run = tid ? sh.scan[tid - 1] : 0.0;
     long long found = n;
     if (run + part > r || tid == kThreads - 1) {
-      for (int64_t i = lo; i < hi; ++i) {
+      int64_t i = lo;
+      for (; i + 8 <= hi && found == n; i += 8) {
+        double x[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) x[u] = s.dist2[i + u];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          if (found != n) break;
+          run += x[u];
+          if (run > r) found = i + u;
+        }
+      }
+      for (; i < hi && found == n; ++i) {
         run += s.dist2[i];
-        if (run > r) { found = i; break; }
+        if (run > r) found = i;
       }
     }
     long long pick = block_min_i(found, sh);
@@ -453,7 +476,22 @@ __global__ void __launch_bounds__(kThreads, 1)
   for (int j = 0; j < k; ++j) {
     double mn = __longlong_as_double(0x7ff0000000000000ll), mx = -mn;
     long long mni = LLONG_MAX, mxi = -1;
-    for (int64_t i = tid; i < n; i += kThreads) {
+    // 4 strided elements per step: labels loaded together, then values
+    int64_t i = tid;
+    for (; i + 3 * kThreads < n; i += 4 * kThreads) {
+      int lb[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) lb[u] = s.lab[i + u * kThreads];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (lb[u] != j) continue;
+        const int64_t ii = i + u * kThreads;
+        const double x = v[ii];
+        if (x < mn || (x == mn && ii < mni)) { mn = x; mni = ii; }
+        if (x > mx || (x == mx && ii > mxi)) { mx = x; mxi = ii; }
+      }
+    }
+    for (; i < n; i += kThreads) {
       if (s.lab[i] != j) continue;
       const double x = v[i];
       if (x < mn || (x == mn && i < mni)) { mn = x; mni = i; }
