@@ -20,7 +20,10 @@
 // are always contiguous (1-D Voronoi cells are intervals), so the device
 // path reports GPIC_E_UNSUPPORTED instead of silently diverging if that
 // invariant is ever violated.
+#include <cooperative_groups.h>
+
 #include <cfloat>
+#include <cstdlib>
 #include <cstdint>
 
 #include "common.cuh"
@@ -34,6 +37,8 @@ constexpr int kThreads = 1024;
 constexpr int kWarps = kThreads / 32;
 constexpr int kMaxK = 64;
 constexpr int kPolishLimit = 4096;  // kmeans.py:22 POLISH_LIMIT
+constexpr int64_t kGridMin = 32768;  // single problems this large run on the whole GPU
+constexpr int kGridMaxCtas = 256;
 
 struct KScratch {
   int32_t* lab;     // n   Lloyd labels
@@ -44,6 +49,7 @@ struct KScratch {
   double* best;     // m + 1
   int32_t* split;   // (kcap + 1) x split_ld, split_ld = m + 1
   double* stats;    // small: [0] = wcss(lloyd), [1] = wcss(dp)
+  double* gpart;    // grid path: per-CTA partials [kGridMaxCtas][kMaxK][4] (8-byte words)
   int64_t split_ld;
 };
 
@@ -61,10 +67,18 @@ __host__ __device__ inline int64_t al(int64_t b) { return (b + 255) & ~int64_t(2
 
 __host__ __device__ inline int64_t polish_len(int64_t n) { return n < kPolishLimit ? n : kPolishLimit; }
 
+// grid path scratch (8-byte words): seeding chunk totals + the draw's index,
+// empty-cluster candidates, and two alternating per-CTA record buffers
+// [CTA][cluster][4] (alternation makes one barrier per pass enough)
+constexpr int64_t kGSeed = 0, kGPick = kGridMaxCtas, kGRepair = kGridMaxCtas + 8,
+                  kGRec = kGRepair + 2 * kGridMaxCtas, kGRecWords = (int64_t)kGridMaxCtas * kMaxK * 4;
+__host__ __device__ constexpr int64_t grid_words() { return kGRec + 2 * kGRecWords; }
+
 __host__ __device__ inline int64_t scratch_size(int64_t n, int kcap) {
   const int64_t m = polish_len(n);
   return al(n * 4) * 2 + al(n * 8) + al(kMaxK * 8) + al(m * 4) + al((m + 1) * 8) +
-         al((int64_t)(kcap + 1) * (m + 1) * 4) + al(64 * 8);
+         al((int64_t)(kcap + 1) * (m + 1) * 4) + al(64 * 8) +
+         (n >= kGridMin ? al(grid_words() * 8) : 0);
 }
 
 __host__ __device__ inline KScratch carve_k(void* base, int64_t n, int kcap) {
@@ -79,6 +93,7 @@ __host__ __device__ inline KScratch carve_k(void* base, int64_t n, int kcap) {
   s.best = reinterpret_cast<double*>(p); p += al((m + 1) * 8);
   s.split = reinterpret_cast<int32_t*>(p); p += al((int64_t)(kcap + 1) * (m + 1) * 4);
   s.stats = reinterpret_cast<double*>(p); p += al(64 * 8);
+  s.gpart = n >= kGridMin ? reinterpret_cast<double*>(p) : nullptr;
   s.split_ld = m + 1;
   return s;
 }
@@ -563,6 +578,289 @@ __global__ void __launch_bounds__(kThreads, 1)
   for (int64_t i = tid; i < n; i += kThreads) out[i] = remap[s.lab[i]];
 }
 
+// ------------------------------------------------ whole-GPU path (n large)
+// The same algorithm as lloyd_kernel + finish_kernel, one cooperative grid
+// (one 1024-thread CTA per SM): a single SM streaming v from L2 is what
+// bounded the one-CTA kernels (~0.85 ms at n = 100k). CTA b owns the
+// contiguous range [n b / G, n (b+1) / G); every cross-CTA reduction writes
+// per-CTA partials and is combined in CTA order by every CTA identically
+// after a grid barrier, so the result is deterministic for a given grid.
+// Lloyd's assignment and the next round's statistics share one pass.
+// Cross-CTA values are read with ld.global.cg (L2): the SMs' L1 caches are
+// not coherent, and a barrier does not invalidate lines read earlier.
+namespace cg = cooperative_groups;
+
+__global__ void __launch_bounds__(kThreads, 1)
+    kmeans_grid_kernel(KProblem P, int k, int max_rounds, double tol) {
+  cg::grid_group grid = cg::this_grid();
+  if (P.ctl->status != GPIC_OK) return;  // uniform across the grid
+  const double* __restrict__ v = P.v;
+  const int64_t n = P.n;
+  const KScratch s = P.s;
+  const int G = gridDim.x, b = blockIdx.x, tid = threadIdx.x;
+  const int w = tid >> 5, l = tid & 31;
+  const int64_t blo = n * b / G, bhi = n * (b + 1) / G;
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  Shared& sh = *reinterpret_cast<Shared*>(smem_raw);
+  __shared__ double sums[kMaxK];
+  __shared__ int64_t cnts[kMaxK];
+  __shared__ double sb_tot, sb_r;
+  __shared__ int sb_star;
+  double* gp = s.gpart;  // [G][kMaxK][4]
+  long long* gpi = reinterpret_cast<long long*>(s.gpart);
+
+  // ---- k-means++ seeding (kmeans.py:39-55)
+  if (tid == 0) sh.centers[0] = v[P.first];
+  __syncthreads();
+  for (int64_t i = blo + tid; i < bhi; i += kThreads) {
+    const double d = v[i] - sh.centers[0];
+    s.dist2[i] = d * d;
+  }
+  __syncthreads();
+  const int64_t chunk = (bhi - blo + kThreads - 1) / kThreads;
+  const int64_t lo = min(bhi, blo + (int64_t)tid * chunk), hi = min(bhi, lo + chunk);
+  for (int j = 1; j < k; ++j) {
+    double part = 0.0;
+    for (int64_t i = lo; i < hi; ++i) part += s.dist2[i];
+    sh.scan[tid] = part;
+    __syncthreads();
+    for (int off = 1; off < kThreads; off <<= 1) {
+      const double add = tid >= off ? sh.scan[tid - off] : 0.0;
+      __syncthreads();
+      sh.scan[tid] += add;
+      __syncthreads();
+    }
+    if (tid == 0) gp[kGSeed + b] = sh.scan[kThreads - 1];
+    grid.sync();
+    if (tid == 0) {
+      // CTA prefix in order; the CTA holding the draw (last CTA if rounding
+      // puts r past the end)
+      double tot = 0.0;
+      for (int q = 0; q < G; ++q) tot += __ldcg(gp + kGSeed + q);
+      sb_tot = tot;
+      const double r = s.unif[j - 1] * tot;
+      double run = 0.0;
+      int star = G - 1;
+      for (int q = 0; q < G; ++q) {
+        if (run + __ldcg(gp + kGSeed + q) > r) { star = q; break; }
+        run += __ldcg(gp + kGSeed + q);
+      }
+      sb_star = star;
+      sb_r = r - run;  // the draw relative to the start of CTA `star`
+    }
+    __syncthreads();
+    if (!(sb_tot > 0.0)) {  // all mass on existing centres: duplicate the first
+      if (tid == 0)
+        for (int q = j; q < k; ++q) sh.centers[q] = sh.centers[0];
+      __syncthreads();
+      break;
+    }
+    if (b == sb_star) {
+      const double r = sb_r;
+      double run = tid ? sh.scan[tid - 1] : 0.0;
+      long long found = n;
+      if (run + part > r || tid == kThreads - 1) {
+        for (int64_t i = lo; i < hi; ++i) {
+          run += s.dist2[i];
+          if (run > r) { found = i; break; }
+        }
+      }
+      long long pick = block_min_i(found, sh);
+      if (pick > bhi - 1) pick = bhi - 1;
+      if (tid == 0) gpi[kGPick] = pick;
+    }
+    grid.sync();
+    if (tid == 0) sh.centers[j] = v[__ldcg(gpi + kGPick)];
+    __syncthreads();
+    const double cj = sh.centers[j];
+    for (int64_t i = blo + tid; i < bhi; i += kThreads) {
+      const double d = v[i] - cj;
+      s.dist2[i] = fmin(s.dist2[i], d * d);
+    }
+    __syncthreads();
+  }
+
+  // ---- assignment + statistics of the new assignment, one pass
+  int ph = 0;  // record buffer of the next pass
+  auto rec = [&](int buf, int q, int j, int slot) { return kGRec + buf * kGRecWords + (q * kMaxK + j) * 4 + slot; };
+  auto assign_stats = [&]() {
+    double ls[kMaxK];
+    int lc[kMaxK];
+    for (int j = 0; j < k; ++j) { ls[j] = 0.0; lc[j] = 0; }
+    for (int64_t i = blo + tid; i < bhi; i += kThreads) {
+      const double x = v[i];
+      const int j = nearest(x, sh.centers, k);
+      s.lab[i] = j;
+      ls[j] += x;
+      lc[j] += 1;
+    }
+    for (int j = 0; j < k; ++j) {
+      const double sm = warp_sum_f64(ls[j]);
+      int c = lc[j];
+      for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+      if (l == 0) { sh.wsum[w][j] = sm; sh.wcnt[w][j] = c; }
+    }
+    __syncthreads();
+    if (tid < k) {
+      double sm = 0.0;
+      long long c = 0;
+      for (int q = 0; q < kWarps; ++q) { sm += sh.wsum[q][tid]; c += sh.wcnt[q][tid]; }
+      gp[rec(ph, b, tid, 0)] = sm;
+      gpi[rec(ph, b, tid, 1)] = c;
+    }
+    grid.sync();
+    if (tid < k) {
+      double sm = 0.0;
+      int64_t c = 0;
+      for (int q = 0; q < G; ++q) { sm += __ldcg(gp + rec(ph, q, tid, 0)); c += __ldcg(gpi + rec(ph, q, tid, 1)); }
+      sums[tid] = sm;
+      cnts[tid] = c;
+    }
+    ph ^= 1;
+    __syncthreads();
+  };
+
+  // ---- Lloyd rounds (kmeans.py:75-94)
+  assign_stats();
+  for (int round = 0; round < max_rounds; ++round) {
+    for (int j = 0; j < k; ++j) {
+      if (cnts[j] != 0) continue;
+      // empty cluster: reseed at the point farthest from its centre (first
+      // index on ties), reassign, refresh the statistics
+      double bv = -1.0;
+      long long bi = n;
+      for (int64_t i = blo + tid; i < bhi; i += kThreads) {
+        const double d = fabs(v[i] - sh.centers[s.lab[i]]);
+        if (d > bv) { bv = d; bi = i; }
+      }
+      const long long far = block_argmax(bv, bi, sh);
+      if (tid == 0) {  // this CTA's candidate (value, index)
+        gp[kGRepair + 2 * b] = far < bhi ? fabs(v[far] - sh.centers[s.lab[far]]) : -1.0;
+        gpi[kGRepair + 2 * b + 1] = far;
+      }
+      grid.sync();
+      if (tid == 0) {
+        double best = -2.0;
+        long long bidx = n;
+        for (int q = 0; q < G; ++q) {
+          const double d = __ldcg(gp + kGRepair + 2 * q);
+          const long long ix = __ldcg(gpi + kGRepair + 2 * q + 1);
+          if (d > best || (d == best && ix < bidx)) { best = d; bidx = ix; }
+        }
+        sh.centers[j] = v[bidx];
+      }
+      grid.sync();  // every CTA has read the candidates before they are reused
+      assign_stats();
+    }
+    if (tid == 0) {
+      double moved = 0.0;
+      for (int j = 0; j < k; ++j) {
+        if (cnts[j]) {
+          const double c = sums[j] / (double)cnts[j];
+          moved = fmax(moved, fabs(c - sh.centers[j]));
+          sh.centers[j] = c;
+        }
+      }
+      sh.flag = moved < tol;
+    }
+    __syncthreads();
+    const int done = sh.flag;
+    __syncthreads();
+    assign_stats();
+    if (done) break;
+  }
+
+  // ---- canonical labels (finish_kernel): cluster extents, contiguity, relabel
+  for (int j = 0; j < k; ++j) {
+    double mn = __longlong_as_double(0x7ff0000000000000ll), mx = -mn;
+    long long mni = LLONG_MAX, mxi = -1;
+    for (int64_t i = blo + tid; i < bhi; i += kThreads) {
+      if (s.lab[i] != j) continue;
+      const double x = v[i];
+      if (x < mn || (x == mn && i < mni)) { mn = x; mni = i; }
+      if (x > mx || (x == mx && i > mxi)) { mx = x; mxi = i; }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      const double a = __shfl_xor_sync(0xffffffffu, mn, o);
+      const long long ai = __shfl_xor_sync(0xffffffffu, mni, o);
+      if (a < mn || (a == mn && ai < mni)) { mn = a; mni = ai; }
+      const double c = __shfl_xor_sync(0xffffffffu, mx, o);
+      const long long ci = __shfl_xor_sync(0xffffffffu, mxi, o);
+      if (c > mx || (c == mx && ci > mxi)) { mx = c; mxi = ci; }
+    }
+    __shared__ double s_mn[kWarps], s_mx[kWarps];
+    __shared__ long long s_mni[kWarps], s_mxi[kWarps];
+    if (l == 0) { s_mn[w] = mn; s_mni[w] = mni; s_mx[w] = mx; s_mxi[w] = mxi; }
+    __syncthreads();
+    if (tid == 0) {
+      for (int q = 1; q < kWarps; ++q) {
+        if (s_mn[q] < mn || (s_mn[q] == mn && s_mni[q] < mni)) { mn = s_mn[q]; mni = s_mni[q]; }
+        if (s_mx[q] > mx || (s_mx[q] == mx && s_mxi[q] > mxi)) { mx = s_mx[q]; mxi = s_mxi[q]; }
+      }
+      gp[rec(ph, b, j, 0)] = mn;  // the buffer the last pass did not use
+      gpi[rec(ph, b, j, 1)] = mni;
+      gp[rec(ph, b, j, 2)] = mx;
+      gpi[rec(ph, b, j, 3)] = mxi;
+    }
+    __syncthreads();
+  }
+  grid.sync();
+  __shared__ int remap[kMaxK];
+  __shared__ double lo_v[kMaxK], hi_v[kMaxK];
+  __shared__ long long lo_i[kMaxK], hi_i[kMaxK];
+  if (tid < k) {  // cluster tid's extent over the CTAs' records
+    const int j = tid;
+    double mn = __longlong_as_double(0x7ff0000000000000ll), mx = -mn;
+    long long mni = LLONG_MAX, mxi = -1;
+    for (int q = 0; q < G; ++q) {
+      const double a = __ldcg(gp + rec(ph, q, j, 0)), c = __ldcg(gp + rec(ph, q, j, 2));
+      const long long ai = __ldcg(gpi + rec(ph, q, j, 1)), ci = __ldcg(gpi + rec(ph, q, j, 3));
+      if (a < mn || (a == mn && ai < mni)) { mn = a; mni = ai; }
+      if (c > mx || (c == mx && ci > mxi)) { mx = c; mxi = ci; }
+    }
+    lo_v[j] = mn; lo_i[j] = mni; hi_v[j] = mx; hi_i[j] = mxi;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    int ids[kMaxK];
+    double cen[kMaxK];
+    int m = 0;
+    for (int j = 0; j < k; ++j)
+      if (cnts[j]) { ids[m] = j; cen[m] = sums[j] / (double)cnts[j]; ++m; }
+    for (int a = 1; a < m; ++a) {  // insertion sort, stable
+      const int id = ids[a];
+      const double c = cen[a];
+      int q = a - 1;
+      while (q >= 0 && cen[q] > c) { ids[q + 1] = ids[q]; cen[q + 1] = cen[q]; --q; }
+      ids[q + 1] = id;
+      cen[q + 1] = c;
+    }
+    for (int j = 0; j < k; ++j) remap[j] = 0;
+    for (int r = 0; r < m; ++r) remap[ids[r]] = r;
+    int by[kMaxK];
+    for (int r = 0; r < m; ++r) by[r] = ids[r];
+    for (int a = 1; a < m; ++a) {
+      const int id = by[a];
+      int q = a - 1;
+      while (q >= 0 && (lo_v[by[q]] > lo_v[id] || (lo_v[by[q]] == lo_v[id] && lo_i[by[q]] > lo_i[id]))) {
+        by[q + 1] = by[q];
+        --q;
+      }
+      by[q + 1] = id;
+    }
+    int ok = 1;
+    for (int r = 1; r < m; ++r) {
+      const int p = by[r - 1], q = by[r];
+      if (!(hi_v[p] < lo_v[q] || (hi_v[p] == lo_v[q] && hi_i[p] < lo_i[q]))) ok = 0;
+    }
+    if (!ok && b == 0) raise_status(P.ctl, GPIC_E_UNSUPPORTED, 0, -1, 0.0);
+  }
+  __syncthreads();
+  for (int64_t i = blo + tid; i < bhi; i += kThreads) P.out[i] = remap[s.lab[i]];
+}
+
+int g_grid_ctas = 0;
+
 int set_kmeans_attributes() {
   static bool done = false;
   if (done) return GPIC_OK;
@@ -572,6 +870,13 @@ int set_kmeans_attributes() {
   GPIC_CUDA_TRY(cudaFuncSetAttribute(choose_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, shm));
   GPIC_CUDA_TRY(cudaFuncSetAttribute(finish_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, shm));
   GPIC_CUDA_TRY(cudaFuncSetAttribute(polish_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, pshm));
+  GPIC_CUDA_TRY(cudaFuncSetAttribute(kmeans_grid_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, shm));
+  int dev = 0, sms = 0, per_sm = 0, coop = 0;
+  GPIC_CUDA_TRY(cudaGetDevice(&dev));
+  GPIC_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  GPIC_CUDA_TRY(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev));
+  GPIC_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kmeans_grid_kernel, kThreads, shm));
+  g_grid_ctas = coop && per_sm > 0 ? (sms < kGridMaxCtas ? sms : kGridMaxCtas) : 0;
   done = true;
   return GPIC_OK;
 }
@@ -615,6 +920,17 @@ int launch_kmeans1d(const double* v, int64_t n, int32_t k, int64_t first_index,
   p.ctl = ctl;
   GPIC_CUDA_TRY(cudaMemcpyAsync(p.s.unif, h_uniforms, sizeof(double) * (k - 1),
                                 cudaMemcpyHostToDevice, st));
+  if (n >= kGridMin && getenv("GPIC_KMEANS_ONE_CTA") == nullptr) {
+    int rc = set_kmeans_attributes();
+    if (rc) return rc;
+    if (g_grid_ctas > 0) {
+      void* args[] = {&p, &k, &max_rounds, &tol};
+      GPIC_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)kmeans_grid_kernel, g_grid_ctas,
+                                                kThreads, args, sizeof(Shared), st));
+      count_launch();
+      return GPIC_OK;
+    }
+  }
   return launch_stages(p, nullptr, 1, k, max_rounds, tol, n <= kPolishLimit, st);
 }
 

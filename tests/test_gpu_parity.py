@@ -181,6 +181,27 @@ def test_kmeans_random_vs_oracle():
         assert np.array_equal(got, po.kmeans_1d(v, k, trial)), f"trial {trial}"
 
 
+@pytest.mark.parametrize("n,k", [(40000, 3), (100000, 10), (150001, 50)])
+def test_kmeans_whole_gpu_path(monkeypatch, n, k):
+    """Large problems run the cooperative whole-GPU k-means: labels equal
+    the oracle's and the one-CTA kernel's, including an empty-cluster case
+    (duplicated levels) and noisy, overlapping levels."""
+    gpu = _gpu()
+    rng = np.random.default_rng(n + k)
+    for trial, (spread, noise) in enumerate([(1e-4, 1e-3), (1e-4, 2e-1), (1e-6, 0.0)]):
+        levels = np.sort(rng.uniform(1e-6, 1e-6 + spread, k))
+        v = rng.choice(levels, n) * (1 + noise * rng.standard_normal(n))
+        if noise == 0.0:
+            v[: n // 2] = levels[0]  # heavy ties: duplicate centres, empty clusters
+        monkeypatch.delenv("GPIC_KMEANS_ONE_CTA", raising=False)
+        grid = gpu.kmeans_1d(v, KMeansParams(k=k, seed=trial))
+        monkeypatch.setenv("GPIC_KMEANS_ONE_CTA", "1")
+        one = gpu.kmeans_1d(v, KMeansParams(k=k, seed=trial))
+        ref = po.kmeans_1d(v, k, trial)
+        assert np.array_equal(grid, ref), (n, k, trial)
+        assert np.array_equal(one, ref), (n, k, trial)
+
+
 def test_kernel_kats(golden):
     gpu = _gpu()
     z = golden("kernels")
