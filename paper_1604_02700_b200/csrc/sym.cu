@@ -35,7 +35,7 @@ constexpr int kStages = 3;  // fp32 tiles (64 KB); fp16 tiles (32 KB) use 2x the
 constexpr int kWarps = 8;                   // consumers; 16 rows each
 constexpr int kRowsPerWarp = kTS / kWarps;  // 16
 constexpr int kThreads = (kWarps + 1) * 32;
-constexpr int kSmem = kStages * kTileFloats * 4 + 2 * kWarps * kTS * 4 + 4 * kTS * 4 + 64 + 128;
+constexpr int kSmem = kStages * kTileFloats * 4 + 2 * kWarps * 4 * kTS * 4 + 64 + 128;
 template <typename T>
 struct TileTraits;  // element type of the stored tiles
 template <>
@@ -125,9 +125,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (ctl != nullptr && *(volatile const int32_t*)&ctl->stop) return;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* st = smem_align<128>(smem_raw);
-  float* red = reinterpret_cast<float*>(st + kStages * kTileBytes);  // [2][kWarps][128] column partials
-  float* colacc = red + 2 * kWarps * kTS;                            // [kSB][128] per super-block
-  uint64_t* full = reinterpret_cast<uint64_t*>(colacc + kSB * kTS);
+  // [2 (super-block parity)][kWarps][kSB columns][128] column products
+  float* red = reinterpret_cast<float*>(st + kStages * kTileBytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(red + 2 * kWarps * kSB * kTS);
   uint64_t* empty = full + kStages;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -172,13 +172,16 @@ __global__ void __launch_bounds__(kThreads, 1)
   int s = 0;
   uint32_t ph = 0;
   int rb = 0;
-  const int t = threadIdx.x;  // consumers: threads < 128 own one column of colacc
-  if (t < kTS)
-    for (int k = 0; k < kSB; ++k) colacc[k * kTS + t] = 0.f;
+  const int t = threadIdx.x;
   w.P = P0;
   w.Q = Q0;
   for (int64_t sb = s0; sb < s1; ++sb, w.next_sb()) {
     w.open(w.P, w.Q);
+    // per lane: the column products of the super-block's kSB tile columns,
+    // accumulated over its tile rows (one cross-warp combine per super-block)
+    float4 cpa[kSB];
+#pragma unroll
+    for (int c = 0; c < kSB; ++c) cpa[c] = make_float4(0.f, 0.f, 0.f, 0.f);
     float acc[kRowsPerWarp];
 #pragma unroll
     for (int i = 0; i < kRowsPerWarp; ++i) acc[i] = 0.f;
@@ -197,37 +200,38 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       mbar_wait(&full[s], ph);
       const uint8_t* tile = st + s * kTileBytes + warp * kRowsPerWarp * kTS * (int)sizeof(T);
-      float4 cp = make_float4(0.f, 0.f, 0.f, 0.f);
+      // row products into acc; off the diagonal, column products into the
+      // accumulator of tile column J (static index: one case per column)
+      auto tile_products = [&](float4& cp, bool col) {
 #pragma unroll
-      for (int i = 0; i < kRowsPerWarp; ++i) {
-        const float4 a = TileTraits<T>::load4(tile + i * kTS * (int)sizeof(T), lane);
-        const float vi = __shfl_sync(0xffffffffu, vi_l, i);
-        float r = fmaf(a.x, vj.x, acc[i]);
-        r = fmaf(a.y, vj.y, r);
-        r = fmaf(a.z, vj.z, r);
-        acc[i] = fmaf(a.w, vj.w, r);
-        cp.x = fmaf(a.x, vi, cp.x);
-        cp.y = fmaf(a.y, vi, cp.y);
-        cp.z = fmaf(a.z, vi, cp.z);
-        cp.w = fmaf(a.w, vi, cp.w);
+        for (int i = 0; i < kRowsPerWarp; ++i) {
+          const float4 a = TileTraits<T>::load4(tile + i * kTS * (int)sizeof(T), lane);
+          float r = fmaf(a.x, vj.x, acc[i]);
+          r = fmaf(a.y, vj.y, r);
+          r = fmaf(a.z, vj.z, r);
+          acc[i] = fmaf(a.w, vj.w, r);
+          if (col) {
+            const float vi = __shfl_sync(0xffffffffu, vi_l, i);
+            cp.x = fmaf(a.x, vi, cp.x);
+            cp.y = fmaf(a.y, vi, cp.y);
+            cp.z = fmaf(a.z, vi, cp.z);
+            cp.w = fmaf(a.w, vi, cp.w);
+          }
+        }
+      };
+      if (I == J) {
+        tile_products(cpa[0], false);
+      } else {
+        switch ((int)(J - kSB * w.Q)) {
+          case 0: tile_products(cpa[0], true); break;
+          case 1: tile_products(cpa[1], true); break;
+          case 2: tile_products(cpa[2], true); break;
+          default: tile_products(cpa[3], true); break;
+        }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
       if (++s == kStages) { s = 0; ph ^= 1; }
-      if (I != J) {
-        // column products of this tile: the 8 warps combine in order, then
-        // accumulate into the super-block's record of column tile J (I order)
-        float* rw = red + rb * kWarps * kTS;
-        reinterpret_cast<float4*>(rw + warp * kTS)[lane] = cp;
-        asm volatile("bar.sync 1, %0;" ::"n"(kWarps * 32) : "memory");
-        if (t < kTS) {
-          float c = 0.f;
-#pragma unroll
-          for (int w8 = 0; w8 < kWarps; ++w8) c += rw[w8 * kTS + t];
-          colacc[(J - kSB * w.Q) * kTS + t] += c;
-        }
-        rb ^= 1;  // double-buffered: the next tile writes the other half
-      }
       if (row_end) {
         // transpose-reduce the 16 row accumulators across the 32 lanes
         // (fixed pattern): after 4 halving steps lane l holds row f(l) over
@@ -271,13 +275,21 @@ __global__ void __launch_bounds__(kThreads, 1)
       vi_l = vi_n;
       if (!more) break;
     }
-    // the super-block's column records (thread t owns column t of every
-    // record: its own adds precede these reads in program order)
+    // the super-block's column records: the 8 warps combine in order
+    // (double-buffered by super-block, one barrier)
+    float* rw = red + rb * kWarps * kSB * kTS;
+#pragma unroll
+    for (int c = 0; c < kSB; ++c) reinterpret_cast<float4*>(rw + (warp * kSB + c) * kTS)[lane] = cpa[c];
+    asm volatile("bar.sync 1, %0;" ::"n"(kWarps * 32) : "memory");
     if (t < kTS)
-      for (int k = 0; k < kSB; ++k) {
-        colp[(sb * kSB + k) * kTS + t] = colacc[k * kTS + t];
-        colacc[k * kTS + t] = 0.f;
+#pragma unroll
+      for (int c = 0; c < kSB; ++c) {
+        float sum = 0.f;
+#pragma unroll
+        for (int w8 = 0; w8 < kWarps; ++w8) sum += rw[(w8 * kSB + c) * kTS + t];
+        colp[(sb * kSB + c) * kTS + t] = sum;
       }
+    rb ^= 1;
   }
 }
 
