@@ -454,7 +454,8 @@ def run_ours_sharded(args, cfg, rank, world):
     d = config_dataset(cfg, seed=0)
     n, m, k, sigma = d.n, d.m, c["k"], c["sigma"]
     params = PicParams(k=k)
-    config = KernelConfig(p=world, device=local, affinity_impl=args.engine, storage="dense")
+    storage = "packed" if args.storage == "packed" and args.engine == "tc" else "dense"
+    config = KernelConfig(p=world, device=local, affinity_impl=args.engine, storage=storage)
     runner = sharded.ShardedRunner(n, config)
     x = torch.from_numpy(d.points).to(dev)
     stream = torch.cuda.current_stream(dev)
@@ -502,8 +503,10 @@ def run_ours_sharded(args, cfg, rank, world):
             "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
             "dtype": "f32 (3-term fp16-split tensor Gram, fp32 accumulate; fp64 vectors/reductions)",
             "data": "synthetic (SURVEY App. B gaussian blobs, seed 0)",
-            "config": dict(workload(cfg, world), affinity_engine=args.engine, storage="dense",
-                           parallelism=f"row-shard x{world}, fused P2P y all-gather"),
+            "config": dict(workload(cfg, world), affinity_engine=args.engine, storage=storage,
+                           parallelism=(f"packed symmetric super-row shards x{world}, P2P partial-y "
+                                        "exchange summed in rank order" if storage == "packed" else
+                                        f"row-shard x{world}, fused P2P y all-gather")),
             "iterations": trace.iterations_run, "converged": trace.converged,
             "ari_vs_truth": adjusted_rand_index(contingency(d.labels, lab_np)),
             "ranks_agree_bitwise": agree,

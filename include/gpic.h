@@ -290,6 +290,25 @@ typedef struct gpic_shard {
   double* ypart;      /* gpic_mf_ypart_doubles(n, d, rows) doubles          */
 } gpic_shard;
 
+/* Packed shards (symmetric storage across ranks, GPIC_STORAGE_PACKED in
+ * gpic_shard): rank r owns the 512-row super-rows [row_lo, row_hi) returned
+ * by gpic_packed_shard_range (balanced by stored tile count) and stores the
+ * upper-triangle tiles of those rows (gpic_packed_shard_tiles x 64 KB).
+ * gpic_packed_shard_build computes them plus the shard's partial degrees
+ * (d_deg_partial: n doubles, global row index). In the gpic_shard: a = the
+ * tiles, deg = the partial degrees, row_lo / rows = the range, ypart = the
+ * build's scratch (gpic_packed_shard_scratch_bytes). Every iteration each
+ * rank sends its partial y to every rank (P2P, NVLink) and each rank sums
+ * the P partials in rank order: deterministic for a given P. */
+int gpic_packed_shard_range(int64_t n, int32_t nranks, int32_t rank, int64_t* row_lo,
+                            int64_t* row_hi);
+int64_t gpic_packed_shard_tiles(int64_t n, int64_t row_lo, int64_t row_hi);
+int64_t gpic_packed_shard_scratch_bytes(int64_t n, int64_t row_lo, int64_t row_hi);
+int gpic_packed_shard_build(const float* d_xhi, const float* d_xlo, const float* d_sqn, int64_t n,
+                            int32_t d, int64_t row_lo, int64_t row_hi, double sigma, int32_t kind,
+                            float* d_tiles, double* d_deg_partial, void* d_scratch,
+                            void* stream);
+
 /* Matrix-free degrees of rows [row_lo, row_hi): deg = A 1 recomputed from the
  * prepared points (gpic_prepare_points). d_ones: gpic_vector_pitch(n) floats
  * of scratch; d_ypart: gpic_mf_ypart_doubles(n, d, rows) doubles. */

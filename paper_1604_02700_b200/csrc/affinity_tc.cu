@@ -132,7 +132,10 @@ struct TcArgs {
   float ns;  // -log2(e) / (2 sigma^2)
   float* rowpart;    // dense: [n_ctiles][rows_pad] fp32 row partials
   int64_t rows_pad;
-  int64_t n_rtiles;  // row blocks of 128*MB rows
+  int64_t n_rtiles;  // row blocks of 128*MB rows (packed shards: global end)
+  int64_t rb_base;   // packed shards: first row block (global); else 0
+  int64_t u_lo;      // packed shards: units before rb_base (contiguous order)
+  int64_t tile_base; // packed shards: global index of the shard's first stored tile
   int64_t n_ctiles;  // column tiles of 128
   const float* v32;  // matvec: vector_pitch(n) floats
   double* ypart;     // matvec: [n_chunks * parts][rows_pad] fp64 row partials
@@ -212,8 +215,8 @@ struct Cursor {
   __device__ bool start_row(const TcArgs& a) {
     const int G = gridDim.x, k = blockIdx.x;
     for (;; ++wave) {
-      if ((int64_t)wave * G >= a.n_rtiles) return false;
-      rb = wave * G + ((wave & 1) && (MODE != kModeMatvec || a.sym) ? G - 1 - k : k);
+      if ((int64_t)wave * G >= a.n_rtiles - a.rb_base) return false;
+      rb = (int)a.rb_base + wave * G + ((wave & 1) && (MODE != kModeMatvec || a.sym) ? G - 1 - k : k);
       if (rb < a.n_rtiles) break;
     }
     if (MODE == kModeMatvec) {
@@ -307,9 +310,9 @@ __global__ void __launch_bounds__(kCtaThreads<MODE>, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int64_t total = total_units<MB, MODE>(args);
-  const int64_t u_begin = total * blockIdx.x / gridDim.x;
-  const int64_t u_end = total * (blockIdx.x + 1) / gridDim.x;
+  const int64_t total = total_units<MB, MODE>(args) - args.u_lo;
+  const int64_t u_begin = args.u_lo + total * blockIdx.x / gridDim.x;
+  const int64_t u_end = args.u_lo + total * (blockIdx.x + 1) / gridDim.x;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < ST; ++s) {
@@ -704,7 +707,7 @@ __global__ void __launch_bounds__(kCtaThreads<MODE>, 1)
           __syncwarp();
           if (lane == 0 && store_ok) {
             const int64_t out_row0 = is_packed(MODE)
-                                         ? tile_index(tI, cb, args.n_ctiles) * 128 + q * 32
+                                         ? (tile_index(tI, cb, args.n_ctiles) - args.tile_base) * 128 + q * 32
                                          : lr0;
             if (args.store_hint)
               tma_store_2d(&map_out, is_packed(MODE) ? ch * 32 : (int)col0, (int)out_row0, stage,
@@ -744,7 +747,7 @@ __global__ void __launch_bounds__(kCtaThreads<MODE>, 1)
             }
             const int k = (b4 ? 4 : 0) + (b3 ? 2 : 0) + (b2 ? 1 : 0);  // = tq
             const int col = 8 * (k >> 1) + tc + (k & 1);
-            args.degcol[(tile_index(tI, cb, args.n_ctiles) * 4 + q) * 128 + ch * 32 + col] = cs[0];
+            args.degcol[((tile_index(tI, cb, args.n_ctiles) - args.tile_base) * 4 + q) * 128 + ch * 32 + col] = cs[0];
           }
         }
       };
@@ -859,7 +862,7 @@ __global__ void __launch_bounds__(kCtaThreads<MODE>, 1)
           for (int rr = 0; rr < 4; ++rr) {
             const int rloc = (rr >> 1) * 16 + tq + (rr & 1) * 8;  // row within the warp's 32
             if constexpr (is_packed(MODE)) {
-              args.degrow[tile_index(tI, cb, args.n_ctiles) * 128 + q * 32 + rloc] = tot[rr];
+              args.degrow[(tile_index(tI, cb, args.n_ctiles) - args.tile_base) * 128 + q * 32 + rloc] = tot[rr];
             } else {
               const int64_t lrow = lr0 + rloc;
               if (lrow < args.rows) args.rowpart[cb * args.rows_pad + lrow] = tot[rr];
@@ -912,6 +915,11 @@ int launch_kb(const CUtensorMap& mh, const CUtensorMap& ml, const CUtensorMap& m
   TcArgs a = a0;
   a.n_rtiles = ceil_div(a.rows, 128 * MB);
   a.n_chunks = ceil_div(a.n_ctiles, kChunkTiles);
+  if (is_packed(MODE)) {  // shard = row blocks [row_lo / (128 MB), n_rtiles), rows stay global
+    a.rb_base = a.row_lo / (128 * MB);
+    a.u_lo = packed_items(a.rb_base, a.n_ctiles, MB);
+    a.row_lo = 0;
+  }
   static bool attr = false;
   if (!attr) {
     GPIC_CUDA_TRY(cudaFuncSetAttribute(affinity_tc_kernel<KB, MODE, GPIC_KIND_RBF>,
@@ -936,11 +944,12 @@ int launch_kb(const CUtensorMap& mh, const CUtensorMap& ml, const CUtensorMap& m
   // balance (3.1 vs 3.4 ms) while its operands fit in ~L2/4.
   a.strided = MODE == kModePacked16
                   ? (int64_t)row_pad(a.n) * kKBlk * KB * 4 > (32ll << 20)
-                  : a.n_rtiles >= g_num_sms;
+                  : a.n_rtiles - a.rb_base >= g_num_sms;
   if (const char* o = getenv("GPIC_TC_ORDER")) a.strided = atoi(o) != 0;  // tests: force an order
   a.store_hint = 1;
   if (const char* o = getenv("GPIC_TC_STORE_HINT")) a.store_hint = atoi(o) != 0;  // measurement
-  const int64_t total = (MODE == kModeMatvec || a.strided) ? a.n_rtiles : total_units<MB, MODE>(a);
+  const int64_t total = (MODE == kModeMatvec || a.strided) ? a.n_rtiles - a.rb_base
+                                                            : total_units<MB, MODE>(a) - a.u_lo;
   const int grid = (int)(total < g_num_sms ? total : g_num_sms);
   if (grid < 1) return GPIC_OK;
   // the similarity kind is a template parameter: a runtime select would
@@ -1004,14 +1013,19 @@ int packed_row_halves(int32_t /*dp*/) { return 1; }  // the epilogue combines a 
 
 int launch_affinity_tc_packed(const float* xhi, const float* xlo, const float* sqn, int64_t n,
                               int32_t dp, float neg_scale_log2, void* a_packed, float* degrow,
-                              float* degcol, cudaStream_t s, int kind, bool half_out) {
+                              float* degcol, cudaStream_t s, int kind, bool half_out,
+                              int64_t row_lo, int64_t row_hi) {
+  if (row_hi <= 0) row_hi = n;
+  const int64_t nt = ceil_div(n, kBN);
+  const int64_t t_lo = tile_index(row_lo / 128, row_lo / 128, nt);
+  const int64_t t_hi = row_hi >= n ? packed_tiles(n) : tile_index(row_hi / 128, row_hi / 128, nt);
   Maps mp;
   int rc = operand_maps(xhi, n, dp, &mp);
   if (rc) return rc;
-  const bool ok = half_out ? make_map(&mp.out, a_packed, 128, (uint64_t)packed_tiles(n) * 128, 256,
+  const bool ok = half_out ? make_map(&mp.out, a_packed, 128, (uint64_t)(t_hi - t_lo) * 128, 256,
                                       32, 32, CU_TENSOR_MAP_DATA_TYPE_FLOAT16,
                                       CU_TENSOR_MAP_SWIZZLE_64B)
-                           : make_map(&mp.out, a_packed, 128, (uint64_t)packed_tiles(n) * 128, 512,
+                           : make_map(&mp.out, a_packed, 128, (uint64_t)(t_hi - t_lo) * 128, 512,
                                       32, 32);
   if (!ok) return fail(GPIC_E_CUDA, "cuTensorMapEncodeTiled failed");
   TcArgs args{};
@@ -1019,7 +1033,9 @@ int launch_affinity_tc_packed(const float* xhi, const float* xlo, const float* s
   args.sqn = sqn;
   args.gscale = sqn + row_pad(n) - 1;
   args.n = n;
-  args.rows = n;
+  args.row_lo = row_lo;  // launch_kb turns the row range into row blocks
+  args.rows = row_hi;
+  args.tile_base = t_lo;
   args.ns = neg_scale_log2;
   args.n_ctiles = ceil_div(n, kBN);
   args.out = static_cast<float*>(a_packed);

@@ -323,6 +323,91 @@ int gpic_matvec(const float* d_a, int64_t lda, int64_t rows, int64_t n, const fl
 int64_t gpic_packed_tiles(int64_t n) { return n < 1 ? -1 : packed_tiles(n); }
 int64_t gpic_sym_partial_floats(int64_t n) { return n < 1 ? -1 : sym_partial_floats(n); }
 
+// ---- packed shards (multi-rank symmetric storage) ----------------------
+// Rank r of P owns super-rows (512 rows) [P_r, P_r+1), balanced by stored
+// tile count; its tiles are the contiguous packed range of those rows.
+static int64_t super_rows(int64_t n) { return ceil_div(ceil_div(n, kTileN), 4); }
+static int64_t tiles_before_row(int64_t n, int64_t tile_row) {
+  const int64_t nt = ceil_div(n, kTileN);
+  const int64_t I = tile_row < nt ? tile_row : nt;
+  return I * nt - I * (I - 1) / 2;
+}
+
+int gpic_packed_shard_range(int64_t n, int32_t nranks, int32_t rank, int64_t* row_lo,
+                            int64_t* row_hi) {
+  if (n < 1 || nranks < 1 || rank < 0 || rank >= nranks || !row_lo || !row_hi)
+    return fail(GPIC_E_INVALID, "bad packed shard parameters");
+  const int64_t ns = super_rows(n);
+  if (ns < nranks) return fail(GPIC_E_INVALID, "too few 512-row super-rows for the rank count");
+  const int64_t total = tiles_before_row(n, 4 * ns);
+  auto cut = [&](int64_t r) {  // first super-row whose tile prefix reaches r / P of the total
+    if (r <= 0) return (int64_t)0;
+    if (r >= nranks) return ns;
+    const int64_t want = total * r / nranks;
+    int64_t lo = 0, hi = ns;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) / 2;
+      if (tiles_before_row(n, 4 * mid) >= want) hi = mid; else lo = mid + 1;
+    }
+    // every rank keeps at least one super-row
+    if (lo < r) lo = r;
+    if (lo > ns - (nranks - r)) lo = ns - (nranks - r);
+    return lo;
+  };
+  const int64_t p0 = cut(rank), p1 = cut(rank + 1);
+  *row_lo = 512 * p0;
+  *row_hi = 512 * p1 < n ? 512 * p1 : n;
+  return GPIC_OK;
+}
+
+int64_t gpic_packed_shard_tiles(int64_t n, int64_t row_lo, int64_t row_hi) {
+  if (n < 1 || row_lo % 512 || row_hi <= row_lo) return -1;
+  return tiles_before_row(n, ceil_div(row_hi, kTileN)) - tiles_before_row(n, row_lo / kTileN);
+}
+
+// scratch: [GEMV row records][GEMV column records][degree row partials]
+// [degree column partials (4 quadrants)], each 256-byte aligned
+static int64_t shard_records(int64_t n, int64_t row_lo, int64_t row_hi) {
+  const int64_t ns = super_rows(n);
+  const int64_t p0 = row_lo / 512, p1 = ceil_div(row_hi, 512);
+  const int64_t a = p0 * ns - p0 * (p0 - 1) / 2, b = p1 * ns - p1 * (p1 - 1) / 2;
+  return (b - a) * 4 * 128;
+}
+int64_t gpic_packed_shard_scratch_bytes(int64_t n, int64_t row_lo, int64_t row_hi) {
+  const int64_t t = gpic_packed_shard_tiles(n, row_lo, row_hi);
+  if (t < 0) return -1;
+  const int64_t r = shard_records(n, row_lo, row_hi);
+  return 2 * al(r * 4) + al(t * 128 * 4) + al(t * 4 * 128 * 4);
+}
+
+int gpic_packed_shard_build(const float* d_xhi, const float* d_xlo, const float* d_sqn, int64_t n,
+                            int32_t d, int64_t row_lo, int64_t row_hi, double sigma, int32_t kind,
+                            float* d_tiles, double* d_deg_partial, void* d_scratch,
+                            void* stream) {
+  if (kind == GPIC_KIND_RBF && !(sigma > 0)) return fail(GPIC_E_INVALID, "sigma must be positive");
+  if (kind == GPIC_KIND_COSINE) sigma = 1.0;
+  const int64_t t = gpic_packed_shard_tiles(n, row_lo, row_hi);
+  if (t < 0) return fail(GPIC_E_INVALID, "bad packed shard row range");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int32_t dp = feature_pitch(d);
+  const int64_t r = shard_records(n, row_lo, row_hi);
+  uint8_t* base = static_cast<uint8_t*>(d_scratch) + 2 * al(r * 4);
+  float* degrow = reinterpret_cast<float*>(base);
+  float* degcol = reinterpret_cast<float*>(base + al(t * 128 * 4));
+  const float neg_scale_log2 = (float)(-1.4426950408889634 / (2.0 * sigma * sigma));
+  int rc = launch_affinity_tc_packed(d_xhi, d_xlo, d_sqn, n, dp, neg_scale_log2, d_tiles, degrow,
+                                     degcol, s, kind, false, row_lo, row_hi);
+  if (rc) return rc;
+  GPIC_CUDA_TRY(cudaMemsetAsync(d_deg_partial, 0, n * 8, s));
+  ShardRange sr;
+  sr.p_lo = row_lo / 512;
+  sr.p_hi = ceil_div(row_hi, 512);
+  sr.tile_base = tiles_before_row(n, row_lo / kTileN);
+  launch_sym_degree(degrow, degcol, n, packed_row_halves(dp), d_deg_partial, nullptr, s, sr);
+  GPIC_CUDA_TRY(cudaGetLastError());
+  return GPIC_OK;
+}
+
 int64_t gpic_cluster_workspace_bytes(int64_t n, int32_t d, int32_t k, int32_t max_iter,
                                      int32_t storage) {
   if (n < 1 || d < 1) return -1;

@@ -51,7 +51,15 @@ namespace gpic {
 namespace {
 
 inline int64_t al(int64_t b) { return (b + 255) & ~int64_t(255); }
-inline int64_t region_bytes(int64_t n) { return 3 * al(n * 8) + al(kFlagSlots * 8); }
+// per rank: y0 | y1 | degf | flags | slots[kMaxRanks][2] (packed shards'
+// y / degree partials, written by their owners, summed by this rank)
+inline int64_t region_bytes(int64_t n) {
+  return 3 * al(n * 8) + al(kFlagSlots * 8) + 2 * kMaxRanks * al(n * 8);
+}
+inline double* r_slot(uint8_t* r, int64_t n, int rank, int parity) {
+  return reinterpret_cast<double*>(r + 3 * al(n * 8) + al(kFlagSlots * 8) +
+                                   (2 * rank + parity) * al(n * 8));
+}
 inline double* r_y(uint8_t* r, int64_t n, int p) { return reinterpret_cast<double*>(r + p * al(n * 8)); }
 inline double* r_deg(uint8_t* r, int64_t n) { return reinterpret_cast<double*>(r + 2 * al(n * 8)); }
 inline uint64_t* r_flags(uint8_t* r, int64_t n) {
@@ -157,6 +165,37 @@ int gather(gpic_comm* c, const gpic_shard* shards, bool with_data, cudaStream_t 
     const int self = c->rank0 + li;
     launch_peer_wait(r_flags(c->region[self], c->n), kMaxRanks, c->nranks, epoch, 0,
                      c->loc[li].ctl, s);
+  }
+  GPIC_CUDA_TRY(cudaGetLastError());
+  return GPIC_OK;
+}
+
+// Packed shards: every local shard publishes its partial degrees (rows
+// [row_lo, n)) into its slot (parity 0) of every rank, waits for all P, then
+// each rank sums the P partials in rank order into its degf.
+int gather_sum(gpic_comm* c, const gpic_shard* shards, cudaStream_t s) {
+  const uint64_t epoch = ++c->gather_epoch;
+  for (int li = 0; li < c->nlocal; ++li) {
+    const int self = c->rank0 + li;
+    PubArgs pa;
+    std::memset(&pa, 0, sizeof pa);
+    for (int p = 0; p < c->nranks; ++p) {
+      pa.dsts[p] = r_slot(c->region[p], c->n, self, 0);
+      pa.flags[p] = r_flags(c->region[p], c->n);
+    }
+    const int64_t rows = c->n - shards[li].row_lo;
+    const int grid = rows > 0 ? (int)std::min<int64_t>(ceil_div(rows, 256), 148) : 1;
+    publish_entry<<<grid, 256, 0, s>>>(shards[li].deg + shards[li].row_lo, rows, shards[li].row_lo,
+                                       pa, c->nranks, self, epoch, &c->loc[li].ctl->arrive[3]);
+    count_launch();
+  }
+  for (int li = 0; li < c->nlocal; ++li) {
+    const int self = c->rank0 + li;
+    launch_peer_wait(r_flags(c->region[self], c->n), kMaxRanks, c->nranks, epoch, 0,
+                     c->loc[li].ctl, s);
+    const int64_t stride = al(c->n * 8) / 8;
+    launch_slot_combine(r_slot(c->region[self], c->n, 0, 0), stride, c->nranks, c->n, nullptr,
+                        r_deg(c->region[self], c->n), r_deg(c->region[self], c->n), nullptr, s);
   }
   GPIC_CUDA_TRY(cudaGetLastError());
   return GPIC_OK;
@@ -269,7 +308,11 @@ int gpic_comm_gather_degrees(gpic_comm* c, const gpic_shard* shards, int32_t nlo
   if (!c || nlocal != c->nlocal) return fail(GPIC_E_INVALID, "shard count does not match the comm");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   for (int li = 0; li < nlocal; ++li) launch_ctl_init(c->loc[li].ctl, 0.0, 1, s);
-  int rc = gather(c, shards, true, s);
+  const bool packed = shards[0].storage == GPIC_STORAGE_PACKED;
+  for (int li = 1; li < nlocal; ++li)
+    if ((shards[li].storage == GPIC_STORAGE_PACKED) != packed)
+      return fail(GPIC_E_INVALID, "all shards of a comm use the same storage");
+  int rc = packed ? gather_sum(c, shards, s) : gather(c, shards, true, s);
   if (rc) return rc;
   // every rank now holds all n degrees: the ZeroDegree check is global
   const double* degf = r_deg(c->region[c->rank0], c->n);
@@ -318,6 +361,26 @@ int gpic_comm_iterate(gpic_comm* c, const gpic_shard* shards, int32_t nlocal, do
     std::memset(&S, 0, sizeof S);
     S.a = shards[li].a;
     S.lda = shards[li].lda;
+    if (shards[li].storage == GPIC_STORAGE_PACKED) {
+      // packed shard: its super-rows' tiles; y partials go to every rank's
+      // slot of this shard, each rank sums the slots in rank order
+      const gpic_shard& sh = shards[li];
+      S.mode = kLoopPackedShard;
+      const int64_t nt = ceil_div(n, kTileN);
+      S.sr.p_lo = sh.row_lo / 512;
+      S.sr.p_hi = ceil_div(sh.row_lo + sh.rows, 512);
+      S.sr.tile_base = 4 * S.sr.p_lo * nt - 4 * S.sr.p_lo * (4 * S.sr.p_lo - 1) / 2;
+      const int64_t ns = ceil_div(nt, 4);
+      const int64_t recs = (S.sr.sb_hi(ns) - S.sr.sb_lo(ns)) * 4 * 128;
+      S.rowp = reinterpret_cast<float*>(sh.ypart);
+      S.colp = S.rowp + ((recs * 4 + 255) / 256) * 64;
+      S.pt_slots = table(c, self);
+      for (int p = 0; p < c->nranks; ++p)
+        for (int par = 0; par < 2; ++par) S.pt_slots.y[p][par] = r_slot(c->region[p], n, self, par);
+      S.slots = r_slot(c->region[self], n, 0, 0);
+      S.slot_stride = al(n * 8) / 8;
+      S.deg_full = r_deg(c->region[self], n);
+    }
     if (shards[li].storage == GPIC_STORAGE_NONE) {
       const gpic_shard& sh = shards[li];
       S.mode = kLoopMatrixFree;

@@ -2,12 +2,25 @@
 // libgpic. Everything here is asynchronous on `stream`.
 #pragma once
 
+#include <cstdint>
+
 #include <cuda_runtime.h>
 #include <stdint.h>
 
 #include "../../include/gpic.h"
 
 namespace gpic {
+
+// A packed shard (sym.cu): super-rows [p_lo, p_hi) of 4 x 128 rows, its
+// tiles stored from global tile index tile_base. Default: the whole matrix.
+struct ShardRange {
+  int64_t p_lo = 0;
+  int64_t p_hi = INT64_MAX / 4;
+  int64_t tile_base = 0;
+  __host__ __device__ int64_t sb_lo(int64_t ns) const;
+  __host__ __device__ int64_t sb_hi(int64_t ns) const;
+};
+
 
 constexpr int kTileM = 128;  // affinity row tile
 constexpr int kTileN = 128;  // affinity column tile
@@ -34,9 +47,10 @@ int packed_row_halves(int32_t dp);
 int launch_affinity_tc_packed(const float* xhi, const float* xlo, const float* sqn, int64_t n,
                               int32_t dp, float neg_scale_log2, void* a_packed, float* degrow,
                               float* degcol, cudaStream_t s, int kind = GPIC_KIND_RBF,
-                              bool half_out = false);
+                              bool half_out = false, int64_t row_lo = 0, int64_t row_hi = 0);
 void launch_sym_degree(const float* degrow, const float* degcol, int64_t n, int nhalf,
-                       double* deg, gpic_ctl* ctl, cudaStream_t s);
+                       double* deg, gpic_ctl* ctl, cudaStream_t s,
+                       const ShardRange& sr = ShardRange());
 void sym_prepare();
 
 // Workspace carve-up (see capi.cu).
@@ -112,6 +126,9 @@ void launch_gemv(const float* a, int64_t lda, int64_t rows, int64_t row_lo, cons
                  const double* deg, const PeerTable& pt, gpic_ctl* ctl, cudaStream_t s);
 void launch_peer_wait(const uint64_t* flags_self, int slot0, int count, uint64_t base,
                       int add_iter, gpic_ctl* ctl, cudaStream_t s);
+// y = (sum over ranks of the packed shards' y partials, rank order) / deg
+void launch_slot_combine(const double* slots, int64_t stride, int nranks, int64_t n,
+                         const double* deg, double* y0, double* y1, gpic_ctl* ctl, cudaStream_t s);
 void launch_iteration_tail(const double* y0, const double* y1, int64_t n, double* redpart,
                            double* v64, float* v32, double* hist, gpic_ctl* ctl, cudaStream_t s);
 void launch_copy_result(const double* v64, int64_t n, double* out, const gpic_ctl* ctl,
@@ -119,7 +136,8 @@ void launch_copy_result(const double* v64, int64_t n, double* out, const gpic_ct
 
 struct PeerTable;
 void launch_sym_gemv(const float* tiles, int64_t n, const float* v32, float* rowp, float* colp,
-                     const double* deg, const PeerTable& pt, gpic_ctl* ctl, cudaStream_t s);
+                     const double* deg, const PeerTable& pt, gpic_ctl* ctl, cudaStream_t s,
+                     const ShardRange& sr = ShardRange());
 // fp16 packed tiles (GPIC_STORAGE_PACKED16): same partials / reduce
 void launch_sym_gemv16(const void* tiles, int64_t n, const float* v32, float* rowp, float* colp,
                        const double* deg, const PeerTable& pt, gpic_ctl* ctl, cudaStream_t s);
@@ -151,7 +169,7 @@ int launch_mf_matvec(const MfOperands& op, int64_t row_lo, int64_t rows, const f
 int launch_mf_degrees(const MfOperands& op, int64_t row_lo, int64_t rows, float* ones,
                       double* ypart, double* deg, cudaStream_t s);
 
-enum { kLoopDense = 0, kLoopPacked = 1, kLoopMatrixFree = 2, kLoopPacked16 = 3 };
+enum { kLoopDense = 0, kLoopPacked = 1, kLoopMatrixFree = 2, kLoopPacked16 = 3, kLoopPackedShard = 4 };
 
 // One shard's loop state (a single-rank run is one shard with nranks = 1).
 struct ShardLoop {
@@ -171,6 +189,13 @@ struct ShardLoop {
   double* hist;
   gpic_ctl* ctl;
   PeerTable pt;
+  // packed shards (kLoopPackedShard): super-row range, the y-partial table
+  // (every rank's slot of this shard), this rank's slots and full degrees
+  ShardRange sr;
+  PeerTable pt_slots;
+  const double* slots;   // this rank's slot [0][0]; (rank, parity) at (2 rank + parity) * stride
+  int64_t slot_stride;
+  const double* deg_full;
 };
 // Capture max_iter iterations of every local shard into one CUDA graph
 // (virtual ranks: all GEMVs of an iteration precede all tails) and launch it.

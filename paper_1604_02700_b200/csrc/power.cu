@@ -219,6 +219,27 @@ void launch_scale_by(const double* src, int64_t n, double tau, double* dst, floa
   count_launch();
 }
 
+namespace {
+__global__ void slot_combine_kernel(const double* __restrict__ slots, int64_t stride, int nranks,
+                                    int64_t n, const double* __restrict__ deg, double* y0,
+                                    double* y1, gpic_ctl* ctl) {
+  if (ctl != nullptr && *(volatile const int32_t*)&ctl->stop) return;
+  const int parity = ctl != nullptr ? (ctl->iter & 1) : 0;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double t = 0.0;
+  for (int r = 0; r < nranks; ++r) t += slots[(2 * r + parity) * stride + i];
+  (parity ? y1 : y0)[i] = deg != nullptr ? t / deg[i] : t;
+}
+}  // namespace
+
+void launch_slot_combine(const double* slots, int64_t stride, int nranks, int64_t n,
+                         const double* deg, double* y0, double* y1, gpic_ctl* ctl, cudaStream_t s) {
+  slot_combine_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, s>>>(slots, stride, nranks, n, deg, y0,
+                                                                 y1, ctl);
+  count_launch();
+}
+
 void launch_iteration_tail(const double* y0, const double* y1, int64_t n, double* redpart,
                            double* v64, float* v32, double* hist, gpic_ctl* ctl, cudaStream_t s) {
   const unsigned nb = (unsigned)ceil_div(n, kRedBlock);
@@ -302,6 +323,9 @@ int run_power_loops(ShardLoop* shards, int nlocal, int64_t n, int32_t max_iter, 
           launch_sym_gemv(L.a, n, L.v32, L.rowp, L.colp, L.deg, L.pt, L.ctl, cs);
         } else if (L.mode == kLoopPacked16) {
           launch_sym_gemv16(L.a, n, L.v32, L.rowp, L.colp, L.deg, L.pt, L.ctl, cs);
+        } else if (L.mode == kLoopPackedShard) {
+          // partial y over the shard's tiles into every rank's slot of this shard
+          launch_sym_gemv(L.a, n, L.v32, L.rowp, L.colp, nullptr, L.pt_slots, L.ctl, cs, L.sr);
         } else if (L.mode == kLoopMatrixFree) {
           const int rc = launch_mf_matvec(L.mf, L.row_lo, L.rows, L.v32, L.ypart, L.deg, L.pt,
                                           L.ctl, cs);
@@ -320,6 +344,9 @@ int run_power_loops(ShardLoop* shards, int nlocal, int64_t n, int32_t max_iter, 
         const PeerTable& pt = L.pt;
         if (pt.flags[0] != nullptr)
           launch_peer_wait(pt.flags[pt.self], 0, pt.nranks, 0, 1, L.ctl, cs);
+        if (L.mode == kLoopPackedShard)
+          launch_slot_combine(L.slots, L.slot_stride, pt.nranks, n, L.deg_full, pt.y[pt.self][0],
+                              pt.y[pt.self][1], L.ctl, cs);
         launch_iteration_tail(pt.y[pt.self][0], pt.y[pt.self][1], n, L.redpart, L.v64, L.v32,
                               L.hist, L.ctl, cs);
       }

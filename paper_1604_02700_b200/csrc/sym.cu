@@ -76,6 +76,21 @@ __device__ inline void tile_coords(int64_t t, int64_t nt, int64_t& I, int64_t& J
 // NS x NS triangle (NS = ceil(NT / kSB)), same index formula as the tiles.
 constexpr int kSB = 4;
 
+}  // namespace
+
+// A packed shard: super-rows [p_lo, p_hi) of the super-block triangle (tile
+// rows [kSB p_lo, kSB p_hi)), stored from global tile index tile_base.
+// Whole matrix: {0, huge, 0}.
+__host__ __device__ int64_t ShardRange::sb_lo(int64_t ns) const {
+  return p_lo * ns - p_lo * (p_lo - 1) / 2;
+}
+__host__ __device__ int64_t ShardRange::sb_hi(int64_t ns) const {
+  const int64_t p = p_hi < ns ? p_hi : ns;
+  return p * ns - p * (p - 1) / 2;
+}
+
+namespace {
+
 // The tiles of one super-block, in the order both roles walk them: rows
 // I = kSB P .. (< NT), then columns J = max(I, kSB Q) .. (< NT).
 struct SbWalk {
@@ -119,7 +134,7 @@ template <typename T>
 __global__ void __launch_bounds__(kThreads, 1)
     sym_gemv_kernel(const T* __restrict__ tiles, int64_t nt, const float* __restrict__ v32,
                     float* __restrict__ rowp, float* __restrict__ colp,
-                    const gpic_ctl* __restrict__ ctl) {
+                    const gpic_ctl* __restrict__ ctl, ShardRange sr) {
   constexpr int kStages = TileTraits<T>::kStg;
   constexpr int kTileBytes = kTileFloats * (int)sizeof(T);
   if (ctl != nullptr && *(volatile const int32_t*)&ctl->stop) return;
@@ -139,9 +154,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   __syncthreads();
   const int64_t ns = (nt + kSB - 1) / kSB;
-  const int64_t total = ns * (ns + 1) / 2;
-  const int64_t s0 = total * blockIdx.x / gridDim.x;
-  const int64_t s1 = total * (blockIdx.x + 1) / gridDim.x;
+  // the shard's super-blocks [sb_lo, sb_hi) (whole matrix: all of them);
+  // records are indexed from sb_lo, tiles from the shard's first tile
+  const int64_t sb_lo = sr.sb_lo(ns), total = sr.sb_hi(ns) - sb_lo;
+  const int64_t s0 = sb_lo + total * blockIdx.x / gridDim.x;
+  const int64_t s1 = sb_lo + total * (blockIdx.x + 1) / gridDim.x;
   if (s0 >= s1) return;
   SbWalk w;
   w.nt = nt;
@@ -161,7 +178,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       do {
         mbar_wait(&empty[s], ph ^ 1);
         mbar_expect_tx(&full[s], kTileBytes);
-        bulk_load(st + s * kTileBytes, src0 + tile_index(w.I, w.J, nt) * kTileBytes, kTileBytes,
+        bulk_load(st + s * kTileBytes, src0 + (tile_index(w.I, w.J, nt) - sr.tile_base) * kTileBytes, kTileBytes,
                   &full[s]);
         if (++s == kStages) { s = 0; ph ^= 1; }
       } while (w.next());
@@ -267,7 +284,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int row = ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 +
                         ((lane >> 1) & 1);
         if ((lane & 1) == 0)
-          rowp[(sb * kSB + (I - kSB * w.P)) * kTS + warp * kRowsPerWarp + row] = acc[0];
+          rowp[((sb - sb_lo) * kSB + (I - kSB * w.P)) * kTS + warp * kRowsPerWarp + row] = acc[0];
 #pragma unroll
         for (int i = 0; i < kRowsPerWarp; ++i) acc[i] = 0.f;
       }
@@ -287,7 +304,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         float sum = 0.f;
 #pragma unroll
         for (int w8 = 0; w8 < kWarps; ++w8) sum += rw[(w8 * kSB + c) * kTS + t];
-        colp[(sb * kSB + c) * kTS + t] = sum;
+        colp[((sb - sb_lo) * kSB + c) * kTS + t] = sum;
       }
     rb ^= 1;
   }
@@ -307,18 +324,24 @@ constexpr int kSeg = 8;
 __global__ void __launch_bounds__(kTS * kSeg)
     sym_reduce_kernel(const float* __restrict__ rowp, const float* __restrict__ colp, int64_t n,
                       int64_t nt, const double* __restrict__ deg, const PeerTable pt,
-                      gpic_ctl* ctl) {
+                      gpic_ctl* ctl, ShardRange sr) {
   if (ctl != nullptr && *(volatile const int32_t*)&ctl->stop) return;
   __shared__ double part[kSeg][kTS];
-  const int64_t R = blockIdx.x;
-  const int o = threadIdx.x % kTS, sg = threadIdx.x / kTS;
   const int64_t ns = (nt + kSB - 1) / kSB;
+  const int64_t p_hi = sr.p_hi < ns ? sr.p_hi : ns;
+  const int64_t R = kSB * sr.p_lo + blockIdx.x;  // rows above the shard get nothing from it
+  const int o = threadIdx.x % kTS, sg = threadIdx.x / kTS;
   const int64_t Q = R / kSB, k = R - kSB * Q;
-  const int64_t terms = ns + 1;
+  const int64_t sb0 = sr.sb_lo(ns);
+  // the shard's records of row R: column records of (P', Q), P' in
+  // [p_lo, min(Q, p_hi - 1)], then row records of (Q, Q') if Q is its own
+  const int64_t ncol = (Q < p_hi - 1 ? Q : p_hi - 1) - sr.p_lo + 1;
+  const int64_t nrow = Q < p_hi ? ns - Q : 0;
+  const int64_t terms = ncol + nrow;
   const int64_t p0 = terms * sg / kSeg, p1 = terms * (sg + 1) / kSeg;
   auto load = [&](int64_t p) {
-    return p <= Q ? colp[(tile_index(p, Q, ns) * kSB + k) * kTS + o]
-                  : rowp[(tile_index(Q, Q + (p - Q - 1), ns) * kSB + k) * kTS + o];
+    return p < ncol ? colp[((tile_index(sr.p_lo + p, Q, ns) - sb0) * kSB + k) * kTS + o]
+                    : rowp[((tile_index(Q, Q + (p - ncol), ns) - sb0) * kSB + k) * kTS + o];
   };
   double s = 0.0;
   int64_t p = p0;
@@ -360,20 +383,28 @@ __global__ void __launch_bounds__(kTS * kSeg)
 // then row partials (nhalf column halves) of tiles (R, p), p >= R.
 __global__ void __launch_bounds__(kTS * kSeg)
     sym_degree_kernel(const float* __restrict__ degrow, const float* __restrict__ degcol,
-                      int64_t n, int64_t nt, int nhalf, double* __restrict__ deg, gpic_ctl* ctl) {
+                      int64_t n, int64_t nt, int nhalf, double* __restrict__ deg, gpic_ctl* ctl,
+                      ShardRange sr) {
   __shared__ double part[kSeg][kTS];
-  const int64_t R = blockIdx.x;
+  // shard: tile rows [tr_lo, tr_hi) are stored (from tile_base); row R gets
+  // the column partials of its stored tiles (p, R) and, if R is its own,
+  // the row partials of (R, p >= R). deg is then the shard's partial.
+  const int64_t tr_lo = kSB * sr.p_lo, tr_hi = kSB * sr.p_hi < nt ? kSB * sr.p_hi : nt;
+  const int64_t R = tr_lo + blockIdx.x;
   const int o = threadIdx.x % kTS, sg = threadIdx.x / kTS;
   const int64_t p0 = nt * sg / kSeg, p1 = nt * (sg + 1) / kSeg;
   double s = 0.0;
   // 4 tiles' partials in flight per step, then added in order
   auto load4 = [&](int64_t p, float (&x)[4]) {
+    x[0] = x[1] = x[2] = x[3] = 0.f;
     if (p < R) {
-      const float* c = degcol + tile_index(p, R, nt) * 4 * kTS + o;
+      if (p < tr_lo || p >= tr_hi) return;  // tile (p, R) lives on another shard
+      const float* c = degcol + (tile_index(p, R, nt) - sr.tile_base) * 4 * kTS + o;
       x[0] = c[0]; x[1] = c[kTS]; x[2] = c[2 * kTS]; x[3] = c[3 * kTS];
     } else {
-      const float* r = degrow + tile_index(R, p, nt) * nhalf * kTS + o;
-      x[0] = r[0]; x[1] = nhalf == 2 ? r[kTS] : 0.f; x[2] = x[3] = 0.f;
+      if (R >= tr_hi) return;
+      const float* r = degrow + (tile_index(R, p, nt) - sr.tile_base) * nhalf * kTS + o;
+      x[0] = r[0]; x[1] = nhalf == 2 ? r[kTS] : 0.f;
     }
   };
   auto add4 = [&](int64_t p, const float (&x)[4]) {
@@ -405,7 +436,7 @@ __global__ void __launch_bounds__(kTS * kSeg)
 #pragma unroll
     for (int q = 0; q < kSeg; ++q) t += part[q][o];
     deg[i] = t;
-    if (t <= 0.0) raise_status(ctl, GPIC_E_ZERO_DEGREE, i, -1, t);
+    if (ctl != nullptr && t <= 0.0) raise_status(ctl, GPIC_E_ZERO_DEGREE, i, -1, t);
   }
 }
 
@@ -414,9 +445,12 @@ int g_sms = 0;
 }  // namespace
 
 void launch_sym_degree(const float* degrow, const float* degcol, int64_t n, int nhalf,
-                       double* deg, gpic_ctl* ctl, cudaStream_t s) {
+                       double* deg, gpic_ctl* ctl, cudaStream_t s, const ShardRange& sr) {
   const int64_t nt = ceil_div(n, kTS);
-  sym_degree_kernel<<<(unsigned)nt, kTS * kSeg, 0, s>>>(degrow, degcol, n, nt, nhalf, deg, ctl);
+  const int64_t rows = nt - kSB * sr.p_lo;  // tile rows that can receive partials
+  if (rows < 1) return;
+  sym_degree_kernel<<<(unsigned)rows, kTS * kSeg, 0, s>>>(degrow, degcol, n, nt, nhalf, deg, ctl,
+                                                          sr);
   count_launch();
 }
 
@@ -440,14 +474,17 @@ int64_t sym_partial_floats(int64_t n) {
 }
 
 void launch_sym_gemv(const float* tiles, int64_t n, const float* v32, float* rowp, float* colp,
-                     const double* deg, const PeerTable& pt, gpic_ctl* ctl, cudaStream_t s) {
+                     const double* deg, const PeerTable& pt, gpic_ctl* ctl, cudaStream_t s,
+                     const ShardRange& sr) {
   sym_prepare();
   const int64_t nt = ceil_div(n, kTS);
   const int64_t ns = (nt + kSB - 1) / kSB;
-  const int64_t total = ns * (ns + 1) / 2;  // super-blocks
+  const int64_t total = sr.sb_hi(ns) - sr.sb_lo(ns);  // the shard's super-blocks
   const int grid = (int)(total < g_sms ? total : g_sms);
-  sym_gemv_kernel<float><<<grid, kThreads, kSmem, s>>>(tiles, nt, v32, rowp, colp, ctl);
-  sym_reduce_kernel<<<(unsigned)nt, kTS * kSeg, 0, s>>>(rowp, colp, n, nt, deg, pt, ctl);
+  const int64_t rows = nt - kSB * sr.p_lo;
+  if (grid < 1 || rows < 1) return;
+  sym_gemv_kernel<float><<<grid, kThreads, kSmem, s>>>(tiles, nt, v32, rowp, colp, ctl, sr);
+  sym_reduce_kernel<<<(unsigned)rows, kTS * kSeg, 0, s>>>(rowp, colp, n, nt, deg, pt, ctl, sr);
   count_launch(2);
 }
 
@@ -458,9 +495,10 @@ void launch_sym_gemv16(const void* tiles, int64_t n, const float* v32, float* ro
   const int64_t ns = (nt + kSB - 1) / kSB;
   const int64_t total = ns * (ns + 1) / 2;  // super-blocks
   const int grid = (int)(total < g_sms ? total : g_sms);
+  const ShardRange all{};
   sym_gemv_kernel<__half><<<grid, kThreads, kSmem, s>>>(static_cast<const __half*>(tiles), nt, v32,
-                                                            rowp, colp, ctl);
-  sym_reduce_kernel<<<(unsigned)nt, kTS * kSeg, 0, s>>>(rowp, colp, n, nt, deg, pt, ctl);
+                                                            rowp, colp, ctl, all);
+  sym_reduce_kernel<<<(unsigned)nt, kTS * kSeg, 0, s>>>(rowp, colp, n, nt, deg, pt, ctl, all);
   count_launch(2);
 }
 

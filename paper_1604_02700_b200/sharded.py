@@ -122,6 +122,18 @@ class ShardedRunner:
                 )
             self.locals = [self.rank]
         self.dev = gpu._device(config)
+        # packed symmetric shards (tcgen05 engine) unless dense rows were asked
+        # for (dense row shards are bitwise independent of P)
+        self.packed = config.storage == "packed" and config.affinity_impl == "tc"
+        if self.packed:
+            L = _lib.lib()
+            self.packed_ranges = []
+            for r in range(P):
+                lo, hi = C.c_int64(), C.c_int64()
+                if L.gpic_packed_shard_range(n, P, r, C.byref(lo), C.byref(hi)) != _lib.GPIC_OK:
+                    self.packed = False  # fewer 512-row super-rows than ranks: dense rows
+                    break
+                self.packed_ranges.append((lo.value, hi.value))
         self.comm = Comm(n, P, config.virtual_ranks, self.rank)
 
     def close(self):
@@ -154,6 +166,23 @@ class ShardedRunner:
                 shards[i] = _lib.Shard(None, 0, deg.data_ptr(), lo, hi - lo, _lib.STORAGE_NONE,
                                        prep.d, prep.xhi.data_ptr(), prep.xlo.data_ptr(),
                                        prep.sqn.data_ptr(), sigma, code, ypart.data_ptr())
+        elif self.packed:
+            # symmetric packed shards: upper-triangle tiles of the rank's
+            # 512-row super-rows, partial degrees summed across ranks
+            for i, r in enumerate(self.locals):
+                lo, hi = self.packed_ranges[r]
+                ntile = int(L.gpic_packed_shard_tiles(n, lo, hi))
+                tiles = torch.empty(ntile * 128 * 128, dtype=torch.float32, device=dev)
+                deg = torch.empty(n, dtype=torch.float64, device=dev)
+                scratch = torch.empty(int(L.gpic_packed_shard_scratch_bytes(n, lo, hi)),
+                                      dtype=torch.uint8, device=dev)
+                _lib.check(L.gpic_packed_shard_build(
+                    gpu._ptr(prep.xhi), gpu._ptr(prep.xlo), gpu._ptr(prep.sqn), n, prep.d, lo, hi,
+                    sigma, code, gpu._ptr(tiles), gpu._ptr(deg), gpu._ptr(scratch), st))
+                keep += [tiles, deg, scratch]
+                shards[i] = _lib.Shard(tiles.data_ptr(), 0, deg.data_ptr(), lo, hi - lo,
+                                       _lib.STORAGE_PACKED, prep.d, None, None, None, sigma, code,
+                                       scratch.data_ptr())
         else:
             for i, r in enumerate(self.locals):
                 lo, hi = self.ranges[r]

@@ -97,7 +97,8 @@ def test_virtual_ranks_bitwise_invariant(engine):
                    seed=1)
     for p in (2, 3, 4, 8):
         got = cluster(d, kind, params, seed=1,
-                      config=KernelConfig(p=p, virtual_ranks=True, affinity_impl=engine))
+                      config=KernelConfig(p=p, virtual_ranks=True, affinity_impl=engine,
+                                          storage="dense"))
         assert np.array_equal(got[0], base[0]), p
         assert np.array_equal(got[1], base[1]), p
         assert got[2].iterations_run == base[2].iterations_run
@@ -110,7 +111,7 @@ def test_virtual_ranks_forced_iterations_and_repeat():
     kind = GaussianRbf(2.0)
     params = PicParams(k=4, epsilon=5e-324, max_iterations=9)
     base = cluster(d, kind, params, config=KernelConfig(storage="dense"))
-    cfg = KernelConfig(p=4, virtual_ranks=True)
+    cfg = KernelConfig(p=4, virtual_ranks=True, storage="dense")
     a = cluster(d, kind, params, config=cfg)
     b = cluster(d, kind, params, config=cfg)   # second run: epochs keep increasing
     for r in (a, b):
@@ -158,3 +159,51 @@ def test_matrix_free_virtual_ranks_bitwise():
                       config=KernelConfig(p=p, virtual_ranks=True, storage="none"))
         assert np.array_equal(got[0], base[0]) and np.array_equal(got[1], base[1]), p
         assert np.array_equal(got[2].delta_history, base[2].delta_history)
+
+
+@pytest.mark.gpu
+def test_packed_shards_match_single_rank():
+    """Symmetric packed storage across ranks (super-row shards, partial y
+    summed in rank order): same labels and iteration count as one rank,
+    embedding within 1e-6 relative L1 (only the summation grouping changes),
+    deterministic across repeats, forced iterations and a second run."""
+    d = gaussian_blobs(6000, 64, 6, seed=5)
+    kind, params = GaussianRbf(4.0), PicParams(k=6)
+    single = cluster(d, kind, params, config=KernelConfig(), seed=4)
+    for p in (2, 3, 5):
+        cfg = KernelConfig(p=p, virtual_ranks=True)
+        a = cluster(d, kind, params, config=cfg, seed=4)
+        b = cluster(d, kind, params, config=cfg, seed=4)
+        assert np.array_equal(a[0], single[0]), p
+        assert a[2].iterations_run == single[2].iterations_run, p
+        assert np.abs(a[1] - single[1]).sum() / np.abs(single[1]).sum() <= 1e-6, p
+        assert np.array_equal(a[1], b[1]) and np.array_equal(a[0], b[0]), p
+    forced = PicParams(k=6, epsilon=5e-324, max_iterations=8)
+    f1 = cluster(d, kind, forced, config=KernelConfig(), seed=4)
+    f3 = cluster(d, kind, forced, config=KernelConfig(p=3, virtual_ranks=True), seed=4)
+    assert f3[2].iterations_run == 8 and not f3[2].converged
+    assert np.abs(f3[1] - f1[1]).sum() / np.abs(f1[1]).sum() <= 1e-6
+
+
+@pytest.mark.gpu
+def test_packed_shard_ranges_cover_the_triangle():
+    """gpic_packed_shard_range: 512-row aligned, contiguous, covering, and
+    balanced by stored tiles; too many ranks for the rows is rejected."""
+    from paper_1604_02700_b200 import _lib
+    import ctypes as C
+
+    L = _lib.lib()
+    for n, P in ((6000, 2), (6000, 5), (100000, 8), (1025, 2)):
+        lo_prev, tiles = 0, []
+        for r in range(P):
+            lo, hi = C.c_int64(), C.c_int64()
+            assert L.gpic_packed_shard_range(n, P, r, C.byref(lo), C.byref(hi)) == 0
+            assert lo.value == lo_prev and lo.value % 512 == 0 and hi.value > lo.value
+            tiles.append(L.gpic_packed_shard_tiles(n, lo.value, hi.value))
+            lo_prev = hi.value
+        assert lo_prev == n
+        assert sum(tiles) == L.gpic_packed_tiles(n)
+        if n >= 100000:
+            assert max(tiles) / min(tiles) < 1.15, tiles  # 512-row granularity
+    lo, hi = C.c_int64(), C.c_int64()
+    assert L.gpic_packed_shard_range(1000, 3, 0, C.byref(lo), C.byref(hi)) != 0
