@@ -229,6 +229,7 @@ int gpic_power_iterate(const float* d_a, int64_t lda, const double* d_deg, int64
   int rc = run_power_loop(d_a, lda, d_deg, n, y, part, d_v64, d_v32, d_delta_hist, d_ctl,
                           max_iter, s);
   if (rc != GPIC_OK) return rc;
+  note_loop_iterations(1);  // asynchronous: at least one iteration ran
   launch_copy_result(d_v64, n, d_v64_out, d_ctl, s);
   GPIC_CUDA_TRY(cudaGetLastError());
   return GPIC_OK;
@@ -540,6 +541,7 @@ int cluster_impl(const double* d_x, int64_t n, int32_t d, double sigma, int32_t 
   gpic_ctl h;
   rc = gpic_ctl_read(ws.ctl, &h, stream);
   if (rc) return rc;
+  note_loop_iterations(h.iter);
   rc = status_from_ctl(h, d);
   if (rc) return rc;
   rc = launch_kmeans1d(d_v, n, k, first_index, h_uniforms, 100, 1e-12, d_labels, ws.kscratch,

@@ -406,6 +406,7 @@ int gpic_comm_iterate(gpic_comm* c, const gpic_shard* shards, int32_t nlocal, do
                                   cudaMemcpyDeviceToHost, s));
   }
   GPIC_CUDA_TRY(cudaStreamSynchronize(s));
+  note_loop_iterations(h_ctl[0].iter);
   for (int li = 0; li < nlocal; ++li)
     if (h_ctl[li].status != GPIC_OK) return h_ctl[li].status;
   return GPIC_OK;

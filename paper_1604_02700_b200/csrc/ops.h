@@ -200,6 +200,8 @@ struct ShardLoop {
 // Capture max_iter iterations of every local shard into one CUDA graph
 // (virtual ranks: all GEMVs of an iteration precede all tails) and launch it.
 int run_power_loops(ShardLoop* shards, int nlocal, int64_t n, int32_t max_iter, cudaStream_t s);
+// launch accounting for the conditional loop graph: iterations x kernels
+void note_loop_iterations(int32_t iters);
 int run_power_loop(const float* a, int64_t lda, const double* deg, int64_t n, double* y,
                    double* redpart, double* v64, float* v32, double* hist, gpic_ctl* ctl,
                    int32_t max_iter, cudaStream_t s);

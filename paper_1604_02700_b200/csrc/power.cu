@@ -281,10 +281,23 @@ constexpr size_t kGraphCache = 8;
 
 }  // namespace
 
-// The whole loop as one CUDA graph: max_iter copies of, per iteration,
-// every local shard's GEMV (+ fused peer stores / epoch publish), then every
-// local shard's [peer wait] + tau + normalise. Kernels after convergence
-// exit at their first instruction, so the replay needs no host decisions.
+namespace {
+// WHILE-node condition: another iteration unless the stop rule fired
+__global__ void loop_cond_kernel(cudaGraphConditionalHandle h, const gpic_ctl* ctl) {
+  cudaGraphSetConditional(h, *(volatile const int32_t*)&ctl->stop ? 0u : 1u);
+}
+}  // namespace
+
+unsigned long long g_loop_per_iter = 0;  // kernels of one iteration of the last loop graph
+void note_loop_iterations(int32_t iters) { g_launches += (unsigned long long)iters * g_loop_per_iter; }
+
+// The whole loop as one CUDA graph: a conditional WHILE node whose body is
+// one iteration — every local shard's GEMV (+ fused peer stores / epoch
+// publish), then every local shard's [peer wait] + tau + normalise — and a
+// one-thread kernel that sets the condition from the stop flag. The device
+// decides when to stop; the graph replays no idle iterations (before:
+// max_iter unrolled copies whose kernels exited at once, ~14 us per
+// iteration of launch overhead after convergence).
 int run_power_loops(ShardLoop* shards, int nlocal, int64_t n, int32_t max_iter, cudaStream_t s) {
   if (nlocal < 1 || nlocal > kMaxRanks) return fail(GPIC_E_INVALID, "bad local shard count");
   GraphKey key;
@@ -315,8 +328,20 @@ int run_power_loops(ShardLoop* shards, int nlocal, int64_t n, int32_t max_iter, 
     GraphEntry ent;
     ent.key = key;
     const unsigned long long before = g_launches;
-    GPIC_CUDA_TRY(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
-    for (int t = 0; t < max_iter; ++t) {
+    GPIC_CUDA_TRY(cudaGraphCreate(&graph, 0));
+    cudaGraphConditionalHandle cond;
+    GPIC_CUDA_TRY(cudaGraphConditionalHandleCreate(&cond, graph, 1, cudaGraphCondAssignDefault));
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = cond;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t loop_node;
+    GPIC_CUDA_TRY(cudaGraphAddNode(&loop_node, graph, nullptr, 0, &cp));
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    GPIC_CUDA_TRY(cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0,
+                                                cudaStreamCaptureModeThreadLocal));
+    for (int t = 0; t < 1; ++t) {
       for (int i = 0; i < nlocal; ++i) {
         const ShardLoop& L = shards[i];
         if (L.mode == kLoopPacked) {
@@ -332,7 +357,7 @@ int run_power_loops(ShardLoop* shards, int nlocal, int64_t n, int32_t max_iter, 
           if (rc) {
             cudaGraph_t junk;
             cudaStreamEndCapture(cs, &junk);
-            if (junk) cudaGraphDestroy(junk);
+            cudaGraphDestroy(graph);
             return rc;
           }
         } else {
@@ -351,7 +376,10 @@ int run_power_loops(ShardLoop* shards, int nlocal, int64_t n, int32_t max_iter, 
                               L.hist, L.ctl, cs);
       }
     }
-    GPIC_CUDA_TRY(cudaStreamEndCapture(cs, &graph));
+    loop_cond_kernel<<<1, 1, 0, cs>>>(cond, shards[nlocal - 1].ctl);
+    count_launch();
+    cudaGraph_t captured;
+    GPIC_CUDA_TRY(cudaStreamEndCapture(cs, &captured));
     GPIC_CUDA_TRY(cudaGraphInstantiate(&ent.exec, graph, 0));
     GPIC_CUDA_TRY(cudaGraphDestroy(graph));
     ent.launches = g_launches - before;
@@ -364,7 +392,7 @@ int run_power_loops(ShardLoop* shards, int nlocal, int64_t n, int32_t max_iter, 
     hit = &g_graphs.back();
   }
   GPIC_CUDA_TRY(cudaGraphLaunch(hit->exec, cs));
-  g_launches += hit->launches;
+  g_loop_per_iter = hit->launches;  // callers add iterations x this once they know the count
   if (own) {
     cudaEvent_t ev;
     GPIC_CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
