@@ -13,6 +13,7 @@
 // Every reduction has a fixed shape over GLOBAL indices, so results are
 // bitwise independent of how rows are sharded across ranks.
 #include <cfloat>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <vector>
@@ -275,6 +276,7 @@ struct GraphEntry {
   GraphKey key;
   cudaGraphExec_t exec;
   unsigned long long launches;
+  bool unrolled;
 };
 std::vector<GraphEntry> g_graphs;
 constexpr size_t kGraphCache = 8;
@@ -328,20 +330,27 @@ int run_power_loops(ShardLoop* shards, int nlocal, int64_t n, int32_t max_iter, 
     GraphEntry ent;
     ent.key = key;
     const unsigned long long before = g_launches;
+    // GPIC_LOOP_UNROLLED=1: max_iter unrolled copies instead of the WHILE
+    // node (Nsight Compute does not trace kernels inside conditional graph
+    // bodies; the profiling scripts use this for the launch list)
+    const bool unrolled = getenv("GPIC_LOOP_UNROLLED") != nullptr;
     GPIC_CUDA_TRY(cudaGraphCreate(&graph, 0));
-    cudaGraphConditionalHandle cond;
-    GPIC_CUDA_TRY(cudaGraphConditionalHandleCreate(&cond, graph, 1, cudaGraphCondAssignDefault));
-    cudaGraphNodeParams cp = {};
-    cp.type = cudaGraphNodeTypeConditional;
-    cp.conditional.handle = cond;
-    cp.conditional.type = cudaGraphCondTypeWhile;
-    cp.conditional.size = 1;
-    cudaGraphNode_t loop_node;
-    GPIC_CUDA_TRY(cudaGraphAddNode(&loop_node, graph, nullptr, 0, &cp));
-    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    cudaGraphConditionalHandle cond{};
+    cudaGraph_t body = graph;
+    if (!unrolled) {
+      GPIC_CUDA_TRY(cudaGraphConditionalHandleCreate(&cond, graph, 1, cudaGraphCondAssignDefault));
+      cudaGraphNodeParams cp = {};
+      cp.type = cudaGraphNodeTypeConditional;
+      cp.conditional.handle = cond;
+      cp.conditional.type = cudaGraphCondTypeWhile;
+      cp.conditional.size = 1;
+      cudaGraphNode_t loop_node;
+      GPIC_CUDA_TRY(cudaGraphAddNode(&loop_node, graph, nullptr, 0, &cp));
+      body = cp.conditional.phGraph_out[0];
+    }
     GPIC_CUDA_TRY(cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0,
                                                 cudaStreamCaptureModeThreadLocal));
-    for (int t = 0; t < 1; ++t) {
+    for (int t = 0; t < (unrolled ? max_iter : 1); ++t) {
       for (int i = 0; i < nlocal; ++i) {
         const ShardLoop& L = shards[i];
         if (L.mode == kLoopPacked) {
@@ -376,13 +385,16 @@ int run_power_loops(ShardLoop* shards, int nlocal, int64_t n, int32_t max_iter, 
                               L.hist, L.ctl, cs);
       }
     }
-    loop_cond_kernel<<<1, 1, 0, cs>>>(cond, shards[nlocal - 1].ctl);
-    count_launch();
+    if (!unrolled) {
+      loop_cond_kernel<<<1, 1, 0, cs>>>(cond, shards[nlocal - 1].ctl);
+      count_launch();
+    }
     cudaGraph_t captured;
     GPIC_CUDA_TRY(cudaStreamEndCapture(cs, &captured));
     GPIC_CUDA_TRY(cudaGraphInstantiate(&ent.exec, graph, 0));
     GPIC_CUDA_TRY(cudaGraphDestroy(graph));
     ent.launches = g_launches - before;
+    ent.unrolled = unrolled;
     g_launches = before;
     if (g_graphs.size() >= kGraphCache) {
       cudaGraphExecDestroy(g_graphs.front().exec);
@@ -392,7 +404,12 @@ int run_power_loops(ShardLoop* shards, int nlocal, int64_t n, int32_t max_iter, 
     hit = &g_graphs.back();
   }
   GPIC_CUDA_TRY(cudaGraphLaunch(hit->exec, cs));
-  g_loop_per_iter = hit->launches;  // callers add iterations x this once they know the count
+  if (hit->unrolled) {
+    g_launches += hit->launches;
+    g_loop_per_iter = 0;
+  } else {
+    g_loop_per_iter = hit->launches;  // callers add iterations x this once they know the count
+  }
   if (own) {
     cudaEvent_t ev;
     GPIC_CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));

@@ -4,10 +4,10 @@
 OUT=gpurun_out
 TAG=${TAG:-r1}
 STORAGE=${STORAGE:-packed}
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv \
+GPIC_LOOP_UNROLLED=1 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv \
   --log-file $OUT/launches_${TAG}_cfg3_${STORAGE}.csv python bench.py --config 3 --steps 1 --warmup 0 \
   --no-cpu-baseline --e2e-steps 1 --gemv-reps 1 --storage $STORAGE > $OUT/launches_${TAG}.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"sym_gemv|gemv_bulk" -s 3 -c 1 \
+GPIC_LOOP_UNROLLED=1 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"sym_gemv|gemv_bulk" -s 3 -c 1 \
   -o $OUT/prof_${TAG}_gemv_cfg3_${STORAGE} -f python bench.py --config 3 --steps 1 --warmup 0 \
   --no-cpu-baseline --e2e-steps 0 --gemv-reps 1 --storage $STORAGE > $OUT/prof_${TAG}_gemv.log 2>&1
 TCCFG=${TCCFG:-3}
