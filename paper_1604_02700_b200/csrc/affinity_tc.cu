@@ -154,18 +154,6 @@ struct TcArgs {
   float* colpart;       // matvec sym: [packed (row block, column tile)][128] fp32
 };
 
-// fixed-shape pairwise sum of 32 values (short dependency chains)
-__device__ __forceinline__ float tree_sum32(const float (&v)[32]) {
-  float t[16];
-#pragma unroll
-  for (int j = 0; j < 16; ++j) t[j] = v[2 * j] + v[2 * j + 1];
-#pragma unroll
-  for (int w = 8; w >= 1; w >>= 1)
-#pragma unroll
-    for (int j = 0; j < w; ++j) t[j] = t[2 * j] + t[2 * j + 1];
-  return t[0];
-}
-
 __host__ __device__ inline int64_t packed_items(int64_t nrt, int64_t nct, int mb) {
   return nrt * nct - (int64_t)mb * nrt * (nrt - 1) / 2;
 }

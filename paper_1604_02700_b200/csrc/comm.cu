@@ -1,9 +1,15 @@
-// Row-sharded multi-rank power iteration.
+// Multi-rank power iteration, two shard storages.
 //
-// Rank r owns rows [row_lo_r, row_lo_r + rows_r) of A (built by
-// gpic_affinity_rbf with that row range; no communication). The only
-// exchanges are (1) the degree slices, once, for v0 = d / sum(d), and (2) the
-// y slices every iteration. Both are FUSED into the producing kernel: the
+// Packed symmetric shards (GPIC_STORAGE_PACKED): rank r owns 512-row
+// super-rows and stores the upper-triangle tiles of its rows; its GEMV
+// yields a PARTIAL y (and, once, partial degrees) that it P2P-stores into its
+// slot of every rank's region; each rank sums the P slots in rank order
+// (slot_combine) before the tail. Deterministic for a given P.
+//
+// Dense row shards: rank r owns rows [row_lo_r, row_lo_r + rows_r) of A
+// (built by gpic_affinity_rbf with that row range; no communication). The
+// only exchanges are (1) the degree slices, once, for v0 = d / sum(d), and
+// (2) the y slices every iteration. Both are FUSED into the producing kernel: the
 // GEMV's epilogue stores each finished row straight into every rank's y
 // buffer (NVLink P2P stores through CUDA-IPC mappings of the peers' buffers),
 // then its last CTA release-stores an epoch into every rank's flag slot; the
@@ -14,8 +20,9 @@
 //
 // Virtual ranks: the same code with all P shards in one process on one
 // device (peer pointers are ordinary device pointers), which is how the
-// multi-rank path is exercised on a single GPU: results are bitwise equal to
-// the single-rank run for any P (every reduction has a fixed global shape).
+// multi-rank path is exercised on a single GPU: with dense row shards the
+// results are bitwise equal to the single-rank run for any P (every
+// reduction has a fixed global shape).
 #include <algorithm>
 #include <cstdio>
 #include <cstring>

@@ -114,17 +114,6 @@ struct Shared {
   int flag;
 };
 
-__device__ double block_sum(double v, Shared& sh) {
-  v = warp_sum_f64(v);
-  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-  __syncthreads();
-  if (l == 0) sh.red_d[w] = v;
-  __syncthreads();
-  double t = 0.0;
-  for (int i = 0; i < kWarps; ++i) t += sh.red_d[i];
-  return t;
-}
-
 // argmax of val with lowest index on ties (np.argmax semantics).
 __device__ long long block_argmax(double val, long long idx, Shared& sh) {
   for (int o = 16; o > 0; o >>= 1) {
@@ -877,6 +866,8 @@ int set_kmeans_attributes() {
   GPIC_CUDA_TRY(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev));
   GPIC_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kmeans_grid_kernel, kThreads, shm));
   g_grid_ctas = coop && per_sm > 0 ? (sms < kGridMaxCtas ? sms : kGridMaxCtas) : 0;
+  if (const char* e = getenv("GPIC_KMEANS_CTAS"))  // measurement: grid size of the whole-GPU path
+    if (g_grid_ctas > 0 && atoi(e) > 0 && atoi(e) < g_grid_ctas) g_grid_ctas = atoi(e);
   done = true;
   return GPIC_OK;
 }

@@ -101,6 +101,27 @@ __global__ void bulk_store_kernel(char* __restrict__ a, size_t bytes, uint32_t c
   asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
+// 4 KB "boxes" written as 32 rows x 128 B with a 512 B row pitch (the packed
+// tile's 32 x 32 fp32 box layout), 16 boxes per 64 KB tile, by 128 threads
+// with 8-byte stores; or contiguous 4 KB per box (box-major layout)
+__global__ void box_store_kernel(float* __restrict__ a, size_t tiles, int strided) {
+  const int t = threadIdx.x;
+  const float val = (float)t;
+  for (size_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+    float* base = a + tile * 16384;
+    for (int box = 0; box < 16; ++box) {
+      const int q = box >> 2, ch = box & 3;
+      // 1024 floats per box, 8 per thread (two float4)
+      for (int k = 0; k < 2; ++k) {
+        const int e = (k * 128 + t) * 4;  // element within the box
+        const int r = e >> 5, c = e & 31;
+        float* dst = strided ? base + (q * 32 + r) * 128 + ch * 32 + c : base + box * 1024 + e;
+        __stcs(reinterpret_cast<float4*>(dst), make_float4(val, val, val, val));
+      }
+    }
+  }
+}
+
 int main(int argc, char** argv) {
   const double gb = argc > 1 ? atof(argv[1]) : 20.0;
   const size_t bytes = (size_t)(gb * 1e9) / (1 << 16) * (1 << 16);
@@ -171,6 +192,11 @@ int main(int argc, char** argv) {
     timeit(nm, [&] { bulk_store_kernel<<<sms, 128, chunk + 256>>>(a, bytes, chunk, 16); });
   }
   timeit("cudaMemsetAsync (write)", [&] { cudaMemsetAsync(a, 1, bytes); });
+  for (int strided : {1, 0}) {
+    char nm[64];
+    snprintf(nm, sizeof nm, "box stores %s (write)", strided ? "32x128B pitch 512B" : "contiguous 4KB");
+    timeit(nm, [&] { box_store_kernel<<<sms * 8, 128>>>((float*)a, bytes / 65536, strided); });
+  }
   printf("err: %s\n", cudaGetErrorString(cudaGetLastError()));
   return 0;
 }
