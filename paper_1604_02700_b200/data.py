@@ -57,8 +57,10 @@ def check_labels(d: DataSet) -> None:
         return
     if d.labels.shape != (d.n,):
         raise LabelLengthMismatch(d.n, int(d.labels.size))
-    ids = np.unique(d.labels)
-    if not np.array_equal(ids, np.arange(ids.size)):
+    # np.unique(labels) == arange(k) without the O(n log n) sort: ids start
+    # at 0 and every id up to the maximum occurs
+    if d.labels.size and (d.labels.min() != 0 or
+                          not np.bincount(d.labels, minlength=int(d.labels.max()) + 1).all()):
         raise DataError("class ids must be contiguous integers starting at 0")
 
 
