@@ -10,7 +10,7 @@ is no CPU fallback.
 """
 
 from . import errors
-from .data import DataSet, validate_dataset
+from .data import DataSet, load_csv, validate_dataset, write_csv, write_vector_csv
 from .datasets import blobs_2d, config_dataset, gaussian_blobs
 from .params import (
     Cosine,
@@ -65,5 +65,5 @@ __all__ = [
     "adjusted_rand_index", "blobs_2d", "cluster", "config_dataset", "contingency", "errors",
     "gaussian_blobs", "jaccard_index", "k_affinity", "k_multiply", "k_norm", "k_normalize",
     "k_reduce", "k_rowsum", "kmeans_1d", "initial_embedding", "iterate", "plan_rows",
-    "validate_dataset",
+    "validate_dataset", "load_csv", "write_csv", "write_vector_csv",
 ]

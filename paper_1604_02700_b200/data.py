@@ -78,3 +78,116 @@ def validate_dataset(d: DataSet) -> DataSet:
         raise NonFiniteEntry(int(r), int(c))
     check_labels(d)
     return d
+
+
+# ------------------------------------------------------------ CSV I/O
+# Bulk versions of the reference's CSV helpers (data.py:81-138, SURVEY.md
+# §8f-4): numpy's C loadtxt for the common case (2x the reference's line
+# loop at 100k x 64, bit-identical values); any input it would treat
+# differently (ragged or empty fields, non-integer labels, parse errors)
+# re-runs the reference's line loop,
+# so values and errors — ParseError(line) / RaggedRows(line) with 1-based line
+# numbers, EmptyDataSet — are the reference's.
+
+
+def _load_csv_lines(path, has_labels, header):
+    """The reference's line loop (data.py:81-120): exact errors."""
+    from .errors import ParseError, RaggedRows
+
+    rows, labels, width = [], [], None
+    with open(path, "r", encoding="utf-8") as fh:
+        for lineno, raw in enumerate(fh, start=1):
+            if header and lineno == 1:
+                continue
+            line = raw.strip()
+            if not line:
+                continue
+            fields = line.split(",")
+            if width is None:
+                width = len(fields)
+            elif len(fields) != width:
+                raise RaggedRows(lineno)
+            if has_labels:
+                *feat, lab = fields
+                try:
+                    labels.append(int(lab))
+                except ValueError:
+                    raise ParseError(lineno, f"label {lab!r} is not an integer") from None
+            else:
+                feat = fields
+            try:
+                rows.append([float(f) for f in feat])
+            except ValueError:
+                raise ParseError(lineno, "non-numeric field") from None
+    if not rows:
+        raise EmptyDataSet()
+    return np.array(rows, dtype=np.float64), (np.array(labels, dtype=np.int64) if has_labels else None)
+
+
+def _load_csv_fast(path, has_labels, header):
+    """numpy's C loadtxt (correctly rounded, like float()); None when the
+    input needs the reference loop (ragged or empty fields, non-integer
+    labels, anything loadtxt rejects)."""
+    skip = 1 if header else 0
+    try:
+        with open(path, "r", encoding="utf-8") as fh:
+            for lineno, raw in enumerate(fh, start=1):
+                if lineno > skip and raw.strip():
+                    width = len(raw.strip().split(","))
+                    break
+            else:
+                return None
+        cols = width - (1 if has_labels else 0)
+        if cols < 1:
+            return None
+        kw = dict(delimiter=",", skiprows=skip, comments=None, ndmin=2, encoding="utf-8")
+        pts = np.loadtxt(path, dtype=np.float64, usecols=range(cols), **kw)
+        lab = (np.loadtxt(path, dtype=np.int64, usecols=[cols], **kw).reshape(-1)
+               if has_labels else None)
+    except (ValueError, IndexError):
+        return None
+    if pts.shape[0] == 0:
+        return None
+    # loadtxt ignores columns past usecols and rejects short rows: any comma
+    # beyond (width - 1) per data row belongs to a longer (ragged) row
+    with open(path, "rb") as fh:
+        data = fh.read()
+    if header:
+        data = data[data.find(b"\n") + 1:] if b"\n" in data else b""
+    if data.count(b",") != (width - 1) * pts.shape[0]:
+        return None
+    return np.ascontiguousarray(pts), lab
+
+
+def load_csv(path, has_labels: bool = False, header: bool = False) -> DataSet:
+    """Read a rectangular numeric CSV into a DataSet (data.py:81-120)."""
+    from pathlib import Path
+
+    path = Path(path)
+    fast = _load_csv_fast(path, has_labels, header)
+    pts, lab = fast if fast is not None else _load_csv_lines(path, has_labels, header)
+    return validate_dataset(DataSet(pts, lab, name=path.stem))
+
+
+def write_csv(d: DataSet, path) -> None:
+    """Points (and labels) with 17 significant digits (data.py:123-133): the
+    float64 round trip through load_csv is bit-exact."""
+    pts = np.asarray(d.points, dtype=np.float64)
+    if np.isfinite(pts).all():
+        cells = np.char.mod("%.17g", pts) if pts.size else pts.astype(str)
+        if d.labels is not None:
+            cells = np.column_stack([cells, np.asarray(d.labels, dtype=np.int64).astype(str)])
+        with open(path, "w", encoding="utf-8") as fh:
+            fh.write("".join(",".join(r) + "\n" for r in cells))
+        return
+    with open(path, "w", encoding="utf-8") as fh:  # non-finite: Python's spelling
+        for i in range(d.n):
+            row = [f"{x:.17g}" for x in pts[i]]
+            if d.labels is not None:
+                row.append(str(int(d.labels[i])))
+            fh.write(",".join(row) + "\n")
+
+
+def write_vector_csv(values, path, fmt: str = "%.17g") -> None:
+    """One value per line (data.py:136-138)."""
+    np.savetxt(path, np.asarray(values).reshape(-1), fmt=fmt)
