@@ -207,3 +207,21 @@ def test_packed_shard_ranges_cover_the_triangle():
             assert max(tiles) / min(tiles) < 1.15, tiles  # 512-row granularity
     lo, hi = C.c_int64(), C.c_int64()
     assert L.gpic_packed_shard_range(1000, 3, 0, C.byref(lo), C.byref(hi)) != 0
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("m,kind_name", [(100, "rbf"), (20, "cosine")])
+def test_packed_shards_other_shapes_and_kinds(m, kind_name):
+    """Packed shards with 128-row affinity blocks (d > 64) and with the
+    cosine kind: labels and iterations equal to one rank."""
+    from paper_1604_02700_b200 import Cosine
+
+    d = gaussian_blobs(5000, m, 4, seed=11)
+    kind = GaussianRbf(float(np.sqrt(m) / 2)) if kind_name == "rbf" else Cosine()
+    params = PicParams(k=4)
+    single = cluster(d, kind, params, config=KernelConfig(), seed=2)
+    for p in (2, 4):
+        got = cluster(d, kind, params, config=KernelConfig(p=p, virtual_ranks=True), seed=2)
+        assert np.array_equal(got[0], single[0]), p
+        assert got[2].iterations_run == single[2].iterations_run, p
+        assert np.abs(got[1] - single[1]).sum() / np.abs(single[1]).sum() <= 1e-6, p
