@@ -173,6 +173,12 @@ int gpic_reduce_sum(const double* d_v, int64_t n, double* d_out, void* d_work, v
  * scale = d_inv_deg (fp64, may be NULL for 1). */
 int gpic_matvec(const float* d_a, int64_t lda, int64_t rows, int64_t n, const float* d_v,
                 const double* d_row_scale, double* d_y, void* stream);
+/* check_row_stochastic (serial.py:63-74) on an fp64 row-major matrix
+ * (leading dimension ldw doubles): per-row sum, min and max into d_sum /
+ * d_min / d_max (rows doubles each); NaN propagates. The caller applies the
+ * reference's tolerance (row sums within 1e-9 of 1, entries in [0, 1]). */
+int gpic_row_stats(const double* d_w, int64_t rows, int64_t n, int64_t ldw, double* d_sum,
+                   double* d_min, double* d_max, void* stream);
 /* k_multiply on PACKED symmetric tiles (gpic_packed_tiles(n) tiles of
  * 128 x 128 fp32, upper triangle): y = (A v) * scale_i. d_v holds
  * gpic_vector_pitch(n) floats (zero padded); d_rowp / d_colp hold

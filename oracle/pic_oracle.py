@@ -164,6 +164,26 @@ def resolved_epsilon(epsilon, n: int) -> float:
     return float(epsilon) if epsilon is not None else 1e-5 / n
 
 
+ROW_SUM_TOL = 1e-9  # serial.py:20
+
+
+def row_stochastic_violation(w: np.ndarray):
+    """check_row_stochastic (serial.py:63-74) as a verdict, not an exception.
+
+    Returns None when every row sums to 1 within 1e-9 and entries lie in
+    [0, 1] (1e-12 slack); else ("row", i, sum_i) for the worst row, or
+    ("range", None, None).
+    """
+    w = np.asarray(w, dtype=np.float64)
+    sums = w.sum(axis=1)
+    if np.max(np.abs(sums - 1.0)) > ROW_SUM_TOL:
+        bad = int(np.argmax(np.abs(sums - 1.0)))
+        return ("row", bad, float(sums[bad]))
+    if w.min() < -1e-12 or w.max() > 1.0 + 1e-12:
+        return ("range", None, None)
+    return None
+
+
 def power_iteration(w: np.ndarray, v0: np.ndarray, eps: float, max_iterations: int):
     """v <- W v / |W v|_1 with the acceleration stop (serial.py:104-128).
 

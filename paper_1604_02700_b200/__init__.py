@@ -53,7 +53,8 @@ def __getattr__(name):
     # stage functions live in .gpu (imported lazily so CPU-only hosts can
     # import the package, e.g. for the oracle tests)
     if name in {"k_affinity", "k_rowsum", "k_normalize", "k_reduce", "k_norm", "k_multiply",
-                "initial_embedding", "iterate", "gpu"}:
+                "initial_embedding", "iterate", "power_iterate", "check_row_stochastic", "build_affinity", "degree",
+                "normalize", "initial_vector", "gpu"}:
         g = _gpu()
         return g if name == "gpu" else getattr(g, name)
     raise AttributeError(name)
@@ -64,6 +65,7 @@ __all__ = [
     "KernelConfig", "PartitionPlan", "PicParams", "PicTrace", "SimilarityKind",
     "adjusted_rand_index", "blobs_2d", "cluster", "config_dataset", "contingency", "errors",
     "gaussian_blobs", "jaccard_index", "k_affinity", "k_multiply", "k_norm", "k_normalize",
-    "k_reduce", "k_rowsum", "kmeans_1d", "initial_embedding", "iterate", "plan_rows",
+    "k_reduce", "k_rowsum", "kmeans_1d", "initial_embedding", "iterate", "power_iterate",
+    "check_row_stochastic", "build_affinity", "degree", "normalize", "initial_vector", "plan_rows",
     "validate_dataset", "load_csv", "write_csv", "write_vector_csv",
 ]

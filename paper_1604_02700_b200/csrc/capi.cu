@@ -321,6 +321,15 @@ int gpic_matvec(const float* d_a, int64_t lda, int64_t rows, int64_t n, const fl
   return GPIC_OK;
 }
 
+int gpic_row_stats(const double* d_w, int64_t rows, int64_t n, int64_t ldw, double* d_sum,
+                   double* d_min, double* d_max, void* stream) {
+  if (rows < 1 || n < 1) return fail(GPIC_E_EMPTY, "empty matrix");
+  if (ldw < n) return fail(GPIC_E_INVALID, "ldw must be >= n");
+  launch_row_stats(d_w, rows, n, ldw, d_sum, d_min, d_max, static_cast<cudaStream_t>(stream));
+  GPIC_CUDA_TRY(cudaGetLastError());
+  return GPIC_OK;
+}
+
 int64_t gpic_packed_tiles(int64_t n) { return n < 1 ? -1 : packed_tiles(n); }
 int64_t gpic_sym_partial_floats(int64_t n) { return n < 1 ? -1 : sym_partial_floats(n); }
 

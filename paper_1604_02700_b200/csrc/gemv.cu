@@ -138,6 +138,39 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// check_row_stochastic (serial.py:63-74) on an fp64 matrix: per-row sum,
+// min and max, one warp per row (coalesced lane-strided reads, fixed
+// butterfly, so a row's result depends only on that row). NaN propagates
+// into all three, as numpy's sum/min/max would.
+__global__ void __launch_bounds__(256) row_stats_kernel(const double* __restrict__ w,
+                                                        int64_t rows, int64_t n, int64_t ldw,
+                                                        double* sum, double* mn, double* mx) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (row >= rows) return;
+  const double* r = w + row * ldw;
+  double s = 0.0, lo = INFINITY, hi = -INFINITY;
+  for (int64_t j = lane; j < n; j += 32) {
+    const double x = __ldcs(r + j);
+    s += x;
+    lo = (x < lo || x != x) ? x : lo;
+    hi = (x > hi || x != x) ? x : hi;
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    s += __shfl_xor_sync(0xffffffffu, s, o);
+    const double l2 = __shfl_xor_sync(0xffffffffu, lo, o);
+    const double h2 = __shfl_xor_sync(0xffffffffu, hi, o);
+    lo = (l2 < lo || l2 != l2) ? l2 : lo;
+    hi = (h2 > hi || h2 != h2) ? h2 : hi;
+  }
+  if (lane == 0) {
+    sum[row] = s;
+    mn[row] = lo;
+    mx[row] = hi;
+  }
+}
+
 }  // namespace
 
 static int g_num_sms = 0;
@@ -159,6 +192,13 @@ void launch_gemv(const float* a, int64_t lda, int64_t rows, int64_t row_lo, cons
   const int64_t groups = (rows + kRG - 1) / kRG;
   const int grid = (int)(groups < num_sms ? groups : num_sms);
   gemv_bulk_kernel<<<grid, kThreads, kSmem, s>>>(a, lda, rows, row_lo, v32, deg, pt, ctl);
+  count_launch();
+}
+
+void launch_row_stats(const double* w, int64_t rows, int64_t n, int64_t ldw, double* sum,
+                      double* mn, double* mx, cudaStream_t s) {
+  const int64_t grid = (rows + 7) / 8;
+  row_stats_kernel<<<(unsigned)grid, 256, 0, s>>>(w, rows, n, ldw, sum, mn, mx);
   count_launch();
 }
 

@@ -122,6 +122,8 @@ void launch_scale_vector(const double* src, int64_t n, const double* tau, double
 void launch_scale_by(const double* src, int64_t n, double tau, double* dst, float* dst32,
                      int64_t f32_len, cudaStream_t s);
 void gemv_prepare();
+void launch_row_stats(const double* w, int64_t rows, int64_t n, int64_t ldw, double* sum,
+                      double* mn, double* mx, cudaStream_t s);
 void launch_gemv(const float* a, int64_t lda, int64_t rows, int64_t row_lo, const float* v32,
                  const double* deg, const PeerTable& pt, gpic_ctl* ctl, cudaStream_t s);
 void launch_peer_wait(const uint64_t* flags_self, int slot0, int count, uint64_t base,

@@ -267,20 +267,26 @@ def affinity_rows(prep: PreparedPoints, lo: int, hi: int, sigma: float, engine: 
 
 
 def k_rowsum(a, config: KernelConfig | None = None):
-    """Row sums = degrees (parallel.py:131-143). ZeroDegree(first row) if any <= 0."""
+    """Row sums = degrees (parallel.py:131-143). ZeroDegree(first row) if any <= 0.
+
+    A device block returns its fused degrees; a host fp64 matrix is summed in
+    fp64 on the device (gpic_row_stats), as the reference sums it.
+    """
     torch = _torch()
     if isinstance(a, DeviceAffinity):
         h = _read_ctl(a.ctl, a.a.device)
         _raise_ctl(h, a.d)
         return a.deg
+    wn = np.ascontiguousarray(np.asarray(a, dtype=np.float64))
+    if wn.ndim != 2 or wn.size == 0:
+        raise InvalidSpec(f"expected a non-empty matrix, got shape {wn.shape}")
+    rows, n = wn.shape
     dev = _device(config)
-    t, rows, n, lda = _as_device_matrix(a, dev)
-    ones = torch.zeros(lda, dtype=torch.float32, device=dev)
-    ones[:n] = 1.0
-    out = torch.empty(rows, dtype=torch.float64, device=dev)
-    _lib.check(_lib.lib().gpic_matvec(_ptr(t), lda, rows, n, _ptr(ones), None, _ptr(out),
-                                      _stream(dev)))
-    res = out.cpu().numpy()
+    t = torch.from_numpy(wn).to(dev)
+    stats = torch.empty((3, rows), dtype=torch.float64, device=dev)
+    _lib.check(_lib.lib().gpic_row_stats(_ptr(t), rows, n, n, _ptr(stats[0]), _ptr(stats[1]),
+                                         _ptr(stats[2]), _stream(dev)))
+    res = stats[0].cpu().numpy()
     bad = np.flatnonzero(res <= 0.0)
     if bad.size:
         raise ZeroDegree(int(bad[0]))
@@ -428,6 +434,80 @@ def iterate(w, v, params: PicParams, config: KernelConfig | None = None):
     _raise_ctl(h)
     trace = PicTrace(int(h.iter), hist[: h.iter].cpu().numpy(), bool(h.converged))
     return (out.cpu().numpy() if (was_np or v_np) else out), trace
+
+
+ROW_SUM_TOL = 1e-9  # serial.py:20
+
+
+def check_row_stochastic(w, config: KernelConfig | None = None):
+    """serial.py:63-74: every row of w sums to 1 within 1e-9, entries in [0, 1].
+
+    The fp64 matrix is scanned on the device (gpic_row_stats: per-row sum,
+    min, max); the verdict and the InvalidSpec messages follow the
+    reference (the worst row is named). Returns w as float64.
+    """
+    torch = _torch()
+    wn = np.ascontiguousarray(np.asarray(w, dtype=np.float64))
+    if wn.ndim != 2 or wn.shape[0] != wn.shape[1]:
+        raise InvalidSpec(f"expected a square matrix, got shape {wn.shape}")
+    n = wn.shape[0]
+    if n == 0:
+        raise InvalidSpec("expected a non-empty matrix")
+    dev = _device(config)
+    t = torch.from_numpy(wn).to(dev)
+    stats = torch.empty((3, n), dtype=torch.float64, device=dev)
+    _lib.check(_lib.lib().gpic_row_stats(_ptr(t), n, n, n, _ptr(stats[0]), _ptr(stats[1]),
+                                         _ptr(stats[2]), _stream(dev)))
+    sums, lo, hi = stats.cpu().numpy()
+    if np.max(np.abs(sums - 1.0)) > ROW_SUM_TOL:
+        bad = int(np.argmax(np.abs(sums - 1.0)))
+        raise InvalidSpec(f"row {bad} sums to {sums[bad]!r}, not 1")
+    if lo.min() < -1e-12 or hi.max() > 1.0 + 1e-12:
+        raise InvalidSpec("entries must lie in [0, 1]")
+    return wn
+
+
+def power_iterate(w, params: PicParams, v0, config: KernelConfig | None = None):
+    """serial.py:104-128: validate W row-stochastic, then the device power loop.
+
+    Same contract as the serial entry point: (v, PicTrace), v float64 of
+    length n. W is streamed in fp32 by the GEMV (DESIGN.md §2 tolerance).
+    A `NormalizedAffinity` (from `normalize`/`k_normalize`) is row-stochastic
+    by construction (D^-1 A with the degrees of the same A) and is not
+    re-scanned.
+    """
+    if not isinstance(w, (NormalizedAffinity, DeviceAffinity)):
+        w = check_row_stochastic(w, config)
+    return iterate(w, v0, params, config)
+
+
+# ---- serial-module names (affinity.py:107-127, serial.py:77-101) --------
+def build_affinity(d: DataSet, kind, config: KernelConfig | None = None) -> np.ndarray:
+    """affinity.py:107-110: the dense A (zero diagonal) as a host float64 array.
+
+    Computed by the same device engine as `k_affinity` (fp32 storage) and
+    copied out; use `k_affinity` to keep A on the device.
+    """
+    a = k_affinity(d, kind, config)
+    _raise_ctl(_read_ctl(a.ctl, a.a.device), a.d)
+    return a.a[:, : a.n].cpu().numpy().astype(np.float64)
+
+
+def degree(a, config: KernelConfig | None = None):
+    """affinity.py:113-119: row sums, ZeroDegree(first row) if any <= 0."""
+    return k_rowsum(a, config)
+
+
+def normalize(a, deg, config: KernelConfig | None = None):
+    """affinity.py:122-127: W = A / deg, as the folded `NormalizedAffinity`
+    view (no second n x n; `.numpy()` materialises it)."""
+    return k_normalize(a, deg, config)
+
+
+def initial_vector(deg, choice, config: KernelConfig | None = None):
+    """serial.py:77-101: "degree" -> deg / sum(deg) (device tree sum),
+    "uniform" -> 1/n, or a validated explicit vector."""
+    return initial_embedding(deg, PicParams(k=2, v0=choice), config)
 
 
 def kmeans_1d(values, params: KMeansParams, config: KernelConfig | None = None):

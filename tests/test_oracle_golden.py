@@ -161,3 +161,15 @@ def test_oracle_reproduces_reference_experiment2_runs():
             assert np.array_equal(labels, run["labels"]), (case["kind"], run["fraction"])
             assert np.max(np.abs(v - run["v"])) <= 1e-12 * np.max(np.abs(run["v"]))
             assert len(deltas) == run["iterations"]
+
+
+def test_row_stochastic_verdict():
+    """check_row_stochastic (serial.py:63-74): np.ones((2,2)) is rejected
+    (test_serial.py:110-112); 1e-9 on the row sum; [0,1] with 1e-12 slack."""
+    assert po.row_stochastic_violation(np.ones((2, 2)))[:2] == ("row", 0)
+    assert po.row_stochastic_violation(np.eye(3)) is None
+    assert po.row_stochastic_violation(np.array([[0.5, 0.5], [0.5, 0.5 + 5e-10]])) is None
+    assert po.row_stochastic_violation(np.array([[0.5, 0.5], [0.5, 0.5 + 2e-9]]))[:2] == ("row", 1)
+    assert po.row_stochastic_violation(np.array([[1.5, -0.5], [0.0, 1.0]])) == ("range", None, None)
+    # NaN compares false everywhere, so the reference lets it through
+    assert po.row_stochastic_violation(np.array([[np.nan, 0.0], [0.0, 1.0]])) is None
