@@ -173,6 +173,16 @@ int gpic_reduce_sum(const double* d_v, int64_t n, double* d_out, void* d_work, v
  * scale = d_inv_deg (fp64, may be NULL for 1). */
 int gpic_matvec(const float* d_a, int64_t lda, int64_t rows, int64_t n, const float* d_v,
                 const double* d_row_scale, double* d_y, void* stream);
+/* App-B Gaussian blobs generated in device memory (the
+ * host generator is datasets.gaussian_blobs): row i of blob c
+ * (d_offsets[c] <= i < d_offsets[c+1], k+1 entries, d_offsets[k] = n) is
+ * d_centers[c] + noise * z + offset, z standard normal from Philox4x32-10
+ * keyed by `seed` (element pair p -> counter (p, 0, 0), Box-Muller on two
+ * 53-bit uniforms). d_x: n x d fp64 row-major; d_labels: n int64 or NULL.
+ * Deterministic in (seed, n, d, centres, offsets). */
+int gpic_generate_blobs(const double* d_centers, const int64_t* d_offsets, int64_t n, int32_t d,
+                        int32_t k, uint64_t seed, double noise, double offset, double* d_x,
+                        int64_t* d_labels, void* stream);
 /* check_row_stochastic (serial.py:63-74) on an fp64 row-major matrix
  * (leading dimension ldw doubles): per-row sum, min and max into d_sum /
  * d_min / d_max (rows doubles each); NaN propagates. The caller applies the

@@ -423,3 +423,56 @@ def matvec_threaded(w: np.ndarray, v: np.ndarray, p: int | None = None) -> np.nd
 
     _fan_out(work, row_ranges(w.shape[0], p), p)
     return out
+
+
+# --------------------------------------------------------------------------
+# Device App-B generator restated (csrc/generate.cu). The
+# reference has no such generator (its datasets.py:147-172 is 2-D only); this
+# pins the CUDA kernel's stream: Philox4x32-10 keyed by the seed, counter =
+# element-pair index, Box-Muller on two 53-bit uniforms.
+# --------------------------------------------------------------------------
+
+_M0, _M1 = np.uint64(0xD2511F53), np.uint64(0xCD9E8D57)
+_W0, _W1 = np.uint64(0x9E3779B9), np.uint64(0xBB67AE85)
+_MASK = np.uint64(0xFFFFFFFF)
+
+
+def philox4x32_10(ctr: np.ndarray, seed: int) -> np.ndarray:
+    """ctr: (m, 4) uint64 words < 2^32 -> (m, 4) output words."""
+    c0, c1, c2, c3 = (ctr[:, j].astype(np.uint64) for j in range(4))
+    k0 = np.uint64(seed & 0xFFFFFFFF)
+    k1 = np.uint64((seed >> 32) & 0xFFFFFFFF)
+    for _ in range(10):
+        p0 = _M0 * c0
+        p1 = _M1 * c2
+        hi0, lo0 = p0 >> np.uint64(32), p0 & _MASK
+        hi1, lo1 = p1 >> np.uint64(32), p1 & _MASK
+        c0, c1, c2, c3 = hi1 ^ c1 ^ k0, lo1, hi0 ^ c3 ^ k1, lo0
+        k0 = (k0 + _W0) & _MASK
+        k1 = (k1 + _W1) & _MASK
+    return np.stack([c0, c1, c2, c3], axis=1)
+
+
+def device_blobs(centers: np.ndarray, counts, seed: int, noise: float, offset: float):
+    """X (n x d) and labels exactly as gpic_generate_blobs lays them out."""
+    k, d = centers.shape
+    counts = np.asarray(counts, dtype=np.int64)
+    n = int(counts.sum())
+    total = n * d
+    pairs = (total + 1) // 2
+    p = np.arange(pairs, dtype=np.uint64)
+    ctr = np.zeros((pairs, 4), dtype=np.uint64)
+    ctr[:, 0] = p & _MASK
+    ctr[:, 1] = p >> np.uint64(32)
+    w = philox4x32_10(ctr, seed)
+    a = (w[:, 0] << np.uint64(21)) | (w[:, 1] >> np.uint64(11))
+    b = (w[:, 2] << np.uint64(21)) | (w[:, 3] >> np.uint64(11))
+    u1 = 1.0 - a.astype(np.float64) * 2.0 ** -53
+    u2 = b.astype(np.float64) * 2.0 ** -53
+    r = np.sqrt(-2.0 * np.log(u1))
+    z = np.empty(2 * pairs)
+    z[0::2] = r * np.cos(2.0 * np.pi * u2)
+    z[1::2] = r * np.sin(2.0 * np.pi * u2)
+    labels = np.repeat(np.arange(k, dtype=np.int64), counts)
+    x = centers[labels] + noise * z[:total].reshape(n, d) + offset
+    return x, labels

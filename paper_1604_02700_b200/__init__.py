@@ -54,7 +54,7 @@ def __getattr__(name):
     # import the package, e.g. for the oracle tests)
     if name in {"k_affinity", "k_rowsum", "k_normalize", "k_reduce", "k_norm", "k_multiply",
                 "initial_embedding", "iterate", "power_iterate", "check_row_stochastic", "build_affinity", "degree",
-                "normalize", "initial_vector", "gpu"}:
+                "normalize", "initial_vector", "generate_blobs", "cluster_points", "gpu"}:
         g = _gpu()
         return g if name == "gpu" else getattr(g, name)
     raise AttributeError(name)
@@ -67,5 +67,6 @@ __all__ = [
     "gaussian_blobs", "jaccard_index", "k_affinity", "k_multiply", "k_norm", "k_normalize",
     "k_reduce", "k_rowsum", "kmeans_1d", "initial_embedding", "iterate", "power_iterate",
     "check_row_stochastic", "build_affinity", "degree", "normalize", "initial_vector", "plan_rows",
+    "generate_blobs", "cluster_points",
     "validate_dataset", "load_csv", "write_csv", "write_vector_csv",
 ]

@@ -88,6 +88,7 @@ SIGNATURES = {
     "gpic_reduce_sum": (C.c_int, [P, I64, P, P, P]),
     "gpic_scale": (C.c_int, [P, I64, F64, P, P, I64, P]),
     "gpic_matvec": (C.c_int, [P, I64, I64, I64, P, P, P, P]),
+    "gpic_generate_blobs": (C.c_int, [P, P, I64, I32, I32, C.c_uint64, F64, F64, P, P, P]),
     "gpic_row_stats": (C.c_int, [P, I64, I64, I64, P, P, P, P]),
     "gpic_packed_tiles": (I64, [I64]),
     "gpic_vector_pitch": (I64, [I64]),

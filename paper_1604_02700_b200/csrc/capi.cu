@@ -321,6 +321,15 @@ int gpic_matvec(const float* d_a, int64_t lda, int64_t rows, int64_t n, const fl
   return GPIC_OK;
 }
 
+int gpic_generate_blobs(const double* d_centers, const int64_t* d_offsets, int64_t n, int32_t d,
+                        int32_t k, uint64_t seed, double noise, double offset, double* d_x,
+                        int64_t* d_labels, void* stream) {
+  if (n < 1 || d < 1 || k < 1 || k > n) return fail(GPIC_E_INVALID, "need n >= k >= 1, d >= 1");
+  if (!(noise >= 0.0)) return fail(GPIC_E_INVALID, "noise must be >= 0");
+  return launch_generate_blobs(d_centers, d_offsets, n, d, k, seed, noise, offset, d_x, d_labels,
+                               static_cast<cudaStream_t>(stream));
+}
+
 int gpic_row_stats(const double* d_w, int64_t rows, int64_t n, int64_t ldw, double* d_sum,
                    double* d_min, double* d_max, void* stream) {
   if (rows < 1 || n < 1) return fail(GPIC_E_EMPTY, "empty matrix");

@@ -210,6 +210,10 @@ int run_power_loop(const float* a, int64_t lda, const double* deg, int64_t n, do
 
 // kmeans.cu
 int64_t kmeans_scratch_bytes(int64_t n, int32_t k);
+// Device App-B generator (generate.cu): X row-major n x d fp64, labels int64
+int launch_generate_blobs(const double* centers, const int64_t* offsets, int64_t n, int d, int k,
+                          uint64_t seed, double noise, double offset, double* x, int64_t* labels,
+                          cudaStream_t s);
 int launch_kmeans1d(const double* v, int64_t n, int32_t k, int64_t first_index,
                     const double* h_uniforms, int32_t max_rounds, double tol, int64_t* labels,
                     void* scratch, gpic_ctl* ctl, cudaStream_t s);

@@ -439,6 +439,44 @@ def iterate(w, v, params: PicParams, config: KernelConfig | None = None):
 ROW_SUM_TOL = 1e-9  # serial.py:20
 
 
+def generate_blobs(n: int, d: int, k: int, seed: int = 0, noise: float = 1.0,
+                   radius: float = 40.0, offset: float = 8.0, sizes: str = "graded",
+                   config: KernelConfig | None = None):
+    """App-B Gaussian blobs generated in HBM (gpic_generate_blobs; §8f-4).
+
+    Centres and blob sizes are exactly those of `datasets.gaussian_blobs`
+    for the same arguments (the first k*d draws of the seeded numpy
+    generator); the per-point noise comes from the device Philox stream, so
+    X follows the same distribution but not the same draws. Returns
+    (X float64 CUDA tensor (n, d), labels int64 CUDA tensor (n,)).
+    """
+    from .datasets import _even_split, graded_sizes
+
+    torch = _torch()
+    if k < 1 or n < k or d < 1:
+        raise InvalidSpec("generate_blobs needs k >= 1, n >= k, d >= 1")
+    if sizes == "graded":
+        counts = graded_sizes(n, k)
+    elif sizes == "balanced":
+        counts = np.asarray(_even_split(n, k), dtype=np.int64)
+    else:
+        raise InvalidSpec(f"sizes must be 'graded' or 'balanced', got {sizes!r}")
+    rng = np.random.default_rng(seed)
+    centers = rng.standard_normal((k, d))
+    centers /= np.linalg.norm(centers, axis=1, keepdims=True)
+    centers *= radius
+    offsets = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+    dev = _device(config)
+    c_t = torch.from_numpy(np.ascontiguousarray(centers)).to(dev)
+    o_t = torch.from_numpy(offsets).to(dev)
+    x = torch.empty((n, d), dtype=torch.float64, device=dev)
+    labels = torch.empty(n, dtype=torch.int64, device=dev)
+    _lib.check(_lib.lib().gpic_generate_blobs(_ptr(c_t), _ptr(o_t), n, d, k, seed & (2**64 - 1),
+                                              float(noise), float(offset), _ptr(x), _ptr(labels),
+                                              _stream(dev)))
+    return x, labels
+
+
 def check_row_stochastic(w, config: KernelConfig | None = None):
     """serial.py:63-74: every row of w sums to 1 within 1e-9, entries in [0, 1].
 
@@ -575,16 +613,35 @@ def cluster_fused(d: DataSet, kind, params: PicParams, config: KernelConfig, see
     """One gpic_cluster call (p == 1, degree start). With ``timed`` the
     per-phase device milliseconds come back as a dict (report.py:28 PHASES)."""
     torch = _torch()
-    code, sigma = _check_kind(kind)
-    n, m = d.points.shape
-    k = params.k
     dev = _device(config)
+    x = torch.from_numpy(d.points).to(dev, non_blocking=True)
+    return _cluster_x(x, kind, params, config, seed, timed)
+
+
+def cluster_points(x, kind, params: PicParams, config: KernelConfig | None = None, seed: int = 0,
+                   timed: bool = False):
+    """`cluster` on a device-resident fp64 (n, d) tensor (e.g. from
+    `generate_blobs`): no host copy of X. Returns numpy labels / embedding
+    and the PicTrace (+ phase ms when ``timed``), like `cluster_fused`."""
+    torch = _torch()
+    if not (hasattr(x, "is_cuda") and x.is_cuda and x.dtype == torch.float64 and x.dim() == 2):
+        raise InvalidSpec("cluster_points needs a CUDA float64 (n, d) tensor")
+    if x.shape[0] < params.k:
+        raise KTooLarge(params.k, x.shape[0])
+    return _cluster_x(x.contiguous(), kind, params, config or KernelConfig(), seed, timed)
+
+
+def _cluster_x(x, kind, params, config, seed, timed):
+    torch = _torch()
+    code, sigma = _check_kind(kind)
+    n, m = x.shape
+    k = params.k
+    dev = x.device
     L = _lib.lib()
     eps = params.resolved_epsilon(n)
     T = params.max_iterations
     impl = _lib.AFFINITY_TC if config.affinity_impl == "tc" else _lib.AFFINITY_SIMT
     storage = config.storage_code()
-    x = torch.from_numpy(d.points).to(dev, non_blocking=True)
     nbytes = workspace_bytes(n, m, k, T, storage)
     work = torch.empty(nbytes, dtype=torch.uint8, device=dev)
     labels = torch.empty(n, dtype=torch.int64, device=dev)

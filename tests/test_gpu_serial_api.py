@@ -180,3 +180,41 @@ def test_build_affinity_rejects_nonfinite():
     pts[2, 1] = np.inf
     with pytest.raises(errors.NonFiniteEntry):
         _gpu().build_affinity(DataSet(pts), GaussianRbf(1.0))
+
+
+def test_generate_blobs_matches_oracle_stream():
+    """gpic_generate_blobs vs the oracle's numpy restatement (Philox4x32-10,
+    KAT-pinned in test_oracle_golden.py): labels exact, X to libm rounding."""
+    from paper_1604_02700_b200.datasets import gaussian_blobs as host_blobs, graded_sizes
+
+    gpu = _gpu()
+    for n, d, k, seed in ((1001, 3, 3, 0), (5000, 64, 10, 7), (777, 1, 2, 2**40 + 5)):
+        x, lab = gpu.generate_blobs(n, d, k, seed=seed)
+        host = host_blobs(n, d, k, seed=seed)
+        rng = np.random.default_rng(seed)
+        c = rng.standard_normal((k, d))
+        c = c / np.linalg.norm(c, axis=1, keepdims=True) * 40.0
+        ref_x, ref_lab = po.device_blobs(c, graded_sizes(n, k), seed, 1.0, 8.0)
+        xs = x.cpu().numpy()
+        assert np.array_equal(lab.cpu().numpy(), ref_lab)
+        assert np.array_equal(ref_lab, host.labels)
+        assert np.abs(xs - ref_x).max() <= 1e-12 * np.abs(ref_x).max()
+        x2, _ = gpu.generate_blobs(n, d, k, seed=seed)
+        assert np.array_equal(x2.cpu().numpy(), xs)
+
+
+def test_cluster_points_on_generated_data():
+    """Device-generated X clusters exactly like the same X passed from the host."""
+    from paper_1604_02700_b200 import KernelConfig, adjusted_rand_index, contingency
+
+    gpu = _gpu()
+    x, lab = gpu.generate_blobs(20000, 32, 5, seed=1)
+    kind = GaussianRbf(np.sqrt(32) / 2)
+    params = PicParams(k=5)
+    l1, v1, t1, _ = gpu.cluster_points(x, kind, params, KernelConfig(), seed=0)
+    l2, v2, t2, _ = gpu.cluster_fused(DataSet(x.cpu().numpy()), kind, params, KernelConfig(), seed=0)
+    assert np.array_equal(l1, l2) and np.array_equal(v1, v2)
+    assert t1.iterations_run == t2.iterations_run
+    assert adjusted_rand_index(contingency(lab.cpu().numpy(), l1)) == 1.0
+    with pytest.raises(errors.InvalidSpec):
+        gpu.cluster_points(x.float(), kind, params)

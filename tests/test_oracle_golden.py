@@ -173,3 +173,27 @@ def test_row_stochastic_verdict():
     assert po.row_stochastic_violation(np.array([[1.5, -0.5], [0.0, 1.0]])) == ("range", None, None)
     # NaN compares false everywhere, so the reference lets it through
     assert po.row_stochastic_violation(np.array([[np.nan, 0.0], [0.0, 1.0]])) is None
+
+
+def test_philox_known_answers():
+    """The device generator's stream (csrc/generate.cu) restated in the oracle
+    reproduces the published Philox4x32-10 known-answer vectors (Random123
+    kat_vectors: zero, all-ones and pi-digit counter/key)."""
+    def run(c, k):
+        return [int(v) for v in po.philox4x32_10(np.array([c], dtype=np.uint64), k)[0]]
+
+    assert run([0, 0, 0, 0], 0) == [0x6627E8D5, 0xE169C58D, 0xBC57AC4C, 0x9B00DBD8]
+    assert run([0xFFFFFFFF] * 4, 2**64 - 1) == [0x408F276D, 0x41C83B0E, 0xA20BC7C6, 0x6D5451FD]
+    assert run([0x243F6A88, 0x85A308D3, 0x13198A2E, 0x03707344],
+               0xA4093822 | (0x299F31D0 << 32)) == [0xD16CFE09, 0x94FDCCEB, 0x5001E420, 0x24126EA1]
+
+
+def test_device_blobs_restatement_statistics():
+    """The restated device stream is standard normal noise around the App-B
+    centres (mean/variance within sampling error), labels in blob order."""
+    rng = np.random.default_rng(3)
+    centers = rng.standard_normal((3, 5)) * 10
+    x, lab = po.device_blobs(centers, [4000, 5000, 6001], seed=9, noise=1.0, offset=8.0)
+    assert x.shape == (15001, 5) and np.array_equal(np.bincount(lab), [4000, 5000, 6001])
+    z = x - centers[lab] - 8.0
+    assert abs(z.mean()) < 0.02 and abs(z.var() - 1.0) < 0.03
