@@ -336,7 +336,7 @@ __global__ void __launch_bounds__(kCtaThreads<MODE>, 1)
   // run with different register budgets after setmaxnreg)
   auto teardown = [&]() {
     tc_fence_before();
-    asm volatile("bar.sync 15, %0;" ::"n"(kCtaThreads<MODE>) : "memory");
+    asm volatile("barrier.sync 15, %0;" ::"n"(kCtaThreads<MODE>) : "memory");
     if (warp == 1) {
       tc_fence_after();
       asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
