@@ -13,12 +13,12 @@ from paper_1604_02700_b200 import (  # noqa: E402
     Cosine, GaussianRbf, KernelConfig, PicParams, blobs_2d, cluster, gaussian_blobs)
 
 which = sys.argv[1] if len(sys.argv) > 1 else "all"
-d = blobs_2d(700, components=3, noise=0.3, seed=0)
+d = blobs_2d(int(os.environ.get("SAN_N", "700")), components=3, noise=0.3, seed=0)
 ref_labels, _, _, _ = po.pic_cluster(d.points, 1.0, 3, seed=0)
 cases = [("tc", "packed"), ("tc", "dense"), ("tc", "packed16"), ("tc", "none"), ("simt", "packed"),
          ("simt", "dense")]
 for engine, storage in cases:
-    if which not in ("all", storage, engine):
+    if which not in ("all", storage, engine, f"{engine}:{storage}"):
         continue
     labels, _, _ = cluster(d, GaussianRbf(1.0), PicParams(k=3),
                            config=KernelConfig(affinity_impl=engine, storage=storage), seed=0)
