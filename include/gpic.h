@@ -51,9 +51,13 @@ extern "C" {
 #define GPIC_KIND_RBF 0    /* GaussianRbf(sigma): exp(-|x-y|^2 / 2 sigma^2) */
 #define GPIC_KIND_COSINE 1 /* Cosine(): max(0, x.y / (|x||y|)), sigma ignored */
 
-/* Affinity engines (KernelConfig.affinity_impl). */
-#define GPIC_AFFINITY_TC 0   /* tcgen05 kind::tf32, 3xTF32 split, TMEM accumulators */
-#define GPIC_AFFINITY_SIMT 1 /* FP32 FFMA comparator */
+/* Affinity engines (KernelConfig.affinity_impl). The tcgen05 engine holds a
+ * row block's operands in shared memory: d <= 192 with stored A (dense /
+ * packed / packed16), d <= 256 matrix-free. Wider data asked of it runs on the
+ * SIMT engine with dense rows (the cluster calls and their workspace query
+ * apply the same rule, so the caller's sizes stay consistent). */
+#define GPIC_AFFINITY_TC 0   /* tcgen05 kind::f16, 3-term fp16 split, TMEM accumulators */
+#define GPIC_AFFINITY_SIMT 1 /* FP32 FFMA engine, any d */
 
 /* Device-resident control block of one power-iteration run (64-bit aligned,
  * 256 bytes). Written by the kernels; read back once at the end. */

@@ -865,6 +865,9 @@ __global__ void __launch_bounds__(kCtaThreads<MODE>, 1)
 }
 
 // ---------------------------------------------------------- host side
+}  // namespace
+bool tc_supports_pitch(int32_t dp, bool matvec);
+namespace {
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   if (!fn) {
@@ -900,6 +903,9 @@ template <int KB, int MODE>
 int launch_kb(const CUtensorMap& mh, const CUtensorMap& ml, const CUtensorMap& mo,
               const CUtensorMap& mn, const TcArgs& a0, cudaStream_t s) {
   constexpr int MB = mblocks(KB);
+  if (!tc_supports_pitch(KB * kKBlk, MODE == kModeMatvec))
+    return fail(GPIC_E_UNSUPPORTED,
+                "tcgen05 affinity engine: d too wide for this storage mode (SIMT engine: any d)");
   TcArgs a = a0;
   a.n_rtiles = ceil_div(a.rows, 128 * MB);
   a.n_chunks = ceil_div(a.n_ctiles, kChunkTiles);
@@ -1101,6 +1107,26 @@ int launch_affinity_tc_matvec(const float* xhi, const float* xlo, const float* s
   args.sym = colpart != nullptr && row_lo == 0 && row_hi == n;
   args.colpart = colpart;
   return dispatch_kb<kModeMatvec>(dp / kKBlk, mp, args, s);
+}
+
+// Feature pitches the engine runs: 64 * KB with the CTA's shared memory
+// (resident row operands + at least one B stage + the epilogue buffers)
+// within the 227 KB opt-in. Store modes stop at KB = 3 (d <= 192): their
+// 64 KB of per-warp staging leaves no room for a KB = 4 stage.
+bool tc_supports_pitch(int32_t dp, bool matvec) {
+  if (dp % kKBlk) return false;
+  const int KB = dp / kKBlk;
+  constexpr int kLimit = kSmemBudget + 256 + 1024;
+  auto fits = [&](int kb, int mode) {
+    return stages_raw(kb, mode) >= 1 && smem_bytes(kb, mode) <= kLimit;
+  };
+  switch (KB) {
+    case 1: return matvec ? fits(1, kModeMatvec) : fits(1, kModePacked) && fits(1, kModeDense);
+    case 2: return matvec ? fits(2, kModeMatvec) : fits(2, kModePacked) && fits(2, kModeDense);
+    case 3: return matvec ? fits(3, kModeMatvec) : fits(3, kModePacked) && fits(3, kModeDense);
+    case 4: return matvec ? fits(4, kModeMatvec) : fits(4, kModePacked) && fits(4, kModeDense);
+    default: return false;
+  }
 }
 
 }  // namespace gpic

@@ -158,6 +158,19 @@ int gpic_prepare_points(const double* d_x, int64_t n, int32_t d, int32_t kind, f
   return GPIC_OK;
 }
 
+// The tcgen05 engine keeps a row block's operands resident in shared memory:
+// d <= 192 for the storing modes, d <= 256 matrix-free (tc_supports_pitch).
+// Wider data runs on the SIMT engine with dense rows, which has no limit on
+// d; applied the same way by the workspace query, the cluster entry points
+// and the stage-wise affinity calls. Matrix-free beyond 256 stays an error.
+static void effective_engine(int32_t d, int32_t* impl, int32_t* storage) {
+  if (storage && *storage == GPIC_STORAGE_NONE) return;
+  if (tc_supports_pitch(feature_pitch(d), false)) return;
+  if (*impl == GPIC_AFFINITY_TC) *impl = GPIC_AFFINITY_SIMT;
+  if (storage && (*storage == GPIC_STORAGE_PACKED || *storage == GPIC_STORAGE_PACKED16))
+    *storage = GPIC_STORAGE_DENSE;
+}
+
 static int affinity_rows(int kind, const float* d_xhi, const float* d_xlo, const float* d_sqn,
                          int64_t n, int32_t d, int64_t row_lo, int64_t row_hi, double sigma,
                          int32_t impl, float* d_a, int64_t lda, double* d_deg, void* d_work,
@@ -191,6 +204,7 @@ static int affinity_rows(int kind, const float* d_xhi, const float* d_xlo, const
   const int32_t dp = feature_pitch(d);
   const float neg_scale_log2 = (float)(-1.4426950408889634 / (2.0 * sigma * sigma));
   float* rowpart = static_cast<float*>(d_work);  // n_ctiles x rows_pad
+  effective_engine(d, &impl, nullptr);
   if (impl == GPIC_AFFINITY_TC) {
     int rc = launch_affinity_tc(d_xhi, d_xlo, d_sqn, n, dp, row_lo, row_hi, neg_scale_log2, d_a,
                                 lda, rowpart, rows_pad, s, kind);
@@ -430,6 +444,8 @@ int gpic_packed_shard_build(const float* d_xhi, const float* d_xlo, const float*
 int64_t gpic_cluster_workspace_bytes(int64_t n, int32_t d, int32_t k, int32_t max_iter,
                                      int32_t storage) {
   if (n < 1 || d < 1) return -1;
+  int32_t impl = GPIC_AFFINITY_TC;
+  effective_engine(d, &impl, &storage);
   const int64_t scratch = workspace_bytes(n, d, k, n, max_iter);
   if (storage == GPIC_STORAGE_PACKED)  // tiles + GEMV partials (2) + degree partials (<= 2 + 4)
     return scratch + packed_tiles(n) * 128 * 128 * 4 + 8 * al(sym_partial_floats(n) * 4);
@@ -471,6 +487,7 @@ int cluster_impl(const double* d_x, int64_t n, int32_t d, double sigma, int32_t 
   if (kind != GPIC_KIND_RBF && kind != GPIC_KIND_COSINE) return fail(GPIC_E_INVALID, "unknown kind");
   if (kind == GPIC_KIND_RBF && !(sigma > 0)) return fail(GPIC_E_INVALID, "sigma must be positive");
   if (kind == GPIC_KIND_COSINE) sigma = 1.0;  // unused
+  effective_engine(d, &impl, &storage);
   if (storage != GPIC_STORAGE_DENSE && impl != GPIC_AFFINITY_TC)
     return fail(GPIC_E_UNSUPPORTED, "packed / matrix-free storage runs on the tcgen05 engine");
   if (storage < GPIC_STORAGE_DENSE || storage > GPIC_STORAGE_PACKED16)

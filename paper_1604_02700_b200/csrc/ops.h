@@ -44,6 +44,8 @@ int64_t sym_partial_floats(int64_t n);  // packed_tiles(n) * 128
 // and degcol [tile][4][128] (column sums per 32-row quadrant, off-diagonal
 // tiles), combined by launch_sym_degree.
 int packed_row_halves(int32_t dp);
+// feature pitches the tcgen05 engine runs (store modes / matrix-free)
+bool tc_supports_pitch(int32_t dp, bool matvec);
 int launch_affinity_tc_packed(const float* xhi, const float* xlo, const float* sqn, int64_t n,
                               int32_t dp, float neg_scale_log2, void* a_packed, float* degrow,
                               float* degcol, cudaStream_t s, int kind = GPIC_KIND_RBF,

@@ -146,6 +146,8 @@ class ShardedRunner:
         st = gpu._stream(dev)
         code, sigma = gpu._check_kind(kind)
         prep = gpu.prepare_points(points, dev, code)
+        # d > 192: the SIMT engine with dense row shards, as gpic_cluster does
+        packed = self.packed and int(_lib.lib().gpic_feature_pitch(prep.d)) <= 192
         nl = len(self.locals)
         shards = (_lib.Shard * nl)()
         keep = []  # device buffers referenced by the shard structs
@@ -166,7 +168,7 @@ class ShardedRunner:
                 shards[i] = _lib.Shard(None, 0, deg.data_ptr(), lo, hi - lo, _lib.STORAGE_NONE,
                                        prep.d, prep.xhi.data_ptr(), prep.xlo.data_ptr(),
                                        prep.sqn.data_ptr(), sigma, code, ypart.data_ptr())
-        elif self.packed:
+        elif packed:
             # symmetric packed shards: upper-triangle tiles of the rank's
             # 512-row super-rows, partial degrees summed across ranks
             for i, r in enumerate(self.locals):
