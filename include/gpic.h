@@ -55,7 +55,9 @@ extern "C" {
  * row block's operands in shared memory: d <= 192 with stored A (dense /
  * packed / packed16), d <= 256 matrix-free. Wider data asked of it runs on the
  * SIMT engine with dense rows (the cluster calls and their workspace query
- * apply the same rule, so the caller's sizes stay consistent). */
+ * apply the same rule, so the caller's sizes stay consistent). RBF with
+ * d <= 8 and stored A runs on the SIMT engine in difference form (the tensor
+ * Gram's fp32 cancellation would exceed the 1e-4 embedding gate there). */
 #define GPIC_AFFINITY_TC 0   /* tcgen05 kind::f16, 3-term fp16 split, TMEM accumulators */
 #define GPIC_AFFINITY_SIMT 1 /* FP32 FFMA engine, any d */
 

@@ -20,19 +20,36 @@ namespace {
 
 constexpr int BM = 128, BN = 128, BK = 16, PADS = 4;
 
+// DIFF (RBF): accumulate sum_f (x_if - x_jf)^2 directly instead of the Gram
+// form |x_i|^2 + |x_j|^2 - 2 x_i.x_j: the fp32 rounding of the coordinates
+// then costs ~2^-24 |x_i - x_j| |x| in d2 instead of ~2^-23 |x|^2, which is
+// what keeps near pairs exact when the spread is large against sigma.
+// PACKED: one CTA per upper-triangle tile (I <= J) of the packed layout,
+// writing the tile plus its per-tile degree partials (row sums; column sums
+// per 32-row quadrant off the diagonal) for launch_sym_degree.
+template <bool DIFF, bool PACKED>
 __global__ void __launch_bounds__(256, 2)
     affinity_simt_kernel(const float* __restrict__ xc, const float* __restrict__ sqn, int64_t n, int32_t dp, int64_t row_lo,
                          int64_t row_hi, float neg_scale_log2, float* __restrict__ a, int64_t lda,
-                         float* __restrict__ rowpart, int64_t rows_pad, int kind) {
+                         float* __restrict__ rowpart, int64_t rows_pad, int kind,
+                         float* __restrict__ degcol) {
   __shared__ __align__(16) float As[BK][BM + PADS];
   __shared__ __align__(16) float Bs[BK][BN + PADS];
 
   const int tid = threadIdx.x;
   const int tx = tid & 15;   // column group
   const int ty = tid >> 4;   // row group
-  const int64_t col0 = (int64_t)blockIdx.x * BN;
-  const int64_t lrow0 = (int64_t)blockIdx.y * BM;  // local (shard) row of the tile
-  const int64_t grow0 = row_lo + lrow0;            // global row
+  int64_t tI = blockIdx.y, tJ = blockIdx.x;
+  const int64_t nt = (n + BN - 1) / BN;
+  if (PACKED) {  // packed tile index -> (I, J), row-major upper triangle
+    int64_t t = blockIdx.x;
+    tI = 0;
+    while (t >= nt - tI) { t -= nt - tI; ++tI; }
+    tJ = tI + t;
+  }
+  const int64_t col0 = tJ * BN;
+  const int64_t lrow0 = tI * BM;         // local (shard) row of the tile
+  const int64_t grow0 = row_lo + lrow0;  // global row
 
   float acc[8][8];
 #pragma unroll
@@ -72,12 +89,21 @@ __global__ void __launch_bounds__(256, 2)
 #pragma unroll
       for (int i = 0; i < 8; ++i)
 #pragma unroll
-        for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(ar[i], br[j], acc[i][j]);
+        for (int j = 0; j < 8; ++j) {
+          if (DIFF) {
+            const float t = ar[i] - br[j];
+            acc[i][j] = fmaf(t, t, acc[i][j]);
+          } else {
+            acc[i][j] = fmaf(ar[i], br[j], acc[i][j]);
+          }
+        }
     }
     __syncthreads();
   }
 
   // fused epilogue
+  __shared__ float csum[PACKED ? 16 : 1][PACKED ? BN : 1];  // packed: per-ty column sums
+  float cs[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
   float sqb[8];
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
@@ -97,18 +123,29 @@ __global__ void __launch_bounds__(256, 2)
       float e;
       if (kind == GPIC_KIND_COSINE) {
         e = fmaxf(acc[i][j], 0.f);  // unit rows: the Gram entry is the cosine
+      } else if (DIFF) {
+        e = exp2f(acc[i][j] * neg_scale_log2);
       } else {
         const float d2 = fmaxf(sqa + sqb[j] - 2.f * acc[i][j], 0.f);
         e = exp2f(d2 * neg_scale_log2);
       }
-      if (cj == gr || cj >= n) e = 0.f;
+      if (cj == gr || cj >= n || (PACKED && gr >= n)) e = 0.f;
       vals[j] = e;
       rs += e;
+      cs[j] += e;
     }
     // 16 column-group lanes share this row: fixed butterfly
 #pragma unroll
     for (int o = 1; o < 16; o <<= 1) rs += __shfl_xor_sync(0xffffffffu, rs, o);
-    if (gr < row_hi) {
+    if (PACKED) {
+      const int64_t tile = tI * nt - tI * (tI - 1) / 2 + (tJ - tI);
+      float* trow = a + tile * (BM * BN) + (ty * 8 + i) * BN;
+      st_stream_f4(reinterpret_cast<float4*>(trow + tx * 4),
+                   make_float4(vals[0], vals[1], vals[2], vals[3]));
+      st_stream_f4(reinterpret_cast<float4*>(trow + 64 + tx * 4),
+                   make_float4(vals[4], vals[5], vals[6], vals[7]));
+      if (tx == 0) rowpart[tile * BM + ty * 8 + i] = rs;  // degrow
+    } else if (gr < row_hi) {
       float* arow = a + lr * lda;
       const int64_t c0 = col0 + tx * 4;
       const int64_t c1 = col0 + 64 + tx * 4;
@@ -117,6 +154,18 @@ __global__ void __launch_bounds__(256, 2)
       if (c1 < lda) st_stream_f4(reinterpret_cast<float4*>(arow + c1),
                                  make_float4(vals[4], vals[5], vals[6], vals[7]));
       if (tx == 0) rowpart[(int64_t)blockIdx.x * rows_pad + lr] = rs;
+    }
+  }
+  if (PACKED && tI < tJ) {
+    // column sums per 32-row quadrant q (row groups ty = 4q..4q+3, in order)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) csum[ty][j < 4 ? tx * 4 + j : 64 + tx * 4 + (j - 4)] = cs[j];
+    __syncthreads();
+    const int64_t tile = tI * nt - tI * (tI - 1) / 2 + (tJ - tI);
+    for (int e = tid; e < 4 * BN; e += 256) {
+      const int q = e / BN, c = e % BN;
+      degcol[(tile * 4 + q) * BN + c] =
+          ((csum[4 * q][c] + csum[4 * q + 1][c]) + csum[4 * q + 2][c]) + csum[4 * q + 3][c];
     }
   }
 }
@@ -141,8 +190,25 @@ void launch_affinity_simt(const float* xhi, const float* xlo, const float* sqn, 
                           cudaStream_t s, int kind) {
   const int64_t rows = row_hi - row_lo;
   dim3 grid((unsigned)ceil_div(n, BN), (unsigned)ceil_div(rows, BM));
-  affinity_simt_kernel<<<grid, 256, 0, s>>>(xlo, sqn, n, dp, row_lo, row_hi, neg_scale_log2,
-                                            a, lda, rowpart, rows_pad, kind);
+  if (kind == GPIC_KIND_COSINE)
+    affinity_simt_kernel<false, false><<<grid, 256, 0, s>>>(
+        xlo, sqn, n, dp, row_lo, row_hi, neg_scale_log2, a, lda, rowpart, rows_pad, kind, nullptr);
+  else
+    affinity_simt_kernel<true, false><<<grid, 256, 0, s>>>(
+        xlo, sqn, n, dp, row_lo, row_hi, neg_scale_log2, a, lda, rowpart, rows_pad, kind, nullptr);
+  count_launch();
+}
+
+void launch_affinity_simt_packed(const float* xlo, const float* sqn, int64_t n, int32_t dp,
+                                 float neg_scale_log2, float* a_packed, float* degrow,
+                                 float* degcol, cudaStream_t s, int kind) {
+  const unsigned grid = (unsigned)packed_tiles(n);
+  if (kind == GPIC_KIND_COSINE)
+    affinity_simt_kernel<false, true><<<grid, 256, 0, s>>>(
+        xlo, sqn, n, dp, 0, n, neg_scale_log2, a_packed, 0, degrow, 0, kind, degcol);
+  else
+    affinity_simt_kernel<true, true><<<grid, 256, 0, s>>>(
+        xlo, sqn, n, dp, 0, n, neg_scale_log2, a_packed, 0, degrow, 0, kind, degcol);
   count_launch();
 }
 

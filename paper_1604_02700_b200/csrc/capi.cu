@@ -158,17 +158,30 @@ int gpic_prepare_points(const double* d_x, int64_t n, int32_t d, int32_t kind, f
   return GPIC_OK;
 }
 
-// The tcgen05 engine keeps a row block's operands resident in shared memory:
-// d <= 192 for the storing modes, d <= 256 matrix-free (tc_supports_pitch).
-// Wider data runs on the SIMT engine with dense rows, which has no limit on
-// d; applied the same way by the workspace query, the cluster entry points
-// and the stage-wise affinity calls. Matrix-free beyond 256 stays an error.
-static void effective_engine(int32_t d, int32_t* impl, int32_t* storage) {
+// Engine routing, applied the same way by the workspace query, the cluster
+// entry points and the stage-wise affinity calls:
+//  * the tcgen05 engine keeps a row block's operands resident in shared
+//    memory: d <= 192 with stored A, d <= 256 matrix-free (tc_supports_pitch);
+//    wider stored-A runs go to the SIMT engine with dense rows (any d);
+//  * RBF with d <= kSimtDiffMaxD stored-A runs on the SIMT engine, which
+//    forms |x_i - x_j|^2 from coordinate differences: the Gram form's
+//    cancellation error (~2^-22 |x|^2 / 2 sigma^2 relative in A) exceeds the
+//    1e-4 embedding gate when the spread is large against sigma, which is
+//    typical at low d (sigma = sqrt(d)/2); there the tensor Gram also runs
+//    at <= 8/64 of its K width, so the difference form costs nothing.
+//  * matrix-free stays on tcgen05 (an error beyond d = 256).
+constexpr int32_t kSimtDiffMaxD = 8;
+static void effective_engine(int kind, int32_t d, int32_t* impl, int32_t* storage) {
   if (storage && *storage == GPIC_STORAGE_NONE) return;
-  if (tc_supports_pitch(feature_pitch(d), false)) return;
-  if (*impl == GPIC_AFFINITY_TC) *impl = GPIC_AFFINITY_SIMT;
-  if (storage && (*storage == GPIC_STORAGE_PACKED || *storage == GPIC_STORAGE_PACKED16))
-    *storage = GPIC_STORAGE_DENSE;
+  if (!tc_supports_pitch(feature_pitch(d), false)) {
+    if (*impl == GPIC_AFFINITY_TC) *impl = GPIC_AFFINITY_SIMT;
+    if (storage && (*storage == GPIC_STORAGE_PACKED || *storage == GPIC_STORAGE_PACKED16))
+      *storage = GPIC_STORAGE_DENSE;
+    return;
+  }
+  if (kind == GPIC_KIND_RBF && d <= kSimtDiffMaxD && *impl == GPIC_AFFINITY_TC &&
+      !(storage && *storage == GPIC_STORAGE_PACKED16))
+    *impl = GPIC_AFFINITY_SIMT;
 }
 
 static int affinity_rows(int kind, const float* d_xhi, const float* d_xlo, const float* d_sqn,
@@ -204,7 +217,7 @@ static int affinity_rows(int kind, const float* d_xhi, const float* d_xlo, const
   const int32_t dp = feature_pitch(d);
   const float neg_scale_log2 = (float)(-1.4426950408889634 / (2.0 * sigma * sigma));
   float* rowpart = static_cast<float*>(d_work);  // n_ctiles x rows_pad
-  effective_engine(d, &impl, nullptr);
+  effective_engine(kind, d, &impl, nullptr);
   if (impl == GPIC_AFFINITY_TC) {
     int rc = launch_affinity_tc(d_xhi, d_xlo, d_sqn, n, dp, row_lo, row_hi, neg_scale_log2, d_a,
                                 lda, rowpart, rows_pad, s, kind);
@@ -445,7 +458,7 @@ int64_t gpic_cluster_workspace_bytes(int64_t n, int32_t d, int32_t k, int32_t ma
                                      int32_t storage) {
   if (n < 1 || d < 1) return -1;
   int32_t impl = GPIC_AFFINITY_TC;
-  effective_engine(d, &impl, &storage);
+  effective_engine(GPIC_KIND_RBF, d, &impl, &storage);
   const int64_t scratch = workspace_bytes(n, d, k, n, max_iter);
   if (storage == GPIC_STORAGE_PACKED)  // tiles + GEMV partials (2) + degree partials (<= 2 + 4)
     return scratch + packed_tiles(n) * 128 * 128 * 4 + 8 * al(sym_partial_floats(n) * 4);
@@ -487,9 +500,10 @@ int cluster_impl(const double* d_x, int64_t n, int32_t d, double sigma, int32_t 
   if (kind != GPIC_KIND_RBF && kind != GPIC_KIND_COSINE) return fail(GPIC_E_INVALID, "unknown kind");
   if (kind == GPIC_KIND_RBF && !(sigma > 0)) return fail(GPIC_E_INVALID, "sigma must be positive");
   if (kind == GPIC_KIND_COSINE) sigma = 1.0;  // unused
-  effective_engine(d, &impl, &storage);
-  if (storage != GPIC_STORAGE_DENSE && impl != GPIC_AFFINITY_TC)
-    return fail(GPIC_E_UNSUPPORTED, "packed / matrix-free storage runs on the tcgen05 engine");
+  effective_engine(kind, d, &impl, &storage);
+  if ((storage == GPIC_STORAGE_NONE || storage == GPIC_STORAGE_PACKED16) &&
+      impl != GPIC_AFFINITY_TC)
+    return fail(GPIC_E_UNSUPPORTED, "fp16 packed / matrix-free storage runs on the tcgen05 engine");
   if (storage < GPIC_STORAGE_DENSE || storage > GPIC_STORAGE_PACKED16)
     return fail(GPIC_E_INVALID, "unknown storage mode");
   Workspace ws;
@@ -519,9 +533,14 @@ int cluster_impl(const double* d_x, int64_t n, int32_t d, double sigma, int32_t 
     const int64_t pf = al(sym_partial_floats(n) * 4) / 4;
     float* degrow = colp + pf;
     float* degcol = degrow + 2 * pf;
-    rc = launch_affinity_tc_packed(ws.xhi, ws.xlo, ws.sqn, n, dp, neg_scale_log2, a, degrow,
-                                   degcol, s, kind, half);
-    if (rc) return rc;
+    if (impl == GPIC_AFFINITY_SIMT) {
+      launch_affinity_simt_packed(ws.xlo, ws.sqn, n, dp, neg_scale_log2, a, degrow, degcol, s,
+                                  kind);
+    } else {
+      rc = launch_affinity_tc_packed(ws.xhi, ws.xlo, ws.sqn, n, dp, neg_scale_log2, a, degrow,
+                                     degcol, s, kind, half);
+      if (rc) return rc;
+    }
     mark(ev, 1, s);
     launch_sym_degree(degrow, degcol, n, packed_row_halves(dp), deg, ws.ctl, s);
     L.mode = half ? kLoopPacked16 : kLoopPacked;

@@ -44,6 +44,10 @@ int64_t sym_partial_floats(int64_t n);  // packed_tiles(n) * 128
 // and degcol [tile][4][128] (column sums per 32-row quadrant, off-diagonal
 // tiles), combined by launch_sym_degree.
 int packed_row_halves(int32_t dp);
+// SIMT engine, packed upper-triangle tiles + per-tile degree partials
+void launch_affinity_simt_packed(const float* xlo, const float* sqn, int64_t n, int32_t dp,
+                                 float neg_scale_log2, float* a_packed, float* degrow,
+                                 float* degcol, cudaStream_t s, int kind);
 // feature pitches the tcgen05 engine runs (store modes / matrix-free)
 bool tc_supports_pitch(int32_t dp, bool matvec);
 int launch_affinity_tc_packed(const float* xhi, const float* xlo, const float* sqn, int64_t n,

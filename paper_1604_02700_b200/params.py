@@ -132,8 +132,8 @@ class KernelConfig:
             raise InvalidSpec(f"storage must be one of {STORAGES}")
 
     def storage_code(self) -> int:
-        """GPIC_STORAGE_*: packed symmetric tiles need the tcgen05 engine and a
-        single rank; matrix-free ("none") needs the tcgen05 engine."""
+        """GPIC_STORAGE_*: packed symmetric tiles need a single rank (either
+        engine); fp16 tiles and matrix-free ("none") need the tcgen05 engine."""
         if self.storage == "none":
             if self.affinity_impl != "tc":
                 raise InvalidSpec("matrix-free storage runs on the tcgen05 engine")
@@ -142,7 +142,7 @@ class KernelConfig:
             if self.affinity_impl != "tc" or self.p != 1:
                 raise InvalidSpec("fp16 packed storage runs on the tcgen05 engine, one rank")
             return 3
-        if self.storage == "packed" and self.affinity_impl == "tc" and self.p == 1:
+        if self.storage == "packed" and self.p == 1:
             return 1
         return 0
 

@@ -146,8 +146,10 @@ class ShardedRunner:
         st = gpu._stream(dev)
         code, sigma = gpu._check_kind(kind)
         prep = gpu.prepare_points(points, dev, code)
-        # d > 192: the SIMT engine with dense row shards, as gpic_cluster does
-        packed = self.packed and int(_lib.lib().gpic_feature_pitch(prep.d)) <= 192
+        # the engine routing of gpic_cluster (capi.cu effective_engine): d > 192
+        # and RBF with d <= 8 run on the SIMT engine, here with dense row shards
+        packed = (self.packed and int(_lib.lib().gpic_feature_pitch(prep.d)) <= 192
+                  and not (code == _lib.KIND_RBF and prep.d <= 8))
         nl = len(self.locals)
         shards = (_lib.Shard * nl)()
         keep = []  # device buffers referenced by the shard structs
