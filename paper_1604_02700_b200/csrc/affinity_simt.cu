@@ -27,7 +27,9 @@ constexpr int BM = 128, BN = 128, BK = 16, PADS = 4;
 // PACKED: one CTA per upper-triangle tile (I <= J) of the packed layout,
 // writing the tile plus its per-tile degree partials (row sums; column sums
 // per 32-row quadrant off the diagonal) for launch_sym_degree.
-template <bool DIFF, bool PACKED>
+// KD > 0: the data has at most KD (<= 16) non-zero features: one K chunk
+// whose inner loop stops at KD (the padding columns are zero either way).
+template <bool DIFF, bool PACKED, int KD>
 __global__ void __launch_bounds__(256, 2)
     affinity_simt_kernel(const float* __restrict__ xc, const float* __restrict__ sqn, int64_t n, int32_t dp, int64_t row_lo,
                          int64_t row_hi, float neg_scale_log2, float* __restrict__ a, int64_t lda,
@@ -58,7 +60,8 @@ __global__ void __launch_bounds__(256, 2)
     for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
 
   // loader mapping: 128 rows x 16 features = 512 float4; 256 threads x 2
-  for (int k0 = 0; k0 < dp; k0 += BK) {
+  const int kend = KD > 0 ? BK : dp;
+  for (int k0 = 0; k0 < kend; k0 += BK) {
 #pragma unroll
     for (int q = 0; q < 2; ++q) {
       const int e = tid + q * 256;       // 0..511
@@ -79,7 +82,7 @@ __global__ void __launch_bounds__(256, 2)
     }
     __syncthreads();
 #pragma unroll
-    for (int k = 0; k < BK; ++k) {
+    for (int k = 0; k < (KD > 0 ? KD : BK); ++k) {
       const float4 a0 = *reinterpret_cast<const float4*>(&As[k][ty * 8]);
       const float4 a1 = *reinterpret_cast<const float4*>(&As[k][ty * 8 + 4]);
       const float4 b0 = *reinterpret_cast<const float4*>(&Bs[k][tx * 4]);
@@ -185,30 +188,36 @@ __global__ void degree_kernel(const float* __restrict__ rowpart, int64_t rows, i
 }  // namespace
 
 void launch_affinity_simt(const float* xhi, const float* xlo, const float* sqn, int64_t n,
-                          int32_t dp, int64_t row_lo, int64_t row_hi, float neg_scale_log2,
+                          int32_t d, int32_t dp, int64_t row_lo, int64_t row_hi, float neg_scale_log2,
                           float* a, int64_t lda, float* rowpart, int64_t rows_pad,
                           cudaStream_t s, int kind) {
   const int64_t rows = row_hi - row_lo;
   dim3 grid((unsigned)ceil_div(n, BN), (unsigned)ceil_div(rows, BM));
-  if (kind == GPIC_KIND_COSINE)
-    affinity_simt_kernel<false, false><<<grid, 256, 0, s>>>(
-        xlo, sqn, n, dp, row_lo, row_hi, neg_scale_log2, a, lda, rowpart, rows_pad, kind, nullptr);
-  else
-    affinity_simt_kernel<true, false><<<grid, 256, 0, s>>>(
-        xlo, sqn, n, dp, row_lo, row_hi, neg_scale_log2, a, lda, rowpart, rows_pad, kind, nullptr);
+#define GPIC_SIMT_LAUNCH(DIFF, PACKED, KD) \
+  affinity_simt_kernel<DIFF, PACKED, KD><<<grid, 256, 0, s>>>( \
+      xlo, sqn, n, dp, row_lo, row_hi, neg_scale_log2, a, lda, rowpart, rows_pad, kind, nullptr)
+  if (kind == GPIC_KIND_COSINE) GPIC_SIMT_LAUNCH(false, false, 0);
+  else if (d <= 2) GPIC_SIMT_LAUNCH(true, false, 2);
+  else if (d <= 4) GPIC_SIMT_LAUNCH(true, false, 4);
+  else if (d <= 8) GPIC_SIMT_LAUNCH(true, false, 8);
+  else GPIC_SIMT_LAUNCH(true, false, 0);
+#undef GPIC_SIMT_LAUNCH
   count_launch();
 }
 
-void launch_affinity_simt_packed(const float* xlo, const float* sqn, int64_t n, int32_t dp,
-                                 float neg_scale_log2, float* a_packed, float* degrow,
+void launch_affinity_simt_packed(const float* xlo, const float* sqn, int64_t n, int32_t d,
+                                 int32_t dp, float neg_scale_log2, float* a_packed, float* degrow,
                                  float* degcol, cudaStream_t s, int kind) {
   const unsigned grid = (unsigned)packed_tiles(n);
-  if (kind == GPIC_KIND_COSINE)
-    affinity_simt_kernel<false, true><<<grid, 256, 0, s>>>(
-        xlo, sqn, n, dp, 0, n, neg_scale_log2, a_packed, 0, degrow, 0, kind, degcol);
-  else
-    affinity_simt_kernel<true, true><<<grid, 256, 0, s>>>(
-        xlo, sqn, n, dp, 0, n, neg_scale_log2, a_packed, 0, degrow, 0, kind, degcol);
+#define GPIC_SIMT_LAUNCH(DIFF, KD) \
+  affinity_simt_kernel<DIFF, true, KD><<<grid, 256, 0, s>>>( \
+      xlo, sqn, n, dp, 0, n, neg_scale_log2, a_packed, 0, degrow, 0, kind, degcol)
+  if (kind == GPIC_KIND_COSINE) GPIC_SIMT_LAUNCH(false, 0);
+  else if (d <= 2) GPIC_SIMT_LAUNCH(true, 2);
+  else if (d <= 4) GPIC_SIMT_LAUNCH(true, 4);
+  else if (d <= 8) GPIC_SIMT_LAUNCH(true, 8);
+  else GPIC_SIMT_LAUNCH(true, 0);
+#undef GPIC_SIMT_LAUNCH
   count_launch();
 }
 

@@ -223,7 +223,7 @@ static int affinity_rows(int kind, const float* d_xhi, const float* d_xlo, const
                                 lda, rowpart, rows_pad, s, kind);
     if (rc != GPIC_OK) return rc;
   } else if (impl == GPIC_AFFINITY_SIMT) {
-    launch_affinity_simt(d_xhi, d_xlo, d_sqn, n, dp, row_lo, row_hi, neg_scale_log2, d_a, lda,
+    launch_affinity_simt(d_xhi, d_xlo, d_sqn, n, d, dp, row_lo, row_hi, neg_scale_log2, d_a, lda,
                          rowpart, rows_pad, s, kind);
   } else {
     return fail(GPIC_E_INVALID, "unknown affinity engine");
@@ -534,7 +534,7 @@ int cluster_impl(const double* d_x, int64_t n, int32_t d, double sigma, int32_t 
     float* degrow = colp + pf;
     float* degcol = degrow + 2 * pf;
     if (impl == GPIC_AFFINITY_SIMT) {
-      launch_affinity_simt_packed(ws.xlo, ws.sqn, n, dp, neg_scale_log2, a, degrow, degcol, s,
+      launch_affinity_simt_packed(ws.xlo, ws.sqn, n, d, dp, neg_scale_log2, a, degrow, degcol, s,
                                   kind);
     } else {
       rc = launch_affinity_tc_packed(ws.xhi, ws.xlo, ws.sqn, n, dp, neg_scale_log2, a, degrow,
@@ -565,7 +565,7 @@ int cluster_impl(const double* d_x, int64_t n, int32_t d, double sigma, int32_t 
                               ws.rowpart, rows_pad, s, kind);
       if (rc) return rc;
     } else {
-      launch_affinity_simt(ws.xhi, ws.xlo, ws.sqn, n, dp, 0, n, neg_scale_log2, a, lda,
+      launch_affinity_simt(ws.xhi, ws.xlo, ws.sqn, n, d, dp, 0, n, neg_scale_log2, a, lda,
                            ws.rowpart, rows_pad, s, kind);
     }
     mark(ev, 1, s);

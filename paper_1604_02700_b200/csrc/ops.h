@@ -45,7 +45,7 @@ int64_t sym_partial_floats(int64_t n);  // packed_tiles(n) * 128
 // tiles), combined by launch_sym_degree.
 int packed_row_halves(int32_t dp);
 // SIMT engine, packed upper-triangle tiles + per-tile degree partials
-void launch_affinity_simt_packed(const float* xlo, const float* sqn, int64_t n, int32_t dp,
+void launch_affinity_simt_packed(const float* xlo, const float* sqn, int64_t n, int32_t d, int32_t dp,
                                  float neg_scale_log2, float* a_packed, float* degrow,
                                  float* degcol, cudaStream_t s, int kind);
 // feature pitches the tcgen05 engine runs (store modes / matrix-free)
@@ -89,7 +89,7 @@ void launch_prepare(const double* x, int64_t n, int32_t d, float* xhi, float* xl
                     int kind = GPIC_KIND_RBF);
 
 // affinity_simt.cu / affinity_tc.cu
-void launch_affinity_simt(const float* xhi, const float* xlo, const float* sqn, int64_t n,
+void launch_affinity_simt(const float* xhi, const float* xlo, const float* sqn, int64_t n, int32_t d,
                           int32_t dp, int64_t row_lo, int64_t row_hi, float neg_scale_log2,
                           float* a, int64_t lda, float* rowpart, int64_t rows_pad,
                           cudaStream_t s, int kind = GPIC_KIND_RBF);
