@@ -13,6 +13,7 @@
 // shape.
 #include "common.cuh"
 #include "ops.h"
+#include "sm100.cuh"
 
 namespace gpic {
 
@@ -44,10 +45,17 @@ __global__ void __launch_bounds__(256, 2)
   int64_t tI = blockIdx.y, tJ = blockIdx.x;
   const int64_t nt = (n + BN - 1) / BN;
   if (PACKED) {  // packed tile index -> (I, J), row-major upper triangle
-    int64_t t = blockIdx.x;
-    tI = 0;
-    while (t >= nt - tI) { t -= nt - tI; ++tI; }
-    tJ = tI + t;
+    // row I starts at S(I) = I nt - I (I - 1) / 2: invert the quadratic,
+    // then correct the floating-point estimate by one step either way
+    const int64_t t = blockIdx.x;
+    const double b = 2.0 * (double)nt + 1.0;
+    int64_t I = (int64_t)((b - sqrt(b * b - 8.0 * (double)t)) * 0.5);
+    auto start = [&](int64_t r) { return r * nt - r * (r - 1) / 2; };
+    if (I < 0) I = 0;
+    while (I > 0 && start(I) > t) --I;
+    while (start(I + 1) <= t) ++I;
+    tI = I;
+    tJ = I + (t - start(I));
   }
   const int64_t col0 = tJ * BN;
   const int64_t lrow0 = tI * BM;         // local (shard) row of the tile
@@ -127,7 +135,7 @@ __global__ void __launch_bounds__(256, 2)
       if (kind == GPIC_KIND_COSINE) {
         e = fmaxf(acc[i][j], 0.f);  // unit rows: the Gram entry is the cosine
       } else if (DIFF) {
-        e = exp2f(acc[i][j] * neg_scale_log2);
+        e = ex2(acc[i][j] * neg_scale_log2);
       } else {
         const float d2 = fmaxf(sqa + sqb[j] - 2.f * acc[i][j], 0.f);
         e = exp2f(d2 * neg_scale_log2);
