@@ -332,6 +332,7 @@ int gpic_mf_degrees(const float* d_xhi, const float* d_xlo, const float* d_sqn, 
   MfOperands op{d_xhi, d_xlo, d_sqn, n, feature_pitch(d),
                 (float)(-1.4426950408889634 / (2.0 * sigma * sigma)), kind};
   op.sym = mf_sym_default();
+  op.d = d;
   return launch_mf_degrees(op, row_lo, row_hi - row_lo, d_ones, d_ypart, d_deg,
                            static_cast<cudaStream_t>(stream));
 }
@@ -551,6 +552,7 @@ int cluster_impl(const double* d_x, int64_t n, int32_t d, double sigma, int32_t 
     double* ypart = reinterpret_cast<double*>(a);
     L.mode = kLoopMatrixFree;
     L.mf = MfOperands{ws.xhi, ws.xlo, ws.sqn, n, dp, neg_scale_log2, kind};
+    L.mf.d = d;
     L.mf.sym = mf_sym_default();
     L.ypart = ypart;
     mark(ev, 1, s);  // matrix-free: the degree pass is the first A recompute

@@ -393,6 +393,7 @@ int gpic_comm_iterate(gpic_comm* c, const gpic_shard* shards, int32_t nlocal, do
       S.mode = kLoopMatrixFree;
       S.mf = MfOperands{sh.xhi, sh.xlo, sh.sqn, n, feature_pitch(sh.d),
                         (float)(-1.4426950408889634 / (2.0 * sh.sigma * sh.sigma)), sh.kind};
+      S.mf.d = sh.d;
       S.ypart = sh.ypart;
     }
     S.rows = shards[li].rows;

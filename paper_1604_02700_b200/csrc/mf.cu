@@ -53,6 +53,63 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// Difference-form pass for RBF with d <= 8 (the tensor Gram's fp32
+// cancellation exceeds the embedding gate there; capi.cu effective_engine):
+// CTA (chunk c, row block) sums a_ij v_j over the chunk's 4096 columns for
+// 128 rows, a_ij = exp2(ns * sum_k (x_ik - x_jk)^2), a_ii = 0. Thread
+// (row r, half h) takes columns h*64 .. h*64+63 of each 128-column tile
+// (the warp reads one column at a time: shared-memory broadcast); fp32 per
+// tile, fp64 across tiles and halves, fixed order. Writes the chunk's row
+// partial in the tensor pass's layout (ypart[c * rows_pad + r]).
+template <int KD>
+__global__ void __launch_bounds__(256)
+    mf_simt_kernel(const float* __restrict__ xc, int32_t dp, int64_t n, int64_t row_lo,
+                   int64_t rows, int64_t rows_pad, float ns, const float* __restrict__ v32,
+                   double* __restrict__ ypart, gpic_ctl* ctl) {
+  if (ctl != nullptr && *(volatile const int32_t*)&ctl->stop) return;
+  __shared__ float cx[128][KD];
+  __shared__ float cv[128];
+  __shared__ double half1[128];
+  const int t = threadIdx.x, r = t & 127, h = t >> 7;
+  const int64_t lr = (int64_t)blockIdx.y * 128 + r;
+  const int64_t gi = row_lo + lr;
+  float xi[KD];
+#pragma unroll
+  for (int k = 0; k < KD; ++k) xi[k] = gi < n ? xc[gi * dp + k] : 0.f;
+  const int64_t c0 = (int64_t)blockIdx.x * 4096;
+  double acc = 0.0;
+  for (int tile = 0; tile < 32; ++tile) {
+    const int64_t j0 = c0 + tile * 128;
+    if (j0 >= n) break;
+    __syncthreads();
+    for (int e = t; e < 128 * KD; e += 256) {
+      const int jj = e / KD, k = e % KD;
+      const int64_t j = j0 + jj;
+      cx[jj][k] = j < n ? xc[j * dp + k] : 0.f;
+    }
+    if (t < 128) cv[t] = j0 + t < n ? v32[j0 + t] : 0.f;
+    __syncthreads();
+    float s = 0.f;
+#pragma unroll 4
+    for (int jj = h * 64; jj < h * 64 + 64; ++jj) {
+      float d2 = 0.f;
+#pragma unroll
+      for (int k = 0; k < KD; ++k) {
+        const float df = xi[k] - cx[jj][k];
+        d2 = fmaf(df, df, d2);
+      }
+      float a;
+      asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(a) : "f"(d2 * ns));
+      if (j0 + jj == gi) a = 0.f;
+      s = fmaf(a, cv[jj], s);
+    }
+    acc += (double)s;
+  }
+  if (h == 1) half1[r] = acc;
+  __syncthreads();
+  if (h == 0 && lr < rows) ypart[(int64_t)blockIdx.x * rows_pad + lr] = acc + half1[r];
+}
+
 // One CTA per column tile J (128 rows of y), kSeg segments: segment s sums
 // its share of row i's chunk partials (chunks from the row block's first
 // tile on) and of the column records (row blocks I' = 0 .. J / MB), then the
@@ -131,6 +188,24 @@ int launch_mf_matvec(const MfOperands& op, int64_t row_lo, int64_t rows, const f
                      double* ypart, const double* deg, const PeerTable& pt, gpic_ctl* ctl,
                      cudaStream_t s) {
   const int64_t rows_pad = round_up(rows, kTileM);
+  if (op.kind == GPIC_KIND_RBF && op.d > 0 && op.d <= 8) {
+    const dim3 grid((unsigned)mf_parts(op.n, op.dp), (unsigned)ceil_div(rows, 128));
+    if (op.d <= 2)
+      mf_simt_kernel<2><<<grid, 256, 0, s>>>(op.xlo, op.dp, op.n, row_lo, rows, rows_pad, op.ns,
+                                             v32, ypart, ctl);
+    else if (op.d <= 4)
+      mf_simt_kernel<4><<<grid, 256, 0, s>>>(op.xlo, op.dp, op.n, row_lo, rows, rows_pad, op.ns,
+                                             v32, ypart, ctl);
+    else
+      mf_simt_kernel<8><<<grid, 256, 0, s>>>(op.xlo, op.dp, op.n, row_lo, rows, rows_pad, op.ns,
+                                             v32, ypart, ctl);
+    count_launch();
+    mf_reduce_kernel<<<(unsigned)ceil_div(rows, 256), 256, 0, s>>>(
+        ypart, mf_parts(op.n, op.dp), rows_pad, rows, row_lo, deg, pt, ctl);
+    count_launch();
+    GPIC_CUDA_TRY(cudaGetLastError());
+    return GPIC_OK;
+  }
   if (mf_sym(op, row_lo, rows)) {
     float* colpart = reinterpret_cast<float*>(ypart + mf_parts(op.n, op.dp) * rows_pad);
     int rc = launch_affinity_tc_matvec(op.xhi, op.xlo, op.sqn, op.n, op.dp, 0, op.n, op.ns, v32,

@@ -160,6 +160,7 @@ struct MfOperands {
   float ns;  // -log2(e) / (2 sigma^2)
   int kind = GPIC_KIND_RBF;
   int sym = 0;  // whole matrix on one rank: upper-triangle pass (mf.cu)
+  int32_t d = 0;  // features (RBF with d <= 8: the difference-form SIMT pass)
 };
 bool mf_sym_default();
 int64_t mf_parts(int64_t n, int32_t dp);
