@@ -54,3 +54,15 @@ def test_ragged_shapes(storage, n, d):
     assert err <= (1e-3 if storage == "packed16" else 1e-4), f"rel L1 {err:.3e}"
     if separated:
         assert np.array_equal(labels, ref_labels), f"{np.bincount(labels)} vs {np.bincount(ref_labels)}"
+
+
+@pytest.mark.parametrize("d,sigma", [(16, 1.0), (32, 1.5), (64, 1.5), (128, 2.0)])
+def test_small_sigma_on_the_tensor_engine(d, sigma):
+    """Above the d <= 8 cut the tensor Gram stays within the gate even with
+    sigma well below the App-B sqrt(d)/2 (measured 2e-5 at d = 16, sigma = 1)."""
+    g = gaussian_blobs(1500, d, 4, seed=1, sizes="balanced")
+    params = PicParams(k=4, epsilon=TINY_EPS, max_iterations=6)
+    labels, v, _ = cluster(g, GaussianRbf(sigma), params)
+    ref_labels, ref_v, _, _ = po.pic_cluster(g.points, sigma, 4, epsilon=TINY_EPS, max_iterations=6)
+    assert np.abs(v - ref_v).sum() / np.abs(ref_v).sum() <= 1e-4
+    assert np.array_equal(labels, ref_labels)
