@@ -527,7 +527,7 @@ def main():
     ap.add_argument("--config", type=int, default=3)
     ap.add_argument("--engine", choices=["tc", "simt"], default="tc")
     ap.add_argument("--storage", choices=["packed", "dense", "none", "packed16"], default="packed")
-    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--gemv-reps", type=int, default=10)
     ap.add_argument("--ref-rows", type=int, default=256)
     ap.add_argument("--ref-iters", type=int, default=7)
