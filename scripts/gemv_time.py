@@ -23,4 +23,4 @@ torch.cuda.synchronize()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 e0.record(); [run() for _ in range(20)]; e1.record(); e1.synchronize()
 ms = e0.elapsed_time(e1) / 20
-print(f"ablate={os.environ.get('GPIC_SYM_ABLATE','0')}: {ms:.3f} ms  {ntiles*65536/ms/1e6:.0f} GB/s")
+print(f"sym GEMV: {ms:.3f} ms  {ntiles*65536/ms/1e6:.0f} GB/s")
