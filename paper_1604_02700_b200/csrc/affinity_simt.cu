@@ -31,7 +31,7 @@ constexpr int BM = 128, BN = 128, BK = 16, PADS = 4;
 // KD > 0: the data has at most KD (<= 16) non-zero features: one K chunk
 // whose inner loop stops at KD (the padding columns are zero either way).
 template <bool DIFF, bool PACKED, int KD>
-__global__ void __launch_bounds__(256, 2)
+__global__ void __launch_bounds__(256, KD == 2 ? 3 : 2)
     affinity_simt_kernel(const float* __restrict__ xc, const float* __restrict__ sqn, int64_t n, int32_t dp, int64_t row_lo,
                          int64_t row_hi, float neg_scale_log2, float* __restrict__ a, int64_t lda,
                          float* __restrict__ rowpart, int64_t rows_pad, int kind,
