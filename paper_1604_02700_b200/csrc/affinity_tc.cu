@@ -681,13 +681,22 @@ __global__ void __launch_bounds__(kCtaThreads<MODE>, 1)
                            : "memory");
             }
           } else {
+            // a 64-bit store is served 16 lanes at a time: with every lane on
+            // the same column block, lanes (tq, upper pair) and (tq ^ 1,
+            // lower pair) hit one 16-byte chunk (2-way conflict). The upper
+            // column pair of each quad stores block blk ^ 2 in the same
+            // instruction instead, which moves it to the other 64 bytes.
+            const bool up = tc & 4;
 #pragma unroll
             for (int x = 0; x < 32; x += 2) {
+              const int xs = x ^ 8;
               const int R = (x >> 4) * 16 + tq + ((x >> 1) & 1) * 8;
-              const int cq = ((x >> 2) & 3) * 2 + (tc >> 2);  // 16-byte chunk of the columns
+              const int blk = ((x >> 2) & 3) ^ (up ? 2 : 0);
+              const int cq = blk * 2 + (tc >> 2);  // 16-byte chunk of the columns
               const uint32_t addr = su32(stage) + R * 128 + ((cq ^ (R & 7)) << 4) + (tc & 3) * 4;
-              asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(addr), "f"(vals[x]),
-                           "f"(vals[x + 1])
+              const float v0 = up ? vals[xs] : vals[x];
+              const float v1 = up ? vals[xs + 1] : vals[x + 1];
+              asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(addr), "f"(v0), "f"(v1)
                            : "memory");
             }
           }
