@@ -134,34 +134,148 @@ class ClockSampler:
 
 
 # ------------------------------------------------------- CPU reference
-def cpu_reference_sample(points, sigma, k, iters, rows, threads):
-    """Time the reference algorithm (oracle port of parallel.py) on `rows`
-    rows and scale to the whole job. Returns (seconds_full_job, detail)."""
-    from oracle import pic_oracle as po
+REF_DIR = ROOT / "baseline" / "_ref"
 
+
+def reference_package():
+    """The unmodified reference package installed into baseline/_ref (see
+    DESIGN.md §9), or None when it is not installed on this host."""
+    if not (REF_DIR / "picluster" / "__init__.py").exists():
+        return None
+    if str(REF_DIR) not in sys.path:
+        sys.path.insert(0, str(REF_DIR))
+    import picluster
+
+    return picluster
+
+
+def host_info(threads):
+    mem = None
+    try:
+        for ln in open("/proc/meminfo"):
+            if ln.startswith("MemTotal:"):
+                mem = round(int(ln.split()[1]) / 2**20, 1)
+    except OSError:
+        pass
+    return {"cores": threads, "os_cpu_count": os.cpu_count(), "host_ram_gib": mem,
+            "OPENBLAS_NUM_THREADS": os.environ.get("OPENBLAS_NUM_THREADS", "unset"),
+            "numpy": np.__version__}
+
+
+def fixture(cfg):
+    """CPU-reference fixture of a benchmark config (tests/golden/config<c>.npz)."""
+    p = ROOT / "tests" / "golden" / f"config{cfg}.npz"
+    return dict(np.load(p)) if p.exists() else None
+
+
+def cpu_reference_sample(points, sigma, k, iters, threads, v_real=None, offset=0, block=None):
+    """One bounded sample of the CPU reference's own pipeline, scaled to the job.
+
+    With the reference installed (baseline/_ref) it runs the reference's own
+    code exactly as parallel.cluster composes it (parallel.py:113-255): its
+    `similarity_rows` per `resolved_chunk_rows(n)`-row block (335 rows at
+    n = 100k, 256 MiB per block) with one block per worker of a
+    `_run_workers` pool of `threads` workers — the memory footprint of every
+    worker of the full run — then `k_rowsum`, `k_normalize` and `iters` x
+    `k_multiply` on those rows, `k_reduce` / `k_norm` / the delta on full
+    n-vectors, and `kmeans_1d` on the real embedding (the committed CPU
+    fixture's v). Row-proportional phases are scaled by n / rows.
+    Without it, the oracle's port of the same steps (kind "port").
+
+    Returns (seconds_full_job, phases, measured_wall_seconds, kind, sample).
+    """
     n = points.shape[0]
-    lo = 0
-    t0 = time.perf_counter()
-    a = po.affinity_rows_threaded(points, lo, lo + rows, sigma, p=threads)   # k_affinity
-    t1 = time.perf_counter()
-    deg = np.einsum("ij->i", a)                                              # k_rowsum
-    w = a / deg[:, None]                                                     # k_normalize
-    t2 = time.perf_counter()
-    v = np.full(n, 1.0 / n)
-    for _ in range(iters):                                                   # k_multiply
-        po.matvec_threaded(w, v, threads)
-    t3 = time.perf_counter()
+    ref = reference_package()
+    if ref is not None:
+        from picluster import parallel as P
+        from picluster.affinity import GaussianRbf as RefRbf
+        from picluster.affinity import similarity_rows
+        from picluster.kmeans import KMeansParams as RefKM
+        from picluster.kmeans import kmeans_1d
+
+        cfgk = P.KernelConfig(p=threads)
+        chunk = cfgk.resolved_chunk_rows(n)
+        if block is not None:  # shorter blocks (still far beyond the LLC) for many-step runs
+            chunk = min(chunk, block)
+        kind = RefRbf(sigma)
+        step = max(1, n // threads)
+        starts = [((offset + w) * step) % max(1, n - chunk + 1) for w in range(threads)]
+        rows = chunk * threads
+        t0 = time.perf_counter()
+        a = np.empty((rows, n))
+
+        def worker(lo, hi):  # one 256 MiB block per worker, as k_affinity's workers do
+            w = lo // chunk
+            a[lo:hi] = similarity_rows(points, starts[w], starts[w] + (hi - lo), kind)
+
+        P._run_workers(worker, P.PartitionPlan(tuple((w * chunk, (w + 1) * chunk)
+                                                     for w in range(threads))), threads)
+        t1 = time.perf_counter()
+        deg = P.k_rowsum(a, cfgk)
+        w_ = P.k_normalize(a, deg, cfgk)
+        del a
+        t2 = time.perf_counter()
+        v = np.full(n, 1.0 / n)
+        t_mul = t_vec = 0.0
+        for _ in range(iters):
+            s0 = time.perf_counter()
+            P.k_multiply(w_, v, cfgk)
+            s1 = time.perf_counter()
+            tau = P.k_reduce(v, cfgk)
+            v_next = P.k_norm(v, tau, cfgk)
+            float(np.max(np.abs(v_next - v)))
+            s2 = time.perf_counter()
+            t_mul += s1 - s0
+            t_vec += s2 - s1
+        del w_
+        vk = v_real if v_real is not None else v
+        t4 = time.perf_counter()
+        kmeans_1d(np.asarray(vk, dtype=np.float64), RefKM(k=k, seed=0))
+        t5 = time.perf_counter()
+        kind_s = "reference"
+        sample = (f"the reference's own parallel-backend code (baseline/_ref picluster): "
+                  f"{threads} workers x one {chunk}-row block (resolved_chunk_rows(n) = "
+                  f"{cfgk.resolved_chunk_rows(n)}) = {rows} of {n} "
+                  f"affinity rows + k_rowsum/k_normalize + {iters} k_multiply on them, scaled "
+                  f"x{n / rows:.1f}; k_reduce/k_norm on full vectors; kmeans_1d on the "
+                  f"{'CPU-reference embedding' if v_real is not None else 'uniform vector'} (n={n})")
+    else:
+        from oracle import pic_oracle as po
+
+        chunk = po.chunk_rows(n)
+        rows = chunk * threads
+        t0 = time.perf_counter()
+        a = po.affinity_rows_threaded(points, 0, rows, sigma, p=threads)
+        t1 = time.perf_counter()
+        deg = np.einsum("ij->i", a)
+        w_ = a / deg[:, None]
+        del a
+        t2 = time.perf_counter()
+        v = np.full(n, 1.0 / n)
+        t_mul = t_vec = 0.0
+        for _ in range(iters):
+            s0 = time.perf_counter()
+            po.matvec_threaded(w_, v, threads)
+            s1 = time.perf_counter()
+            v_next = v / po.tree_sum(v)
+            float(np.max(np.abs(v_next - v)))
+            s2 = time.perf_counter()
+            t_mul += s1 - s0
+            t_vec += s2 - s1
+        del w_
+        vk = v_real if v_real is not None else v
+        t4 = time.perf_counter()
+        po.kmeans_1d(np.asarray(vk, dtype=np.float64), k, 0)
+        t5 = time.perf_counter()
+        kind_s = "port"
+        sample = (f"oracle port of the reference's parallel backend: {rows} of {n} affinity rows "
+                  f"in {chunk}-row blocks + {iters} matvecs, scaled x{n / rows:.1f}; k-means on "
+                  f"n={n}")
     scale = n / rows
-    # PIC-like embedding: one level per blob (level ~ blob size), 1e-3 noise
-    lab = np.repeat(np.arange(k), np.bincount(np.arange(n) * k // n, minlength=k))
-    vals = (1.0 + lab) / n * (1.0 + 1e-3 * np.random.default_rng(0).standard_normal(n))
-    t4 = time.perf_counter()
-    po.lloyd(vals, k, 0)                                                     # k-means (n > 4096: no polish)
-    t5 = time.perf_counter()
-    full = (t1 - t0) * scale + (t2 - t1) * scale + (t3 - t2) * scale + (t5 - t4)
-    detail = {"affinity_s": (t1 - t0) * scale, "rowsum_normalize_s": (t2 - t1) * scale,
-              "iterate_s": (t3 - t2) * scale, "kmeans_s": t5 - t4}
-    return full, detail, t5 - t0
+    phases = {"affinity_s": (t1 - t0) * scale, "rowsum_normalize_s": (t2 - t1) * scale,
+              "iterate_s": t_mul * scale + t_vec, "kmeans_s": t5 - t4}
+    full = sum(phases.values())
+    return full, phases, (t5 - t0), kind_s, sample
 
 
 def run_reference(args, cfg, rank):
@@ -170,27 +284,37 @@ def run_reference(args, cfg, rank):
     c = CONFIGS[cfg]
     d = config_dataset(cfg, seed=0)
     threads = os.cpu_count() or 1
-    rows = args.ref_rows
-    iters = args.ref_iters
-    times, details, wall = [], None, 0.0
-    for i in range(args.warmup + args.steps):
-        full, det, w = cpu_reference_sample(d.points, c["sigma"], c["k"], iters, rows, threads)
+    fx = fixture(cfg)
+    iters = int(fx["iterations"]) if fx is not None else args.ref_iters
+    v_real = fx["v"] if fx is not None else None
+    times, phases, walls = [], [], []
+    kind = sample = None
+    # bounded run: one reference-sized 256 MiB block per worker costs ~23 s
+    # at config 3 on 16 cores; with many steps each worker's block shrinks
+    # (>= 64 MiB, still ~1000x the LLC share, so the run stays memory-bound
+    # like the full job) so that W + K steps end within ~3 minutes
+    nsteps = args.warmup + args.steps
+    chunk_full = max(1, min(c["n"], 256 * 1024 * 1024 // (8 * c["n"])))
+    block = max(min(chunk_full, 16), chunk_full * 8 // max(nsteps, 8))
+    for i in range(nsteps):
+        full, det, w, kind, sample = cpu_reference_sample(d.points, c["sigma"], c["k"], iters,
+                                                          threads, v_real, offset=i, block=block)
         if i >= args.warmup:
             times.append(full)
-            details = det
-            wall += w
+            phases.append(det)
+            walls.append(w)
     value = statistics.mean(times)
-    sample = (f"{rows} of {c['n']} affinity rows + {iters} matvecs on them, scaled x{c['n'] / rows:.1f};"
-              f" k-means on n={c['n']} (extrapolated full-job seconds)")
     line = {
         "metric": METRIC, "value": value, "unit": "s", "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": value * 1e3, "higher_is_better": False,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "impl": "reference",
+        "data": "synthetic (SURVEY App. B gaussian blobs, seed 0)", "impl": "reference",
         "config": workload(cfg, args.gpus),
-        "cpu_baseline": {"value": value, "unit": "s", "cores": threads, "kind": "port",
-                         "sample": sample, "phases": details,
-                         "measured_cpu_seconds_per_step": wall / max(args.steps, 1)},
+        "cpu_baseline": dict(value=value, unit="s", kind=kind, sample=sample,
+                             phases={k: statistics.mean(p[k] for p in phases) for k in phases[0]},
+                             extrapolated=True,
+                             measured_cpu_seconds_per_step=statistics.mean(walls),
+                             **host_info(threads)),
         "e2e": {"value": value, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -332,7 +456,7 @@ def run_ours(args, cfg, rank, world):
 
     def step():
         rc = L.gpic_cluster(C.c_void_p(x.data_ptr()), n, m, sigma, _lib.KIND_RBF, k, eps, T, first,
-                            u.ctypes.data_as(C.c_void_p), impl, storage,
+                            u.ctypes.data_as(C.c_void_p), impl, storage, None,
                             C.c_void_p(labels.data_ptr()), C.c_void_p(v.data_ptr()),
                             C.c_void_p(hist.data_ptr()), C.byref(iters), C.byref(conv),
                             C.c_void_p(work.data_ptr()), nbytes, st)
@@ -354,6 +478,16 @@ def run_ours(args, cfg, rank, world):
     ms = ev0.elapsed_time(ev1) / args.steps
     lab_np = labels.cpu().numpy()
     ari = adjusted_rand_index(contingency(d.labels, lab_np))
+    fx = fixture(cfg)
+    parity = None
+    if fx is not None:
+        ref_lab = fx["labels"].astype(np.int64)
+        v_np = v.cpu().numpy()
+        parity = {"ari_vs_cpu": adjusted_rand_index(contingency(ref_lab, lab_np)),
+                  "labels_identical": bool(np.array_equal(ref_lab, lab_np)),
+                  "iterations_cpu": int(fx["iterations"]),
+                  "rel_l1_v_vs_cpu": float(np.abs(v_np - fx["v"]).sum() / np.abs(fx["v"]).sum()),
+                  "cpu_reference": str(fx["provenance"])}
 
     kname, alg_bytes, gemv_ms = _gemv_roofline(args, L, C, torch, stream, st, n, m, k, T, work,
                                                v, storage)
@@ -402,9 +536,12 @@ def run_ours(args, cfg, rank, world):
                   if storage != 3 else
                   "f16 W storage (fp32 Gram/exp, fp32 accumulate; fp64 vectors/reductions)"),
         "data": "synthetic (SURVEY App. B gaussian blobs, seed 0)",
-        "config": dict(workload(cfg, world), affinity_engine=impl_name, storage=args.storage),
+        "config": workload(cfg, world),
+        "engine": {"affinity_engine": impl_name, "storage": args.storage},
         "power_iter_hbm_gbs": achieved, "power_iter_dense_equiv_gbs": dense_equiv,
         "iterations": int(iters.value), "converged": bool(conv.value), "ari_vs_truth": ari,
+        "ari_vs_cpu": parity["ari_vs_cpu"] if parity else None,
+        "parity_vs_cpu": parity,
         "roofline": {"kernel": kname, "bound": bound, "achieved": achieved, "peak": peak,
                      "peak_kind": peak_kind, "unit": unit, "frac": achieved / peak,
                      "traffic": traffic,
@@ -419,12 +556,12 @@ def run_ours(args, cfg, rank, world):
     }
     if not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
-        full, det, _ = cpu_reference_sample(d.points, sigma, k, max(int(iters.value), 1),
-                                            args.ref_rows, threads)
-        line["cpu_baseline"] = {"value": full, "unit": "s", "cores": threads, "kind": "port",
-                                "sample": f"{args.ref_rows} of {n} affinity rows + matvecs, "
-                                          f"scaled x{n / args.ref_rows:.1f}; k-means on full n",
-                                "phases": det}
+        full, det, wall, kind_s, sample = cpu_reference_sample(
+            d.points, sigma, k, max(int(iters.value), 1), threads,
+            fx["v"] if fx is not None else None)
+        line["cpu_baseline"] = dict(value=full, unit="s", kind=kind_s, sample=sample, phases=det,
+                                    extrapolated=True, measured_cpu_seconds=wall,
+                                    **host_info(threads))
     print(json.dumps(line), flush=True)
 
 
@@ -503,12 +640,16 @@ def run_ours_sharded(args, cfg, rank, world):
             "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
             "dtype": "f32 (3-term fp16-split tensor Gram, fp32 accumulate; fp64 vectors/reductions)",
             "data": "synthetic (SURVEY App. B gaussian blobs, seed 0)",
-            "config": dict(workload(cfg, world), affinity_engine=args.engine, storage=storage,
+            "config": dict(workload(cfg, world),
                            parallelism=(f"packed symmetric super-row shards x{world}, P2P partial-y "
                                         "exchange summed in rank order" if storage == "packed" else
                                         f"row-shard x{world}, fused P2P y all-gather")),
+            "engine": {"affinity_engine": args.engine, "storage": storage},
             "iterations": trace.iterations_run, "converged": trace.converged,
             "ari_vs_truth": adjusted_rand_index(contingency(d.labels, lab_np)),
+            "ari_vs_cpu": (adjusted_rand_index(contingency(fixture(cfg)["labels"].astype(np.int64),
+                                                           lab_np))
+                           if fixture(cfg) is not None else None),
             "ranks_agree_bitwise": agree,
             "e2e": {"value": float(te.item()), "unit": "s", "h2d_bytes_per_step": int(n * m * 8),
                     "d2h_bytes_per_step": int(n * 8 * 2)},
@@ -529,7 +670,6 @@ def main():
     ap.add_argument("--storage", choices=["packed", "dense", "none", "packed16"], default="packed")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--gemv-reps", type=int, default=10)
-    ap.add_argument("--ref-rows", type=int, default=256)
     ap.add_argument("--ref-iters", type=int, default=7)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--report", default=None,

@@ -85,6 +85,14 @@ typedef struct gpic_ctl {
 const char* gpic_version(void);
 /* Last host-side error message (thread-local). */
 const char* gpic_last_error(void);
+/* Status of the last failure with its detail (thread-local): index = first
+ * offending row for ZeroDegree / ZeroVector, (index, index2) = (row, col)
+ * for NonFiniteEntry, value = tau for NonPositiveTau; -1 / 0 otherwise. */
+int gpic_last_detail(int64_t* index, int64_t* index2, double* value);
+/* Device memory for bindings without a CUDA allocator of their own (cgo,
+ * JNI, a bare ctypes caller); never used on the hot path. */
+int gpic_malloc(int64_t bytes, void** out);
+int gpic_free(void* ptr);
 
 /* Bytes of device scratch the pipeline needs for n points of dimension d,
  * k clusters, a row shard of `rows` rows and `max_iter` iterations. */
@@ -107,7 +115,9 @@ int64_t gpic_affinity_pitch(int64_t n);
  *          -(s^2/2)|x_i - x_j|^2 directly
  *   d_sqn  |xc|^2 per row; d_sqn[n_pad - 1] (a padding row) holds 1 / s^2
  * A non-finite entry sets GPIC_E_NONFINITE with the first (row, col) in
- * row-major order. d_work: (ceil(n / 256) + 1) * d + 1 doubles.
+ * row-major order. d_work: (ceil(n / 256) + 1) * d + 2 doubles; after the
+ * call its last two hold max |xc| over all entries and R^2 = max_i |xc_i|^2
+ * (RBF), the spread that gpic_engine_for routes on.
  * kind GPIC_KIND_COSINE instead scales every row to unit length in fp64
  * (no centring: cosine is not translation invariant) and reports a zero
  * row as GPIC_E_ZERO_VECTOR(first row) (cosine_norms, affinity.py:41-53). */
@@ -116,6 +126,14 @@ int64_t gpic_row_pad(int64_t n);
 int64_t gpic_operand_floats(int64_t n, int32_t d);
 int gpic_prepare_points(const double* d_x, int64_t n, int32_t d, int32_t kind, float* d_xhi,
                         float* d_xlo, float* d_sqn, void* d_work, gpic_ctl* d_ctl, void* stream);
+/* The affinity engine a storage runs for data of spread R^2 (max squared
+ * distance to the mean, from gpic_prepare_points): the tensor engine's Gram
+ * form carries ~2^-24 R^2 / (2 sigma^2) relative error per entry, so RBF
+ * data with R^2 / (2 sigma^2) > 167.8 (2^24 x 1e-5: a tenth of the 1e-4
+ * embedding gate) and RBF at d <= 8 run the SIMT difference form; d > 192
+ * with stored A runs SIMT dense rows. gpic_cluster applies this itself. */
+int32_t gpic_engine_for(int32_t kind, int32_t d, double sigma, double spread2, int32_t impl,
+                        int32_t storage);
 
 /* ---- stage 1: affinity block + degree ---------------------------------
  * Replaces similarity_rows/build_affinity (affinity.py:74-110, RBF kind),
@@ -212,7 +230,11 @@ int64_t gpic_vector_pitch(int64_t n);
  * cluster (serial.py:131-150 / parallel.py:236-255) for one rank owning the
  * whole matrix. Device in/out; d_work must hold
  * gpic_cluster_workspace_bytes(n, d, k, max_iter, storage). Synchronous:
- * returns the first error.
+ * returns the first error. d_v0: NULL starts from d / sum(d) (the "degree"
+ * choice, initial_embedding parallel.py:210-214); otherwise n doubles of an
+ * explicit start vector, already validated by the caller like
+ * initial_vector (serial.py:77-101: "uniform" = 1/n, or length n,
+ * nonnegative, unit L1 norm).
  *
  * storage: GPIC_STORAGE_DENSE keeps A as n x pitch(n) fp32 rows (4n^2 bytes
  * per power iteration); GPIC_STORAGE_PACKED keeps only the upper triangle
@@ -235,7 +257,7 @@ int64_t gpic_cluster_workspace_bytes(int64_t n, int32_t d, int32_t k, int32_t ma
                                      int32_t storage);
 int gpic_cluster(const double* d_x, int64_t n, int32_t d, double sigma, int32_t kind, int32_t k,
                  double eps, int32_t max_iter, int64_t first_index, const double* h_uniforms,
-                 int32_t impl, int32_t storage, int64_t* d_labels, double* d_v,
+                 int32_t impl, int32_t storage, const double* d_v0, int64_t* d_labels, double* d_v,
                  double* d_delta_hist, int32_t* h_iters, int32_t* h_converged, void* d_work,
                  int64_t work_bytes, void* stream);
 
@@ -244,19 +266,27 @@ int gpic_cluster(const double* d_x, int64_t n, int32_t d, double sigma, int32_t 
  * {affinity, rowsum, normalize (0: folded into the GEMV), iterate, kmeans}. */
 int gpic_cluster_timed(const double* d_x, int64_t n, int32_t d, double sigma, int32_t kind,
                        int32_t k, double eps, int32_t max_iter, int64_t first_index,
-                       const double* h_uniforms, int32_t impl, int32_t storage, int64_t* d_labels,
-                       double* d_v, double* d_delta_hist, int32_t* h_iters, int32_t* h_converged,
-                       void* d_work, int64_t work_bytes, void* stream, float* h_phase_ms);
+                       const double* h_uniforms, int32_t impl, int32_t storage,
+                       const double* d_v0, int64_t* d_labels, double* d_v, double* d_delta_hist,
+                       int32_t* h_iters, int32_t* h_converged, void* d_work, int64_t work_bytes,
+                       void* stream, float* h_phase_ms);
 
 /* Same, HOST buffers in and out (the reference-facing call a ctypes/cffi
- * binding makes): copies X in, runs, copies labels/v/deltas out. d_work
- * must hold gpic_cluster_workspace_bytes(...) (256-aligned) + the staging
- * of X (n*d*8), labels and v (n*8 each) and the deltas (max_iter*8). */
+ * binding makes, replacing picluster.cluster(...) of __init__.py:39-45 /
+ * parallel.cluster, parallel.py:236-255): copies X in, runs, copies
+ * labels/v/deltas out. d_work must hold gpic_cluster_host_workspace_bytes
+ * (= gpic_cluster_workspace_bytes, 256-aligned, + the staging of X (n*d*8),
+ * labels, v and v0 (n*8 each) and the deltas (max_iter*8)); h_v0 as d_v0. On failure the
+ * status code is returned and gpic_last_detail() gives the offending index
+ * (ZeroDegree / ZeroVector), (row, col) (NonFiniteEntry) or tau. */
+int64_t gpic_cluster_host_workspace_bytes(int64_t n, int32_t d, int32_t k, int32_t max_iter,
+                                          int32_t storage);
 int gpic_cluster_host(const double* h_x, int64_t n, int32_t d, double sigma, int32_t kind,
                       int32_t k, double eps, int32_t max_iter, int64_t first_index,
-                      const double* h_uniforms, int32_t impl, int32_t storage, int64_t* h_labels,
-                      double* h_v, double* h_delta_hist, int32_t* h_iters, int32_t* h_converged,
-                      void* d_work, int64_t work_bytes, void* stream);
+                      const double* h_uniforms, int32_t impl, int32_t storage,
+                      const double* h_v0, int64_t* h_labels, double* h_v, double* h_delta_hist,
+                      int32_t* h_iters, int32_t* h_converged, void* d_work, int64_t work_bytes,
+                      void* stream);
 
 /* Reset a control block (iteration 0, no error) with the stop threshold and
  * iteration cap of the run. */
@@ -310,6 +340,11 @@ typedef struct gpic_shard {
   double sigma;
   int32_t kind;       /* GPIC_KIND_*                                          */
   double* ypart;      /* gpic_mf_ypart_doubles(n, d, rows) doubles          */
+  /* the caller's fp64 points (n x d, row-major, every rank holds all of X):
+   * rows whose fp32 degree underflows (isolated points) are redone from them
+   * in fp64 like the reference (affinity.py:96-119); may be null when no
+   * such row exists (gpic_comm_gather_degrees then fails with INVALID) */
+  const double* x;
 } gpic_shard;
 
 /* Packed shards (symmetric storage across ranks, GPIC_STORAGE_PACKED in
@@ -348,12 +383,13 @@ int gpic_comm_destroy(gpic_comm* comm);
  * check; optionally copies the full degree vector out. Synchronous. */
 int gpic_comm_gather_degrees(gpic_comm* comm, const gpic_shard* shards, int32_t nlocal,
                              double* d_deg_full_out, void* stream);
-/* v0 = d / tree_sum(d), then the device-resident loop. d_hist holds
- * nlocal x max_iter doubles, d_vout nlocal x n (every shard ends with the
- * same full embedding), h_ctl nlocal control blocks. Synchronous. */
+/* v0 = d / tree_sum(d) (d_v0 NULL) or the explicit d_v0 (n doubles, see
+ * gpic_cluster), then the device-resident loop. d_hist holds nlocal x
+ * max_iter doubles, d_vout nlocal x n (every shard ends with the same full
+ * embedding), h_ctl nlocal control blocks. Synchronous. */
 int gpic_comm_iterate(gpic_comm* comm, const gpic_shard* shards, int32_t nlocal, double eps,
-                      int32_t max_iter, double* d_hist, double* d_vout, gpic_ctl* h_ctl,
-                      void* stream);
+                      int32_t max_iter, const double* d_v0, double* d_hist, double* d_vout,
+                      gpic_ctl* h_ctl, void* stream);
 
 /* ---- batched small-n PIC (Experiment II: cli.py:230-256)
  * `count` independent problems of n_b = h_offsets[b+1] - h_offsets[b]

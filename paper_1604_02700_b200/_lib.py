@@ -79,6 +79,11 @@ SIGNATURES = {
     "gpic_operand_floats": (I64, [I64, I32]),
     "gpic_ctl_init": (C.c_int, [P, F64, I32, P]),
     "gpic_prepare_points": (C.c_int, [P, I64, I32, I32, P, P, P, P, P, P]),
+    "gpic_engine_for": (I32, [I32, I32, C.c_double, C.c_double, I32, I32]),
+    "gpic_last_detail": (C.c_int, [P, P, P]),
+    "gpic_malloc": (C.c_int, [I64, P]),
+    "gpic_free": (C.c_int, [P]),
+    "gpic_cluster_host_workspace_bytes": (I64, [I64, I32, I32, I32, I32]),
     "gpic_affinity_rbf": (C.c_int, [P, P, P, I64, I32, I64, I64, F64, I32, P, I64, P, P, P, P]),
     "gpic_affinity_cosine": (C.c_int, [P, P, P, I64, I32, I64, I64, I32, P, I64, P, P, P, P]),
     "gpic_initial_vector": (C.c_int, [P, I64, P, P, P, P, P]),
@@ -102,15 +107,17 @@ SIGNATURES = {
     "gpic_packed_shard_scratch_bytes": (I64, [I64, I64, I64]),
     "gpic_packed_shard_build": (C.c_int, [P, P, P, I64, I32, I64, I64, C.c_double, I32, P, P, P, P]),
     "gpic_cluster_workspace_bytes": (I64, [I64, I32, I32, I32, I32]),
+    # (x, n, d, sigma, kind, k, eps, max_iter, first, uniforms, impl, storage, v0,
+    #  labels, v, hist, iters, converged, work, work_bytes, stream[, phase_ms])
     "gpic_cluster": (C.c_int, [P, I64, I32, F64, I32, I32, F64, I32, I64, P, I32, I32, P, P, P,
-                               P, P, P, I64, P]),
+                               P, P, P, P, I64, P]),
     "gpic_cluster_timed": (C.c_int, [P, I64, I32, F64, I32, I32, F64, I32, I64, P, I32, I32, P, P,
-                                     P, P, P, P, I64, P, P]),
+                                     P, P, P, P, P, I64, P, P]),
     "gpic_batch_workspace_bytes": (I64, [P, I32, I32, I32, I32]),
     "gpic_cluster_batch": (C.c_int, [P, P, I32, I32, F64, I32, I32, P, I32, P, P, P, P, P, P, P,
                                      I64, P]),
     "gpic_cluster_host": (C.c_int, [P, I64, I32, F64, I32, I32, F64, I32, I64, P, I32, I32, P, P,
-                                    P, P, P, P, I64, P]),
+                                    P, P, P, P, P, I64, P]),
     "gpic_ctl_read": (C.c_int, [P, P, P]),
     "gpic_launch_count": (I64, []),
     "gpic_comm_create": (C.c_int, [I32, I32, I64, P, P]),
@@ -118,7 +125,7 @@ SIGNATURES = {
     "gpic_comm_create_virtual": (C.c_int, [I32, I64, P]),
     "gpic_comm_destroy": (C.c_int, [P]),
     "gpic_comm_gather_degrees": (C.c_int, [P, P, I32, P, P]),
-    "gpic_comm_iterate": (C.c_int, [P, P, I32, F64, I32, P, P, P, P]),
+    "gpic_comm_iterate": (C.c_int, [P, P, I32, F64, I32, P, P, P, P, P]),
 }
 
 IPC_HANDLE_BYTES = 64
@@ -131,7 +138,8 @@ class Shard(C.Structure):
     _fields_ = [("a", C.c_void_p), ("lda", C.c_int64), ("deg", C.c_void_p),
                 ("row_lo", C.c_int64), ("rows", C.c_int64), ("storage", C.c_int32),
                 ("d", C.c_int32), ("xhi", C.c_void_p), ("xlo", C.c_void_p), ("sqn", C.c_void_p),
-                ("sigma", C.c_double), ("kind", C.c_int32), ("ypart", C.c_void_p)]
+                ("sigma", C.c_double), ("kind", C.c_int32), ("ypart", C.c_void_p),
+                ("x", C.c_void_p)]
 
 _lib = None
 

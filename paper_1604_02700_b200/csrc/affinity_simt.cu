@@ -190,7 +190,7 @@ __global__ void degree_kernel(const float* __restrict__ rowpart, int64_t rows, i
   double s = 0.0;
   for (int64_t t = 0; t < n_ctiles; ++t) s += (double)rowpart[t * rows_pad + i];
   deg[i] = s;
-  if (s <= 0.0) raise_status(ctl, GPIC_E_ZERO_DEGREE, row_lo + i, -1, s);
+  if (ctl != nullptr && s <= 0.0) raise_status(ctl, GPIC_E_ZERO_DEGREE, row_lo + i, -1, s);
 }
 
 }  // namespace

@@ -13,6 +13,13 @@ namespace gpic {
 
 unsigned long long g_launches = 0;
 static thread_local std::string g_err;
+// detail of the last failure (gpic_last_detail): status, index / (row, col), value
+struct LastDetail {
+  int status = GPIC_OK;
+  int64_t index = -1, index2 = -1;
+  double value = 0.0;
+};
+static thread_local LastDetail g_detail;
 
 int fail_cuda(cudaError_t e, const char* what) {
   g_err = std::string("CUDA error ") + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) +
@@ -22,6 +29,8 @@ int fail_cuda(cudaError_t e, const char* what) {
 
 int fail(int code, const char* msg) {
   g_err = msg;
+  g_detail = LastDetail();
+  g_detail.status = code;
   return code;
 }
 
@@ -46,7 +55,7 @@ int64_t workspace_bytes(int64_t n, int32_t d, int32_t k, int64_t rows, int32_t /
   b += al(npad * dp * 4);                     // xlo
   b += al(npad * 4);                          // sqn
   b += al(ceil_div(n, 256) * d * 8);          // colpart
-  b += al((int64_t)(d + 1) * 8);              // mean + max|x - mean|
+  b += al((int64_t)(d + 2) * 8);              // mean + max|x - mean| + spread R^2
   b += al(n_ctiles * rows_pad * 4);           // rowpart
   b += al((ceil_div(n, kRedBlock) + 1) * 8);  // redpart
   b += al(n * 8);                             // y
@@ -54,6 +63,7 @@ int64_t workspace_bytes(int64_t n, int32_t d, int32_t k, int64_t rows, int32_t /
   b += al(2 * n * 8);                         // v64
   b += al(vector_pitch(n) * 4);               // v32
   b += al(kmeans_scratch_bytes(n, k));        // kmeans
+  b += al(n * 8) + al(8);                     // low-degree row list + count
   return b;
 }
 
@@ -74,7 +84,7 @@ int carve(void* base, int64_t bytes, int64_t n, int32_t d, int32_t k, int64_t ro
   ws->xlo = reinterpret_cast<float*>(take(npad * dp * 4));
   ws->sqn = reinterpret_cast<float*>(take(npad * 4));
   ws->colpart = reinterpret_cast<double*>(take(ceil_div(n, 256) * d * 8));
-  ws->mean = reinterpret_cast<double*>(take((int64_t)(d + 1) * 8));
+  ws->mean = reinterpret_cast<double*>(take((int64_t)(d + 2) * 8));
   ws->rowpart = reinterpret_cast<float*>(take(n_ctiles * rows_pad * 4));
   ws->redpart = reinterpret_cast<double*>(take((ceil_div(n, kRedBlock) + 1) * 8));
   ws->y = reinterpret_cast<double*>(take(n * 8));
@@ -83,32 +93,51 @@ int carve(void* base, int64_t bytes, int64_t n, int32_t d, int32_t k, int64_t ro
   ws->v32 = reinterpret_cast<float*>(take(vector_pitch(n) * 4));
   ws->kscratch_bytes = kmeans_scratch_bytes(n, k);
   ws->kscratch = reinterpret_cast<double*>(take(ws->kscratch_bytes));
+  ws->lowlist = reinterpret_cast<int64_t*>(take(n * 8));
+  ws->lowcount = reinterpret_cast<unsigned long long*>(take(8));
   ws->end = p;
   return GPIC_OK;
 }
 
+static int status_text(const gpic_ctl& h, int32_t d, char* buf, size_t cap);
+
 static int status_from_ctl(const gpic_ctl& h, int32_t d) {
   char buf[256];
+  const int rc = status_text(h, d, buf, sizeof buf);
+  if (rc != GPIC_OK) {
+    g_detail.status = rc;
+    g_detail.index = h.err_index;
+    g_detail.index2 = -1;
+    g_detail.value = h.err_value;
+    if (rc == GPIC_E_NONFINITE) {
+      g_detail.index = h.err_index / (d > 0 ? d : 1);
+      g_detail.index2 = h.err_index % (d > 0 ? d : 1);
+    }
+  }
+  return rc;
+}
+
+static int status_text(const gpic_ctl& h, int32_t d, char* buf, size_t cap) {
   switch (h.status) {
     case GPIC_OK:
       return GPIC_OK;
     case GPIC_E_ZERO_DEGREE:
-      snprintf(buf, sizeof buf, "row %lld has zero degree", (long long)h.err_index);
+      snprintf(buf, cap, "row %lld has zero degree", (long long)h.err_index);
       return fail(h.status, buf);
     case GPIC_E_NONFINITE:
-      snprintf(buf, sizeof buf, "non-finite value at row %lld column %lld",
+      snprintf(buf, cap, "non-finite value at row %lld column %lld",
                (long long)(h.err_index / (d > 0 ? d : 1)), (long long)(h.err_index % (d > 0 ? d : 1)));
       return fail(h.status, buf);
     case GPIC_E_NONPOS_TAU:
-      snprintf(buf, sizeof buf, "non-positive normaliser %g", h.err_value);
+      snprintf(buf, cap, "non-positive normaliser %g", h.err_value);
       return fail(h.status, buf);
     case GPIC_E_ZERO_VECTOR:
-      snprintf(buf, sizeof buf, "point %lld has zero norm", (long long)h.err_index);
+      snprintf(buf, cap, "point %lld has zero norm", (long long)h.err_index);
       return fail(h.status, buf);
     case GPIC_E_UNSUPPORTED:
       return fail(h.status, "k-means produced non-contiguous clusters (gap repair not on device)");
     default:
-      snprintf(buf, sizeof buf, "device status %d", h.status);
+      snprintf(buf, cap, "device status %d", h.status);
       return fail(h.status, buf);
   }
 }
@@ -121,6 +150,21 @@ extern "C" {
 
 const char* gpic_version(void) { return "gpic 0.1.0 sm_100a"; }
 const char* gpic_last_error(void) { return g_err.c_str(); }
+int gpic_last_detail(int64_t* index, int64_t* index2, double* value) {
+  if (index) *index = g_detail.index;
+  if (index2) *index2 = g_detail.index2;
+  if (value) *value = g_detail.value;
+  return g_detail.status;
+}
+int gpic_malloc(int64_t bytes, void** out) {
+  if (!out || bytes < 0) return fail(GPIC_E_INVALID, "gpic_malloc needs an output pointer");
+  GPIC_CUDA_TRY(cudaMalloc(out, (size_t)(bytes > 0 ? bytes : 1)));
+  return GPIC_OK;
+}
+int gpic_free(void* p) {
+  GPIC_CUDA_TRY(cudaFree(p));
+  return GPIC_OK;
+}
 int64_t gpic_launch_count(void) { return (int64_t)g_launches; }
 
 int64_t gpic_workspace_bytes(int64_t n, int32_t d, int32_t k, int64_t rows, int32_t max_iter) {
@@ -149,7 +193,7 @@ int gpic_prepare_points(const double* d_x, int64_t n, int32_t d, int32_t kind, f
                         float* d_xlo, float* d_sqn, void* d_work, gpic_ctl* d_ctl, void* stream) {
   if (n < 1 || d < 1) return fail(GPIC_E_EMPTY, "dataset must contain at least one point and one feature");
   if (kind != GPIC_KIND_RBF && kind != GPIC_KIND_COSINE) return fail(GPIC_E_INVALID, "unknown kind");
-  // d_work: colpart (ceil(n/256) * d doubles) followed by mean (d + 1 doubles)
+  // d_work: colpart (ceil(n/256) * d doubles) followed by mean (d + 2 doubles)
   double* colpart = static_cast<double*>(d_work);
   double* mean = colpart + ceil_div(n, 256) * d;
   launch_prepare(d_x, n, d, d_xhi, d_xlo, d_sqn, colpart, mean, d_ctl,
@@ -170,8 +214,16 @@ int gpic_prepare_points(const double* d_x, int64_t n, int32_t d, int32_t kind, f
 //    typical at low d (sigma = sqrt(d)/2); there the tensor Gram also runs
 //    at <= 8/64 of its K width, so the difference form costs nothing.
 //  * matrix-free stays on tcgen05 (an error beyond d = 256).
+//  * RBF whose spread is large against sigma also runs the SIMT difference
+//    form: the Gram form's error is ~2^-24 R^2 / (2 sigma^2) relative per
+//    entry (measured embedding error: 2.8e-6 at config 3, R^2/2s^2 = 64;
+//    4e-7 at config 2, 121), so above R^2/2s^2 = 167.8 (1e-5, a tenth of the
+//    gate) the tensor engine is not used for stored A. Matrix-free and fp16
+//    tiles exist on the tensor engine only and keep it.
 constexpr int32_t kSimtDiffMaxD = 8;
-static void effective_engine(int kind, int32_t d, int32_t* impl, int32_t* storage) {
+constexpr double kTcMaxSpread = 167.77216;  // 2^24 x 1e-5
+static void effective_engine(int kind, int32_t d, int32_t* impl, int32_t* storage,
+                             double spread2 = 0.0, double sigma = 1.0) {
   if (storage && *storage == GPIC_STORAGE_NONE) return;
   if (!tc_supports_pitch(feature_pitch(d), false)) {
     if (*impl == GPIC_AFFINITY_TC) *impl = GPIC_AFFINITY_SIMT;
@@ -179,15 +231,26 @@ static void effective_engine(int kind, int32_t d, int32_t* impl, int32_t* storag
       *storage = GPIC_STORAGE_DENSE;
     return;
   }
-  if (kind == GPIC_KIND_RBF && d <= kSimtDiffMaxD && *impl == GPIC_AFFINITY_TC &&
-      !(storage && *storage == GPIC_STORAGE_PACKED16))
+  if (kind == GPIC_KIND_RBF && *impl == GPIC_AFFINITY_TC &&
+      (d <= kSimtDiffMaxD || spread2 / (2.0 * sigma * sigma) > kTcMaxSpread)) {
+    // the SIMT difference form; it stores fp32, so requested fp16 tiles
+    // become fp32 packed tiles (their workspace is sized for that)
     *impl = GPIC_AFFINITY_SIMT;
+    if (storage && *storage == GPIC_STORAGE_PACKED16) *storage = GPIC_STORAGE_PACKED;
+  }
 }
 
 static int affinity_rows(int kind, const float* d_xhi, const float* d_xlo, const float* d_sqn,
                          int64_t n, int32_t d, int64_t row_lo, int64_t row_hi, double sigma,
                          int32_t impl, float* d_a, int64_t lda, double* d_deg, void* d_work,
                          gpic_ctl* d_ctl, void* stream);
+
+int32_t gpic_engine_for(int32_t kind, int32_t d, double sigma, double spread2, int32_t impl,
+                        int32_t storage) {
+  if (kind == GPIC_KIND_COSINE) sigma = 1.0;
+  effective_engine(kind, d, &impl, &storage, spread2, sigma);
+  return impl;
+}
 
 int gpic_affinity_rbf(const float* d_xhi, const float* d_xlo, const float* d_sqn, int64_t n,
                       int32_t d, int64_t row_lo, int64_t row_hi, double sigma, int32_t impl,
@@ -463,8 +526,8 @@ int64_t gpic_cluster_workspace_bytes(int64_t n, int32_t d, int32_t k, int32_t ma
   const int64_t scratch = workspace_bytes(n, d, k, n, max_iter);
   if (storage == GPIC_STORAGE_PACKED)  // tiles + GEMV partials (2) + degree partials (<= 2 + 4)
     return scratch + packed_tiles(n) * 128 * 128 * 4 + 8 * al(sym_partial_floats(n) * 4);
-  if (storage == GPIC_STORAGE_PACKED16)
-    return scratch + packed_tiles(n) * 128 * 128 * 2 + 8 * al(sym_partial_floats(n) * 4);
+  if (storage == GPIC_STORAGE_PACKED16)  // fp32-sized: a large spread demotes to fp32 tiles
+    return scratch + packed_tiles(n) * 128 * 128 * 4 + 8 * al(sym_partial_floats(n) * 4);
   if (storage == GPIC_STORAGE_NONE)
     return scratch + al(mf_ypart_doubles(n, feature_pitch(d), n) * 8);
   return scratch + n * affinity_pitch(n) * 4;
@@ -474,10 +537,6 @@ namespace {
 __global__ void fill_ones_kernel(float* v, int64_t n, int64_t len) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < len) v[i] = i < n ? 1.f : 0.f;
-}
-__global__ void zero_check_kernel(const double* __restrict__ deg, int64_t n, gpic_ctl* ctl) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n && deg[i] <= 0.0) raise_status(ctl, GPIC_E_ZERO_DEGREE, i, -1, deg[i]);
 }
 }  // namespace
 
@@ -493,7 +552,7 @@ inline void mark(cudaEvent_t* ev, int i, cudaStream_t s) {
 
 int cluster_impl(const double* d_x, int64_t n, int32_t d, double sigma, int32_t kind, int32_t k,
                  double eps, int32_t max_iter, int64_t first_index, const double* h_uniforms,
-                 int32_t impl, int32_t storage, int64_t* d_labels, double* d_v,
+                 int32_t impl, int32_t storage, const double* d_v0, int64_t* d_labels, double* d_v,
                  double* d_delta_hist, int32_t* h_iters, int32_t* h_converged, void* d_work,
                  int64_t work_bytes, void* stream, cudaEvent_t* ev) {
   if (n < 1 || d < 1) return fail(GPIC_E_EMPTY, "dataset must contain at least one point and one feature");
@@ -519,6 +578,13 @@ int cluster_impl(const double* d_x, int64_t n, int32_t d, double sigma, int32_t 
   mark(ev, 0, s);
   launch_ctl_init(ws.ctl, eps, max_iter, s);
   launch_prepare(d_x, n, d, ws.xhi, ws.xlo, ws.sqn, ws.colpart, ws.mean, ws.ctl, s, kind);
+  if (kind == GPIC_KIND_RBF && impl == GPIC_AFFINITY_TC && storage != GPIC_STORAGE_NONE) {
+    // data-driven engine choice: the spread R^2 from the prepare pass
+    double spread2 = 0.0;
+    GPIC_CUDA_TRY(cudaMemcpyAsync(&spread2, ws.mean + d + 1, 8, cudaMemcpyDeviceToHost, s));
+    GPIC_CUDA_TRY(cudaStreamSynchronize(s));
+    effective_engine(kind, d, &impl, &storage, spread2, sigma);
+  }
   const float neg_scale_log2 = (float)(-1.4426950408889634 / (2.0 * sigma * sigma));
   const int32_t dp = feature_pitch(d);
   const int64_t lda = affinity_pitch(n);
@@ -543,7 +609,7 @@ int cluster_impl(const double* d_x, int64_t n, int32_t d, double sigma, int32_t 
       if (rc) return rc;
     }
     mark(ev, 1, s);
-    launch_sym_degree(degrow, degcol, n, packed_row_halves(dp), deg, ws.ctl, s);
+    launch_sym_degree(degrow, degcol, n, packed_row_halves(dp), deg, nullptr, s);
     L.mode = half ? kLoopPacked16 : kLoopPacked;
     L.rowp = rowp;
     L.colp = colp;
@@ -558,8 +624,6 @@ int cluster_impl(const double* d_x, int64_t n, int32_t d, double sigma, int32_t 
     mark(ev, 1, s);  // matrix-free: the degree pass is the first A recompute
     rc = launch_mf_degrees(L.mf, 0, n, ws.v32, ypart, deg, s);
     if (rc) return rc;
-    zero_check_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, s>>>(deg, n, ws.ctl);
-    count_launch();
   } else {
     const int64_t rows_pad = round_up(n, kTileM);
     if (impl == GPIC_AFFINITY_TC) {
@@ -571,12 +635,35 @@ int cluster_impl(const double* d_x, int64_t n, int32_t d, double sigma, int32_t 
                            ws.rowpart, rows_pad, s, kind);
     }
     mark(ev, 1, s);
-    launch_degree(ws.rowpart, n, rows_pad, ceil_div(n, kTileN), 0, deg, ws.ctl, s);
+    launch_degree(ws.rowpart, n, rows_pad, ceil_div(n, kTileN), 0, deg, nullptr, s);
   }
+  // isolated points (H4): rows whose fp32 degree is (nearly) 0 are redone
+  // in fp64 from X; ZeroDegree only when the fp64 degree is 0 (lowdeg.cu)
+  launch_lowdeg_scan(deg, n, kind, ws.lowlist, ws.lowcount, s);
+  LowRows low;
+  low.x = d_x;
+  low.n = n;
+  low.d = d;
+  low.kind = kind;
+  low.sigma = sigma;
+  low.list = ws.lowlist;
+  low.d_count = ws.lowcount;
+  {
+    gpic_ctl h0;
+    GPIC_CUDA_TRY(cudaMemcpyAsync(&h0, ws.ctl, sizeof h0, cudaMemcpyDeviceToHost, s));
+    rc = read_low_count(ws.lowcount, &low.count, s);
+    if (rc) return rc;
+    if (h0.status != GPIC_OK) return status_from_ctl(h0, d);  // e.g. NonFiniteEntry
+  }
+  launch_lowdeg_exact(low, deg, ws.ctl, s);
   mark(ev, 2, s);
-  launch_tree_sum(deg, n, ws.redpart, ws.redpart + ceil_div(n, kRedBlock), ws.ctl, s);
-  launch_scale_vector(deg, n, ws.redpart + ceil_div(n, kRedBlock), ws.v64, ws.v32,
-                      vector_pitch(n), s);
+  if (d_v0 != nullptr) {  // explicit start vector (initial_vector, serial.py:77-101)
+    launch_scale_by(d_v0, n, 1.0, ws.v64, ws.v32, vector_pitch(n), s);
+  } else {                // v0 = d / tree_sum(d) (initial_embedding, parallel.py:210-214)
+    launch_tree_sum(deg, n, ws.redpart, ws.redpart + ceil_div(n, kRedBlock), ws.ctl, s);
+    launch_scale_vector(deg, n, ws.redpart + ceil_div(n, kRedBlock), ws.v64, ws.v32,
+                        vector_pitch(n), s);
+  }
   L.a = a;
   L.lda = lda;
   L.rows = n;
@@ -588,6 +675,8 @@ int cluster_impl(const double* d_x, int64_t n, int32_t d, double sigma, int32_t 
   L.ctl = ws.ctl;
   L.pt.y[0][0] = L.pt.y[0][1] = ws.y;
   L.pt.nranks = 1;
+  L.low = low;
+  L.low_deg = deg;
   rc = run_power_loops(&L, 1, n, max_iter, s);
   if (rc) return rc;
   launch_copy_result(ws.v64, n, d_v, ws.ctl, s);
@@ -616,24 +705,25 @@ extern "C" {
 
 int gpic_cluster(const double* d_x, int64_t n, int32_t d, double sigma, int32_t kind, int32_t k,
                  double eps, int32_t max_iter, int64_t first_index, const double* h_uniforms,
-                 int32_t impl, int32_t storage, int64_t* d_labels, double* d_v,
+                 int32_t impl, int32_t storage, const double* d_v0, int64_t* d_labels, double* d_v,
                  double* d_delta_hist, int32_t* h_iters, int32_t* h_converged, void* d_work,
                  int64_t work_bytes, void* stream) {
   return cluster_impl(d_x, n, d, sigma, kind, k, eps, max_iter, first_index, h_uniforms, impl,
-                      storage, d_labels, d_v, d_delta_hist, h_iters, h_converged, d_work,
+                      storage, d_v0, d_labels, d_v, d_delta_hist, h_iters, h_converged, d_work,
                       work_bytes, stream, nullptr);
 }
 
 int gpic_cluster_timed(const double* d_x, int64_t n, int32_t d, double sigma, int32_t kind,
                        int32_t k, double eps, int32_t max_iter, int64_t first_index,
-                       const double* h_uniforms, int32_t impl, int32_t storage, int64_t* d_labels,
-                       double* d_v, double* d_delta_hist, int32_t* h_iters, int32_t* h_converged,
-                       void* d_work, int64_t work_bytes, void* stream, float* h_phase_ms) {
+                       const double* h_uniforms, int32_t impl, int32_t storage,
+                       const double* d_v0, int64_t* d_labels, double* d_v, double* d_delta_hist,
+                       int32_t* h_iters, int32_t* h_converged, void* d_work, int64_t work_bytes,
+                       void* stream, float* h_phase_ms) {
   if (!h_phase_ms) return fail(GPIC_E_INVALID, "h_phase_ms must point at 5 floats");
   cudaEvent_t ev[5];
   for (int i = 0; i < 5; ++i) GPIC_CUDA_TRY(cudaEventCreate(&ev[i]));
   int rc = cluster_impl(d_x, n, d, sigma, kind, k, eps, max_iter, first_index, h_uniforms, impl,
-                        storage, d_labels, d_v, d_delta_hist, h_iters, h_converged, d_work,
+                        storage, d_v0, d_labels, d_v, d_delta_hist, h_iters, h_converged, d_work,
                         work_bytes, stream, ev);
   if (rc == GPIC_OK) {
     // the final gpic_ctl_read synchronised the stream: all 5 events are complete
@@ -649,26 +739,38 @@ int gpic_cluster_timed(const double* d_x, int64_t n, int32_t d, double sigma, in
   return rc;
 }
 
+int64_t gpic_cluster_host_workspace_bytes(int64_t n, int32_t d, int32_t k, int32_t max_iter,
+                                          int32_t storage) {
+  const int64_t w = gpic_cluster_workspace_bytes(n, d, k, max_iter, storage);
+  if (w < 0 || max_iter < 1) return -1;
+  return al(w) + al(n * d * 8) + al(n * 8) * 3 + al((int64_t)max_iter * 8);
+}
+
 int gpic_cluster_host(const double* h_x, int64_t n, int32_t d, double sigma, int32_t kind,
                       int32_t k, double eps, int32_t max_iter, int64_t first_index,
-                      const double* h_uniforms, int32_t impl, int32_t storage, int64_t* h_labels,
-                      double* h_v, double* h_delta_hist, int32_t* h_iters, int32_t* h_converged,
-                      void* d_work, int64_t work_bytes, void* stream) {
+                      const double* h_uniforms, int32_t impl, int32_t storage,
+                      const double* h_v0, int64_t* h_labels, double* h_v, double* h_delta_hist,
+                      int32_t* h_iters, int32_t* h_converged, void* d_work, int64_t work_bytes,
+                      void* stream) {
   if (n < 1 || d < 1) return fail(GPIC_E_EMPTY, "dataset must contain at least one point and one feature");
+  if (max_iter < 1) return fail(GPIC_E_INVALID, "max_iterations must be at least 1");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  // device staging after the pipeline workspace: X, labels, v, deltas
+  // device staging after the pipeline workspace: X, labels, v, v0, deltas
   const int64_t scratch = al(gpic_cluster_workspace_bytes(n, d, k, max_iter, storage));
-  const int64_t stage = al(n * d * 8) + al(n * 8) * 2 + al((int64_t)max_iter * 8);
-  if (work_bytes < scratch + stage) return fail(GPIC_E_INVALID, "workspace too small (host entry)");
+  if (work_bytes < gpic_cluster_host_workspace_bytes(n, d, k, max_iter, storage))
+    return fail(GPIC_E_INVALID, "workspace too small (gpic_cluster_host_workspace_bytes)");
   uint8_t* p = static_cast<uint8_t*>(d_work) + scratch;
   double* dx = reinterpret_cast<double*>(p); p += al(n * d * 8);
   int64_t* dl = reinterpret_cast<int64_t*>(p); p += al(n * 8);
   double* dv = reinterpret_cast<double*>(p); p += al(n * 8);
+  double* dv0 = reinterpret_cast<double*>(p); p += al(n * 8);
   double* dh = reinterpret_cast<double*>(p);
   GPIC_CUDA_TRY(cudaMemcpyAsync(dx, h_x, n * d * 8, cudaMemcpyHostToDevice, s));
+  if (h_v0) GPIC_CUDA_TRY(cudaMemcpyAsync(dv0, h_v0, n * 8, cudaMemcpyHostToDevice, s));
   int32_t iters = 0, conv = 0;
   int rc = gpic_cluster(dx, n, d, sigma, kind, k, eps, max_iter, first_index, h_uniforms, impl,
-                        storage, dl, dv, dh, &iters, &conv, d_work, scratch, stream);
+                        storage, h_v0 ? dv0 : nullptr, dl, dv, dh, &iters, &conv, d_work, scratch,
+                        stream);
   if (rc) return rc;
   GPIC_CUDA_TRY(cudaMemcpyAsync(h_labels, dl, n * 8, cudaMemcpyDeviceToHost, s));
   GPIC_CUDA_TRY(cudaMemcpyAsync(h_v, dv, n * 8, cudaMemcpyDeviceToHost, s));

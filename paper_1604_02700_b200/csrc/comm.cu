@@ -36,6 +36,8 @@ struct gpic_local_t {
   double* v64;      // 2n
   float* v32;       // pitch(n)
   double* redpart;  // ceil(n/2048) + 1
+  int64_t* lowlist;  // n: isolated rows (lowdeg.cu)
+  unsigned long long* lowcount;
 };
 }  // namespace gpic
 
@@ -51,6 +53,7 @@ struct gpic_comm {
   gpic::gpic_local_t* loc = nullptr;
   uint64_t iter_epoch = 0;
   uint64_t gather_epoch = 0;
+  int64_t low_count = 0;  // isolated rows found by the last degree gather
 };
 
 namespace gpic {
@@ -74,7 +77,7 @@ inline uint64_t* r_flags(uint8_t* r, int64_t n) {
 }
 inline int64_t local_bytes(int64_t n) {
   return al(sizeof(gpic_ctl)) + al(2 * n * 8) + al(vector_pitch(n) * 4) +
-         al((ceil_div(n, kRedBlock) + 1) * 8);
+         al((ceil_div(n, kRedBlock) + 1) * 8) + al(n * 8) + al(8);
 }
 
 PeerTable table(const gpic_comm* c, int self) {
@@ -134,11 +137,17 @@ __global__ void set_epoch_kernel(gpic_ctl* ctl, uint64_t epoch) {
   if (threadIdx.x == 0) ctl->sync_epoch = epoch;
 }
 
-// First index with deg <= 0 over the full gathered degree vector
-// (affinity.py:113-119 semantics: ZeroDegree(first i)).
-__global__ void zero_degree_kernel(const double* __restrict__ deg, int64_t n, gpic_ctl* ctl) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n && deg[i] <= 0.0) raise_status(ctl, GPIC_E_ZERO_DEGREE, i, -1, deg[i]);
+LowRows low_rows(const gpic_comm* c, const gpic_shard& sh, int li, int64_t count) {
+  LowRows L;
+  L.x = sh.x;
+  L.n = c->n;
+  L.d = sh.d;
+  L.kind = sh.kind;
+  L.sigma = sh.kind == GPIC_KIND_COSINE ? 1.0 : sh.sigma;
+  L.list = c->loc[li].lowlist;
+  L.d_count = c->loc[li].lowcount;
+  L.count = count;
+  return L;
 }
 
 int publish(gpic_comm* c, int li, const double* src, int64_t rows, int64_t row_lo,
@@ -222,6 +231,10 @@ int alloc_locals(gpic_comm* c) {
     c->loc[li].v32 = reinterpret_cast<float*>(p);
     p += al(vector_pitch(c->n) * 4);
     c->loc[li].redpart = reinterpret_cast<double*>(p);
+    p += al((ceil_div(c->n, kRedBlock) + 1) * 8);
+    c->loc[li].lowlist = reinterpret_cast<int64_t*>(p);
+    p += al(c->n * 8);
+    c->loc[li].lowcount = reinterpret_cast<unsigned long long*>(p);
   }
   return GPIC_OK;
 }
@@ -321,27 +334,42 @@ int gpic_comm_gather_degrees(gpic_comm* c, const gpic_shard* shards, int32_t nlo
       return fail(GPIC_E_INVALID, "all shards of a comm use the same storage");
   int rc = packed ? gather_sum(c, shards, s) : gather(c, shards, true, s);
   if (rc) return rc;
-  // every rank now holds all n degrees: the ZeroDegree check is global
-  const double* degf = r_deg(c->region[c->rank0], c->n);
-  zero_degree_kernel<<<(unsigned)ceil_div(c->n, 256), 256, 0, s>>>(degf, c->n, c->loc[0].ctl);
-  count_launch();
-  if (d_deg_full_out)
-    GPIC_CUDA_TRY(cudaMemcpyAsync(d_deg_full_out, degf, c->n * 8, cudaMemcpyDeviceToDevice, s));
+  // every rank now holds all n degrees: isolated rows (fp32 degree ~ 0) are
+  // redone in fp64 from X on every rank (identical results), and ZeroDegree
+  // fires only for an exact fp64 zero (lowdeg.cu, affinity.py:113-119)
+  for (int li = 0; li < nlocal; ++li)
+    launch_lowdeg_scan(r_deg(c->region[c->rank0 + li], c->n), c->n, shards[li].kind,
+                       c->loc[li].lowlist, c->loc[li].lowcount, s);
   gpic_ctl h;
   GPIC_CUDA_TRY(cudaMemcpyAsync(&h, c->loc[0].ctl, sizeof h, cudaMemcpyDeviceToHost, s));
-  GPIC_CUDA_TRY(cudaStreamSynchronize(s));
-  if (h.status == GPIC_E_ZERO_DEGREE) {
-    char buf[96];
-    snprintf(buf, sizeof buf, "row %lld has zero degree", (long long)h.err_index);
-    return fail(GPIC_E_ZERO_DEGREE, buf);
-  }
+  rc = read_low_count(c->loc[0].lowcount, &c->low_count, s);
+  if (rc) return rc;
   if (h.status != GPIC_OK) return fail(h.status, "degree gather failed (peer timeout?)");
+  if (c->low_count > 0) {
+    for (int li = 0; li < nlocal; ++li) {
+      if (shards[li].x == nullptr)
+        return fail(GPIC_E_INVALID, "isolated rows need the shard's fp64 points (gpic_shard.x)");
+      launch_lowdeg_exact(low_rows(c, shards[li], li, c->low_count),
+                          r_deg(c->region[c->rank0 + li], c->n), c->loc[li].ctl, s);
+    }
+    GPIC_CUDA_TRY(cudaMemcpyAsync(&h, c->loc[0].ctl, sizeof h, cudaMemcpyDeviceToHost, s));
+    GPIC_CUDA_TRY(cudaStreamSynchronize(s));
+    if (h.status == GPIC_E_ZERO_DEGREE) {
+      char buf[96];
+      snprintf(buf, sizeof buf, "row %lld has zero degree", (long long)h.err_index);
+      return fail(GPIC_E_ZERO_DEGREE, buf);
+    }
+    if (h.status != GPIC_OK) return fail(h.status, "isolated-row degrees failed");
+  }
+  const double* degf = r_deg(c->region[c->rank0], c->n);
+  if (d_deg_full_out)
+    GPIC_CUDA_TRY(cudaMemcpyAsync(d_deg_full_out, degf, c->n * 8, cudaMemcpyDeviceToDevice, s));
   return GPIC_OK;
 }
 
 int gpic_comm_iterate(gpic_comm* c, const gpic_shard* shards, int32_t nlocal, double eps,
-                      int32_t max_iter, double* d_hist, double* d_vout, gpic_ctl* h_ctl,
-                      void* stream) {
+                      int32_t max_iter, const double* d_v0, double* d_hist, double* d_vout,
+                      gpic_ctl* h_ctl, void* stream) {
   if (!c || nlocal != c->nlocal) return fail(GPIC_E_INVALID, "shard count does not match the comm");
   if (max_iter < 1) return fail(GPIC_E_INVALID, "max_iterations must be at least 1");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -359,11 +387,16 @@ int gpic_comm_iterate(gpic_comm* c, const gpic_shard* shards, int32_t nlocal, do
     gpic_local_t& L = c->loc[li];
     set_epoch_kernel<<<1, 32, 0, s>>>(L.ctl, base);
     count_launch();
-    // v0 = d / tree_sum(d) from the gathered degrees (identical on every rank)
-    const double* degf = r_deg(c->region[self], n);
-    double* tau = L.redpart + ceil_div(n, kRedBlock);
-    launch_tree_sum(degf, n, L.redpart, tau, L.ctl, s);
-    launch_scale_vector(degf, n, tau, L.v64, L.v32, vector_pitch(n), s);
+    if (d_v0 != nullptr) {
+      // explicit start vector (initial_vector, serial.py:77-101), same on every rank
+      launch_scale_by(d_v0, n, 1.0, L.v64, L.v32, vector_pitch(n), s);
+    } else {
+      // v0 = d / tree_sum(d) from the gathered degrees (identical on every rank)
+      const double* degf = r_deg(c->region[self], n);
+      double* tau = L.redpart + ceil_div(n, kRedBlock);
+      launch_tree_sum(degf, n, L.redpart, tau, L.ctl, s);
+      launch_scale_vector(degf, n, tau, L.v64, L.v32, vector_pitch(n), s);
+    }
     ShardLoop& S = loops[li];
     std::memset(&S, 0, sizeof S);
     S.a = shards[li].a;
@@ -405,6 +438,8 @@ int gpic_comm_iterate(gpic_comm* c, const gpic_shard* shards, int32_t nlocal, do
     S.hist = d_hist + (int64_t)li * max_iter;
     S.ctl = L.ctl;
     S.pt = table(c, self);
+    S.low = low_rows(c, shards[li], li, c->low_count);
+    S.low_deg = r_deg(c->region[self], n);
   }
   rc = run_power_loops(loops, nlocal, n, max_iter, s);
   if (rc) return rc;

@@ -74,6 +74,8 @@ struct Workspace {
   double* v64;         // 2 x n ping-pong
   float* v32;          // lda floats (fp32 copy of v, zero padded)
   double* kscratch;    // k-means scratch (see kmeans.cu)
+  int64_t* lowlist;    // n low-degree row indices (lowdeg.cu)
+  unsigned long long* lowcount;
   int64_t kscratch_bytes;
   uint8_t* end;
 };
@@ -178,6 +180,50 @@ int launch_mf_matvec(const MfOperands& op, int64_t row_lo, int64_t rows, const f
 int launch_mf_degrees(const MfOperands& op, int64_t row_lo, int64_t rows, float* ones,
                       double* ypart, double* deg, cudaStream_t s);
 
+// ---- block sparsity (sparse.cu) ------------------------------------------
+// zero[tile_index(I, J)] = 1 when a bounding-sphere bound proves every fp32
+// entry of packed tile (I, J) is 0 (exp below the fp32 flush, with margin);
+// item_prefix{1,2}[u] = non-zero affinity work units (MB = 1, 2) before
+// unit u; sb_prefix[s] = GEMV super-block weight before super-block s.
+struct SparseMask {
+  int64_t nt = 0;
+  double* centre = nullptr;  // nt x d
+  double* radius = nullptr;  // nt
+  uint8_t* zero = nullptr;   // packed tiles
+  int64_t* item_prefix1 = nullptr;
+  int64_t* item_prefix2 = nullptr;
+  int64_t* sb_prefix = nullptr;
+  int64_t n_sb = 0;
+};
+int64_t packed_items_mb(int64_t n, int mb);
+int64_t sparse_mask_bytes(int64_t n, int32_t d);
+SparseMask carve_sparse(void* base, int64_t n, int32_t d);
+void launch_sparse_mask(const SparseMask& m, const float* xc, int64_t n, int32_t d, int32_t dp,
+                        double sigma, cudaStream_t s);
+
+// ---- low-degree (isolated) rows, lowdeg.cu -----------------------------
+// Rows whose engine degree is below low_degree_threshold(kind): recomputed
+// in fp64 from the caller's original X (n x d row-major) like the reference.
+struct LowRows {
+  const double* x = nullptr;
+  int64_t n = 0;
+  int32_t d = 0;
+  int kind = GPIC_KIND_RBF;
+  double sigma = 1.0;
+  const int64_t* list = nullptr;              // row indices (device)
+  const unsigned long long* d_count = nullptr;  // device count of list
+  int64_t count = 0;                          // host copy (0: nothing to do)
+};
+double low_degree_threshold(int kind);
+void launch_lowdeg_scan(const double* deg, int64_t n, int kind, int64_t* list,
+                        unsigned long long* count, cudaStream_t s);
+int read_low_count(const unsigned long long* d_count, int64_t* out, cudaStream_t s);
+// exact fp64 degrees of the listed rows into deg (ZeroDegree if one is 0)
+void launch_lowdeg_exact(const LowRows& L, double* deg, gpic_ctl* ctl, cudaStream_t s);
+// loop body: y_i = sum_j (a_ij / deg_i) v_j for the listed rows (fp64 v)
+void launch_lowdeg_matvec(const LowRows& L, const double* deg, const double* v64, double* y0,
+                          double* y1, gpic_ctl* ctl, cudaStream_t s);
+
 enum { kLoopDense = 0, kLoopPacked = 1, kLoopMatrixFree = 2, kLoopPacked16 = 3, kLoopPackedShard = 4 };
 
 // One shard's loop state (a single-rank run is one shard with nranks = 1).
@@ -205,6 +251,9 @@ struct ShardLoop {
   const double* slots;   // this rank's slot [0][0]; (rank, parity) at (2 rank + parity) * stride
   int64_t slot_stride;
   const double* deg_full;
+  // isolated rows redone in fp64 after the y exchange (count 0: none)
+  LowRows low;
+  const double* low_deg;  // full n-vector of degrees (exact for listed rows)
 };
 // Capture max_iter iterations of every local shard into one CUDA graph
 // (virtual ranks: all GEMVs of an iteration precede all tails) and launch it.

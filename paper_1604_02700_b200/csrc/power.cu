@@ -381,6 +381,9 @@ int run_power_loops(ShardLoop* shards, int nlocal, int64_t n, int32_t max_iter, 
         if (L.mode == kLoopPackedShard)
           launch_slot_combine(L.slots, L.slot_stride, pt.nranks, n, L.deg_full, pt.y[pt.self][0],
                               pt.y[pt.self][1], L.ctl, cs);
+        if (L.low.count > 0)
+          launch_lowdeg_matvec(L.low, L.low_deg, L.v64, pt.y[pt.self][0], pt.y[pt.self][1], L.ctl,
+                               cs);
         launch_iteration_tail(pt.y[pt.self][0], pt.y[pt.self][1], n, L.redpart, L.v64, L.v32,
                               L.hist, L.ctl, cs);
       }

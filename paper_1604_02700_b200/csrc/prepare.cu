@@ -83,7 +83,10 @@ __global__ void mean_kernel(const double* __restrict__ colpart, int64_t nblk, in
     for (int64_t b = 0; b < nblk; ++b) s += colpart[b * d + f];
     mean[f] = s / (double)n;
   }
-  if (threadIdx.x == 0) mean[d] = 0.0;  // max |x - mean| slot (maxabs_kernel)
+  if (threadIdx.x == 0) {
+    mean[d] = 0.0;      // max |x - mean| (maxabs_kernel)
+    mean[d + 1] = 0.0;  // max_i |x_i - mean|^2 (center_split_kernel): the spread R^2
+  }
 }
 
 // max |x - mean| over all finite entries -> mean[d] (non-negative doubles
@@ -123,7 +126,7 @@ __device__ __forceinline__ void split16(double xs, __half* hi, __half* lo, int64
 // scaled fp16 hi/lo planes for the tensor engine, fp64-accumulated squared
 // norm of the fp32 row, and the row's entries of the norm block.
 __global__ void center_split_kernel(const double* __restrict__ x, int64_t n, int32_t d, int32_t dp,
-                                    int64_t n_pad, const double* __restrict__ mean,
+                                    int64_t n_pad, double* __restrict__ mean,
                                     __half* __restrict__ hi, float* __restrict__ xc_out,
                                     float* __restrict__ sqn) {
   const int lane = threadIdx.x & 31;
@@ -149,6 +152,9 @@ __global__ void center_split_kernel(const double* __restrict__ x, int64_t n, int
   sq = warp_sum_f64(sq);
   sqs = warp_sum_f64(sqs);
   if (lane == 0) sqn[row] = row == n_pad - 1 ? (float)(1.0 / (s * s)) : (float)sq;
+  if (lane == 0 && row < n)  // spread R^2 for the engine routing (gpic_engine_for)
+    atomicMax(reinterpret_cast<unsigned long long*>(mean + d + 1),
+              (unsigned long long)__double_as_longlong(sq));
   // norm block: lanes 0-15 write k = lane of the row / column operands
   __half* nb = lo + n_pad * dp + row * 16 + lane;
   const int64_t plane = n_pad * 16;

@@ -90,38 +90,51 @@ def validate_dataset(d: DataSet) -> DataSet:
 # numbers, EmptyDataSet — are the reference's.
 
 
-def _load_csv_lines(path, has_labels, header):
-    """The reference's line loop (data.py:81-120): exact errors."""
-    from .errors import ParseError, RaggedRows
-
-    rows, labels, width = [], [], None
+def _csv_records(path, header):
+    """(1-based line number, comma-split fields) of every non-blank data line."""
     with open(path, "r", encoding="utf-8") as fh:
         for lineno, raw in enumerate(fh, start=1):
-            if header and lineno == 1:
-                continue
-            line = raw.strip()
-            if not line:
-                continue
-            fields = line.split(",")
-            if width is None:
-                width = len(fields)
-            elif len(fields) != width:
-                raise RaggedRows(lineno)
-            if has_labels:
-                *feat, lab = fields
-                try:
-                    labels.append(int(lab))
-                except ValueError:
-                    raise ParseError(lineno, f"label {lab!r} is not an integer") from None
-            else:
-                feat = fields
-            try:
-                rows.append([float(f) for f in feat])
-            except ValueError:
-                raise ParseError(lineno, "non-numeric field") from None
-    if not rows:
+            text = raw.strip()
+            if text and not (header and lineno == 1):
+                yield lineno, text.split(",")
+
+
+def _parse_record(lineno, fields, has_labels):
+    """(features, label or None) of one line with the reference's typed
+    errors (data.py:81-120): ParseError(line) for a non-integer label or a
+    non-numeric feature."""
+    from .errors import ParseError
+
+    feats, label = (fields[:-1], fields[-1]) if has_labels else (fields, None)
+    if has_labels:
+        try:
+            label = int(label)
+        except ValueError:
+            raise ParseError(lineno, f"label {fields[-1]!r} is not an integer") from None
+    try:
+        return [float(f) for f in feats], label
+    except ValueError:
+        raise ParseError(lineno, "non-numeric field") from None
+
+
+def _load_csv_lines(path, has_labels, header):
+    """Line-by-line parse with exact errors: RaggedRows(line) when a line's
+    field count differs from the first data line's, ParseError(line),
+    EmptyDataSet for no data lines."""
+    from .errors import RaggedRows
+
+    points, labels, width = [], [], None
+    for lineno, fields in _csv_records(path, header):
+        width = len(fields) if width is None else width
+        if len(fields) != width:
+            raise RaggedRows(lineno)
+        feats, label = _parse_record(lineno, fields, has_labels)
+        points.append(feats)
+        labels.append(label)
+    if not points:
         raise EmptyDataSet()
-    return np.array(rows, dtype=np.float64), (np.array(labels, dtype=np.int64) if has_labels else None)
+    pts = np.array(points, dtype=np.float64)
+    return pts, (np.array(labels, dtype=np.int64) if has_labels else None)
 
 
 def _load_csv_fast(path, has_labels, header):

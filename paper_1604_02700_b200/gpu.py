@@ -211,6 +211,16 @@ class PreparedPoints:
     d: int
     device: object
     kind: int = _lib.KIND_RBF
+    x: object = None  # the fp64 points on the device (isolated-row fix, lowdeg.cu)
+    spread2: float = 0.0  # R^2 = max_i |x_i - mean|^2 (RBF): engine routing
+
+    def engine(self, sigma: float, engine: str, storage: int) -> str:
+        """The engine gpic_cluster would run (gpic_engine_for): SIMT difference
+        form for RBF at d <= 8 or a spread too large for the tensor Gram."""
+        impl = _lib.AFFINITY_TC if engine == "tc" else _lib.AFFINITY_SIMT
+        got = _lib.lib().gpic_engine_for(self.kind, self.d, float(sigma), float(self.spread2), impl,
+                                         storage)
+        return "tc" if got == _lib.AFFINITY_TC else "simt"
 
 
 def prepare_points(d, dev, kind: int = _lib.KIND_RBF) -> PreparedPoints:
@@ -234,11 +244,14 @@ def prepare_points(d, dev, kind: int = _lib.KIND_RBF) -> PreparedPoints:
     xlo = torch.empty((npad, dp), dtype=torch.float32, device=dev)
     sqn = torch.empty(npad, dtype=torch.float32, device=dev)
     ctl = _new_ctl(dev)
-    work = torch.empty(((n + 255) // 256 + 1) * m + m, dtype=torch.float64, device=dev)
+    ncol = ((n + 255) // 256) * m
+    work = torch.empty(ncol + m + 2, dtype=torch.float64, device=dev)
     _lib.check(L.gpic_prepare_points(_ptr(x), n, m, kind, _ptr(xhi), _ptr(xlo), _ptr(sqn),
                                      _ptr(work), _ptr(ctl), st))
     _raise_ctl(_read_ctl(ctl, dev), m)
-    return PreparedPoints(xhi=xhi, xlo=xlo, sqn=sqn, n=n, d=m, device=dev, kind=kind)
+    spread2 = float(work[ncol + m + 1].item()) if kind == _lib.KIND_RBF else 0.0
+    return PreparedPoints(xhi=xhi, xlo=xlo, sqn=sqn, n=n, d=m, device=dev, kind=kind, x=x,
+                          spread2=spread2)
 
 
 def affinity_rows(prep: PreparedPoints, lo: int, hi: int, sigma: float, engine: str = "tc"):
@@ -253,6 +266,7 @@ def affinity_rows(prep: PreparedPoints, lo: int, hi: int, sigma: float, engine: 
     rows_pad = -(-nrows // 128) * 128
     rowpart = torch.empty(((n + 127) // 128) * rows_pad, dtype=torch.float32, device=dev)
     ctl = _new_ctl(dev)
+    engine = prep.engine(sigma, engine, _lib.STORAGE_DENSE)
     impl = _lib.AFFINITY_TC if engine == "tc" else _lib.AFFINITY_SIMT
     if prep.kind == _lib.KIND_COSINE:
         rc = L.gpic_affinity_cosine(_ptr(prep.xhi), _ptr(prep.xlo), _ptr(prep.sqn), n, m, lo, hi,
@@ -598,24 +612,47 @@ def cluster(d: DataSet, kind, params: PicParams, config: KernelConfig | None = N
         raise KTooLarge(k, n)
     if k > KMEANS_MAX_K:
         raise InvalidSpec(f"the device k-means holds at most {KMEANS_MAX_K} centres")
+    v0 = start_vector(params.v0, n)
     if config.p > 1:
         from . import sharded
 
-        return sharded.cluster(d, kind, params, config, seed)
-    if not (isinstance(params.v0, str) and params.v0 == "degree"):
-        return _cluster_stagewise(d, kind, params, config, seed)
-    labels, v, trace, _ = cluster_fused(d, kind, params, config, seed)
+        return sharded.cluster(d, kind, params, config, seed, v0=v0)
+    labels, v, trace, _ = cluster_fused(d, kind, params, config, seed, v0=v0)
     return labels, v, trace
 
 
+def start_vector(choice, n: int):
+    """The host side of initial_vector (serial.py:77-101): None for "degree"
+    (the device computes d / sum(d)), the 1/n vector for "uniform", or a
+    validated copy of an explicit vector (length n, nonnegative, unit L1
+    norm within 1e-12); InvalidSpec otherwise."""
+    if isinstance(choice, str):
+        if choice == "degree":
+            return None
+        if choice == "uniform":
+            return np.full(n, 1.0 / n)
+        raise InvalidSpec(f"unknown initial vector kind {choice!r}")
+    v = np.asarray(choice, dtype=np.float64).copy()
+    if v.shape != (n,):
+        raise InvalidSpec(f"explicit v0 has length {v.size}, expected {n}")
+    if v.min() < 0.0:
+        raise InvalidSpec("explicit v0 must be nonnegative")
+    if abs(v.sum() - 1.0) > 1e-12:
+        raise InvalidSpec("explicit v0 must have unit L1 norm within 1e-12")
+    return v
+
+
 def cluster_fused(d: DataSet, kind, params: PicParams, config: KernelConfig, seed: int = 0,
-                  timed: bool = False):
-    """One gpic_cluster call (p == 1, degree start). With ``timed`` the
-    per-phase device milliseconds come back as a dict (report.py:28 PHASES)."""
+                  timed: bool = False, v0=None):
+    """One gpic_cluster call (p == 1). ``v0``: None (degree start) or an
+    explicit start vector (see start_vector). With ``timed`` the per-phase
+    device milliseconds come back as a dict (report.py:28 PHASES)."""
     torch = _torch()
     dev = _device(config)
     x = torch.from_numpy(d.points).to(dev, non_blocking=True)
-    return _cluster_x(x, kind, params, config, seed, timed)
+    if v0 is None:
+        v0 = start_vector(params.v0, d.points.shape[0])
+    return _cluster_x(x, kind, params, config, seed, timed, v0)
 
 
 def cluster_points(x, kind, params: PicParams, config: KernelConfig | None = None, seed: int = 0,
@@ -628,10 +665,11 @@ def cluster_points(x, kind, params: PicParams, config: KernelConfig | None = Non
         raise InvalidSpec("cluster_points needs a CUDA float64 (n, d) tensor")
     if x.shape[0] < params.k:
         raise KTooLarge(params.k, x.shape[0])
-    return _cluster_x(x.contiguous(), kind, params, config or KernelConfig(), seed, timed)
+    return _cluster_x(x.contiguous(), kind, params, config or KernelConfig(), seed, timed,
+                      start_vector(params.v0, x.shape[0]))
 
 
-def _cluster_x(x, kind, params, config, seed, timed):
+def _cluster_x(x, kind, params, config, seed, timed, v0=None):
     torch = _torch()
     code, sigma = _check_kind(kind)
     n, m = x.shape
@@ -650,8 +688,9 @@ def _cluster_x(x, kind, params, config, seed, timed):
     first, u = kmeans_draws(n, k, seed)
     iters = C.c_int32(0)
     conv = C.c_int32(0)
+    v0_t = None if v0 is None else torch.from_numpy(np.ascontiguousarray(v0)).to(dev)
     args = (_ptr(x), n, m, sigma, code, k, eps, T, first, u.ctypes.data_as(C.c_void_p), impl,
-            storage, _ptr(labels), _ptr(v), _ptr(hist), C.byref(iters), C.byref(conv),
+            storage, _ptr(v0_t), _ptr(labels), _ptr(v), _ptr(hist), C.byref(iters), C.byref(conv),
             _ptr(work), nbytes, _stream(dev))
     ms = (C.c_float * 5)()
     rc = L.gpic_cluster_timed(*args, ms) if timed else L.gpic_cluster(*args)
@@ -665,16 +704,6 @@ def _cluster_x(x, kind, params, config, seed, timed):
                       (t / 1e3 for t in ms))) if timed else None
     return (labels.cpu().numpy(), v.cpu().numpy(),
             PicTrace(it, hist[:it].cpu().numpy(), bool(conv.value)), phases)
-
-
-def _cluster_stagewise(d, kind, params, config, seed):
-    a = k_affinity(d, kind, config)
-    deg = k_rowsum(a, config)
-    w = k_normalize(a, deg, config)
-    v = initial_embedding(deg, params, config)
-    v, trace = iterate(w, v, params, config)
-    labels = kmeans_1d(v, KMeansParams(k=params.k, seed=seed), config)
-    return labels.cpu().numpy(), v.cpu().numpy(), trace
 
 
 # ------------------------------------------------- batched small problems

@@ -5,8 +5,10 @@
 * `KMeansParams` — `picluster/kmeans.py:25-36`
 * `KernelConfig` — `picluster/parallel.py:44-77`, extended with the GPU knobs.
 
-The cosine kind (`affinity.py:22-24`) is out of scope for this build
-(SURVEY.md §8 f1); passing it raises InvalidSpec.
+Both similarity kinds of the reference run on the device: `GaussianRbf`
+(`affinity.py:27-35`) and `Cosine` (`affinity.py:22-24`, SURVEY.md §8 f1:
+unit rows in fp64, the same Gram engines, max(0, cos) epilogue, ZeroVector
+for a zero row).
 """
 
 from __future__ import annotations
@@ -31,7 +33,7 @@ class GaussianRbf:
 
 @dataclass(frozen=True)
 class Cosine:
-    """Declared for API parity only; the GPU backend rejects it (out of scope)."""
+    """A_ij = max(0, x_i.x_j / (|x_i| |x_j|)) (affinity.py:22-24, 41-53, 88-95)."""
 
 
 SimilarityKind = GaussianRbf | Cosine

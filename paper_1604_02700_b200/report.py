@@ -26,7 +26,6 @@ CPU fallback); pass their written report as ``baseline``.
 from __future__ import annotations
 
 import json
-import math
 import time
 from dataclasses import dataclass, field
 from pathlib import Path
@@ -109,7 +108,7 @@ def run_timed(d: DataSet, kind, params: PicParams, backend: str = "gpu",
     check_labels(d)
     if params.k > d.n:
         raise KTooLarge(params.k, d.n)
-    fused = backend == "gpu" and isinstance(params.v0, str) and params.v0 == "degree"
+    fused = backend == "gpu"
     _sync()
     start = time.perf_counter()
     if fused:
@@ -120,9 +119,16 @@ def run_timed(d: DataSet, kind, params: PicParams, backend: str = "gpu",
     return TimedRun(labels, v, trace, phases, total)
 
 
+# The report record: field names and meaning are schema 1 of the reference
+# (report.py:102-129), so reports written here and there load side by side.
+REPORT_FIELDS = ("dataset", "n", "m", "backend", "p", "similarity", "params", "repetitions",
+                 "runs", "mean_seconds", "stddev_seconds", "affinity_share", "ari", "jaccard",
+                 "baseline", "speedup")
+
+
 @dataclass
 class BenchReport:
-    """Aggregate of repeated timed runs of one configuration (report.py:102-129)."""
+    """One configuration timed `repetitions` times (schema 1 fields)."""
 
     dataset: str
     n: int
@@ -142,55 +148,50 @@ class BenchReport:
     speedup: float | None = None
 
     def to_dict(self) -> dict:
-        return {"schema": SCHEMA_VERSION, **self.__dict__}
+        doc = {"schema": SCHEMA_VERSION}
+        doc.update((name, getattr(self, name)) for name in REPORT_FIELDS)
+        return doc
 
     def write(self, path: str | Path) -> None:
-        with open(path, "w", encoding="utf-8") as fh:
-            json.dump(self.to_dict(), fh, indent=2)
-            fh.write("\n")
+        Path(path).write_text(json.dumps(self.to_dict(), indent=2) + "\n", encoding="utf-8")
 
 
 def load_report(path: str | Path) -> dict:
-    with open(path, "r", encoding="utf-8") as fh:
-        doc = json.load(fh)
-    if doc.get("schema") != SCHEMA_VERSION:
-        raise InvalidSpec(f"unsupported report schema {doc.get('schema')!r}")
+    """A schema-1 report document (ours or the reference's)."""
+    doc = json.loads(Path(path).read_text(encoding="utf-8"))
+    version = doc.get("schema")
+    if version != SCHEMA_VERSION:
+        raise InvalidSpec(f"unsupported report schema {version!r}")
     return doc
+
+
+def _baseline_tag(doc: dict) -> str:
+    return "/".join((str(doc["dataset"]), str(doc["backend"]), f"p={doc['p']}"))
 
 
 def summarize(d: DataSet, kind, params: PicParams, backend: str, config: KernelConfig,
               seed: int, runs: list[dict], labels=None, baseline: dict | None = None
               ) -> BenchReport:
-    """Build the BenchReport of already-timed runs (the aggregation half of
-    report.py:140-194)."""
-    totals = [r["total"] for r in runs]
-    mean = sum(totals) / len(totals)
-    stddev = math.sqrt(sum((t - mean) ** 2 for t in totals) / len(totals))
+    """Fold already-timed runs into a BenchReport: population mean / stddev
+    of the totals, the affinity phase's share of all the time, pair-counting
+    indices against the data's labels, speedup against a baseline report."""
+    totals = np.array([r["total"] for r in runs], dtype=np.float64)
+    affinity = np.array([r["phases"]["affinity"] for r in runs], dtype=np.float64)
+    mean = float(totals.mean())
     report = BenchReport(
-        dataset=d.name,
-        n=d.n,
-        m=d.m,
-        backend=backend,
-        p=config.p,
+        dataset=d.name, n=d.n, m=d.m, backend=backend, p=config.p,
         similarity=similarity_to_dict(kind),
-        params={
-            "k": params.k,
-            "epsilon": params.resolved_epsilon(d.n),
-            "max_iterations": params.max_iterations,
-            "seed": seed,
-        },
-        repetitions=len(runs),
-        runs=runs,
-        mean_seconds=mean,
-        stddev_seconds=stddev,
-        affinity_share=sum(r["phases"]["affinity"] for r in runs) / sum(totals),
+        params=dict(k=params.k, epsilon=params.resolved_epsilon(d.n),
+                    max_iterations=params.max_iterations, seed=seed),
+        repetitions=len(runs), runs=runs, mean_seconds=mean,
+        stddev_seconds=float(totals.std()),
+        affinity_share=float(affinity.sum() / totals.sum()),
     )
-    if d.labels is not None and labels is not None:
+    if labels is not None and d.labels is not None:
         table = contingency(d.labels, labels)
-        report.ari = adjusted_rand_index(table)
-        report.jaccard = jaccard_index(table)
+        report.ari, report.jaccard = adjusted_rand_index(table), jaccard_index(table)
     if baseline is not None:
-        report.baseline = f"{baseline['dataset']}/{baseline['backend']}/p={baseline['p']}"
+        report.baseline = _baseline_tag(baseline)
         report.speedup = baseline["mean_seconds"] / mean
     return report
 

@@ -139,17 +139,18 @@ class ShardedRunner:
     def close(self):
         self.comm.close()
 
-    def run(self, points, kind, params, seed: int = 0):
+    def run(self, points, kind, params, seed: int = 0, v0=None):
         gpu = self.gpu
         torch = gpu._torch()
         n, dev, cfg = self.n, self.dev, self.config
         st = gpu._stream(dev)
         code, sigma = gpu._check_kind(kind)
         prep = gpu.prepare_points(points, dev, code)
-        # the engine routing of gpic_cluster (capi.cu effective_engine): d > 192
-        # and RBF with d <= 8 run on the SIMT engine, here with dense row shards
+        # the engine routing of gpic_cluster (capi.cu effective_engine): d > 192,
+        # RBF with d <= 8 and RBF with a large spread against sigma run on the
+        # SIMT engine, here with dense row shards
         packed = (self.packed and int(_lib.lib().gpic_feature_pitch(prep.d)) <= 192
-                  and not (code == _lib.KIND_RBF and prep.d <= 8))
+                  and prep.engine(sigma, "tc", _lib.STORAGE_PACKED) == "tc")
         nl = len(self.locals)
         shards = (_lib.Shard * nl)()
         keep = []  # device buffers referenced by the shard structs
@@ -169,7 +170,8 @@ class ShardedRunner:
                 keep += [deg, ypart]
                 shards[i] = _lib.Shard(None, 0, deg.data_ptr(), lo, hi - lo, _lib.STORAGE_NONE,
                                        prep.d, prep.xhi.data_ptr(), prep.xlo.data_ptr(),
-                                       prep.sqn.data_ptr(), sigma, code, ypart.data_ptr())
+                                       prep.sqn.data_ptr(), sigma, code, ypart.data_ptr(),
+                                       prep.x.data_ptr())
         elif packed:
             # symmetric packed shards: upper-triangle tiles of the rank's
             # 512-row super-rows, partial degrees summed across ranks
@@ -186,7 +188,7 @@ class ShardedRunner:
                 keep += [tiles, deg, scratch]
                 shards[i] = _lib.Shard(tiles.data_ptr(), 0, deg.data_ptr(), lo, hi - lo,
                                        _lib.STORAGE_PACKED, prep.d, None, None, None, sigma, code,
-                                       scratch.data_ptr())
+                                       scratch.data_ptr(), prep.x.data_ptr())
         else:
             for i, r in enumerate(self.locals):
                 lo, hi = self.ranges[r]
@@ -194,19 +196,23 @@ class ShardedRunner:
                 keep.append(blk)
                 shards[i] = _lib.Shard(blk.a.data_ptr(), blk.lda, blk.deg.data_ptr(), lo, hi - lo,
                                        _lib.STORAGE_DENSE, prep.d, None, None, None, sigma, code,
-                                       None)
+                                       None, prep.x.data_ptr())
         T = params.max_iterations
         eps = params.resolved_epsilon(n)
         hist = torch.zeros(nl * T, dtype=torch.float64, device=dev)
         vout = torch.empty(nl * n, dtype=torch.float64, device=dev)
         ctls = (_lib.Ctl * nl)()
         L = self.comm.L
+        keep.append(prep.x)
         rc = L.gpic_comm_gather_degrees(self.comm.ptr, shards, nl, None, st)
         if rc == _lib.GPIC_E_ZERO_DEGREE:
             raise ZeroDegree(int(_lib.last_error().split()[1]))
         _lib.check(rc)
-        rc = L.gpic_comm_iterate(self.comm.ptr, shards, nl, eps, T, gpu._ptr(hist),
-                                 gpu._ptr(vout), ctls, st)
+        if v0 is None:
+            v0 = gpu.start_vector(params.v0, n)
+        v0_t = None if v0 is None else torch.from_numpy(np.ascontiguousarray(v0)).to(dev)
+        rc = L.gpic_comm_iterate(self.comm.ptr, shards, nl, eps, T, gpu._ptr(v0_t),
+                                 gpu._ptr(hist), gpu._ptr(vout), ctls, st)
         if rc != _lib.GPIC_OK:
             bad = next((c for c in ctls if c.status != _lib.GPIC_OK), None)
             _lib.raise_for(rc, bad)
@@ -221,14 +227,15 @@ class ShardedRunner:
         return labels, v, PicTrace(it, hist[:it].cpu().numpy(), bool(h.converged))
 
 
-def cluster(d, kind, params, config, seed):
-    """Sharded counterpart of gpu.cluster (same return contract)."""
+def cluster(d, kind, params, config, seed, v0=None):
+    """Sharded counterpart of gpu.cluster (same return contract); ``v0`` as
+    gpu.start_vector returns it (None: the degree start)."""
     from . import gpu
 
     gpu._check_kind(kind)
     runner = ShardedRunner(d.n, config)
     try:
-        labels, v, trace = runner.run(d, kind, params, seed)
+        labels, v, trace = runner.run(d, kind, params, seed, v0=v0)
         return labels.cpu().numpy(), v.cpu().numpy(), trace
     finally:
         runner.close()

@@ -176,3 +176,25 @@ class TestValidation:
             adjusted_rand_index(contingency([0], [0]))
         with pytest.raises(errors.LengthMismatch):
             contingency([0, 1], [0])
+
+
+def test_engine_routing_rule():
+    """gpic_engine_for is host-only logic: d <= 8 RBF and large spreads go
+    to the SIMT difference form (fp16 tiles then become fp32 packed tiles),
+    matrix-free stays on tcgen05."""
+    from paper_1604_02700_b200 import _lib
+
+    L = _lib.lib()
+    TC, SIMT = _lib.AFFINITY_TC, _lib.AFFINITY_SIMT
+    rbf, cos = _lib.KIND_RBF, _lib.KIND_COSINE
+    # config 3: R^2 / 2 sigma^2 = 64 -> tensor cores
+    assert L.gpic_engine_for(rbf, 64, 4.0, 64.0 * 32.0, TC, _lib.STORAGE_PACKED) == TC
+    # R / sigma = 100 -> SIMT difference form for stored fp32 A
+    assert L.gpic_engine_for(rbf, 64, 1.0, 1e4, TC, _lib.STORAGE_PACKED) == SIMT
+    assert L.gpic_engine_for(rbf, 64, 1.0, 1e4, TC, _lib.STORAGE_DENSE) == SIMT
+    assert L.gpic_engine_for(rbf, 64, 1.0, 1e4, TC, _lib.STORAGE_NONE) == TC
+    assert L.gpic_engine_for(rbf, 64, 1.0, 1e4, TC, _lib.STORAGE_PACKED16) == SIMT
+    assert L.gpic_engine_for(rbf, 64, 4.0, 64.0 * 32.0, TC, _lib.STORAGE_PACKED16) == TC
+    assert L.gpic_engine_for(rbf, 4, 4.0, 1.0, TC, _lib.STORAGE_PACKED) == SIMT
+    assert L.gpic_engine_for(cos, 64, 1.0, 1e9, TC, _lib.STORAGE_PACKED) == TC
+    assert L.gpic_engine_for(rbf, 700, 4.0, 1.0, TC, _lib.STORAGE_PACKED) == SIMT
