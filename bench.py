@@ -376,19 +376,33 @@ def _gemv_roofline(args, L, C, torch, stream, st, n, m, k, T, work, v, storage):
                 "with the distance from the MMA, exp2, row + column products)")
         del scr
     elif storage in (1, 3):
+        # the packed GEMV as the run executes it: only tiles with a stored
+        # box are read (block sparsity, csrc/sparse.cu); algorithmic bytes =
+        # the stored tiles' bytes, counted from the run's own box flags
+        offs = (C.c_int64 * 6)()
+        assert L.gpic_cluster_workspace_layout(n, m, k, T, storage, offs) == 0
+        base0 = work.data_ptr()
+        tiles, rowp, colp = base0 + offs[0], base0 + offs[1], base0 + offs[2]
+        boxnz_p, sbp_p = base0 + offs[3], base0 + offs[4]
         ntiles = int(L.gpic_packed_tiles(n))
-        tile_bytes = ntiles * 128 * 128 * (4 if storage == 1 else 2)
-        rowp = base + tile_bytes
-        colp = rowp + ((int(L.gpic_sym_partial_floats(n)) * 4 + 255) // 256) * 256
-        fn = L.gpic_sym_matvec if storage == 1 else L.gpic_sym_matvec16
+        elem = 4 if storage == 1 else 2
+        sparse = os.environ.get("GPIC_SPARSE", "1") != "0"
+        stored = None
+        if sparse:  # the run's flags, read in place from the workspace
+            flags = work[offs[3]: offs[3] + ntiles * 16].view(ntiles, 16)
+            stored = int((flags.amax(dim=1) > 0).sum().item())
+        tile_bytes = (stored if stored is not None else ntiles) * 128 * 128 * elem
 
         def launch():
-            return fn(C.c_void_p(base), n, C.c_void_p(v32.data_ptr()),
-                      C.c_void_p(rowp), C.c_void_p(colp),
-                      C.c_void_p(deg1.data_ptr()), C.c_void_p(yv.data_ptr()), st)
+            return L.gpic_sym_matvec_sparse(
+                C.c_void_p(tiles), 0 if storage == 1 else 1, n, C.c_void_p(v32.data_ptr()),
+                C.c_void_p(rowp), C.c_void_p(colp), C.c_void_p(deg1.data_ptr()),
+                C.c_void_p(yv.data_ptr()), C.c_void_p(boxnz_p if sparse else 0),
+                C.c_void_p(sbp_p if sparse else 0), st)
         alg = float(tile_bytes)
         name = ("sym_gemv_kernel + sym_reduce_kernel (packed symmetric tiles, "
-                + ("fp32)" if storage == 1 else "fp16)"))
+                + ("fp32" if storage == 1 else "fp16")
+                + (f", block-sparse: {stored} of {ntiles} tiles stored)" if sparse else ")"))
     else:
         lda = int(L.gpic_affinity_pitch(n))
 

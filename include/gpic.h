@@ -225,6 +225,15 @@ int64_t gpic_sym_partial_floats(int64_t n);
 int gpic_sym_matvec16(const void* d_tiles, int64_t n, const float* d_v, float* d_rowp,
                       float* d_colp, const double* d_row_scale, double* d_y, void* stream);
 int64_t gpic_vector_pitch(int64_t n);
+/* k_multiply on the packed tiles a gpic_cluster run left in its workspace,
+ * with the run's block sparsity: only tiles with a stored 32 x 32 box are
+ * read, unstored boxes count as the exact zeros they are (d_boxnz, 16
+ * flags per tile; d_sb_prefix the GEMV weights; both NULL = every tile).
+ * half: fp16 tiles (GPIC_STORAGE_PACKED16). Offsets of the tiles, partial
+ * buffers, flags and weights: gpic_cluster_workspace_layout. */
+int gpic_sym_matvec_sparse(const void* d_tiles, int32_t half, int64_t n, const float* d_v,
+                           float* d_rowp, float* d_colp, const double* d_row_scale, double* d_y,
+                           const uint8_t* d_boxnz, const int64_t* d_sb_prefix, void* stream);
 
 /* ---- whole pipeline ----------------------------------------------------
  * cluster (serial.py:131-150 / parallel.py:236-255) for one rank owning the
@@ -255,6 +264,11 @@ int64_t gpic_vector_pitch(int64_t n);
 int64_t gpic_packed_tiles(int64_t n);
 int64_t gpic_cluster_workspace_bytes(int64_t n, int32_t d, int32_t k, int32_t max_iter,
                                      int32_t storage);
+/* Byte offsets inside that workspace (packed storages): [0] tiles, [1] GEMV
+ * row records, [2] column records, [3] stored-box flags, [4] GEMV weights,
+ * [5] degrees (fp64). For measurement and tests. */
+int gpic_cluster_workspace_layout(int64_t n, int32_t d, int32_t k, int32_t max_iter,
+                                  int32_t storage, int64_t* offsets);
 int gpic_cluster(const double* d_x, int64_t n, int32_t d, double sigma, int32_t kind, int32_t k,
                  double eps, int32_t max_iter, int64_t first_index, const double* h_uniforms,
                  int32_t impl, int32_t storage, const double* d_v0, int64_t* d_labels, double* d_v,

@@ -135,10 +135,10 @@ __global__ void __launch_bounds__(256, KD == 2 ? 3 : 2)
       if (kind == GPIC_KIND_COSINE) {
         e = fmaxf(acc[i][j], 0.f);  // unit rows: the Gram entry is the cosine
       } else if (DIFF) {
-        e = ex2(acc[i][j] * neg_scale_log2);
+        e = ex2_flush(acc[i][j] * neg_scale_log2);
       } else {
         const float d2 = fmaxf(sqa + sqb[j] - 2.f * acc[i][j], 0.f);
-        e = exp2f(d2 * neg_scale_log2);
+        e = ex2_flush(d2 * neg_scale_log2);
       }
       if (cj == gr || cj >= n || (PACKED && gr >= n)) e = 0.f;
       vals[j] = e;

@@ -152,6 +152,10 @@ struct TcArgs {
   int sym;              // matvec: upper-triangle tiles only, column partials -> colpart
   int store_hint;       // store modes: L2 evict-first hint on the output stream
   float* colpart;       // matvec sym: [packed (row block, column tile)][128] fp32
+  // packed store modes: non-null -> a 32 x 32 box whose values are all exact
+  // zeros is not stored; boxnz[(tile) * 16 + quadrant * 4 + chunk] records
+  // which boxes were (sparse.cu). Indexed by the global packed tile.
+  uint8_t* boxnz;
 };
 
 __host__ __device__ inline int64_t packed_items(int64_t nrt, int64_t nct, int mb) {
@@ -583,6 +587,28 @@ __global__ void __launch_bounds__(kCtaThreads<MODE>, 1)
             vcol[2 * b2 + 1] = v2.y;
           }
         }
+        if constexpr (KIND == GPIC_KIND_RBF && MODE != kModeDense) {
+          // a box whose every entry flushes (< 2^-64, ex2_flush) is skipped:
+          // no exp, no sums, no store (flags 0 in boxnz, zero column partials)
+          float gm = __uint_as_float(r[0]);
+#pragma unroll
+          for (int x = 1; x < 32; ++x) gm = fmaxf(gm, __uint_as_float(r[x]));
+          if (!__any_sync(0xffffffffu, gm * m2ns >= kFlushLog2)) {
+            if constexpr (MODE == kModeMatvec) {
+              if (args.sym) colx[((buf * MB + m) * 4 + q) * 128 + ch * 32 + lane] = 0.f;
+              return;
+            } else {
+              if (args.boxnz != nullptr) {
+                if (lane == 0 && store_ok)
+                  args.boxnz[tile_index(tI, cb, args.n_ctiles) * 16 + q * 4 + ch] = 0;
+                if (store_ok && tI != cb)
+                  args.degcol[((tile_index(tI, cb, args.n_ctiles) - args.tile_base) * 4 + q) * 128 +
+                              ch * 32 + lane] = 0.f;
+                return;
+              }
+            }
+          }
+        }
         const bool diag = (col0 < row_lo32 + lr0 + 32) && (row_lo32 + lr0 < col0 + 32);
         const bool pad = col0 + 32 > n32 || row_lo32 + lr0 + 32 > n32;
         float vals[32];
@@ -595,7 +621,7 @@ __global__ void __launch_bounds__(kCtaThreads<MODE>, 1)
             // g = -(s^2/2)|x_i - x_j|^2 from the MMA (norm block); no clamp:
             // a near-duplicate's distance^2 rounding below 0 gives
             // exp2(+ulp-scale) = 1 + O(1e-6), the Gram's own rounding order
-            vals[x] = ex2(g * m2ns);
+            vals[x] = ex2_flush(g * m2ns);
         }
         if (diag || pad) {
 #pragma unroll
@@ -660,9 +686,20 @@ __global__ void __launch_bounds__(kCtaThreads<MODE>, 1)
         } else {
 #pragma unroll
           for (int x = 0; x < 32; ++x) rsum[(x >> 4) * 2 + ((x >> 1) & 1)] += vals[x];
+          // sparse: a box of exact zeros is not stored, only flagged
+          bool box_nz = true;
+          if (is_packed(MODE) && args.boxnz != nullptr) {
+            bool any = false;
+#pragma unroll
+            for (int x = 0; x < 32; ++x) any |= vals[x] != 0.f;
+            box_nz = __any_sync(0xffffffffu, any);
+            if (lane == 0 && store_ok)
+              args.boxnz[tile_index(tI, cb, args.n_ctiles) * 16 + q * 4 + ch] = box_nz ? 1 : 0;
+          }
           // full 32-byte sectors straight from registers: each quad writes 8
           // consecutive floats of one row per (block, row)
           // stage the 32 x 32 box (row R at R*128, 16-byte chunk c/4 ^ (R&7))
+          if (box_nz) {
           if (stores > 0) {  // the previous TMA store must have read the box
             if (lane == 0) tma_store_wait_read<0>();
             __syncwarp();
@@ -713,6 +750,7 @@ __global__ void __launch_bounds__(kCtaThreads<MODE>, 1)
               tma_store_2d(&map_out, is_packed(MODE) ? ch * 32 : (int)col0, (int)out_row0, stage);
           }
           ++stores;
+          }  // box_nz
           if (is_packed(MODE) && store_ok && tI != cb) {
             // degrees of the tile's COLUMN rows (A is symmetric): per column
             // slot k, this thread's 4 rows, then a reduce-scatter over the 8
@@ -1017,7 +1055,7 @@ int packed_row_halves(int32_t /*dp*/) { return 1; }  // the epilogue combines a 
 int launch_affinity_tc_packed(const float* xhi, const float* xlo, const float* sqn, int64_t n,
                               int32_t dp, float neg_scale_log2, void* a_packed, float* degrow,
                               float* degcol, cudaStream_t s, int kind, bool half_out,
-                              int64_t row_lo, int64_t row_hi) {
+                              int64_t row_lo, int64_t row_hi, uint8_t* boxnz) {
   if (row_hi <= 0) row_hi = n;
   const int64_t nt = ceil_div(n, kBN);
   const int64_t t_lo = tile_index(row_lo / 128, row_lo / 128, nt);
@@ -1045,6 +1083,7 @@ int launch_affinity_tc_packed(const float* xhi, const float* xlo, const float* s
   args.degrow = degrow;
   args.degcol = degcol;
   args.kind = kind;
+  args.boxnz = boxnz;
   if (half_out) return dispatch_kb<kModePacked16>(dp / kKBlk, mp, args, s);
   return dispatch_kb<kModePacked>(dp / kKBlk, mp, args, s);
 }

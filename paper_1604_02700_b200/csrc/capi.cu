@@ -64,6 +64,7 @@ int64_t workspace_bytes(int64_t n, int32_t d, int32_t k, int64_t rows, int32_t /
   b += al(vector_pitch(n) * 4);               // v32
   b += al(kmeans_scratch_bytes(n, k));        // kmeans
   b += al(n * 8) + al(8);                     // low-degree row list + count
+  b += al(sparse_mask_bytes(n, d));           // block-sparsity mask (sparse.cu)
   return b;
 }
 
@@ -95,6 +96,7 @@ int carve(void* base, int64_t bytes, int64_t n, int32_t d, int32_t k, int64_t ro
   ws->kscratch = reinterpret_cast<double*>(take(ws->kscratch_bytes));
   ws->lowlist = reinterpret_cast<int64_t*>(take(n * 8));
   ws->lowcount = reinterpret_cast<unsigned long long*>(take(8));
+  ws->sparse = take(sparse_mask_bytes(n, d));
   ws->end = p;
   return GPIC_OK;
 }
@@ -380,6 +382,25 @@ int gpic_sym_matvec(const float* d_tiles, int64_t n, const float* d_v, float* d_
   return GPIC_OK;
 }
 
+int gpic_sym_matvec_sparse(const void* d_tiles, int32_t half, int64_t n, const float* d_v,
+                           float* d_rowp, float* d_colp, const double* d_row_scale, double* d_y,
+                           const uint8_t* d_boxnz, const int64_t* d_sb_prefix, void* stream) {
+  if (n < 1) return fail(GPIC_E_EMPTY, "empty matrix");
+  PeerTable pt;
+  std::memset(&pt, 0, sizeof pt);
+  pt.y[0][0] = pt.y[0][1] = d_y;
+  pt.nranks = 1;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (half)
+    launch_sym_gemv16(d_tiles, n, d_v, d_rowp, d_colp, d_row_scale, pt, nullptr, s, d_boxnz,
+                      d_sb_prefix);
+  else
+    launch_sym_gemv(static_cast<const float*>(d_tiles), n, d_v, d_rowp, d_colp, d_row_scale, pt,
+                    nullptr, s, ShardRange(), d_boxnz, d_sb_prefix);
+  GPIC_CUDA_TRY(cudaGetLastError());
+  return GPIC_OK;
+}
+
 int64_t gpic_vector_pitch(int64_t n) { return vector_pitch(n); }
 
 int64_t gpic_mf_ypart_doubles(int64_t n, int32_t d, int64_t rows) {
@@ -518,6 +539,28 @@ int gpic_packed_shard_build(const float* d_xhi, const float* d_xlo, const float*
   return GPIC_OK;
 }
 
+int gpic_cluster_workspace_layout(int64_t n, int32_t d, int32_t k, int32_t max_iter,
+                                  int32_t storage, int64_t* offsets) {
+  if (n < 1 || d < 1 || !offsets) return fail(GPIC_E_INVALID, "bad layout query");
+  const int64_t scratch = workspace_bytes(n, d, k, n, max_iter);
+  Workspace ws;
+  uint8_t* base = reinterpret_cast<uint8_t*>(uintptr_t(1) << 20);  // arithmetic only
+  int rc = carve(base, scratch, n, d, k, n, max_iter, &ws);
+  if (rc) return rc;
+  const bool half = storage == GPIC_STORAGE_PACKED16;
+  const int64_t tiles = scratch;
+  const int64_t rowp = tiles + packed_tiles(n) * 128 * 128 * (half ? 2 : 4);
+  const int64_t colp = rowp + al(sym_partial_floats(n) * 4);
+  const SparseMask sm = carve_sparse(ws.sparse, n, d);
+  offsets[0] = tiles;
+  offsets[1] = rowp;
+  offsets[2] = colp;
+  offsets[3] = reinterpret_cast<uint8_t*>(sm.boxnz) - base;
+  offsets[4] = reinterpret_cast<uint8_t*>(sm.sb_prefix) - base;
+  offsets[5] = reinterpret_cast<uint8_t*>(ws.deg) - base;
+  return GPIC_OK;
+}
+
 int64_t gpic_cluster_workspace_bytes(int64_t n, int32_t d, int32_t k, int32_t max_iter,
                                      int32_t storage) {
   if (n < 1 || d < 1) return -1;
@@ -600,19 +643,27 @@ int cluster_impl(const double* d_x, int64_t n, int32_t d, double sigma, int32_t 
     const int64_t pf = al(sym_partial_floats(n) * 4) / 4;
     float* degrow = colp + pf;
     float* degcol = degrow + 2 * pf;
+    // block sparsity: the tensor engine does not store 32 x 32 boxes whose
+    // values are all exact fp32 zeros and flags the ones it stores; the GEMV
+    // reads only those (sparse.cu; bit-identical to the dense run)
+    const SparseMask sm = carve_sparse(ws.sparse, n, d);
+    const bool sparse = sparse_enabled() && impl == GPIC_AFFINITY_TC;
     if (impl == GPIC_AFFINITY_SIMT) {
       launch_affinity_simt_packed(ws.xlo, ws.sqn, n, d, dp, neg_scale_log2, a, degrow, degcol, s,
                                   kind);
     } else {
       rc = launch_affinity_tc_packed(ws.xhi, ws.xlo, ws.sqn, n, dp, neg_scale_log2, a, degrow,
-                                     degcol, s, kind, half);
+                                     degcol, s, kind, half, 0, 0, sparse ? sm.boxnz : nullptr);
       if (rc) return rc;
     }
+    if (sparse) launch_sparse_prefix(sm, s);
     mark(ev, 1, s);
     launch_sym_degree(degrow, degcol, n, packed_row_halves(dp), deg, nullptr, s);
     L.mode = half ? kLoopPacked16 : kLoopPacked;
     L.rowp = rowp;
     L.colp = colp;
+    L.boxnz = sparse ? sm.boxnz : nullptr;
+    L.sb_prefix = sparse ? sm.sb_prefix : nullptr;
   } else if (storage == GPIC_STORAGE_NONE) {
     // matrix-free: A is recomputed from X for the degrees and every iteration
     double* ypart = reinterpret_cast<double*>(a);

@@ -122,18 +122,21 @@ __global__ void __launch_bounds__(kLowThreads)
 
 }  // namespace
 
-double low_degree_threshold(int kind) {
-  // RBF: below 1e-20 the fp32 entries lost to flush-to-zero (< 1.2e-38
-  // each, n of them) can reach 1e-9 of the degree at n = 1e9; cosine: the
-  // fp32 Gram's ~1e-7 absolute error per entry dominates a degree < 1e-2
-  return kind == GPIC_KIND_COSINE ? 1e-2 : 1e-20;
+double low_degree_threshold(int kind, int64_t n) {
+  // RBF: the engines flush entries below 2^-64 (sm100.cuh kFlushLog2); n of
+  // them stay below 2^-24 of any degree above n 2^-40 (and below 1e-20 the
+  // fp32 row is gone anyway); cosine: the fp32 Gram's ~1e-7 absolute error
+  // per entry dominates a degree < 1e-2
+  if (kind == GPIC_KIND_COSINE) return 1e-2;
+  const double t = (double)n * 0x1p-40;
+  return t > 1e-20 ? t : 1e-20;
 }
 
 void launch_lowdeg_scan(const double* deg, int64_t n, int kind, int64_t* list,
                         unsigned long long* count, cudaStream_t s) {
   cudaMemsetAsync(count, 0, sizeof(unsigned long long), s);
-  lowdeg_scan_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, s>>>(deg, n, low_degree_threshold(kind),
-                                                               list, count);
+  lowdeg_scan_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, s>>>(
+      deg, n, low_degree_threshold(kind, n), list, count);
   count_launch();
 }
 

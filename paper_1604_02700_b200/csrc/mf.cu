@@ -17,6 +17,7 @@
 
 #include "common.cuh"
 #include "ops.h"
+#include "sm100.cuh"
 
 namespace gpic {
 
@@ -98,8 +99,7 @@ __global__ void __launch_bounds__(256)
         const float df = xi[k] - cx[jj][k];
         d2 = fmaf(df, df, d2);
       }
-      float a;
-      asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(a) : "f"(d2 * ns));
+      float a = ex2_flush(d2 * ns);
       if (j0 + jj == gi) a = 0.f;
       s = fmaf(a, cv[jj], s);
     }

@@ -50,10 +50,12 @@ void launch_affinity_simt_packed(const float* xlo, const float* sqn, int64_t n, 
                                  float* degcol, cudaStream_t s, int kind);
 // feature pitches the tcgen05 engine runs (store modes / matrix-free)
 bool tc_supports_pitch(int32_t dp, bool matvec);
+// boxnz: non-null -> zero boxes are not stored and flagged there (sparse.cu)
 int launch_affinity_tc_packed(const float* xhi, const float* xlo, const float* sqn, int64_t n,
                               int32_t dp, float neg_scale_log2, void* a_packed, float* degrow,
                               float* degcol, cudaStream_t s, int kind = GPIC_KIND_RBF,
-                              bool half_out = false, int64_t row_lo = 0, int64_t row_hi = 0);
+                              bool half_out = false, int64_t row_lo = 0, int64_t row_hi = 0,
+                              uint8_t* boxnz = nullptr);
 void launch_sym_degree(const float* degrow, const float* degcol, int64_t n, int nhalf,
                        double* deg, gpic_ctl* ctl, cudaStream_t s,
                        const ShardRange& sr = ShardRange());
@@ -76,6 +78,7 @@ struct Workspace {
   double* kscratch;    // k-means scratch (see kmeans.cu)
   int64_t* lowlist;    // n low-degree row indices (lowdeg.cu)
   unsigned long long* lowcount;
+  uint8_t* sparse;     // SparseMask storage (sparse.cu)
   int64_t kscratch_bytes;
   uint8_t* end;
 };
@@ -145,12 +148,15 @@ void launch_copy_result(const double* v64, int64_t n, double* out, const gpic_ct
                         cudaStream_t s);
 
 struct PeerTable;
+// boxnz / sb_prefix: block sparsity (SparseMask), null = every box stored
 void launch_sym_gemv(const float* tiles, int64_t n, const float* v32, float* rowp, float* colp,
                      const double* deg, const PeerTable& pt, gpic_ctl* ctl, cudaStream_t s,
-                     const ShardRange& sr = ShardRange());
+                     const ShardRange& sr = ShardRange(), const uint8_t* boxnz = nullptr,
+                     const int64_t* sb_prefix = nullptr);
 // fp16 packed tiles (GPIC_STORAGE_PACKED16): same partials / reduce
 void launch_sym_gemv16(const void* tiles, int64_t n, const float* v32, float* rowp, float* colp,
-                       const double* deg, const PeerTable& pt, gpic_ctl* ctl, cudaStream_t s);
+                       const double* deg, const PeerTable& pt, gpic_ctl* ctl, cudaStream_t s,
+                       const uint8_t* boxnz = nullptr, const int64_t* sb_prefix = nullptr);
 
 // ---- matrix-free (affinity_tc.cu matvec mode + mf.cu) --------------------
 struct MfOperands {
@@ -181,25 +187,24 @@ int launch_mf_degrees(const MfOperands& op, int64_t row_lo, int64_t rows, float*
                       double* ypart, double* deg, cudaStream_t s);
 
 // ---- block sparsity (sparse.cu) ------------------------------------------
-// zero[tile_index(I, J)] = 1 when a bounding-sphere bound proves every fp32
-// entry of packed tile (I, J) is 0 (exp below the fp32 flush, with margin);
-// item_prefix{1,2}[u] = non-zero affinity work units (MB = 1, 2) before
-// unit u; sb_prefix[s] = GEMV super-block weight before super-block s.
+// boxnz[tile * 16 + quadrant * 4 + chunk] = 1 when the affinity epilogue
+// stored that 32 x 32 box of packed tile `tile`, 0 when every value of it was
+// an exact fp32 zero (not stored); sb_prefix[s] = GEMV super-block weight
+// (8 per stored tile + 1) before super-block s.
 struct SparseMask {
   int64_t nt = 0;
-  double* centre = nullptr;  // nt x d
-  double* radius = nullptr;  // nt
-  uint8_t* zero = nullptr;   // packed tiles
-  int64_t* item_prefix1 = nullptr;
-  int64_t* item_prefix2 = nullptr;
+  uint8_t* boxnz = nullptr;
   int64_t* sb_prefix = nullptr;
   int64_t n_sb = 0;
 };
-int64_t packed_items_mb(int64_t n, int mb);
 int64_t sparse_mask_bytes(int64_t n, int32_t d);
 SparseMask carve_sparse(void* base, int64_t n, int32_t d);
-void launch_sparse_mask(const SparseMask& m, const float* xc, int64_t n, int32_t d, int32_t dp,
-                        double sigma, cudaStream_t s);
+// the GEMV weights from the box flags the affinity engine wrote
+void launch_sparse_prefix(const SparseMask& m, cudaStream_t s);
+// every box flag = v (engines that store every box)
+void launch_box_fill(const SparseMask& m, uint8_t v, cudaStream_t s);
+// GPIC_SPARSE=0 turns the zero-box skipping off (dense packed runs, for comparisons)
+bool sparse_enabled();
 
 // ---- low-degree (isolated) rows, lowdeg.cu -----------------------------
 // Rows whose engine degree is below low_degree_threshold(kind): recomputed
@@ -214,7 +219,7 @@ struct LowRows {
   const unsigned long long* d_count = nullptr;  // device count of list
   int64_t count = 0;                          // host copy (0: nothing to do)
 };
-double low_degree_threshold(int kind);
+double low_degree_threshold(int kind, int64_t n);
 void launch_lowdeg_scan(const double* deg, int64_t n, int kind, int64_t* list,
                         unsigned long long* count, cudaStream_t s);
 int read_low_count(const unsigned long long* d_count, int64_t* out, cudaStream_t s);
@@ -251,6 +256,9 @@ struct ShardLoop {
   const double* slots;   // this rank's slot [0][0]; (rank, parity) at (2 rank + parity) * stride
   int64_t slot_stride;
   const double* deg_full;
+  // packed modes: stored-box flags + GEMV super-block weights (null: dense)
+  const uint8_t* boxnz;
+  const int64_t* sb_prefix;
   // isolated rows redone in fp64 after the y exchange (count 0: none)
   LowRows low;
   const double* low_deg;  // full n-vector of degrees (exact for listed rows)

@@ -354,9 +354,11 @@ int run_power_loops(ShardLoop* shards, int nlocal, int64_t n, int32_t max_iter, 
       for (int i = 0; i < nlocal; ++i) {
         const ShardLoop& L = shards[i];
         if (L.mode == kLoopPacked) {
-          launch_sym_gemv(L.a, n, L.v32, L.rowp, L.colp, L.deg, L.pt, L.ctl, cs);
+          launch_sym_gemv(L.a, n, L.v32, L.rowp, L.colp, L.deg, L.pt, L.ctl, cs, ShardRange(),
+                          L.boxnz, L.sb_prefix);
         } else if (L.mode == kLoopPacked16) {
-          launch_sym_gemv16(L.a, n, L.v32, L.rowp, L.colp, L.deg, L.pt, L.ctl, cs);
+          launch_sym_gemv16(L.a, n, L.v32, L.rowp, L.colp, L.deg, L.pt, L.ctl, cs, L.boxnz,
+                            L.sb_prefix);
         } else if (L.mode == kLoopPackedShard) {
           // partial y over the shard's tiles into every rank's slot of this shard
           launch_sym_gemv(L.a, n, L.v32, L.rowp, L.colp, nullptr, L.pt_slots, L.ctl, cs, L.sr);

@@ -233,6 +233,17 @@ __device__ __forceinline__ float ex2(float x) {
   return y;
 }
 
+// RBF entries below 2^-64 are stored as exact zeros (every engine, every
+// storage): n such entries move a row's sum by at most n 2^-64, below fp32
+// resolution for any row whose degree exceeds n 2^-40 — rows under that are
+// redone in fp64 (lowdeg.cu) — and a 32 x 32 box of them is then neither
+// computed further nor stored (sparse.cu). ex2.approx.ftz alone flushes at
+// 2^-126.
+constexpr float kFlushLog2 = -64.f;
+__device__ __forceinline__ float ex2_flush(float x) {
+  return x < kFlushLog2 ? 0.f : ex2(x);
+}
+
 
 // 1-D bulk copy global -> shared, completing on an mbarrier (16-byte
 // aligned addresses, size a multiple of 16).

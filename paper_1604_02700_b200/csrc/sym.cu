@@ -76,6 +76,34 @@ __device__ inline void tile_coords(int64_t t, int64_t nt, int64_t& I, int64_t& J
 // NS x NS triangle (NS = ceil(NT / kSB)), same index formula as the tiles.
 constexpr int kSB = 4;
 
+// Block sparsity (sparse.cu): boxnz[t * 16 + quadrant * 4 + chunk] flags the
+// 32 x 32 boxes of packed tile t the affinity engine stored (the others are
+// exact zeros, never written); a tile with no stored box is never read.
+// sbp[s] = weight prefix of the GEMV super-blocks (8 per stored tile + 1),
+// so a super-block of weight 1 holds no stored tile. Both null: dense.
+struct Sparse {
+  const uint8_t* boxnz;
+  const int64_t* sbp;
+  __device__ uint4 flags(int64_t I, int64_t J, int64_t nt) const {
+    return *reinterpret_cast<const uint4*>(boxnz + tile_index(I, J, nt) * 16);
+  }
+  __device__ bool skip_tile(int64_t I, int64_t J, int64_t nt) const {
+    if (boxnz == nullptr) return false;
+    const uint4 f = flags(I, J, nt);
+    return (f.x | f.y | f.z | f.w) == 0u;
+  }
+  __device__ bool empty_sb(int64_t s) const { return sbp != nullptr && sbp[s + 1] - sbp[s] == 1; }
+};
+
+// first s in [lo, hi] with sbp[s] >= target (sbp strictly increasing)
+__device__ inline int64_t lower_bound64(const int64_t* a, int64_t lo, int64_t hi, int64_t target) {
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (a[mid] >= target) hi = mid; else lo = mid + 1;
+  }
+  return lo;
+}
+
 }  // namespace
 
 // A packed shard: super-rows [p_lo, p_hi) of the super-block triangle (tile
@@ -134,7 +162,7 @@ template <typename T>
 __global__ void __launch_bounds__(kThreads, 1)
     sym_gemv_kernel(const T* __restrict__ tiles, int64_t nt, const float* __restrict__ v32,
                     float* __restrict__ rowp, float* __restrict__ colp,
-                    const gpic_ctl* __restrict__ ctl, ShardRange sr) {
+                    const gpic_ctl* __restrict__ ctl, ShardRange sr, Sparse sp) {
   constexpr int kStages = TileTraits<T>::kStg;
   constexpr int kTileBytes = kTileFloats * (int)sizeof(T);
   if (ctl != nullptr && *(volatile const int32_t*)&ctl->stop) return;
@@ -157,8 +185,16 @@ __global__ void __launch_bounds__(kThreads, 1)
   // the shard's super-blocks [sb_lo, sb_hi) (whole matrix: all of them);
   // records are indexed from sb_lo, tiles from the shard's first tile
   const int64_t sb_lo = sr.sb_lo(ns), total = sr.sb_hi(ns) - sb_lo;
-  const int64_t s0 = sb_lo + total * blockIdx.x / gridDim.x;
-  const int64_t s1 = sb_lo + total * (blockIdx.x + 1) / gridDim.x;
+  int64_t s0 = sb_lo + total * blockIdx.x / gridDim.x;
+  int64_t s1 = sb_lo + total * (blockIdx.x + 1) / gridDim.x;
+  if (sp.sbp != nullptr) {  // equal shares of real work (non-zero tiles), not of super-blocks
+    const int64_t sb_hi = sb_lo + total;
+    const int64_t w0 = sp.sbp[sb_lo], W = sp.sbp[sb_hi] - w0;
+    s0 = lower_bound64(sp.sbp, sb_lo, sb_hi, w0 + W * blockIdx.x / gridDim.x);
+    s1 = blockIdx.x + 1 == gridDim.x
+             ? sb_hi
+             : lower_bound64(sp.sbp, sb_lo, sb_hi, w0 + W * (blockIdx.x + 1) / gridDim.x);
+  }
   if (s0 >= s1) return;
   SbWalk w;
   w.nt = nt;
@@ -174,8 +210,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     w.P = P0;
     w.Q = Q0;
     for (int64_t sb = s0; sb < s1; ++sb, w.next_sb()) {
+      if (sp.empty_sb(sb)) continue;
       w.open(w.P, w.Q);
       do {
+        if (sp.skip_tile(w.I, w.J, nt)) continue;  // no stored box: never read
         mbar_wait(&empty[s], ph ^ 1);
         mbar_expect_tx(&full[s], kTileBytes);
         bulk_load(st + s * kTileBytes, src0 + (tile_index(w.I, w.J, nt) - sr.tile_base) * kTileBytes, kTileBytes,
@@ -193,6 +231,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   w.P = P0;
   w.Q = Q0;
   for (int64_t sb = s0; sb < s1; ++sb, w.next_sb()) {
+    if (sp.empty_sb(sb)) continue;  // no stored tile: its records are never read
     w.open(w.P, w.Q);
     // per lane: the column products of the super-block's kSB tile columns,
     // accumulated over its tile rows (one cross-warp combine per super-block)
@@ -206,6 +245,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     float4 vj = __ldg(reinterpret_cast<const float4*>(v32 + w.J * kTS) + lane);
     for (;;) {
       const int64_t I = w.I, J = w.J;
+      const bool zt = sp.skip_tile(I, J, nt);
+      // this lane's box (rows of this warp, columns 4 lane .. +3): stored?
+      bool box_ok = true;
+      if (sp.boxnz != nullptr && !zt)
+        box_ok = sp.boxnz[tile_index(I, J, nt) * 16 + (warp >> 1) * 4 + (lane >> 3)] != 0;
       const bool more = w.next();
       const bool row_end = !more || w.I != I;
       // next tile's v slices, one tile ahead
@@ -215,6 +259,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         vj_n = __ldg(reinterpret_cast<const float4*>(v32 + w.J * kTS) + lane);
         if (row_end && lane < kRowsPerWarp) vi_n = __ldg(v32 + w.I * kTS + warp * kRowsPerWarp + lane);
       }
+      if (!zt) {
       mbar_wait(&full[s], ph);
       const uint8_t* tile = st + s * kTileBytes + warp * kRowsPerWarp * kTS * (int)sizeof(T);
       // row products into acc; off the diagonal, column products into the
@@ -222,7 +267,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       auto tile_products = [&](float4& cp, bool col) {
 #pragma unroll
         for (int i = 0; i < kRowsPerWarp; ++i) {
-          const float4 a = TileTraits<T>::load4(tile + i * kTS * (int)sizeof(T), lane);
+          float4 a = TileTraits<T>::load4(tile + i * kTS * (int)sizeof(T), lane);
+          if (!box_ok) a = make_float4(0.f, 0.f, 0.f, 0.f);  // unstored box: exact zeros
           float r = fmaf(a.x, vj.x, acc[i]);
           r = fmaf(a.y, vj.y, r);
           r = fmaf(a.z, vj.z, r);
@@ -249,6 +295,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
       if (++s == kStages) { s = 0; ph ^= 1; }
+      }
       if (row_end) {
         // transpose-reduce the 16 row accumulators across the 32 lanes
         // (fixed pattern): after 4 halving steps lane l holds row f(l) over
@@ -324,7 +371,7 @@ constexpr int kSeg = 8;
 __global__ void __launch_bounds__(kTS * kSeg)
     sym_reduce_kernel(const float* __restrict__ rowp, const float* __restrict__ colp, int64_t n,
                       int64_t nt, const double* __restrict__ deg, const PeerTable pt,
-                      gpic_ctl* ctl, ShardRange sr) {
+                      gpic_ctl* ctl, ShardRange sr, Sparse sp) {
   if (ctl != nullptr && *(volatile const int32_t*)&ctl->stop) return;
   __shared__ double part[kSeg][kTS];
   const int64_t ns = (nt + kSB - 1) / kSB;
@@ -340,8 +387,10 @@ __global__ void __launch_bounds__(kTS * kSeg)
   const int64_t terms = ncol + nrow;
   const int64_t p0 = terms * sg / kSeg, p1 = terms * (sg + 1) / kSeg;
   auto load = [&](int64_t p) {
-    return p < ncol ? colp[((tile_index(sr.p_lo + p, Q, ns) - sb0) * kSB + k) * kTS + o]
-                    : rowp[((tile_index(Q, Q + (p - ncol), ns) - sb0) * kSB + k) * kTS + o];
+    const int64_t sbi = p < ncol ? tile_index(sr.p_lo + p, Q, ns) : tile_index(Q, Q + (p - ncol), ns);
+    if (sp.empty_sb(sbi)) return 0.f;  // no records: a super-block of zero tiles
+    return p < ncol ? colp[((sbi - sb0) * kSB + k) * kTS + o]
+                    : rowp[((sbi - sb0) * kSB + k) * kTS + o];
   };
   double s = 0.0;
   int64_t p = p0;
@@ -475,7 +524,8 @@ int64_t sym_partial_floats(int64_t n) {
 
 void launch_sym_gemv(const float* tiles, int64_t n, const float* v32, float* rowp, float* colp,
                      const double* deg, const PeerTable& pt, gpic_ctl* ctl, cudaStream_t s,
-                     const ShardRange& sr) {
+                     const ShardRange& sr, const uint8_t* boxnz, const int64_t* sb_prefix) {
+  const Sparse sp{boxnz, boxnz != nullptr ? sb_prefix : nullptr};
   sym_prepare();
   const int64_t nt = ceil_div(n, kTS);
   const int64_t ns = (nt + kSB - 1) / kSB;
@@ -483,13 +533,15 @@ void launch_sym_gemv(const float* tiles, int64_t n, const float* v32, float* row
   const int grid = (int)(total < g_sms ? total : g_sms);
   const int64_t rows = nt - kSB * sr.p_lo;
   if (grid < 1 || rows < 1) return;
-  sym_gemv_kernel<float><<<grid, kThreads, kSmem, s>>>(tiles, nt, v32, rowp, colp, ctl, sr);
-  sym_reduce_kernel<<<(unsigned)rows, kTS * kSeg, 0, s>>>(rowp, colp, n, nt, deg, pt, ctl, sr);
+  sym_gemv_kernel<float><<<grid, kThreads, kSmem, s>>>(tiles, nt, v32, rowp, colp, ctl, sr, sp);
+  sym_reduce_kernel<<<(unsigned)rows, kTS * kSeg, 0, s>>>(rowp, colp, n, nt, deg, pt, ctl, sr, sp);
   count_launch(2);
 }
 
 void launch_sym_gemv16(const void* tiles, int64_t n, const float* v32, float* rowp, float* colp,
-                       const double* deg, const PeerTable& pt, gpic_ctl* ctl, cudaStream_t s) {
+                       const double* deg, const PeerTable& pt, gpic_ctl* ctl, cudaStream_t s,
+                       const uint8_t* boxnz, const int64_t* sb_prefix) {
+  const Sparse sp{boxnz, boxnz != nullptr ? sb_prefix : nullptr};
   sym_prepare();
   const int64_t nt = ceil_div(n, kTS);
   const int64_t ns = (nt + kSB - 1) / kSB;
@@ -497,8 +549,8 @@ void launch_sym_gemv16(const void* tiles, int64_t n, const float* v32, float* ro
   const int grid = (int)(total < g_sms ? total : g_sms);
   const ShardRange all{};
   sym_gemv_kernel<__half><<<grid, kThreads, kSmem, s>>>(static_cast<const __half*>(tiles), nt, v32,
-                                                            rowp, colp, ctl, all);
-  sym_reduce_kernel<<<(unsigned)nt, kTS * kSeg, 0, s>>>(rowp, colp, n, nt, deg, pt, ctl, all);
+                                                            rowp, colp, ctl, all, sp);
+  sym_reduce_kernel<<<(unsigned)nt, kTS * kSeg, 0, s>>>(rowp, colp, n, nt, deg, pt, ctl, all, sp);
   count_launch(2);
 }
 
