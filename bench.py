@@ -344,42 +344,39 @@ def _gemv_roofline(args, L, C, torch, stream, st, n, m, k, T, work, v, storage):
     yv = torch.empty(n, dtype=torch.float64, device=dev)
     deg1 = torch.ones(n, dtype=torch.float64, device=dev)
     if storage == 2:
-        # matrix-free: one recompute pass A v (tcgen05 3-term fp16 Gram + exp + v),
-        # timed through the degree entry (v = 1); work = 3 x 2 n^2 dp flops
-        scr = ((int(L.gpic_workspace_bytes(n, m, k, n, T)) + 255) // 256) * 256
+        # matrix-free: the power loop's own A v pass (tcgen05 3-term fp16 Gram
+        # + exp + v, over the kept tiles after pruning), rerun on the
+        # operands / mask the cluster run left in `work`
         dp = int(L.gpic_feature_pitch(m))
-        npad = int(L.gpic_row_pad(n))
-        # xhi / xlo / sqn live at the head of the workspace (after the ctl)
-        xhi = work.data_ptr() + 256
-        xlo = xhi + ((int(L.gpic_operand_floats(n, m)) * 4 + 255) // 256) * 256
-        sqn = xlo + ((npad * dp * 4 + 255) // 256) * 256
-        ypart = torch.empty(int(L.gpic_mf_ypart_doubles(n, m, n)), dtype=torch.float64, device=dev)
-        ones = torch.empty(vp, dtype=torch.float32, device=dev)
         sigma = CONFIGS_SIGMA[n]
+        pruned = 1 if os.environ.get("GPIC_PRUNE", "1") != "0" and os.environ.get(
+            "GPIC_SPARSE", "1") != "0" and m > 8 else 0
 
         from paper_1604_02700_b200 import _lib
 
         def launch():
-            return L.gpic_mf_degrees(C.c_void_p(xhi), C.c_void_p(xlo), C.c_void_p(sqn), n, m, 0, n,
-                                     sigma, _lib.KIND_RBF, C.c_void_p(ones.data_ptr()),
-                                     C.c_void_p(ypart.data_ptr()), C.c_void_p(yv.data_ptr()), st)
-        # the whole-matrix pass computes the upper triangle of tile pairs
-        # (MB row tiles x 1 column tile each, J >= MB * I): entries actually
-        # computed x 3 terms x 2 x (dp + 16 norm-block columns)
+            return L.gpic_cluster_mf_pass(C.c_void_p(work.data_ptr()), n, m, k, T, sigma,
+                                          _lib.KIND_RBF, pruned, C.c_void_p(v32.data_ptr()),
+                                          C.c_void_p(yv.data_ptr()), st)
+        # units computed (MB row tiles x 1 column tile each, J >= MB * I,
+        # minus the pruned ones) x 128 MB x 128 entries x 3 terms x 2 x
+        # (dp + 16 norm-block columns)
         mb = 2 if dp == 64 else 1
-        nrt, nct = -(-n // (128 * mb)), -(-n // 128)
-        items = nrt * nct - mb * nrt * (nrt - 1) // 2
+        kept, tot = C.c_int64(0), C.c_int64(0)
+        assert L.gpic_cluster_pruned_work(C.c_void_p(work.data_ptr()), n, m, k, T, storage,
+                                          C.byref(kept), C.byref(tot), st) == 0
+        units = kept.value if pruned else tot.value
         if os.environ.get("GPIC_MF_SYM", "1") == "0":
-            items = nrt * nct
-        alg = 3.0 * 2.0 * (dp + 16) * float(items) * 128 * mb * 128
+            units = -(-n // (128 * mb)) * -(-n // 128)
+        alg = 3.0 * 2.0 * (dp + 16) * float(units) * 128 * mb * 128
         name = ("affinity_tc_kernel<matvec> (matrix-free symmetric A v pass: 3-term fp16 Gram "
-                "with the distance from the MMA, exp2, row + column products)")
-        del scr
+                "with the distance from the MMA, exp2, row + column products; "
+                f"{units} of {tot.value} tile units after pruning)")
     elif storage in (1, 3):
         # the packed GEMV as the run executes it: only tiles with a stored
         # box are read (block sparsity, csrc/sparse.cu); algorithmic bytes =
         # the stored tiles' bytes, counted from the run's own box flags
-        offs = (C.c_int64 * 6)()
+        offs = (C.c_int64 * 8)()
         assert L.gpic_cluster_workspace_layout(n, m, k, T, storage, offs) == 0
         base0 = work.data_ptr()
         tiles, rowp, colp = base0 + offs[0], base0 + offs[1], base0 + offs[2]
@@ -505,6 +502,14 @@ def run_ours(args, cfg, rank, world):
 
     kname, alg_bytes, gemv_ms = _gemv_roofline(args, L, C, torch, stream, st, n, m, k, T, work,
                                                v, storage)
+    pruning = None
+    if storage in (1, 2, 3) and args.engine == "tc":
+        kept, tot = C.c_int64(0), C.c_int64(0)
+        if L.gpic_cluster_pruned_work(C.c_void_p(work.data_ptr()), n, m, k, T, storage,
+                                      C.byref(kept), C.byref(tot), st) == 0:
+            pruning = {"tensor_units_computed": int(kept.value), "tensor_units_total": int(tot.value),
+                       "rule": "block pairs whose projection bound puts every entry below 2^-66 "
+                               "are not computed (bit-identical: they flush to 0 at 2^-64)"}
     achieved = alg_bytes / (gemv_ms * 1e-3) / 1e9
     dense_equiv = float(n) * n * 4 / (gemv_ms * 1e-3) / 1e9
     peak, peak_kind = peaks()
@@ -565,6 +570,7 @@ def run_ours(args, cfg, rank, world):
         "e2e": {"value": e2e_s, "unit": "s", "h2d_bytes_per_step": int(n * m * 8),
                 "d2h_bytes_per_step": int(n * 8 * 2 + T * 8)},
         "phases_ms": phases_ms,
+        "pruning": pruning,
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
     }

@@ -184,7 +184,10 @@ int gpic_power_iterate(const float* d_a, int64_t lda, const double* d_deg, int64
  * kmeans.py:43,51,73), Lloyd rounds (<= max_rounds, tol), exact DP polish
  * when n <= 4096 (kmeans.py:97-130), contiguity check/repair
  * (kmeans.py:133-160) and canonical relabel by ascending centroid
- * (kmeans.py:163-175). Writes int64 labels. */
+ * (kmeans.py:163-175). Writes int64 labels. 2 <= k <= min(n, 4096):
+ * k <= 64 keeps per-cluster registers (kmeans.cu); 64 < k runs the same
+ * algorithm on the once-sorted values (kmeans_big.cu: clusters are
+ * contiguous runs, sums are prefix differences). */
 int gpic_kmeans1d(const double* d_v, int64_t n, int32_t k, int64_t first_index,
                   const double* h_uniforms, int32_t max_rounds, double tol, int64_t* d_labels,
                   void* d_work, gpic_ctl* d_ctl, void* stream);
@@ -264,11 +267,27 @@ int gpic_sym_matvec_sparse(const void* d_tiles, int32_t half, int64_t n, const f
 int64_t gpic_packed_tiles(int64_t n);
 int64_t gpic_cluster_workspace_bytes(int64_t n, int32_t d, int32_t k, int32_t max_iter,
                                      int32_t storage);
-/* Byte offsets inside that workspace (packed storages): [0] tiles, [1] GEMV
- * row records, [2] column records, [3] stored-box flags, [4] GEMV weights,
- * [5] degrees (fp64). For measurement and tests. */
+/* Byte offsets inside that workspace (packed storages), offsets[8]: [0]
+ * tiles, [1] GEMV row records, [2] column records, [3] stored-box flags,
+ * [4] GEMV weights, [5] degrees (fp64), [6] the count (int64) of tcgen05
+ * work units computed after tile pruning, [7] the number of units before
+ * pruning (a value, not an offset). For measurement and tests. */
 int gpic_cluster_workspace_layout(int64_t n, int32_t d, int32_t k, int32_t max_iter,
                                   int32_t storage, int64_t* offsets);
+/* Work the tensor engine did in the last gpic_cluster run on this
+ * workspace after tile pruning (prune.cu: block pairs proved to hold only
+ * entries below 2^-64 are never computed): packed storages -> kept / all
+ * work units (128 MB rows x 128 columns); GPIC_STORAGE_NONE -> kept / all
+ * tile units of one symmetric pass. Synchronizes `stream`. */
+int gpic_cluster_pruned_work(const void* d_work, int64_t n, int32_t d, int32_t k,
+                             int32_t max_iter, int32_t storage, int64_t* kept, int64_t* total,
+                             void* stream);
+/* One matrix-free pass y = A v (no 1/deg) on the operands, pruning mask
+ * (pruned != 0) and partial buffers that a GPIC_STORAGE_NONE gpic_cluster
+ * run left in d_work — the power loop's own pass, for kernel timing. */
+int gpic_cluster_mf_pass(void* d_work, int64_t n, int32_t d, int32_t k, int32_t max_iter,
+                         double sigma, int32_t kind, int32_t pruned, const float* d_v32,
+                         double* d_y, void* stream);
 int gpic_cluster(const double* d_x, int64_t n, int32_t d, double sigma, int32_t kind, int32_t k,
                  double eps, int32_t max_iter, int64_t first_index, const double* h_uniforms,
                  int32_t impl, int32_t storage, const double* d_v0, int64_t* d_labels, double* d_v,
@@ -312,7 +331,7 @@ int gpic_ctl_init(gpic_ctl* d_ctl, double eps, int32_t max_iter, void* stream);
 int gpic_scale(const double* d_src, int64_t n, double tau, double* d_dst, float* d_dst32,
                int64_t f32_len, void* stream);
 
-/* Device scratch of gpic_kmeans1d for n values. */
+/* Device scratch of gpic_kmeans1d for n values and k clusters. */
 int64_t gpic_kmeans_scratch_bytes(int64_t n, int32_t k);
 
 /* Read the control block back (synchronizes `stream`). */

@@ -103,6 +103,8 @@ SIGNATURES = {
     "gpic_sym_matvec16": (C.c_int, [P, I64, P, P, P, P, P, P]),
     "gpic_sym_matvec_sparse": (C.c_int, [P, I32, I64, P, P, P, P, P, P, P, P]),
     "gpic_cluster_workspace_layout": (C.c_int, [I64, I32, I32, I32, I32, P]),
+    "gpic_cluster_pruned_work": (C.c_int, [P, I64, I32, I32, I32, I32, P, P, P]),
+    "gpic_cluster_mf_pass": (C.c_int, [P, I64, I32, I32, I32, C.c_double, I32, I32, P, P, P]),
     "gpic_sym_partial_floats": (I64, [I64]),
     "gpic_packed_shard_range": (C.c_int, [I64, I32, I32, P, P]),
     "gpic_packed_shard_tiles": (I64, [I64, I64, I64]),

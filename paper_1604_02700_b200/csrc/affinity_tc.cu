@@ -156,7 +156,33 @@ struct TcArgs {
   // zeros is not stored; boxnz[(tile) * 16 + quadrant * 4 + chunk] records
   // which boxes were (sparse.cu). Indexed by the global packed tile.
   uint8_t* boxnz;
+  // packed store modes: non-null -> only the listed work units (ascending
+  // packed unit ids, *unit_count of them) are computed; the others are
+  // provably zero block pairs (prune.cu) and the CTAs split the list
+  const int32_t* unit_list;
+  const int64_t* unit_count;
+  // matvec sym: non-null -> unit_list holds the kept (row block, chunk)
+  // items (id = rb * n_chunks + chunk) and a tile cb of an item is computed
+  // only if pskip[S(rb) * pnb + T(cb)] == 0 (blocks of pB rows, prune.cu)
+  const uint8_t* pskip;
+  int64_t pB, pnb;
+  const int64_t* wpre;  // matvec listed: kept tiles before each item (CTA balance)
 };
+
+// first u in [lo, hi] with a[u] >= target (a non-decreasing)
+__device__ inline int64_t lower_bound_w(const int64_t* a, int64_t lo, int64_t hi, int64_t target) {
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (a[mid] >= target) hi = mid; else lo = mid + 1;
+  }
+  return lo;
+}
+
+// the work list of a listed run (packed units or matrix-free items)
+template <int MODE>
+__host__ __device__ inline bool run_listed(const TcArgs& a) {
+  return a.unit_list != nullptr && (is_packed(MODE) || (MODE == kModeMatvec && a.sym));
+}
 
 __host__ __device__ inline int64_t packed_items(int64_t nrt, int64_t nct, int mb) {
   return nrt * nct - (int64_t)mb * nrt * (nrt - 1) / 2;
@@ -187,20 +213,23 @@ struct Cursor {
   int chunk;           // matvec: chunk index of the current item
   int wave;            // strided: current wave
   bool strided;
+  bool listed;         // unit list (prune.cu): u indexes the list
+  int64_t uid;         // listed: current unit id
 
-  __device__ void decode_unit(const TcArgs& a) {
+  __device__ void decode_unit(const TcArgs& a) { decode_id(a, u); }
+  __device__ void decode_id(const TcArgs& a, int64_t id) {
     if (MODE == kModeDense) {
-      rb = (int)(u / a.n_ctiles);
-      cb = (int)(u % a.n_ctiles);
+      rb = (int)(id / a.n_ctiles);
+      cb = (int)(id % a.n_ctiles);
     } else {
       int64_t lo = 0, hi = a.n_rtiles - 1;
       while (lo < hi) {
         const int64_t mid = (lo + hi + 1) >> 1;
         const int64_t s = mid * a.n_ctiles - (int64_t)MB * mid * (mid - 1) / 2;
-        if (s <= u) lo = mid; else hi = mid - 1;
+        if (s <= id) lo = mid; else hi = mid - 1;
       }
       rb = (int)lo;
-      cb = (int)(lo * MB + (u - (lo * a.n_ctiles - (int64_t)MB * lo * (lo - 1) / 2)));
+      cb = (int)(lo * MB + (id - (lo * a.n_ctiles - (int64_t)MB * lo * (lo - 1) / 2)));
     }
   }
   // strided: first row block at or after `wave`; false when none is left
@@ -220,7 +249,43 @@ struct Cursor {
     }
     return true;
   }
+  // matvec listed: first kept tile of the current item at or after x
+  // (cb_end if none); pruned blocks are jumped over whole
+  int ncb;  // next kept tile of the item after cb (cb_end: cb is its last)
+  __device__ int find_kept(const TcArgs& a, int x) const {
+    const uint8_t* row = a.pskip + ((int64_t)rb * MB * 128 / a.pB) * a.pnb;
+    while (x < cb_end) {
+      const int64_t T = (int64_t)x * 128 / a.pB;
+      if (row[T] == 0) return x;
+      x = (int)((T + 1) * a.pB / 128);
+    }
+    return cb_end;
+  }
+  __device__ void load_item(const TcArgs& a) {
+    uid = a.unit_list[u];
+    rb = (int)(uid / a.n_chunks);
+    chunk = (int)(uid - (int64_t)rb * a.n_chunks);
+    cb_end = (int)min((int64_t)(chunk + 1) * kChunkTiles, a.n_ctiles);
+    const int first = max(chunk * kChunkTiles, rb * MB);
+    cb = find_kept(a, first);
+    ncb = find_kept(a, cb + 1);
+  }
   __device__ void begin(const TcArgs& a, int64_t u0, int64_t u1) {
+    listed = run_listed<MODE>(a);
+    if (listed) {
+      strided = false;
+      u = u0;
+      u_end = u1;
+      if (u < u_end) {
+        if constexpr (MODE == kModeMatvec) {
+          load_item(a);
+        } else {
+          uid = a.unit_list[u];
+          decode_id(a, uid);
+        }
+      }
+      return;
+    }
     strided = MODE == kModeMatvec || a.strided;
     if (strided) {
       wave = 0;
@@ -233,10 +298,22 @@ struct Cursor {
     if (u < u_end) decode_unit(a);
   }
   __device__ bool valid() const { return u < u_end; }
-  __device__ bool item_last() const { return MODE != kModeMatvec || cb + 1 == cb_end; }
+  __device__ bool item_last() const {
+    if (MODE != kModeMatvec) return true;
+    return listed ? ncb >= cb_end : cb + 1 == cb_end;
+  }
   // units are walked in order, so the successor is found without the
   // division / search of decode_unit (which runs once, in begin())
   __device__ void next(const TcArgs& a) {
+    if (MODE == kModeMatvec && listed) {
+      if (ncb < cb_end) {
+        cb = ncb;
+        ncb = find_kept(a, cb + 1);
+      } else if (++u < u_end) {
+        load_item(a);
+      }
+      return;
+    }
     if (MODE == kModeMatvec) {
       if (cb + 1 < cb_end) {
         ++cb;
@@ -247,6 +324,17 @@ struct Cursor {
         ++wave;
         if (!start_row(a)) u = 1;
       }
+      return;
+    }
+    if (listed) {  // packed units
+      if (++u >= u_end) return;
+      const int64_t id = a.unit_list[u];
+      if (id == uid + 1 && cb + 1 < a.n_ctiles) {
+        ++cb;
+      } else {
+        decode_id(a, id);
+      }
+      uid = id;
       return;
     }
     if (strided) {
@@ -302,9 +390,18 @@ __global__ void __launch_bounds__(kCtaThreads<MODE>, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int64_t total = total_units<MB, MODE>(args) - args.u_lo;
-  const int64_t u_begin = args.u_lo + total * blockIdx.x / gridDim.x;
-  const int64_t u_end = args.u_lo + total * (blockIdx.x + 1) / gridDim.x;
+  // listed (pruned) runs split the list of kept units, else the unit range
+  const bool listed = run_listed<MODE>(args);
+  const int64_t total = listed ? *args.unit_count : total_units<MB, MODE>(args) - args.u_lo;
+  const int64_t u0 = listed ? 0 : args.u_lo;
+  int64_t u_begin = u0 + total * blockIdx.x / gridDim.x;
+  int64_t u_end = u0 + total * (blockIdx.x + 1) / gridDim.x;
+  if (listed && args.wpre != nullptr) {  // equal shares of kept tiles, not of items
+    const int64_t W = args.wpre[total];
+    u_begin = lower_bound_w(args.wpre, 0, total, W * blockIdx.x / gridDim.x);
+    u_end = blockIdx.x + 1 == gridDim.x ? total
+                                        : lower_bound_w(args.wpre, 0, total, W * (blockIdx.x + 1) / gridDim.x);
+  }
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < ST; ++s) {
@@ -989,8 +1086,11 @@ int launch_kb(const CUtensorMap& mh, const CUtensorMap& ml, const CUtensorMap& m
   if (const char* o = getenv("GPIC_TC_ORDER")) a.strided = atoi(o) != 0;  // tests: force an order
   a.store_hint = 1;
   if (const char* o = getenv("GPIC_TC_STORE_HINT")) a.store_hint = atoi(o) != 0;  // measurement
-  const int64_t total = (MODE == kModeMatvec || a.strided) ? a.n_rtiles - a.rb_base
-                                                            : total_units<MB, MODE>(a) - a.u_lo;
+  if (run_listed<MODE>(a)) a.strided = 0;  // the list's order
+  const int64_t total = run_listed<MODE>(a) ? g_num_sms
+                        : (MODE == kModeMatvec || a.strided) ? a.n_rtiles - a.rb_base
+                                                              : total_units<MB, MODE>(a) - a.u_lo;
+  // listed: the kept-unit count is on the device; every SM gets a share
   const int grid = (int)(total < g_num_sms ? total : g_num_sms);
   if (grid < 1) return GPIC_OK;
   // the similarity kind is a template parameter: a runtime select would
@@ -1055,7 +1155,8 @@ int packed_row_halves(int32_t /*dp*/) { return 1; }  // the epilogue combines a 
 int launch_affinity_tc_packed(const float* xhi, const float* xlo, const float* sqn, int64_t n,
                               int32_t dp, float neg_scale_log2, void* a_packed, float* degrow,
                               float* degcol, cudaStream_t s, int kind, bool half_out,
-                              int64_t row_lo, int64_t row_hi, uint8_t* boxnz) {
+                              int64_t row_lo, int64_t row_hi, uint8_t* boxnz,
+                              const int32_t* unit_list, const int64_t* unit_count) {
   if (row_hi <= 0) row_hi = n;
   const int64_t nt = ceil_div(n, kBN);
   const int64_t t_lo = tile_index(row_lo / 128, row_lo / 128, nt);
@@ -1084,6 +1185,8 @@ int launch_affinity_tc_packed(const float* xhi, const float* xlo, const float* s
   args.degcol = degcol;
   args.kind = kind;
   args.boxnz = boxnz;
+  args.unit_list = unit_list;
+  args.unit_count = unit_count;
   if (half_out) return dispatch_kb<kModePacked16>(dp / kKBlk, mp, args, s);
   return dispatch_kb<kModePacked>(dp / kKBlk, mp, args, s);
 }
@@ -1122,6 +1225,8 @@ int64_t mf_parts(int64_t n, int32_t dp) {
 
 int mf_rows_per_block(int32_t dp) { return 128 * mblocks(dp / kKBlk); }
 
+int tc_mblocks(int32_t dp) { return mblocks(dp / kKBlk); }
+
 // sym column-partial records: one per (row block of 128 * MB rows, column
 // tile J >= MB * row block)
 int64_t mf_colpart_floats(int64_t n, int32_t dp) {
@@ -1134,7 +1239,8 @@ int64_t mf_colpart_floats(int64_t n, int32_t dp) {
 int launch_affinity_tc_matvec(const float* xhi, const float* xlo, const float* sqn, int64_t n,
                               int32_t dp, int64_t row_lo, int64_t row_hi, float neg_scale_log2,
                               const float* v32, double* ypart, int64_t rows_pad,
-                              const gpic_ctl* ctl, cudaStream_t s, int kind, float* colpart) {
+                              const gpic_ctl* ctl, cudaStream_t s, int kind, float* colpart,
+                              const PruneMask* pm) {
   Maps mp;
   int rc = operand_maps(xhi, n, dp, &mp);
   if (rc) return rc;
@@ -1154,6 +1260,14 @@ int launch_affinity_tc_matvec(const float* xhi, const float* xlo, const float* s
   args.kind = kind;
   args.sym = colpart != nullptr && row_lo == 0 && row_hi == n;
   args.colpart = colpart;
+  if (pm != nullptr && args.sym) {  // pruned sym pass: the kept items only
+    args.unit_list = pm->items;
+    args.unit_count = pm->item_count;
+    args.pskip = pm->skip;
+    args.pB = pm->B;
+    args.pnb = pm->nb;
+    args.wpre = pm->item_wpre;
+  }
   return dispatch_kb<kModeMatvec>(dp / kKBlk, mp, args, s);
 }
 

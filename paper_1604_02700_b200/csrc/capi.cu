@@ -65,6 +65,7 @@ int64_t workspace_bytes(int64_t n, int32_t d, int32_t k, int64_t rows, int32_t /
   b += al(kmeans_scratch_bytes(n, k));        // kmeans
   b += al(n * 8) + al(8);                     // low-degree row list + count
   b += al(sparse_mask_bytes(n, d));           // block-sparsity mask (sparse.cu)
+  b += al(prune_bytes(n, dp));                // provably-zero block pairs (prune.cu)
   return b;
 }
 
@@ -97,6 +98,7 @@ int carve(void* base, int64_t bytes, int64_t n, int32_t d, int32_t k, int64_t ro
   ws->lowlist = reinterpret_cast<int64_t*>(take(n * 8));
   ws->lowcount = reinterpret_cast<unsigned long long*>(take(8));
   ws->sparse = take(sparse_mask_bytes(n, d));
+  ws->prune = take(prune_bytes(n, dp));
   ws->end = p;
   return GPIC_OK;
 }
@@ -421,6 +423,64 @@ int gpic_mf_degrees(const float* d_xhi, const float* d_xlo, const float* d_sqn, 
                            static_cast<cudaStream_t>(stream));
 }
 
+// One matrix-free A v pass (y = A v, no 1/deg) over the operands, pruning
+// mask and partial buffers a gpic_cluster(storage = NONE) run left in its
+// workspace: the loop's own pass, for kernel-level timing.
+int gpic_cluster_mf_pass(void* d_work, int64_t n, int32_t d, int32_t k, int32_t max_iter,
+                         double sigma, int32_t kind, int32_t pruned, const float* d_v32,
+                         double* d_y, void* stream) {
+  if (n < 1 || d < 1) return fail(GPIC_E_INVALID, "bad shape");
+  Workspace ws;
+  const int64_t scratch = workspace_bytes(n, d, k, n, max_iter);
+  int rc = carve(d_work, scratch, n, d, k, n, max_iter, &ws);
+  if (rc) return rc;
+  const int32_t dp = feature_pitch(d);
+  MfOperands op{ws.xhi, ws.xlo, ws.sqn, n, dp,
+                (float)(-1.4426950408889634 / (2.0 * sigma * sigma)), kind};
+  op.sym = mf_sym_default();
+  op.d = d;
+  if (pruned) {
+    op.prune = carve_prune(ws.prune, n, dp);
+    op.pruned = 1;
+  }
+  PeerTable pt;
+  std::memset(&pt, 0, sizeof pt);
+  pt.y[0][0] = pt.y[0][1] = d_y;
+  pt.nranks = 1;
+  double* ypart = reinterpret_cast<double*>(static_cast<uint8_t*>(d_work) + scratch);
+  return launch_mf_matvec(op, 0, n, d_v32, ypart, nullptr, pt, nullptr,
+                          static_cast<cudaStream_t>(stream));
+}
+
+// Work the tensor engine did in a gpic_cluster run after tile pruning:
+// packed storages -> kept / all work units (128 MB x 128 tiles); matrix-free
+// -> kept / all tile units of one sym pass. Synchronizes `stream`.
+int gpic_cluster_pruned_work(const void* d_work, int64_t n, int32_t d, int32_t k,
+                             int32_t max_iter, int32_t storage, int64_t* kept, int64_t* total,
+                             void* stream) {
+  if (n < 1 || d < 1 || !kept || !total) return fail(GPIC_E_INVALID, "bad query");
+  Workspace ws;
+  const int64_t scratch = workspace_bytes(n, d, k, n, max_iter);
+  int rc = carve(const_cast<void*>(d_work), scratch, n, d, k, n, max_iter, &ws);
+  if (rc) return rc;
+  const int32_t dp = feature_pitch(d);
+  const PruneMask pm = carve_prune(ws.prune, n, dp);
+  const int64_t mb = tc_mblocks(dp);
+  const int64_t nrt = ceil_div(n, 128 * mb), nct = ceil_div(n, 128);
+  *total = nrt * nct - mb * nrt * (nrt - 1) / 2;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (storage == GPIC_STORAGE_NONE) {
+    int64_t cnt = 0;
+    GPIC_CUDA_TRY(cudaMemcpyAsync(&cnt, pm.item_count, 8, cudaMemcpyDeviceToHost, s));
+    GPIC_CUDA_TRY(cudaStreamSynchronize(s));
+    GPIC_CUDA_TRY(cudaMemcpyAsync(kept, pm.item_wpre + cnt, 8, cudaMemcpyDeviceToHost, s));
+  } else {
+    GPIC_CUDA_TRY(cudaMemcpyAsync(kept, pm.count, 8, cudaMemcpyDeviceToHost, s));
+  }
+  GPIC_CUDA_TRY(cudaStreamSynchronize(s));
+  return GPIC_OK;
+}
+
 int gpic_matvec(const float* d_a, int64_t lda, int64_t rows, int64_t n, const float* d_v,
                 const double* d_row_scale, double* d_y, void* stream) {
   if (lda % 4 || lda < n) return fail(GPIC_E_INVALID, "lda must be >= n and a multiple of 4");
@@ -558,6 +618,11 @@ int gpic_cluster_workspace_layout(int64_t n, int32_t d, int32_t k, int32_t max_i
   offsets[3] = reinterpret_cast<uint8_t*>(sm.boxnz) - base;
   offsets[4] = reinterpret_cast<uint8_t*>(sm.sb_prefix) - base;
   offsets[5] = reinterpret_cast<uint8_t*>(ws.deg) - base;
+  const PruneMask pm = carve_prune(ws.prune, n, feature_pitch(d));
+  offsets[6] = reinterpret_cast<uint8_t*>(pm.count) - base;
+  const int64_t mb = tc_mblocks(feature_pitch(d));
+  const int64_t nrt = ceil_div(n, 128 * mb), nct = ceil_div(n, 128);
+  offsets[7] = nrt * nct - mb * nrt * (nrt - 1) / 2;
   return GPIC_OK;
 }
 
@@ -648,17 +713,27 @@ int cluster_impl(const double* d_x, int64_t n, int32_t d, double sigma, int32_t 
     // reads only those (sparse.cu; bit-identical to the dense run)
     const SparseMask sm = carve_sparse(ws.sparse, n, d);
     const bool sparse = sparse_enabled() && impl == GPIC_AFFINITY_TC;
+    // tile pruning (RBF): block pairs proved to hold only flushed entries are
+    // not computed at all (prune.cu); their box flags stay 0
+    const bool prune = sparse && kind == GPIC_KIND_RBF && prune_enabled();
+    const PruneMask pm = carve_prune(ws.prune, n, dp);
+    if (prune) {
+      GPIC_CUDA_TRY(cudaMemsetAsync(sm.boxnz, 0, packed_tiles(n) * 16, s));
+      launch_prune(pm, ws.xlo, ws.colpart, ws.mean, n, d, dp, sigma, tc_mblocks(dp), 0, s);
+    }
     if (impl == GPIC_AFFINITY_SIMT) {
       launch_affinity_simt_packed(ws.xlo, ws.sqn, n, d, dp, neg_scale_log2, a, degrow, degcol, s,
                                   kind);
     } else {
       rc = launch_affinity_tc_packed(ws.xhi, ws.xlo, ws.sqn, n, dp, neg_scale_log2, a, degrow,
-                                     degcol, s, kind, half, 0, 0, sparse ? sm.boxnz : nullptr);
+                                     degcol, s, kind, half, 0, 0, sparse ? sm.boxnz : nullptr,
+                                     prune ? pm.units : nullptr, prune ? pm.count : nullptr);
       if (rc) return rc;
     }
     if (sparse) launch_sparse_prefix(sm, s);
     mark(ev, 1, s);
-    launch_sym_degree(degrow, degcol, n, packed_row_halves(dp), deg, nullptr, s);
+    launch_sym_degree(degrow, degcol, n, packed_row_halves(dp), deg, nullptr, s, ShardRange(),
+                      sparse ? sm.boxnz : nullptr, prune ? &pm : nullptr);
     L.mode = half ? kLoopPacked16 : kLoopPacked;
     L.rowp = rowp;
     L.colp = colp;
@@ -671,6 +746,13 @@ int cluster_impl(const double* d_x, int64_t n, int32_t d, double sigma, int32_t 
     L.mf = MfOperands{ws.xhi, ws.xlo, ws.sqn, n, dp, neg_scale_log2, kind};
     L.mf.d = d;
     L.mf.sym = mf_sym_default();
+    // tile pruning of the sym tensor pass (RBF, d > 8): the kept items only
+    if (L.mf.sym && kind == GPIC_KIND_RBF && d > 8 && impl == GPIC_AFFINITY_TC &&
+        sparse_enabled() && prune_enabled()) {
+      L.mf.prune = carve_prune(ws.prune, n, dp);
+      launch_prune(L.mf.prune, ws.xlo, ws.colpart, ws.mean, n, d, dp, sigma, -tc_mblocks(dp), 0, s);
+      L.mf.pruned = 1;
+    }
     L.ypart = ypart;
     mark(ev, 1, s);  // matrix-free: the degree pass is the first A recompute
     rc = launch_mf_degrees(L.mf, 0, n, ws.v32, ypart, deg, s);

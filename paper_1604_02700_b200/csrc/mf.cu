@@ -119,7 +119,9 @@ constexpr int kSeg = 8;
 __global__ void __launch_bounds__(128 * kSeg)
     mf_sym_reduce_kernel(const double* __restrict__ ypart, const float* __restrict__ colpart,
                          int64_t nparts, int64_t rows_pad, int64_t n, int64_t nct, int mb,
-                         const double* __restrict__ deg, const PeerTable pt, gpic_ctl* ctl) {
+                         const double* __restrict__ deg, const PeerTable pt, gpic_ctl* ctl,
+                         const uint8_t* __restrict__ item_kept, const uint8_t* __restrict__ pskip,
+                         int64_t pB, int64_t pnb) {
   if (ctl != nullptr && *(volatile const int32_t*)&ctl->stop) return;
   __shared__ double part[kSeg][128];
   const int64_t J = blockIdx.x;
@@ -129,12 +131,17 @@ __global__ void __launch_bounds__(128 * kSeg)
   const int64_t c0 = rb * mb / 32;  // first chunk written for this row block (kChunkTiles = 32)
   const int64_t p0 = c0 + (nparts - c0) * sg / kSeg, p1 = c0 + (nparts - c0) * (sg + 1) / kSeg;
   double s = 0.0;
+  // pruned pass: chunk partials of kept items and records of kept tiles
+  // only (the others are exact zeros and never written)
   if (i < n)
-    for (int64_t p = p0; p < p1; ++p) s += ypart[p * rows_pad + i];
+    for (int64_t p = p0; p < p1; ++p)
+      if (item_kept == nullptr || item_kept[rb * nparts + p] != 0) s += ypart[p * rows_pad + i];
   const int64_t nrec = rb + 1;  // row blocks 0 .. rb hold tiles (I', J) with I' <= J
   const int64_t r0 = nrec * sg / kSeg, r1 = nrec * (sg + 1) / kSeg;
+  const int64_t TJ = pskip != nullptr ? J * 128 / pB : 0;
 #pragma unroll 4
   for (int64_t r = r0; r < r1; ++r) {
+    if (pskip != nullptr && pskip[(r * mb * 128 / pB) * pnb + TJ]) continue;
     const int64_t rec = r * nct - (int64_t)mb * r * (r - 1) / 2 + (J - r * mb);
     s += (double)colpart[rec * 128 + o];
   }
@@ -208,13 +215,15 @@ int launch_mf_matvec(const MfOperands& op, int64_t row_lo, int64_t rows, const f
   }
   if (mf_sym(op, row_lo, rows)) {
     float* colpart = reinterpret_cast<float*>(ypart + mf_parts(op.n, op.dp) * rows_pad);
+    const PruneMask* pm = op.pruned ? &op.prune : nullptr;
     int rc = launch_affinity_tc_matvec(op.xhi, op.xlo, op.sqn, op.n, op.dp, 0, op.n, op.ns, v32,
-                                       ypart, rows_pad, ctl, s, op.kind, colpart);
+                                       ypart, rows_pad, ctl, s, op.kind, colpart, pm);
     if (rc) return rc;
     const int64_t nct = ceil_div(op.n, kTileN);
     mf_sym_reduce_kernel<<<(unsigned)nct, 128 * kSeg, 0, s>>>(
         ypart, colpart, mf_parts(op.n, op.dp), rows_pad, op.n, nct,
-        mf_rows_per_block(op.dp) / 128, deg, pt, ctl);
+        mf_rows_per_block(op.dp) / 128, deg, pt, ctl, pm ? pm->item_kept : nullptr,
+        pm ? pm->skip : nullptr, pm ? pm->B : 1, pm ? pm->nb : 0);
     count_launch();
     GPIC_CUDA_TRY(cudaGetLastError());
     return GPIC_OK;

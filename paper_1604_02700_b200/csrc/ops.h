@@ -55,10 +55,17 @@ int launch_affinity_tc_packed(const float* xhi, const float* xlo, const float* s
                               int32_t dp, float neg_scale_log2, void* a_packed, float* degrow,
                               float* degcol, cudaStream_t s, int kind = GPIC_KIND_RBF,
                               bool half_out = false, int64_t row_lo = 0, int64_t row_hi = 0,
-                              uint8_t* boxnz = nullptr);
+                              uint8_t* boxnz = nullptr, const int32_t* unit_list = nullptr,
+                              const int64_t* unit_count = nullptr);
+// M blocks (128-row tiles) per tcgen05 work unit at feature pitch dp
+int tc_mblocks(int32_t dp);
+// boxnz non-null: tiles without a stored box contribute zero (not read);
+// pm non-null: pruned block pairs are not even looked at (prune.cu)
+struct PruneMask;
 void launch_sym_degree(const float* degrow, const float* degcol, int64_t n, int nhalf,
                        double* deg, gpic_ctl* ctl, cudaStream_t s,
-                       const ShardRange& sr = ShardRange());
+                       const ShardRange& sr = ShardRange(), const uint8_t* boxnz = nullptr,
+                       const PruneMask* pm = nullptr);
 void sym_prepare();
 
 // Workspace carve-up (see capi.cu).
@@ -79,6 +86,7 @@ struct Workspace {
   int64_t* lowlist;    // n low-degree row indices (lowdeg.cu)
   unsigned long long* lowcount;
   uint8_t* sparse;     // SparseMask storage (sparse.cu)
+  uint8_t* prune;      // PruneMask storage (prune.cu)
   int64_t kscratch_bytes;
   uint8_t* end;
 };
@@ -158,6 +166,38 @@ void launch_sym_gemv16(const void* tiles, int64_t n, const float* v32, float* ro
                        const double* deg, const PeerTable& pt, gpic_ctl* ctl, cudaStream_t s,
                        const uint8_t* boxnz = nullptr, const int64_t* sb_prefix = nullptr);
 
+// ---- provably-zero block pairs (prune.cu) -------------------------------
+// Row blocks of B rows; skip[S * nb + T] = 1 when every entry between
+// blocks S and T is proved to flush to zero; units = ascending list of the
+// tcgen05 packed work units that are not skipped, *count of them.
+struct PruneMask {
+  int64_t B = 0, nb = 0;
+  float* cent = nullptr;    // nb x dp block centroids
+  float* own = nullptr;     // n: x_i . c_{S(i)}
+  unsigned* mmax = nullptr; // nb x nb order-preserving max images
+  uint8_t* skip = nullptr;  // nb x nb
+  int32_t* units = nullptr;
+  int64_t* count = nullptr;
+  unsigned* scal = nullptr; // |c|max, |x|max (float bits)
+  int32_t* rbcount = nullptr;  // kept units (items) per row block
+  // matrix-free sym pass: kept (row block, chunk) items, id rb * chunks + c
+  int32_t* items = nullptr;
+  int64_t* item_count = nullptr;
+  uint8_t* item_kept = nullptr;  // [row block][chunk] kept tiles of the item (0: pruned)
+  int32_t* rbtiles = nullptr;    // kept tiles per row block
+  int64_t* item_wpre = nullptr;  // kept tiles before list entry u (count + 1 entries)
+};
+bool prune_enabled();  // GPIC_PRUNE=0 computes every tile (comparisons)
+int64_t prune_block_rows(int64_t n);
+int64_t prune_bytes(int64_t n, int32_t dp);
+PruneMask carve_prune(void* base, int64_t n, int32_t dp);
+// xc: the centred fp32 rows (pitch dp); colpart / mean: the prepare pass's
+// 256-row column sums and centring mean; mb: tc_mblocks(dp) for the packed
+// unit list, -tc_mblocks(dp) for the matrix-free item list
+void launch_prune(const PruneMask& m, const float* xc, const double* colpart, const double* mean,
+                  int64_t n, int32_t d, int32_t dp, double sigma, int mb, int64_t row_lo,
+                  cudaStream_t s);
+
 // ---- matrix-free (affinity_tc.cu matvec mode + mf.cu) --------------------
 struct MfOperands {
   const float* xhi;
@@ -169,6 +209,8 @@ struct MfOperands {
   int kind = GPIC_KIND_RBF;
   int sym = 0;  // whole matrix on one rank: upper-triangle pass (mf.cu)
   int32_t d = 0;  // features (RBF with d <= 8: the difference-form SIMT pass)
+  int pruned = 0;  // sym pass over the kept items of `prune` only (prune.cu)
+  PruneMask prune;
 };
 bool mf_sym_default();
 int64_t mf_parts(int64_t n, int32_t dp);
@@ -179,7 +221,7 @@ int launch_affinity_tc_matvec(const float* xhi, const float* xlo, const float* s
                               int32_t dp, int64_t row_lo, int64_t row_hi, float neg_scale_log2,
                               const float* v32, double* ypart, int64_t rows_pad,
                               const gpic_ctl* ctl, cudaStream_t s, int kind = GPIC_KIND_RBF,
-                              float* colpart = nullptr);
+                              float* colpart = nullptr, const PruneMask* pm = nullptr);
 int launch_mf_matvec(const MfOperands& op, int64_t row_lo, int64_t rows, const float* v32,
                      double* ypart, const double* deg, const PeerTable& pt, gpic_ctl* ctl,
                      cudaStream_t s);
@@ -198,6 +240,8 @@ struct SparseMask {
   int64_t n_sb = 0;
 };
 int64_t sparse_mask_bytes(int64_t n, int32_t d);
+// per super-block box bits (16 tiles x 16 boxes), stored behind sb_prefix
+const uint16_t* sb_bits(const int64_t* sb_prefix, int64_t n);
 SparseMask carve_sparse(void* base, int64_t n, int32_t d);
 // the GEMV weights from the box flags the affinity engine wrote
 void launch_sparse_prefix(const SparseMask& m, cudaStream_t s);
@@ -278,6 +322,12 @@ int64_t kmeans_scratch_bytes(int64_t n, int32_t k);
 int launch_generate_blobs(const double* centers, const int64_t* offsets, int64_t n, int d, int k,
                           uint64_t seed, double noise, double offset, double* x, int64_t* labels,
                           cudaStream_t s);
+// 64 < k <= kmeans_big_max_k(): sorted-domain Lloyd (kmeans_big.cu)
+int kmeans_big_max_k();
+int64_t kmeans_big_scratch_bytes(int64_t n, int32_t k);
+int launch_kmeans1d_big(const double* v, int64_t n, int32_t k, int64_t first_index,
+                        const double* h_uniforms, int32_t max_rounds, double tol, int64_t* labels,
+                        void* scratch, gpic_ctl* ctl, cudaStream_t st);
 int launch_kmeans1d(const double* v, int64_t n, int32_t k, int64_t first_index,
                     const double* h_uniforms, int32_t max_rounds, double tol, int64_t* labels,
                     void* scratch, gpic_ctl* ctl, cudaStream_t s);

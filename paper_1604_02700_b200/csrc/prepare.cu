@@ -58,32 +58,74 @@ __global__ void ctl_init_kernel(gpic_ctl* ctl, double eps, int32_t max_iter) {
 
 // Partial column sums over a fixed block of kColRows rows, plus the
 // non-finite scan (first offending element in row-major order wins).
+// blockDim = kGroups x (d rounded up to 32, <= 256): group g sums rows
+// r0 + g, r0 + g + kGroups, ... (8 loads in flight), the groups are added
+// in order through shared memory — a fixed order.
+constexpr int kGroups = 4;
 __global__ void colsum_kernel(const double* __restrict__ x, int64_t n, int32_t d,
                               double* __restrict__ colpart, gpic_ctl* ctl) {
+  __shared__ double part[kGroups][256];
   const int64_t r0 = (int64_t)blockIdx.x * kColRows;
   const int64_t r1 = min(r0 + kColRows, n);
-  for (int f = threadIdx.x; f < d; f += blockDim.x) {
+  const int width = blockDim.x / kGroups;
+  const int g = threadIdx.x / width, t = threadIdx.x % width;
+  for (int f0 = 0; f0 < d; f0 += width) {
+    const int f = f0 + t;
     double s = 0.0;
-    for (int64_t i = r0; i < r1; ++i) {
-      double v = x[i * d + f];
-      if (!isfinite(v)) {
-        raise_status(ctl, GPIC_E_NONFINITE, i * d + f, -1, v);
-        v = 0.0;
+    if (f < d) {
+      int64_t i = r0 + g;
+      for (; i + 7 * kGroups < r1; i += 8 * kGroups) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = x[(i + u * kGroups) * d + f];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          if (!isfinite(v[u])) {
+            raise_status(ctl, GPIC_E_NONFINITE, (i + u * kGroups) * d + f, -1, v[u]);
+            v[u] = 0.0;
+          }
+          s += v[u];
+        }
       }
-      s += v;
+      for (; i < r1; i += kGroups) {
+        double v = x[i * d + f];
+        if (!isfinite(v)) {
+          raise_status(ctl, GPIC_E_NONFINITE, i * d + f, -1, v);
+          v = 0.0;
+        }
+        s += v;
+      }
     }
-    colpart[(int64_t)blockIdx.x * d + f] = s;
+    part[g][t] = s;
+    __syncthreads();
+    if (g == 0 && f < d) {
+      double tot = part[0][t];
+#pragma unroll
+      for (int q = 1; q < kGroups; ++q) tot += part[q][t];
+      colpart[(int64_t)blockIdx.x * d + f] = tot;
+    }
+    __syncthreads();
   }
 }
 
+// mean[f] = sum of the block partials / n: 8 segments per feature (a warp
+// of 32 threads covers 4 features), segment sums added in order
 __global__ void mean_kernel(const double* __restrict__ colpart, int64_t nblk, int64_t n, int32_t d,
                             double* __restrict__ mean) {
-  for (int f = threadIdx.x; f < d; f += blockDim.x) {
-    double s = 0.0;
-    for (int64_t b = 0; b < nblk; ++b) s += colpart[b * d + f];
-    mean[f] = s / (double)n;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int f = (blockIdx.x * (blockDim.x >> 5) + w) * 4 + (lane >> 3);
+  const int sg = lane & 7;
+  double s = 0.0;
+  if (f < d) {
+    const int64_t b0 = nblk * sg / 8, b1 = nblk * (sg + 1) / 8;
+    for (int64_t b = b0; b < b1; ++b) s += colpart[b * d + f];
   }
-  if (threadIdx.x == 0) {
+  // segments 0..7 of a feature sit in consecutive lanes: add them in order
+  double tot = 0.0;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) tot += __shfl_sync(0xffffffffu, s, (lane & ~7) + q);
+  if (sg == 0 && f < d) mean[f] = tot / (double)n;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
     mean[d] = 0.0;      // max |x - mean| (maxabs_kernel)
     mean[d + 1] = 0.0;  // max_i |x_i - mean|^2 (center_split_kernel): the spread R^2
   }
@@ -115,58 +157,72 @@ __device__ __forceinline__ double operand_scale(double maxabs) {
   return ldexp(1.0, sh < -60 ? -60 : (sh > 60 ? 60 : sh));
 }
 
-__device__ __forceinline__ void split16(double xs, __half* hi, __half* lo, int64_t at) {
+// returns (double)(hi + lo), the split operand's value
+__device__ __forceinline__ double split16(double xs, __half* hi, __half* lo, int64_t at) {
   const float x32 = (float)xs;
   const __half h = __float2half_rn(x32);
+  const __half l = __float2half_rn(x32 - __half2float(h));
   hi[at] = h;
-  lo[at] = __float2half_rn(x32 - __half2float(h));
+  lo[at] = l;
+  return (double)__half2float(h) + (double)__half2float(l);
 }
 
-// One warp per (padded) row: centre in fp64, fp32 row for the FFMA engine,
-// scaled fp16 hi/lo planes for the tensor engine, fp64-accumulated squared
-// norm of the fp32 row, and the row's entries of the norm block.
-__global__ void center_split_kernel(const double* __restrict__ x, int64_t n, int32_t d, int32_t dp,
-                                    int64_t n_pad, double* __restrict__ mean,
-                                    __half* __restrict__ hi, float* __restrict__ xc_out,
-                                    float* __restrict__ sqn) {
-  const int lane = threadIdx.x & 31;
-  const int64_t row = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
-  if (row >= n_pad) return;
+// Warps stride over the (padded) rows: centre in fp64, fp32 row for the
+// FFMA engine, scaled fp16 hi/lo planes for the tensor engine,
+// fp64-accumulated squared norm of the fp32 row, and the row's entries of
+// the norm block. The spread max_i |x_i - mean|^2 is reduced per CTA and
+// published with one atomic per CTA (a per-row atomic on one address
+// serialised the kernel).
+__global__ void __launch_bounds__(256)
+    center_split_kernel(const double* __restrict__ x, int64_t n, int32_t d, int32_t dp,
+                        int64_t n_pad, double* __restrict__ mean, __half* __restrict__ hi,
+                        float* __restrict__ xc_out, float* __restrict__ sqn) {
+  __shared__ double wmax[8];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   __half* lo = hi + n_pad * dp;
   const double s = operand_scale(mean[d]);
-  double sq = 0.0, sqs = 0.0;
-  for (int f = lane; f < dp; f += 32) {
-    double c = 0.0;
-    if (row < n && f < d) {
-      double v = x[row * d + f];
-      if (!isfinite(v)) v = mean[f];
-      c = v - mean[f];
-    }
-    const float xc = (float)c;
-    xc_out[row * dp + f] = xc;
-    split16(c * s, hi, lo, row * dp + f);
-    sq += (double)xc * (double)xc;
-    const double t = (double)__half2float(hi[row * dp + f]) + (double)__half2float(lo[row * dp + f]);
-    sqs += t * t;  // |x~ s|^2 of the split operands
-  }
-  sq = warp_sum_f64(sq);
-  sqs = warp_sum_f64(sqs);
-  if (lane == 0) sqn[row] = row == n_pad - 1 ? (float)(1.0 / (s * s)) : (float)sq;
-  if (lane == 0 && row < n)  // spread R^2 for the engine routing (gpic_engine_for)
-    atomicMax(reinterpret_cast<unsigned long long*>(mean + d + 1),
-              (unsigned long long)__double_as_longlong(sq));
-  // norm block: lanes 0-15 write k = lane of the row / column operands
-  __half* nb = lo + n_pad * dp + row * 16 + lane;
   const int64_t plane = n_pad * 16;
-  if (lane < 16) {
-    const double m = row < n ? -0.5 * sqs / 1024.0 : 0.0;
-    const __half mh = __float2half_rn((float)m);
-    const __half ml = __float2half_rn((float)(m - (double)__half2float(mh)));
-    const __half one = __float2half_rn(1024.f), zero = __float2half_rn(0.f);
-    nb[0] = lane == 0 ? one : (lane == 1 ? mh : zero);          // row operand hi
-    nb[plane] = lane == 1 ? ml : zero;                           // row operand lo
-    nb[2 * plane] = lane == 0 ? mh : (lane == 1 ? one : zero);   // column operand hi
-    nb[3 * plane] = lane == 0 ? ml : zero;                       // column operand lo
+  double spread = 0.0;
+  for (int64_t row = (int64_t)blockIdx.x * 8 + warp; row < n_pad; row += (int64_t)gridDim.x * 8) {
+    double sq = 0.0, sqs = 0.0;
+    for (int f = lane; f < dp; f += 32) {
+      double c = 0.0;
+      if (row < n && f < d) {
+        double v = x[row * d + f];
+        if (!isfinite(v)) v = mean[f];
+        c = v - mean[f];
+      }
+      const float xc = (float)c;
+      xc_out[row * dp + f] = xc;
+      const double t = split16(c * s, hi, lo, row * dp + f);
+      sq += (double)xc * (double)xc;
+      sqs += t * t;  // |x~ s|^2 of the split operands
+    }
+    sq = warp_sum_f64(sq);
+    sqs = warp_sum_f64(sqs);
+    if (lane == 0) sqn[row] = row == n_pad - 1 ? (float)(1.0 / (s * s)) : (float)sq;
+    if (row < n) spread = fmax(spread, sq);  // spread R^2 for the engine routing
+    // norm block: lanes 0-15 write k = lane of the row / column operands
+    __half* nb = lo + n_pad * dp + row * 16 + lane;
+    if (lane < 16) {
+      const double m = row < n ? -0.5 * sqs / 1024.0 : 0.0;
+      const __half mh = __float2half_rn((float)m);
+      const __half ml = __float2half_rn((float)(m - (double)__half2float(mh)));
+      const __half one = __float2half_rn(1024.f), zero = __float2half_rn(0.f);
+      nb[0] = lane == 0 ? one : (lane == 1 ? mh : zero);          // row operand hi
+      nb[plane] = lane == 1 ? ml : zero;                           // row operand lo
+      nb[2 * plane] = lane == 0 ? mh : (lane == 1 ? one : zero);   // column operand hi
+      nb[3 * plane] = lane == 0 ? ml : zero;                       // column operand lo
+    }
+  }
+  if (lane == 0) wmax[warp] = spread;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double m = wmax[0];
+    for (int w = 1; w < 8; ++w) m = fmax(m, wmax[w]);
+    if (m > 0.0)  // non-negative doubles order like their bit patterns
+      atomicMax(reinterpret_cast<unsigned long long*>(mean + d + 1),
+                (unsigned long long)__double_as_longlong(m));
   }
 }
 
@@ -224,18 +280,19 @@ void launch_prepare(const double* x, int64_t n, int32_t d, float* xhi, float* xl
   const int32_t dp = feature_pitch(d);
   const int64_t n_pad = row_pad(n);
   __half* planes = reinterpret_cast<__half*>(xhi);
-  colsum_kernel<<<(unsigned)nblk, threads, 0, s>>>(x, n, d, colpart, ctl);  // + finiteness scan
+  colsum_kernel<<<(unsigned)nblk, kGroups * threads, 0, s>>>(x, n, d, colpart, ctl);  // + finiteness scan
   if (kind == GPIC_KIND_COSINE) {
     normalize_split_kernel<<<(unsigned)ceil_div(n_pad, 8), 256, 0, s>>>(x, n, d, dp, n_pad, planes,
                                                                         xlo, sqn, ctl);
     count_launch(2);
     return;
   }
-  mean_kernel<<<1, threads, 0, s>>>(colpart, nblk, n, d, mean);
+  mean_kernel<<<(unsigned)ceil_div(d, 32), 256, 0, s>>>(colpart, nblk, n, d, mean);
   const int64_t mblk = ceil_div(n * d, 256);
   maxabs_kernel<<<(unsigned)(mblk < 1184 ? mblk : 1184), 256, 0, s>>>(x, n, d, mean);
-  center_split_kernel<<<(unsigned)ceil_div(n_pad, 8), 256, 0, s>>>(x, n, d, dp, n_pad, mean, planes,
-                                                                  xlo, sqn);
+  const int64_t cblk = ceil_div(n_pad, 8);
+  center_split_kernel<<<(unsigned)(cblk < 148 * 8 ? cblk : 148 * 8), 256, 0, s>>>(
+      x, n, d, dp, n_pad, mean, planes, xlo, sqn);
   count_launch(4);
 }
 

@@ -37,54 +37,69 @@ __device__ __forceinline__ bool tile_stored(const uint8_t* boxnz, int64_t t) {
   return (f.x | f.y | f.z | f.w) != 0u;
 }
 
-// prefix[s + 1] = prefix[s] + 8 x (stored tiles of super-block s) + 1 over
-// the packed super-block triangle; one CTA, contiguous per-thread segments
-// (super-block coordinates stepped, not searched), then a block scan.
+// weight of super-block s (packed triangle of kSB x kSB tile super-blocks):
+// 8 x its stored tiles + 1, written to prefix[s + 1]; and its box bits:
+// bits[s][(I - kSB P) * kSB + (J - kSB Q)] = the 16 box flags of tile (I, J)
+// (bit quadrant * 4 + chunk), 0 for tiles below the diagonal / past nt —
+// one 32-byte record the GEMV reads per super-block instead of a flag load
+// per tile. One thread each.
+__global__ void sb_weight_kernel(const uint8_t* __restrict__ boxnz, int64_t nt,
+                                 int64_t* __restrict__ prefix, uint16_t* __restrict__ bits) {
+  const int64_t ns = (nt + kSB - 1) / kSB;
+  const int64_t count = ns * (ns + 1) / 2;
+  const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s == 0) prefix[0] = 0;
+  if (s >= count) return;
+  int64_t lo = 0, hi = ns - 1;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi + 1) >> 1;
+    if (mid * ns - mid * (mid - 1) / 2 <= s) lo = mid; else hi = mid - 1;
+  }
+  const int64_t P = lo, Q = P + (s - (P * ns - P * (P - 1) / 2));
+  int64_t w = 1;
+  uint16_t b[kSB * kSB];
+#pragma unroll
+  for (int q = 0; q < kSB * kSB; ++q) b[q] = 0;
+  for (int64_t I = kSB * P; I < min(kSB * P + kSB, nt); ++I)
+    for (int64_t J = max(I, kSB * Q); J < min(kSB * Q + kSB, nt); ++J) {
+      const uint4 f = *reinterpret_cast<const uint4*>(boxnz + (I * nt - I * (I - 1) / 2 + (J - I)) * 16);
+      const uint32_t wd[4] = {f.x, f.y, f.z, f.w};
+      uint16_t m = 0;
+#pragma unroll
+      for (int q = 0; q < 16; ++q) m |= (uint16_t)(((wd[q >> 2] >> (8 * (q & 3))) & 0xffu) != 0u) << q;
+      b[(I - kSB * P) * kSB + (J - kSB * Q)] = m;
+      if (m) w += 8;
+    }
+  prefix[s + 1] = w;
+  uint4* out = reinterpret_cast<uint4*>(bits + s * kSB * kSB);
+  out[0] = make_uint4(b[0] | (uint32_t)b[1] << 16, b[2] | (uint32_t)b[3] << 16,
+                      b[4] | (uint32_t)b[5] << 16, b[6] | (uint32_t)b[7] << 16);
+  out[1] = make_uint4(b[8] | (uint32_t)b[9] << 16, b[10] | (uint32_t)b[11] << 16,
+                      b[12] | (uint32_t)b[13] << 16, b[14] | (uint32_t)b[15] << 16);
+}
+
+// in-place inclusive scan of prefix[1 .. count]: one CTA walks the array in
+// coalesced 1024-element chunks (block scan + running carry)
 __global__ void __launch_bounds__(kScanThreads)
-    sb_weight_scan_kernel(const uint8_t* __restrict__ boxnz, int64_t nt,
-                          int64_t* __restrict__ prefix) {
+    sb_scan_kernel(int64_t nt, int64_t* __restrict__ prefix) {
   __shared__ int64_t sh[kScanThreads];
   const int64_t ns = (nt + kSB - 1) / kSB;
   const int64_t count = ns * (ns + 1) / 2;
   const int t = threadIdx.x;
-  const int64_t seg = (count + kScanThreads - 1) / kScanThreads;
-  const int64_t a = min(count, t * seg), b = min(count, a + seg);
-  auto coords = [&](int64_t s, int64_t& P, int64_t& Q) {
-    int64_t lo = 0, hi = ns - 1;
-    while (lo < hi) {
-      const int64_t mid = (lo + hi + 1) >> 1;
-      if (mid * ns - mid * (mid - 1) / 2 <= s) lo = mid; else hi = mid - 1;
+  int64_t carry = 0;
+  for (int64_t c0 = 0; c0 < count; c0 += kScanThreads) {
+    const int64_t i = c0 + t;
+    sh[t] = i < count ? prefix[i + 1] : 0;
+    __syncthreads();
+    for (int o = 1; o < kScanThreads; o <<= 1) {
+      const int64_t add = t >= o ? sh[t - o] : 0;
+      __syncthreads();
+      sh[t] += add;
+      __syncthreads();
     }
-    P = lo;
-    Q = P + (s - (P * ns - P * (P - 1) / 2));
-  };
-  auto weight = [&](int64_t P, int64_t Q) {
-    int64_t w = 1;
-    for (int64_t I = kSB * P; I < min(kSB * P + kSB, nt); ++I)
-      for (int64_t J = max(I, kSB * Q); J < min(kSB * Q + kSB, nt); ++J)
-        if (tile_stored(boxnz, I * nt - I * (I - 1) / 2 + (J - I))) w += 8;
-    return w;
-  };
-  auto step = [&](int64_t& P, int64_t& Q) {
-    if (++Q == ns) Q = ++P;
-  };
-  int64_t s = 0, P = 0, Q = 0;
-  if (a < b) coords(a, P, Q);
-  for (int64_t i = a; i < b; ++i, step(P, Q)) s += weight(P, Q);
-  sh[t] = s;
-  __syncthreads();
-  for (int o = 1; o < kScanThreads; o <<= 1) {  // Hillis-Steele inclusive scan
-    const int64_t v = t >= o ? sh[t - o] : 0;
+    if (i < count) prefix[i + 1] = carry + sh[t];
+    carry += sh[kScanThreads - 1];
     __syncthreads();
-    sh[t] += v;
-    __syncthreads();
-  }
-  int64_t run = t > 0 ? sh[t - 1] : 0;
-  if (t == 0) prefix[0] = 0;
-  if (a < b) coords(a, P, Q);
-  for (int64_t i = a; i < b; ++i, step(P, Q)) {
-    run += weight(P, Q);
-    prefix[i + 1] = run;
   }
 }
 
@@ -104,7 +119,16 @@ int64_t sparse_mask_bytes(int64_t n, int32_t /*d*/) {
   const int64_t nt = ceil_div(n, kT);
   const int64_t ns = ceil_div(nt, kSB);
   auto al = [](int64_t b) { return (b + 255) & ~int64_t(255); };
-  return al(nt * (nt + 1) / 2 * 16) + al((ns * (ns + 1) / 2 + 1) * 8);
+  return al(nt * (nt + 1) / 2 * 16) + al((ns * (ns + 1) / 2 + 1) * 8) +
+         al(ns * (ns + 1) / 2 * kSB * kSB * 2);
+}
+
+// the per-super-block box bits live right behind the GEMV weights
+const uint16_t* sb_bits(const int64_t* sb_prefix, int64_t n) {
+  if (sb_prefix == nullptr) return nullptr;
+  const int64_t ns = ceil_div(ceil_div(n, kT), kSB);
+  const int64_t b = ((ns * (ns + 1) / 2 + 1) * 8 + 255) & ~int64_t(255);
+  return reinterpret_cast<const uint16_t*>(reinterpret_cast<const uint8_t*>(sb_prefix) + b);
 }
 
 SparseMask carve_sparse(void* base, int64_t n, int32_t /*d*/) {
@@ -122,8 +146,10 @@ SparseMask carve_sparse(void* base, int64_t n, int32_t /*d*/) {
 }
 
 void launch_sparse_prefix(const SparseMask& m, cudaStream_t s) {
-  sb_weight_scan_kernel<<<1, kScanThreads, 0, s>>>(m.boxnz, m.nt, m.sb_prefix);
-  count_launch();
+  sb_weight_kernel<<<(unsigned)ceil_div(m.n_sb, 256), 256, 0, s>>>(
+      m.boxnz, m.nt, m.sb_prefix, const_cast<uint16_t*>(sb_bits(m.sb_prefix, m.nt * kT)));
+  sb_scan_kernel<<<1, kScanThreads, 0, s>>>(m.nt, m.sb_prefix);
+  count_launch(2);
 }
 
 void launch_box_fill(const SparseMask& m, uint8_t v, cudaStream_t s) {

@@ -84,6 +84,20 @@ constexpr int kSB = 4;
 struct Sparse {
   const uint8_t* boxnz;
   const int64_t* sbp;
+  const uint16_t* bits;  // [super-block][16 tiles] box masks (sb_bits), or null
+  // the 16 tile masks of super-block s (two 16-byte loads)
+  __device__ void record(int64_t s, uint32_t (&r)[8]) const {
+    const uint4* p = reinterpret_cast<const uint4*>(bits + s * kSB * kSB);
+    const uint4 a = __ldg(p), b = __ldg(p + 1);
+    r[0] = a.x; r[1] = a.y; r[2] = a.z; r[3] = a.w;
+    r[4] = b.x; r[5] = b.y; r[6] = b.z; r[7] = b.w;
+  }
+  __device__ static uint32_t mask_of(const uint32_t (&r)[8], int idx) {
+    uint32_t w = r[0];
+#pragma unroll
+    for (int q = 1; q < 8; ++q) w = (idx >> 1) == q ? r[q] : w;
+    return (idx & 1) ? (w >> 16) : (w & 0xffffu);
+  }
   __device__ uint4 flags(int64_t I, int64_t J, int64_t nt) const {
     return *reinterpret_cast<const uint4*>(boxnz + tile_index(I, J, nt) * 16);
   }
@@ -209,11 +223,18 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint8_t* src0 = reinterpret_cast<const uint8_t*>(tiles);
     w.P = P0;
     w.Q = Q0;
+    uint32_t rec[8];
     for (int64_t sb = s0; sb < s1; ++sb, w.next_sb()) {
       if (sp.empty_sb(sb)) continue;
       w.open(w.P, w.Q);
+      if (sp.bits != nullptr) sp.record(sb, rec);
       do {
-        if (sp.skip_tile(w.I, w.J, nt)) continue;  // no stored box: never read
+        // no stored box: never read
+        if (sp.bits != nullptr) {
+          if (Sparse::mask_of(rec, (int)((w.I - kSB * w.P) * kSB + (w.J - kSB * w.Q))) == 0u) continue;
+        } else if (sp.skip_tile(w.I, w.J, nt)) {
+          continue;
+        }
         mbar_wait(&empty[s], ph ^ 1);
         mbar_expect_tx(&full[s], kTileBytes);
         bulk_load(st + s * kTileBytes, src0 + (tile_index(w.I, w.J, nt) - sr.tile_base) * kTileBytes, kTileBytes,
@@ -230,9 +251,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int t = threadIdx.x;
   w.P = P0;
   w.Q = Q0;
+  uint32_t rec[8];
   for (int64_t sb = s0; sb < s1; ++sb, w.next_sb()) {
     if (sp.empty_sb(sb)) continue;  // no stored tile: its records are never read
     w.open(w.P, w.Q);
+    if (sp.bits != nullptr) sp.record(sb, rec);
     // per lane: the column products of the super-block's kSB tile columns,
     // accumulated over its tile rows (one cross-warp combine per super-block)
     float4 cpa[kSB];
@@ -245,11 +268,17 @@ __global__ void __launch_bounds__(kThreads, 1)
     float4 vj = __ldg(reinterpret_cast<const float4*>(v32 + w.J * kTS) + lane);
     for (;;) {
       const int64_t I = w.I, J = w.J;
-      const bool zt = sp.skip_tile(I, J, nt);
-      // this lane's box (rows of this warp, columns 4 lane .. +3): stored?
-      bool box_ok = true;
-      if (sp.boxnz != nullptr && !zt)
-        box_ok = sp.boxnz[tile_index(I, J, nt) * 16 + (warp >> 1) * 4 + (lane >> 3)] != 0;
+      bool zt, box_ok = true;
+      if (sp.bits != nullptr) {
+        const uint32_t m = Sparse::mask_of(rec, (int)((I - kSB * w.P) * kSB + (J - kSB * w.Q)));
+        zt = m == 0u;
+        // this lane's box (rows of this warp, columns 4 lane .. +3): stored?
+        box_ok = (m >> ((warp >> 1) * 4 + (lane >> 3))) & 1u;
+      } else {
+        zt = sp.skip_tile(I, J, nt);
+        if (sp.boxnz != nullptr && !zt)
+          box_ok = sp.boxnz[tile_index(I, J, nt) * 16 + (warp >> 1) * 4 + (lane >> 3)] != 0;
+      }
       const bool more = w.next();
       const bool row_end = !more || w.I != I;
       // next tile's v slices, one tile ahead
@@ -433,8 +462,12 @@ __global__ void __launch_bounds__(kTS * kSeg)
 __global__ void __launch_bounds__(kTS * kSeg)
     sym_degree_kernel(const float* __restrict__ degrow, const float* __restrict__ degcol,
                       int64_t n, int64_t nt, int nhalf, double* __restrict__ deg, gpic_ctl* ctl,
-                      ShardRange sr) {
+                      ShardRange sr, Sparse sp, const uint8_t* __restrict__ pskip, int64_t pB,
+                      int64_t pnb) {
+  extern __shared__ int32_t live[];  // sparse: the row's tiles that hold a stored box, ascending
   __shared__ double part[kSeg][kTS];
+  __shared__ int32_t wcount[kSeg * kTS / 32];
+  __shared__ int32_t nlive;
   // shard: tile rows [tr_lo, tr_hi) are stored (from tile_base); row R gets
   // the column partials of its stored tiles (p, R) and, if R is its own,
   // the row partials of (R, p >= R). deg is then the shard's partial.
@@ -464,18 +497,65 @@ __global__ void __launch_bounds__(kTS * kSeg)
       if (nhalf == 2) s += (double)x[1];
     }
   };
-  int64_t p = p0;
-  for (; p + 4 <= p1; p += 4) {
-    float x[4][4];
+  if (sp.boxnz != nullptr) {
+    // sparse: first the ordered list of tiles with a stored box (pruned
+    // block pairs and all-zero tiles are exact zeros: skipping them leaves
+    // every fp64 sum bit-identical), then the same segments over it
+    const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+    if (t == 0) nlive = 0;
+    __syncthreads();
+    for (int64_t c0 = 0; c0 < nt; c0 += kSeg * kTS) {
+      const int64_t p = c0 + t;
+      bool k = p < nt;
+      if (k && pskip != nullptr) k = pskip[(R * kTS / pB) * pnb + p * kTS / pB] == 0;
+      if (k) k = !sp.skip_tile(p < R ? p : R, p < R ? R : p, nt);
+      const unsigned m = __ballot_sync(0xffffffffu, k);
+      if (lane == 0) wcount[w] = __popc(m);
+      __syncthreads();
+      if (k) {
+        int pos = nlive + __popc(m & ((1u << lane) - 1u));
+        for (int q = 0; q < w; ++q) pos += wcount[q];
+        live[pos] = (int32_t)p;
+      }
+      __syncthreads();
+      if (t == 0) {
+        int tot = 0;
+        for (int q = 0; q < kSeg * kTS / 32; ++q) tot += wcount[q];
+        nlive += tot;
+      }
+      __syncthreads();
+    }
+    const int L = nlive;
+    int a = 0;
+    while (a < L && live[a] < p0) ++a;
+    int b = a;
+    while (b < L && live[b] < p1) ++b;
+    for (; a + 4 <= b; a += 4) {
+      float x[4][4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) load4(p + u, x[u]);
+      for (int u = 0; u < 4; ++u) load4(live[a + u], x[u]);
 #pragma unroll
-    for (int u = 0; u < 4; ++u) add4(p + u, x[u]);
-  }
-  for (; p < p1; ++p) {
-    float x[4];
-    load4(p, x);
-    add4(p, x);
+      for (int u = 0; u < 4; ++u) add4(live[a + u], x[u]);
+    }
+    for (; a < b; ++a) {
+      float x[4];
+      load4(live[a], x);
+      add4(live[a], x);
+    }
+  } else {
+    int64_t p = p0;
+    for (; p + 4 <= p1; p += 4) {
+      float x[4][4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) load4(p + u, x[u]);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) add4(p + u, x[u]);
+    }
+    for (; p < p1; ++p) {
+      float x[4];
+      load4(p, x);
+      add4(p, x);
+    }
   }
   part[sg][o] = s;
   __syncthreads();
@@ -494,12 +574,18 @@ int g_sms = 0;
 }  // namespace
 
 void launch_sym_degree(const float* degrow, const float* degcol, int64_t n, int nhalf,
-                       double* deg, gpic_ctl* ctl, cudaStream_t s, const ShardRange& sr) {
+                       double* deg, gpic_ctl* ctl, cudaStream_t s, const ShardRange& sr,
+                       const uint8_t* boxnz, const PruneMask* pm) {
   const int64_t nt = ceil_div(n, kTS);
   const int64_t rows = nt - kSB * sr.p_lo;  // tile rows that can receive partials
   if (rows < 1) return;
-  sym_degree_kernel<<<(unsigned)rows, kTS * kSeg, 0, s>>>(degrow, degcol, n, nt, nhalf, deg, ctl,
-                                                          sr);
+  const Sparse sp{boxnz, nullptr, nullptr};
+  const size_t dyn = boxnz != nullptr ? (size_t)nt * 4 : 0;  // the live-tile list
+  if (dyn > 48 * 1024)
+    cudaFuncSetAttribute(sym_degree_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+  sym_degree_kernel<<<(unsigned)rows, kTS * kSeg, dyn, s>>>(
+      degrow, degcol, n, nt, nhalf, deg, ctl, sr, sp, pm ? pm->skip : nullptr, pm ? pm->B : 1,
+      pm ? pm->nb : 0);
   count_launch();
 }
 
@@ -525,7 +611,10 @@ int64_t sym_partial_floats(int64_t n) {
 void launch_sym_gemv(const float* tiles, int64_t n, const float* v32, float* rowp, float* colp,
                      const double* deg, const PeerTable& pt, gpic_ctl* ctl, cudaStream_t s,
                      const ShardRange& sr, const uint8_t* boxnz, const int64_t* sb_prefix) {
-  const Sparse sp{boxnz, boxnz != nullptr ? sb_prefix : nullptr};
+  // packed shards keep per-tile flags (their super-block records are not built)
+  const bool whole = sr.p_lo == 0 && sr.tile_base == 0 && sr.p_hi >= ceil_div(ceil_div(n, kTS), kSB);
+  const Sparse sp{boxnz, boxnz != nullptr ? sb_prefix : nullptr,
+                  boxnz != nullptr && whole ? sb_bits(sb_prefix, n) : nullptr};
   sym_prepare();
   const int64_t nt = ceil_div(n, kTS);
   const int64_t ns = (nt + kSB - 1) / kSB;
@@ -541,7 +630,8 @@ void launch_sym_gemv(const float* tiles, int64_t n, const float* v32, float* row
 void launch_sym_gemv16(const void* tiles, int64_t n, const float* v32, float* rowp, float* colp,
                        const double* deg, const PeerTable& pt, gpic_ctl* ctl, cudaStream_t s,
                        const uint8_t* boxnz, const int64_t* sb_prefix) {
-  const Sparse sp{boxnz, boxnz != nullptr ? sb_prefix : nullptr};
+  const Sparse sp{boxnz, boxnz != nullptr ? sb_prefix : nullptr,
+                  boxnz != nullptr ? sb_bits(sb_prefix, n) : nullptr};
   sym_prepare();
   const int64_t nt = ceil_div(n, kTS);
   const int64_t ns = (nt + kSB - 1) / kSB;

@@ -45,7 +45,8 @@ from .params import (
     PicTrace,
 )
 
-KMEANS_MAX_K = 64
+KMEANS_MAX_K = 4096      # single problems (k > 64: the sorted-domain variant, kmeans_big.cu)
+BATCH_MAX_K = 64         # the batched Experiment-II engine
 
 
 def _torch():
@@ -739,8 +740,8 @@ def cluster_batch(datasets, kind, params: PicParams, seeds, config: KernelConfig
     for d in datasets:
         if k > d.n:
             raise KTooLarge(k, d.n)
-    if k > KMEANS_MAX_K:
-        raise InvalidSpec(f"the device k-means holds at most {KMEANS_MAX_K} centres")
+    if k > BATCH_MAX_K:
+        raise InvalidSpec(f"the batched k-means holds at most {BATCH_MAX_K} centres")
     if max(d.n for d in datasets) > BATCH_MAX_N:
         raise InvalidSpec(f"batched problems hold at most {BATCH_MAX_N} points; use cluster()")
     B = len(datasets)

@@ -1,9 +1,10 @@
-"""Block sparsity (csrc/sparse.cu) changes no bit of the result.
+"""Block sparsity (csrc/sparse.cu + csrc/prune.cu) changes no bit of the result.
 
-Tiles proved all-zero in fp32 (bounding-sphere bound, exponent margin) are
-skipped by the affinity engine, the degree combine and every GEMV; since an
-exact zero adds nothing to any fp32 / fp64 sum, labels, embedding and delta
-history must equal the dense run's bit for bit (GPIC_SPARSE=0).
+32 x 32 boxes whose values all flush to zero are not stored and not read
+(sparse.cu), and block pairs proved to hold only such values are not even
+computed (prune.cu, projection bound with an exponent margin); since an exact
+zero adds nothing to any fp32 / fp64 sum, labels, embedding and delta history
+must equal the dense run's bit for bit (GPIC_SPARSE=0 turns both off).
 """
 
 import numpy as np
