@@ -85,17 +85,27 @@ struct Sparse {
   const uint8_t* boxnz;
   const int64_t* sbp;
   const uint16_t* bits;  // [super-block][16 tiles] box masks (sb_bits), or null
-  // the 16 tile masks of super-block s (two 16-byte loads)
-  __device__ void record(int64_t s, uint32_t (&r)[8]) const {
+  int prefetch;          // producer: tiles prefetched into L2 ahead of the smem ring
+  int bits_consumer;     // consumers read the super-block records too (else per-tile flags)
+  int evict_first;       // tile loads with the L2 evict-first policy
+  // the 16 tile masks of super-block s (two 16-byte loads), kept in
+  // registers: selected by comparisons, never indexed (an indexed array
+  // went to local memory)
+  struct Rec {
+    uint4 a, b;
+  };
+  __device__ Rec record(int64_t s) const {
     const uint4* p = reinterpret_cast<const uint4*>(bits + s * kSB * kSB);
-    const uint4 a = __ldg(p), b = __ldg(p + 1);
-    r[0] = a.x; r[1] = a.y; r[2] = a.z; r[3] = a.w;
-    r[4] = b.x; r[5] = b.y; r[6] = b.z; r[7] = b.w;
+    return Rec{__ldg(p), __ldg(p + 1)};
   }
-  __device__ static uint32_t mask_of(const uint32_t (&r)[8], int idx) {
-    uint32_t w = r[0];
-#pragma unroll
-    for (int q = 1; q < 8; ++q) w = (idx >> 1) == q ? r[q] : w;
+  __device__ static bool empty(const Rec& r) {
+    return ((r.a.x | r.a.y | r.a.z | r.a.w) | (r.b.x | r.b.y | r.b.z | r.b.w)) == 0u;
+  }
+  __device__ static uint32_t mask_of(const Rec& r, int idx) {
+    const int q = idx >> 1;
+    const uint4 h = q < 4 ? r.a : r.b;
+    const int c = q & 3;
+    const uint32_t w = c < 2 ? (c == 0 ? h.x : h.y) : (c == 2 ? h.z : h.w);
     return (idx & 1) ? (w >> 16) : (w & 0xffffu);
   }
   __device__ uint4 flags(int64_t I, int64_t J, int64_t nt) const {
@@ -162,6 +172,54 @@ struct SbWalk {
   }
 };
 
+// Enumerates the stored tiles (global packed index) of super-blocks
+// [sb, s1) in the walk order; -1 at the end.
+struct TileEnum {
+  SbWalk w;
+  int64_t sb, s1;
+  Sparse::Rec rec;
+  bool open, fresh;
+  __device__ void begin(int64_t P0, int64_t Q0, int64_t s0, int64_t s_end, int64_t nt,
+                        int64_t ns) {
+    w.nt = nt;
+    w.ns = ns;
+    w.P = P0;
+    w.Q = Q0;
+    sb = s0;
+    s1 = s_end;
+    open = false;
+  }
+  __device__ int64_t next(const Sparse& sp) {
+    for (;;) {
+      if (!open) {
+        if (sb >= s1) return -1;
+        if (sp.bits != nullptr) {
+          rec = sp.record(sb);
+          if (Sparse::empty(rec)) { ++sb; w.next_sb(); continue; }
+        } else if (sp.empty_sb(sb)) {
+          ++sb;
+          w.next_sb();
+          continue;
+        }
+        w.open(w.P, w.Q);
+        open = true;
+        fresh = true;
+      }
+      if (!fresh && !w.next()) {
+        open = false;
+        ++sb;
+        w.next_sb();
+        continue;
+      }
+      fresh = false;
+      const bool stored = sp.bits != nullptr
+                              ? Sparse::mask_of(rec, (int)((w.I - kSB * w.P) * kSB + (w.J - kSB * w.Q))) != 0u
+                              : !sp.skip_tile(w.I, w.J, w.nt);
+      if (stored) return tile_index(w.I, w.J, w.nt);
+    }
+  }
+};
+
 // Packed GEMV with super-block aggregation. Per stored tile (I, J) the 8
 // consumer warps (16 rows each) form the row products sum_j T[i][j] v_J[j]
 // (kept per lane across the row's tiles of the super-block) and, off the
@@ -221,26 +279,34 @@ __global__ void __launch_bounds__(kThreads, 1)
     int s = 0;
     uint32_t ph = 0;
     const uint8_t* src0 = reinterpret_cast<const uint8_t*>(tiles);
-    w.P = P0;
-    w.Q = Q0;
-    uint32_t rec[8];
-    for (int64_t sb = s0; sb < s1; ++sb, w.next_sb()) {
-      if (sp.empty_sb(sb)) continue;
-      w.open(w.P, w.Q);
-      if (sp.bits != nullptr) sp.record(sb, rec);
-      do {
-        // no stored box: never read
-        if (sp.bits != nullptr) {
-          if (Sparse::mask_of(rec, (int)((w.I - kSB * w.P) * kSB + (w.J - kSB * w.Q))) == 0u) continue;
-        } else if (sp.skip_tile(w.I, w.J, nt)) {
-          continue;
-        }
-        mbar_wait(&empty[s], ph ^ 1);
-        mbar_expect_tx(&full[s], kTileBytes);
-        bulk_load(st + s * kTileBytes, src0 + (tile_index(w.I, w.J, nt) - sr.tile_base) * kTileBytes, kTileBytes,
-                  &full[s]);
-        if (++s == kStages) { s = 0; ph ^= 1; }
-      } while (w.next());
+    // the stored tiles of the CTA's super-blocks, in the consumers' order;
+    // a second enumerator runs `ahead` tiles in front and prefetches them
+    // into L2 (more bytes in flight than the smem ring holds)
+    const uint64_t stream_pol = policy_evict_first();
+    TileEnum cur, pre;
+    cur.begin(P0, Q0, s0, s1, nt, ns);
+    pre.begin(P0, Q0, s0, s1, nt, ns);
+    const int ahead = sp.prefetch;
+    for (int d = 0; d < ahead; ++d) {
+      const int64_t t = pre.next(sp);
+      if (t < 0) break;
+      bulk_prefetch_l2(src0 + (t - sr.tile_base) * kTileBytes, kTileBytes);
+    }
+    for (;;) {
+      const int64_t t = cur.next(sp);
+      if (t < 0) break;
+      mbar_wait(&empty[s], ph ^ 1);
+      mbar_expect_tx(&full[s], kTileBytes);
+      if (sp.evict_first)  // the tile stream must not push the flags / v out of L2
+        bulk_load(st + s * kTileBytes, src0 + (t - sr.tile_base) * kTileBytes, kTileBytes, &full[s],
+                  stream_pol);
+      else
+        bulk_load(st + s * kTileBytes, src0 + (t - sr.tile_base) * kTileBytes, kTileBytes, &full[s]);
+      if (++s == kStages) { s = 0; ph ^= 1; }
+      if (ahead > 0) {
+        const int64_t ta = pre.next(sp);
+        if (ta >= 0) bulk_prefetch_l2(src0 + (ta - sr.tile_base) * kTileBytes, kTileBytes);
+      }
     }
     return;
   }
@@ -251,11 +317,18 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int t = threadIdx.x;
   w.P = P0;
   w.Q = Q0;
-  uint32_t rec[8];
+  Sparse::Rec rec{};
+  Sparse cs = sp;  // the consumers' view
+  if (!sp.bits_consumer) cs.bits = nullptr;
   for (int64_t sb = s0; sb < s1; ++sb, w.next_sb()) {
-    if (sp.empty_sb(sb)) continue;  // no stored tile: its records are never read
+    // no stored tile: its records are never read
+    if (cs.bits != nullptr) {
+      rec = cs.record(sb);
+      if (Sparse::empty(rec)) continue;
+    } else if (cs.empty_sb(sb)) {
+      continue;
+    }
     w.open(w.P, w.Q);
-    if (sp.bits != nullptr) sp.record(sb, rec);
     // per lane: the column products of the super-block's kSB tile columns,
     // accumulated over its tile rows (one cross-warp combine per super-block)
     float4 cpa[kSB];
@@ -269,15 +342,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (;;) {
       const int64_t I = w.I, J = w.J;
       bool zt, box_ok = true;
-      if (sp.bits != nullptr) {
+      if (cs.bits != nullptr) {
         const uint32_t m = Sparse::mask_of(rec, (int)((I - kSB * w.P) * kSB + (J - kSB * w.Q)));
         zt = m == 0u;
         // this lane's box (rows of this warp, columns 4 lane .. +3): stored?
         box_ok = (m >> ((warp >> 1) * 4 + (lane >> 3))) & 1u;
       } else {
-        zt = sp.skip_tile(I, J, nt);
-        if (sp.boxnz != nullptr && !zt)
-          box_ok = sp.boxnz[tile_index(I, J, nt) * 16 + (warp >> 1) * 4 + (lane >> 3)] != 0;
+        zt = cs.skip_tile(I, J, nt);
+        if (cs.boxnz != nullptr && !zt)
+          box_ok = cs.boxnz[tile_index(I, J, nt) * 16 + (warp >> 1) * 4 + (lane >> 3)] != 0;
       }
       const bool more = w.next();
       const bool row_end = !more || w.I != I;
@@ -571,6 +644,18 @@ __global__ void __launch_bounds__(kTS * kSeg)
 
 int g_sms = 0;
 
+// tiles each GEMV producer prefetches into L2 ahead of its smem ring
+// (GPIC_GEMV_PREFETCH, default 0: measured slower at config 3)
+int gemv_evict_first() {
+  const char* e = getenv("GPIC_GEMV_EVICT");
+  return e != nullptr ? atoi(e) : 1;
+}
+
+int gemv_prefetch() {
+  const char* e = getenv("GPIC_GEMV_PREFETCH");
+  return e != nullptr ? atoi(e) : 0;
+}
+
 }  // namespace
 
 void launch_sym_degree(const float* degrow, const float* degcol, int64_t n, int nhalf,
@@ -579,7 +664,7 @@ void launch_sym_degree(const float* degrow, const float* degcol, int64_t n, int 
   const int64_t nt = ceil_div(n, kTS);
   const int64_t rows = nt - kSB * sr.p_lo;  // tile rows that can receive partials
   if (rows < 1) return;
-  const Sparse sp{boxnz, nullptr, nullptr};
+  const Sparse sp{boxnz, nullptr, nullptr, 0, 0, 0};
   const size_t dyn = boxnz != nullptr ? (size_t)nt * 4 : 0;  // the live-tile list
   if (dyn > 48 * 1024)
     cudaFuncSetAttribute(sym_degree_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
@@ -613,8 +698,12 @@ void launch_sym_gemv(const float* tiles, int64_t n, const float* v32, float* row
                      const ShardRange& sr, const uint8_t* boxnz, const int64_t* sb_prefix) {
   // packed shards keep per-tile flags (their super-block records are not built)
   const bool whole = sr.p_lo == 0 && sr.tile_base == 0 && sr.p_hi >= ceil_div(ceil_div(n, kTS), kSB);
+  // GPIC_SB_BITS: 0 per-tile flags everywhere, 1 super-block records for
+  // producer and consumers, 2 records for the producer only (default)
+  const int bits_mode = getenv("GPIC_SB_BITS") != nullptr ? atoi(getenv("GPIC_SB_BITS")) : 2;
   const Sparse sp{boxnz, boxnz != nullptr ? sb_prefix : nullptr,
-                  boxnz != nullptr && whole ? sb_bits(sb_prefix, n) : nullptr};
+                  boxnz != nullptr && whole && bits_mode != 0 ? sb_bits(sb_prefix, n) : nullptr,
+                  gemv_prefetch(), bits_mode == 1, gemv_evict_first()};
   sym_prepare();
   const int64_t nt = ceil_div(n, kTS);
   const int64_t ns = (nt + kSB - 1) / kSB;
@@ -631,7 +720,8 @@ void launch_sym_gemv16(const void* tiles, int64_t n, const float* v32, float* ro
                        const double* deg, const PeerTable& pt, gpic_ctl* ctl, cudaStream_t s,
                        const uint8_t* boxnz, const int64_t* sb_prefix) {
   const Sparse sp{boxnz, boxnz != nullptr ? sb_prefix : nullptr,
-                  boxnz != nullptr ? sb_bits(sb_prefix, n) : nullptr};
+                  boxnz != nullptr ? sb_bits(sb_prefix, n) : nullptr, gemv_prefetch(), 0,
+                  gemv_evict_first()};
   sym_prepare();
   const int64_t nt = ceil_div(n, kTS);
   const int64_t ns = (nt + kSB - 1) / kSB;

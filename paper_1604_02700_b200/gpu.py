@@ -683,9 +683,11 @@ def _cluster_x(x, kind, params, config, seed, timed, v0=None):
     storage = config.storage_code()
     nbytes = workspace_bytes(n, m, k, T, storage)
     work = torch.empty(nbytes, dtype=torch.uint8, device=dev)
-    labels = torch.empty(n, dtype=torch.int64, device=dev)
-    v = torch.empty(n, dtype=torch.float64, device=dev)
-    hist = torch.zeros(T, dtype=torch.float64, device=dev)
+    # labels, v and the delta history side by side: one device->host copy
+    out = torch.zeros(2 * n + T, dtype=torch.int64, device=dev)
+    labels = out[:n]
+    v = out[n:2 * n].view(torch.float64)
+    hist = out[2 * n:].view(torch.float64)
     first, u = kmeans_draws(n, k, seed)
     iters = C.c_int32(0)
     conv = C.c_int32(0)
@@ -703,8 +705,9 @@ def _cluster_x(x, kind, params, config, seed, timed, v0=None):
     it = int(iters.value)
     phases = dict(zip(("affinity", "rowsum", "normalize", "iterate", "kmeans"),
                       (t / 1e3 for t in ms))) if timed else None
-    return (labels.cpu().numpy(), v.cpu().numpy(),
-            PicTrace(it, hist[:it].cpu().numpy(), bool(conv.value)), phases)
+    host = out.cpu().numpy()
+    return (host[:n], host[n:2 * n].view(np.float64),
+            PicTrace(it, host[2 * n:2 * n + it].view(np.float64).copy(), bool(conv.value)), phases)
 
 
 # ------------------------------------------------- batched small problems
