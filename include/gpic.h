@@ -407,6 +407,24 @@ int gpic_mf_degrees(const float* d_xhi, const float* d_xlo, const float* d_sqn, 
                     int32_t d, int64_t row_lo, int64_t row_hi, double sigma, int32_t kind,
                     float* d_ones, double* d_ypart, double* d_deg, void* stream);
 
+/* Matrix-free item shards (GPIC_STORAGE_NONE with row_lo = 0, rows = n in
+ * gpic_shard): every rank holds all of X; the pruned symmetric pass's kept
+ * (row block, column chunk) items (prune.cu) are split across the ranks by
+ * kept-tile count, and each rank's reduce yields a PARTIAL y over all rows
+ * that is exchanged and summed in rank order like the packed shards'
+ * (half the exp / MMA work of row bands, and no pruned pair is computed).
+ * Such a shard is marked lda = 1 (row_lo = 0, rows = n, ypart = d_scratch).
+ * gpic_mf_shard_build builds the pruning mask (d_prep_work: the work buffer
+ * of gpic_prepare_points) and the shard's partial degrees (n doubles);
+ * d_scratch (gpic_mf_shard_scratch_bytes) is the gpic_shard's ypart. RBF
+ * with d > 8 on the tensor engine; GPIC_E_UNSUPPORTED otherwise (row bands
+ * then). */
+int64_t gpic_mf_shard_scratch_bytes(int64_t n, int32_t d);
+int gpic_mf_shard_build(const float* d_xhi, const float* d_xlo, const float* d_sqn,
+                        const double* d_prep_work, int64_t n, int32_t d, double sigma,
+                        int32_t nranks, int32_t rank, double* d_deg_partial, void* d_scratch,
+                        void* stream);
+
 int gpic_comm_create(int32_t nranks, int32_t rank, int64_t n, gpic_comm** out,
                      uint8_t* h_ipc_handle);
 int gpic_comm_open(gpic_comm* comm, const uint8_t* h_all_handles /* nranks x 64 bytes */);

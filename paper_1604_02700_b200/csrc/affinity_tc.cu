@@ -167,7 +167,11 @@ struct TcArgs {
   const uint8_t* pskip;
   int64_t pB, pnb;
   const int64_t* wpre;  // matvec listed: kept tiles before each item (CTA balance)
+  int share_r, share_n;  // matvec listed across ranks: this rank's tile-balanced share
 };
+
+// [ua, ub): the list entries of rank share_r of share_n, tile-balanced
+__device__ inline void item_share(const TcArgs& a, int64_t total, int64_t& ua, int64_t& ub);
 
 // first u in [lo, hi] with a[u] >= target (a non-decreasing)
 __device__ inline int64_t lower_bound_w(const int64_t* a, int64_t lo, int64_t hi, int64_t target) {
@@ -176,6 +180,17 @@ __device__ inline int64_t lower_bound_w(const int64_t* a, int64_t lo, int64_t hi
     if (a[mid] >= target) hi = mid; else lo = mid + 1;
   }
   return lo;
+}
+
+__device__ inline void item_share(const TcArgs& a, int64_t total, int64_t& ua, int64_t& ub) {
+  ua = 0;
+  ub = total;
+  if (a.share_n > 1) {
+    const int64_t W = a.wpre[total];
+    ua = lower_bound_w(a.wpre, 0, total, W * a.share_r / a.share_n);
+    ub = a.share_r + 1 == a.share_n ? total
+                                    : lower_bound_w(a.wpre, 0, total, W * (a.share_r + 1) / a.share_n);
+  }
 }
 
 // the work list of a listed run (packed units or matrix-free items)
@@ -397,10 +412,12 @@ __global__ void __launch_bounds__(kCtaThreads<MODE>, 1)
   int64_t u_begin = u0 + total * blockIdx.x / gridDim.x;
   int64_t u_end = u0 + total * (blockIdx.x + 1) / gridDim.x;
   if (listed && args.wpre != nullptr) {  // equal shares of kept tiles, not of items
-    const int64_t W = args.wpre[total];
-    u_begin = lower_bound_w(args.wpre, 0, total, W * blockIdx.x / gridDim.x);
-    u_end = blockIdx.x + 1 == gridDim.x ? total
-                                        : lower_bound_w(args.wpre, 0, total, W * (blockIdx.x + 1) / gridDim.x);
+    int64_t ua, ub;  // this rank's share of the list (all of it on one rank)
+    item_share(args, total, ua, ub);
+    const int64_t Wa = args.wpre[ua], W = args.wpre[ub] - Wa;
+    u_begin = lower_bound_w(args.wpre, ua, ub, Wa + W * blockIdx.x / gridDim.x);
+    u_end = blockIdx.x + 1 == gridDim.x ? ub
+                                        : lower_bound_w(args.wpre, ua, ub, Wa + W * (blockIdx.x + 1) / gridDim.x);
   }
 
   if (threadIdx.x == 0) {
@@ -1240,7 +1257,7 @@ int launch_affinity_tc_matvec(const float* xhi, const float* xlo, const float* s
                               int32_t dp, int64_t row_lo, int64_t row_hi, float neg_scale_log2,
                               const float* v32, double* ypart, int64_t rows_pad,
                               const gpic_ctl* ctl, cudaStream_t s, int kind, float* colpart,
-                              const PruneMask* pm) {
+                              const PruneMask* pm, int share_r, int share_n) {
   Maps mp;
   int rc = operand_maps(xhi, n, dp, &mp);
   if (rc) return rc;
@@ -1267,6 +1284,8 @@ int launch_affinity_tc_matvec(const float* xhi, const float* xlo, const float* s
     args.pB = pm->B;
     args.pnb = pm->nb;
     args.wpre = pm->item_wpre;
+    args.share_r = share_r;
+    args.share_n = share_n;
   }
   return dispatch_kb<kModeMatvec>(dp / kKBlk, mp, args, s);
 }

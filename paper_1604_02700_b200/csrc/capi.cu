@@ -481,6 +481,38 @@ int gpic_cluster_pruned_work(const void* d_work, int64_t n, int32_t d, int32_t k
   return GPIC_OK;
 }
 
+int64_t gpic_mf_shard_scratch_bytes(int64_t n, int32_t d) { return mf_shard_scratch_bytes(n, d); }
+
+int gpic_mf_shard_build(const float* d_xhi, const float* d_xlo, const float* d_sqn,
+                        const double* d_prep_work, int64_t n, int32_t d, double sigma,
+                        int32_t nranks, int32_t rank, double* d_deg_partial, void* d_scratch,
+                        void* stream) {
+  if (n < 1 || d < 1 || nranks < 1 || rank < 0 || rank >= nranks)
+    return fail(GPIC_E_INVALID, "bad matrix-free shard parameters");
+  if (!(sigma > 0)) return fail(GPIC_E_INVALID, "sigma must be positive");
+  const int32_t dp = feature_pitch(d);
+  if (d <= 8 || !tc_supports_pitch(dp, true) || !mf_sym_default() || !sparse_enabled() ||
+      !prune_enabled())
+    return fail(GPIC_E_UNSUPPORTED, "matrix-free item shards need the pruned tcgen05 sym pass");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  double* ypart = static_cast<double*>(d_scratch);
+  MfOperands op{d_xhi, d_xlo, d_sqn, n, dp, (float)(-1.4426950408889634 / (2.0 * sigma * sigma)),
+                GPIC_KIND_RBF};
+  op.d = d;
+  op.sym = 1;
+  op.pruned = 1;
+  op.prune = mf_shard_prune(ypart, n, d);
+  op.share_r = rank;
+  op.share_n = nranks;
+  const double* colpart = d_prep_work;  // gpic_prepare_points: column sums, then the mean
+  const double* mean = d_prep_work + ceil_div(n, 256) * d;
+  launch_prune(op.prune, d_xlo, colpart, mean, n, d, dp, sigma, -tc_mblocks(dp), 0, s);
+  float* ones = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ypart) +
+                                         round_up(mf_ypart_doubles(n, dp, n) * 8, 256) +
+                                         round_up(prune_bytes(n, dp), 256));
+  return launch_mf_degrees(op, 0, n, ones, ypart, d_deg_partial, s);
+}
+
 int gpic_matvec(const float* d_a, int64_t lda, int64_t rows, int64_t n, const float* d_v,
                 const double* d_row_scale, double* d_y, void* stream) {
   if (lda % 4 || lda < n) return fail(GPIC_E_INVALID, "lda must be >= n and a multiple of 4");

@@ -137,6 +137,12 @@ __global__ void set_epoch_kernel(gpic_ctl* ctl, uint64_t epoch) {
   if (threadIdx.x == 0) ctl->sync_epoch = epoch;
 }
 
+// a matrix-free shard over all rows marked lda = 1: an item shard of the
+// pruned sym pass (gpic_mf_shard_build)
+bool mf_item_shard(const gpic_shard& sh, int64_t n) {
+  return sh.storage == GPIC_STORAGE_NONE && sh.row_lo == 0 && sh.rows == n && sh.lda == 1;
+}
+
 LowRows low_rows(const gpic_comm* c, const gpic_shard& sh, int li, int64_t count) {
   LowRows L;
   L.x = sh.x;
@@ -328,9 +334,14 @@ int gpic_comm_gather_degrees(gpic_comm* c, const gpic_shard* shards, int32_t nlo
   if (!c || nlocal != c->nlocal) return fail(GPIC_E_INVALID, "shard count does not match the comm");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   for (int li = 0; li < nlocal; ++li) launch_ctl_init(c->loc[li].ctl, 0.0, 1, s);
-  const bool packed = shards[0].storage == GPIC_STORAGE_PACKED;
+  // packed shards and matrix-free item shards hold partial degrees of all
+  // rows (summed across ranks); row shards hold complete degrees of theirs
+  auto partial = [&](const gpic_shard& sh) {
+    return sh.storage == GPIC_STORAGE_PACKED || mf_item_shard(sh, c->n);
+  };
+  const bool packed = partial(shards[0]);
   for (int li = 1; li < nlocal; ++li)
-    if ((shards[li].storage == GPIC_STORAGE_PACKED) != packed)
+    if (partial(shards[li]) != packed)
       return fail(GPIC_E_INVALID, "all shards of a comm use the same storage");
   int rc = packed ? gather_sum(c, shards, s) : gather(c, shards, true, s);
   if (rc) return rc;
@@ -428,6 +439,22 @@ int gpic_comm_iterate(gpic_comm* c, const gpic_shard* shards, int32_t nlocal, do
                         (float)(-1.4426950408889634 / (2.0 * sh.sigma * sh.sigma)), sh.kind};
       S.mf.d = sh.d;
       S.ypart = sh.ypart;
+      if (mf_item_shard(sh, n)) {
+        // item shard: this rank's share of the pruned sym pass; partial y
+        // over all rows into every rank's slot, summed in rank order
+        S.mode = kLoopMfShard;
+        S.mf.sym = 1;
+        S.mf.pruned = 1;
+        S.mf.prune = mf_shard_prune(sh.ypart, n, sh.d);
+        S.mf.share_r = self;
+        S.mf.share_n = c->nranks;
+        S.pt_slots = table(c, self);
+        for (int p = 0; p < c->nranks; ++p)
+          for (int par = 0; par < 2; ++par) S.pt_slots.y[p][par] = r_slot(c->region[p], n, self, par);
+        S.slots = r_slot(c->region[self], n, 0, 0);
+        S.slot_stride = al(n * 8) / 8;
+        S.deg_full = r_deg(c->region[self], n);
+      }
     }
     S.rows = shards[li].rows;
     S.row_lo = shards[li].row_lo;

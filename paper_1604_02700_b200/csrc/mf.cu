@@ -110,6 +110,33 @@ __global__ void __launch_bounds__(256)
   if (h == 0 && lr < rows) ypart[(int64_t)blockIdx.x * rows_pad + lr] = acc + half1[r];
 }
 
+// The item ids [lo, hi) a rank owns in a pruned sym pass shared by
+// share_n ranks (the same tile-balanced split as the engine's, prune.cu
+// list order); everything when unshared.
+struct ItemShare {
+  const int32_t* items;
+  const int64_t* count;
+  const int64_t* wpre;
+  int r, nr;
+  __device__ void range(int64_t* out) const {
+    out[0] = 0;
+    out[1] = INT64_MAX;
+    if (items == nullptr || nr <= 1) return;
+    const int64_t total = *count, W = wpre[total];
+    auto lb = [&](int64_t target) {
+      int64_t lo = 0, hi = total;
+      while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (wpre[mid] >= target) hi = mid; else lo = mid + 1;
+      }
+      return lo;
+    };
+    const int64_t ua = lb(W * r / nr), ub = r + 1 == nr ? total : lb(W * (r + 1) / nr);
+    out[0] = ua < total ? items[ua] : INT64_MAX;
+    out[1] = ub < total ? items[ub] : INT64_MAX;
+  }
+};
+
 // One CTA per column tile J (128 rows of y), kSeg segments: segment s sums
 // its share of row i's chunk partials (chunks from the row block's first
 // tile on) and of the column records (row blocks I' = 0 .. J / MB), then the
@@ -121,9 +148,13 @@ __global__ void __launch_bounds__(128 * kSeg)
                          int64_t nparts, int64_t rows_pad, int64_t n, int64_t nct, int mb,
                          const double* __restrict__ deg, const PeerTable pt, gpic_ctl* ctl,
                          const uint8_t* __restrict__ item_kept, const uint8_t* __restrict__ pskip,
-                         int64_t pB, int64_t pnb) {
+                         int64_t pB, int64_t pnb, ItemShare sh) {
   if (ctl != nullptr && *(volatile const int32_t*)&ctl->stop) return;
   __shared__ double part[kSeg][128];
+  __shared__ int64_t id_rng[2];
+  if (threadIdx.x == 0) sh.range(id_rng);
+  __syncthreads();
+  const int64_t id_lo = id_rng[0], id_hi = id_rng[1];  // this rank's item ids
   const int64_t J = blockIdx.x;
   const int o = threadIdx.x % 128, sg = threadIdx.x / 128;
   const int64_t i = J * 128 + o;
@@ -134,14 +165,19 @@ __global__ void __launch_bounds__(128 * kSeg)
   // pruned pass: chunk partials of kept items and records of kept tiles
   // only (the others are exact zeros and never written)
   if (i < n)
-    for (int64_t p = p0; p < p1; ++p)
-      if (item_kept == nullptr || item_kept[rb * nparts + p] != 0) s += ypart[p * rows_pad + i];
+    for (int64_t p = p0; p < p1; ++p) {
+      const int64_t id = rb * nparts + p;
+      if ((item_kept == nullptr || item_kept[id] != 0) && id >= id_lo && id < id_hi)
+        s += ypart[p * rows_pad + i];
+    }
   const int64_t nrec = rb + 1;  // row blocks 0 .. rb hold tiles (I', J) with I' <= J
   const int64_t r0 = nrec * sg / kSeg, r1 = nrec * (sg + 1) / kSeg;
   const int64_t TJ = pskip != nullptr ? J * 128 / pB : 0;
 #pragma unroll 4
   for (int64_t r = r0; r < r1; ++r) {
     if (pskip != nullptr && pskip[(r * mb * 128 / pB) * pnb + TJ]) continue;
+    const int64_t id = r * nparts + J / 32;  // the item that wrote this record
+    if (id < id_lo || id >= id_hi) continue;
     const int64_t rec = r * nct - (int64_t)mb * r * (r - 1) / 2 + (J - r * mb);
     s += (double)colpart[rec * 128 + o];
   }
@@ -217,13 +253,16 @@ int launch_mf_matvec(const MfOperands& op, int64_t row_lo, int64_t rows, const f
     float* colpart = reinterpret_cast<float*>(ypart + mf_parts(op.n, op.dp) * rows_pad);
     const PruneMask* pm = op.pruned ? &op.prune : nullptr;
     int rc = launch_affinity_tc_matvec(op.xhi, op.xlo, op.sqn, op.n, op.dp, 0, op.n, op.ns, v32,
-                                       ypart, rows_pad, ctl, s, op.kind, colpart, pm);
+                                       ypart, rows_pad, ctl, s, op.kind, colpart, pm, op.share_r,
+                                       op.share_n);
     if (rc) return rc;
     const int64_t nct = ceil_div(op.n, kTileN);
+    const ItemShare sh{pm ? pm->items : nullptr, pm ? pm->item_count : nullptr,
+                       pm ? pm->item_wpre : nullptr, op.share_r, op.share_n};
     mf_sym_reduce_kernel<<<(unsigned)nct, 128 * kSeg, 0, s>>>(
         ypart, colpart, mf_parts(op.n, op.dp), rows_pad, op.n, nct,
         mf_rows_per_block(op.dp) / 128, deg, pt, ctl, pm ? pm->item_kept : nullptr,
-        pm ? pm->skip : nullptr, pm ? pm->B : 1, pm ? pm->nb : 0);
+        pm ? pm->skip : nullptr, pm ? pm->B : 1, pm ? pm->nb : 0, sh);
     count_launch();
     GPIC_CUDA_TRY(cudaGetLastError());
     return GPIC_OK;
@@ -236,6 +275,18 @@ int launch_mf_matvec(const MfOperands& op, int64_t row_lo, int64_t rows, const f
   count_launch();
   GPIC_CUDA_TRY(cudaGetLastError());
   return GPIC_OK;
+}
+
+int64_t mf_shard_scratch_bytes(int64_t n, int32_t d) {
+  const int32_t dp = feature_pitch(d);
+  return round_up(mf_ypart_doubles(n, dp, n) * 8, 256) + round_up(prune_bytes(n, dp), 256) +
+         round_up(vector_pitch(n) * 4, 256);
+}
+
+PruneMask mf_shard_prune(double* ypart, int64_t n, int32_t d) {
+  const int32_t dp = feature_pitch(d);
+  uint8_t* p = reinterpret_cast<uint8_t*>(ypart) + round_up(mf_ypart_doubles(n, dp, n) * 8, 256);
+  return carve_prune(p, n, dp);
 }
 
 // deg[i] = sum_j a_ij for the shard's rows (v = 1 through the same pass).

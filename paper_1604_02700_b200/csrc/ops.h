@@ -211,7 +211,14 @@ struct MfOperands {
   int32_t d = 0;  // features (RBF with d <= 8: the difference-form SIMT pass)
   int pruned = 0;  // sym pass over the kept items of `prune` only (prune.cu)
   PruneMask prune;
+  // pruned sym pass split across ranks: this rank computes the tile-balanced
+  // share share_r of share_n of the kept items; its reduce yields a partial y
+  int share_r = 0, share_n = 1;
 };
+// workspace of a matrix-free item shard: full-matrix partial buffers, the
+// pruning mask, one fp32 vector
+int64_t mf_shard_scratch_bytes(int64_t n, int32_t d);
+PruneMask mf_shard_prune(double* ypart, int64_t n, int32_t d);
 bool mf_sym_default();
 int64_t mf_parts(int64_t n, int32_t dp);
 int mf_rows_per_block(int32_t dp);
@@ -221,7 +228,8 @@ int launch_affinity_tc_matvec(const float* xhi, const float* xlo, const float* s
                               int32_t dp, int64_t row_lo, int64_t row_hi, float neg_scale_log2,
                               const float* v32, double* ypart, int64_t rows_pad,
                               const gpic_ctl* ctl, cudaStream_t s, int kind = GPIC_KIND_RBF,
-                              float* colpart = nullptr, const PruneMask* pm = nullptr);
+                              float* colpart = nullptr, const PruneMask* pm = nullptr,
+                              int share_r = 0, int share_n = 1);
 int launch_mf_matvec(const MfOperands& op, int64_t row_lo, int64_t rows, const float* v32,
                      double* ypart, const double* deg, const PeerTable& pt, gpic_ctl* ctl,
                      cudaStream_t s);
@@ -273,7 +281,8 @@ void launch_lowdeg_exact(const LowRows& L, double* deg, gpic_ctl* ctl, cudaStrea
 void launch_lowdeg_matvec(const LowRows& L, const double* deg, const double* v64, double* y0,
                           double* y1, gpic_ctl* ctl, cudaStream_t s);
 
-enum { kLoopDense = 0, kLoopPacked = 1, kLoopMatrixFree = 2, kLoopPacked16 = 3, kLoopPackedShard = 4 };
+enum { kLoopDense = 0, kLoopPacked = 1, kLoopMatrixFree = 2, kLoopPacked16 = 3, kLoopPackedShard = 4,
+       kLoopMfShard = 5 };
 
 // One shard's loop state (a single-rank run is one shard with nranks = 1).
 struct ShardLoop {

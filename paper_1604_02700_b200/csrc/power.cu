@@ -362,8 +362,11 @@ int run_power_loops(ShardLoop* shards, int nlocal, int64_t n, int32_t max_iter, 
         } else if (L.mode == kLoopPackedShard) {
           // partial y over the shard's tiles into every rank's slot of this shard
           launch_sym_gemv(L.a, n, L.v32, L.rowp, L.colp, nullptr, L.pt_slots, L.ctl, cs, L.sr);
-        } else if (L.mode == kLoopMatrixFree) {
-          const int rc = launch_mf_matvec(L.mf, L.row_lo, L.rows, L.v32, L.ypart, L.deg, L.pt,
+        } else if (L.mode == kLoopMatrixFree || L.mode == kLoopMfShard) {
+          // item shard: partial y (no 1/deg) into every rank's slot of this shard
+          const bool item = L.mode == kLoopMfShard;
+          const int rc = launch_mf_matvec(L.mf, L.row_lo, L.rows, L.v32, L.ypart,
+                                          item ? nullptr : L.deg, item ? L.pt_slots : L.pt,
                                           L.ctl, cs);
           if (rc) {
             cudaGraph_t junk;
@@ -380,7 +383,7 @@ int run_power_loops(ShardLoop* shards, int nlocal, int64_t n, int32_t max_iter, 
         const PeerTable& pt = L.pt;
         if (pt.flags[0] != nullptr)
           launch_peer_wait(pt.flags[pt.self], 0, pt.nranks, 0, 1, L.ctl, cs);
-        if (L.mode == kLoopPackedShard)
+        if (L.mode == kLoopPackedShard || L.mode == kLoopMfShard)
           launch_slot_combine(L.slots, L.slot_stride, pt.nranks, n, L.deg_full, pt.y[pt.self][0],
                               pt.y[pt.self][1], L.ctl, cs);
         if (L.low.count > 0)

@@ -214,6 +214,7 @@ class PreparedPoints:
     kind: int = _lib.KIND_RBF
     x: object = None  # the fp64 points on the device (isolated-row fix, lowdeg.cu)
     spread2: float = 0.0  # R^2 = max_i |x_i - mean|^2 (RBF): engine routing
+    work: object = None  # gpic_prepare_points' column sums + mean (tile pruning)
 
     def engine(self, sigma: float, engine: str, storage: int) -> str:
         """The engine gpic_cluster would run (gpic_engine_for): SIMT difference
@@ -252,7 +253,7 @@ def prepare_points(d, dev, kind: int = _lib.KIND_RBF) -> PreparedPoints:
     _raise_ctl(_read_ctl(ctl, dev), m)
     spread2 = float(work[ncol + m + 1].item()) if kind == _lib.KIND_RBF else 0.0
     return PreparedPoints(xhi=xhi, xlo=xlo, sqn=sqn, n=n, d=m, device=dev, kind=kind, x=x,
-                          spread2=spread2)
+                          spread2=spread2, work=work)
 
 
 def affinity_rows(prep: PreparedPoints, lo: int, hi: int, sigma: float, engine: str = "tc"):

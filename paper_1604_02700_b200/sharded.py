@@ -155,7 +155,34 @@ class ShardedRunner:
         shards = (_lib.Shard * nl)()
         keep = []  # device buffers referenced by the shard structs
         L = _lib.lib()
-        if cfg.storage == "none":
+        # matrix-free item shards: the pruned symmetric pass's kept items split
+        # across the ranks by tile count (RBF, d > 8 on the tensor engine);
+        # other matrix-free inputs fall back to row bands (full-square rows)
+        item_shards = (cfg.storage == "none" and cfg.affinity_impl == "tc"
+                       and code == _lib.KIND_RBF and prep.d > 8
+                       and prep.engine(sigma, "tc", _lib.STORAGE_NONE) == "tc")
+        if item_shards:
+            P = cfg.p
+            for i, r in enumerate(self.locals):
+                deg = torch.empty(n, dtype=torch.float64, device=dev)
+                scratch = torch.empty(int(L.gpic_mf_shard_scratch_bytes(n, prep.d)),
+                                      dtype=torch.uint8, device=dev)
+                rc = L.gpic_mf_shard_build(gpu._ptr(prep.xhi), gpu._ptr(prep.xlo),
+                                           gpu._ptr(prep.sqn), gpu._ptr(prep.work), n, prep.d,
+                                           sigma, P, r, gpu._ptr(deg), gpu._ptr(scratch), st)
+                if rc == _lib.GPIC_E_UNSUPPORTED:  # pruning disabled (GPIC_PRUNE=0 ...)
+                    item_shards = False
+                    keep.clear()
+                    break
+                _lib.check(rc)
+                keep += [deg, scratch]
+                shards[i] = _lib.Shard(None, 1, deg.data_ptr(), 0, n, _lib.STORAGE_NONE, prep.d,
+                                       prep.xhi.data_ptr(), prep.xlo.data_ptr(),
+                                       prep.sqn.data_ptr(), sigma, code, scratch.data_ptr(),
+                                       prep.x.data_ptr())
+        if item_shards:
+            pass
+        elif cfg.storage == "none":
             if cfg.affinity_impl != "tc":
                 raise InvalidSpec("matrix-free storage runs on the tcgen05 engine")
             ones = torch.empty(int(L.gpic_vector_pitch(n)), dtype=torch.float32, device=dev)

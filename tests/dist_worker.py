@@ -30,15 +30,21 @@ def main():
                                seed=2)
     # packed symmetric shards: same labels as one rank, embedding within 1e-6
     lp, vp, tp = cluster(d, kind, params, config=KernelConfig(p=world, device=dev), seed=2)
-    agree = sharded.all_ranks_agree(labels, v) and sharded.all_ranks_agree(lp, vp)
+    # matrix-free item shards of the pruned symmetric pass
+    lm, vm, tm = cluster(d, kind, params, config=KernelConfig(p=world, device=dev, storage="none"),
+                         seed=2)
+    agree = (sharded.all_ranks_agree(labels, v) and sharded.all_ranks_agree(lp, vp)
+             and sharded.all_ranks_agree(lm, vm))
     if rank == 0:
         single = cluster(d, kind, params, config=KernelConfig(device=dev, storage="dense"), seed=2)
         same = (np.array_equal(single[0], labels) and np.array_equal(single[1], v)
                 and np.array_equal(single[2].delta_history, trace.delta_history))
         packed_ok = (np.array_equal(single[0], lp) and tp.iterations_run == trace.iterations_run
                      and np.abs(vp - single[1]).sum() / np.abs(single[1]).sum() <= 1e-6)
+        mf_ok = (np.array_equal(single[0], lm) and tm.iterations_run == trace.iterations_run
+                 and np.abs(vm - single[1]).sum() / np.abs(single[1]).sum() <= 1e-6)
         print("RANKS_AGREE", agree, flush=True)
-        print("MATCHES_SINGLE", same and packed_ok, flush=True)
+        print("MATCHES_SINGLE", same and packed_ok and mf_ok, flush=True)
     dist.barrier()
     dist.destroy_process_group()
 

@@ -144,11 +144,37 @@ def test_two_processes_one_device_ipc():
 
 
 @pytest.mark.gpu
-def test_matrix_free_virtual_ranks_bitwise():
+def test_matrix_free_item_shards_match_single_rank():
+    """Matrix-free item shards: the pruned symmetric pass's kept items split
+    across P ranks by tile count, partial y summed in rank order. Same labels
+    and iteration count as one rank, embedding within 1e-6 relative L1 (only
+    the summation grouping changes), deterministic across repeats; forced
+    iterations too."""
+    d = gaussian_blobs(9000, 64, 6, seed=8)
+    kind, params = GaussianRbf(4.0), PicParams(k=6)
+    single = cluster(d, kind, params, config=KernelConfig(storage="none"), seed=3)
+    for p in (2, 3, 8):
+        cfg = KernelConfig(p=p, virtual_ranks=True, storage="none")
+        a = cluster(d, kind, params, config=cfg, seed=3)
+        b = cluster(d, kind, params, config=cfg, seed=3)
+        assert np.array_equal(a[0], single[0]), p
+        assert a[2].iterations_run == single[2].iterations_run, p
+        assert np.abs(a[1] - single[1]).sum() / np.abs(single[1]).sum() <= 1e-6, p
+        assert np.array_equal(a[1], b[1]), p
+    forced = PicParams(k=6, epsilon=5e-324, max_iterations=6)
+    f1 = cluster(d, kind, forced, config=KernelConfig(storage="none"), seed=3)
+    f4 = cluster(d, kind, forced, config=KernelConfig(p=4, virtual_ranks=True, storage="none"), seed=3)
+    assert f4[2].iterations_run == 6
+    assert np.abs(f4[1] - f1[1]).sum() / np.abs(f1[1]).sum() <= 1e-6
+
+
+@pytest.mark.gpu
+def test_matrix_free_virtual_ranks_bitwise(monkeypatch):
+    # without pruning the matrix-free shards are row bands (full-square
+    # pass), bitwise P-invariant; one rank runs the upper-triangle pass
+    monkeypatch.setenv("GPIC_PRUNE", "0")
     d = gaussian_blobs(2600, 64, 4, seed=8)
     kind, params = GaussianRbf(4.0), PicParams(k=4)
-    # one rank runs the upper-triangle pass; row shards the full-square pass,
-    # which is bitwise P-invariant
     single = cluster(d, kind, params, config=KernelConfig(storage="none"), seed=3)
     base = cluster(d, kind, params, seed=3,
                    config=KernelConfig(p=2, virtual_ranks=True, storage="none"))
