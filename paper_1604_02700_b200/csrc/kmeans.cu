@@ -655,7 +655,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
       long long pick = block_min_i(found, sh);
-      if (pick > bhi - 1) pick = bhi - 1;
+      // rounding can keep this CTA's sequential sum at or below r although
+      // its scanned total exceeds it: the crossing is then at the next
+      // CTA's first index, as searchsorted would place it (clamped, as
+      // kmeans.py:53 clamps to n - 1)
+      if (pick > bhi - 1) pick = bhi < n ? bhi : n - 1;
       if (tid == 0) gpi[kGPick] = pick;
     }
     grid.sync();

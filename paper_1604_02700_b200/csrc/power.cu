@@ -164,10 +164,10 @@ __global__ void scale_by_kernel(const double* __restrict__ src, int64_t n, doubl
 }
 
 // Acquire-spin until flags[slot0 .. slot0+count) all reach base (+ iter + 1
-// when add_iter). A peer that never arrives (dead rank) trips a ~10 s
-// timeout: the run stops with GPIC_E_COMM instead of hanging the device.
+// when add_iter). A peer that never arrives (dead rank) trips the timeout
+// (launch_peer_wait): the run stops with GPIC_E_COMM instead of hanging.
 __global__ void peer_wait_kernel(const uint64_t* flags, int slot0, int count, uint64_t base,
-                                 int add_iter, gpic_ctl* ctl) {
+                                 int add_iter, gpic_ctl* ctl, uint64_t timeout_ns) {
   if (threadIdx.x != 0) return;
   if (add_iter && *(volatile int32_t*)&ctl->stop) return;
   // loop mode: the epoch base lives in the control block so one captured
@@ -182,7 +182,7 @@ __global__ void peer_wait_kernel(const uint64_t* flags, int slot0, int count, ui
       if (v >= target) break;
       uint64_t now;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
-      if (now - t0 > 10ull * 1000 * 1000 * 1000) {
+      if (now - t0 > timeout_ns) {
         raise_status(ctl, GPIC_E_COMM, slot0 + s, -1, 0.0);
         return;
       }
@@ -249,9 +249,18 @@ void launch_iteration_tail(const double* y0, const double* y1, int64_t n, double
   count_launch(2);
 }
 
+// Timeouts: a per-iteration wait (add_iter) covers one GEMV of the slowest
+// rank, GPIC_PEER_TIMEOUT_S (default 10 s); barrier / gather waits also cover
+// skew between ranks (graph instantiation, a slow host, a large shard
+// build): 12x that (default 120 s).
 void launch_peer_wait(const uint64_t* flags_self, int slot0, int count, uint64_t base,
                       int add_iter, gpic_ctl* ctl, cudaStream_t s) {
-  peer_wait_kernel<<<1, 32, 0, s>>>(flags_self, slot0, count, base, add_iter, ctl);
+  double secs = 10.0;
+  if (const char* e = getenv("GPIC_PEER_TIMEOUT_S"))
+    if (atof(e) > 0.0) secs = atof(e);
+  if (!add_iter) secs *= 12.0;
+  peer_wait_kernel<<<1, 32, 0, s>>>(flags_self, slot0, count, base, add_iter, ctl,
+                                    (uint64_t)(secs * 1e9));
   count_launch();
 }
 
