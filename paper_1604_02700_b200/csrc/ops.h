@@ -250,6 +250,13 @@ struct SparseMask {
 int64_t sparse_mask_bytes(int64_t n, int32_t d);
 // per super-block box bits (16 tiles x 16 boxes), stored behind sb_prefix
 const uint16_t* sb_bits(const int64_t* sb_prefix, int64_t n);
+// the non-empty super-blocks (ascending ids, weight prefix per entry, count)
+struct SbList {
+  const int32_t* list;
+  const int64_t* lpre;
+  const int64_t* count;
+};
+SbList sb_list(const int64_t* sb_prefix, int64_t n);
 SparseMask carve_sparse(void* base, int64_t n, int32_t d);
 // the GEMV weights from the box flags the affinity engine wrote
 void launch_sparse_prefix(const SparseMask& m, cudaStream_t s);

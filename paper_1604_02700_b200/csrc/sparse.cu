@@ -103,6 +103,42 @@ __global__ void __launch_bounds__(kScanThreads)
   }
 }
 
+// the ascending list of non-empty super-blocks (weight > 1) with the weight
+// prefix at each entry (lpre[e] = prefix[list[e]], lpre[count] = total): the
+// GEMV walks only these, so its CTAs never touch (and never load the
+// weights of) the ~80 % empty ones. One CTA, contiguous segments.
+__global__ void __launch_bounds__(kScanThreads)
+    sb_list_kernel(int64_t nt, const int64_t* __restrict__ prefix, int32_t* __restrict__ list,
+                   int64_t* __restrict__ lpre, int64_t* __restrict__ count) {
+  __shared__ int64_t sh[kScanThreads];
+  const int64_t ns = (nt + kSB - 1) / kSB;
+  const int64_t total = ns * (ns + 1) / 2;
+  const int t = threadIdx.x;
+  const int64_t seg = (total + kScanThreads - 1) / kScanThreads;
+  const int64_t a = min(total, t * seg), b = min(total, a + seg);
+  int64_t c = 0;
+  for (int64_t s = a; s < b; ++s) c += prefix[s + 1] - prefix[s] > 1;
+  sh[t] = c;
+  __syncthreads();
+  for (int o = 1; o < kScanThreads; o <<= 1) {
+    const int64_t add = t >= o ? sh[t - o] : 0;
+    __syncthreads();
+    sh[t] += add;
+    __syncthreads();
+  }
+  int64_t w = t > 0 ? sh[t - 1] : 0;
+  for (int64_t s = a; s < b; ++s)
+    if (prefix[s + 1] - prefix[s] > 1) {
+      list[w] = (int32_t)s;
+      lpre[w] = prefix[s];
+      ++w;
+    }
+  if (t == kScanThreads - 1) {
+    *count = sh[t];
+    lpre[sh[t]] = prefix[total];
+  }
+}
+
 __global__ void fill_kernel(uint8_t* p, int64_t n, uint8_t v) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) p[i] = v;
@@ -119,8 +155,25 @@ int64_t sparse_mask_bytes(int64_t n, int32_t /*d*/) {
   const int64_t nt = ceil_div(n, kT);
   const int64_t ns = ceil_div(nt, kSB);
   auto al = [](int64_t b) { return (b + 255) & ~int64_t(255); };
-  return al(nt * (nt + 1) / 2 * 16) + al((ns * (ns + 1) / 2 + 1) * 8) +
-         al(ns * (ns + 1) / 2 * kSB * kSB * 2);
+  const int64_t nsb = ns * (ns + 1) / 2;
+  return al(nt * (nt + 1) / 2 * 16) + al((nsb + 1) * 8) + al(nsb * kSB * kSB * 2) + al(8) +
+         al((nsb + 1) * 8) + al(nsb * 4);
+}
+
+// the non-empty super-block list behind the box bits (sb_list_kernel)
+SbList sb_list(const int64_t* sb_prefix, int64_t n) {
+  SbList L{nullptr, nullptr, nullptr};
+  if (sb_prefix == nullptr) return L;
+  auto al = [](int64_t b) { return (b + 255) & ~int64_t(255); };
+  const int64_t ns = ceil_div(ceil_div(n, kT), kSB), nsb = ns * (ns + 1) / 2;
+  const uint8_t* p = reinterpret_cast<const uint8_t*>(sb_prefix) + al((nsb + 1) * 8) +
+                     al(nsb * kSB * kSB * 2);
+  L.count = reinterpret_cast<const int64_t*>(p);
+  p += al(8);
+  L.lpre = reinterpret_cast<const int64_t*>(p);
+  p += al((nsb + 1) * 8);
+  L.list = reinterpret_cast<const int32_t*>(p);
+  return L;
 }
 
 // the per-super-block box bits live right behind the GEMV weights
@@ -149,7 +202,11 @@ void launch_sparse_prefix(const SparseMask& m, cudaStream_t s) {
   sb_weight_kernel<<<(unsigned)ceil_div(m.n_sb, 256), 256, 0, s>>>(
       m.boxnz, m.nt, m.sb_prefix, const_cast<uint16_t*>(sb_bits(m.sb_prefix, m.nt * kT)));
   sb_scan_kernel<<<1, kScanThreads, 0, s>>>(m.nt, m.sb_prefix);
-  count_launch(2);
+  const SbList L = sb_list(m.sb_prefix, m.nt * kT);
+  sb_list_kernel<<<1, kScanThreads, 0, s>>>(m.nt, m.sb_prefix, const_cast<int32_t*>(L.list),
+                                            const_cast<int64_t*>(L.lpre),
+                                            const_cast<int64_t*>(L.count));
+  count_launch(3);
 }
 
 void launch_box_fill(const SparseMask& m, uint8_t v, cudaStream_t s) {

@@ -88,6 +88,9 @@ struct Sparse {
   int prefetch;          // producer: tiles prefetched into L2 ahead of the smem ring
   int bits_consumer;     // consumers read the super-block records too (else per-tile flags)
   int evict_first;       // tile loads with the L2 evict-first policy
+  const int32_t* list;   // non-empty super-blocks (sb_list), or null: walk the id range
+  const int64_t* lpre;
+  const int64_t* lcount;
   // the 16 tile masks of super-block s (two 16-byte loads), kept in
   // registers: selected by comparisons, never indexed (an indexed array
   // went to local memory)
@@ -172,43 +175,82 @@ struct SbWalk {
   }
 };
 
-// Enumerates the stored tiles (global packed index) of super-blocks
-// [sb, s1) in the walk order; -1 at the end.
-struct TileEnum {
-  SbWalk w;
-  int64_t sb, s1;
-  Sparse::Rec rec;
-  bool open, fresh;
-  __device__ void begin(int64_t P0, int64_t Q0, int64_t s0, int64_t s_end, int64_t nt,
-                        int64_t ns) {
-    w.nt = nt;
-    w.ns = ns;
-    w.P = P0;
-    w.Q = Q0;
+// The CTA's super-blocks, in order: either the id range [sb, s1) (every
+// super-block, empty ones skipped by their weight) or, with a list of the
+// non-empty ones (sparse.cu sb_list_kernel), the entries [e, e1) of it.
+// (P, Q) follow the current super-block.
+struct SbCursor {
+  const int32_t* list;
+  int64_t e, e1;    // list mode
+  int64_t sb, s1;   // current id (both modes); range end
+  int64_t P, Q, ns;
+  __device__ void begin_range(int64_t s0, int64_t s_end, int64_t ns_) {
+    list = nullptr;
+    ns = ns_;
     sb = s0;
     s1 = s_end;
+    if (sb < s1) tile_coords(sb, ns, P, Q);
+  }
+  __device__ void begin_list(const int32_t* l, int64_t e0, int64_t e_end, int64_t ns_) {
+    list = l;
+    ns = ns_;
+    e = e0;
+    e1 = e_end;
+    if (e < e1) {
+      sb = list[e];
+      tile_coords(sb, ns, P, Q);
+    }
+  }
+  __device__ bool valid() const { return list ? e < e1 : sb < s1; }
+  __device__ void step() {
+    if (list) {
+      if (++e < e1) {
+        sb = list[e];
+        tile_coords(sb, ns, P, Q);
+      }
+      return;
+    }
+    ++sb;
+    if (++Q == ns) {
+      ++P;
+      Q = P;
+    }
+  }
+  // range mode: a super-block without a stored tile is skipped
+  __device__ bool skip(const Sparse& sp) const { return list == nullptr && sp.empty_sb(sb); }
+};
+
+// Enumerates the stored tiles (global packed index) of the CTA's
+// super-blocks in the walk order; -1 at the end.
+struct TileEnum {
+  SbWalk w;
+  SbCursor c;
+  Sparse::Rec rec;
+  bool open, fresh;
+  __device__ void begin(const SbCursor& c0, int64_t nt) {
+    c = c0;
+    w.nt = nt;
+    w.ns = c.ns;
     open = false;
   }
   __device__ int64_t next(const Sparse& sp) {
     for (;;) {
       if (!open) {
-        if (sb >= s1) return -1;
+        if (!c.valid()) return -1;
         if (sp.bits != nullptr) {
-          rec = sp.record(sb);
-          if (Sparse::empty(rec)) { ++sb; w.next_sb(); continue; }
-        } else if (sp.empty_sb(sb)) {
-          ++sb;
-          w.next_sb();
+          rec = sp.record(c.sb);
+          if (Sparse::empty(rec)) { c.step(); continue; }
+        } else if (c.skip(sp)) {
+          c.step();
           continue;
         }
-        w.open(w.P, w.Q);
+        w.open(c.P, c.Q);
         open = true;
         fresh = true;
       }
       if (!fresh && !w.next()) {
         open = false;
-        ++sb;
-        w.next_sb();
+        c.step();
         continue;
       }
       fresh = false;
@@ -257,22 +299,34 @@ __global__ void __launch_bounds__(kThreads, 1)
   // the shard's super-blocks [sb_lo, sb_hi) (whole matrix: all of them);
   // records are indexed from sb_lo, tiles from the shard's first tile
   const int64_t sb_lo = sr.sb_lo(ns), total = sr.sb_hi(ns) - sb_lo;
-  int64_t s0 = sb_lo + total * blockIdx.x / gridDim.x;
-  int64_t s1 = sb_lo + total * (blockIdx.x + 1) / gridDim.x;
-  if (sp.sbp != nullptr) {  // equal shares of real work (non-zero tiles), not of super-blocks
-    const int64_t sb_hi = sb_lo + total;
-    const int64_t w0 = sp.sbp[sb_lo], W = sp.sbp[sb_hi] - w0;
-    s0 = lower_bound64(sp.sbp, sb_lo, sb_hi, w0 + W * blockIdx.x / gridDim.x);
-    s1 = blockIdx.x + 1 == gridDim.x
-             ? sb_hi
-             : lower_bound64(sp.sbp, sb_lo, sb_hi, w0 + W * (blockIdx.x + 1) / gridDim.x);
+  SbCursor cur0;
+  if (sp.list != nullptr) {
+    // the non-empty super-blocks only, equal shares of their weight
+    const int64_t cnt = *sp.lcount;
+    const int64_t w0 = sp.lpre[0], W = sp.lpre[cnt] - w0;
+    const int64_t e0 = lower_bound64(sp.lpre, 0, cnt, w0 + W * blockIdx.x / gridDim.x);
+    const int64_t e1 = blockIdx.x + 1 == gridDim.x
+                           ? cnt
+                           : lower_bound64(sp.lpre, 0, cnt, w0 + W * (blockIdx.x + 1) / gridDim.x);
+    if (e0 >= e1) return;
+    cur0.begin_list(sp.list, e0, e1, ns);
+  } else {
+    int64_t s0 = sb_lo + total * blockIdx.x / gridDim.x;
+    int64_t s1 = sb_lo + total * (blockIdx.x + 1) / gridDim.x;
+    if (sp.sbp != nullptr) {  // equal shares of real work (non-zero tiles), not of super-blocks
+      const int64_t sb_hi = sb_lo + total;
+      const int64_t w0 = sp.sbp[sb_lo], W = sp.sbp[sb_hi] - w0;
+      s0 = lower_bound64(sp.sbp, sb_lo, sb_hi, w0 + W * blockIdx.x / gridDim.x);
+      s1 = blockIdx.x + 1 == gridDim.x
+               ? sb_hi
+               : lower_bound64(sp.sbp, sb_lo, sb_hi, w0 + W * (blockIdx.x + 1) / gridDim.x);
+    }
+    if (s0 >= s1) return;
+    cur0.begin_range(s0, s1, ns);
   }
-  if (s0 >= s1) return;
   SbWalk w;
   w.nt = nt;
   w.ns = ns;
-  int64_t P0, Q0;
-  tile_coords(s0, ns, P0, Q0);
 
   if (warp == kWarps) {  // producer
     if (lane != 0) return;
@@ -284,8 +338,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     // into L2 (more bytes in flight than the smem ring holds)
     const uint64_t stream_pol = policy_evict_first();
     TileEnum cur, pre;
-    cur.begin(P0, Q0, s0, s1, nt, ns);
-    pre.begin(P0, Q0, s0, s1, nt, ns);
+    cur.begin(cur0, nt);
+    pre.begin(cur0, nt);
     const int ahead = sp.prefetch;
     for (int d = 0; d < ahead; ++d) {
       const int64_t t = pre.next(sp);
@@ -315,20 +369,19 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t ph = 0;
   int rb = 0;
   const int t = threadIdx.x;
-  w.P = P0;
-  w.Q = Q0;
   Sparse::Rec rec{};
   Sparse cs = sp;  // the consumers' view
   if (!sp.bits_consumer) cs.bits = nullptr;
-  for (int64_t sb = s0; sb < s1; ++sb, w.next_sb()) {
+  for (SbCursor cur = cur0; cur.valid(); cur.step()) {
+    const int64_t sb = cur.sb;
     // no stored tile: its records are never read
     if (cs.bits != nullptr) {
       rec = cs.record(sb);
       if (Sparse::empty(rec)) continue;
-    } else if (cs.empty_sb(sb)) {
+    } else if (cur.skip(cs)) {
       continue;
     }
-    w.open(w.P, w.Q);
+    w.open(cur.P, cur.Q);
     // per lane: the column products of the super-block's kSB tile columns,
     // accumulated over its tile rows (one cross-warp combine per super-block)
     float4 cpa[kSB];
@@ -646,6 +699,12 @@ int g_sms = 0;
 
 // tiles each GEMV producer prefetches into L2 ahead of its smem ring
 // (GPIC_GEMV_PREFETCH, default 0: measured slower at config 3)
+// GPIC_GEMV_LIST=0: walk every super-block id (A/B against the list)
+int gemv_use_list() {
+  const char* e = getenv("GPIC_GEMV_LIST");
+  return e != nullptr ? atoi(e) : 1;
+}
+
 int gemv_evict_first() {
   const char* e = getenv("GPIC_GEMV_EVICT");
   return e != nullptr ? atoi(e) : 1;
@@ -664,7 +723,7 @@ void launch_sym_degree(const float* degrow, const float* degcol, int64_t n, int 
   const int64_t nt = ceil_div(n, kTS);
   const int64_t rows = nt - kSB * sr.p_lo;  // tile rows that can receive partials
   if (rows < 1) return;
-  const Sparse sp{boxnz, nullptr, nullptr, 0, 0, 0};
+  const Sparse sp{boxnz, nullptr, nullptr, 0, 0, 0, nullptr, nullptr, nullptr};
   const size_t dyn = boxnz != nullptr ? (size_t)nt * 4 : 0;  // the live-tile list
   if (dyn > 48 * 1024)
     cudaFuncSetAttribute(sym_degree_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
@@ -699,11 +758,15 @@ void launch_sym_gemv(const float* tiles, int64_t n, const float* v32, float* row
   // packed shards keep per-tile flags (their super-block records are not built)
   const bool whole = sr.p_lo == 0 && sr.tile_base == 0 && sr.p_hi >= ceil_div(ceil_div(n, kTS), kSB);
   // GPIC_SB_BITS: 0 per-tile flags everywhere, 1 super-block records for
-  // producer and consumers, 2 records for the producer only (default)
-  const int bits_mode = getenv("GPIC_SB_BITS") != nullptr ? atoi(getenv("GPIC_SB_BITS")) : 2;
+  // producer and consumers (default), 2 records for the producer only.
+  // Measured at config 3 (scripts/gemv_ab.py, one box): id walk + flags
+  // 0.500 ms, list + flags 0.465, list + records 0.424
+  const int bits_mode = getenv("GPIC_SB_BITS") != nullptr ? atoi(getenv("GPIC_SB_BITS")) : 1;
+  const SbList sl = boxnz != nullptr && whole && gemv_use_list() ? sb_list(sb_prefix, n)
+                                                                  : SbList{nullptr, nullptr, nullptr};
   const Sparse sp{boxnz, boxnz != nullptr ? sb_prefix : nullptr,
                   boxnz != nullptr && whole && bits_mode != 0 ? sb_bits(sb_prefix, n) : nullptr,
-                  gemv_prefetch(), bits_mode == 1, gemv_evict_first()};
+                  gemv_prefetch(), bits_mode == 1, gemv_evict_first(), sl.list, sl.lpre, sl.count};
   sym_prepare();
   const int64_t nt = ceil_div(n, kTS);
   const int64_t ns = (nt + kSB - 1) / kSB;
@@ -719,9 +782,11 @@ void launch_sym_gemv(const float* tiles, int64_t n, const float* v32, float* row
 void launch_sym_gemv16(const void* tiles, int64_t n, const float* v32, float* rowp, float* colp,
                        const double* deg, const PeerTable& pt, gpic_ctl* ctl, cudaStream_t s,
                        const uint8_t* boxnz, const int64_t* sb_prefix) {
+  const SbList sl = boxnz != nullptr && gemv_use_list() ? sb_list(sb_prefix, n)
+                                                        : SbList{nullptr, nullptr, nullptr};
   const Sparse sp{boxnz, boxnz != nullptr ? sb_prefix : nullptr,
                   boxnz != nullptr ? sb_bits(sb_prefix, n) : nullptr, gemv_prefetch(), 0,
-                  gemv_evict_first()};
+                  gemv_evict_first(), sl.list, sl.lpre, sl.count};
   sym_prepare();
   const int64_t nt = ceil_div(n, kTS);
   const int64_t ns = (nt + kSB - 1) / kSB;
