@@ -198,6 +198,24 @@ typedef struct {
   int64_t next; /* atomic row cursor */
 } job_t;
 
+/*
+ * Optional block skip (picmf_set_skip), for the n = 1M fixture only: skip[S *
+ * nb + T] = 1 marks a pair of BLK-row / BLK-column blocks whose every entry
+ * is proved (by the caller's fp64 projection bound, oracle/pic_mf.py) to be
+ * below e^-70. Such a block's sum is <= BLK e^-70 ~ 4e-28 per row, far below
+ * half an ulp of any row sum that contains a block with real neighbours
+ * (>= 1e-8 here), so adding it or not leaves the fp64 row sum bit for bit
+ * unchanged — whether it comes before or after the significant blocks (a
+ * tiny prefix is absorbed by the first significant block sum). Checked
+ * against the unskipped pass on config 3 (tests/test_oracle_mf.py).
+ */
+static const uint8_t *g_skip = NULL;
+static int64_t g_skip_nb = 0;
+void picmf_set_skip(const uint8_t *skip, int64_t nb) {
+  g_skip = skip;
+  g_skip_nb = nb;
+}
+
 static int n_threads(void) {
   const char *e = getenv("PICMF_THREADS");
   long t = e ? atol(e) : sysconf(_SC_NPROCESSORS_ONLN);
@@ -218,6 +236,9 @@ static void *worker(void *arg) {
     double acc[2] = {0.0, 0.0};
     for (int64_t j0 = 0; j0 < n; j0 += BLK) {
       const int64_t w = j0 + BLK < n ? BLK : n - j0;
+      if (g_skip != NULL && jb->mode != 2 && g_skip[(ia / BLK) * g_skip_nb + j0 / BLK] &&
+          g_skip[(ib / BLK) * g_skip_nb + j0 / BLK])
+        continue; /* both rows' blocks proved negligible (see picmf_set_skip) */
       double *oa = buf, *ob = buf + BLK;
       if (jb->cosine)
         pair_dot(jb->xp, xa, xb, jb->m, j0 / PW, (j0 + w + PW - 1) / PW, oa, ob);
@@ -298,3 +319,5 @@ void picmf_rows(const double *x, int64_t n, int32_t m, double sigma, int64_t lo,
 }
 
 double picmf_exp(double x) { return pic_exp(x); }
+
+int64_t picmf_block(void) { return BLK; }

@@ -46,6 +46,9 @@ def lib():
             f.restype = None
         L.picmf_exp.argtypes = [ctypes.c_double]
         L.picmf_exp.restype = ctypes.c_double
+        L.picmf_set_skip.argtypes = [ctypes.c_void_p, ctypes.c_int64]
+        L.picmf_set_skip.restype = None
+        L.picmf_block.restype = ctypes.c_int64
         _lib = L
     return _lib
 
@@ -89,6 +92,48 @@ def matvec(points, sigma, deg, v, lo: int = 0, hi: int | None = None) -> np.ndar
     lib().picmf_matvec(x.ctypes.data, x.shape[0], x.shape[1], _sig(sigma), lo, hi,
                        deg.ctypes.data, v.ctypes.data, out.ctypes.data)
     return out
+
+
+class negligible_blocks:
+    """Context manager: skip BLK x BLK block pairs (pic_mf.c picmf_set_skip)
+    whose every entry is proved below e^-``exponent`` (RBF only).
+
+    The proof is the projection on the line joining the two block centroids,
+    in fp64: for i in S, j in T, |x_i - x_j| >= (min_T u.x_j - max_S u.x_i) /
+    |u|, u = c_T - c_S, less a generous rounding allowance. Skipping leaves
+    every fp64 row sum bit-identical (see pic_mf.c), which
+    tests/test_oracle_mf.py checks against the unskipped pass.
+    """
+
+    def __init__(self, points, sigma, exponent: float = 70.0):
+        x = _x(points)
+        n = x.shape[0]
+        B = int(lib().picmf_block())
+        nb = -(-n // B)
+        cent = np.stack([x[S * B:(S + 1) * B].mean(axis=0) for S in range(nb)])
+        M = np.empty((nb, nb))  # M[S][T] = max_{i in S} x_i.(c_T - c_S)
+        for S in range(nb):
+            P = x[S * B:(S + 1) * B] @ cent.T
+            M[S] = (P - P[:, S:S + 1]).max(axis=0)
+        gap = -(M + M.T)
+        u = np.sqrt(((cent[:, None, :] - cent[None, :, :]) ** 2).sum(-1))
+        xm = float(np.sqrt((x * x).sum(1)).max())
+        cm = float(np.sqrt((cent * cent).sum(1)).max())
+        err = 8.0 * (x.shape[1] + 2) * 2.0 ** -53 * xm * cm
+        with np.errstate(divide="ignore", invalid="ignore"):
+            lb = (gap - err) / u * (1 - 1e-9)
+        skip = (u > 0) & (lb > 0) & (lb * lb / (2.0 * sigma * sigma) >= exponent)
+        np.fill_diagonal(skip, False)
+        self.skip = np.ascontiguousarray(skip, dtype=np.uint8)
+        self.nb = nb
+        self.fraction = float(skip.mean())
+
+    def __enter__(self):
+        lib().picmf_set_skip(self.skip.ctypes.data, self.nb)
+        return self
+
+    def __exit__(self, *exc):
+        lib().picmf_set_skip(None, 0)
 
 
 def power_trajectory(points, sigma, epsilon=None, max_iterations: int = 50, v0="degree",

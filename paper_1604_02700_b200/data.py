@@ -58,10 +58,17 @@ def check_labels(d: DataSet) -> None:
     if d.labels.shape != (d.n,):
         raise LabelLengthMismatch(d.n, int(d.labels.size))
     # np.unique(labels) == arange(k) without the O(n log n) sort: ids start
-    # at 0 and every id up to the maximum occurs
-    if d.labels.size and (d.labels.min() != 0 or
-                          not np.bincount(d.labels, minlength=int(d.labels.max()) + 1).all()):
-        raise DataError("class ids must be contiguous integers starting at 0")
+    # at 0 and every id up to the maximum occurs. Labels in ascending order
+    # (generator output, class-sorted files) satisfy it iff the first is 0
+    # and no step exceeds 1 — two vector passes instead of a histogram.
+    lab = d.labels
+    if lab.size:
+        if lab.size > 1:
+            step = np.diff(lab)
+            if lab[0] == 0 and step.min() >= 0 and step.max() <= 1:
+                return
+        if lab.min() != 0 or not np.bincount(lab, minlength=int(lab.max()) + 1).all():
+            raise DataError("class ids must be contiguous integers starting at 0")
 
 
 def validate_dataset(d: DataSet) -> DataSet:

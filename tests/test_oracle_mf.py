@@ -78,3 +78,20 @@ def test_config_fixture_degrees(golden, c):
         assert abs(deg - float(z["deg"][r])) <= 1e-12 * deg
     assert int(z["iterations"]) == len(z["deltas"])
     assert np.array_equal(np.sort(np.unique(z["labels"])), np.arange(int(z["k"])))
+
+
+def test_negligible_block_skip_is_bitwise_neutral():
+    """The n = 1M fixture's block skip (pic_mf.c picmf_set_skip): block pairs
+    proved below e^-70 are left out and every fp64 row sum stays bit-identical."""
+    from paper_1604_02700_b200 import gaussian_blobs
+
+    d = gaussian_blobs(8192, 24, 6, seed=3)
+    x, sigma = d.points, float(np.sqrt(24) / 2)
+    blocks = pm.negligible_blocks(x, sigma)
+    assert blocks.fraction > 0.2  # well-separated blobs: many pairs provable
+    deg = pm.degree(x, sigma)
+    v = np.random.default_rng(1).random(x.shape[0])
+    y = pm.matvec(x, sigma, deg, v)
+    with blocks:
+        assert np.array_equal(pm.degree(x, sigma), deg)
+        assert np.array_equal(pm.matvec(x, sigma, deg, v), y)
