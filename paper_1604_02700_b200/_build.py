@@ -46,16 +46,20 @@ def _stale(force: bool) -> bool:
     return newest > OUT.stat().st_mtime
 
 
-def build(force: bool = False, verbose: bool = False) -> pathlib.Path:
-    if not _stale(force):
+def build(force: bool = False, verbose: bool = False, out: pathlib.Path | None = None,
+          objdir: pathlib.Path | None = None) -> pathlib.Path:
+    target = out or OUT
+    if out is None and not _stale(force):
         return OUT
-    objdir = CSRC / "build"
+    objdir = objdir or CSRC / "build"
     objdir.mkdir(exist_ok=True)
     cc = nvcc()
 
     def compile_one(src: pathlib.Path):
         obj = objdir / (src.stem + ".o")
-        cmd = [cc, *ARCH, *NVCC_FLAGS, "-c", str(src), "-o", str(obj)]
+        # GPIC_NVCC_EXTRA: extra flags for measurement builds (e.g. -D knobs)
+        extra = os.environ.get("GPIC_NVCC_EXTRA", "").split()
+        cmd = [cc, *ARCH, *NVCC_FLAGS, *extra, "-c", str(src), "-o", str(obj)]
         res = subprocess.run(cmd, capture_output=True, text=True)
         if res.returncode != 0:
             raise RuntimeError(f"nvcc failed for {src.name}:\n{res.stderr}")
@@ -66,13 +70,13 @@ def build(force: bool = False, verbose: bool = False) -> pathlib.Path:
 
     with ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
         objs = list(ex.map(compile_one, sources()))
-    tmp = OUT.with_suffix(".so.tmp")
+    tmp = target.with_suffix(".so.tmp")
     cmd = [cc, *ARCH, "-shared", "-o", str(tmp), *map(str, objs), "-lcuda"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError(f"nvcc link failed:\n{res.stderr}")
-    os.replace(tmp, OUT)
-    return OUT
+    os.replace(tmp, target)
+    return target
 
 
 if __name__ == "__main__":

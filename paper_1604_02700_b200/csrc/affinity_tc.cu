@@ -90,20 +90,26 @@ constexpr int kChunkTiles = 32;              // matvec: column tiles per work it
 
 // rows per CTA block: 256 (two M blocks sharing every B stage) while the
 // operands fit, else 128
-__host__ __device__ constexpr int mblocks(int KB) { return KB == 1 ? 2 : 1; }
+// packed store modes: M blocks per unit at KB = 1 (GPIC_TC_PACKED_MB build knob)
+#ifndef GPIC_TC_PACKED_MB
+#define GPIC_TC_PACKED_MB 2
+#endif
+__host__ __device__ constexpr int mblocks(int KB, int MODE) {
+  return KB == 1 ? (is_packed(MODE) ? GPIC_TC_PACKED_MB : 2) : 1;
+}
 // norm block (prepare.cu): per 128-row tile, hi + lo planes of 128 x 16 fp16
 // (32-byte swizzle), one extra K = 16 step that adds -(s^2/2)(|x_i|^2+|x_j|^2)
 constexpr int kNrmPlane = 128 * 16 * 2;   // 4 KB
 constexpr int kNrmBytes = 2 * kNrmPlane;  // hi + lo
-__host__ __device__ constexpr int a_main_bytes(int KB) { return 2 * mblocks(KB) * KB * kTileBytes; }
-__host__ __device__ constexpr int a_bytes(int KB) { return a_main_bytes(KB) + mblocks(KB) * kNrmBytes; }
+__host__ __device__ constexpr int a_main_bytes(int KB, int MODE) { return 2 * mblocks(KB, MODE) * KB * kTileBytes; }
+__host__ __device__ constexpr int a_bytes(int KB, int MODE) { return a_main_bytes(KB, MODE) + mblocks(KB, MODE) * kNrmBytes; }
 constexpr int kStageBytes = 2 * kTileBytes + kNrmBytes;  // B hi, B lo, B norm block
 // store modes: one 4 KB staging buffer (a swizzled 32 x 32 fp32 box) per
 // epilogue warp, also used for the row-sum combine; matvec: a fp64
 // [warp][32 rows] combine scratch + the sym column-partial exchange
 // [tile parity][m][quadrant][128 columns] fp32
 constexpr int kStageOutBytes = 32 * 128;
-__host__ __device__ constexpr int colx_bytes(int KB) { return 2 * mblocks(KB) * 4 * 128 * 4; }
+__host__ __device__ constexpr int colx_bytes(int KB) { return 2 * mblocks(KB, kModeMatvec) * 4 * 128 * 4; }
 __host__ __device__ constexpr int out_bytes(int KB, int MODE) {
   return MODE == kModeMatvec ? kEpiWarps * 32 * 8 + colx_bytes(KB) : kEpiWarps * kStageOutBytes;
 }
@@ -112,13 +118,13 @@ __host__ __device__ constexpr int col_bytes(int MODE) {
   return MODE == kModeMatvec ? kEpiWarps * 2 * 64 * 4 : 0;
 }
 __host__ __device__ constexpr int stages_raw(int KB, int MODE) {
-  return (kSmemBudget - a_bytes(KB) - out_bytes(KB, MODE) - col_bytes(MODE)) / kStageBytes;
+  return (kSmemBudget - a_bytes(KB, MODE) - out_bytes(KB, MODE) - col_bytes(MODE)) / kStageBytes;
 }
 __host__ __device__ constexpr int stages(int KB, int MODE) {
   return stages_raw(KB, MODE) > 4 ? 4 : (stages_raw(KB, MODE) < 1 ? 1 : stages_raw(KB, MODE));
 }
 __host__ __device__ constexpr int smem_bytes(int KB, int MODE) {
-  return a_bytes(KB) + stages(KB, MODE) * kStageBytes + out_bytes(KB, MODE) + col_bytes(MODE) +
+  return a_bytes(KB, MODE) + stages(KB, MODE) * kStageBytes + out_bytes(KB, MODE) + col_bytes(MODE) +
          256 + 1024;
 }
 
@@ -382,7 +388,7 @@ __global__ void __launch_bounds__(kCtaThreads<MODE>, 1)
                        const __grid_constant__ CUtensorMap map_out,
                        const __grid_constant__ CUtensorMap map_nrm, const TcArgs args) {
   constexpr bool kNorm = KIND == GPIC_KIND_RBF;  // the distance comes out of the MMA
-  constexpr int MB = mblocks(KB);
+  constexpr int MB = mblocks(KB, MODE);
   constexpr int ST = stages(KB, MODE);
   constexpr int kTmemCols = 2 * MB * kBN;  // 2 accumulators
   if (MODE == kModeMatvec && args.ctl != nullptr && *(volatile const int32_t*)&args.ctl->stop)
@@ -390,8 +396,8 @@ __global__ void __launch_bounds__(kCtaThreads<MODE>, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* base = smem_align<1024>(smem_raw);
   uint8_t* sA = base;                                     // [hl][m][kb] 16 KB tiles
-  uint8_t* sAn = sA + a_main_bytes(KB);                   // [m][hl] 4 KB norm planes
-  uint8_t* sB = sA + a_bytes(KB);                         // [stage]{hi, lo, norm hi, norm lo}
+  uint8_t* sAn = sA + a_main_bytes(KB, MODE);                   // [m][hl] 4 KB norm planes
+  uint8_t* sB = sA + a_bytes(KB, MODE);                         // [stage]{hi, lo, norm hi, norm lo}
   uint8_t* sOut = sB + ST * kStageBytes;                  // [epi warp] staging / combine
   float* sCol = reinterpret_cast<float*>(sOut + out_bytes(KB, MODE));  // matvec: [warp][buf][v][64]
   uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sCol) + col_bytes(MODE));
@@ -481,7 +487,7 @@ __global__ void __launch_bounds__(kCtaThreads<MODE>, 1)
         if (c.rb != cur_rb) {
           mbar_wait_sleep(a_empty, a_par);
           a_par ^= 1;
-          mbar_expect_tx(a_full, kNorm ? a_bytes(KB) : a_main_bytes(KB));
+          mbar_expect_tx(a_full, kNorm ? a_bytes(KB, MODE) : a_main_bytes(KB, MODE));
           for (int hl = 0; hl < 2; ++hl)
             for (int m = 0; m < MB; ++m) {
               const int row0 = (int)(args.row_lo + (c.rb * MB + m) * 128);
@@ -644,6 +650,10 @@ __global__ void __launch_bounds__(kCtaThreads<MODE>, 1)
       const int tI = rb * MB + m;  // tile row of this warp's rows
       // packed: the lower-triangle half of a diagonal row block is not stored
       const bool store_ok = !is_packed(MODE) || tI <= cb;
+      // packed: this warp's tile, global (flags) and shard-relative (values,
+      // degree partials) — once per unit, not per chunk
+      const int64_t tg = is_packed(MODE) && store_ok ? tile_index(tI, cb, args.n_ctiles) : 0;
+      const int64_t tl = tg - args.tile_base;
       // matvec sym: row partials from tiles J >= I, column partials from J > I
       const bool row_ok = MODE != kModeMatvec || !args.sym || tI <= cb;
       const bool col_ok = MODE == kModeMatvec && args.sym && tI < cb;
@@ -714,9 +724,9 @@ __global__ void __launch_bounds__(kCtaThreads<MODE>, 1)
             } else {
               if (args.boxnz != nullptr) {
                 if (lane == 0 && store_ok)
-                  args.boxnz[tile_index(tI, cb, args.n_ctiles) * 16 + q * 4 + ch] = 0;
+                  args.boxnz[tg * 16 + q * 4 + ch] = 0;
                 if (store_ok && tI != cb)
-                  args.degcol[((tile_index(tI, cb, args.n_ctiles) - args.tile_base) * 4 + q) * 128 +
+                  args.degcol[(tl * 4 + q) * 128 +
                               ch * 32 + lane] = 0.f;
                 return;
               }
@@ -808,7 +818,7 @@ __global__ void __launch_bounds__(kCtaThreads<MODE>, 1)
             for (int x = 0; x < 32; ++x) any |= vals[x] != 0.f;
             box_nz = __any_sync(0xffffffffu, any);
             if (lane == 0 && store_ok)
-              args.boxnz[tile_index(tI, cb, args.n_ctiles) * 16 + q * 4 + ch] = box_nz ? 1 : 0;
+              args.boxnz[tg * 16 + q * 4 + ch] = box_nz ? 1 : 0;
           }
           // full 32-byte sectors straight from registers: each quad writes 8
           // consecutive floats of one row per (block, row)
@@ -855,7 +865,7 @@ __global__ void __launch_bounds__(kCtaThreads<MODE>, 1)
           __syncwarp();
           if (lane == 0 && store_ok) {
             const int64_t out_row0 = is_packed(MODE)
-                                         ? (tile_index(tI, cb, args.n_ctiles) - args.tile_base) * 128 + q * 32
+                                         ? tl * 128 + q * 32
                                          : lr0;
             if (args.store_hint)
               tma_store_2d(&map_out, is_packed(MODE) ? ch * 32 : (int)col0, (int)out_row0, stage,
@@ -896,7 +906,7 @@ __global__ void __launch_bounds__(kCtaThreads<MODE>, 1)
             }
             const int k = (b4 ? 4 : 0) + (b3 ? 2 : 0) + (b2 ? 1 : 0);  // = tq
             const int col = 8 * (k >> 1) + tc + (k & 1);
-            args.degcol[((tile_index(tI, cb, args.n_ctiles) - args.tile_base) * 4 + q) * 128 + ch * 32 + col] = cs[0];
+            args.degcol[(tl * 4 + q) * 128 + ch * 32 + col] = cs[0];
           }
         }
       };
@@ -1011,7 +1021,7 @@ __global__ void __launch_bounds__(kCtaThreads<MODE>, 1)
           for (int rr = 0; rr < 4; ++rr) {
             const int rloc = (rr >> 1) * 16 + tq + (rr & 1) * 8;  // row within the warp's 32
             if constexpr (is_packed(MODE)) {
-              args.degrow[(tile_index(tI, cb, args.n_ctiles) - args.tile_base) * 128 + q * 32 + rloc] = tot[rr];
+              args.degrow[tl * 128 + q * 32 + rloc] = tot[rr];
             } else {
               const int64_t lrow = lr0 + rloc;
               if (lrow < args.rows) args.rowpart[cb * args.rows_pad + lrow] = tot[rr];
@@ -1063,7 +1073,7 @@ int g_num_sms = 0;
 template <int KB, int MODE>
 int launch_kb(const CUtensorMap& mh, const CUtensorMap& ml, const CUtensorMap& mo,
               const CUtensorMap& mn, const TcArgs& a0, cudaStream_t s) {
-  constexpr int MB = mblocks(KB);
+  constexpr int MB = mblocks(KB, MODE);
   if (!tc_supports_pitch(KB * kKBlk, MODE == kModeMatvec))
     return fail(GPIC_E_UNSUPPORTED,
                 "tcgen05 affinity engine: d too wide for this storage mode (SIMT engine: any d)");
@@ -1240,14 +1250,15 @@ int64_t mf_parts(int64_t n, int32_t dp) {
   return chunks;  // one fp64 partial per (chunk item, row): the row's warps combine in-CTA
 }
 
-int mf_rows_per_block(int32_t dp) { return 128 * mblocks(dp / kKBlk); }
+int mf_rows_per_block(int32_t dp) { return 128 * mblocks(dp / kKBlk, kModeMatvec); }
 
-int tc_mblocks(int32_t dp) { return mblocks(dp / kKBlk); }
+int tc_mblocks(int32_t dp) { return mblocks(dp / kKBlk, kModePacked); }
+int tc_mblocks_mf(int32_t dp) { return mblocks(dp / kKBlk, kModeMatvec); }
 
 // sym column-partial records: one per (row block of 128 * MB rows, column
 // tile J >= MB * row block)
 int64_t mf_colpart_floats(int64_t n, int32_t dp) {
-  const int mb = mblocks(dp / kKBlk);
+  const int mb = mblocks(dp / kKBlk, kModeMatvec);
   return packed_items(ceil_div(n, 128 * mb), ceil_div(n, kBN), mb) * 128;
 }
 

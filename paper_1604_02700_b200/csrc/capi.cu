@@ -465,7 +465,7 @@ int gpic_cluster_pruned_work(const void* d_work, int64_t n, int32_t d, int32_t k
   if (rc) return rc;
   const int32_t dp = feature_pitch(d);
   const PruneMask pm = carve_prune(ws.prune, n, dp);
-  const int64_t mb = tc_mblocks(dp);
+  const int64_t mb = storage == GPIC_STORAGE_NONE ? tc_mblocks_mf(dp) : tc_mblocks(dp);
   const int64_t nrt = ceil_div(n, 128 * mb), nct = ceil_div(n, 128);
   *total = nrt * nct - mb * nrt * (nrt - 1) / 2;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -506,7 +506,7 @@ int gpic_mf_shard_build(const float* d_xhi, const float* d_xlo, const float* d_s
   op.share_n = nranks;
   const double* colpart = d_prep_work;  // gpic_prepare_points: column sums, then the mean
   const double* mean = d_prep_work + ceil_div(n, 256) * d;
-  launch_prune(op.prune, d_xlo, colpart, mean, n, d, dp, sigma, -tc_mblocks(dp), 0, s);
+  launch_prune(op.prune, d_xlo, colpart, mean, n, d, dp, sigma, -tc_mblocks_mf(dp), 0, s);
   float* ones = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ypart) +
                                          round_up(mf_ypart_doubles(n, dp, n) * 8, 256) +
                                          round_up(prune_bytes(n, dp), 256));
@@ -782,7 +782,7 @@ int cluster_impl(const double* d_x, int64_t n, int32_t d, double sigma, int32_t 
     if (L.mf.sym && kind == GPIC_KIND_RBF && d > 8 && impl == GPIC_AFFINITY_TC &&
         sparse_enabled() && prune_enabled()) {
       L.mf.prune = carve_prune(ws.prune, n, dp);
-      launch_prune(L.mf.prune, ws.xlo, ws.colpart, ws.mean, n, d, dp, sigma, -tc_mblocks(dp), 0, s);
+      launch_prune(L.mf.prune, ws.xlo, ws.colpart, ws.mean, n, d, dp, sigma, -tc_mblocks_mf(dp), 0, s);
       L.mf.pruned = 1;
     }
     L.ypart = ypart;

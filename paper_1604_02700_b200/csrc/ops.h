@@ -58,7 +58,8 @@ int launch_affinity_tc_packed(const float* xhi, const float* xlo, const float* s
                               uint8_t* boxnz = nullptr, const int32_t* unit_list = nullptr,
                               const int64_t* unit_count = nullptr);
 // M blocks (128-row tiles) per tcgen05 work unit at feature pitch dp
-int tc_mblocks(int32_t dp);
+int tc_mblocks(int32_t dp);     // packed store modes
+int tc_mblocks_mf(int32_t dp);  // the matrix-free pass
 // boxnz non-null: tiles without a stored box contribute zero (not read);
 // pm non-null: pruned block pairs are not even looked at (prune.cu)
 struct PruneMask;
