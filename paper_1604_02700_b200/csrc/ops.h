@@ -256,6 +256,9 @@ struct SbList {
   const int32_t* list;
   const int64_t* lpre;
   const int64_t* count;
+  // ranges[0] = the grid they were cut for, ranges[1 + b] = first entry of
+  // CTA b (ranges[1 + grid] = count)
+  const int64_t* ranges = nullptr;
 };
 SbList sb_list(const int64_t* sb_prefix, int64_t n);
 SparseMask carve_sparse(void* base, int64_t n, int32_t d);

@@ -30,6 +30,16 @@ namespace {
 
 constexpr int kT = 128;  // rows per tile
 constexpr int kSB = 4;   // tiles per super-block side (sym.cu)
+constexpr int kMaxGrid = 1024;  // GEMV CTAs the precomputed ranges cover
+// host copies of the grid sizes (a stable source for the async H2D copy)
+struct GridWords {
+  int64_t v[kMaxGrid + 1];
+  constexpr GridWords() : v() {
+    for (int i = 0; i <= kMaxGrid; ++i) v[i] = i;
+  }
+  const int64_t& operator[](int i) const { return v[i]; }
+};
+constexpr GridWords kGridWords{};
 constexpr int kScanThreads = 1024;
 
 __device__ __forceinline__ bool tile_stored(const uint8_t* boxnz, int64_t t) {
@@ -109,7 +119,8 @@ __global__ void __launch_bounds__(kScanThreads)
 // weights of) the ~80 % empty ones. One CTA, contiguous segments.
 __global__ void __launch_bounds__(kScanThreads)
     sb_list_kernel(int64_t nt, const int64_t* __restrict__ prefix, int32_t* __restrict__ list,
-                   int64_t* __restrict__ lpre, int64_t* __restrict__ count) {
+                   int64_t* __restrict__ lpre, int64_t* __restrict__ count, int grid,
+                   int64_t* __restrict__ ranges) {
   __shared__ int64_t sh[kScanThreads];
   const int64_t ns = (nt + kSB - 1) / kSB;
   const int64_t total = ns * (ns + 1) / 2;
@@ -137,6 +148,27 @@ __global__ void __launch_bounds__(kScanThreads)
     *count = sh[t];
     lpre[sh[t]] = prefix[total];
   }
+  // the GEMV's CTA ranges over the list for a grid of `grid` CTAs (equal
+  // shares of weight, the kernel's own lower_bound), so its CTAs start
+  // without a search: ranges[b] .. ranges[b + 1]
+  __syncthreads();
+  const int64_t cnt = sh[kScanThreads - 1];
+  const int64_t w0 = lpre[0], W = lpre[cnt] - w0;
+  for (int b = t; b <= grid; b += kScanThreads) {
+    int64_t e;
+    if (b == grid) {
+      e = cnt;
+    } else {
+      const int64_t target = w0 + W * b / grid;
+      int64_t lo = 0, hi = cnt;
+      while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (lpre[mid] >= target) hi = mid; else lo = mid + 1;
+      }
+      e = lo;
+    }
+    ranges[b] = e;
+  }
 }
 
 __global__ void fill_kernel(uint8_t* p, int64_t n, uint8_t v) {
@@ -157,7 +189,7 @@ int64_t sparse_mask_bytes(int64_t n, int32_t /*d*/) {
   auto al = [](int64_t b) { return (b + 255) & ~int64_t(255); };
   const int64_t nsb = ns * (ns + 1) / 2;
   return al(nt * (nt + 1) / 2 * 16) + al((nsb + 1) * 8) + al(nsb * kSB * kSB * 2) + al(8) +
-         al((nsb + 1) * 8) + al(nsb * 4);
+         al((nsb + 1) * 8) + al(nsb * 4) + al((kMaxGrid + 2) * 8);
 }
 
 // the non-empty super-block list behind the box bits (sb_list_kernel)
@@ -173,6 +205,8 @@ SbList sb_list(const int64_t* sb_prefix, int64_t n) {
   L.lpre = reinterpret_cast<const int64_t*>(p);
   p += al((nsb + 1) * 8);
   L.list = reinterpret_cast<const int32_t*>(p);
+  p += al(nsb * 4);
+  L.ranges = reinterpret_cast<const int64_t*>(p);  // [0] = grid, then grid + 1 bounds
   return L;
 }
 
@@ -203,9 +237,18 @@ void launch_sparse_prefix(const SparseMask& m, cudaStream_t s) {
       m.boxnz, m.nt, m.sb_prefix, const_cast<uint16_t*>(sb_bits(m.sb_prefix, m.nt * kT)));
   sb_scan_kernel<<<1, kScanThreads, 0, s>>>(m.nt, m.sb_prefix);
   const SbList L = sb_list(m.sb_prefix, m.nt * kT);
+  static int sms = 0;
+  if (sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const int grid = sms < kMaxGrid ? sms : kMaxGrid;
+  int64_t* ranges = const_cast<int64_t*>(L.ranges);
+  cudaMemcpyAsync(ranges, &kGridWords[grid], 8, cudaMemcpyHostToDevice, s);
   sb_list_kernel<<<1, kScanThreads, 0, s>>>(m.nt, m.sb_prefix, const_cast<int32_t*>(L.list),
                                             const_cast<int64_t*>(L.lpre),
-                                            const_cast<int64_t*>(L.count));
+                                            const_cast<int64_t*>(L.count), grid, ranges + 1);
   count_launch(3);
 }
 

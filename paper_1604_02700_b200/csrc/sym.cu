@@ -91,6 +91,7 @@ struct Sparse {
   const int32_t* list;   // non-empty super-blocks (sb_list), or null: walk the id range
   const int64_t* lpre;
   const int64_t* lcount;
+  const int64_t* ranges;  // precomputed CTA ranges over the list (sb_list), or null
   // the 16 tile masks of super-block s (two 16-byte loads), kept in
   // registers: selected by comparisons, never indexed (an indexed array
   // went to local memory)
@@ -301,13 +302,20 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int64_t sb_lo = sr.sb_lo(ns), total = sr.sb_hi(ns) - sb_lo;
   SbCursor cur0;
   if (sp.list != nullptr) {
-    // the non-empty super-blocks only, equal shares of their weight
-    const int64_t cnt = *sp.lcount;
-    const int64_t w0 = sp.lpre[0], W = sp.lpre[cnt] - w0;
-    const int64_t e0 = lower_bound64(sp.lpre, 0, cnt, w0 + W * blockIdx.x / gridDim.x);
-    const int64_t e1 = blockIdx.x + 1 == gridDim.x
-                           ? cnt
-                           : lower_bound64(sp.lpre, 0, cnt, w0 + W * (blockIdx.x + 1) / gridDim.x);
+    // the non-empty super-blocks only, equal shares of their weight (cut
+    // in advance by sb_list_kernel when it used this grid size)
+    int64_t e0, e1;
+    if (sp.ranges != nullptr && sp.ranges[0] == gridDim.x) {
+      e0 = sp.ranges[1 + blockIdx.x];
+      e1 = sp.ranges[2 + blockIdx.x];
+    } else {
+      const int64_t cnt = *sp.lcount;
+      const int64_t w0 = sp.lpre[0], W = sp.lpre[cnt] - w0;
+      e0 = lower_bound64(sp.lpre, 0, cnt, w0 + W * blockIdx.x / gridDim.x);
+      e1 = blockIdx.x + 1 == gridDim.x
+               ? cnt
+               : lower_bound64(sp.lpre, 0, cnt, w0 + W * (blockIdx.x + 1) / gridDim.x);
+    }
     if (e0 >= e1) return;
     cur0.begin_list(sp.list, e0, e1, ns);
   } else {
@@ -723,7 +731,7 @@ void launch_sym_degree(const float* degrow, const float* degcol, int64_t n, int 
   const int64_t nt = ceil_div(n, kTS);
   const int64_t rows = nt - kSB * sr.p_lo;  // tile rows that can receive partials
   if (rows < 1) return;
-  const Sparse sp{boxnz, nullptr, nullptr, 0, 0, 0, nullptr, nullptr, nullptr};
+  const Sparse sp{boxnz, nullptr, nullptr, 0, 0, 0, nullptr, nullptr, nullptr, nullptr};
   const size_t dyn = boxnz != nullptr ? (size_t)nt * 4 : 0;  // the live-tile list
   if (dyn > 48 * 1024)
     cudaFuncSetAttribute(sym_degree_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
@@ -766,7 +774,8 @@ void launch_sym_gemv(const float* tiles, int64_t n, const float* v32, float* row
                                                                   : SbList{nullptr, nullptr, nullptr};
   const Sparse sp{boxnz, boxnz != nullptr ? sb_prefix : nullptr,
                   boxnz != nullptr && whole && bits_mode != 0 ? sb_bits(sb_prefix, n) : nullptr,
-                  gemv_prefetch(), bits_mode == 1, gemv_evict_first(), sl.list, sl.lpre, sl.count};
+                  gemv_prefetch(), bits_mode == 1, gemv_evict_first(), sl.list, sl.lpre, sl.count,
+                  sl.ranges};
   sym_prepare();
   const int64_t nt = ceil_div(n, kTS);
   const int64_t ns = (nt + kSB - 1) / kSB;
@@ -786,7 +795,7 @@ void launch_sym_gemv16(const void* tiles, int64_t n, const float* v32, float* ro
                                                         : SbList{nullptr, nullptr, nullptr};
   const Sparse sp{boxnz, boxnz != nullptr ? sb_prefix : nullptr,
                   boxnz != nullptr ? sb_bits(sb_prefix, n) : nullptr, gemv_prefetch(), 0,
-                  gemv_evict_first(), sl.list, sl.lpre, sl.count};
+                  gemv_evict_first(), sl.list, sl.lpre, sl.count, sl.ranges};
   sym_prepare();
   const int64_t nt = ceil_div(n, kTS);
   const int64_t ns = (nt + kSB - 1) / kSB;
