@@ -282,6 +282,13 @@ int gpic_cluster_workspace_layout(int64_t n, int32_t d, int32_t k, int32_t max_i
 int gpic_cluster_pruned_work(const void* d_work, int64_t n, int32_t d, int32_t k,
                              int32_t max_iter, int32_t storage, int64_t* kept, int64_t* total,
                              void* stream);
+/* The locality order of the last gpic_cluster run on this workspace
+ * (randomly ordered inputs are permuted so that block sparsity and tile
+ * pruning apply; v is scattered back): *reordered = 1 and d_perm[p] (n
+ * int32) = the caller's index of permuted position p, or *reordered = 0.
+ * Measurement / tests. Synchronizes `stream`. */
+int gpic_cluster_permutation(const void* d_work, int64_t n, int32_t d, int32_t k, int32_t max_iter,
+                             int32_t* d_perm, int32_t* reordered, void* stream);
 /* One matrix-free pass y = A v (no 1/deg) on the operands, pruning mask
  * (pruned != 0) and partial buffers that a GPIC_STORAGE_NONE gpic_cluster
  * run left in d_work — the power loop's own pass, for kernel timing. */

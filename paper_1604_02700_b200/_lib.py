@@ -105,6 +105,7 @@ SIGNATURES = {
     "gpic_cluster_workspace_layout": (C.c_int, [I64, I32, I32, I32, I32, P]),
     "gpic_cluster_pruned_work": (C.c_int, [P, I64, I32, I32, I32, I32, P, P, P]),
     "gpic_mf_shard_scratch_bytes": (I64, [I64, I32]),
+    "gpic_cluster_permutation": (C.c_int, [P, I64, I32, I32, I32, P, P, P]),
     "gpic_mf_shard_build": (C.c_int, [P, P, P, P, I64, I32, C.c_double, I32, I32, P, P, P]),
     "gpic_cluster_mf_pass": (C.c_int, [P, I64, I32, I32, I32, C.c_double, I32, I32, P, P, P]),
     "gpic_sym_partial_floats": (I64, [I64]),

@@ -66,6 +66,7 @@ int64_t workspace_bytes(int64_t n, int32_t d, int32_t k, int64_t rows, int32_t /
   b += al(n * 8) + al(8);                     // low-degree row list + count
   b += al(sparse_mask_bytes(n, d));           // block-sparsity mask (sparse.cu)
   b += al(prune_bytes(n, dp));                // provably-zero block pairs (prune.cu)
+  b += al(locality_bytes(n, d));              // locality order (locality.cu)
   return b;
 }
 
@@ -99,6 +100,7 @@ int carve(void* base, int64_t bytes, int64_t n, int32_t d, int32_t k, int64_t ro
   ws->lowcount = reinterpret_cast<unsigned long long*>(take(8));
   ws->sparse = take(sparse_mask_bytes(n, d));
   ws->prune = take(prune_bytes(n, dp));
+  ws->locality = take(locality_bytes(n, d));
   ws->end = p;
   return GPIC_OK;
 }
@@ -452,6 +454,28 @@ int gpic_cluster_mf_pass(void* d_work, int64_t n, int32_t d, int32_t k, int32_t 
                           static_cast<cudaStream_t>(stream));
 }
 
+// The locality permutation of the last gpic_cluster run on this workspace
+// (locality.cu): *reordered = 1 and perm[p] = original index of position p,
+// or *reordered = 0 (the input order was kept). Synchronizes `stream`.
+int gpic_cluster_permutation(const void* d_work, int64_t n, int32_t d, int32_t k, int32_t max_iter,
+                             int32_t* d_perm, int32_t* reordered, void* stream) {
+  if (n < 1 || d < 1 || !reordered) return fail(GPIC_E_INVALID, "bad query");
+  Workspace ws;
+  int rc = carve(const_cast<void*>(d_work), workspace_bytes(n, d, k, n, max_iter), n, d, k, n,
+                 max_iter, &ws);
+  if (rc) return rc;
+  const Locality loc = carve_locality(ws.locality, n, d);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  double flag = 0.0;
+  GPIC_CUDA_TRY(cudaMemcpyAsync(&flag, loc.metric + 2, 8, cudaMemcpyDeviceToHost, s));
+  GPIC_CUDA_TRY(cudaStreamSynchronize(s));
+  *reordered = flag == 1.0;
+  if (*reordered && d_perm)
+    GPIC_CUDA_TRY(cudaMemcpyAsync(d_perm, loc.perm, n * 4, cudaMemcpyDeviceToDevice, s));
+  GPIC_CUDA_TRY(cudaStreamSynchronize(s));
+  return GPIC_OK;
+}
+
 // Work the tensor engine did in a gpic_cluster run after tile pruning:
 // packed storages -> kept / all work units (128 MB x 128 tiles); matrix-free
 // -> kept / all tile units of one sym pass. Synchronizes `stream`.
@@ -718,15 +742,39 @@ int cluster_impl(const double* d_x, int64_t n, int32_t d, double sigma, int32_t 
   mark(ev, 0, s);
   launch_ctl_init(ws.ctl, eps, max_iter, s);
   launch_prepare(d_x, n, d, ws.xhi, ws.xlo, ws.sqn, ws.colpart, ws.mean, ws.ctl, s, kind);
+  const int32_t dp = feature_pitch(d);
+  // locality order (locality.cu): randomly ordered inputs are permuted so
+  // that block sparsity and tile pruning apply; the metric is read at the
+  // engine-routing sync below
+  const Locality loc = carve_locality(ws.locality, n, d);
+  const bool packed_any = storage == GPIC_STORAGE_PACKED || storage == GPIC_STORAGE_PACKED16;
+  const bool may_reorder = kind == GPIC_KIND_RBF && impl == GPIC_AFFINITY_TC && packed_any &&
+                           n >= 16384 && locality_enabled() && sparse_enabled() && prune_enabled();
+  if (may_reorder) launch_order_metric(loc, ws.xlo, n, dp, s);
+  GPIC_CUDA_TRY(cudaMemsetAsync(loc.metric + 2, 0, 8, s));
+  bool reordered = false;
+  const double* x_run = d_x;  // the points the run works on (permuted when reordered)
   if (kind == GPIC_KIND_RBF && impl == GPIC_AFFINITY_TC && storage != GPIC_STORAGE_NONE) {
     // data-driven engine choice: the spread R^2 from the prepare pass
-    double spread2 = 0.0;
+    double spread2 = 0.0, metric[2] = {0.0, 0.0};
     GPIC_CUDA_TRY(cudaMemcpyAsync(&spread2, ws.mean + d + 1, 8, cudaMemcpyDeviceToHost, s));
+    if (may_reorder) GPIC_CUDA_TRY(cudaMemcpyAsync(metric, loc.metric, 16, cudaMemcpyDeviceToHost, s));
     GPIC_CUDA_TRY(cudaStreamSynchronize(s));
     effective_engine(kind, d, &impl, &storage, spread2, sigma);
+    // index neighbours about as far apart as random pairs (E|x_i - x_j|^2 =
+    // 2 E|x|^2 for centred data): reorder; cluster-ordered data sit near 0
+    if (may_reorder && impl == GPIC_AFFINITY_TC &&
+        (locality_forced() || metric[0] > 1.0 * metric[1])) {
+      int rc2 = launch_locality_order(loc, ws.xlo, d_x, n, d, dp, s);
+      if (rc2) return rc2;
+      x_run = loc.xp;
+      reordered = true;
+      static const double one = 1.0;  // recorded for gpic_cluster_permutation
+      GPIC_CUDA_TRY(cudaMemcpyAsync(loc.metric + 2, &one, 8, cudaMemcpyHostToDevice, s));
+      launch_prepare(x_run, n, d, ws.xhi, ws.xlo, ws.sqn, ws.colpart, ws.mean, ws.ctl, s, kind);
+    }
   }
   const float neg_scale_log2 = (float)(-1.4426950408889634 / (2.0 * sigma * sigma));
-  const int32_t dp = feature_pitch(d);
   const int64_t lda = affinity_pitch(n);
   ShardLoop L;
   std::memset(&L, 0, sizeof L);
@@ -806,7 +854,7 @@ int cluster_impl(const double* d_x, int64_t n, int32_t d, double sigma, int32_t 
   // in fp64 from X; ZeroDegree only when the fp64 degree is 0 (lowdeg.cu)
   launch_lowdeg_scan(deg, n, kind, ws.lowlist, ws.lowcount, s);
   LowRows low;
-  low.x = d_x;
+  low.x = x_run;
   low.n = n;
   low.d = d;
   low.kind = kind;
@@ -844,7 +892,12 @@ int cluster_impl(const double* d_x, int64_t n, int32_t d, double sigma, int32_t 
   L.low_deg = deg;
   rc = run_power_loops(&L, 1, n, max_iter, s);
   if (rc) return rc;
-  launch_copy_result(ws.v64, n, d_v, ws.ctl, s);
+  if (reordered) {  // back to the caller's order before the k-means
+    launch_copy_result(ws.v64, n, ws.y, ws.ctl, s);
+    launch_unpermute(ws.y, loc.perm, n, d_v, s);
+  } else {
+    launch_copy_result(ws.v64, n, d_v, ws.ctl, s);
+  }
   mark(ev, 3, s);
   GPIC_CUDA_TRY(cudaGetLastError());
   // k-means needs the status of the loop: read the control block once.

@@ -88,6 +88,7 @@ struct Workspace {
   unsigned long long* lowcount;
   uint8_t* sparse;     // SparseMask storage (sparse.cu)
   uint8_t* prune;      // PruneMask storage (prune.cu)
+  uint8_t* locality;   // Locality storage (locality.cu)
   int64_t kscratch_bytes;
   uint8_t* end;
 };
@@ -268,6 +269,31 @@ void launch_sparse_prefix(const SparseMask& m, cudaStream_t s);
 void launch_box_fill(const SparseMask& m, uint8_t v, cudaStream_t s);
 // GPIC_SPARSE=0 turns the zero-box skipping off (dense packed runs, for comparisons)
 bool sparse_enabled();
+
+// ---- locality order (locality.cu) -----------------------------------------
+// Points of a randomly ordered input permuted so that index neighbours are
+// space neighbours (seed Voronoi cells, ordered by super-seed); the run
+// proceeds on xp and v is scattered back through perm.
+struct Locality {
+  double* xp = nullptr;      // n x d fp64, the permuted points
+  int32_t* perm = nullptr;   // perm[p] = original index at position p
+  int32_t *cell = nullptr, *keys = nullptr, *keys_out = nullptr, *iota = nullptr;
+  int32_t *seed_idx = nullptr, *super_idx = nullptr, *seed_super = nullptr, *rank = nullptr;
+  int32_t* super_pos = nullptr;  // chain position of each super-seed
+  float* snorm = nullptr;
+  double* metric = nullptr;  // [0] sum |x_i - x_(i+1)|^2, [1] sum |x_i|^2 (sampled)
+  void* tmp = nullptr;
+  size_t tmp_bytes = 0;
+  int64_t m = 0;
+};
+int64_t locality_bytes(int64_t n, int32_t d);
+Locality carve_locality(void* base, int64_t n, int32_t d);
+bool locality_enabled();  // GPIC_REORDER=0: never; 2: always (tests)
+bool locality_forced();
+void launch_order_metric(const Locality& L, const float* xc, int64_t n, int32_t dp, cudaStream_t s);
+int launch_locality_order(const Locality& L, const float* xc, const double* x, int64_t n, int32_t d,
+                          int32_t dp, cudaStream_t s);
+void launch_unpermute(const double* v, const int32_t* perm, int64_t n, double* out, cudaStream_t s);
 
 // ---- low-degree (isolated) rows, lowdeg.cu -----------------------------
 // Rows whose engine degree is below low_degree_threshold(kind): recomputed

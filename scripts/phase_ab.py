@@ -12,6 +12,10 @@ cfg = int(os.environ.get("CFG", "3"))
 storage = os.environ.get("STORAGE", "packed")
 c = CONFIGS[cfg]
 d = config_dataset(cfg, 0)
+if os.environ.get("SHUFFLE") == "1":  # the same points in random order
+    from paper_1604_02700_b200 import DataSet
+    import numpy as np
+    d = DataSet(d.points[np.random.default_rng(5).permutation(d.n)])
 for variant in sys.argv[1:] or ["NONE=0"]:
     for kv in variant.split(","):
         key, val = kv.split("=")
