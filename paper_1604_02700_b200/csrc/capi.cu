@@ -748,13 +748,16 @@ int cluster_impl(const double* d_x, int64_t n, int32_t d, double sigma, int32_t 
   // engine-routing sync below
   const Locality loc = carve_locality(ws.locality, n, d);
   const bool packed_any = storage == GPIC_STORAGE_PACKED || storage == GPIC_STORAGE_PACKED16;
-  const bool may_reorder = kind == GPIC_KIND_RBF && impl == GPIC_AFFINITY_TC && packed_any &&
+  // packed storage, or the pruned matrix-free symmetric pass (d > 8)
+  const bool prunable = packed_any || (storage == GPIC_STORAGE_NONE && d > 8 && mf_sym_default());
+  const bool may_reorder = kind == GPIC_KIND_RBF && impl == GPIC_AFFINITY_TC && prunable &&
                            n >= 16384 && locality_enabled() && sparse_enabled() && prune_enabled();
   if (may_reorder) launch_order_metric(loc, ws.xlo, n, dp, s);
   GPIC_CUDA_TRY(cudaMemsetAsync(loc.metric + 2, 0, 8, s));
   bool reordered = false;
   const double* x_run = d_x;  // the points the run works on (permuted when reordered)
-  if (kind == GPIC_KIND_RBF && impl == GPIC_AFFINITY_TC && storage != GPIC_STORAGE_NONE) {
+  if (kind == GPIC_KIND_RBF && impl == GPIC_AFFINITY_TC &&
+      (storage != GPIC_STORAGE_NONE || may_reorder)) {
     // data-driven engine choice: the spread R^2 from the prepare pass
     double spread2 = 0.0, metric[2] = {0.0, 0.0};
     GPIC_CUDA_TRY(cudaMemcpyAsync(&spread2, ws.mean + d + 1, 8, cudaMemcpyDeviceToHost, s));

@@ -40,7 +40,7 @@ def test_shuffled_config2_matches_cpu_reference():
     assert rel_l1(v3, z["v_T3"][perm]) <= 1e-4
 
 
-@pytest.mark.parametrize("storage", ["packed", "packed16"])
+@pytest.mark.parametrize("storage", ["packed", "packed16", "none"])
 def test_shuffled_equals_ordered_run(storage):
     d = gaussian_blobs(30000, 32, 6, seed=2)
     sh, perm = _shuffled(d, 3)
