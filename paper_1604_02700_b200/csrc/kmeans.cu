@@ -908,7 +908,6 @@ int launch_stages(const KProblem& one, const KProblem* many, int grid, int k, in
 
 int64_t kmeans_scratch_bytes(int64_t n, int32_t k) {
   const int64_t small = scratch_size(n, kMaxK);
-  if (k <= kMaxK) return small;
   const int64_t big = kmeans_big_scratch_bytes(n, k);  // 64 < k: kmeans_big.cu
   return big > small ? big : small;
 }
@@ -919,7 +918,10 @@ int launch_kmeans1d(const double* v, int64_t n, int32_t k, int64_t first_index,
   if (k > n) return fail(GPIC_E_K_TOO_LARGE, "k exceeds the number of points");
   if (k < 2) return fail(GPIC_E_INVALID, "k must be at least 2");
   if (first_index < 0 || first_index >= n) return fail(GPIC_E_INVALID, "first_index out of range");
-  if (k > kMaxK)  // many clusters: the sorted-domain variant (kmeans_big.cu)
+  // many clusters: the sorted-domain variant (kmeans_big.cu); GPIC_KMEANS_SORTED=1
+  // routes every k there (measurement)
+  const char* srt = getenv("GPIC_KMEANS_SORTED");
+  if (k > kMaxK || (srt != nullptr && atoi(srt) != 0))
     return launch_kmeans1d_big(v, n, k, first_index, h_uniforms, max_rounds, tol, labels, scratch,
                                ctl, st);
   KProblem p;
