@@ -711,13 +711,20 @@ __global__ void __launch_bounds__(kCtaThreads<MODE>, 1)
             vcol[2 * b2 + 1] = v2.y;
           }
         }
+        // RBF, stored-tile / matrix-free modes: the flush to exact zeros is
+        // decided per 32 x 32 box — a box whose every entry is below 2^-64
+        // is zero (skipped: no exp, no sums, no store; flags 0 in boxnz, zero
+        // column partials); a box with one entry above keeps all its entries
+        // (ex2.approx.ftz still flushes below 2^-126). The dropped mass of a
+        // row stays below n 2^-64, as with a per-element flush, and every
+        // storage and pass sees the same boxes, so runs agree bit for bit.
+        bool box_big = true;
         if constexpr (KIND == GPIC_KIND_RBF && MODE != kModeDense) {
-          // a box whose every entry flushes (< 2^-64, ex2_flush) is skipped:
-          // no exp, no sums, no store (flags 0 in boxnz, zero column partials)
           float gm = __uint_as_float(r[0]);
 #pragma unroll
           for (int x = 1; x < 32; ++x) gm = fmaxf(gm, __uint_as_float(r[x]));
-          if (!__any_sync(0xffffffffu, gm * m2ns >= kFlushLog2)) {
+          box_big = __any_sync(0xffffffffu, gm * m2ns >= kFlushLog2);
+          if (!box_big) {
             if constexpr (MODE == kModeMatvec) {
               if (args.sym) colx[((buf * MB + m) * 4 + q) * 128 + ch * 32 + lane] = 0.f;
               return;
@@ -741,11 +748,13 @@ __global__ void __launch_bounds__(kCtaThreads<MODE>, 1)
           const float g = __uint_as_float(r[x]);
           if constexpr (KIND == GPIC_KIND_COSINE)
             vals[x] = fmaxf(g * gs, 0.f);  // unit rows: G = cos, clamped (affinity.py:93-94)
-          else
+          else if constexpr (MODE == kModeDense)
             // g = -(s^2/2)|x_i - x_j|^2 from the MMA (norm block); no clamp:
             // a near-duplicate's distance^2 rounding below 0 gives
             // exp2(+ulp-scale) = 1 + O(1e-6), the Gram's own rounding order
             vals[x] = ex2_flush(g * m2ns);
+          else
+            vals[x] = box_big ? ex2(g * m2ns) : 0.f;  // box-level flush (above)
         }
         if (diag || pad) {
 #pragma unroll
