@@ -37,6 +37,8 @@
 // affinity_tc.cu, row blocks of 128 MB rows x column tiles J >= MB rb) that
 // are NOT skipped, ascending, and its length — the engine's CTAs split the
 // list evenly.
+#include <mma.h>
+
 #include <cstdlib>
 
 #include "common.cuh"
@@ -180,6 +182,82 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// The same maxima from TF32 tensor-core products (wmma m16n16k8, fp32
+// accumulate): CTA = 128 rows x 64 centroids, warp w owns rows 16w .. +16
+// and the four 16-column tiles. The TF32 rounding of both operands is in
+// the pair test's error bound (kTf32Err).
+__global__ void __launch_bounds__(256)
+    proj_max_tf32_kernel(const float* __restrict__ xc, int64_t n, int32_t dp, int64_t B, int64_t nb,
+                         const float* __restrict__ cent, const float* __restrict__ own,
+                         unsigned* __restrict__ mmax) {
+  using namespace nvcuda;
+  constexpr int kLdA = kGemmK + 4, kLdB = kGemmK + 4, kLdC = kGemmCols + 4;
+  // the operand stages and, after the K loop, the 128 x 64 products
+  constexpr int kAB = kGemmRows * kLdA + kGemmCols * kLdB, kCn = kGemmRows * kLdC;
+  __shared__ __align__(32) float sbuf[kAB > kCn ? kAB : kCn];
+  float* sA = sbuf;
+  float* sB = sbuf + kGemmRows * kLdA;
+  float* sC = sbuf;
+  const int64_t r0 = (int64_t)blockIdx.x * kGemmRows;
+  const int64_t c0 = (int64_t)blockIdx.y * kGemmCols;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  wmma::fragment<wmma::accumulator, 16, 16, 8, float> acc[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) wmma::fill_fragment(acc[j], 0.f);
+  for (int k0 = 0; k0 < dp; k0 += kGemmK) {
+    __syncthreads();
+    for (int e = tid; e < kGemmRows * kGemmK; e += 256) {
+      const int r = e / kGemmK, f = e % kGemmK;
+      const int64_t row = r0 + r;
+      sA[r * kLdA + f] = (row < n && k0 + f < dp) ? xc[row * dp + k0 + f] : 0.f;
+    }
+    for (int e = tid; e < kGemmCols * kGemmK; e += 256) {
+      const int c = e / kGemmK, f = e % kGemmK;
+      const int64_t col = c0 + c;
+      sB[c * kLdB + f] = (col < nb && k0 + f < dp) ? cent[col * dp + k0 + f] : 0.f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < kGemmK; kk += 8) {
+      wmma::fragment<wmma::matrix_a, 16, 16, 8, wmma::precision::tf32, wmma::row_major> a;
+      wmma::load_matrix_sync(a, sA + warp * 16 * kLdA + kk, kLdA);
+#pragma unroll
+      for (int t = 0; t < a.num_elements; ++t) a.x[t] = wmma::__float_to_tf32(a.x[t]);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        // B (K x N) with B[k][c] = cent[c][k]: column-major in sB
+        wmma::fragment<wmma::matrix_b, 16, 16, 8, wmma::precision::tf32, wmma::col_major> b;
+        wmma::load_matrix_sync(b, sB + j * 16 * kLdB + kk, kLdB);
+#pragma unroll
+        for (int t = 0; t < b.num_elements; ++t) b.x[t] = wmma::__float_to_tf32(b.x[t]);
+        wmma::mma_sync(acc[j], a, b, acc[j]);
+      }
+    }
+  }
+  __syncthreads();  // every warp is done with the operand stages
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+    wmma::store_matrix_sync(sC + warp * 16 * kLdC + j * 16, acc[j], kLdC, wmma::mem_row_major);
+  __syncthreads();
+  // column maxima of (P - own) over the 128 rows: 4 row groups of 32
+  __shared__ unsigned cmax[4][kGemmCols];
+  {
+    const int c = tid & (kGemmCols - 1), g = tid >> 6;
+    float m = -INFINITY;
+    for (int r = g * 32; r < g * 32 + 32; ++r) {
+      const int64_t row = r0 + r;
+      if (row < n) m = fmaxf(m, sC[r * kLdC + c] - own[row]);
+    }
+    cmax[g][c] = f2ord(m);
+  }
+  __syncthreads();
+  if (tid < kGemmCols && c0 + tid < nb) {
+    unsigned m = cmax[0][tid];
+    for (int g = 1; g < 4; ++g) m = max(m, cmax[g][tid]);
+    atomicMax(mmax + (r0 / B) * nb + c0 + tid, m);
+  }
+}
+
 __global__ void fill_u32_kernel(unsigned* p, int64_t count, unsigned v) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < count) p[i] = v;
@@ -188,7 +266,7 @@ __global__ void fill_u32_kernel(unsigned* p, int64_t count, unsigned v) {
 // skip[S][S'] for every block pair (symmetric, diagonal 0)
 __global__ void pair_skip_kernel(const float* __restrict__ cent, const unsigned* __restrict__ mmax,
                                  const unsigned* __restrict__ scal, int64_t nb, int32_t dp,
-                                 int32_t d, double d2_thr, uint8_t* __restrict__ skip) {
+                                 int32_t d, double d2_thr, int tf32, uint8_t* __restrict__ skip) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= nb * nb) return;
   const int64_t S = t / nb, T = t % nb;
@@ -205,7 +283,11 @@ __global__ void pair_skip_kernel(const float* __restrict__ cent, const unsigned*
   }
   const double gap = -((double)ord2f(mmax[S * nb + T]) + (double)ord2f(mmax[T * nb + S]));
   const double xm = (double)__uint_as_float(scal[1]), cm = (double)__uint_as_float(scal[0]);
-  const double err = 4.0 * (2.0 * d + 2.0) * 0x1p-24 * xm * cm;
+  // |dot error| <= (operand rounding + d fp32 adds) |x| |c| per product,
+  // four products per gap, doubled for safety: fp32 operands (SIMT) or TF32
+  // (tensor cores, 2^-10 relative per operand)
+  const double per = (tf32 ? 2.0 * 0x1p-11 : 0.0) + (d + 2.0) * 0x1p-24;
+  const double err = 8.0 * per * xm * cm;
   const double lb = (gap - err) / sqrt(u2) * (1.0 - 1e-6);
   skip[t] = (u2 > 0.0 && lb > 0.0 && lb * lb >= d2_thr) ? 1 : 0;
 }
@@ -449,11 +531,17 @@ void launch_prune(const PruneMask& m, const float* xc, const double* colpart, co
   fill_u32_kernel<<<1, 32, 0, s>>>(m.scal, 2, 0u);
   block_centroid_kernel<<<(unsigned)nb, 128, 0, s>>>(colpart, mean, n, d, dp, B, m.cent, m.scal);
   own_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, s>>>(xc, n, dp, B, m.cent, m.own, m.scal);
-  proj_max_kernel<<<dim3((unsigned)ceil_div(n, kGemmRows), (unsigned)ceil_div(nb, kGemmCols)), 256, 0,
-                    s>>>(xc, n, dp, B, nb, m.cent, m.own, m.mmax);
+  // GPIC_PRUNE_TF32=0: the fp32 SIMT products (measurement)
+  const char* tfe = getenv("GPIC_PRUNE_TF32");
+  const int tf32 = tfe == nullptr || atoi(tfe) != 0;
+  const dim3 pg((unsigned)ceil_div(n, kGemmRows), (unsigned)ceil_div(nb, kGemmCols));
+  if (tf32)
+    proj_max_tf32_kernel<<<pg, 256, 0, s>>>(xc, n, dp, B, nb, m.cent, m.own, m.mmax);
+  else
+    proj_max_kernel<<<pg, 256, 0, s>>>(xc, n, dp, B, nb, m.cent, m.own, m.mmax);
   const double d2_thr = kSkipLog2 * 2.0 * sigma * sigma / 1.4426950408889634 * (1.0 + 1e-6);
   pair_skip_kernel<<<(unsigned)ceil_div(nb * nb, 256), 256, 0, s>>>(m.cent, m.mmax, m.scal, nb, dp,
-                                                                    d, d2_thr, m.skip);
+                                                                    d, d2_thr, tf32, m.skip);
   if (mb <= 0) {  // matrix-free: the item list instead of the unit list
     ItemGeom g;
     g.mb = -mb;
