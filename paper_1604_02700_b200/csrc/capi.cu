@@ -816,7 +816,8 @@ int cluster_impl(const double* d_x, int64_t n, int32_t d, double sigma, int32_t 
     if (sparse) launch_sparse_prefix(sm, s);
     mark(ev, 1, s);
     launch_sym_degree(degrow, degcol, n, packed_row_halves(dp), deg, nullptr, s, ShardRange(),
-                      sparse ? sm.boxnz : nullptr, prune ? &pm : nullptr);
+                      sparse ? sm.boxnz : nullptr, prune ? &pm : nullptr,
+                      sparse ? sm.sb_prefix : nullptr);
     L.mode = half ? kLoopPacked16 : kLoopPacked;
     L.rowp = rowp;
     L.colp = colp;

@@ -66,7 +66,7 @@ struct PruneMask;
 void launch_sym_degree(const float* degrow, const float* degcol, int64_t n, int nhalf,
                        double* deg, gpic_ctl* ctl, cudaStream_t s,
                        const ShardRange& sr = ShardRange(), const uint8_t* boxnz = nullptr,
-                       const PruneMask* pm = nullptr);
+                       const PruneMask* pm = nullptr, const int64_t* sb_prefix = nullptr);
 void sym_prepare();
 
 // Workspace carve-up (see capi.cu).
@@ -260,7 +260,13 @@ struct SbList {
   // ranges[0] = the grid they were cut for, ranges[1 + b] = first entry of
   // CTA b (ranges[1 + grid] = count)
   const int64_t* ranges = nullptr;
+  // the reduce's per-super-row lists of non-empty record terms (sym.cu)
+  const int32_t* tlist = nullptr;
+  const int32_t* tcount = nullptr;
+  int64_t tld = 0;
 };
+void launch_reduce_terms(const int64_t* sb_prefix, int64_t nt, int32_t* tlist, int32_t* tcount,
+                         int64_t tld, cudaStream_t s);
 SbList sb_list(const int64_t* sb_prefix, int64_t n);
 SparseMask carve_sparse(void* base, int64_t n, int32_t d);
 // the GEMV weights from the box flags the affinity engine wrote

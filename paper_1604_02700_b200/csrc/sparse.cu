@@ -189,7 +189,8 @@ int64_t sparse_mask_bytes(int64_t n, int32_t /*d*/) {
   auto al = [](int64_t b) { return (b + 255) & ~int64_t(255); };
   const int64_t nsb = ns * (ns + 1) / 2;
   return al(nt * (nt + 1) / 2 * 16) + al((nsb + 1) * 8) + al(nsb * kSB * kSB * 2) + al(8) +
-         al((nsb + 1) * 8) + al(nsb * 4) + al((kMaxGrid + 2) * 8);
+         al((nsb + 1) * 8) + al(nsb * 4) + al((kMaxGrid + 2) * 8) + al(ns * (ns + 2) * 4) +
+         al(ns * 4);
 }
 
 // the non-empty super-block list behind the box bits (sb_list_kernel)
@@ -207,6 +208,11 @@ SbList sb_list(const int64_t* sb_prefix, int64_t n) {
   L.list = reinterpret_cast<const int32_t*>(p);
   p += al(nsb * 4);
   L.ranges = reinterpret_cast<const int64_t*>(p);  // [0] = grid, then grid + 1 bounds
+  p += al((kMaxGrid + 2) * 8);
+  L.tld = ns + 2;
+  L.tlist = reinterpret_cast<const int32_t*>(p);
+  p += al(ns * (ns + 2) * 4);
+  L.tcount = reinterpret_cast<const int32_t*>(p);
   return L;
 }
 
@@ -249,6 +255,8 @@ void launch_sparse_prefix(const SparseMask& m, cudaStream_t s) {
   sb_list_kernel<<<1, kScanThreads, 0, s>>>(m.nt, m.sb_prefix, const_cast<int32_t*>(L.list),
                                             const_cast<int64_t*>(L.lpre),
                                             const_cast<int64_t*>(L.count), grid, ranges + 1);
+  launch_reduce_terms(m.sb_prefix, m.nt, const_cast<int32_t*>(L.tlist),
+                      const_cast<int32_t*>(L.tcount), L.tld, s);
   count_launch(3);
 }
 

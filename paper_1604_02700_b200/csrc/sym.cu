@@ -92,6 +92,12 @@ struct Sparse {
   const int64_t* lpre;
   const int64_t* lcount;
   const int64_t* ranges;  // precomputed CTA ranges over the list (sb_list), or null
+  // reduce: per super-row Q the ascending term indices of its non-empty
+  // records (column records of (P', Q) as P', then row records of (Q, Q')
+  // as Q + 1 + Q' - Q), tlist[Q * tld ...], tcount[Q] of them; or null
+  const int32_t* tlist;
+  const int32_t* tcount;
+  int64_t tld;
   // the 16 tile masks of super-block s (two 16-byte loads), kept in
   // registers: selected by comparisons, never indexed (an indexed array
   // went to local memory)
@@ -549,6 +555,22 @@ __global__ void __launch_bounds__(kTS * kSeg)
   const int64_t nrow = Q < p_hi ? ns - Q : 0;
   const int64_t terms = ncol + nrow;
   const int64_t p0 = terms * sg / kSeg, p1 = terms * (sg + 1) / kSeg;
+  if (sp.tlist != nullptr) {
+    // only the non-empty records, in the same order and segments: the sum
+    // is the one below bit for bit (the skipped terms are exact zeros)
+    const int32_t* tl = sp.tlist + Q * sp.tld;
+    const int L = sp.tcount[Q];
+    double s2 = 0.0;
+    for (int e = 0; e < L; ++e) {
+      const int64_t p = tl[e];
+      if (p < p0) continue;
+      if (p >= p1) break;
+      const int64_t sbi = p < ncol ? tile_index(sr.p_lo + p, Q, ns) : tile_index(Q, Q + (p - ncol), ns);
+      s2 += (double)(p < ncol ? colp[((sbi - sb0) * kSB + k) * kTS + o]
+                              : rowp[((sbi - sb0) * kSB + k) * kTS + o]);
+    }
+    part[sg][o] = s2;
+  } else {
   auto load = [&](int64_t p) {
     const int64_t sbi = p < ncol ? tile_index(sr.p_lo + p, Q, ns) : tile_index(Q, Q + (p - ncol), ns);
     if (sp.empty_sb(sbi)) return 0.f;  // no records: a super-block of zero tiles
@@ -566,6 +588,7 @@ __global__ void __launch_bounds__(kTS * kSeg)
   }
   for (; p < p1; ++p) s += (double)load(p);
   part[sg][o] = s;
+  }
   __syncthreads();
   const int64_t i = R * kTS + o;
   if (sg == 0 && i < n) {
@@ -588,6 +611,151 @@ __global__ void __launch_bounds__(kTS * kSeg)
       for (int r = 0; r < pt.nranks; ++r) st_release_sys(pt.flags[r] + pt.self, epoch);
     }
   }
+}
+
+// The reduce over the per-super-row term lists (whole matrix, sparse): one
+// thread per row, all kSeg segments in turn — the same per-segment sums and
+// the same in-order combine as sym_reduce_kernel (bit for bit), without the
+// 8 threads per row that each walked the list, and small CTAs that all fit
+// on the GPU at once. The stop / flag epilogue is sym_reduce_kernel's.
+__global__ void __launch_bounds__(kTS)
+    sym_reduce_list_kernel(const float* __restrict__ rowp, const float* __restrict__ colp,
+                           int64_t n, int64_t nt, const double* __restrict__ deg,
+                           const PeerTable pt, gpic_ctl* ctl, Sparse sp) {
+  if (ctl != nullptr && *(volatile const int32_t*)&ctl->stop) return;
+  const int64_t ns = (nt + kSB - 1) / kSB;
+  const int64_t R = blockIdx.x;
+  const int o = threadIdx.x;
+  const int64_t Q = R / kSB, k = R - kSB * Q;
+  const int64_t ncol = Q + 1, terms = ncol + (ns - Q);
+  const int32_t* tl = sp.tlist + Q * sp.tld;
+  const int L = sp.tcount[Q];
+  double t = 0.0, seg_sum = 0.0;
+  int sg = 0;
+  int64_t p1 = terms / kSeg;  // end of segment 0
+  for (int e = 0; e < L; ++e) {
+    const int64_t p = tl[e];
+    while (p >= p1) {  // close the segments before p, in order
+      t += seg_sum;
+      seg_sum = 0.0;
+      ++sg;
+      p1 = terms * (sg + 1) / kSeg;
+    }
+    const int64_t sbi = p < ncol ? tile_index(p, Q, ns) : tile_index(Q, Q + (p - ncol), ns);
+    seg_sum += (double)(p < ncol ? colp[(sbi * kSB + k) * kTS + o] : rowp[(sbi * kSB + k) * kTS + o]);
+  }
+  for (; sg < kSeg; ++sg) {
+    t += seg_sum;
+    seg_sum = 0.0;
+  }
+  const int64_t i = R * kTS + o;
+  if (i < n) {
+    const double val = deg != nullptr ? t / deg[i] : t;
+    const int parity = ctl != nullptr ? (ctl->iter & 1) : 0;
+    for (int r = 0; r < pt.nranks; ++r) pt.y[r][parity][i] = val;
+  }
+  if (pt.flags[0] == nullptr) return;
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned prev = atomicAdd(&ctl->arrive[2], 1u);
+    if (prev == gridDim.x - 1) {
+      ctl->arrive[2] = 0u;
+      __threadfence_system();
+      const uint64_t epoch = ctl->sync_epoch + (uint64_t)ctl->iter + 1;
+      for (int r = 0; r < pt.nranks; ++r) st_release_sys(pt.flags[r] + pt.self, epoch);
+    }
+  }
+}
+
+// Degrees over the same per-super-row term lists (whole matrix, sparse):
+// one thread per row; the live tiles of row tile R come, in ascending p,
+// from the non-empty super-blocks of its column (tiles (p, R), p < R) and
+// row (tiles (R, p), p >= R) with their 32-byte box records; the segment
+// sums and their in-order combine are sym_degree_kernel's, bit for bit.
+__global__ void __launch_bounds__(kTS)
+    sym_degree_list_kernel(const float* __restrict__ degrow, const float* __restrict__ degcol,
+                           int64_t n, int64_t nt, int nhalf, double* __restrict__ deg,
+                           gpic_ctl* ctl, Sparse sp) {
+  const int64_t ns = (nt + kSB - 1) / kSB;
+  const int64_t R = blockIdx.x;
+  const int o = threadIdx.x;
+  const int64_t Q = R / kSB, k = R - kSB * Q;
+  const int64_t ncol = Q + 1;
+  const int32_t* tl = sp.tlist + Q * sp.tld;
+  const int L = sp.tcount[Q];
+  double t = 0.0, seg = 0.0;
+  int sg = 0;
+  int64_t p1 = nt / kSeg;
+  auto to_segment = [&](int64_t p) {
+    while (p >= p1) {
+      t += seg;
+      seg = 0.0;
+      ++sg;
+      p1 = nt * (sg + 1) / kSeg;
+    }
+  };
+  for (int e = 0; e < L; ++e) {
+    const int64_t term = tl[e];
+    if (term < ncol) {  // super-block (term, Q): tiles (p, R), p < R
+      const int64_t P = term;
+      const Sparse::Rec rec = sp.record(tile_index(P, Q, ns));
+      const int64_t pe = min(min(kSB * P + kSB, R), nt);
+      for (int64_t p = kSB * P; p < pe; ++p) {
+        if (Sparse::mask_of(rec, (int)((p - kSB * P) * kSB + k)) == 0u) continue;
+        to_segment(p);
+        const float* c = degcol + tile_index(p, R, nt) * 4 * kTS + o;
+        seg += (double)c[0] + (double)c[kTS] + (double)c[2 * kTS] + (double)c[3 * kTS];
+      }
+    } else {  // super-block (Q, Q'): tiles (R, p), p >= R
+      const int64_t Qp = Q + (term - ncol);
+      const Sparse::Rec rec = sp.record(tile_index(Q, Qp, ns));
+      const int64_t pe = min(kSB * Qp + kSB, nt);
+      for (int64_t p = max(kSB * Qp, R); p < pe; ++p) {
+        if (Sparse::mask_of(rec, (int)(k * kSB + (p - kSB * Qp))) == 0u) continue;
+        to_segment(p);
+        const float* r = degrow + tile_index(R, p, nt) * nhalf * kTS + o;
+        seg += (double)r[0];
+        if (nhalf == 2) seg += (double)r[kTS];
+      }
+    }
+  }
+  for (; sg < kSeg; ++sg) {
+    t += seg;
+    seg = 0.0;
+  }
+  const int64_t i = R * kTS + o;
+  if (i < n) {
+    deg[i] = t;
+    if (ctl != nullptr && t <= 0.0) raise_status(ctl, GPIC_E_ZERO_DEGREE, i, -1, t);
+  }
+}
+
+// Per super-row Q (one warp each): the term indices of its non-empty
+// records in ascending order — column records (P', Q), P' <= Q, as P', then
+// row records (Q, Q'), Q' >= Q, as Q + 1 + (Q' - Q) — from the super-block
+// weights (weight 1: no stored tile, no record). Whole matrix only.
+__global__ void reduce_terms_kernel(const int64_t* __restrict__ sbp, int64_t ns,
+                                    int32_t* __restrict__ tlist, int32_t* __restrict__ tcount,
+                                    int64_t tld) {
+  const int lane = threadIdx.x & 31;
+  const int64_t Q = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (Q >= ns) return;
+  int32_t* out = tlist + Q * tld;
+  int cnt = 0;
+  const int64_t ncol = Q + 1, terms = ncol + (ns - Q);
+  for (int64_t c0 = 0; c0 < terms; c0 += 32) {
+    const int64_t p = c0 + lane;
+    bool nz = false;
+    if (p < terms) {
+      const int64_t sbi = p < ncol ? tile_index(p, Q, ns) : tile_index(Q, Q + (p - ncol), ns);
+      nz = sbp[sbi + 1] - sbp[sbi] > 1;
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, nz);
+    if (nz) out[cnt + __popc(m & ((1u << lane) - 1u))] = (int32_t)p;
+    cnt += __popc(m);
+  }
+  if (lane == 0) tcount[Q] = cnt;
 }
 
 // deg_i from the affinity epilogue's partials (same segmented fixed shape as
@@ -727,11 +895,21 @@ int gemv_prefetch() {
 
 void launch_sym_degree(const float* degrow, const float* degcol, int64_t n, int nhalf,
                        double* deg, gpic_ctl* ctl, cudaStream_t s, const ShardRange& sr,
-                       const uint8_t* boxnz, const PruneMask* pm) {
+                       const uint8_t* boxnz, const PruneMask* pm, const int64_t* sb_prefix) {
   const int64_t nt = ceil_div(n, kTS);
   const int64_t rows = nt - kSB * sr.p_lo;  // tile rows that can receive partials
   if (rows < 1) return;
-  const Sparse sp{boxnz, nullptr, nullptr, 0, 0, 0, nullptr, nullptr, nullptr, nullptr};
+  if (boxnz != nullptr && sb_prefix != nullptr && sr.p_lo == 0 && sr.tile_base == 0 &&
+      gemv_use_list()) {
+    // the per-super-row term lists and box records of the sparse prefix pass
+    const SbList sl = sb_list(sb_prefix, n);
+    const Sparse lp{boxnz, sb_prefix, sb_bits(sb_prefix, n), 0, 0, 0, sl.list, sl.lpre, sl.count,
+                    sl.ranges, sl.tlist, sl.tcount, sl.tld};
+    sym_degree_list_kernel<<<(unsigned)nt, kTS, 0, s>>>(degrow, degcol, n, nt, nhalf, deg, ctl, lp);
+    count_launch();
+    return;
+  }
+  const Sparse sp{boxnz, nullptr, nullptr, 0, 0, 0, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 0};
   const size_t dyn = boxnz != nullptr ? (size_t)nt * 4 : 0;  // the live-tile list
   if (dyn > 48 * 1024)
     cudaFuncSetAttribute(sym_degree_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
@@ -749,6 +927,13 @@ void sym_prepare() {
     cudaFuncSetAttribute(sym_gemv_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
     cudaFuncSetAttribute(sym_gemv_kernel<__half>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
   }
+}
+
+void launch_reduce_terms(const int64_t* sb_prefix, int64_t nt, int32_t* tlist, int32_t* tcount,
+                         int64_t tld, cudaStream_t s) {
+  const int64_t ns = (nt + kSB - 1) / kSB;
+  reduce_terms_kernel<<<(unsigned)ceil_div(ns, 8), 256, 0, s>>>(sb_prefix, ns, tlist, tcount, tld);
+  count_launch();
 }
 
 // GEMV partial records (super-block rows / columns) or the affinity
@@ -775,7 +960,7 @@ void launch_sym_gemv(const float* tiles, int64_t n, const float* v32, float* row
   const Sparse sp{boxnz, boxnz != nullptr ? sb_prefix : nullptr,
                   boxnz != nullptr && whole && bits_mode != 0 ? sb_bits(sb_prefix, n) : nullptr,
                   gemv_prefetch(), bits_mode == 1, gemv_evict_first(), sl.list, sl.lpre, sl.count,
-                  sl.ranges};
+                  sl.ranges, sl.tlist, sl.tcount, sl.tld};
   sym_prepare();
   const int64_t nt = ceil_div(n, kTS);
   const int64_t ns = (nt + kSB - 1) / kSB;
@@ -784,7 +969,10 @@ void launch_sym_gemv(const float* tiles, int64_t n, const float* v32, float* row
   const int64_t rows = nt - kSB * sr.p_lo;
   if (grid < 1 || rows < 1) return;
   sym_gemv_kernel<float><<<grid, kThreads, kSmem, s>>>(tiles, nt, v32, rowp, colp, ctl, sr, sp);
-  sym_reduce_kernel<<<(unsigned)rows, kTS * kSeg, 0, s>>>(rowp, colp, n, nt, deg, pt, ctl, sr, sp);
+  if (sp.tlist != nullptr)
+    sym_reduce_list_kernel<<<(unsigned)nt, kTS, 0, s>>>(rowp, colp, n, nt, deg, pt, ctl, sp);
+  else
+    sym_reduce_kernel<<<(unsigned)rows, kTS * kSeg, 0, s>>>(rowp, colp, n, nt, deg, pt, ctl, sr, sp);
   count_launch(2);
 }
 
@@ -795,7 +983,8 @@ void launch_sym_gemv16(const void* tiles, int64_t n, const float* v32, float* ro
                                                         : SbList{nullptr, nullptr, nullptr};
   const Sparse sp{boxnz, boxnz != nullptr ? sb_prefix : nullptr,
                   boxnz != nullptr ? sb_bits(sb_prefix, n) : nullptr, gemv_prefetch(), 0,
-                  gemv_evict_first(), sl.list, sl.lpre, sl.count, sl.ranges};
+                  gemv_evict_first(), sl.list, sl.lpre, sl.count, sl.ranges, sl.tlist, sl.tcount,
+                  sl.tld};
   sym_prepare();
   const int64_t nt = ceil_div(n, kTS);
   const int64_t ns = (nt + kSB - 1) / kSB;
@@ -804,7 +993,10 @@ void launch_sym_gemv16(const void* tiles, int64_t n, const float* v32, float* ro
   const ShardRange all{};
   sym_gemv_kernel<__half><<<grid, kThreads, kSmem, s>>>(static_cast<const __half*>(tiles), nt, v32,
                                                             rowp, colp, ctl, all, sp);
-  sym_reduce_kernel<<<(unsigned)nt, kTS * kSeg, 0, s>>>(rowp, colp, n, nt, deg, pt, ctl, all, sp);
+  if (sp.tlist != nullptr)
+    sym_reduce_list_kernel<<<(unsigned)nt, kTS, 0, s>>>(rowp, colp, n, nt, deg, pt, ctl, sp);
+  else
+    sym_reduce_kernel<<<(unsigned)nt, kTS * kSeg, 0, s>>>(rowp, colp, n, nt, deg, pt, ctl, all, sp);
   count_launch(2);
 }
 
