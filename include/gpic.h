@@ -401,10 +401,14 @@ int gpic_packed_shard_range(int64_t n, int32_t nranks, int32_t rank, int64_t* ro
                             int64_t* row_hi);
 int64_t gpic_packed_shard_tiles(int64_t n, int64_t row_lo, int64_t row_hi);
 int64_t gpic_packed_shard_scratch_bytes(int64_t n, int64_t row_lo, int64_t row_hi);
+/* d_prep_work: the work buffer of gpic_prepare_points (column sums + mean):
+ * with it (RBF) the shard's provably-zero block pairs are not computed; its
+ * zero 32 x 32 boxes are never stored either way (block sparsity, flags in
+ * d_scratch). NULL: no pruning. */
 int gpic_packed_shard_build(const float* d_xhi, const float* d_xlo, const float* d_sqn, int64_t n,
                             int32_t d, int64_t row_lo, int64_t row_hi, double sigma, int32_t kind,
                             float* d_tiles, double* d_deg_partial, void* d_scratch,
-                            void* stream);
+                            const double* d_prep_work, void* stream);
 
 /* Matrix-free degrees of rows [row_lo, row_hi): deg = A 1 recomputed from the
  * prepared points (gpic_prepare_points). d_ones: gpic_vector_pitch(n) floats

@@ -112,7 +112,8 @@ SIGNATURES = {
     "gpic_packed_shard_range": (C.c_int, [I64, I32, I32, P, P]),
     "gpic_packed_shard_tiles": (I64, [I64, I64, I64]),
     "gpic_packed_shard_scratch_bytes": (I64, [I64, I64, I64]),
-    "gpic_packed_shard_build": (C.c_int, [P, P, P, I64, I32, I64, I64, C.c_double, I32, P, P, P, P]),
+    "gpic_packed_shard_build": (C.c_int, [P, P, P, I64, I32, I64, I64, C.c_double, I32, P, P, P, P,
+                                          P]),
     "gpic_cluster_workspace_bytes": (I64, [I64, I32, I32, I32, I32]),
     # (x, n, d, sigma, kind, k, eps, max_iter, first, uniforms, impl, storage, v0,
     #  labels, v, hist, iters, converged, work, work_bytes, stream[, phase_ms])

@@ -620,17 +620,44 @@ static int64_t shard_records(int64_t n, int64_t row_lo, int64_t row_hi) {
   const int64_t a = p0 * ns - p0 * (p0 - 1) / 2, b = p1 * ns - p1 * (p1 - 1) / 2;
   return (b - a) * 4 * 128;
 }
+// [records][records][degree partials][degree partials][block sparsity of the
+// whole triangle (sparse.cu; flags of other shards' tiles stay 0)][pruning
+// mask (prune.cu), sized for the widest pitch]
 int64_t gpic_packed_shard_scratch_bytes(int64_t n, int64_t row_lo, int64_t row_hi) {
   const int64_t t = gpic_packed_shard_tiles(n, row_lo, row_hi);
   if (t < 0) return -1;
   const int64_t r = shard_records(n, row_lo, row_hi);
-  return 2 * al(r * 4) + al(t * 128 * 4) + al(t * 4 * 128 * 4);
+  return 2 * al(r * 4) + al(t * 128 * 4) + al(t * 4 * 128 * 4) + al(sparse_mask_bytes(n, 256)) +
+         al(prune_bytes(n, 256));
 }
+
+// the shard scratch's block-sparsity and pruning regions
+static void shard_sparse(void* d_scratch, int64_t n, int64_t row_lo, int64_t row_hi, int32_t d,
+                         SparseMask* sm, PruneMask* pm) {
+  const int64_t t = gpic_packed_shard_tiles(n, row_lo, row_hi);
+  const int64_t r = shard_records(n, row_lo, row_hi);
+  uint8_t* p = static_cast<uint8_t*>(d_scratch) + 2 * al(r * 4) + al(t * 128 * 4) +
+               al(t * 4 * 128 * 4);
+  *sm = carve_sparse(p, n, d);
+  *pm = carve_prune(p + al(sparse_mask_bytes(n, 256)), n, feature_pitch(d));
+}
+
+}  // extern "C"
+namespace gpic {
+SparseMask packed_shard_sparse(void* d_scratch, int64_t n, int64_t row_lo, int64_t row_hi,
+                               int32_t d) {
+  SparseMask sm;
+  PruneMask pm;
+  shard_sparse(d_scratch, n, row_lo, row_hi, d, &sm, &pm);
+  return sm;
+}
+}  // namespace gpic
+extern "C" {
 
 int gpic_packed_shard_build(const float* d_xhi, const float* d_xlo, const float* d_sqn, int64_t n,
                             int32_t d, int64_t row_lo, int64_t row_hi, double sigma, int32_t kind,
                             float* d_tiles, double* d_deg_partial, void* d_scratch,
-                            void* stream) {
+                            const double* d_prep_work, void* stream) {
   if (kind == GPIC_KIND_RBF && !(sigma > 0)) return fail(GPIC_E_INVALID, "sigma must be positive");
   if (kind == GPIC_KIND_COSINE) sigma = 1.0;
   const int64_t t = gpic_packed_shard_tiles(n, row_lo, row_hi);
@@ -642,15 +669,30 @@ int gpic_packed_shard_build(const float* d_xhi, const float* d_xlo, const float*
   float* degrow = reinterpret_cast<float*>(base);
   float* degcol = reinterpret_cast<float*>(base + al(t * 128 * 4));
   const float neg_scale_log2 = (float)(-1.4426950408889634 / (2.0 * sigma * sigma));
+  // block sparsity of the shard's tiles (flags in a whole-triangle array) and,
+  // with the prepare pass's column sums (RBF), tile pruning of its units
+  SparseMask sm;
+  PruneMask pm;
+  shard_sparse(d_scratch, n, row_lo, row_hi, d, &sm, &pm);
+  const bool sparse = sparse_enabled();
+  const bool prune = sparse && kind == GPIC_KIND_RBF && prune_enabled() && d_prep_work != nullptr;
+  if (sparse) GPIC_CUDA_TRY(cudaMemsetAsync(sm.boxnz, 0, packed_tiles(n) * 16, s));
+  if (prune)
+    launch_prune(pm, d_xlo, d_prep_work, d_prep_work + ceil_div(n, 256) * d, n, d, dp, sigma,
+                 tc_mblocks(dp), row_lo, s, row_hi);
   int rc = launch_affinity_tc_packed(d_xhi, d_xlo, d_sqn, n, dp, neg_scale_log2, d_tiles, degrow,
-                                     degcol, s, kind, false, row_lo, row_hi);
+                                     degcol, s, kind, false, row_lo, row_hi,
+                                     sparse ? sm.boxnz : nullptr, prune ? pm.units : nullptr,
+                                     prune ? pm.count : nullptr);
   if (rc) return rc;
+  if (sparse) launch_sparse_prefix(sm, s);
   GPIC_CUDA_TRY(cudaMemsetAsync(d_deg_partial, 0, n * 8, s));
   ShardRange sr;
   sr.p_lo = row_lo / 512;
   sr.p_hi = ceil_div(row_hi, 512);
   sr.tile_base = tiles_before_row(n, row_lo / kTileN);
-  launch_sym_degree(degrow, degcol, n, packed_row_halves(dp), d_deg_partial, nullptr, s, sr);
+  launch_sym_degree(degrow, degcol, n, packed_row_halves(dp), d_deg_partial, nullptr, s, sr,
+                    sparse ? sm.boxnz : nullptr, prune ? &pm : nullptr);
   GPIC_CUDA_TRY(cudaGetLastError());
   return GPIC_OK;
 }

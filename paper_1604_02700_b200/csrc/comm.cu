@@ -431,6 +431,11 @@ int gpic_comm_iterate(gpic_comm* c, const gpic_shard* shards, int32_t nlocal, do
       S.slots = r_slot(c->region[self], n, 0, 0);
       S.slot_stride = al(n * 8) / 8;
       S.deg_full = r_deg(c->region[self], n);
+      if (sparse_enabled()) {  // the build's box flags and GEMV weights (gpic_packed_shard_build)
+        const SparseMask sm = packed_shard_sparse(sh.ypart, n, sh.row_lo, sh.row_lo + sh.rows, sh.d);
+        S.boxnz = sm.boxnz;
+        S.sb_prefix = sm.sb_prefix;
+      }
     }
     if (shards[li].storage == GPIC_STORAGE_NONE) {
       const gpic_shard& sh = shards[li];

@@ -196,9 +196,11 @@ PruneMask carve_prune(void* base, int64_t n, int32_t dp);
 // xc: the centred fp32 rows (pitch dp); colpart / mean: the prepare pass's
 // 256-row column sums and centring mean; mb: tc_mblocks(dp) for the packed
 // unit list, -tc_mblocks(dp) for the matrix-free item list
+// row_lo / row_hi: a packed shard's rows (the unit list covers its row
+// blocks only); row_hi <= 0: n
 void launch_prune(const PruneMask& m, const float* xc, const double* colpart, const double* mean,
                   int64_t n, int32_t d, int32_t dp, double sigma, int mb, int64_t row_lo,
-                  cudaStream_t s);
+                  cudaStream_t s, int64_t row_hi = 0);
 
 // ---- matrix-free (affinity_tc.cu matvec mode + mf.cu) --------------------
 struct MfOperands {
@@ -275,6 +277,9 @@ void launch_sparse_prefix(const SparseMask& m, cudaStream_t s);
 void launch_box_fill(const SparseMask& m, uint8_t v, cudaStream_t s);
 // GPIC_SPARSE=0 turns the zero-box skipping off (dense packed runs, for comparisons)
 bool sparse_enabled();
+// a packed shard's block-sparsity region inside its build scratch (capi.cu)
+SparseMask packed_shard_sparse(void* d_scratch, int64_t n, int64_t row_lo, int64_t row_hi,
+                               int32_t d);
 
 // ---- locality order (locality.cu) -----------------------------------------
 // Points of a randomly ordered input permuted so that index neighbours are

@@ -370,7 +370,8 @@ int run_power_loops(ShardLoop* shards, int nlocal, int64_t n, int32_t max_iter, 
                             L.sb_prefix);
         } else if (L.mode == kLoopPackedShard) {
           // partial y over the shard's tiles into every rank's slot of this shard
-          launch_sym_gemv(L.a, n, L.v32, L.rowp, L.colp, nullptr, L.pt_slots, L.ctl, cs, L.sr);
+          launch_sym_gemv(L.a, n, L.v32, L.rowp, L.colp, nullptr, L.pt_slots, L.ctl, cs, L.sr,
+                          L.boxnz, L.sb_prefix);
         } else if (L.mode == kLoopMatrixFree || L.mode == kLoopMfShard) {
           // item shard: partial y (no 1/deg) into every rank's slot of this shard
           const bool item = L.mode == kLoopMfShard;

@@ -525,7 +525,8 @@ PruneMask carve_prune(void* base, int64_t n, int32_t dp) {
 
 void launch_prune(const PruneMask& m, const float* xc, const double* colpart, const double* mean,
                   int64_t n, int32_t d, int32_t dp, double sigma, int mb, int64_t row_lo,
-                  cudaStream_t s) {
+                  cudaStream_t s, int64_t row_hi) {
+  if (row_hi <= 0) row_hi = n;
   const int64_t nb = m.nb, B = m.B;
   fill_u32_kernel<<<(unsigned)ceil_div(nb * nb + 2, 256), 256, 0, s>>>(m.mmax, nb * nb, 0u);
   fill_u32_kernel<<<1, 32, 0, s>>>(m.scal, 2, 0u);
@@ -559,7 +560,7 @@ void launch_prune(const PruneMask& m, const float* xc, const double* colpart, co
   }
   UnitGeom g;
   g.nct = ceil_div(n, 128);
-  g.nrt = ceil_div(n, 128 * mb);
+  g.nrt = ceil_div(row_hi, 128 * mb);  // a packed shard's units end at its last row block
   g.nb = nb;
   g.B = B;
   g.mb = mb;

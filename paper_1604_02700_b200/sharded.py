@@ -211,7 +211,8 @@ class ShardedRunner:
                                       dtype=torch.uint8, device=dev)
                 _lib.check(L.gpic_packed_shard_build(
                     gpu._ptr(prep.xhi), gpu._ptr(prep.xlo), gpu._ptr(prep.sqn), n, prep.d, lo, hi,
-                    sigma, code, gpu._ptr(tiles), gpu._ptr(deg), gpu._ptr(scratch), st))
+                    sigma, code, gpu._ptr(tiles), gpu._ptr(deg), gpu._ptr(scratch),
+                    gpu._ptr(prep.work), st))
                 keep += [tiles, deg, scratch]
                 shards[i] = _lib.Shard(tiles.data_ptr(), 0, deg.data_ptr(), lo, hi - lo,
                                        _lib.STORAGE_PACKED, prep.d, None, None, None, sigma, code,
