@@ -182,79 +182,101 @@ __global__ void __launch_bounds__(256)
   }
 }
 
-// The same maxima from TF32 tensor-core products (wmma m16n16k8, fp32
-// accumulate): CTA = 128 rows x 64 centroids, warp w owns rows 16w .. +16
-// and the four 16-column tiles. The TF32 rounding of both operands is in
-// the pair test's error bound (kTf32Err).
+// One pass per 128 rows (all in one block S): the X tile stays in shared
+// memory, own_i = x_i . c_S and |x_i| are formed there, then every chunk of
+// 64 centroids goes through TF32 tensor-core products (wmma m16n16k8, fp32
+// accumulate; the operand rounding is in the pair test's bound) and the
+// column maxima of P - own. Dynamic smem: X tile [128][dp + 4], then a
+// buffer shared by the centroid chunk [64][dp + 4] and the products
+// [128][68].
 __global__ void __launch_bounds__(256)
-    proj_max_tf32_kernel(const float* __restrict__ xc, int64_t n, int32_t dp, int64_t B, int64_t nb,
-                         const float* __restrict__ cent, const float* __restrict__ own,
-                         unsigned* __restrict__ mmax) {
+    proj_fused_kernel(const float* __restrict__ xc, int64_t n, int32_t dp, int64_t B, int64_t nb,
+                      const float* __restrict__ cent, unsigned* __restrict__ mmax,
+                      unsigned* __restrict__ scal) {
   using namespace nvcuda;
-  constexpr int kLdA = kGemmK + 4, kLdB = kGemmK + 4, kLdC = kGemmCols + 4;
-  // the operand stages and, after the K loop, the 128 x 64 products
-  constexpr int kAB = kGemmRows * kLdA + kGemmCols * kLdB, kCn = kGemmRows * kLdC;
-  __shared__ __align__(32) float sbuf[kAB > kCn ? kAB : kCn];
-  float* sA = sbuf;
-  float* sB = sbuf + kGemmRows * kLdA;
-  float* sC = sbuf;
+  extern __shared__ __align__(128) float fsm[];
+  const int ldx = dp + 4, ldc = kGemmCols + 4;
+  float* sX = fsm;
+  float* sU = fsm + kGemmRows * ldx;  // centroid chunk / products
+  __shared__ float own[kGemmRows];
+  __shared__ unsigned cmax[4][kGemmCols];
+  __shared__ float xmax[8];
   const int64_t r0 = (int64_t)blockIdx.x * kGemmRows;
-  const int64_t c0 = (int64_t)blockIdx.y * kGemmCols;
-  const int tid = threadIdx.x, warp = tid >> 5;
-  wmma::fragment<wmma::accumulator, 16, 16, 8, float> acc[4];
-#pragma unroll
-  for (int j = 0; j < 4; ++j) wmma::fill_fragment(acc[j], 0.f);
-  for (int k0 = 0; k0 < dp; k0 += kGemmK) {
-    __syncthreads();
-    for (int e = tid; e < kGemmRows * kGemmK; e += 256) {
-      const int r = e / kGemmK, f = e % kGemmK;
-      const int64_t row = r0 + r;
-      sA[r * kLdA + f] = (row < n && k0 + f < dp) ? xc[row * dp + k0 + f] : 0.f;
+  const int64_t S = r0 / B;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int e = tid; e < kGemmRows * dp; e += 256) {
+    const int r = e / dp, f = e % dp;
+    const int64_t row = r0 + r;
+    sX[r * ldx + f] = row < n ? xc[row * dp + f] : 0.f;
+  }
+  __syncthreads();
+  // own products and norms: a warp per 16 rows, lanes over the features
+  {
+    const float* c = cent + S * dp;
+    float xm = 0.f;
+    for (int r = warp * 16; r < warp * 16 + 16; ++r) {
+      float a = 0.f, b = 0.f;
+      for (int f = lane; f < dp; f += 32) {
+        const float x = sX[r * ldx + f];
+        a = fmaf(x, __ldg(c + f), a);
+        b = fmaf(x, x, b);
+      }
+      a = warp_sum_f32(a);
+      b = warp_sum_f32(b);
+      if (lane == 0) own[r] = a;
+      if (r0 + r < n) xm = fmaxf(xm, sqrtf(b) * 1.0001f);
     }
-    for (int e = tid; e < kGemmCols * kGemmK; e += 256) {
-      const int c = e / kGemmK, f = e % kGemmK;
+    if (lane == 0) xmax[warp] = xm;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    float m = xmax[0];
+    for (int w = 1; w < 8; ++w) m = fmaxf(m, xmax[w]);
+    atomicMax(scal + 1, __float_as_uint(m));
+  }
+  for (int64_t c0 = 0; c0 < nb; c0 += kGemmCols) {
+    __syncthreads();  // the previous chunk's products are consumed
+    for (int e = tid; e < kGemmCols * dp; e += 256) {
+      const int c = e / dp, f = e % dp;
       const int64_t col = c0 + c;
-      sB[c * kLdB + f] = (col < nb && k0 + f < dp) ? cent[col * dp + k0 + f] : 0.f;
+      sU[c * ldx + f] = col < nb ? cent[col * dp + f] : 0.f;
     }
     __syncthreads();
+    wmma::fragment<wmma::accumulator, 16, 16, 8, float> acc[4];
 #pragma unroll
-    for (int kk = 0; kk < kGemmK; kk += 8) {
+    for (int j = 0; j < 4; ++j) wmma::fill_fragment(acc[j], 0.f);
+    for (int kk = 0; kk < dp; kk += 8) {
       wmma::fragment<wmma::matrix_a, 16, 16, 8, wmma::precision::tf32, wmma::row_major> a;
-      wmma::load_matrix_sync(a, sA + warp * 16 * kLdA + kk, kLdA);
+      wmma::load_matrix_sync(a, sX + warp * 16 * ldx + kk, ldx);
 #pragma unroll
       for (int t = 0; t < a.num_elements; ++t) a.x[t] = wmma::__float_to_tf32(a.x[t]);
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        // B (K x N) with B[k][c] = cent[c][k]: column-major in sB
         wmma::fragment<wmma::matrix_b, 16, 16, 8, wmma::precision::tf32, wmma::col_major> b;
-        wmma::load_matrix_sync(b, sB + j * 16 * kLdB + kk, kLdB);
+        wmma::load_matrix_sync(b, sU + j * 16 * ldx + kk, ldx);
 #pragma unroll
         for (int t = 0; t < b.num_elements; ++t) b.x[t] = wmma::__float_to_tf32(b.x[t]);
         wmma::mma_sync(acc[j], a, b, acc[j]);
       }
     }
-  }
-  __syncthreads();  // every warp is done with the operand stages
+    __syncthreads();  // every warp is done with the chunk: reuse its buffer
 #pragma unroll
-  for (int j = 0; j < 4; ++j)
-    wmma::store_matrix_sync(sC + warp * 16 * kLdC + j * 16, acc[j], kLdC, wmma::mem_row_major);
-  __syncthreads();
-  // column maxima of (P - own) over the 128 rows: 4 row groups of 32
-  __shared__ unsigned cmax[4][kGemmCols];
-  {
-    const int c = tid & (kGemmCols - 1), g = tid >> 6;
-    float m = -INFINITY;
-    for (int r = g * 32; r < g * 32 + 32; ++r) {
-      const int64_t row = r0 + r;
-      if (row < n) m = fmaxf(m, sC[r * kLdC + c] - own[row]);
+    for (int j = 0; j < 4; ++j)
+      wmma::store_matrix_sync(sU + warp * 16 * ldc + j * 16, acc[j], ldc, wmma::mem_row_major);
+    __syncthreads();
+    {
+      const int c = tid & (kGemmCols - 1), g = tid >> 6;
+      float m = -INFINITY;
+      for (int r = g * 32; r < g * 32 + 32; ++r)
+        if (r0 + r < n) m = fmaxf(m, sU[r * ldc + c] - own[r]);
+      cmax[g][c] = f2ord(m);
     }
-    cmax[g][c] = f2ord(m);
-  }
-  __syncthreads();
-  if (tid < kGemmCols && c0 + tid < nb) {
-    unsigned m = cmax[0][tid];
-    for (int g = 1; g < 4; ++g) m = max(m, cmax[g][tid]);
-    atomicMax(mmax + (r0 / B) * nb + c0 + tid, m);
+    __syncthreads();
+    if (tid < kGemmCols && c0 + tid < nb) {
+      unsigned m = cmax[0][tid];
+      for (int g = 1; g < 4; ++g) m = max(m, cmax[g][tid]);
+      atomicMax(mmax + S * nb + c0 + tid, m);
+    }
   }
 }
 
@@ -531,15 +553,26 @@ void launch_prune(const PruneMask& m, const float* xc, const double* colpart, co
   fill_u32_kernel<<<(unsigned)ceil_div(nb * nb + 2, 256), 256, 0, s>>>(m.mmax, nb * nb, 0u);
   fill_u32_kernel<<<1, 32, 0, s>>>(m.scal, 2, 0u);
   block_centroid_kernel<<<(unsigned)nb, 128, 0, s>>>(colpart, mean, n, d, dp, B, m.cent, m.scal);
-  own_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, s>>>(xc, n, dp, B, m.cent, m.own, m.scal);
   // GPIC_PRUNE_TF32=0: the fp32 SIMT products (measurement)
   const char* tfe = getenv("GPIC_PRUNE_TF32");
   const int tf32 = tfe == nullptr || atoi(tfe) != 0;
-  const dim3 pg((unsigned)ceil_div(n, kGemmRows), (unsigned)ceil_div(nb, kGemmCols));
-  if (tf32)
-    proj_max_tf32_kernel<<<pg, 256, 0, s>>>(xc, n, dp, B, nb, m.cent, m.own, m.mmax);
-  else
+  if (!tf32) own_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, s>>>(xc, n, dp, B, m.cent, m.own, m.scal);
+  if (tf32) {
+    const int ldx = dp + 4;
+    const int ubuf = kGemmCols * ldx > kGemmRows * (kGemmCols + 4) ? kGemmCols * ldx
+                                                                     : kGemmRows * (kGemmCols + 4);
+    const size_t shm = (size_t)(kGemmRows * ldx + ubuf) * 4;
+    static size_t shm_set = 0;
+    if (shm > 48 * 1024 && shm > shm_set) {
+      cudaFuncSetAttribute(proj_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm);
+      shm_set = shm;
+    }
+    proj_fused_kernel<<<(unsigned)ceil_div(n, kGemmRows), 256, shm, s>>>(xc, n, dp, B, nb, m.cent,
+                                                                        m.mmax, m.scal);
+  } else {
+    const dim3 pg((unsigned)ceil_div(n, kGemmRows), (unsigned)ceil_div(nb, kGemmCols));
     proj_max_kernel<<<pg, 256, 0, s>>>(xc, n, dp, B, nb, m.cent, m.own, m.mmax);
+  }
   const double d2_thr = kSkipLog2 * 2.0 * sigma * sigma / 1.4426950408889634 * (1.0 + 1e-6);
   pair_skip_kernel<<<(unsigned)ceil_div(nb * nb, 256), 256, 0, s>>>(m.cent, m.mmax, m.scal, nb, dp,
                                                                     d, d2_thr, tf32, m.skip);
