@@ -946,19 +946,16 @@ int cluster_impl(const double* d_x, int64_t n, int32_t d, double sigma, int32_t 
   }
   mark(ev, 3, s);
   GPIC_CUDA_TRY(cudaGetLastError());
-  // k-means needs the status of the loop: read the control block once.
-  gpic_ctl h;
-  rc = gpic_ctl_read(ws.ctl, &h, stream);
-  if (rc) return rc;
-  note_loop_iterations(h.iter);
-  rc = status_from_ctl(h, d);
-  if (rc) return rc;
+  // the k-means kernels read the loop's status on the device (a failed loop
+  // leaves them no-ops), so the control block is read once, at the end
   rc = launch_kmeans1d(d_v, n, k, first_index, h_uniforms, 100, 1e-12, d_labels, ws.kscratch,
                        ws.ctl, s);
   if (rc) return rc;
   mark(ev, 4, s);
+  gpic_ctl h;
   rc = gpic_ctl_read(ws.ctl, &h, stream);
   if (rc) return rc;
+  note_loop_iterations(h.iter);
   if (h_iters) *h_iters = h.iter;
   if (h_converged) *h_converged = h.converged;
   return status_from_ctl(h, d);
