@@ -907,13 +907,11 @@ int cluster_impl(const double* d_x, int64_t n, int32_t d, double sigma, int32_t 
   low.sigma = sigma;
   low.list = ws.lowlist;
   low.d_count = ws.lowcount;
-  {
-    gpic_ctl h0;
-    GPIC_CUDA_TRY(cudaMemcpyAsync(&h0, ws.ctl, sizeof h0, cudaMemcpyDeviceToHost, s));
-    rc = read_low_count(ws.lowcount, &low.count, s);
-    if (rc) return rc;
-    if (h0.status != GPIC_OK) return status_from_ctl(h0, d);  // e.g. NonFiniteEntry
-  }
+  // the listed rows are handled by kernels striding over the device-side
+  // count (no host read here); a failure so far (NonFiniteEntry, ...) has
+  // set ctl->stop, so the loop and the k-means are no-ops and the final
+  // control-block read reports it
+  low.count = -1;
   launch_lowdeg_exact(low, deg, ws.ctl, s);
   mark(ev, 2, s);
   if (d_v0 != nullptr) {  // explicit start vector (initial_vector, serial.py:77-101)

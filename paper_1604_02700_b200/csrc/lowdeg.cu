@@ -92,8 +92,10 @@ __global__ void __launch_bounds__(kLowThreads)
   __shared__ double sh[kLowThreads / 32];
   extern __shared__ double xs[];
   if (kMatvec && *(volatile int32_t*)&ctl->stop) return;
-  if ((unsigned long long)blockIdx.x >= *count) return;
-  const int64_t i = list[blockIdx.x];
+  const unsigned long long cnt = *count;  // the grid strides over the listed rows
+  for (unsigned long long r = blockIdx.x; r < cnt; r += gridDim.x) {
+  const int64_t i = list[r];
+  __syncthreads();  // xs of the previous row is consumed
   const double* xi = d <= kSmemD ? xs : x + i * d;
   if (d <= kSmemD)
     for (int32_t f = threadIdx.x; f < d; f += blockDim.x) xs[f] = x[i * d + f];
@@ -111,12 +113,14 @@ __global__ void __launch_bounds__(kLowThreads)
     s += kMatvec ? __ddiv_rn(a, di) * v[j] : a;  // W = A / d (affinity.py:126), W v
   }
   s = block_sum(s, sh);
-  if (threadIdx.x != 0) return;
-  if (kMatvec) {
-    ((t & 1) ? y1 : y0)[i] = s;
-  } else {
-    deg[i] = s;
-    if (!(s > 0.0)) raise_status(ctl, GPIC_E_ZERO_DEGREE, i, -1, s);
+  if (threadIdx.x == 0) {
+    if (kMatvec) {
+      ((t & 1) ? y1 : y0)[i] = s;
+    } else {
+      deg[i] = s;
+      if (!(s > 0.0)) raise_status(ctl, GPIC_E_ZERO_DEGREE, i, -1, s);
+    }
+  }
   }
 }
 
@@ -151,17 +155,24 @@ int read_low_count(const unsigned long long* d_count, int64_t* out, cudaStream_t
 static double rbf_scale(const LowRows& L) { return -1.0 / (2.0 * L.sigma * L.sigma); }
 static size_t smem_bytes(int32_t d) { return (size_t)(d <= kSmemD ? d : 0) * sizeof(double); }
 
+// grid: one CTA per listed row up to kLowGrid; count < 0 = not read back
+// (the kernel strides over the device-side count, no host sync)
+constexpr int64_t kLowGrid = 296;
+static unsigned low_grid(int64_t count) {
+  return (unsigned)(count < 0 || count > kLowGrid ? kLowGrid : count);
+}
+
 void launch_lowdeg_exact(const LowRows& L, double* deg, gpic_ctl* ctl, cudaStream_t s) {
-  if (L.count < 1) return;
-  lowdeg_row_kernel<false><<<(unsigned)L.count, kLowThreads, smem_bytes(L.d), s>>>(
+  if (L.count == 0) return;
+  lowdeg_row_kernel<false><<<low_grid(L.count), kLowThreads, smem_bytes(L.d), s>>>(
       L.x, L.n, L.d, L.kind, rbf_scale(L), L.list, L.d_count, deg, nullptr, nullptr, nullptr, ctl);
   count_launch();
 }
 
 void launch_lowdeg_matvec(const LowRows& L, const double* deg, const double* v64, double* y0,
                           double* y1, gpic_ctl* ctl, cudaStream_t s) {
-  if (L.count < 1) return;
-  lowdeg_row_kernel<true><<<(unsigned)L.count, kLowThreads, smem_bytes(L.d), s>>>(
+  if (L.count == 0) return;
+  lowdeg_row_kernel<true><<<low_grid(L.count), kLowThreads, smem_bytes(L.d), s>>>(
       L.x, L.n, L.d, L.kind, rbf_scale(L), L.list, L.d_count, const_cast<double*>(deg), v64, y0,
       y1, ctl);
   count_launch();

@@ -317,7 +317,7 @@ struct LowRows {
   double sigma = 1.0;
   const int64_t* list = nullptr;              // row indices (device)
   const unsigned long long* d_count = nullptr;  // device count of list
-  int64_t count = 0;                          // host copy (0: nothing to do)
+  int64_t count = 0;  // host copy (0: nothing to do; < 0: unknown, kernels read d_count)
 };
 double low_degree_threshold(int kind, int64_t n);
 void launch_lowdeg_scan(const double* deg, int64_t n, int kind, int64_t* list,

@@ -396,7 +396,7 @@ int run_power_loops(ShardLoop* shards, int nlocal, int64_t n, int32_t max_iter, 
         if (L.mode == kLoopPackedShard || L.mode == kLoopMfShard)
           launch_slot_combine(L.slots, L.slot_stride, pt.nranks, n, L.deg_full, pt.y[pt.self][0],
                               pt.y[pt.self][1], L.ctl, cs);
-        if (L.low.count > 0)
+        if (L.low.count != 0)  // < 0: the count stays on the device
           launch_lowdeg_matvec(L.low, L.low_deg, L.v64, pt.y[pt.self][0], pt.y[pt.self][1], L.ctl,
                                cs);
         launch_iteration_tail(pt.y[pt.self][0], pt.y[pt.self][1], n, L.redpart, L.v64, L.v32,
