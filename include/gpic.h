@@ -78,7 +78,9 @@ typedef struct gpic_ctl {
   uint32_t arrive[4];  /* last-CTA-done counters                         */
   double tau;          /* current L1 normaliser                          */
   uint64_t sync_epoch; /* cross-rank exchange epoch                      */
-  uint8_t pad[256 - 96];
+  uint32_t tau_gen;    /* bumped each time the fused tail publishes tau  */
+  uint32_t reserved;
+  uint8_t pad[256 - 104];
 } gpic_ctl;
 
 /* Library identity: "gpic <version> sm_100a". */

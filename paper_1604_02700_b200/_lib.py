@@ -57,7 +57,9 @@ class Ctl(C.Structure):
         ("arrive", C.c_uint32 * 4),
         ("tau", C.c_double),
         ("sync_epoch", C.c_uint64),
-        ("pad", C.c_uint8 * (256 - 96)),
+        ("tau_gen", C.c_uint32),
+        ("reserved", C.c_uint32),
+        ("pad", C.c_uint8 * (256 - 104)),
     ]
 
 

@@ -10,6 +10,7 @@
 //   gemv (gemv.cu) y_i = (sum_j A_ij v_j) / deg_i       HBM-bound, 4n^2 bytes
 //   tau_kernel    tau = fixed-shape sum of y             (k_reduce, parallel.py:161-178)
 //   norm_kernel   v' = y / tau, delta = max|v' - v|, history, stop test
+// (in the loop both run as one tail_kernel with an in-kernel grid barrier)
 // Every reduction has a fixed shape over GLOBAL indices, so results are
 // bitwise independent of how rows are sharded across ranks.
 #include <cfloat>
@@ -112,6 +113,103 @@ __global__ void __launch_bounds__(kRedThreads)
       m = fmax(m, fabs(vn - vold[i]));
       vnew[i] = vn;
       v32[i] = (float)vn;
+    }
+  }
+  m = block_max(m, sh);
+  if (threadIdx.x == 0)
+    atomicMax(reinterpret_cast<unsigned long long*>(&ctl->delta_bits),
+              (unsigned long long)__double_as_longlong(m));
+  if (!last_block_done(&ctl->arrive[1])) return;
+  if (threadIdx.x == 0) {
+    const double delta = __longlong_as_double((long long)ctl->delta_bits);
+    hist[t] = delta;
+    ctl->delta_bits = 0ull;
+    ctl->arrive[1] = 0u;
+    const int done = t + 1;
+    ctl->iter = done;
+    if (done >= 2 && fabs(delta - hist[t - 1]) <= ctl->eps) {
+      ctl->converged = 1;
+      ctl->stop = 1;
+    } else if (done >= ctl->max_iter) {
+      ctl->stop = 1;
+    }
+  }
+}
+
+// tau_kernel + norm_kernel in one launch (loop mode). The CTAs stride over
+// the same 2048-element chunks with the same fixed-shape sums, the last CTA
+// to arrive combines the partials exactly as tau_kernel does (bitwise the
+// same tau) and publishes it by bumping ctl->tau_gen; the others spin on
+// that generation (grid <= SM count, so every CTA is resident) and then
+// normalise their chunks while y is still in L2.
+__global__ void __launch_bounds__(kRedThreads)
+    tail_kernel(const double* __restrict__ y0, const double* __restrict__ y1, int64_t n,
+                double* __restrict__ part, double* __restrict__ v64, float* __restrict__ v32,
+                double* __restrict__ hist, gpic_ctl* ctl) {
+  __shared__ double sh[kRedThreads];
+  __shared__ bool s_last;
+  __shared__ double s_tau;
+  if (*(volatile int32_t*)&ctl->stop) return;
+  const int t = ctl->iter;
+  const double* __restrict__ y = (t & 1) ? y1 : y0;
+  const unsigned gen0 = *(volatile unsigned*)&ctl->tau_gen;  // read before arriving
+  const int64_t nb = (n + kRedBlock - 1) / kRedBlock;
+  for (int64_t b = blockIdx.x; b < nb; b += gridDim.x) {
+    const int64_t b0 = b * kRedBlock;
+    double s = 0.0;
+#pragma unroll
+    for (int q = 0; q < kRedPer; ++q) {
+      const int64_t i = b0 + threadIdx.x + q * kRedThreads;
+      if (i < n) s += y[i];
+    }
+    s = block_sum_fixed(s, sh);
+    if (threadIdx.x == 0) part[b] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    s_last = atomicAdd(&ctl->arrive[0], 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (s_last) {
+    __threadfence();
+    double tt = 0.0;  // tau_kernel's last-block pattern
+    for (int64_t i = threadIdx.x; i < nb; i += kRedThreads) tt += __ldcg(part + i);
+    tt = block_sum_fixed(tt, sh);
+    if (threadIdx.x == 0) {
+      ctl->arrive[0] = 0u;
+      ctl->tau = tt;
+      s_tau = tt;
+      if (!(tt > 0.0)) raise_status(ctl, GPIC_E_NONPOS_TAU, 0, -1, tt);
+      __threadfence();
+      atomicAdd(&ctl->tau_gen, 1u);
+    }
+  } else if (threadIdx.x == 0) {
+    unsigned g;
+    for (;;) {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(g) : "l"(&ctl->tau_gen) : "memory");
+      if (g != gen0) break;
+      __nanosleep(32);
+    }
+    s_tau = *(volatile double*)&ctl->tau;
+  }
+  __syncthreads();
+  if (*(volatile int32_t*)&ctl->stop) return;  // NonPositiveTau
+  const double tau = s_tau;
+  const double* __restrict__ vold = v64 + (int64_t)(t & 1) * n;
+  double* __restrict__ vnew = v64 + (int64_t)((t + 1) & 1) * n;
+  double m = 0.0;
+  for (int64_t b = blockIdx.x; b < nb; b += gridDim.x) {
+    const int64_t b0 = b * kRedBlock;
+#pragma unroll
+    for (int q = 0; q < kRedPer; ++q) {
+      const int64_t i = b0 + threadIdx.x + q * kRedThreads;
+      if (i < n) {
+        const double vn = y[i] / tau;
+        m = fmax(m, fabs(vn - vold[i]));
+        vnew[i] = vn;
+        v32[i] = (float)vn;
+      }
     }
   }
   m = block_max(m, sh);
@@ -244,9 +342,24 @@ void launch_slot_combine(const double* slots, int64_t stride, int nranks, int64_
 void launch_iteration_tail(const double* y0, const double* y1, int64_t n, double* redpart,
                            double* v64, float* v32, double* hist, gpic_ctl* ctl, cudaStream_t s) {
   const unsigned nb = (unsigned)ceil_div(n, kRedBlock);
-  tau_kernel<<<nb, kRedThreads, 0, s>>>(y0, y1, n, redpart, nullptr, ctl, 1);
-  norm_kernel<<<nb, kRedThreads, 0, s>>>(y0, y1, n, v64, v32, hist, ctl);
-  count_launch(2);
+  static const bool split = [] {
+    const char* e = getenv("GPIC_TAIL_SPLIT");  // 1: the two-kernel tail (A/B)
+    return e != nullptr && atoi(e) != 0;
+  }();
+  if (split) {
+    tau_kernel<<<nb, kRedThreads, 0, s>>>(y0, y1, n, redpart, nullptr, ctl, 1);
+    norm_kernel<<<nb, kRedThreads, 0, s>>>(y0, y1, n, v64, v32, hist, ctl);
+    count_launch(2);
+    return;
+  }
+  static const unsigned sms = [] {
+    int dev = 0, v = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return (unsigned)v;
+  }();
+  tail_kernel<<<nb < sms ? nb : sms, kRedThreads, 0, s>>>(y0, y1, n, redpart, v64, v32, hist, ctl);
+  count_launch();
 }
 
 // Timeouts: a per-iteration wait (add_iter) covers one GEMV of the slowest

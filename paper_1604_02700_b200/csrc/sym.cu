@@ -630,27 +630,46 @@ __global__ void __launch_bounds__(kTS)
   const int64_t ncol = Q + 1, terms = ncol + (ns - Q);
   const int32_t* tl = sp.tlist + Q * sp.tld;
   const int L = sp.tcount[Q];
+  const int64_t i = R * kTS + o;
+  const double di = deg != nullptr && i < n ? deg[i] : 1.0;  // in flight with the partials
   double t = 0.0, seg_sum = 0.0;
   int sg = 0;
   int64_t p1 = terms / kSeg;  // end of segment 0
-  for (int e = 0; e < L; ++e) {
-    const int64_t p = tl[e];
-    while (p >= p1) {  // close the segments before p, in order
-      t += seg_sum;
-      seg_sum = 0.0;
-      ++sg;
-      p1 = terms * (sg + 1) / kSeg;
+  // kBatch independent loads in flight per thread, then the in-order adds
+  // (the loads, not the adds, are the latency: ~40 records per row)
+  constexpr int kBatch = 16;
+  for (int e0 = 0; e0 < L; e0 += kBatch) {
+    // unconditional (clamped) loads: a guarded load becomes a branch that
+    // serialises load and use
+    float val[kBatch];
+    int32_t pp[kBatch];
+#pragma unroll
+    for (int j = 0; j < kBatch; ++j) pp[j] = tl[min(e0 + j, L - 1)];
+#pragma unroll
+    for (int j = 0; j < kBatch; ++j) {
+      const int64_t p = pp[j];
+      const int64_t sbi = p < ncol ? tile_index(p, Q, ns) : tile_index(Q, Q + (p - ncol), ns);
+      const float* src = p < ncol ? colp : rowp;
+      val[j] = __ldcs(src + (sbi * kSB + k) * kTS + o);
     }
-    const int64_t sbi = p < ncol ? tile_index(p, Q, ns) : tile_index(Q, Q + (p - ncol), ns);
-    seg_sum += (double)(p < ncol ? colp[(sbi * kSB + k) * kTS + o] : rowp[(sbi * kSB + k) * kTS + o]);
+#pragma unroll
+    for (int j = 0; j < kBatch; ++j) {
+      if (e0 + j >= L) break;
+      while (pp[j] >= p1) {  // close the segments before p, in order
+        t += seg_sum;
+        seg_sum = 0.0;
+        ++sg;
+        p1 = terms * (sg + 1) / kSeg;
+      }
+      seg_sum += (double)val[j];
+    }
   }
   for (; sg < kSeg; ++sg) {
     t += seg_sum;
     seg_sum = 0.0;
   }
-  const int64_t i = R * kTS + o;
   if (i < n) {
-    const double val = deg != nullptr ? t / deg[i] : t;
+    const double val = deg != nullptr ? t / di : t;
     const int parity = ctl != nullptr ? (ctl->iter & 1) : 0;
     for (int r = 0; r < pt.nranks; ++r) pt.y[r][parity][i] = val;
   }
@@ -695,28 +714,52 @@ __global__ void __launch_bounds__(kTS)
       p1 = nt * (sg + 1) / kSeg;
     }
   };
+  // per term: every live tile's partials loaded first (up to 4 tiles x 4
+  // values in flight), then added in the order of the one-at-a-time walk
   for (int e = 0; e < L; ++e) {
     const int64_t term = tl[e];
-    if (term < ncol) {  // super-block (term, Q): tiles (p, R), p < R
+    float c[kSB][4];
+    bool live[kSB];
+    int64_t p0;
+    const bool col = term < ncol;
+    if (col) {  // super-block (term, Q): tiles (p, R), p < R
       const int64_t P = term;
       const Sparse::Rec rec = sp.record(tile_index(P, Q, ns));
       const int64_t pe = min(min(kSB * P + kSB, R), nt);
-      for (int64_t p = kSB * P; p < pe; ++p) {
-        if (Sparse::mask_of(rec, (int)((p - kSB * P) * kSB + k)) == 0u) continue;
-        to_segment(p);
-        const float* c = degcol + tile_index(p, R, nt) * 4 * kTS + o;
-        seg += (double)c[0] + (double)c[kTS] + (double)c[2 * kTS] + (double)c[3 * kTS];
+      p0 = kSB * P;
+#pragma unroll
+      for (int j = 0; j < kSB; ++j) {
+        const int64_t p = p0 + j;
+        live[j] = p < pe && Sparse::mask_of(rec, (int)(j * kSB + k)) != 0u;
+        // unconditional loads (a dead slot reads a valid dummy address):
+        // guarded loads compile to branches that serialise load and use
+        const float* src = degcol + (live[j] ? tile_index(p, R, nt) * 4 * kTS : 0) + o;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) c[j][q] = src[q * kTS];
       }
     } else {  // super-block (Q, Q'): tiles (R, p), p >= R
       const int64_t Qp = Q + (term - ncol);
       const Sparse::Rec rec = sp.record(tile_index(Q, Qp, ns));
       const int64_t pe = min(kSB * Qp + kSB, nt);
-      for (int64_t p = max(kSB * Qp, R); p < pe; ++p) {
-        if (Sparse::mask_of(rec, (int)(k * kSB + (p - kSB * Qp))) == 0u) continue;
-        to_segment(p);
-        const float* r = degrow + tile_index(R, p, nt) * nhalf * kTS + o;
-        seg += (double)r[0];
-        if (nhalf == 2) seg += (double)r[kTS];
+      p0 = kSB * Qp;
+#pragma unroll
+      for (int j = 0; j < kSB; ++j) {
+        const int64_t p = p0 + j;
+        live[j] = p >= R && p < pe && Sparse::mask_of(rec, (int)(k * kSB + j)) != 0u;
+        const float* src = degrow + (live[j] ? tile_index(R, p, nt) * nhalf * kTS : 0) + o;
+        c[j][0] = src[0];
+        c[j][1] = src[(nhalf - 1) * kTS];
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < kSB; ++j) {
+      if (!live[j]) continue;
+      to_segment(p0 + j);
+      if (col) {
+        seg += (double)c[j][0] + (double)c[j][1] + (double)c[j][2] + (double)c[j][3];
+      } else {
+        seg += (double)c[j][0];
+        if (nhalf == 2) seg += (double)c[j][1];
       }
     }
   }
