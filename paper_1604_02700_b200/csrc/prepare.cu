@@ -133,14 +133,27 @@ __global__ void mean_kernel(const double* __restrict__ colpart, int64_t nblk, in
 
 // max |x - mean| over all finite entries -> mean[d] (non-negative doubles
 // order like their bit patterns, so an integer atomicMax is exact)
-__global__ void maxabs_kernel(const double* __restrict__ x, int64_t n, int32_t d,
-                              double* __restrict__ mean) {
+// A warp per row (lanes over the features, no index division), four rows
+// of loads in flight per warp.
+__global__ void __launch_bounds__(256)
+    maxabs_kernel(const double* __restrict__ x, int64_t n, int32_t d,
+                  double* __restrict__ mean) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t stride = (int64_t)gridDim.x * 8;
   double m = 0.0;
-  const int64_t total = n * d;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const double v = x[i];
-    if (isfinite(v)) m = fmax(m, fabs(v - mean[i % d]));
+  for (int64_t r0 = (int64_t)blockIdx.x * 8 + warp; r0 < n; r0 += 4 * stride) {
+    for (int f = lane; f < d; f += 32) {
+      const double mf = mean[f];
+      double v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t row = r0 + u * stride;
+        v[u] = row < n ? x[row * d + f] : mf;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (isfinite(v[u])) m = fmax(m, fabs(v[u] - mf));
+    }
   }
   m = warp_max_f64(m);
   if ((threadIdx.x & 31) == 0)
@@ -183,36 +196,59 @@ __global__ void __launch_bounds__(256)
   const double s = operand_scale(mean[d]);
   const int64_t plane = n_pad * 16;
   double spread = 0.0;
-  for (int64_t row = (int64_t)blockIdx.x * 8 + warp; row < n_pad; row += (int64_t)gridDim.x * 8) {
-    double sq = 0.0, sqs = 0.0;
+  // two rows per warp pass (both rows' loads in flight together)
+  constexpr int kR = 2;
+  const int64_t step = (int64_t)gridDim.x * 8 * kR;
+  for (int64_t row0 = ((int64_t)blockIdx.x * 8 + warp) * kR; row0 < n_pad; row0 += step) {
+    double sq[kR], sqs[kR];
+#pragma unroll
+    for (int u = 0; u < kR; ++u) sq[u] = sqs[u] = 0.0;
     for (int f = lane; f < dp; f += 32) {
-      double c = 0.0;
-      if (row < n && f < d) {
-        double v = x[row * d + f];
-        if (!isfinite(v)) v = mean[f];
-        c = v - mean[f];
+      double c[kR];
+#pragma unroll
+      for (int u = 0; u < kR; ++u) {
+        const int64_t row = row0 + u;
+        c[u] = 0.0;
+        if (row < n && f < d) {
+          double v = x[row * d + f];
+          if (!isfinite(v)) v = mean[f];
+          c[u] = v - mean[f];
+        }
       }
-      const float xc = (float)c;
-      xc_out[row * dp + f] = xc;
-      const double t = split16(c * s, hi, lo, row * dp + f);
-      sq += (double)xc * (double)xc;
-      sqs += t * t;  // |x~ s|^2 of the split operands
+#pragma unroll
+      for (int u = 0; u < kR; ++u) {
+        const int64_t row = row0 + u;
+        if (row >= n_pad) break;
+        const float xc = (float)c[u];
+        xc_out[row * dp + f] = xc;
+        const double t = split16(c[u] * s, hi, lo, row * dp + f);
+        sq[u] += (double)xc * (double)xc;
+        sqs[u] += t * t;  // |x~ s|^2 of the split operands
+      }
     }
-    sq = warp_sum_f64(sq);
-    sqs = warp_sum_f64(sqs);
-    if (lane == 0) sqn[row] = row == n_pad - 1 ? (float)(1.0 / (s * s)) : (float)sq;
-    if (row < n) spread = fmax(spread, sq);  // spread R^2 for the engine routing
-    // norm block: lanes 0-15 write k = lane of the row / column operands
-    __half* nb = lo + n_pad * dp + row * 16 + lane;
-    if (lane < 16) {
-      const double m = row < n ? -0.5 * sqs / 1024.0 : 0.0;
-      const __half mh = __float2half_rn((float)m);
-      const __half ml = __float2half_rn((float)(m - (double)__half2float(mh)));
-      const __half one = __float2half_rn(1024.f), zero = __float2half_rn(0.f);
-      nb[0] = lane == 0 ? one : (lane == 1 ? mh : zero);          // row operand hi
-      nb[plane] = lane == 1 ? ml : zero;                           // row operand lo
-      nb[2 * plane] = lane == 0 ? mh : (lane == 1 ? one : zero);   // column operand hi
-      nb[3 * plane] = lane == 0 ? ml : zero;                       // column operand lo
+#pragma unroll
+    for (int u = 0; u < kR; ++u) {
+      sq[u] = warp_sum_f64(sq[u]);
+      sqs[u] = warp_sum_f64(sqs[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < kR; ++u) {
+      const int64_t row = row0 + u;
+      if (row >= n_pad) break;
+      if (lane == 0) sqn[row] = row == n_pad - 1 ? (float)(1.0 / (s * s)) : (float)sq[u];
+      if (row < n) spread = fmax(spread, sq[u]);  // spread R^2 for the engine routing
+      // norm block: lanes 0-15 write k = lane of the row / column operands
+      __half* nb = lo + n_pad * dp + row * 16 + lane;
+      if (lane < 16) {
+        const double m = row < n ? -0.5 * sqs[u] / 1024.0 : 0.0;
+        const __half mh = __float2half_rn((float)m);
+        const __half ml = __float2half_rn((float)(m - (double)__half2float(mh)));
+        const __half one = __float2half_rn(1024.f), zero = __float2half_rn(0.f);
+        nb[0] = lane == 0 ? one : (lane == 1 ? mh : zero);          // row operand hi
+        nb[plane] = lane == 1 ? ml : zero;                           // row operand lo
+        nb[2 * plane] = lane == 0 ? mh : (lane == 1 ? one : zero);   // column operand hi
+        nb[3 * plane] = lane == 0 ? ml : zero;                       // column operand lo
+      }
     }
   }
   if (lane == 0) wmax[warp] = spread;
@@ -289,8 +325,10 @@ void launch_prepare(const double* x, int64_t n, int32_t d, float* xhi, float* xl
   }
   mean_kernel<<<(unsigned)ceil_div(d, 32), 256, 0, s>>>(colpart, nblk, n, d, mean);
   const int64_t mblk = ceil_div(n * d, 256);
-  maxabs_kernel<<<(unsigned)(mblk < 1184 ? mblk : 1184), 256, 0, s>>>(x, n, d, mean);
-  const int64_t cblk = ceil_div(n_pad, 8);
+  (void)mblk;
+  const int64_t xblk = ceil_div(n, 32);  // 8 warps x 4 rows per CTA pass
+  maxabs_kernel<<<(unsigned)(xblk < 1184 ? xblk : 1184), 256, 0, s>>>(x, n, d, mean);
+  const int64_t cblk = ceil_div(n_pad, 16);
   center_split_kernel<<<(unsigned)(cblk < 148 * 8 ? cblk : 148 * 8), 256, 0, s>>>(
       x, n, d, dp, n_pad, mean, planes, xlo, sqn);
   count_launch(4);

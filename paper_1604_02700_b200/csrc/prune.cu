@@ -204,10 +204,14 @@ __global__ void __launch_bounds__(256)
   const int64_t r0 = (int64_t)blockIdx.x * kGemmRows;
   const int64_t S = r0 / B;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  for (int e = tid; e < kGemmRows * dp; e += 256) {
-    const int r = e / dp, f = e % dp;
+  // float4 copies, a warp per row (dp is a multiple of 64: no index division)
+  for (int r = warp; r < kGemmRows; r += 8) {
     const int64_t row = r0 + r;
-    sX[r * ldx + f] = row < n ? xc[row * dp + f] : 0.f;
+    for (int f = lane * 4; f < dp; f += 128) {
+      const float4 v = row < n ? *reinterpret_cast<const float4*>(xc + row * dp + f)
+                               : make_float4(0.f, 0.f, 0.f, 0.f);
+      *reinterpret_cast<float4*>(sX + r * ldx + f) = v;
+    }
   }
   __syncthreads();
   // own products and norms: a warp per 16 rows, lanes over the features
@@ -236,10 +240,18 @@ __global__ void __launch_bounds__(256)
   }
   for (int64_t c0 = 0; c0 < nb; c0 += kGemmCols) {
     __syncthreads();  // the previous chunk's products are consumed
-    for (int e = tid; e < kGemmCols * dp; e += 256) {
-      const int c = e / dp, f = e % dp;
+    for (int c = warp; c < kGemmCols; c += 8) {
       const int64_t col = c0 + c;
-      sU[c * ldx + f] = col < nb ? cent[col * dp + f] : 0.f;
+      for (int f = lane * 4; f < dp; f += 128) {
+        float4 v = col < nb ? *reinterpret_cast<const float4*>(cent + col * dp + f)
+                            : make_float4(0.f, 0.f, 0.f, 0.f);
+        // rounded to TF32 once here, not in every warp's fragments
+        v.x = wmma::__float_to_tf32(v.x);
+        v.y = wmma::__float_to_tf32(v.y);
+        v.z = wmma::__float_to_tf32(v.z);
+        v.w = wmma::__float_to_tf32(v.w);
+        *reinterpret_cast<float4*>(sU + c * ldx + f) = v;
+      }
     }
     __syncthreads();
     wmma::fragment<wmma::accumulator, 16, 16, 8, float> acc[4];
@@ -253,9 +265,7 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         wmma::fragment<wmma::matrix_b, 16, 16, 8, wmma::precision::tf32, wmma::col_major> b;
-        wmma::load_matrix_sync(b, sU + j * 16 * ldx + kk, ldx);
-#pragma unroll
-        for (int t = 0; t < b.num_elements; ++t) b.x[t] = wmma::__float_to_tf32(b.x[t]);
+        wmma::load_matrix_sync(b, sU + j * 16 * ldx + kk, ldx);  // already TF32
         wmma::mma_sync(acc[j], a, b, acc[j]);
       }
     }
@@ -289,20 +299,26 @@ __global__ void fill_u32_kernel(unsigned* p, int64_t count, unsigned v) {
 __global__ void pair_skip_kernel(const float* __restrict__ cent, const unsigned* __restrict__ mmax,
                                  const unsigned* __restrict__ scal, int64_t nb, int32_t dp,
                                  int32_t d, double d2_thr, int tf32, uint8_t* __restrict__ skip) {
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  // a warp per block pair, lanes over the features (coalesced rows);
+  // the summation order of |u|^2 only moves the bound by ~1e-16 relative,
+  // far inside its (1 - 1e-6) margin — and a skip is safe either way
+  const int lane = threadIdx.x & 31;
+  const int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (t >= nb * nb) return;
-  const int64_t S = t / nb, T = t % nb;
+  const int64_t S = t / nb, T = t - S * nb;
   if (S == T) {
-    skip[t] = 0;
+    if (lane == 0) skip[t] = 0;
     return;
   }
   const float* a = cent + S * dp;
   const float* b = cent + T * dp;
   double u2 = 0.0;
-  for (int f = 0; f < dp; ++f) {
+  for (int f = lane; f < dp; f += 32) {
     const double q = (double)b[f] - (double)a[f];
     u2 += q * q;
   }
+  u2 = warp_sum_f64(u2);
+  if (lane != 0) return;
   const double gap = -((double)ord2f(mmax[S * nb + T]) + (double)ord2f(mmax[T * nb + S]));
   const double xm = (double)__uint_as_float(scal[1]), cm = (double)__uint_as_float(scal[0]);
   // |dot error| <= (operand rounding + d fp32 adds) |x| |c| per product,
@@ -574,7 +590,7 @@ void launch_prune(const PruneMask& m, const float* xc, const double* colpart, co
     proj_max_kernel<<<pg, 256, 0, s>>>(xc, n, dp, B, nb, m.cent, m.own, m.mmax);
   }
   const double d2_thr = kSkipLog2 * 2.0 * sigma * sigma / 1.4426950408889634 * (1.0 + 1e-6);
-  pair_skip_kernel<<<(unsigned)ceil_div(nb * nb, 256), 256, 0, s>>>(m.cent, m.mmax, m.scal, nb, dp,
+  pair_skip_kernel<<<(unsigned)ceil_div(nb * nb, 8), 256, 0, s>>>(m.cent, m.mmax, m.scal, nb, dp,
                                                                     d, d2_thr, tf32, m.skip);
   if (mb <= 0) {  // matrix-free: the item list instead of the unit list
     ItemGeom g;

@@ -92,24 +92,38 @@ __global__ void sb_weight_kernel(const uint8_t* __restrict__ boxnz, int64_t nt,
 // coalesced 1024-element chunks (block scan + running carry)
 __global__ void __launch_bounds__(kScanThreads)
     sb_scan_kernel(int64_t nt, int64_t* __restrict__ prefix) {
-  __shared__ int64_t sh[kScanThreads];
+  // each thread a contiguous segment: its sum, one warp-shuffle block scan of
+  // the segment sums, then the segment rewritten from its offset
+  __shared__ int64_t wsum[kScanThreads / 32];
   const int64_t ns = (nt + kSB - 1) / kSB;
   const int64_t count = ns * (ns + 1) / 2;
-  const int t = threadIdx.x;
-  int64_t carry = 0;
-  for (int64_t c0 = 0; c0 < count; c0 += kScanThreads) {
-    const int64_t i = c0 + t;
-    sh[t] = i < count ? prefix[i + 1] : 0;
-    __syncthreads();
-    for (int o = 1; o < kScanThreads; o <<= 1) {
-      const int64_t add = t >= o ? sh[t - o] : 0;
-      __syncthreads();
-      sh[t] += add;
-      __syncthreads();
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  const int64_t seg = (count + kScanThreads - 1) / kScanThreads;
+  const int64_t a = min(count, t * seg), b = min(count, a + seg);
+  int64_t c = 0;
+  for (int64_t i = a; i < b; ++i) c += prefix[i + 1];
+  int64_t incl = c;  // inclusive scan within the warp
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int64_t y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) wsum[w] = incl;
+  __syncthreads();
+  if (w == 0) {
+    int64_t v = lane < kScanThreads / 32 ? wsum[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t y = __shfl_up_sync(0xffffffffu, v, o);
+      if (lane >= o) v += y;
     }
-    if (i < count) prefix[i + 1] = carry + sh[t];
-    carry += sh[kScanThreads - 1];
-    __syncthreads();
+    if (lane < kScanThreads / 32) wsum[lane] = v;  // inclusive over warps
+  }
+  __syncthreads();
+  int64_t run = (w > 0 ? wsum[w - 1] : 0) + incl - c;  // exclusive offset of the segment
+  for (int64_t i = a; i < b; ++i) {
+    run += prefix[i + 1];
+    prefix[i + 1] = run;
   }
 }
 
