@@ -266,6 +266,8 @@ struct SbList {
   const int32_t* tlist = nullptr;
   const int32_t* tcount = nullptr;
   int64_t tld = 0;
+  // the GEMV's dynamic schedule counters (2 words, zeroed by sb_list_kernel)
+  unsigned* sched = nullptr;
 };
 void launch_reduce_terms(const int64_t* sb_prefix, int64_t nt, int32_t* tlist, int32_t* tcount,
                          int64_t tld, cudaStream_t s);

@@ -161,6 +161,9 @@ __global__ void __launch_bounds__(kScanThreads)
   if (t == kScanThreads - 1) {
     *count = sh[t];
     lpre[sh[t]] = prefix[total];
+    unsigned* sched = reinterpret_cast<unsigned*>(reinterpret_cast<uint8_t*>(count) + 64);
+    sched[0] = 0u;  // the GEMV's dynamic schedule (sym.cu)
+    sched[1] = 0u;
   }
   // the GEMV's CTA ranges over the list for a grid of `grid` CTAs (equal
   // shares of weight, the kernel's own lower_bound), so its CTAs start
@@ -216,6 +219,7 @@ SbList sb_list(const int64_t* sb_prefix, int64_t n) {
   const uint8_t* p = reinterpret_cast<const uint8_t*>(sb_prefix) + al((nsb + 1) * 8) +
                      al(nsb * kSB * kSB * 2);
   L.count = reinterpret_cast<const int64_t*>(p);
+  L.sched = reinterpret_cast<unsigned*>(const_cast<uint8_t*>(p) + 64);  // same 256-byte slot
   p += al(8);
   L.lpre = reinterpret_cast<const int64_t*>(p);
   p += al((nsb + 1) * 8);

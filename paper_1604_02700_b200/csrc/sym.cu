@@ -98,6 +98,10 @@ struct Sparse {
   const int32_t* tlist;
   const int32_t* tcount;
   int64_t tld;
+  // dynamic GEMV schedule (list mode): [0] next list entry to claim, [1]
+  // CTAs past their last claim (the last one resets both); or null: the
+  // static weight ranges
+  unsigned* sched;
   // the 16 tile masks of super-block s (two 16-byte loads), kept in
   // registers: selected by comparisons, never indexed (an indexed array
   // went to local memory)
@@ -307,7 +311,24 @@ __global__ void __launch_bounds__(kThreads, 1)
   // records are indexed from sb_lo, tiles from the shard's first tile
   const int64_t sb_lo = sr.sb_lo(ns), total = sr.sb_hi(ns) - sb_lo;
   SbCursor cur0;
-  if (sp.list != nullptr) {
+  // dynamic schedule: super-blocks are claimed one at a time from the list
+  // (atomic counter); the producer passes each claim to the consumers
+  // through a small ring in shared memory. A super-block's records are
+  // the same whichever CTA computes it, so results stay bitwise identical.
+  const bool dyn = sp.list != nullptr && sp.sched != nullptr;
+  constexpr int kQ = 4;
+  __shared__ int32_t q_entry[kQ];
+  __shared__ __align__(8) uint64_t q_full[kQ], q_empty[kQ];
+  if (dyn) {
+    if (threadIdx.x == 0) {
+      for (int q = 0; q < kQ; ++q) {
+        mbar_init(&q_full[q], 1);
+        mbar_init(&q_empty[q], kWarps);
+      }
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+  } else if (sp.list != nullptr) {
     // the non-empty super-blocks only, equal shares of their weight (cut
     // in advance by sb_list_kernel when it used this grid size)
     int64_t e0, e1;
@@ -342,6 +363,47 @@ __global__ void __launch_bounds__(kThreads, 1)
   w.nt = nt;
   w.ns = ns;
 
+  if (warp == kWarps && dyn) {  // producer, dynamic schedule
+    if (lane != 0) return;
+    int s = 0, q = 0;
+    uint32_t ph = 0, qph = 0;
+    const uint8_t* src0 = reinterpret_cast<const uint8_t*>(tiles);
+    const uint64_t stream_pol = policy_evict_first();
+    const int64_t cnt = *sp.lcount;
+    for (;;) {
+      const int64_t e = (int64_t)atomicAdd(sp.sched, 1u);
+      const bool end = e >= cnt;
+      mbar_wait(&q_empty[q], qph ^ 1);
+      q_entry[q] = end ? -1 : (int32_t)e;
+      mbar_arrive(&q_full[q]);
+      if (++q == kQ) { q = 0; qph ^= 1; }
+      if (end) break;
+      SbCursor c1;
+      c1.begin_list(sp.list, e, e + 1, ns);
+      TileEnum cur;
+      cur.begin(c1, nt);
+      for (;;) {
+        const int64_t t = cur.next(sp);
+        if (t < 0) break;
+        mbar_wait(&empty[s], ph ^ 1);
+        mbar_expect_tx(&full[s], kTileBytes);
+        if (sp.evict_first)
+          bulk_load(st + s * kTileBytes, src0 + (t - sr.tile_base) * kTileBytes, kTileBytes,
+                    &full[s], stream_pol);
+        else
+          bulk_load(st + s * kTileBytes, src0 + (t - sr.tile_base) * kTileBytes, kTileBytes,
+                    &full[s]);
+        if (++s == kStages) { s = 0; ph ^= 1; }
+      }
+    }
+    // every CTA has made its last claim once all have counted in: the last
+    // one resets the schedule for the next launch
+    if (atomicAdd(sp.sched + 1, 1u) == gridDim.x - 1) {
+      atomicExch(sp.sched, 0u);
+      atomicExch(sp.sched + 1, 0u);
+    }
+    return;
+  }
   if (warp == kWarps) {  // producer
     if (lane != 0) return;
     int s = 0;
@@ -386,6 +448,18 @@ __global__ void __launch_bounds__(kThreads, 1)
   Sparse::Rec rec{};
   Sparse cs = sp;  // the consumers' view
   if (!sp.bits_consumer) cs.bits = nullptr;
+  int q = 0;
+  uint32_t qph = 0;
+  for (;;) {
+  if (dyn) {  // the producer's next claim
+    mbar_wait(&q_full[q], qph);
+    const int32_t e = q_entry[q];
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&q_empty[q]);
+    if (++q == kQ) { q = 0; qph ^= 1; }
+    if (e < 0) break;
+    cur0.begin_list(sp.list, e, e + 1, ns);
+  }
   for (SbCursor cur = cur0; cur.valid(); cur.step()) {
     const int64_t sb = cur.sb;
     // no stored tile: its records are never read
@@ -523,6 +597,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         colp[((sb - sb_lo) * kSB + c) * kTS + t] = sum;
       }
     rb ^= 1;
+  }
+  if (!dyn) break;
   }
 }
 
@@ -924,6 +1000,14 @@ int gemv_use_list() {
   return e != nullptr ? atoi(e) : 1;
 }
 
+// GPIC_GEMV_DYN=0: static CTA ranges by super-block weight instead of the
+// dynamic claims (A/B; measured at config 3: SM busy time max / mean 1.28
+// with the static ranges)
+int gemv_dynamic() {
+  const char* e = getenv("GPIC_GEMV_DYN");
+  return e != nullptr ? atoi(e) : 1;
+}
+
 int gemv_evict_first() {
   const char* e = getenv("GPIC_GEMV_EVICT");
   return e != nullptr ? atoi(e) : 1;
@@ -947,12 +1031,12 @@ void launch_sym_degree(const float* degrow, const float* degcol, int64_t n, int 
     // the per-super-row term lists and box records of the sparse prefix pass
     const SbList sl = sb_list(sb_prefix, n);
     const Sparse lp{boxnz, sb_prefix, sb_bits(sb_prefix, n), 0, 0, 0, sl.list, sl.lpre, sl.count,
-                    sl.ranges, sl.tlist, sl.tcount, sl.tld};
+                    sl.ranges, sl.tlist, sl.tcount, sl.tld, nullptr};
     sym_degree_list_kernel<<<(unsigned)nt, kTS, 0, s>>>(degrow, degcol, n, nt, nhalf, deg, ctl, lp);
     count_launch();
     return;
   }
-  const Sparse sp{boxnz, nullptr, nullptr, 0, 0, 0, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 0};
+  const Sparse sp{boxnz, nullptr, nullptr, 0, 0, 0, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 0, nullptr};
   const size_t dyn = boxnz != nullptr ? (size_t)nt * 4 : 0;  // the live-tile list
   if (dyn > 48 * 1024)
     cudaFuncSetAttribute(sym_degree_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
@@ -1000,10 +1084,11 @@ void launch_sym_gemv(const float* tiles, int64_t n, const float* v32, float* row
   const int bits_mode = getenv("GPIC_SB_BITS") != nullptr ? atoi(getenv("GPIC_SB_BITS")) : 1;
   const SbList sl = boxnz != nullptr && whole && gemv_use_list() ? sb_list(sb_prefix, n)
                                                                   : SbList{nullptr, nullptr, nullptr};
-  const Sparse sp{boxnz, boxnz != nullptr ? sb_prefix : nullptr,
-                  boxnz != nullptr && whole && bits_mode != 0 ? sb_bits(sb_prefix, n) : nullptr,
-                  gemv_prefetch(), bits_mode == 1, gemv_evict_first(), sl.list, sl.lpre, sl.count,
-                  sl.ranges, sl.tlist, sl.tcount, sl.tld};
+  Sparse sp{boxnz, boxnz != nullptr ? sb_prefix : nullptr,
+            boxnz != nullptr && whole && bits_mode != 0 ? sb_bits(sb_prefix, n) : nullptr,
+            gemv_prefetch(), bits_mode == 1, gemv_evict_first(), sl.list, sl.lpre, sl.count,
+            sl.ranges, sl.tlist, sl.tcount, sl.tld, nullptr};
+  if (sl.list != nullptr && gemv_dynamic() && gemv_prefetch() == 0) sp.sched = sl.sched;
   sym_prepare();
   const int64_t nt = ceil_div(n, kTS);
   const int64_t ns = (nt + kSB - 1) / kSB;
@@ -1024,10 +1109,11 @@ void launch_sym_gemv16(const void* tiles, int64_t n, const float* v32, float* ro
                        const uint8_t* boxnz, const int64_t* sb_prefix) {
   const SbList sl = boxnz != nullptr && gemv_use_list() ? sb_list(sb_prefix, n)
                                                         : SbList{nullptr, nullptr, nullptr};
-  const Sparse sp{boxnz, boxnz != nullptr ? sb_prefix : nullptr,
-                  boxnz != nullptr ? sb_bits(sb_prefix, n) : nullptr, gemv_prefetch(), 0,
-                  gemv_evict_first(), sl.list, sl.lpre, sl.count, sl.ranges, sl.tlist, sl.tcount,
-                  sl.tld};
+  Sparse sp{boxnz, boxnz != nullptr ? sb_prefix : nullptr,
+            boxnz != nullptr ? sb_bits(sb_prefix, n) : nullptr, gemv_prefetch(), 0,
+            gemv_evict_first(), sl.list, sl.lpre, sl.count, sl.ranges, sl.tlist, sl.tcount,
+            sl.tld, nullptr};
+  if (sl.list != nullptr && gemv_dynamic() && gemv_prefetch() == 0) sp.sched = sl.sched;
   sym_prepare();
   const int64_t nt = ceil_div(n, kTS);
   const int64_t ns = (nt + kSB - 1) / kSB;
