@@ -174,6 +174,66 @@ struct TcArgs {
   int64_t pB, pnb;
   const int64_t* wpre;  // matvec listed: kept tiles before each item (CTA balance)
   int share_r, share_n;  // matvec listed across ranks: this rank's tile-balanced share
+  // listed runs: [0] claim counter, [1] CTAs done claiming (the last resets
+  // both) — list ranges are claimed at run time instead of split in advance;
+  // null: the static split
+  unsigned* sched;
+};
+
+// Claim k of a dynamic run over list entries [lo, hi) on G CTAs: G claims
+// of 5/8 of an equal share, 2G of 1/8, then 1/64-share claims to the end
+// (large first claims keep row blocks contiguous, small last ones even out
+// the finish). false: nothing left.
+__device__ inline bool claim_range(int64_t k, int64_t lo, int64_t hi, int64_t G, int64_t& e0,
+                                   int64_t& e1) {
+  const int64_t n = hi - lo;
+  const int64_t s1 = max((int64_t)1, n * 5 / (8 * G)), s2 = max((int64_t)1, n / (8 * G));
+  const int64_t s3 = max((int64_t)1, n / (64 * G));
+  int64_t off, sz;
+  if (k < G) {
+    off = k * s1;
+    sz = s1;
+  } else if (k < 3 * G) {
+    off = G * s1 + (k - G) * s2;
+    sz = s2;
+  } else {
+    off = G * s1 + 2 * G * s2 + (k - 3 * G) * s3;
+    sz = s3;
+  }
+  e0 = lo + off;
+  if (e0 >= hi) return false;
+  e1 = min(e0 + sz, hi);
+  return true;
+}
+
+// The producer's claims reach the MMA issuer and the epilogue warps through
+// a 4-slot ring in the barrier area: [0] = first entry (-1: no more), [1] = end.
+constexpr int kFeedSlots = 4;
+struct Feed {
+  uint64_t* full;   // [kFeedSlots], count 1 (the producer)
+  uint64_t* empty;  // [kFeedSlots], count 1 + kEpiWarps (MMA issuer + epilogue warps)
+  int32_t* rng;     // [kFeedSlots][2]
+  int q = 0;
+  uint32_t ph = 0;
+  // reader: the next range (false: the run is over); `arrive`: this thread
+  // releases the slot (lane 0 of a reading warp)
+  __device__ bool read(int64_t& e0, int64_t& e1, bool arrive) {
+    mbar_wait(&full[q], ph);
+    const int32_t a = rng[2 * q], b = rng[2 * q + 1];
+    __syncwarp(__activemask());
+    if (arrive) mbar_arrive(&empty[q]);
+    if (++q == kFeedSlots) { q = 0; ph ^= 1; }
+    e0 = a;
+    e1 = b;
+    return a >= 0;
+  }
+  __device__ void write(int64_t e0, int64_t e1) {
+    mbar_wait(&empty[q], ph ^ 1);
+    rng[2 * q] = (int32_t)e0;
+    rng[2 * q + 1] = (int32_t)e1;
+    mbar_arrive(&full[q]);
+    if (++q == kFeedSlots) { q = 0; ph ^= 1; }
+  }
 };
 
 // [ua, ub): the list entries of rank share_r of share_n, tile-balanced
@@ -374,6 +434,10 @@ struct Cursor {
   }
 };
 
+// the feed ring sits behind the pipeline barriers and the TMEM slot word
+// (2 ST + 8 words; with ST <= 4 it ends within the 256-byte barrier area)
+__device__ inline uint64_t* tmem_slot_bars(uint64_t* bars, int st) { return bars + 2 * st + 8; }
+
 template <int MB, int MODE>
 __host__ __device__ inline int64_t total_units(const TcArgs& a) {
   if (is_packed(MODE)) return packed_items(a.n_rtiles, a.n_ctiles, MB);
@@ -426,7 +490,21 @@ __global__ void __launch_bounds__(kCtaThreads<MODE>, 1)
                                         : lower_bound_w(args.wpre, ua, ub, Wa + W * (blockIdx.x + 1) / gridDim.x);
   }
 
+  // dynamic claims (listed runs): the range is this rank's share
+  static_assert(2 * ST + 8 + 2 * kFeedSlots + kFeedSlots <= 32, "feed ring outside the barrier area");
+  const bool dyn = listed && args.sched != nullptr;
+  int64_t d_lo = 0, d_hi = total;
+  if (dyn && args.wpre != nullptr) item_share(args, total, d_lo, d_hi);
+  Feed feed;
+  feed.full = tmem_slot_bars(bars, ST);
+  feed.empty = feed.full + kFeedSlots;
+  feed.rng = reinterpret_cast<int32_t*>(feed.empty + kFeedSlots);
   if (threadIdx.x == 0) {
+    if (dyn)
+      for (int q = 0; q < kFeedSlots; ++q) {
+        mbar_init(&feed.full[q], 1);
+        mbar_init(&feed.empty[q], 1 + kEpiWarps);
+      }
     for (int s = 0; s < ST; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
@@ -483,7 +561,25 @@ __global__ void __launch_bounds__(kCtaThreads<MODE>, 1)
       // the GB-scale output stream
       const uint64_t keep = policy_evict_last();
       Cursor<MB, MODE> c;
-      for (c.begin(args, u_begin, u_end); c.valid(); c.next(args)) {
+      // dynamic: claim the next range, hand it to the other roles; at the
+      // end the last CTA to finish claiming resets the counters
+      auto claim = [&]() {
+        int64_t e0, e1;
+        const int64_t k = (int64_t)atomicAdd(args.sched, 1u);
+        if (claim_range(k, d_lo, d_hi, gridDim.x, e0, e1)) {
+          feed.write(e0, e1);
+          c.begin(args, e0, e1);
+        } else {
+          feed.write(-1, -1);
+          c.u = c.u_end = 0;
+          if (atomicAdd(args.sched + 1, 1u) == gridDim.x - 1) {
+            atomicExch(args.sched, 0u);
+            atomicExch(args.sched + 1, 0u);
+          }
+        }
+      };
+      if (dyn) claim(); else c.begin(args, u_begin, u_end);
+      for (; c.valid(); ) {
         if (c.rb != cur_rb) {
           mbar_wait_sleep(a_empty, a_par);
           a_par ^= 1;
@@ -513,6 +609,8 @@ __global__ void __launch_bounds__(kCtaThreads<MODE>, 1)
                           (int)((2 + hl) * args.n_pad + c.cb * kBN), &full[s], keep);
           if (++s == ST) { s = 0; ph ^= 1; }
         }
+        c.next(args);
+        if (dyn && !c.valid()) claim();
       }
     }
   } else if (warp == 1) {
@@ -525,7 +623,12 @@ __global__ void __launch_bounds__(kCtaThreads<MODE>, 1)
       uint32_t ph = 0;
       int i = 0;
       Cursor<MB, MODE> c;
-      for (c.begin(args, u_begin, u_end); c.valid(); ++i) {
+      auto pull = [&]() {
+        int64_t e0, e1;
+        if (feed.read(e0, e1, true)) c.begin(args, e0, e1); else c.u = c.u_end = 0;
+      };
+      if (dyn) pull(); else c.begin(args, u_begin, u_end);
+      for (; c.valid(); ++i) {
         const int64_t rb = c.rb;
         if (rb != cur_rb) {
           mbar_wait_sleep(a_full, a_par);
@@ -569,6 +672,7 @@ __global__ void __launch_bounds__(kCtaThreads<MODE>, 1)
         }
         tc_commit(&t_full[buf]);
         c.next(args);
+        if (dyn && !c.valid()) pull();
         if (!c.valid() || c.rb != rb) tc_commit(a_empty);  // last tile of this row block
       }
     }
@@ -640,7 +744,11 @@ __global__ void __launch_bounds__(kCtaThreads<MODE>, 1)
       }
     };
     Cursor<MB, MODE> c;
-    c.begin(args, u_begin, u_end);
+    auto pull = [&]() {
+      int64_t e0, e1;
+      if (feed.read(e0, e1, lane == 0)) c.begin(args, e0, e1); else c.u = c.u_end = 0;
+    };
+    if (dyn) pull(); else c.begin(args, u_begin, u_end);
     if (c.valid()) fetch_cols(c.cb, 0);
     for (; c.valid(); ++i) {
       const int rb = c.rb, cb = c.cb;
@@ -668,6 +776,7 @@ __global__ void __launch_bounds__(kCtaThreads<MODE>, 1)
         cur_rb = rb;
       }
       c.next(args);
+      if (dyn && !c.valid()) pull();
       if constexpr (MODE == kModeMatvec) {
         if (c.valid()) {
           fetch_cols(c.cb, (i + 1) & 1);
@@ -1188,6 +1297,13 @@ int64_t packed_tiles(int64_t n) {
 // 128 x 128 fp32 block at tile_index(I, J) (row-major over the triangle).
 int packed_row_halves(int32_t /*dp*/) { return 1; }  // the epilogue combines a row's warps
 
+// GPIC_TC_DYN=0: the static split of a listed run over the CTAs (A/B;
+// measured at config 3: SM busy time max / mean 1.27 with it)
+static bool tc_dynamic() {
+  const char* e = getenv("GPIC_TC_DYN");
+  return e == nullptr || atoi(e) != 0;
+}
+
 int launch_affinity_tc_packed(const float* xhi, const float* xlo, const float* sqn, int64_t n,
                               int32_t dp, float neg_scale_log2, void* a_packed, float* degrow,
                               float* degcol, cudaStream_t s, int kind, bool half_out,
@@ -1223,6 +1339,8 @@ int launch_affinity_tc_packed(const float* xhi, const float* xlo, const float* s
   args.boxnz = boxnz;
   args.unit_list = unit_list;
   args.unit_count = unit_count;
+  // the prune mask's count slot holds the schedule counters too (prune.cu)
+  if (unit_list != nullptr && tc_dynamic()) args.sched = prune_sched(unit_count);
   if (half_out) return dispatch_kb<kModePacked16>(dp / kKBlk, mp, args, s);
   return dispatch_kb<kModePacked>(dp / kKBlk, mp, args, s);
 }
@@ -1306,6 +1424,7 @@ int launch_affinity_tc_matvec(const float* xhi, const float* xlo, const float* s
     args.wpre = pm->item_wpre;
     args.share_r = share_r;
     args.share_n = share_n;
+    if (tc_dynamic()) args.sched = pm->sched;
   }
   return dispatch_kb<kModeMatvec>(dp / kKBlk, mp, args, s);
 }

@@ -188,7 +188,10 @@ struct PruneMask {
   uint8_t* item_kept = nullptr;  // [row block][chunk] kept tiles of the item (0: pruned)
   int32_t* rbtiles = nullptr;    // kept tiles per row block
   int64_t* item_wpre = nullptr;  // kept tiles before list entry u (count + 1 entries)
+  unsigned* sched = nullptr;     // affinity_tc's dynamic schedule counters (2 words)
 };
+// the schedule counters in the count slot of a mask (from its unit count)
+unsigned* prune_sched(const int64_t* unit_count);
 bool prune_enabled();  // GPIC_PRUNE=0 computes every tile (comparisons)
 int64_t prune_block_rows(int64_t n);
 int64_t prune_bytes(int64_t n, int32_t dp);

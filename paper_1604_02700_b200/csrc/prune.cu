@@ -538,6 +538,12 @@ int64_t prune_bytes(int64_t n, int32_t dp) {
          al256(max_items(n)) + al256(nt * 4) + al256((max_items(n) + 1) * 8);
 }
 
+// count slot: [0] unit count, [8] item count, [16] scal, [32] sched; c is
+// the unit count (the slot start)
+unsigned* prune_sched(const int64_t* c) {
+  return reinterpret_cast<unsigned*>(reinterpret_cast<uintptr_t>(c) + 32);
+}
+
 PruneMask carve_prune(void* base, int64_t n, int32_t dp) {
   PruneMask m;
   m.B = prune_block_rows(n);
@@ -551,6 +557,7 @@ PruneMask carve_prune(void* base, int64_t n, int32_t dp) {
   m.units = reinterpret_cast<int32_t*>(p); p += al256(nt * (nt + 1) / 2 * 4);
   m.count = reinterpret_cast<int64_t*>(p);
   m.scal = reinterpret_cast<unsigned*>(p + 16);
+  m.sched = reinterpret_cast<unsigned*>(p + 32);  // zeroed with scal by launch_prune
   p += al256(64);
   m.rbcount = reinterpret_cast<int32_t*>(p); p += al256(nt * 4);
   m.items = reinterpret_cast<int32_t*>(p); p += al256(max_items(n) * 4);
@@ -567,7 +574,7 @@ void launch_prune(const PruneMask& m, const float* xc, const double* colpart, co
   if (row_hi <= 0) row_hi = n;
   const int64_t nb = m.nb, B = m.B;
   fill_u32_kernel<<<(unsigned)ceil_div(nb * nb + 2, 256), 256, 0, s>>>(m.mmax, nb * nb, 0u);
-  fill_u32_kernel<<<1, 32, 0, s>>>(m.scal, 2, 0u);
+  fill_u32_kernel<<<1, 32, 0, s>>>(m.scal, 6, 0u);  // scal[2], pad, sched[2]
   block_centroid_kernel<<<(unsigned)nb, 128, 0, s>>>(colpart, mean, n, d, dp, B, m.cent, m.scal);
   // GPIC_PRUNE_TF32=0: the fp32 SIMT products (measurement)
   const char* tfe = getenv("GPIC_PRUNE_TF32");
