@@ -492,7 +492,12 @@ __global__ void __launch_bounds__(kCtaThreads<MODE>, 1)
 
   // dynamic claims (listed runs): the range is this rank's share
   static_assert(2 * ST + 8 + 2 * kFeedSlots + kFeedSlots <= 32, "feed ring outside the barrier area");
-  const bool dyn = listed && args.sched != nullptr;
+  // packed store modes only: in the matrix-free pass the claims measured
+  // slower at config 5 (its tile-balanced static split keeps the column
+  // operands' L2 reuse; 162 -> 198 ms per run), and the feed's registers
+  // cost the register-tight matvec epilogue even when unused
+  constexpr bool kDynMode = MODE != kModeMatvec;
+  const bool dyn = kDynMode && listed && args.sched != nullptr;
   int64_t d_lo = 0, d_hi = total;
   if (dyn && args.wpre != nullptr) item_share(args, total, d_lo, d_hi);
   Feed feed;
@@ -1424,7 +1429,6 @@ int launch_affinity_tc_matvec(const float* xhi, const float* xlo, const float* s
     args.wpre = pm->item_wpre;
     args.share_r = share_r;
     args.share_n = share_n;
-    if (tc_dynamic()) args.sched = pm->sched;
   }
   return dispatch_kb<kModeMatvec>(dp / kKBlk, mp, args, s);
 }
