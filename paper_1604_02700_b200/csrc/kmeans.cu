@@ -111,6 +111,7 @@ struct Shared {
   double red_d[kWarps];
   long long red_i[kWarps];
   double scan[kThreads];
+  double gstage[kGridMaxCtas];  // grid path: the CTAs' seeding totals, staged in parallel
   int flag;
 };
 
@@ -621,18 +622,22 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     if (tid == 0) gp[kGSeed + b] = sh.scan[kThreads - 1];
     grid.sync();
+    // the G totals: one L2 load per thread, then thread 0 walks them in
+    // shared memory (a serial walk over L2 cost a round trip per CTA)
+    if (tid < G) sh.gstage[tid] = __ldcg(gp + kGSeed + tid);
+    __syncthreads();
     if (tid == 0) {
       // CTA prefix in order; the CTA holding the draw (last CTA if rounding
       // puts r past the end)
       double tot = 0.0;
-      for (int q = 0; q < G; ++q) tot += __ldcg(gp + kGSeed + q);
+      for (int q = 0; q < G; ++q) tot += sh.gstage[q];
       sb_tot = tot;
       const double r = s.unif[j - 1] * tot;
       double run = 0.0;
       int star = G - 1;
       for (int q = 0; q < G; ++q) {
-        if (run + __ldcg(gp + kGSeed + q) > r) { star = q; break; }
-        run += __ldcg(gp + kGSeed + q);
+        if (run + sh.gstage[q] > r) { star = q; break; }
+        run += sh.gstage[q];
       }
       sb_star = star;
       sb_r = r - run;  // the draw relative to the start of CTA `star`
@@ -705,7 +710,19 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (tid < k) {
       double sm = 0.0;
       int64_t c = 0;
-      for (int q = 0; q < G; ++q) { sm += __ldcg(gp + rec(ph, q, tid, 0)); c += __ldcg(gpi + rec(ph, q, tid, 1)); }
+      int q = 0;
+      for (; q + 8 <= G; q += 8) {  // 8 records' loads in flight, added in order
+        double xs[8];
+        long long xc[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          xs[u] = __ldcg(gp + rec(ph, q + u, tid, 0));
+          xc[u] = __ldcg(gpi + rec(ph, q + u, tid, 1));
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) { sm += xs[u]; c += xc[u]; }
+      }
+      for (; q < G; ++q) { sm += __ldcg(gp + rec(ph, q, tid, 0)); c += __ldcg(gpi + rec(ph, q, tid, 1)); }
       sums[tid] = sm;
       cnts[tid] = c;
     }
