@@ -104,6 +104,7 @@ __device__ __forceinline__ KProblem problem(const KProblem& one, const KProblem*
 }
 
 // ------------------------------------------------------- block primitives
+constexpr int kStageRecs = 2048;
 struct Shared {
   double wsum[kWarps][kMaxK];
   int wcnt[kWarps][kMaxK];
@@ -112,6 +113,10 @@ struct Shared {
   long long red_i[kWarps];
   double scan[kThreads];
   double gstage[kGridMaxCtas];  // grid path: the CTAs' seeding totals, staged in parallel
+  // grid path: the CTAs' Lloyd records (sums, counts) staged in parallel
+  // when G x k fits (else read in place)
+  double gsum[kStageRecs];
+  long long gcnt[kStageRecs];
   int flag;
 };
 
@@ -707,7 +712,23 @@ __global__ void __launch_bounds__(kThreads, 1)
       gpi[rec(ph, b, tid, 1)] = c;
     }
     grid.sync();
-    if (tid < k) {
+    if (G * k <= kStageRecs) {
+      // every record loaded once, all in flight, then the in-order sums
+      // from shared memory
+      for (int e = tid; e < G * k; e += kThreads) {
+        const int q = e / k, j = e - q * k;
+        sh.gsum[e] = __ldcg(gp + rec(ph, q, j, 0));
+        sh.gcnt[e] = __ldcg(gpi + rec(ph, q, j, 1));
+      }
+      __syncthreads();
+      if (tid < k) {
+        double sm = 0.0;
+        int64_t c = 0;
+        for (int q = 0; q < G; ++q) { sm += sh.gsum[q * k + tid]; c += sh.gcnt[q * k + tid]; }
+        sums[tid] = sm;
+        cnts[tid] = c;
+      }
+    } else if (tid < k) {
       double sm = 0.0;
       int64_t c = 0;
       int q = 0;
