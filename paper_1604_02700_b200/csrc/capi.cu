@@ -497,7 +497,10 @@ int gpic_cluster_pruned_work(const void* d_work, int64_t n, int32_t d, int32_t k
     int64_t cnt = 0;
     GPIC_CUDA_TRY(cudaMemcpyAsync(&cnt, pm.item_count, 8, cudaMemcpyDeviceToHost, s));
     GPIC_CUDA_TRY(cudaStreamSynchronize(s));
-    GPIC_CUDA_TRY(cudaMemcpyAsync(kept, pm.item_wpre + cnt, 8, cudaMemcpyDeviceToHost, s));
+    int64_t w = 0;
+    GPIC_CUDA_TRY(cudaMemcpyAsync(&w, pm.item_wpre + cnt, 8, cudaMemcpyDeviceToHost, s));
+    GPIC_CUDA_TRY(cudaStreamSynchronize(s));
+    *kept = (w - cnt * prune_item_weight()) / 4;  // the weights count quarter tiles
   } else {
     GPIC_CUDA_TRY(cudaMemcpyAsync(kept, pm.count, 8, cudaMemcpyDeviceToHost, s));
   }

@@ -193,6 +193,7 @@ struct PruneMask {
 // the schedule counters in the count slot of a mask (from its unit count)
 unsigned* prune_sched(const int64_t* unit_count);
 bool prune_enabled();  // GPIC_PRUNE=0 computes every tile (comparisons)
+int prune_item_weight();  // matrix-free items: item_wpre = 4 tiles + this per item
 int64_t prune_block_rows(int64_t n);
 int64_t prune_bytes(int64_t n, int32_t dp);
 PruneMask carve_prune(void* base, int64_t n, int32_t dp);

@@ -49,6 +49,7 @@ namespace gpic {
 namespace {
 
 constexpr double kSkipLog2 = 66.0;
+constexpr int kItemW = 0;  // per-item balance overhead (quarter tiles)
 constexpr int kGemmRows = 128;  // rows per GEMM CTA (within one block)
 constexpr int kGemmCols = 64;   // centroids per GEMM CTA
 constexpr int kGemmK = 32;      // features per smem stage
@@ -413,13 +414,21 @@ __global__ void unit_write_kernel(const uint8_t* __restrict__ skip, UnitGeom g, 
 struct ItemGeom {
   int64_t nrt, nct, nch, nb, B;
   int mb;
+  int item_w;  // per-item CTA-balance overhead in quarter tiles (item_weight)
   __device__ bool tile_kept(const uint8_t* skip, int64_t rb, int64_t cb) const {
     return skip[(rb * mb * 128 / B) * nb + cb * 128 / B] == 0;
   }
 };
 
+// CTA-balance weight of a kept item with kt kept tiles: 4 per tile plus a
+// fixed per-item cost (item set-up, its partial-row stores), in quarter tiles
+__device__ __forceinline__ int item_weight(int kt, int item_w) {
+  return kt > 0 ? 4 * kt + item_w : 0;
+}
+
 // kept[rb][ch] = number of kept tiles of item (rb, ch) (0: the item is
-// pruned); cnt[rb] = kept items, tiles[rb] = kept tiles of the row block
+// pruned); cnt[rb] = kept items, tiles[rb] = the row block's item weights
+
 __global__ void item_count_kernel(const uint8_t* __restrict__ skip, ItemGeom g,
                                   uint8_t* __restrict__ kept, int32_t* __restrict__ cnt,
                                   int32_t* __restrict__ tiles) {
@@ -433,7 +442,7 @@ __global__ void item_count_kernel(const uint8_t* __restrict__ skip, ItemGeom g,
     const int m = __popc(__ballot_sync(0xffffffffu, k));
     if (lane == 0) kept[rb * g.nch + ch] = (uint8_t)m;
     c += m > 0;
-    t += m;
+    t += item_weight(m, g.item_w);
   }
   if (lane == 0) {
     cnt[rb] = c;
@@ -485,7 +494,7 @@ __global__ void item_write_kernel(const uint8_t* __restrict__ kept, ItemGeom g,
   }
   for (int64_t c0 = 0; c0 < g.nch; c0 += 32) {
     const int64_t ch = c0 + lane;
-    const int kt = ch < g.nch ? kept[rb * g.nch + ch] : 0;
+    const int kt = ch < g.nch ? item_weight(kept[rb * g.nch + ch], g.item_w) : 0;
     const bool k = kt > 0;
     const unsigned m = __ballot_sync(0xffffffffu, k);
     // inclusive scan of the kept-tile counts over the lanes
@@ -515,6 +524,14 @@ int64_t al256(int64_t b) { return (b + 255) & ~int64_t(255); }
 int64_t max_items(int64_t n) { return ceil_div(n, 128) * ceil_div(ceil_div(n, 128), 32); }
 
 }  // namespace
+
+// per-item CTA-balance overhead of the matrix-free item list, in quarter
+// tiles (GPIC_MF_ITEM_W: measurement knob); item_wpre[count] =
+// 4 * kept tiles + count * this
+int prune_item_weight() {
+  const char* iw = getenv("GPIC_MF_ITEM_W");
+  return iw != nullptr ? atoi(iw) : kItemW;
+}
 
 bool prune_enabled() {
   const char* e = getenv("GPIC_PRUNE");
@@ -602,6 +619,7 @@ void launch_prune(const PruneMask& m, const float* xc, const double* colpart, co
   if (mb <= 0) {  // matrix-free: the item list instead of the unit list
     ItemGeom g;
     g.mb = -mb;
+    g.item_w = prune_item_weight();
     g.nct = ceil_div(n, 128);
     g.nrt = ceil_div(n, 128 * g.mb);
     g.nch = ceil_div(g.nct, 32);
