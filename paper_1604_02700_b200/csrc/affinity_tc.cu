@@ -210,27 +210,30 @@ __device__ inline bool claim_range(int64_t k, int64_t lo, int64_t hi, int64_t G,
 // a 4-slot ring in the barrier area: [0] = first entry (-1: no more), [1] = end.
 constexpr int kFeedSlots = 4;
 struct Feed {
-  uint64_t* full;   // [kFeedSlots], count 1 (the producer)
-  uint64_t* empty;  // [kFeedSlots], count 1 + kEpiWarps (MMA issuer + epilogue warps)
-  int32_t* rng;     // [kFeedSlots][2]
+  // one base: full [kFeedSlots] (count 1, the producer), empty [kFeedSlots]
+  // (count 1 + kEpiWarps: MMA issuer + epilogue warps), then the ranges
+  // [kFeedSlots][2] as int32 — the epilogue's registers are tight
+  uint64_t* full;
   int q = 0;
   uint32_t ph = 0;
+  __device__ uint64_t* empty_bar(int i) const { return full + kFeedSlots + i; }
+  __device__ int32_t* rng() const { return reinterpret_cast<int32_t*>(full + 2 * kFeedSlots); }
   // reader: the next range (false: the run is over); `arrive`: this thread
   // releases the slot (lane 0 of a reading warp)
   __device__ bool read(int64_t& e0, int64_t& e1, bool arrive) {
     mbar_wait(&full[q], ph);
-    const int32_t a = rng[2 * q], b = rng[2 * q + 1];
+    const int32_t a = rng()[2 * q], b = rng()[2 * q + 1];
     __syncwarp(__activemask());
-    if (arrive) mbar_arrive(&empty[q]);
+    if (arrive) mbar_arrive(empty_bar(q));
     if (++q == kFeedSlots) { q = 0; ph ^= 1; }
     e0 = a;
     e1 = b;
     return a >= 0;
   }
   __device__ void write(int64_t e0, int64_t e1) {
-    mbar_wait(&empty[q], ph ^ 1);
-    rng[2 * q] = (int32_t)e0;
-    rng[2 * q + 1] = (int32_t)e1;
+    mbar_wait(empty_bar(q), ph ^ 1);
+    rng()[2 * q] = (int32_t)e0;
+    rng()[2 * q + 1] = (int32_t)e1;
     mbar_arrive(&full[q]);
     if (++q == kFeedSlots) { q = 0; ph ^= 1; }
   }
@@ -502,13 +505,11 @@ __global__ void __launch_bounds__(kCtaThreads<MODE>, 1)
   if (dyn && args.wpre != nullptr) item_share(args, total, d_lo, d_hi);
   Feed feed;
   feed.full = tmem_slot_bars(bars, ST);
-  feed.empty = feed.full + kFeedSlots;
-  feed.rng = reinterpret_cast<int32_t*>(feed.empty + kFeedSlots);
   if (threadIdx.x == 0) {
     if (dyn)
       for (int q = 0; q < kFeedSlots; ++q) {
         mbar_init(&feed.full[q], 1);
-        mbar_init(&feed.empty[q], 1 + kEpiWarps);
+        mbar_init(feed.empty_bar(q), 1 + kEpiWarps);
       }
     for (int s = 0; s < ST; ++s) {
       mbar_init(&full[s], 1);
