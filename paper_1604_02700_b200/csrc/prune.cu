@@ -291,6 +291,129 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// The same products on raw mma.sync m16n8k8 TF32 with the column maxima
+// taken on the accumulator fragments (no product tile through shared
+// memory, no wmma address arithmetic): warp w owns rows 16w..16w+15 of the
+// CTA's 128 and all 64 centroid columns of a chunk (8 n-tiles); thread
+// (g = lane / 4, t = lane % 4) holds P[g][2t, 2t+1] and P[g+8][2t, 2t+1] of
+// each n-tile. Rows are padded with own = +inf so they never win a max.
+// Row operands are rounded to TF32 per fragment (sX keeps fp32 for own /
+// |x|), centroid chunks once when staged.
+__device__ __forceinline__ uint32_t to_tf32(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return r;
+}
+
+__global__ void __launch_bounds__(256)
+    proj_mma_kernel(const float* __restrict__ xc, int64_t n, int32_t dp, int64_t B, int64_t nb,
+                    const float* __restrict__ cent, unsigned* __restrict__ mmax,
+                    unsigned* __restrict__ scal) {
+  extern __shared__ __align__(128) float fsm[];
+  const int ldx = dp + 4;  // conflict-free fragment loads: bank = 4 g + t
+  float* sX = fsm;                      // [128][ldx]
+  float* sU = fsm + kGemmRows * ldx;    // [64][ldx], TF32-rounded
+  __shared__ float sOwn[kGemmRows];
+  __shared__ unsigned wmx[8][kGemmCols];
+  __shared__ float xmax[8];
+  const int64_t r0 = (int64_t)blockIdx.x * kGemmRows;
+  const int64_t S = r0 / B;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t = lane & 3;
+  // stage the rows; own products and norms in fp32 on the way
+  {
+    const float* cS = cent + S * dp;
+    float xm = 0.f;
+    for (int r = warp; r < kGemmRows; r += 8) {
+      const int64_t row = r0 + r;
+      float a = 0.f, b = 0.f;
+      for (int f = lane * 4; f < dp; f += 128) {
+        const float4 v = row < n ? *reinterpret_cast<const float4*>(xc + row * dp + f)
+                                 : make_float4(0.f, 0.f, 0.f, 0.f);
+        *reinterpret_cast<float4*>(sX + r * ldx + f) = v;
+        const float4 c = *reinterpret_cast<const float4*>(cS + f);
+        a = fmaf(v.x, c.x, a);
+        a = fmaf(v.y, c.y, a);
+        a = fmaf(v.z, c.z, a);
+        a = fmaf(v.w, c.w, a);
+        b = fmaf(v.x, v.x, b);
+        b = fmaf(v.y, v.y, b);
+        b = fmaf(v.z, v.z, b);
+        b = fmaf(v.w, v.w, b);
+      }
+      a = warp_sum_f32(a);
+      b = warp_sum_f32(b);
+      if (lane == 0) sOwn[r] = row < n ? a : INFINITY;
+      if (row < n) xm = fmaxf(xm, sqrtf(b) * 1.0001f);
+    }
+    if (lane == 0) xmax[warp] = xm;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    float m = xmax[0];
+    for (int w = 1; w < 8; ++w) m = fmaxf(m, xmax[w]);
+    atomicMax(scal + 1, __float_as_uint(m));
+  }
+  const float own0 = sOwn[warp * 16 + g], own1 = sOwn[warp * 16 + g + 8];
+  const float* a_lo = sX + (warp * 16 + g) * ldx + t;
+  const float* a_hi = a_lo + 8 * ldx;
+  for (int64_t c0 = 0; c0 < nb; c0 += kGemmCols) {
+    __syncthreads();  // the previous chunk is consumed
+    for (int c = warp; c < kGemmCols; c += 8) {
+      const int64_t col = c0 + c;
+      for (int f = lane * 4; f < dp; f += 128) {
+        float4 v = col < nb ? *reinterpret_cast<const float4*>(cent + col * dp + f)
+                            : make_float4(0.f, 0.f, 0.f, 0.f);
+        v.x = __uint_as_float(to_tf32(v.x));
+        v.y = __uint_as_float(to_tf32(v.y));
+        v.z = __uint_as_float(to_tf32(v.z));
+        v.w = __uint_as_float(to_tf32(v.w));
+        *reinterpret_cast<float4*>(sU + c * ldx + f) = v;
+      }
+    }
+    __syncthreads();
+    float acc[8][4];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
+    for (int k0 = 0; k0 < dp; k0 += 8) {
+      const uint32_t a0 = to_tf32(a_lo[k0]), a1 = to_tf32(a_hi[k0]);
+      const uint32_t a2 = to_tf32(a_lo[k0 + 4]), a3 = to_tf32(a_hi[k0 + 4]);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float* bp = sU + (j * 8 + g) * ldx + k0 + t;
+        const uint32_t b0 = __float_as_uint(bp[0]), b1 = __float_as_uint(bp[4]);
+        asm volatile(
+            "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, "
+            "{%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+            : "+f"(acc[j][0]), "+f"(acc[j][1]), "+f"(acc[j][2]), "+f"(acc[j][3])
+            : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+      }
+    }
+    // max over the warp's 16 rows of P[i][c] - own_i, per column
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      float m0 = fmaxf(acc[j][0] - own0, acc[j][2] - own1);
+      float m1 = fmaxf(acc[j][1] - own0, acc[j][3] - own1);
+#pragma unroll
+      for (int o = 4; o < 32; o <<= 1) {
+        m0 = fmaxf(m0, __shfl_xor_sync(0xffffffffu, m0, o));
+        m1 = fmaxf(m1, __shfl_xor_sync(0xffffffffu, m1, o));
+      }
+      if (g == 0) {
+        wmx[warp][j * 8 + 2 * t] = f2ord(m0);
+        wmx[warp][j * 8 + 2 * t + 1] = f2ord(m1);
+      }
+    }
+    __syncthreads();
+    if (tid < kGemmCols && c0 + tid < nb) {
+      unsigned m = wmx[0][tid];
+#pragma unroll
+      for (int w = 1; w < 8; ++w) m = max(m, wmx[w][tid]);
+      atomicMax(mmax + S * nb + c0 + tid, m);
+    }
+  }
+}
+
 __global__ void fill_u32_kernel(unsigned* p, int64_t count, unsigned v) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < count) p[i] = v;
@@ -593,11 +716,22 @@ void launch_prune(const PruneMask& m, const float* xc, const double* colpart, co
   fill_u32_kernel<<<(unsigned)ceil_div(nb * nb + 2, 256), 256, 0, s>>>(m.mmax, nb * nb, 0u);
   fill_u32_kernel<<<1, 32, 0, s>>>(m.scal, 6, 0u);  // scal[2], pad, sched[2]
   block_centroid_kernel<<<(unsigned)nb, 128, 0, s>>>(colpart, mean, n, d, dp, B, m.cent, m.scal);
-  // GPIC_PRUNE_TF32=0: the fp32 SIMT products (measurement)
+  // GPIC_PRUNE_TF32=0: the fp32 SIMT products, =1: wmma, =2 (default):
+  // mma.sync with the maxima on the fragments (measurement knob)
   const char* tfe = getenv("GPIC_PRUNE_TF32");
-  const int tf32 = tfe == nullptr || atoi(tfe) != 0;
+  const int tfm = tfe == nullptr ? 2 : atoi(tfe);
+  const int tf32 = tfm != 0;
   if (!tf32) own_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, s>>>(xc, n, dp, B, m.cent, m.own, m.scal);
-  if (tf32) {
+  if (tfm == 2) {
+    const size_t shm = (size_t)(kGemmRows + kGemmCols) * (dp + 4) * 4;
+    static size_t shm_mma = 0;
+    if (shm > 48 * 1024 && shm > shm_mma) {
+      cudaFuncSetAttribute(proj_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm);
+      shm_mma = shm;
+    }
+    proj_mma_kernel<<<(unsigned)ceil_div(n, kGemmRows), 256, shm, s>>>(xc, n, dp, B, nb, m.cent,
+                                                                      m.mmax, m.scal);
+  } else if (tf32) {
     const int ldx = dp + 4;
     const int ubuf = kGemmCols * ldx > kGemmRows * (kGemmCols + 4) ? kGemmCols * ldx
                                                                      : kGemmRows * (kGemmCols + 4);
