@@ -80,6 +80,16 @@ inline int64_t local_bytes(int64_t n) {
          al((ceil_div(n, kRedBlock) + 1) * 8) + al(n * 8) + al(8);
 }
 
+// Partial-y exchange of the slotted shards: all-to-all (every rank gets
+// every partial: P n doubles out per rank per iteration) or reduce-scatter +
+// all-gather of the y slices (2 n, one more epoch wait). Same sums in the
+// same order either way. GPIC_EXCHANGE=bcast / rs overrides the default
+// (reduce-scatter from P = 3, where it moves less).
+int reduce_scatter(int nranks) {
+  if (const char* e = getenv("GPIC_EXCHANGE")) return strcmp(e, "rs") == 0 ? 1 : 0;
+  return nranks >= 3 ? 1 : 0;
+}
+
 PeerTable table(const gpic_comm* c, int self) {
   PeerTable pt;
   std::memset(&pt, 0, sizeof pt);
@@ -428,6 +438,7 @@ int gpic_comm_iterate(gpic_comm* c, const gpic_shard* shards, int32_t nlocal, do
       S.pt_slots = table(c, self);
       for (int p = 0; p < c->nranks; ++p)
         for (int par = 0; par < 2; ++par) S.pt_slots.y[p][par] = r_slot(c->region[p], n, self, par);
+      S.pt_slots.scatter = reduce_scatter(c->nranks);
       S.slots = r_slot(c->region[self], n, 0, 0);
       S.slot_stride = al(n * 8) / 8;
       S.deg_full = r_deg(c->region[self], n);
@@ -456,6 +467,7 @@ int gpic_comm_iterate(gpic_comm* c, const gpic_shard* shards, int32_t nlocal, do
         S.pt_slots = table(c, self);
         for (int p = 0; p < c->nranks; ++p)
           for (int par = 0; par < 2; ++par) S.pt_slots.y[p][par] = r_slot(c->region[p], n, self, par);
+        S.pt_slots.scatter = reduce_scatter(c->nranks);
         S.slots = r_slot(c->region[self], n, 0, 0);
         S.slot_stride = al(n * 8) / 8;
         S.deg_full = r_deg(c->region[self], n);

@@ -189,7 +189,9 @@ __global__ void __launch_bounds__(128 * kSeg)
     for (int q = 0; q < kSeg; ++q) t += part[q][o];
     const double val = deg != nullptr ? t / deg[i] : t;
     const int parity = ctl != nullptr ? (ctl->iter & 1) : 0;
-    for (int p = 0; p < pt.nranks; ++p) pt.y[p][parity][i] = val;
+    const int own = pt.scatter ? slice_owner(i, n, pt.nranks) : -1;
+    for (int p = 0; p < pt.nranks; ++p)
+      if (own < 0 || own == p) pt.y[p][parity][i] = val;
   }
   if (pt.flags[0] == nullptr) return;
   __threadfence_system();

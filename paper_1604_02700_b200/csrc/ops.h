@@ -124,13 +124,19 @@ void launch_degree(const float* rowpart, int64_t rows, int64_t rows_pad, int64_t
 // epochs have arrived. y is double-buffered by iteration parity, so a fast
 // rank writing iteration t+1 never races a slow rank still reading t.
 constexpr int kMaxRanks = 8;
-constexpr int kFlagSlots = 2 * kMaxRanks;  // [0,P): iteration epochs, [P,2P): gather epochs
+// [0,P): iteration epochs, [P,2P): gather epochs, [2P,3P): the y slices'
+// all-gather epochs of a reduce-scatter exchange
+constexpr int kFlagSlots = 3 * kMaxRanks;
 
 struct PeerTable {
   double* y[kMaxRanks][2];     // y ping-pong of every rank, as seen from this process
   uint64_t* flags[kMaxRanks];  // kFlagSlots epochs per rank (nullptr: single rank)
   int nranks;
   int self;                    // global rank index of the local shard
+  // partial-y slots (packed / matrix-free item shards): 0 = every rank gets
+  // the whole partial (all-to-all), 1 = row i goes to its slice owner only
+  // (reduce-scatter; the owners all-gather the finished y slices)
+  int scatter;
   // the epoch base of a loop is ctl->sync_epoch (device-side, so one
   // captured graph is replayed for every run)
 };
@@ -150,6 +156,20 @@ void launch_gemv(const float* a, int64_t lda, int64_t rows, int64_t row_lo, cons
 void launch_peer_wait(const uint64_t* flags_self, int slot0, int count, uint64_t base,
                       int add_iter, gpic_ctl* ctl, cudaStream_t s);
 // y = (sum over ranks of the packed shards' y partials, rank order) / deg
+// reduce-scatter exchange: the owner's rows [n r / P, n (r+1) / P)
+__host__ __device__ inline int64_t slice_lo(int64_t n, int r, int nranks) {
+  return n * r / nranks;
+}
+__host__ __device__ inline int slice_owner(int64_t i, int64_t n, int nranks) {
+  int r = (int)((i * nranks) / n);
+  while (r + 1 < nranks && slice_lo(n, r + 1, nranks) <= i) ++r;
+  while (r > 0 && slice_lo(n, r, nranks) > i) --r;
+  return r;
+}
+// sum of the P slots for this rank's slice (rank order) / deg, stored into
+// every rank's y, then the all-gather epoch published
+void launch_slice_combine(const double* slots, int64_t stride, int64_t n, const double* deg,
+                          const PeerTable& pt, gpic_ctl* ctl, cudaStream_t s);
 void launch_slot_combine(const double* slots, int64_t stride, int nranks, int64_t n,
                          const double* deg, double* y0, double* y1, gpic_ctl* ctl, cudaStream_t s);
 void launch_iteration_tail(const double* y0, const double* y1, int64_t n, double* redpart,

@@ -332,6 +332,50 @@ __global__ void slot_combine_kernel(const double* __restrict__ slots, int64_t st
 }
 }  // namespace
 
+namespace {
+__device__ __forceinline__ void st_release_sys64(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// reduce-scatter exchange, second half: this rank's slice of y from the P
+// partial slots (rank order, as slot_combine) stored into every rank's y;
+// the last CTA publishes the all-gather epoch (flag slots [2P, 3P))
+__global__ void slice_combine_kernel(const double* __restrict__ slots, int64_t stride, int64_t n,
+                                     const double* __restrict__ deg, const PeerTable pt,
+                                     gpic_ctl* ctl) {
+  if (*(volatile const int32_t*)&ctl->stop) return;
+  const int parity = ctl->iter & 1;
+  const int64_t lo = slice_lo(n, pt.self, pt.nranks), hi = slice_lo(n, pt.self + 1, pt.nranks);
+  const int64_t i = lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < hi) {
+    double t = 0.0;
+    for (int r = 0; r < pt.nranks; ++r) t += slots[(2 * r + parity) * stride + i];
+    const double val = deg != nullptr ? t / deg[i] : t;
+    for (int r = 0; r < pt.nranks; ++r) pt.y[r][parity][i] = val;
+  }
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned prev = atomicAdd(&ctl->arrive[3], 1u);
+    if (prev == gridDim.x - 1) {
+      ctl->arrive[3] = 0u;
+      __threadfence_system();
+      const uint64_t epoch = ctl->sync_epoch + (uint64_t)ctl->iter + 1;
+      for (int r = 0; r < pt.nranks; ++r)
+        st_release_sys64(pt.flags[r] + 2 * kMaxRanks + pt.self, epoch);
+    }
+  }
+}
+}  // namespace
+
+void launch_slice_combine(const double* slots, int64_t stride, int64_t n, const double* deg,
+                          const PeerTable& pt, gpic_ctl* ctl, cudaStream_t s) {
+  const int64_t rows = slice_lo(n, pt.self + 1, pt.nranks) - slice_lo(n, pt.self, pt.nranks);
+  const unsigned grid = (unsigned)(rows > 0 ? ceil_div(rows, 256) : 1);
+  slice_combine_kernel<<<grid, 256, 0, s>>>(slots, stride, n, deg, pt, ctl);
+  count_launch();
+}
+
 void launch_slot_combine(const double* slots, int64_t stride, int nranks, int64_t n,
                          const double* deg, double* y0, double* y1, gpic_ctl* ctl, cudaStream_t s) {
   slot_combine_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, s>>>(slots, stride, nranks, n, deg, y0,
@@ -501,14 +545,30 @@ int run_power_loops(ShardLoop* shards, int nlocal, int64_t n, int32_t max_iter, 
           launch_gemv(L.a, L.lda, L.rows, L.row_lo, L.v32, L.deg, L.pt, L.ctl, cs);
         }
       }
+      // reduce-scatter shards: every local shard's slice combine (and its
+      // all-gather stores) before any shard waits for the all-gather —
+      // virtual ranks share one stream
       for (int i = 0; i < nlocal; ++i) {
         const ShardLoop& L = shards[i];
         const PeerTable& pt = L.pt;
-        if (pt.flags[0] != nullptr)
-          launch_peer_wait(pt.flags[pt.self], 0, pt.nranks, 0, 1, L.ctl, cs);
-        if (L.mode == kLoopPackedShard || L.mode == kLoopMfShard)
-          launch_slot_combine(L.slots, L.slot_stride, pt.nranks, n, L.deg_full, pt.y[pt.self][0],
-                              pt.y[pt.self][1], L.ctl, cs);
+        if (!(L.mode == kLoopPackedShard || L.mode == kLoopMfShard) || !L.pt_slots.scatter)
+          continue;
+        launch_peer_wait(pt.flags[pt.self], 0, pt.nranks, 0, 1, L.ctl, cs);
+        launch_slice_combine(L.slots, L.slot_stride, n, L.deg_full, pt, L.ctl, cs);
+      }
+      for (int i = 0; i < nlocal; ++i) {
+        const ShardLoop& L = shards[i];
+        const PeerTable& pt = L.pt;
+        const bool slotted = L.mode == kLoopPackedShard || L.mode == kLoopMfShard;
+        if (slotted && L.pt_slots.scatter) {
+          launch_peer_wait(pt.flags[pt.self], 2 * kMaxRanks, pt.nranks, 0, 1, L.ctl, cs);
+        } else {
+          if (pt.flags[0] != nullptr)
+            launch_peer_wait(pt.flags[pt.self], 0, pt.nranks, 0, 1, L.ctl, cs);
+          if (slotted)
+            launch_slot_combine(L.slots, L.slot_stride, pt.nranks, n, L.deg_full,
+                                pt.y[pt.self][0], pt.y[pt.self][1], L.ctl, cs);
+        }
         if (L.low.count != 0)  // < 0: the count stays on the device
           launch_lowdeg_matvec(L.low, L.low_deg, L.v64, pt.y[pt.self][0], pt.y[pt.self][1], L.ctl,
                                cs);

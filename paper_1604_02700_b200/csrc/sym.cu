@@ -673,7 +673,9 @@ __global__ void __launch_bounds__(kTS * kSeg)
     for (int q = 0; q < kSeg; ++q) t += part[q][o];
     const double val = deg != nullptr ? t / deg[i] : t;
     const int parity = ctl != nullptr ? (ctl->iter & 1) : 0;
-    for (int r = 0; r < pt.nranks; ++r) pt.y[r][parity][i] = val;
+    const int own = pt.scatter ? slice_owner(i, n, pt.nranks) : -1;
+    for (int r = 0; r < pt.nranks; ++r)
+      if (own < 0 || own == r) pt.y[r][parity][i] = val;
   }
   if (pt.flags[0] == nullptr) return;
   __threadfence_system();
@@ -747,7 +749,9 @@ __global__ void __launch_bounds__(kTS)
   if (i < n) {
     const double val = deg != nullptr ? t / di : t;
     const int parity = ctl != nullptr ? (ctl->iter & 1) : 0;
-    for (int r = 0; r < pt.nranks; ++r) pt.y[r][parity][i] = val;
+    const int own = pt.scatter ? slice_owner(i, n, pt.nranks) : -1;
+    for (int r = 0; r < pt.nranks; ++r)
+      if (own < 0 || own == r) pt.y[r][parity][i] = val;
   }
   if (pt.flags[0] == nullptr) return;
   __threadfence_system();

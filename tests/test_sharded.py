@@ -251,3 +251,23 @@ def test_packed_shards_other_shapes_and_kinds(m, kind_name):
         assert np.array_equal(got[0], single[0]), p
         assert got[2].iterations_run == single[2].iterations_run, p
         assert np.abs(got[1] - single[1]).sum() / np.abs(single[1]).sum() <= 1e-6, p
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("storage", ["packed", "none"])
+def test_reduce_scatter_exchange_matches_all_to_all(monkeypatch, storage):
+    """The slotted shards' two exchanges (every partial to every rank, or
+    reduce-scatter of the partials + all-gather of the y slices) add the
+    same terms in the same rank order: bitwise-equal embeddings, labels and
+    delta histories, for P = 2..5 virtual ranks."""
+    d = gaussian_blobs(7000, 64, 5, seed=12)
+    kind, params = GaussianRbf(4.0), PicParams(k=5)
+    for p in (2, 3, 5):
+        cfg = KernelConfig(p=p, virtual_ranks=True, storage=storage)
+        monkeypatch.setenv("GPIC_EXCHANGE", "bcast")
+        a = cluster(d, kind, params, config=cfg, seed=2)
+        monkeypatch.setenv("GPIC_EXCHANGE", "rs")
+        b = cluster(d, kind, params, config=cfg, seed=2)
+        assert np.array_equal(a[0], b[0]), p
+        assert np.array_equal(a[1], b[1]), p
+        assert np.array_equal(a[2].delta_history, b[2].delta_history), p
