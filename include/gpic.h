@@ -389,6 +389,18 @@ typedef struct gpic_shard {
   const double* x;
 } gpic_shard;
 
+/* Packed shard rows balanced by WORK: the whole matrix's tile-pruning mask
+ * (prune.cu, the same on every rank) gives the kept tensor units per row
+ * block; bounds[0..nranks] are 512-aligned rows cutting the kept-unit
+ * prefix into equal parts (bounds[nranks] = n). gpic_packed_shard_range
+ * balances the dense triangle instead, which leaves block-sparse ranks
+ * unequal. d_xlo / d_prep_work: gpic_prepare_points' outputs; d_scratch:
+ * gpic_prune_scratch_bytes(n, d) bytes. Replaces: parallel.py:44-77
+ * plan_rows for the packed symmetric shards. */
+int64_t gpic_prune_scratch_bytes(int64_t n, int32_t d);
+int gpic_packed_shard_ranges_pruned(const float* d_xlo, const double* d_prep_work, int64_t n,
+                                    int32_t d, double sigma, int32_t nranks, void* d_scratch,
+                                    int64_t* bounds, void* stream);
 /* Packed shards (symmetric storage across ranks, GPIC_STORAGE_PACKED in
  * gpic_shard): rank r owns the 512-row super-rows [row_lo, row_hi) returned
  * by gpic_packed_shard_range (balanced by stored tile count) and stores the
@@ -396,9 +408,11 @@ typedef struct gpic_shard {
  * gpic_packed_shard_build computes them plus the shard's partial degrees
  * (d_deg_partial: n doubles, global row index). In the gpic_shard: a = the
  * tiles, deg = the partial degrees, row_lo / rows = the range, ypart = the
- * build's scratch (gpic_packed_shard_scratch_bytes). Every iteration each
- * rank sends its partial y to every rank (P2P, NVLink) and each rank sums
- * the P partials in rank order: deterministic for a given P. */
+ * build's scratch (gpic_packed_shard_scratch_bytes). Every iteration the
+ * partial y go over NVLink P2P either to every rank (P = 2) or, from P = 3,
+ * to their row slice's owner, which sums the P partials and all-gathers the
+ * finished y slice (GPIC_EXCHANGE=bcast / rs forces one); the P partials
+ * are summed in rank order either way: deterministic for a given P. */
 int gpic_packed_shard_range(int64_t n, int32_t nranks, int32_t rank, int64_t* row_lo,
                             int64_t* row_hi);
 int64_t gpic_packed_shard_tiles(int64_t n, int64_t row_lo, int64_t row_hi);

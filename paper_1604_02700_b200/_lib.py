@@ -113,6 +113,8 @@ SIGNATURES = {
     "gpic_sym_partial_floats": (I64, [I64]),
     "gpic_packed_shard_range": (C.c_int, [I64, I32, I32, P, P]),
     "gpic_packed_shard_tiles": (I64, [I64, I64, I64]),
+    "gpic_prune_scratch_bytes": (I64, [I64, I32]),
+    "gpic_packed_shard_ranges_pruned": (C.c_int, [P, P, I64, I32, F64, I32, P, P, P]),
     "gpic_packed_shard_scratch_bytes": (I64, [I64, I64, I64]),
     "gpic_packed_shard_build": (C.c_int, [P, P, P, I64, I32, I64, I64, C.c_double, I32, P, P, P, P,
                                           P]),

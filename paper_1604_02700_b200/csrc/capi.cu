@@ -1,7 +1,9 @@
 // extern "C" entry points of libgpic.so (declared in include/gpic.h).
 #include <cmath>
 #include <cstdio>
+#include <algorithm>
 #include <cstring>
+#include <vector>
 #include <string>
 
 #include "common.cuh"
@@ -607,6 +609,51 @@ int gpic_packed_shard_range(int64_t n, int32_t nranks, int32_t rank, int64_t* ro
   const int64_t p0 = cut(rank), p1 = cut(rank + 1);
   *row_lo = 512 * p0;
   *row_hi = 512 * p1 < n ? 512 * p1 : n;
+  return GPIC_OK;
+}
+
+int64_t gpic_prune_scratch_bytes(int64_t n, int32_t d) {
+  if (n < 1 || d < 1) return -1;
+  return prune_bytes(n, feature_pitch(d));
+}
+
+int gpic_packed_shard_ranges_pruned(const float* d_xlo, const double* d_prep_work, int64_t n,
+                                    int32_t d, double sigma, int32_t nranks, void* d_scratch,
+                                    int64_t* bounds, void* stream) {
+  if (n < 1 || d < 1 || nranks < 1 || !d_xlo || !d_prep_work || !d_scratch || !bounds)
+    return fail(GPIC_E_INVALID, "bad packed shard parameters");
+  if (!(sigma > 0)) return fail(GPIC_E_INVALID, "sigma must be positive");
+  const int64_t ns = super_rows(n);
+  if (ns < nranks) return fail(GPIC_E_INVALID, "too few 512-row super-rows for the rank count");
+  const int32_t dp = feature_pitch(d);
+  const int mb = tc_mblocks(dp);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  // the whole matrix's pruning mask: kept tensor units per row block
+  const PruneMask pm = carve_prune(d_scratch, n, dp);
+  launch_prune(pm, d_xlo, d_prep_work, d_prep_work + ceil_div(n, 256) * d, n, d, dp, sigma, mb, 0,
+               s);
+  const int64_t nrt = ceil_div(n, 128 * mb);
+  std::vector<int32_t> cnt(nrt);
+  GPIC_CUDA_TRY(cudaMemcpyAsync(cnt.data(), pm.rbcount, nrt * 4, cudaMemcpyDeviceToHost, s));
+  GPIC_CUDA_TRY(cudaStreamSynchronize(s));
+  // super-row weights: its row blocks' kept units (+1: a super-row is never free)
+  std::vector<int64_t> pre(ns + 1, 0);
+  for (int64_t q = 0; q < ns; ++q) {
+    int64_t w = 1;
+    for (int64_t rb = q * 512 / (128 * mb); rb < (q + 1) * 512 / (128 * mb) && rb < nrt; ++rb)
+      w += cnt[rb];
+    pre[q + 1] = pre[q] + w;
+  }
+  bounds[0] = 0;
+  for (int32_t r = 1; r < nranks; ++r) {
+    const int64_t want = pre[ns] * r / nranks;
+    int64_t q = std::lower_bound(pre.begin(), pre.end(), want) - pre.begin();
+    const int64_t prev = bounds[r - 1] / 512;
+    if (q < prev + 1) q = prev + 1;                  // every rank keeps a super-row
+    if (q > ns - (nranks - r)) q = ns - (nranks - r);
+    bounds[r] = 512 * q;
+  }
+  bounds[nranks] = n;
   return GPIC_OK;
 }
 

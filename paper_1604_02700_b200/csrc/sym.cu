@@ -1012,6 +1012,13 @@ int gemv_dynamic() {
   return e != nullptr ? atoi(e) : 1;
 }
 
+// GPIC_GEMV_SHARD_LIST=0: packed shards walk their super-block id range with
+// static weight ranges (A/B)
+int gemv_shard_list() {
+  const char* e = getenv("GPIC_GEMV_SHARD_LIST");
+  return e == nullptr || atoi(e) != 0;
+}
+
 int gemv_evict_first() {
   const char* e = getenv("GPIC_GEMV_EVICT");
   return e != nullptr ? atoi(e) : 1;
@@ -1079,19 +1086,24 @@ int64_t sym_partial_floats(int64_t n) {
 void launch_sym_gemv(const float* tiles, int64_t n, const float* v32, float* rowp, float* colp,
                      const double* deg, const PeerTable& pt, gpic_ctl* ctl, cudaStream_t s,
                      const ShardRange& sr, const uint8_t* boxnz, const int64_t* sb_prefix) {
-  // packed shards keep per-tile flags (their super-block records are not built)
+  // packed shards: their box flags, super-block records and the list of
+  // their non-empty super-blocks live in whole-triangle arrays (only the
+  // shard's tiles flagged), so the list walk and its claims apply; the
+  // per-super-row term lists of the list reduce are whole-matrix only
   const bool whole = sr.p_lo == 0 && sr.tile_base == 0 && sr.p_hi >= ceil_div(ceil_div(n, kTS), kSB);
   // GPIC_SB_BITS: 0 per-tile flags everywhere, 1 super-block records for
   // producer and consumers (default), 2 records for the producer only.
   // Measured at config 3 (scripts/gemv_ab.py, one box): id walk + flags
   // 0.500 ms, list + flags 0.465, list + records 0.424
   const int bits_mode = getenv("GPIC_SB_BITS") != nullptr ? atoi(getenv("GPIC_SB_BITS")) : 1;
-  const SbList sl = boxnz != nullptr && whole && gemv_use_list() ? sb_list(sb_prefix, n)
-                                                                  : SbList{nullptr, nullptr, nullptr};
+  const bool lists = boxnz != nullptr && sb_prefix != nullptr && (whole || gemv_shard_list());
+  const SbList sl = lists && gemv_use_list() ? sb_list(sb_prefix, n)
+                                             : SbList{nullptr, nullptr, nullptr};
   Sparse sp{boxnz, boxnz != nullptr ? sb_prefix : nullptr,
-            boxnz != nullptr && whole && bits_mode != 0 ? sb_bits(sb_prefix, n) : nullptr,
+            lists && bits_mode != 0 ? sb_bits(sb_prefix, n) : nullptr,
             gemv_prefetch(), bits_mode == 1, gemv_evict_first(), sl.list, sl.lpre, sl.count,
-            sl.ranges, sl.tlist, sl.tcount, sl.tld, nullptr};
+            whole ? sl.ranges : nullptr, whole ? sl.tlist : nullptr, whole ? sl.tcount : nullptr,
+            sl.tld, nullptr};
   if (sl.list != nullptr && gemv_dynamic() && gemv_prefetch() == 0) sp.sched = sl.sched;
   sym_prepare();
   const int64_t nt = ceil_div(n, kTS);

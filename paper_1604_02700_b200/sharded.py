@@ -21,6 +21,7 @@ Two launch modes share that code path:
 from __future__ import annotations
 
 import ctypes as C
+import os
 
 import numpy as np
 
@@ -201,9 +202,20 @@ class ShardedRunner:
                                        prep.x.data_ptr())
         elif packed:
             # symmetric packed shards: upper-triangle tiles of the rank's
-            # 512-row super-rows, partial degrees summed across ranks
+            # 512-row super-rows, partial degrees summed across ranks; rows
+            # balanced by the pruning mask's kept units (the same on every
+            # rank) when the RBF kind prunes, else by triangle tiles
+            ranges = self.packed_ranges
+            if code == _lib.KIND_RBF and os.environ.get("GPIC_SHARD_BALANCE", "1") != "0":
+                scratch = torch.empty(int(L.gpic_prune_scratch_bytes(n, prep.d)),
+                                      dtype=torch.uint8, device=dev)
+                bounds = (C.c_int64 * (cfg.p + 1))()
+                _lib.check(L.gpic_packed_shard_ranges_pruned(
+                    gpu._ptr(prep.xlo), gpu._ptr(prep.work), n, prep.d, sigma, cfg.p,
+                    gpu._ptr(scratch), bounds, st))
+                ranges = [(bounds[r], bounds[r + 1]) for r in range(cfg.p)]
             for i, r in enumerate(self.locals):
-                lo, hi = self.packed_ranges[r]
+                lo, hi = ranges[r]
                 ntile = int(L.gpic_packed_shard_tiles(n, lo, hi))
                 tiles = torch.empty(ntile * 128 * 128, dtype=torch.float32, device=dev)
                 deg = torch.empty(n, dtype=torch.float64, device=dev)
