@@ -586,7 +586,9 @@ def run_ours(args, cfg, rank, world):
 
 
 def run_ours_sharded(args, cfg, rank, world):
-    """N > 1: one rank per GPU, row-sharded dense A, fused P2P y exchange."""
+    """N > 1: one rank per GPU, packed symmetric super-row shards balanced by
+    kept tensor units, P2P partial-y exchange (reduce-scatter + all-gather
+    from N = 3); dense row shards with the fused y all-gather otherwise."""
     import torch
     import torch.distributed as dist
 
@@ -662,7 +664,8 @@ def run_ours_sharded(args, cfg, rank, world):
             "data": "synthetic (SURVEY App. B gaussian blobs, seed 0)",
             "config": dict(workload(cfg, world),
                            parallelism=(f"packed symmetric super-row shards x{world}, P2P partial-y "
-                                        "exchange summed in rank order" if storage == "packed" else
+                                        "exchange (reduce-scatter + all-gather from 3 ranks) summed "
+                                        "in rank order" if storage == "packed" else
                                         f"row-shard x{world}, fused P2P y all-gather")),
             "engine": {"affinity_engine": args.engine, "storage": storage},
             "iterations": trace.iterations_run, "converged": trace.converged,
