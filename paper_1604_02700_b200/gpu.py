@@ -685,7 +685,9 @@ def _cluster_x(x, kind, params, config, seed, timed, v0=None):
     nbytes = workspace_bytes(n, m, k, T, storage)
     work = torch.empty(nbytes, dtype=torch.uint8, device=dev)
     # labels, v and the delta history side by side: one device->host copy
-    out = torch.zeros(2 * n + T, dtype=torch.int64, device=dev)
+    # (every entry read back is written by the run: labels and v in full,
+    # the history up to the iteration count)
+    out = torch.empty(2 * n + T, dtype=torch.int64, device=dev)
     labels = out[:n]
     v = out[n:2 * n].view(torch.float64)
     hist = out[2 * n:].view(torch.float64)
@@ -706,7 +708,13 @@ def _cluster_x(x, kind, params, config, seed, timed, v0=None):
     it = int(iters.value)
     phases = dict(zip(("affinity", "rowsum", "normalize", "iterate", "kmeans"),
                       (t / 1e3 for t in ms))) if timed else None
-    host = out.cpu().numpy()
+    # into page-locked memory from torch's caching host allocator (a
+    # pageable destination halves the copy rate); the returned arrays are
+    # views that keep that block alive
+    host_t = torch.empty(out.shape, dtype=out.dtype, pin_memory=True)
+    host_t.copy_(out, non_blocking=True)
+    torch.cuda.current_stream(dev).synchronize()
+    host = host_t.numpy()
     return (host[:n], host[n:2 * n].view(np.float64),
             PicTrace(it, host[2 * n:2 * n + it].view(np.float64).copy(), bool(conv.value)), phases)
 
