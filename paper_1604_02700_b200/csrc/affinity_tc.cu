@@ -87,6 +87,7 @@ template <int MODE>
 constexpr int kCtaThreads = 32 * kEpiBase<MODE> + kEpiWarps * 32;
 constexpr int kSmemBudget = 232448 - 1024 - 256;  // 227 KB opt-in minus alignment + barriers
 constexpr int kChunkTiles = 32;              // matvec: column tiles per work item
+constexpr int kMaxRebalanceGrid = 256;       // matvec re-balance: CTAs per pass at most
 
 // rows per CTA block: 256 (two M blocks sharing every B stage) while the
 // operands fit, else 128
@@ -178,6 +179,11 @@ struct TcArgs {
   // both) — list ranges are claimed at run time instead of split in advance;
   // null: the static split
   unsigned* sched;
+  // matvec listed: CTA cuts measured by the previous pass (mf.cu rebalance:
+  // [0] grid, [1] ua, [2] ub, then grid + 1 list positions; used when the
+  // header matches this launch) and this pass's per-CTA time in ns
+  const int64_t* cuts;
+  uint64_t* cta_ns;
 };
 
 // Claim k of a dynamic run over list entries [lo, hi) on G CTAs: G claims
@@ -487,10 +493,17 @@ __global__ void __launch_bounds__(kCtaThreads<MODE>, 1)
   if (listed && args.wpre != nullptr) {  // equal shares of kept tiles, not of items
     int64_t ua, ub;  // this rank's share of the list (all of it on one rank)
     item_share(args, total, ua, ub);
-    const int64_t Wa = args.wpre[ua], W = args.wpre[ub] - Wa;
-    u_begin = lower_bound_w(args.wpre, ua, ub, Wa + W * blockIdx.x / gridDim.x);
-    u_end = blockIdx.x + 1 == gridDim.x ? ub
-                                        : lower_bound_w(args.wpre, ua, ub, Wa + W * (blockIdx.x + 1) / gridDim.x);
+    if (args.cuts != nullptr && args.cuts[0] == gridDim.x && args.cuts[1] == ua &&
+        args.cuts[2] == ub) {
+      // cuts re-balanced by the previous pass's measured CTA times
+      u_begin = args.cuts[3 + blockIdx.x];
+      u_end = args.cuts[4 + blockIdx.x];
+    } else {
+      const int64_t Wa = args.wpre[ua], W = args.wpre[ub] - Wa;
+      u_begin = lower_bound_w(args.wpre, ua, ub, Wa + W * blockIdx.x / gridDim.x);
+      u_end = blockIdx.x + 1 == gridDim.x ? ub
+                                          : lower_bound_w(args.wpre, ua, ub, Wa + W * (blockIdx.x + 1) / gridDim.x);
+    }
   }
 
   // dynamic claims (listed runs): the range is this rank's share
@@ -542,9 +555,34 @@ __global__ void __launch_bounds__(kCtaThreads<MODE>, 1)
   const uint32_t tmem_base = *tmem_slot;
   // every role ends here (no code after the role branches: the warpgroups
   // run with different register budgets after setmaxnreg)
+  // the CTA's span (thread 0): the matrix-free rebalance reads it
+  uint64_t trace_t0 = 0;
+  if (threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(trace_t0));
   auto teardown = [&]() {
     tc_fence_before();
     asm volatile("barrier.sync 15, %0;" ::"n"(kCtaThreads<MODE>) : "memory");
+    if (MODE == kModeMatvec && args.cta_ns != nullptr && threadIdx.x == 0) {
+      uint64_t t1;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+      args.cta_ns[blockIdx.x] = t1 - trace_t0;
+    }
+#ifdef GPIC_TC_TRACE
+    if (threadIdx.x == 0) {
+      uint64_t t1;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+      const int64_t tiles = args.wpre != nullptr ? args.wpre[u_end] - args.wpre[u_begin] : -1;
+      int64_t rbs = 0, prev = -1;
+      if (listed && MODE == kModeMatvec)
+        for (int64_t u = u_begin; u < u_end; ++u) {
+          const int64_t rb = args.unit_list[u] / args.n_chunks;
+          rbs += rb != prev;
+          prev = rb;
+        }
+      printf("TCTRACE %d %llu %lld %lld %lld %lld\n", (int)blockIdx.x,
+             (unsigned long long)(t1 - trace_t0), (long long)(u_end - u_begin), (long long)tiles,
+             (long long)rbs, (long long)u_begin);
+    }
+#endif
     if (warp == 1) {
       tc_fence_after();
       asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
@@ -1397,6 +1435,104 @@ int64_t mf_colpart_floats(int64_t n, int32_t dp) {
 
 // Matrix-free row block: ypart[p][i - row_lo] = sum over chunk p of
 // a_ij v_j (fp64 across tiles); gpic's mf_reduce combines the parts.
+// ---- matrix-free CTA re-balance from measured times -------------------
+// After a listed pass: the CTAs' measured times over their list ranges give
+// a piecewise-constant cost density over the kept tiles; the next pass cuts
+// the same range at equal predicted cost (alpha: step toward that target).
+// Which CTA computes an item never changes a value, so results stay
+// bitwise identical; only the finish time moves.
+__global__ void __launch_bounds__(kMaxRebalanceGrid + 1)
+    mf_rebalance_kernel(const TcArgs a, int G, int64_t* __restrict__ cuts,
+                        const uint64_t* __restrict__ ns, float alpha) {
+  __shared__ double xpos[kMaxRebalanceGrid + 1];
+  __shared__ double cpre[kMaxRebalanceGrid + 1];  // measured cost before CTA b
+  __shared__ int64_t newc[kMaxRebalanceGrid + 1];
+  __shared__ bool have;
+  if (a.ctl != nullptr && *(volatile const int32_t*)&a.ctl->stop) return;
+  const int t = threadIdx.x;
+  const int64_t total = *a.unit_count;
+  int64_t ua, ub;
+  item_share(a, total, ua, ub);
+  const int64_t Wa = a.wpre[ua], W = a.wpre[ub] - Wa;
+  if (t == 0) have = cuts[0] == G && cuts[1] == ua && cuts[2] == ub;
+  __syncthreads();
+  // the cuts the pass used (one thread per cut, each its own search)
+  if (t <= G) {
+    int64_t c;
+    if (have) c = cuts[3 + t];
+    else if (t == G) c = ub;
+    else c = lower_bound_w(a.wpre, ua, ub, Wa + W * t / G);
+    xpos[t] = (double)(a.wpre[c] - Wa);
+  }
+  if (t == 0) {
+    double acc = 0.0;
+    for (int b = 0; b < G; ++b) {
+      cpre[b] = acc;
+      acc += (double)ns[b];
+    }
+    cpre[G] = acc;
+  }
+  __syncthreads();
+  const double T = cpre[G];
+  if (!(T > 0.0) || W <= 0) return;
+  // cut k: where the piecewise-linear measured cost reaches k T / G
+  if (t >= 1 && t < G) {
+    const double target = T * t / G;
+    int lo = 0, hi = G - 1;  // last segment with cpre[seg] <= target
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (cpre[mid] <= target) lo = mid; else hi = mid - 1;
+    }
+    const double len = cpre[lo + 1] - cpre[lo];
+    const double frac = len > 0.0 ? (target - cpre[lo]) / len : 0.0;
+    const double xt = xpos[lo] + fmin(fmax(frac, 0.0), 1.0) * (xpos[lo + 1] - xpos[lo]);
+    const double x = xpos[t] + alpha * (xt - xpos[t]);
+    newc[t] = lower_bound_w(a.wpre, ua, ub, Wa + (int64_t)(x + 0.5));
+  }
+  if (t == 0) {
+    newc[0] = ua;
+    newc[G] = ub;
+  }
+  __syncthreads();
+  if (t == 0) {  // monotone, then the header last
+    for (int k = 1; k <= G; ++k)
+      if (newc[k] < newc[k - 1]) newc[k] = newc[k - 1];
+    for (int k = 0; k <= G; ++k) cuts[3 + k] = newc[k];
+    cuts[1] = ua;
+    cuts[2] = ub;
+    __threadfence();
+    cuts[0] = G;
+  }
+}
+
+int launch_mf_rebalance(const PruneMask* pm, int share_r, int share_n, const gpic_ctl* ctl,
+                        cudaStream_t s) {
+  if (g_num_sms == 0) {
+    int dev;
+    GPIC_CUDA_TRY(cudaGetDevice(&dev));
+    GPIC_CUDA_TRY(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev));
+  }
+  if (g_num_sms > kMaxRebalanceGrid) return GPIC_OK;
+  TcArgs a{};
+  a.unit_list = pm->items;
+  a.unit_count = pm->item_count;
+  a.wpre = pm->item_wpre;
+  a.share_r = share_r;
+  a.share_n = share_n;
+  a.ctl = ctl;
+  const char* e = getenv("GPIC_MF_REBALANCE_ALPHA");
+  const float alpha = e != nullptr ? (float)atof(e) : 1.0f;
+  mf_rebalance_kernel<<<1, kMaxRebalanceGrid + 1, 0, s>>>(a, g_num_sms, pm->cta_cuts, pm->cta_ns,
+                                                         alpha);
+  count_launch();
+  return GPIC_OK;
+}
+
+bool mf_rebalance_enabled() {
+  const char* e = getenv("GPIC_MF_REBALANCE");
+  return e == nullptr || atoi(e) != 0;
+}
+
 int launch_affinity_tc_matvec(const float* xhi, const float* xlo, const float* sqn, int64_t n,
                               int32_t dp, int64_t row_lo, int64_t row_hi, float neg_scale_log2,
                               const float* v32, double* ypart, int64_t rows_pad,
@@ -1430,6 +1566,10 @@ int launch_affinity_tc_matvec(const float* xhi, const float* xlo, const float* s
     args.wpre = pm->item_wpre;
     args.share_r = share_r;
     args.share_n = share_n;
+    if (mf_rebalance_enabled()) {
+      args.cuts = pm->cta_cuts;
+      args.cta_ns = pm->cta_ns;
+    }
   }
   return dispatch_kb<kModeMatvec>(dp / kKBlk, mp, args, s);
 }

@@ -266,6 +266,10 @@ int launch_mf_matvec(const MfOperands& op, int64_t row_lo, int64_t rows, const f
         mf_rows_per_block(op.dp) / 128, deg, pt, ctl, pm ? pm->item_kept : nullptr,
         pm ? pm->skip : nullptr, pm ? pm->B : 1, pm ? pm->nb : 0, sh);
     count_launch();
+    if (pm != nullptr && mf_rebalance_enabled()) {
+      rc = launch_mf_rebalance(pm, op.share_r, op.share_n, ctl, s);
+      if (rc) return rc;
+    }
     GPIC_CUDA_TRY(cudaGetLastError());
     return GPIC_OK;
   }

@@ -209,7 +209,15 @@ struct PruneMask {
   int32_t* rbtiles = nullptr;    // kept tiles per row block
   int64_t* item_wpre = nullptr;  // kept tiles before list entry u (count + 1 entries)
   unsigned* sched = nullptr;     // affinity_tc's dynamic schedule counters (2 words)
+  // matrix-free passes: CTA cuts re-balanced from the last pass's measured
+  // per-CTA times (header: grid, ua, ub; then grid + 1 cuts) and those times
+  int64_t* cta_cuts = nullptr;
+  uint64_t* cta_ns = nullptr;
 };
+// after a pruned matrix-free pass: the next pass's CTA cuts from its times
+int launch_mf_rebalance(const PruneMask* pm, int share_r, int share_n, const gpic_ctl* ctl,
+                        cudaStream_t s);
+bool mf_rebalance_enabled();
 // the schedule counters in the count slot of a mask (from its unit count)
 unsigned* prune_sched(const int64_t* unit_count);
 bool prune_enabled();  // GPIC_PRUNE=0 computes every tile (comparisons)

@@ -675,7 +675,8 @@ int64_t prune_bytes(int64_t n, int32_t dp) {
   const int64_t nt = ceil_div(n, 128);
   return al256(nb * dp * 4) + al256(n * 4) + al256(nb * nb * 4) + al256(nb * nb) +
          al256(nt * (nt + 1) / 2 * 4) + al256(64) + al256(nt * 4) + al256(max_items(n) * 4) +
-         al256(max_items(n)) + al256(nt * 4) + al256((max_items(n) + 1) * 8);
+         al256(max_items(n)) + al256(nt * 4) + al256((max_items(n) + 1) * 8) +
+         al256((3 + 257) * 8) + al256(256 * 8);
 }
 
 // count slot: [0] unit count, [8] item count, [16] scal, [32] sched; c is
@@ -703,7 +704,9 @@ PruneMask carve_prune(void* base, int64_t n, int32_t dp) {
   m.items = reinterpret_cast<int32_t*>(p); p += al256(max_items(n) * 4);
   m.item_kept = p; p += al256(max_items(n));
   m.rbtiles = reinterpret_cast<int32_t*>(p); p += al256(nt * 4);
-  m.item_wpre = reinterpret_cast<int64_t*>(p);
+  m.item_wpre = reinterpret_cast<int64_t*>(p); p += al256((max_items(n) + 1) * 8);
+  m.cta_cuts = reinterpret_cast<int64_t*>(p); p += al256((3 + 257) * 8);
+  m.cta_ns = reinterpret_cast<uint64_t*>(p);
   m.item_count = m.count + 1;
   return m;
 }
@@ -715,6 +718,7 @@ void launch_prune(const PruneMask& m, const float* xc, const double* colpart, co
   const int64_t nb = m.nb, B = m.B;
   fill_u32_kernel<<<(unsigned)ceil_div(nb * nb + 2, 256), 256, 0, s>>>(m.mmax, nb * nb, 0u);
   fill_u32_kernel<<<1, 32, 0, s>>>(m.scal, 6, 0u);  // scal[2], pad, sched[2]
+  fill_u32_kernel<<<1, 32, 0, s>>>(reinterpret_cast<unsigned*>(m.cta_cuts), 2, 0u);  // no cuts yet
   block_centroid_kernel<<<(unsigned)nb, 128, 0, s>>>(colpart, mean, n, d, dp, B, m.cent, m.scal);
   // GPIC_PRUNE_TF32=0: the fp32 SIMT products, =1: wmma, =2 (default):
   // mma.sync with the maxima on the fragments (measurement knob)
