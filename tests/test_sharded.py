@@ -271,3 +271,39 @@ def test_reduce_scatter_exchange_matches_all_to_all(monkeypatch, storage):
         assert np.array_equal(a[0], b[0]), p
         assert np.array_equal(a[1], b[1]), p
         assert np.array_equal(a[2].delta_history, b[2].delta_history), p
+
+
+@pytest.mark.gpu
+def test_work_balanced_packed_shard_ranges():
+    """gpic_packed_shard_ranges_pruned: 512-aligned, strictly increasing,
+    covering [0, n), every rank a super-row, identical on repeat (every rank
+    computes it independently), and balanced by kept tensor units."""
+    import ctypes as C
+
+    import torch
+
+    from paper_1604_02700_b200 import _lib, gpu
+
+    L = _lib.lib()
+    d = gaussian_blobs(20000, 64, 8, seed=3)
+    dev = torch.device("cuda", 0)
+    prep = gpu.prepare_points(torch.from_numpy(d.points).to(dev), dev, _lib.KIND_RBF)
+    scratch = torch.empty(int(L.gpic_prune_scratch_bytes(d.n, prep.d)), dtype=torch.uint8,
+                          device=dev)
+    st = gpu._stream(dev)
+    for P in (2, 3, 8):
+        got = []
+        for _ in range(2):
+            b = (C.c_int64 * (P + 1))()
+            assert L.gpic_packed_shard_ranges_pruned(gpu._ptr(prep.xlo), gpu._ptr(prep.work),
+                                                     d.n, prep.d, 4.0, P, gpu._ptr(scratch), b,
+                                                     st) == _lib.GPIC_OK
+            got.append(list(b))
+        assert got[0] == got[1]
+        b = got[0]
+        assert b[0] == 0 and b[-1] == d.n
+        assert all(x % 512 == 0 for x in b[:-1])
+        assert all(b[r + 1] > b[r] for r in range(P))
+    b = (C.c_int64 * 42)()  # 40 super-rows: 41 ranks are too many
+    assert L.gpic_packed_shard_ranges_pruned(gpu._ptr(prep.xlo), gpu._ptr(prep.work), d.n,
+                                             prep.d, 4.0, 41, gpu._ptr(scratch), b, st) != 0
