@@ -795,16 +795,28 @@ __global__ void __launch_bounds__(kTS)
     }
   };
   // per term: every live tile's partials loaded first (up to 4 tiles x 4
-  // values in flight), then added in the order of the one-at-a-time walk
+  // values in flight), then added in the order of the one-at-a-time walk;
+  // the next term's index and box record are loaded a term ahead (a deeper
+  // pipeline holding the next term's partials too measured slower: 97 vs
+  // 66 us, registers)
+  auto term_sb = [&](int64_t term) {
+    return term < ncol ? tile_index(term, Q, ns) : tile_index(Q, Q + (term - ncol), ns);
+  };
+  int64_t term_next = L > 0 ? tl[0] : 0;
+  Sparse::Rec rec_next = L > 0 ? sp.record(term_sb(term_next)) : Sparse::Rec{};
   for (int e = 0; e < L; ++e) {
-    const int64_t term = tl[e];
+    const int64_t term = term_next;
+    const Sparse::Rec rec = rec_next;
+    if (e + 1 < L) {
+      term_next = tl[e + 1];
+      rec_next = sp.record(term_sb(term_next));
+    }
     float c[kSB][4];
     bool live[kSB];
     int64_t p0;
     const bool col = term < ncol;
     if (col) {  // super-block (term, Q): tiles (p, R), p < R
       const int64_t P = term;
-      const Sparse::Rec rec = sp.record(tile_index(P, Q, ns));
       const int64_t pe = min(min(kSB * P + kSB, R), nt);
       p0 = kSB * P;
 #pragma unroll
@@ -819,7 +831,6 @@ __global__ void __launch_bounds__(kTS)
       }
     } else {  // super-block (Q, Q'): tiles (R, p), p >= R
       const int64_t Qp = Q + (term - ncol);
-      const Sparse::Rec rec = sp.record(tile_index(Q, Qp, ns));
       const int64_t pe = min(kSB * Qp + kSB, nt);
       p0 = kSB * Qp;
 #pragma unroll
