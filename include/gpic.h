@@ -79,8 +79,9 @@ typedef struct gpic_ctl {
   double tau;          /* current L1 normaliser                          */
   uint64_t sync_epoch; /* cross-rank exchange epoch                      */
   uint32_t tau_gen;    /* bumped each time the fused tail publishes tau  */
-  uint32_t reserved;
-  uint8_t pad[256 - 104];
+  uint32_t bar_count;  /* grid barrier of the fused iteration kernel     */
+  uint32_t bar_gen;    /* its generation                                 */
+  uint8_t pad[256 - 108];
 } gpic_ctl;
 
 /* Library identity: "gpic <version> sm_100a". */

@@ -58,8 +58,9 @@ class Ctl(C.Structure):
         ("tau", C.c_double),
         ("sync_epoch", C.c_uint64),
         ("tau_gen", C.c_uint32),
-        ("reserved", C.c_uint32),
-        ("pad", C.c_uint8 * (256 - 104)),
+        ("bar_count", C.c_uint32),
+        ("bar_gen", C.c_uint32),
+        ("pad", C.c_uint8 * (256 - 108)),
     ]
 
 

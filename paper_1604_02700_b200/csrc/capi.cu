@@ -59,7 +59,7 @@ int64_t workspace_bytes(int64_t n, int32_t d, int32_t k, int64_t rows, int32_t /
   b += al(ceil_div(n, 256) * d * 8);          // colpart
   b += al((int64_t)(d + 2) * 8);              // mean + max|x - mean| + spread R^2
   b += al(n_ctiles * rows_pad * 4);           // rowpart
-  b += al((ceil_div(n, kRedBlock) + 1) * 8);  // redpart
+  b += al((ceil_div(n, kRedBlock) + 1) * 8 + ceil_div(n, kRedBlock) * 4);  // redpart + chunk counters
   b += al(n * 8);                             // y
   b += al(n * 8);                             // deg
   b += al(2 * n * 8);                         // v64
@@ -91,7 +91,8 @@ int carve(void* base, int64_t bytes, int64_t n, int32_t d, int32_t k, int64_t ro
   ws->colpart = reinterpret_cast<double*>(take(ceil_div(n, 256) * d * 8));
   ws->mean = reinterpret_cast<double*>(take((int64_t)(d + 2) * 8));
   ws->rowpart = reinterpret_cast<float*>(take(n_ctiles * rows_pad * 4));
-  ws->redpart = reinterpret_cast<double*>(take((ceil_div(n, kRedBlock) + 1) * 8));
+  ws->redpart = reinterpret_cast<double*>(
+      take((ceil_div(n, kRedBlock) + 1) * 8 + ceil_div(n, kRedBlock) * 4));
   ws->y = reinterpret_cast<double*>(take(n * 8));
   ws->deg = reinterpret_cast<double*>(take(n * 8));
   ws->v64 = reinterpret_cast<double*>(take(2 * n * 8));
@@ -976,6 +977,10 @@ int cluster_impl(const double* d_x, int64_t n, int32_t d, double sigma, int32_t 
   L.rows = n;
   L.deg = deg;
   L.redpart = ws.redpart;
+  // the fused iteration kernel's per-chunk ready counters (sym.cu), behind
+  // the tail's partials; each chunk's owner resets its counter after use
+  GPIC_CUDA_TRY(cudaMemsetAsync(ws.redpart + ceil_div(n, kRedBlock) + 1, 0,
+                                ceil_div(n, kRedBlock) * 4, s));
   L.v64 = ws.v64;
   L.v32 = ws.v32;
   L.hist = d_delta_hist;

@@ -26,14 +26,18 @@
 #include <cstring>
 
 #include "common.cuh"
+#include "lowdeg.cuh"
 #include "ops.h"
 
 namespace gpic {
 
 namespace {
 
-constexpr int kLowThreads = 256;
-constexpr int32_t kSmemD = 4096;  // x_i staged in shared memory up to 32 KB
+using lowdeg::kLowThreads;
+using lowdeg::kSmemD;
+using lowdeg::affinity_f64;
+using lowdeg::norm_f64;
+using lowdeg::block_sum;
 
 __global__ void lowdeg_scan_kernel(const double* __restrict__ deg, int64_t n, double thresh,
                                    int64_t* __restrict__ list, unsigned long long* count) {
@@ -44,41 +48,6 @@ __global__ void lowdeg_scan_kernel(const double* __restrict__ deg, int64_t n, do
     const unsigned long long slot = atomicAdd(count, 1ull);
     list[slot] = i;
   }
-}
-
-// a_ij in fp64, the reference's operation order (affinity.py:89-101)
-__device__ __forceinline__ double affinity_f64(const double* xi,
-                                               const double* __restrict__ xj, int32_t d,
-                                               int kind, double scale, double ni, double nj) {
-  double acc = 0.0;
-  if (kind == GPIC_KIND_COSINE) {
-    for (int32_t f = 0; f < d; ++f) acc = __dadd_rn(acc, __dmul_rn(xi[f], xj[f]));
-    const double c = __ddiv_rn(acc, __dmul_rn(ni, nj));
-    return c > 0.0 ? c : 0.0;
-  }
-  for (int32_t f = 0; f < d; ++f) {
-    const double df = __dsub_rn(xi[f], xj[f]);
-    acc = __dadd_rn(acc, __dmul_rn(df, df));
-  }
-  return exp(__dmul_rn(acc, scale));
-}
-
-__device__ __forceinline__ double norm_f64(const double* __restrict__ x, int32_t d) {
-  double s = 0.0;
-  for (int32_t f = 0; f < d; ++f) s = __dadd_rn(s, __dmul_rn(x[f], x[f]));
-  return sqrt(s);
-}
-
-__device__ __forceinline__ double block_sum(double v, double* sh) {
-  v = warp_sum_f64(v);
-  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-  if (l == 0) sh[w] = v;
-  __syncthreads();
-  double t = 0.0;
-  if (threadIdx.x == 0)
-    for (int q = 0; q < kLowThreads / 32; ++q) t += sh[q];
-  __syncthreads();
-  return t;
 }
 
 // One CTA per listed row: sum_j a_ij * (v_j [/ d_i]) in a fixed order
@@ -94,33 +63,32 @@ __global__ void __launch_bounds__(kLowThreads)
   if (kMatvec && *(volatile int32_t*)&ctl->stop) return;
   const unsigned long long cnt = *count;  // the grid strides over the listed rows
   for (unsigned long long r = blockIdx.x; r < cnt; r += gridDim.x) {
-  const int64_t i = list[r];
-  __syncthreads();  // xs of the previous row is consumed
-  const double* xi = d <= kSmemD ? xs : x + i * d;
-  if (d <= kSmemD)
-    for (int32_t f = threadIdx.x; f < d; f += blockDim.x) xs[f] = x[i * d + f];
-  __syncthreads();
-  const double ni = kind == GPIC_KIND_COSINE ? norm_f64(xi, d) : 1.0;
-  const int t = kMatvec ? ctl->iter : 0;
-  const double* __restrict__ v = kMatvec ? v64 + (int64_t)(t & 1) * n : nullptr;
-  const double di = kMatvec ? deg[i] : 1.0;
-  double s = 0.0;
-  for (int64_t j = threadIdx.x; j < n; j += blockDim.x) {
-    if (j == i) continue;  // affinity.py:102-103
-    const double* xj = x + j * d;
-    const double nj = kind == GPIC_KIND_COSINE ? norm_f64(xj, d) : 1.0;
-    const double a = affinity_f64(xi, xj, d, kind, scale, ni, nj);
-    s += kMatvec ? __ddiv_rn(a, di) * v[j] : a;  // W = A / d (affinity.py:126), W v
-  }
-  s = block_sum(s, sh);
-  if (threadIdx.x == 0) {
+    const int64_t i = list[r];
     if (kMatvec) {
-      ((t & 1) ? y1 : y0)[i] = s;
-    } else {
+      const int t = ctl->iter;
+      const double s = lowdeg::matvec_row(x, n, d, kind, scale, i, deg[i],
+                                          v64 + (int64_t)(t & 1) * n, xs, sh);
+      if (threadIdx.x == 0) ((t & 1) ? y1 : y0)[i] = s;
+      continue;
+    }
+    __syncthreads();  // xs of the previous row is consumed
+    const double* xi = d <= kSmemD ? xs : x + i * d;
+    if (d <= kSmemD)
+      for (int32_t f = threadIdx.x; f < d; f += blockDim.x) xs[f] = x[i * d + f];
+    __syncthreads();
+    const double ni = kind == GPIC_KIND_COSINE ? norm_f64(xi, d) : 1.0;
+    double s = 0.0;
+    for (int64_t j = threadIdx.x; j < n; j += blockDim.x) {
+      if (j == i) continue;  // affinity.py:102-103
+      const double* xj = x + j * d;
+      const double nj = kind == GPIC_KIND_COSINE ? norm_f64(xj, d) : 1.0;
+      s += affinity_f64(xi, xj, d, kind, scale, ni, nj);
+    }
+    s = block_sum(s, sh);
+    if (threadIdx.x == 0) {
       deg[i] = s;
       if (!(s > 0.0)) raise_status(ctl, GPIC_E_ZERO_DEGREE, i, -1, s);
     }
-  }
   }
 }
 

@@ -179,14 +179,16 @@ void launch_copy_result(const double* v64, int64_t n, double* out, const gpic_ct
 
 struct PeerTable;
 // boxnz / sb_prefix: block sparsity (SparseMask), null = every box stored
-void launch_sym_gemv(const float* tiles, int64_t n, const float* v32, float* rowp, float* colp,
+struct IterTail;  // below
+bool launch_sym_gemv(const float* tiles, int64_t n, const float* v32, float* rowp, float* colp,
                      const double* deg, const PeerTable& pt, gpic_ctl* ctl, cudaStream_t s,
                      const ShardRange& sr = ShardRange(), const uint8_t* boxnz = nullptr,
-                     const int64_t* sb_prefix = nullptr);
+                     const int64_t* sb_prefix = nullptr, const IterTail* it = nullptr);
 // fp16 packed tiles (GPIC_STORAGE_PACKED16): same partials / reduce
-void launch_sym_gemv16(const void* tiles, int64_t n, const float* v32, float* rowp, float* colp,
+bool launch_sym_gemv16(const void* tiles, int64_t n, const float* v32, float* rowp, float* colp,
                        const double* deg, const PeerTable& pt, gpic_ctl* ctl, cudaStream_t s,
-                       const uint8_t* boxnz = nullptr, const int64_t* sb_prefix = nullptr);
+                       const uint8_t* boxnz = nullptr, const int64_t* sb_prefix = nullptr,
+                       const IterTail* it = nullptr);
 
 // ---- provably-zero block pairs (prune.cu) -------------------------------
 // Row blocks of B rows; skip[S * nb + T] = 1 when every entry between
@@ -352,6 +354,20 @@ struct LowRows {
   const int64_t* list = nullptr;              // row indices (device)
   const unsigned long long* d_count = nullptr;  // device count of list
   int64_t count = 0;  // host copy (0: nothing to do; < 0: unknown, kernels read d_count)
+};
+// What the fused iteration kernel (sym.cu) needs beyond the GEMV's operands:
+// the y ping-pong, the tail's buffers and the low-degree rows. The launch
+// returns true when it replaced reduce + low rows + tail (one whole-matrix
+// rank, list reduce; opt-in: GPIC_FUSED_TAIL=1).
+struct IterTail {
+  double* y0 = nullptr;
+  double* y1 = nullptr;
+  double* redpart = nullptr;
+  double* v64 = nullptr;
+  float* v32 = nullptr;
+  double* hist = nullptr;
+  LowRows low;               // low.count == 0: no listed rows (d_count may be null)
+  const double* low_deg = nullptr;
 };
 double low_degree_threshold(int kind, int64_t n);
 void launch_lowdeg_scan(const double* deg, int64_t n, int kind, int64_t* list,

@@ -21,42 +21,16 @@
 
 #include "common.cuh"
 #include "ops.h"
+#include "tail.cuh"
 
 namespace gpic {
 
 namespace {
 
-constexpr int kRedThreads = 256;
-constexpr int kRedPer = kRedBlock / kRedThreads;  // 8 elements per thread
-
-// ------------------------------------------------- fixed-shape reductions
-// Block b sums y[b*2048, (b+1)*2048) in a fixed pattern; the last block
-// combines the per-block partials in a fixed pattern.
-__device__ __forceinline__ double block_sum_fixed(double v, double* sh) {
-  sh[threadIdx.x] = v;
-  __syncthreads();
-#pragma unroll
-  for (int s = kRedThreads / 2; s > 0; s >>= 1) {
-    if (threadIdx.x < s) sh[threadIdx.x] += sh[threadIdx.x + s];
-    __syncthreads();
-  }
-  const double r = sh[0];
-  __syncthreads();
-  return r;
-}
-
-__device__ __forceinline__ double block_max(double v, double* sh) {
-  sh[threadIdx.x] = v;
-  __syncthreads();
-#pragma unroll
-  for (int s = kRedThreads / 2; s > 0; s >>= 1) {
-    if (threadIdx.x < s) sh[threadIdx.x] = fmax(sh[threadIdx.x], sh[threadIdx.x + s]);
-    __syncthreads();
-  }
-  const double r = sh[0];
-  __syncthreads();
-  return r;
-}
+using tail::kRedThreads;
+using tail::kRedPer;
+using tail::block_sum_fixed;
+using tail::block_max;
 
 // Sum of v[0, n) into *out (and ctl->tau when ctl != null). `guarded` skips
 // when ctl->stop is set (loop mode).
@@ -136,101 +110,18 @@ __global__ void __launch_bounds__(kRedThreads)
   }
 }
 
-// tau_kernel + norm_kernel in one launch (loop mode). The CTAs stride over
-// the same 2048-element chunks with the same fixed-shape sums, the last CTA
-// to arrive combines the partials exactly as tau_kernel does (bitwise the
-// same tau) and publishes it by bumping ctl->tau_gen; the others spin on
-// that generation (grid <= SM count, so every CTA is resident) and then
-// normalise their chunks while y is still in L2.
+// tau_kernel + norm_kernel in one launch (loop mode): tail.cuh.
 __global__ void __launch_bounds__(kRedThreads)
     tail_kernel(const double* __restrict__ y0, const double* __restrict__ y1, int64_t n,
                 double* __restrict__ part, double* __restrict__ v64, float* __restrict__ v32,
                 double* __restrict__ hist, gpic_ctl* ctl) {
   __shared__ double sh[kRedThreads];
-  __shared__ bool s_last;
-  __shared__ double s_tau;
   if (*(volatile int32_t*)&ctl->stop) return;
   const int t = ctl->iter;
   const double* __restrict__ y = (t & 1) ? y1 : y0;
   const unsigned gen0 = *(volatile unsigned*)&ctl->tau_gen;  // read before arriving
-  const int64_t nb = (n + kRedBlock - 1) / kRedBlock;
-  for (int64_t b = blockIdx.x; b < nb; b += gridDim.x) {
-    const int64_t b0 = b * kRedBlock;
-    double s = 0.0;
-#pragma unroll
-    for (int q = 0; q < kRedPer; ++q) {
-      const int64_t i = b0 + threadIdx.x + q * kRedThreads;
-      if (i < n) s += y[i];
-    }
-    s = block_sum_fixed(s, sh);
-    if (threadIdx.x == 0) part[b] = s;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    s_last = atomicAdd(&ctl->arrive[0], 1u) == gridDim.x - 1;
-  }
-  __syncthreads();
-  if (s_last) {
-    __threadfence();
-    double tt = 0.0;  // tau_kernel's last-block pattern
-    for (int64_t i = threadIdx.x; i < nb; i += kRedThreads) tt += __ldcg(part + i);
-    tt = block_sum_fixed(tt, sh);
-    if (threadIdx.x == 0) {
-      ctl->arrive[0] = 0u;
-      ctl->tau = tt;
-      s_tau = tt;
-      if (!(tt > 0.0)) raise_status(ctl, GPIC_E_NONPOS_TAU, 0, -1, tt);
-      __threadfence();
-      atomicAdd(&ctl->tau_gen, 1u);
-    }
-  } else if (threadIdx.x == 0) {
-    unsigned g;
-    for (;;) {
-      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(g) : "l"(&ctl->tau_gen) : "memory");
-      if (g != gen0) break;
-      __nanosleep(32);
-    }
-    s_tau = *(volatile double*)&ctl->tau;
-  }
-  __syncthreads();
-  if (*(volatile int32_t*)&ctl->stop) return;  // NonPositiveTau
-  const double tau = s_tau;
-  const double* __restrict__ vold = v64 + (int64_t)(t & 1) * n;
-  double* __restrict__ vnew = v64 + (int64_t)((t + 1) & 1) * n;
-  double m = 0.0;
-  for (int64_t b = blockIdx.x; b < nb; b += gridDim.x) {
-    const int64_t b0 = b * kRedBlock;
-#pragma unroll
-    for (int q = 0; q < kRedPer; ++q) {
-      const int64_t i = b0 + threadIdx.x + q * kRedThreads;
-      if (i < n) {
-        const double vn = y[i] / tau;
-        m = fmax(m, fabs(vn - vold[i]));
-        vnew[i] = vn;
-        v32[i] = (float)vn;
-      }
-    }
-  }
-  m = block_max(m, sh);
-  if (threadIdx.x == 0)
-    atomicMax(reinterpret_cast<unsigned long long*>(&ctl->delta_bits),
-              (unsigned long long)__double_as_longlong(m));
-  if (!last_block_done(&ctl->arrive[1])) return;
-  if (threadIdx.x == 0) {
-    const double delta = __longlong_as_double((long long)ctl->delta_bits);
-    hist[t] = delta;
-    ctl->delta_bits = 0ull;
-    ctl->arrive[1] = 0u;
-    const int done = t + 1;
-    ctl->iter = done;
-    if (done >= 2 && fabs(delta - hist[t - 1]) <= ctl->eps) {
-      ctl->converged = 1;
-      ctl->stop = 1;
-    } else if (done >= ctl->max_iter) {
-      ctl->stop = 1;
-    }
-  }
+  tail::chunk_sums<false>(y, n, part, sh, gridDim.x);
+  tail::finish<false>(y, n, part, v64, v32, hist, ctl, t, gen0, sh, gridDim.x);
 }
 
 // src / tau[0] -> fp64 + fp32 copies (start vector: k_norm(deg, k_reduce(deg))).
@@ -517,14 +408,28 @@ int run_power_loops(ShardLoop* shards, int nlocal, int64_t n, int32_t max_iter, 
     GPIC_CUDA_TRY(cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0,
                                                 cudaStreamCaptureModeThreadLocal));
     for (int t = 0; t < (unrolled ? max_iter : 1); ++t) {
+      // packed whole-matrix rank: reduce + low rows + tail fused into one
+      // kernel after the GEMV (sym.cu sym_iter_tail_kernel)
+      bool fused[kMaxRanks] = {};
       for (int i = 0; i < nlocal; ++i) {
         const ShardLoop& L = shards[i];
+        IterTail it;
+        it.y0 = L.pt.y[L.pt.self][0];
+        it.y1 = L.pt.y[L.pt.self][1];
+        it.redpart = L.redpart;
+        it.v64 = L.v64;
+        it.v32 = L.v32;
+        it.hist = L.hist;
+        it.low = L.low;
+        if (L.low.count == 0) it.low.d_count = nullptr;
+        it.low_deg = L.low_deg;
+        const IterTail* itp = nlocal == 1 ? &it : nullptr;
         if (L.mode == kLoopPacked) {
-          launch_sym_gemv(L.a, n, L.v32, L.rowp, L.colp, L.deg, L.pt, L.ctl, cs, ShardRange(),
-                          L.boxnz, L.sb_prefix);
+          fused[i] = launch_sym_gemv(L.a, n, L.v32, L.rowp, L.colp, L.deg, L.pt, L.ctl, cs,
+                                     ShardRange(), L.boxnz, L.sb_prefix, itp);
         } else if (L.mode == kLoopPacked16) {
-          launch_sym_gemv16(L.a, n, L.v32, L.rowp, L.colp, L.deg, L.pt, L.ctl, cs, L.boxnz,
-                            L.sb_prefix);
+          fused[i] = launch_sym_gemv16(L.a, n, L.v32, L.rowp, L.colp, L.deg, L.pt, L.ctl, cs,
+                                       L.boxnz, L.sb_prefix, itp);
         } else if (L.mode == kLoopPackedShard) {
           // partial y over the shard's tiles into every rank's slot of this shard
           launch_sym_gemv(L.a, n, L.v32, L.rowp, L.colp, nullptr, L.pt_slots, L.ctl, cs, L.sr,
@@ -557,6 +462,7 @@ int run_power_loops(ShardLoop* shards, int nlocal, int64_t n, int32_t max_iter, 
         launch_slice_combine(L.slots, L.slot_stride, n, L.deg_full, pt, L.ctl, cs);
       }
       for (int i = 0; i < nlocal; ++i) {
+        if (fused[i]) continue;
         const ShardLoop& L = shards[i];
         const PeerTable& pt = L.pt;
         const bool slotted = L.mode == kLoopPackedShard || L.mode == kLoopMfShard;

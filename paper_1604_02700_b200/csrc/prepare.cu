@@ -53,6 +53,7 @@ __global__ void ctl_init_kernel(gpic_ctl* ctl, double eps, int32_t max_iter) {
     for (int i = 0; i < 4; ++i) ctl->arrive[i] = 0u;
     ctl->tau = 0.0;
     ctl->sync_epoch = 0ull;
+    ctl->bar_count = 0u;
   }
 }
 

@@ -24,6 +24,8 @@
 #include "common.cuh"
 #include "ops.h"
 #include "sm100.cuh"
+#include "lowdeg.cuh"
+#include "tail.cuh"
 
 namespace gpic {
 
@@ -695,15 +697,12 @@ __global__ void __launch_bounds__(kTS * kSeg)
 // thread per row, all kSeg segments in turn — the same per-segment sums and
 // the same in-order combine as sym_reduce_kernel (bit for bit), without the
 // 8 threads per row that each walked the list, and small CTAs that all fit
-// on the GPU at once. The stop / flag epilogue is sym_reduce_kernel's.
-__global__ void __launch_bounds__(kTS)
-    sym_reduce_list_kernel(const float* __restrict__ rowp, const float* __restrict__ colp,
-                           int64_t n, int64_t nt, const double* __restrict__ deg,
-                           const PeerTable pt, gpic_ctl* ctl, Sparse sp) {
-  if (ctl != nullptr && *(volatile const int32_t*)&ctl->stop) return;
+// on the GPU at once. Row i = R kTS + o; returns sum / deg_i (deg != null).
+__device__ __forceinline__ double reduce_list_row(const float* __restrict__ rowp,
+                                                  const float* __restrict__ colp, int64_t n,
+                                                  int64_t nt, const double* __restrict__ deg,
+                                                  const Sparse& sp, int64_t R, int o) {
   const int64_t ns = (nt + kSB - 1) / kSB;
-  const int64_t R = blockIdx.x;
-  const int o = threadIdx.x;
   const int64_t Q = R / kSB, k = R - kSB * Q;
   const int64_t ncol = Q + 1, terms = ncol + (ns - Q);
   const int32_t* tl = sp.tlist + Q * sp.tld;
@@ -746,8 +745,20 @@ __global__ void __launch_bounds__(kTS)
     t += seg_sum;
     seg_sum = 0.0;
   }
+  return deg != nullptr ? t / di : t;
+}
+
+// The stop / flag epilogue is sym_reduce_kernel's.
+__global__ void __launch_bounds__(kTS)
+    sym_reduce_list_kernel(const float* __restrict__ rowp, const float* __restrict__ colp,
+                           int64_t n, int64_t nt, const double* __restrict__ deg,
+                           const PeerTable pt, gpic_ctl* ctl, Sparse sp) {
+  if (ctl != nullptr && *(volatile const int32_t*)&ctl->stop) return;
+  const int64_t R = blockIdx.x;
+  const int o = threadIdx.x;
+  const int64_t i = R * kTS + o;
+  const double val = reduce_list_row(rowp, colp, n, nt, deg, sp, R, o);
   if (i < n) {
-    const double val = deg != nullptr ? t / di : t;
     const int parity = ctl != nullptr ? (ctl->iter & 1) : 0;
     const int own = pt.scatter ? slice_owner(i, n, pt.nranks) : -1;
     for (int r = 0; r < pt.nranks; ++r)
@@ -765,6 +776,92 @@ __global__ void __launch_bounds__(kTS)
       for (int r = 0; r < pt.nranks; ++r) st_release_sys(pt.flags[r] + pt.self, epoch);
     }
   }
+}
+
+// Grid barrier of the fused iteration kernel (every CTA resident: the grid
+// is sized from the occupancy): arrive on ctl->bar_count, the last CTA
+// resets it and bumps ctl->bar_gen (read as gen0 before arriving).
+__device__ __forceinline__ void grid_barrier(gpic_ctl* ctl, unsigned gen0) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(&ctl->bar_count, 1u) == gridDim.x - 1) {
+      ctl->bar_count = 0u;
+      __threadfence();
+      atomicAdd(&ctl->bar_gen, 1u);
+    } else {
+      unsigned g;
+      for (;;) {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(g) : "l"(&ctl->bar_gen) : "memory");
+        if (g != gen0) break;
+        __nanosleep(32);
+      }
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+// One iteration's tail in one launch (whole matrix, one rank, list reduce):
+// y = the list reduce (two tile rows per 256-thread CTA) -> grid barrier ->
+// the low-degree rows' fp64 y (lowdeg.cuh, only when the device-side count
+// is non-zero; one more barrier) -> tau, v' = y / tau, delta, stop
+// (tail.cuh). Every value is computed by the same device code, with the
+// same shapes, as sym_reduce_list_kernel + lowdeg_row_kernel + tail_kernel:
+// results are bitwise those of the three-kernel sequence.
+__global__ void __launch_bounds__(tail::kRedThreads, 3)
+    sym_iter_tail_kernel(const float* __restrict__ rowp, const float* __restrict__ colp,
+                         int64_t n, int64_t nt, const double* __restrict__ deg, double* y0,
+                         double* y1, Sparse sp, LowRows low, const double* low_deg,
+                         double low_scale, double* __restrict__ part, double* __restrict__ v64,
+                         float* __restrict__ v32, double* __restrict__ hist, gpic_ctl* ctl,
+                         unsigned tail_ctas, unsigned* ready) {
+  __shared__ double sh[tail::kRedThreads];
+  extern __shared__ double xs[];
+  if (*(volatile int32_t*)&ctl->stop) return;
+  const int t = ctl->iter;
+  double* y = (t & 1) ? y1 : y0;
+  const unsigned tgen0 = *(volatile unsigned*)&ctl->tau_gen;  // read before arriving
+  unsigned bgen = *(volatile unsigned*)&ctl->bar_gen;
+  constexpr int kRows = tail::kRedThreads / kTS;  // tile rows per CTA pass
+  const int o = threadIdx.x % kTS;
+  const unsigned long long cnt = low.d_count != nullptr ? *low.d_count : 0ull;
+  constexpr int64_t kChunkTiles = kRedBlock / kTS;  // 16 tile rows per tail chunk
+  static_assert(kChunkTiles % kRows == 0, "a CTA pass stays inside one chunk");
+  for (int64_t R0 = (int64_t)blockIdx.x * kRows; R0 < nt; R0 += (int64_t)gridDim.x * kRows) {
+    const int64_t R = R0 + threadIdx.x / kTS;
+    if (R < nt) {
+      const double val = reduce_list_row(rowp, colp, n, nt, deg, sp, R, o);
+      const int64_t i = R * kTS + o;
+      if (i < n) y[i] = val;
+    }
+    if (cnt == 0ull) {  // publish the pass's tile rows to the chunk's owner
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(ready + R0 / kChunkTiles, (unsigned)(nt - R0 < kRows ? nt - R0 : kRows));
+      }
+    }
+  }
+  if (cnt != 0ull) {
+    grid_barrier(ctl, bgen);
+    bgen = *(volatile unsigned*)&ctl->bar_gen;  // stable: nobody arrives before this CTA
+    const double* v = v64 + (int64_t)(t & 1) * n;
+    for (unsigned long long r = blockIdx.x; r < cnt; r += gridDim.x) {
+      const int64_t i = low.list[r];
+      const double s = lowdeg::matvec_row(low.x, n, low.d, low.kind, low_scale, i, low_deg[i], v,
+                                          xs, sh);
+      if (threadIdx.x == 0) y[i] = s;
+    }
+    grid_barrier(ctl, bgen);
+  }
+  // the tail on as many CTAs as tail_kernel's grid (one per 2048-row chunk,
+  // at most one per SM): fewer CTAs arriving at and spinning on its barrier
+  const int64_t nb = (n + kRedBlock - 1) / kRedBlock;
+  const unsigned ncta = (unsigned)min(nb, (int64_t)min(gridDim.x, tail_ctas));
+  if (blockIdx.x >= ncta) return;
+  tail::chunk_sums<true>(y, n, part, sh, ncta, cnt == 0ull ? ready : nullptr);
+  tail::finish<true>(y, n, part, v64, v32, hist, ctl, t, tgen0, sh, ncta);
 }
 
 // Degrees over the same per-super-row term lists (whole matrix, sparse):
@@ -1040,6 +1137,50 @@ int gemv_prefetch() {
   return e != nullptr ? atoi(e) : 0;
 }
 
+// GPIC_FUSED_TAIL=1: the fused iteration kernel instead of the three-kernel
+// tail. Off by default: bitwise the same results, but measured no faster at
+// config 3 (ncu: 33.0 us fused vs 14.2 + 3.2 + 16.0 us; in the graph
+// 2.055 vs 2.038 ms per 6 iterations): the tail's time is the latency
+// chain of its fixed-shape reductions, not the launches.
+int fused_tail_enabled() {
+  const char* e = getenv("GPIC_FUSED_TAIL");
+  return e != nullptr && atoi(e) != 0;
+}
+
+// The fused iteration kernel in place of reduce + low rows + tail when the
+// list reduce applies to one whole-matrix rank (no peer stores); false:
+// nothing launched. Grid: the CTAs that are resident at once (its grid
+// barriers spin), at most one per two tile rows.
+bool launch_iter_tail(const IterTail* it, const float* rowp, const float* colp, int64_t n,
+                      int64_t nt, const double* deg, const PeerTable& pt, gpic_ctl* ctl,
+                      const Sparse& sp, cudaStream_t s) {
+  if (it == nullptr || ctl == nullptr || sp.tlist == nullptr || pt.flags[0] != nullptr ||
+      pt.nranks != 1 || pt.scatter || !fused_tail_enabled())
+    return false;
+  if (pt.y[0][0] != it->y0 || pt.y[0][1] != it->y1) return false;
+  const size_t dyn = it->low.d <= lowdeg::kSmemD ? (size_t)it->low.d * sizeof(double) : 0;
+  static int sms = 0;
+  if (sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sym_iter_tail_kernel,
+                                                    tail::kRedThreads, dyn) != cudaSuccess ||
+      per_sm < 1)
+    return false;
+  const int64_t want = (nt + 1) / 2;
+  const int64_t cap = (int64_t)per_sm * sms;
+  const unsigned grid = (unsigned)(want < cap ? want : cap);
+  const double scale = -1.0 / (2.0 * it->low.sigma * it->low.sigma);
+  sym_iter_tail_kernel<<<grid, tail::kRedThreads, dyn, s>>>(
+      rowp, colp, n, nt, deg, it->y0, it->y1, sp, it->low, it->low_deg, scale, it->redpart,
+      it->v64, it->v32, it->hist, ctl, (unsigned)sms,
+      reinterpret_cast<unsigned*>(it->redpart + ceil_div(n, kRedBlock) + 1));
+  return true;
+}
+
 }  // namespace
 
 void launch_sym_degree(const float* degrow, const float* degcol, int64_t n, int nhalf,
@@ -1094,9 +1235,10 @@ int64_t sym_partial_floats(int64_t n) {
   return (tiles > recs ? tiles : recs) * kTS;
 }
 
-void launch_sym_gemv(const float* tiles, int64_t n, const float* v32, float* rowp, float* colp,
+bool launch_sym_gemv(const float* tiles, int64_t n, const float* v32, float* rowp, float* colp,
                      const double* deg, const PeerTable& pt, gpic_ctl* ctl, cudaStream_t s,
-                     const ShardRange& sr, const uint8_t* boxnz, const int64_t* sb_prefix) {
+                     const ShardRange& sr, const uint8_t* boxnz, const int64_t* sb_prefix,
+                     const IterTail* it) {
   // packed shards: their box flags, super-block records and the list of
   // their non-empty super-blocks live in whole-triangle arrays (only the
   // shard's tiles flagged), so the list walk and its claims apply; the
@@ -1122,18 +1264,23 @@ void launch_sym_gemv(const float* tiles, int64_t n, const float* v32, float* row
   const int64_t total = sr.sb_hi(ns) - sr.sb_lo(ns);  // the shard's super-blocks
   const int grid = (int)(total < g_sms ? total : g_sms);
   const int64_t rows = nt - kSB * sr.p_lo;
-  if (grid < 1 || rows < 1) return;
+  if (grid < 1 || rows < 1) return false;
   sym_gemv_kernel<float><<<grid, kThreads, kSmem, s>>>(tiles, nt, v32, rowp, colp, ctl, sr, sp);
+  if (launch_iter_tail(it, rowp, colp, n, nt, deg, pt, ctl, sp, s)) {
+    count_launch(2);
+    return true;
+  }
   if (sp.tlist != nullptr)
     sym_reduce_list_kernel<<<(unsigned)nt, kTS, 0, s>>>(rowp, colp, n, nt, deg, pt, ctl, sp);
   else
     sym_reduce_kernel<<<(unsigned)rows, kTS * kSeg, 0, s>>>(rowp, colp, n, nt, deg, pt, ctl, sr, sp);
   count_launch(2);
+  return false;
 }
 
-void launch_sym_gemv16(const void* tiles, int64_t n, const float* v32, float* rowp, float* colp,
+bool launch_sym_gemv16(const void* tiles, int64_t n, const float* v32, float* rowp, float* colp,
                        const double* deg, const PeerTable& pt, gpic_ctl* ctl, cudaStream_t s,
-                       const uint8_t* boxnz, const int64_t* sb_prefix) {
+                       const uint8_t* boxnz, const int64_t* sb_prefix, const IterTail* it) {
   const SbList sl = boxnz != nullptr && gemv_use_list() ? sb_list(sb_prefix, n)
                                                         : SbList{nullptr, nullptr, nullptr};
   Sparse sp{boxnz, boxnz != nullptr ? sb_prefix : nullptr,
@@ -1149,11 +1296,16 @@ void launch_sym_gemv16(const void* tiles, int64_t n, const float* v32, float* ro
   const ShardRange all{};
   sym_gemv_kernel<__half><<<grid, kThreads, kSmem, s>>>(static_cast<const __half*>(tiles), nt, v32,
                                                             rowp, colp, ctl, all, sp);
+  if (launch_iter_tail(it, rowp, colp, n, nt, deg, pt, ctl, sp, s)) {
+    count_launch(2);
+    return true;
+  }
   if (sp.tlist != nullptr)
     sym_reduce_list_kernel<<<(unsigned)nt, kTS, 0, s>>>(rowp, colp, n, nt, deg, pt, ctl, sp);
   else
     sym_reduce_kernel<<<(unsigned)nt, kTS * kSeg, 0, s>>>(rowp, colp, n, nt, deg, pt, ctl, all, sp);
   count_launch(2);
+  return false;
 }
 
 }  // namespace gpic
