@@ -172,20 +172,31 @@ void launch_slice_combine(const double* slots, int64_t stride, int64_t n, const 
                           const PeerTable& pt, gpic_ctl* ctl, cudaStream_t s);
 void launch_slot_combine(const double* slots, int64_t stride, int nranks, int64_t n,
                          const double* deg, double* y0, double* y1, gpic_ctl* ctl, cudaStream_t s);
-void launch_iteration_tail(const double* y0, const double* y1, int64_t n, double* redpart,
-                           double* v64, float* v32, double* hist, gpic_ctl* ctl, cudaStream_t s);
+// tau_mode: kTailTauAlways / kTailTauIfNoLow (*lowcnt == 0): ctl->tau was
+// computed by the reduce, the tail only normalises
+// low / low_deg: the low-degree rows, whose fp64 y_i the tail computes
+// first (low.count == 0: none; < 0: the device-side count decides)
+struct LowRows;
+void launch_iteration_tail(double* y0, double* y1, int64_t n, double* redpart, double* v64,
+                           float* v32, double* hist, gpic_ctl* ctl, cudaStream_t s, int tau_mode,
+                           const LowRows& low, const double* low_deg);
 void launch_copy_result(const double* v64, int64_t n, double* out, const gpic_ctl* ctl,
                         cudaStream_t s);
 
 struct PeerTable;
 // boxnz / sb_prefix: block sparsity (SparseMask), null = every box stored
 struct IterTail;  // below
-bool launch_sym_gemv(const float* tiles, int64_t n, const float* v32, float* rowp, float* colp,
+// what the GEMV launch took over from the iteration tail (IterTail given):
+// kTailSeparate nothing; kTailTauAlways tau computed in the reduce;
+// kTailTauIfNoLow tau in the reduce when the device-side low-row count is
+// 0; kTailFused reduce + low rows + tau + normalise (GPIC_FUSED_TAIL=1)
+enum : int { kTailSeparate = 0, kTailTauAlways = 1, kTailTauIfNoLow = 2, kTailFused = 3 };
+int launch_sym_gemv(const float* tiles, int64_t n, const float* v32, float* rowp, float* colp,
                      const double* deg, const PeerTable& pt, gpic_ctl* ctl, cudaStream_t s,
                      const ShardRange& sr = ShardRange(), const uint8_t* boxnz = nullptr,
                      const int64_t* sb_prefix = nullptr, const IterTail* it = nullptr);
 // fp16 packed tiles (GPIC_STORAGE_PACKED16): same partials / reduce
-bool launch_sym_gemv16(const void* tiles, int64_t n, const float* v32, float* rowp, float* colp,
+int launch_sym_gemv16(const void* tiles, int64_t n, const float* v32, float* rowp, float* colp,
                        const double* deg, const PeerTable& pt, gpic_ctl* ctl, cudaStream_t s,
                        const uint8_t* boxnz = nullptr, const int64_t* sb_prefix = nullptr,
                        const IterTail* it = nullptr);

@@ -21,6 +21,7 @@
 
 #include "common.cuh"
 #include "ops.h"
+#include "lowdeg.cuh"
 #include "tail.cuh"
 
 namespace gpic {
@@ -111,17 +112,43 @@ __global__ void __launch_bounds__(kRedThreads)
 }
 
 // tau_kernel + norm_kernel in one launch (loop mode): tail.cuh.
+// Low-degree rows (lowdeg.cuh; listed by the device-side count low.d_count,
+// null: none): their fp64 y_i are computed here first, one CTA per listed
+// row as lowdeg_row_kernel does (bitwise the same), then a grid barrier.
 __global__ void __launch_bounds__(kRedThreads)
-    tail_kernel(const double* __restrict__ y0, const double* __restrict__ y1, int64_t n,
-                double* __restrict__ part, double* __restrict__ v64, float* __restrict__ v32,
-                double* __restrict__ hist, gpic_ctl* ctl) {
+    tail_kernel(double* y0, double* y1, int64_t n, double* __restrict__ part,
+                double* __restrict__ v64, float* __restrict__ v32, double* __restrict__ hist,
+                gpic_ctl* ctl, int tau_mode, LowRows low, const double* __restrict__ low_deg,
+                double low_scale) {
   __shared__ double sh[kRedThreads];
+  extern __shared__ double xs[];
   if (*(volatile int32_t*)&ctl->stop) return;
   const int t = ctl->iter;
-  const double* __restrict__ y = (t & 1) ? y1 : y0;
+  double* y = (t & 1) ? y1 : y0;
+  const unsigned long long cnt = low.d_count != nullptr ? *low.d_count : 0ull;
+  if (tau_mode == kTailTauAlways || (tau_mode == kTailTauIfNoLow && cnt == 0ull)) {
+    // the reduce stored this iteration's tau (tail.cuh tau_in_reduce)
+    tail::normalise<false>(y, n, v64, v32, hist, ctl, t, *(volatile double*)&ctl->tau, sh,
+                           gridDim.x);
+    return;
+  }
   const unsigned gen0 = *(volatile unsigned*)&ctl->tau_gen;  // read before arriving
-  tail::chunk_sums<false>(y, n, part, sh, gridDim.x);
-  tail::finish<false>(y, n, part, v64, v32, hist, ctl, t, gen0, sh, gridDim.x);
+  if (cnt == 0ull) {
+    tail::chunk_sums<false>(y, n, part, sh, gridDim.x);
+    tail::finish<false>(y, n, part, v64, v32, hist, ctl, t, gen0, sh, gridDim.x);
+    return;
+  }
+  const unsigned bgen = *(volatile unsigned*)&ctl->bar_gen;
+  const double* v = v64 + (int64_t)(t & 1) * n;
+  for (unsigned long long r = blockIdx.x; r < cnt; r += gridDim.x) {
+    const int64_t i = low.list[r];
+    const double s = lowdeg::matvec_row(low.x, n, low.d, low.kind, low_scale, i, low_deg[i], v, xs,
+                                        sh);
+    if (threadIdx.x == 0) y[i] = s;
+  }
+  tail::grid_barrier(ctl, bgen);
+  tail::chunk_sums<true>(y, n, part, sh, gridDim.x);
+  tail::finish<true>(y, n, part, v64, v32, hist, ctl, t, gen0, sh, gridDim.x);
 }
 
 // src / tau[0] -> fp64 + fp32 copies (start vector: k_norm(deg, k_reduce(deg))).
@@ -274,14 +301,16 @@ void launch_slot_combine(const double* slots, int64_t stride, int nranks, int64_
   count_launch();
 }
 
-void launch_iteration_tail(const double* y0, const double* y1, int64_t n, double* redpart,
-                           double* v64, float* v32, double* hist, gpic_ctl* ctl, cudaStream_t s) {
+void launch_iteration_tail(double* y0, double* y1, int64_t n, double* redpart, double* v64,
+                           float* v32, double* hist, gpic_ctl* ctl, cudaStream_t s, int tau_mode,
+                           const LowRows& low, const double* low_deg) {
   const unsigned nb = (unsigned)ceil_div(n, kRedBlock);
   static const bool split = [] {
     const char* e = getenv("GPIC_TAIL_SPLIT");  // 1: the two-kernel tail (A/B)
     return e != nullptr && atoi(e) != 0;
   }();
   if (split) {
+    if (low.count != 0) launch_lowdeg_matvec(low, low_deg, v64, y0, y1, ctl, s);
     tau_kernel<<<nb, kRedThreads, 0, s>>>(y0, y1, n, redpart, nullptr, ctl, 1);
     norm_kernel<<<nb, kRedThreads, 0, s>>>(y0, y1, n, v64, v32, hist, ctl);
     count_launch(2);
@@ -293,7 +322,12 @@ void launch_iteration_tail(const double* y0, const double* y1, int64_t n, double
     cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
     return (unsigned)v;
   }();
-  tail_kernel<<<nb < sms ? nb : sms, kRedThreads, 0, s>>>(y0, y1, n, redpart, v64, v32, hist, ctl);
+  LowRows lr = low;
+  if (low.count == 0) lr.d_count = nullptr;  // no listed row
+  const size_t dyn = lr.d_count != nullptr && low.d <= lowdeg::kSmemD ? (size_t)low.d * 8 : 0;
+  tail_kernel<<<nb < sms ? nb : sms, kRedThreads, dyn, s>>>(
+      y0, y1, n, redpart, v64, v32, hist, ctl, tau_mode, lr, low_deg,
+      -1.0 / (2.0 * low.sigma * low.sigma));
   count_launch();
 }
 
@@ -410,7 +444,7 @@ int run_power_loops(ShardLoop* shards, int nlocal, int64_t n, int32_t max_iter, 
     for (int t = 0; t < (unrolled ? max_iter : 1); ++t) {
       // packed whole-matrix rank: reduce + low rows + tail fused into one
       // kernel after the GEMV (sym.cu sym_iter_tail_kernel)
-      bool fused[kMaxRanks] = {};
+      int took[kMaxRanks] = {};  // what the GEMV launch took over (ops.h kTail*)
       for (int i = 0; i < nlocal; ++i) {
         const ShardLoop& L = shards[i];
         IterTail it;
@@ -425,10 +459,10 @@ int run_power_loops(ShardLoop* shards, int nlocal, int64_t n, int32_t max_iter, 
         it.low_deg = L.low_deg;
         const IterTail* itp = nlocal == 1 ? &it : nullptr;
         if (L.mode == kLoopPacked) {
-          fused[i] = launch_sym_gemv(L.a, n, L.v32, L.rowp, L.colp, L.deg, L.pt, L.ctl, cs,
+          took[i] = launch_sym_gemv(L.a, n, L.v32, L.rowp, L.colp, L.deg, L.pt, L.ctl, cs,
                                      ShardRange(), L.boxnz, L.sb_prefix, itp);
         } else if (L.mode == kLoopPacked16) {
-          fused[i] = launch_sym_gemv16(L.a, n, L.v32, L.rowp, L.colp, L.deg, L.pt, L.ctl, cs,
+          took[i] = launch_sym_gemv16(L.a, n, L.v32, L.rowp, L.colp, L.deg, L.pt, L.ctl, cs,
                                        L.boxnz, L.sb_prefix, itp);
         } else if (L.mode == kLoopPackedShard) {
           // partial y over the shard's tiles into every rank's slot of this shard
@@ -462,7 +496,7 @@ int run_power_loops(ShardLoop* shards, int nlocal, int64_t n, int32_t max_iter, 
         launch_slice_combine(L.slots, L.slot_stride, n, L.deg_full, pt, L.ctl, cs);
       }
       for (int i = 0; i < nlocal; ++i) {
-        if (fused[i]) continue;
+        if (took[i] == kTailFused) continue;
         const ShardLoop& L = shards[i];
         const PeerTable& pt = L.pt;
         const bool slotted = L.mode == kLoopPackedShard || L.mode == kLoopMfShard;
@@ -475,11 +509,9 @@ int run_power_loops(ShardLoop* shards, int nlocal, int64_t n, int32_t max_iter, 
             launch_slot_combine(L.slots, L.slot_stride, pt.nranks, n, L.deg_full,
                                 pt.y[pt.self][0], pt.y[pt.self][1], L.ctl, cs);
         }
-        if (L.low.count != 0)  // < 0: the count stays on the device
-          launch_lowdeg_matvec(L.low, L.low_deg, L.v64, pt.y[pt.self][0], pt.y[pt.self][1], L.ctl,
-                               cs);
+        // the low-degree rows' y (count < 0: on the device) inside the tail
         launch_iteration_tail(pt.y[pt.self][0], pt.y[pt.self][1], n, L.redpart, L.v64, L.v32,
-                              L.hist, L.ctl, cs);
+                              L.hist, L.ctl, cs, took[i], L.low, L.low_deg);
       }
     }
     if (!unrolled) {

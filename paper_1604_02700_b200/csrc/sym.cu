@@ -752,18 +752,24 @@ __device__ __forceinline__ double reduce_list_row(const float* __restrict__ rowp
 __global__ void __launch_bounds__(kTS)
     sym_reduce_list_kernel(const float* __restrict__ rowp, const float* __restrict__ colp,
                            int64_t n, int64_t nt, const double* __restrict__ deg,
-                           const PeerTable pt, gpic_ctl* ctl, Sparse sp) {
+                           const PeerTable pt, gpic_ctl* ctl, Sparse sp, double* tau_part,
+                           unsigned* tau_ready, int tau_mode,
+                           const unsigned long long* lowcnt) {
   if (ctl != nullptr && *(volatile const int32_t*)&ctl->stop) return;
   const int64_t R = blockIdx.x;
   const int o = threadIdx.x;
   const int64_t i = R * kTS + o;
   const double val = reduce_list_row(rowp, colp, n, nt, deg, sp, R, o);
+  const int parity = ctl != nullptr ? (ctl->iter & 1) : 0;
   if (i < n) {
-    const int parity = ctl != nullptr ? (ctl->iter & 1) : 0;
     const int own = pt.scatter ? slice_owner(i, n, pt.nranks) : -1;
     for (int r = 0; r < pt.nranks; ++r)
       if (own < 0 || own == r) pt.y[r][parity][i] = val;
   }
+  // one whole-matrix rank: tau right here (kTailTauAlways), or when no
+  // low-degree row will still rewrite y (kTailTauIfNoLow, device count)
+  if (tau_mode == kTailTauAlways || (tau_mode == kTailTauIfNoLow && *lowcnt == 0ull))
+    tail::tau_in_reduce(pt.y[0][parity], n, R, nt, tau_part, tau_ready, ctl);
   if (pt.flags[0] == nullptr) return;
   __threadfence_system();
   __syncthreads();
@@ -776,30 +782,6 @@ __global__ void __launch_bounds__(kTS)
       for (int r = 0; r < pt.nranks; ++r) st_release_sys(pt.flags[r] + pt.self, epoch);
     }
   }
-}
-
-// Grid barrier of the fused iteration kernel (every CTA resident: the grid
-// is sized from the occupancy): arrive on ctl->bar_count, the last CTA
-// resets it and bumps ctl->bar_gen (read as gen0 before arriving).
-__device__ __forceinline__ void grid_barrier(gpic_ctl* ctl, unsigned gen0) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    if (atomicAdd(&ctl->bar_count, 1u) == gridDim.x - 1) {
-      ctl->bar_count = 0u;
-      __threadfence();
-      atomicAdd(&ctl->bar_gen, 1u);
-    } else {
-      unsigned g;
-      for (;;) {
-        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(g) : "l"(&ctl->bar_gen) : "memory");
-        if (g != gen0) break;
-        __nanosleep(32);
-      }
-    }
-    __threadfence();
-  }
-  __syncthreads();
 }
 
 // One iteration's tail in one launch (whole matrix, one rank, list reduce):
@@ -844,7 +826,7 @@ __global__ void __launch_bounds__(tail::kRedThreads, 3)
     }
   }
   if (cnt != 0ull) {
-    grid_barrier(ctl, bgen);
+    tail::grid_barrier(ctl, bgen);
     bgen = *(volatile unsigned*)&ctl->bar_gen;  // stable: nobody arrives before this CTA
     const double* v = v64 + (int64_t)(t & 1) * n;
     for (unsigned long long r = blockIdx.x; r < cnt; r += gridDim.x) {
@@ -853,7 +835,7 @@ __global__ void __launch_bounds__(tail::kRedThreads, 3)
                                           xs, sh);
       if (threadIdx.x == 0) y[i] = s;
     }
-    grid_barrier(ctl, bgen);
+    tail::grid_barrier(ctl, bgen);
   }
   // the tail on as many CTAs as tail_kernel's grid (one per 2048-row chunk,
   // at most one per SM): fewer CTAs arriving at and spinning on its barrier
@@ -1181,6 +1163,40 @@ bool launch_iter_tail(const IterTail* it, const float* rowp, const float* colp, 
   return true;
 }
 
+// tau inside the list reduce (tail.cuh tau_in_reduce) for one whole-matrix
+// rank without peer stores: opt-in, GPIC_TAU_IN_REDUCE=1 (not with
+// GPIC_TAIL_SPLIT=1). Bitwise the tail's tau, but measured no faster at
+// config 3 (2.002 vs 2.006 ms per 6 iterations): the chunk-completion chain
+// at the end of the reduce costs what the tail's barrier did.
+struct TauPlan {
+  double* part = nullptr;
+  unsigned* ready = nullptr;
+  int mode = kTailSeparate;
+  const unsigned long long* lowcnt = nullptr;
+};
+TauPlan tau_plan(const IterTail* it, const PeerTable& pt, const gpic_ctl* ctl, int64_t n) {
+  static const bool on = [] {
+    const char* e = getenv("GPIC_TAU_IN_REDUCE");
+    const char* sp = getenv("GPIC_TAIL_SPLIT");
+    return (e != nullptr && atoi(e) != 0) && !(sp != nullptr && atoi(sp) != 0);
+  }();
+  TauPlan tp;
+  if (!on || it == nullptr || ctl == nullptr || pt.flags[0] != nullptr || pt.nranks != 1 ||
+      pt.scatter || pt.y[0][0] != it->y0 || pt.y[0][1] != it->y1)
+    return tp;
+  if (it->low.count == 0) {
+    tp.mode = kTailTauAlways;
+  } else if (it->low.count < 0 && it->low.d_count != nullptr) {
+    tp.mode = kTailTauIfNoLow;
+    tp.lowcnt = it->low.d_count;
+  } else {
+    return tp;  // listed rows rewrite y after the reduce: the tail sums
+  }
+  tp.part = it->redpart;
+  tp.ready = reinterpret_cast<unsigned*>(it->redpart + ceil_div(n, kRedBlock) + 1);
+  return tp;
+}
+
 }  // namespace
 
 void launch_sym_degree(const float* degrow, const float* degcol, int64_t n, int nhalf,
@@ -1235,7 +1251,7 @@ int64_t sym_partial_floats(int64_t n) {
   return (tiles > recs ? tiles : recs) * kTS;
 }
 
-bool launch_sym_gemv(const float* tiles, int64_t n, const float* v32, float* rowp, float* colp,
+int launch_sym_gemv(const float* tiles, int64_t n, const float* v32, float* rowp, float* colp,
                      const double* deg, const PeerTable& pt, gpic_ctl* ctl, cudaStream_t s,
                      const ShardRange& sr, const uint8_t* boxnz, const int64_t* sb_prefix,
                      const IterTail* it) {
@@ -1264,21 +1280,26 @@ bool launch_sym_gemv(const float* tiles, int64_t n, const float* v32, float* row
   const int64_t total = sr.sb_hi(ns) - sr.sb_lo(ns);  // the shard's super-blocks
   const int grid = (int)(total < g_sms ? total : g_sms);
   const int64_t rows = nt - kSB * sr.p_lo;
-  if (grid < 1 || rows < 1) return false;
+  if (grid < 1 || rows < 1) return kTailSeparate;
   sym_gemv_kernel<float><<<grid, kThreads, kSmem, s>>>(tiles, nt, v32, rowp, colp, ctl, sr, sp);
   if (launch_iter_tail(it, rowp, colp, n, nt, deg, pt, ctl, sp, s)) {
     count_launch(2);
-    return true;
+    return kTailFused;
   }
-  if (sp.tlist != nullptr)
-    sym_reduce_list_kernel<<<(unsigned)nt, kTS, 0, s>>>(rowp, colp, n, nt, deg, pt, ctl, sp);
+  if (sp.tlist != nullptr) {
+    const TauPlan tp = tau_plan(it, pt, ctl, n);
+    sym_reduce_list_kernel<<<(unsigned)nt, kTS, 0, s>>>(rowp, colp, n, nt, deg, pt, ctl, sp,
+                                                        tp.part, tp.ready, tp.mode, tp.lowcnt);
+    count_launch(2);
+    return tp.mode;
+  }
   else
     sym_reduce_kernel<<<(unsigned)rows, kTS * kSeg, 0, s>>>(rowp, colp, n, nt, deg, pt, ctl, sr, sp);
   count_launch(2);
-  return false;
+  return kTailSeparate;
 }
 
-bool launch_sym_gemv16(const void* tiles, int64_t n, const float* v32, float* rowp, float* colp,
+int launch_sym_gemv16(const void* tiles, int64_t n, const float* v32, float* rowp, float* colp,
                        const double* deg, const PeerTable& pt, gpic_ctl* ctl, cudaStream_t s,
                        const uint8_t* boxnz, const int64_t* sb_prefix, const IterTail* it) {
   const SbList sl = boxnz != nullptr && gemv_use_list() ? sb_list(sb_prefix, n)
@@ -1298,14 +1319,19 @@ bool launch_sym_gemv16(const void* tiles, int64_t n, const float* v32, float* ro
                                                             rowp, colp, ctl, all, sp);
   if (launch_iter_tail(it, rowp, colp, n, nt, deg, pt, ctl, sp, s)) {
     count_launch(2);
-    return true;
+    return kTailFused;
   }
-  if (sp.tlist != nullptr)
-    sym_reduce_list_kernel<<<(unsigned)nt, kTS, 0, s>>>(rowp, colp, n, nt, deg, pt, ctl, sp);
+  if (sp.tlist != nullptr) {
+    const TauPlan tp = tau_plan(it, pt, ctl, n);
+    sym_reduce_list_kernel<<<(unsigned)nt, kTS, 0, s>>>(rowp, colp, n, nt, deg, pt, ctl, sp,
+                                                        tp.part, tp.ready, tp.mode, tp.lowcnt);
+    count_launch(2);
+    return tp.mode;
+  }
   else
     sym_reduce_kernel<<<(unsigned)nt, kTS * kSeg, 0, s>>>(rowp, colp, n, nt, deg, pt, ctl, all, sp);
   count_launch(2);
-  return false;
+  return kTailSeparate;
 }
 
 }  // namespace gpic

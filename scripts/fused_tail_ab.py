@@ -2,7 +2,9 @@
 three-kernel tail (reduce + low rows + tail): embeddings, delta histories and
 labels must be bitwise equal; prints the iterate-phase time of each.
 
-    python scripts/fused_tail_ab.py            # parent: runs both settings
+    python scripts/fused_tail_ab.py [KNOB]     # parent: runs KNOB=0 and KNOB=1
+                                               # (default GPIC_FUSED_TAIL; also
+                                               # GPIC_TAU_IN_REDUCE)
 """
 import os
 import subprocess
@@ -48,13 +50,14 @@ def child(out):
 
 
 if __name__ == "__main__":
-    if len(sys.argv) > 1:
+    if len(sys.argv) > 1 and sys.argv[1].endswith(".npz"):
         child(sys.argv[1])
         sys.exit(0)
+    knob = sys.argv[1] if len(sys.argv) > 1 else "GPIC_FUSED_TAIL"
     outs = {}
     for flag in ("0", "1"):
-        out = f"/tmp/fused_tail_{flag}.npz"
-        env = dict(os.environ, GPIC_FUSED_TAIL=flag)
+        out = f"/tmp/tail_ab_{knob}_{flag}.npz"
+        env = dict(os.environ, **{knob: flag})
         subprocess.run([sys.executable, __file__, out], check=True, env=env)
         outs[flag] = np.load(out)
     a, b = outs["0"], outs["1"]
@@ -63,6 +66,6 @@ if __name__ == "__main__":
         same = all(np.array_equal(a[f"{name}_{k}"], b[f"{name}_{k}"]) for k in ("labels", "v", "hist"))
         ok &= same
         print(f"{name}: bitwise {'equal' if same else 'DIFFERENT'}; iterate "
-              f"{float(a[name + '_iterate_ms']):.3f} ms (three kernels) -> "
-              f"{float(b[name + '_iterate_ms']):.3f} ms (fused), T = {len(b[name + '_hist'])}")
+              f"{float(a[name + '_iterate_ms']):.3f} ms ({knob}=0) -> "
+              f"{float(b[name + '_iterate_ms']):.3f} ms ({knob}=1), T = {len(b[name + '_hist'])}")
     sys.exit(0 if ok else 1)

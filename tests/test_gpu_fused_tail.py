@@ -1,7 +1,11 @@
-"""The opt-in fused iteration kernel (GPIC_FUSED_TAIL=1: reduce + low rows +
-tau + normalise in one launch, sym.cu sym_iter_tail_kernel) gives bitwise the
-results of the default three-kernel tail. The graph cache keys do not
-include the knob, so each setting runs in its own process."""
+"""Iteration-tail variants give bitwise the same results:
+* GPIC_FUSED_TAIL=1 (opt-in): reduce + low rows + tau + normalise in one
+  launch (sym.cu sym_iter_tail_kernel) against the separate kernels;
+* GPIC_TAU_IN_REDUCE=1 (opt-in): tau formed inside the list reduce by the
+  CTAs that complete each chunk (tail.cuh tau_in_reduce) against the tail's
+  own chunk sums and barrier.
+The graph cache keys do not include the knobs, so each setting runs in its
+own process."""
 
 import os
 import subprocess
@@ -36,11 +40,12 @@ np.savez(sys.argv[1], **out)
 
 
 @pytest.mark.gpu
-def test_fused_tail_is_bitwise_the_three_kernel_tail(tmp_path):
+@pytest.mark.parametrize("knob", ["GPIC_FUSED_TAIL", "GPIC_TAU_IN_REDUCE"])
+def test_tail_variants_are_bitwise_equal(tmp_path, knob):
     res = {}
     for flag in ("0", "1"):
         out = str(tmp_path / f"r{flag}.npz")
-        env = dict(os.environ, GPIC_FUSED_TAIL=flag)
+        env = dict(os.environ, **{knob: flag})
         subprocess.run([sys.executable, "-c", CHILD, out, ROOT], check=True, env=env, timeout=600)
         res[flag] = np.load(out)
     for key in res["0"].files:
