@@ -307,3 +307,30 @@ def test_work_balanced_packed_shard_ranges():
     b = (C.c_int64 * 42)()  # 40 super-rows: 41 ranks are too many
     assert L.gpic_packed_shard_ranges_pruned(gpu._ptr(prep.xlo), gpu._ptr(prep.work), d.n,
                                              prep.d, 4.0, 41, gpu._ptr(scratch), b, st) != 0
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("storage", ["dense", "packed"])
+def test_virtual_ranks_honour_the_start_vector(storage):
+    """v0 = 'uniform' and an explicit start vector on p > 1 ranks give the
+    single-rank run's embedding (parallel.py:210-214 honours v0 for any p):
+    bitwise on dense row shards, within 1e-6 relative L1 on packed shards
+    (partial y summed in rank order); a degree start differs from both."""
+    d = gaussian_blobs(3000, 32, 5, seed=2)
+    kind = GaussianRbf(float(np.sqrt(32) / 2))
+    rng = np.random.default_rng(7)
+    w = rng.uniform(0.5, 1.5, d.n)
+    for v0 in ("uniform", w / w.sum()):
+        params = PicParams(k=5, epsilon=5e-324, max_iterations=5, v0=v0)
+        base = cluster(d, kind, params, config=KernelConfig(storage=storage), seed=1)
+        deg = cluster(d, kind, PicParams(k=5, epsilon=5e-324, max_iterations=5),
+                      config=KernelConfig(storage=storage), seed=1)
+        assert not np.array_equal(base[1], deg[1])
+        for p in (2, 3):
+            got = cluster(d, kind, params, seed=1,
+                          config=KernelConfig(p=p, virtual_ranks=True, storage=storage))
+            assert got[2].iterations_run == 5
+            if storage == "dense":
+                assert np.array_equal(got[1], base[1]), (p, storage)
+            else:
+                assert np.abs(got[1] - base[1]).sum() / np.abs(base[1]).sum() <= 1e-6, (p, storage)
