@@ -48,6 +48,14 @@ int64_t operand_floats(int64_t n, int32_t d) { return row_pad(n) * (feature_pitc
 
 static inline int64_t al(int64_t b) { return (b + 255) & ~int64_t(255); }
 
+// Page-locked readback slots of the routing decision (one set per host
+// thread): a pageable destination would make the copy itself the sync.
+static double* routing_probe() {
+  static thread_local double* p = nullptr;
+  if (p == nullptr && cudaMallocHost(reinterpret_cast<void**>(&p), 64) != cudaSuccess) p = nullptr;
+  return p;
+}
+
 int64_t workspace_bytes(int64_t n, int32_t d, int32_t k, int64_t rows, int32_t /*max_iter*/) {
   const int64_t dp = feature_pitch(d), npad = row_pad(n);
   const int64_t rows_pad = round_up(rows, kTileM);
@@ -849,14 +857,50 @@ int cluster_impl(const double* d_x, int64_t n, int32_t d, double sigma, int32_t 
   GPIC_CUDA_TRY(cudaMemsetAsync(loc.metric + 2, 0, 8, s));
   bool reordered = false;
   const double* x_run = d_x;  // the points the run works on (permuted when reordered)
+  // packed storage, RBF, tensor engine: the tile pruning of the input order
+  // is launched before the host waits for the routing decision below, so
+  // the GPU runs it while the host wakes up and decides (kept when the
+  // decision is the tensor engine on the input order, the common case;
+  // otherwise redone / unused — it only writes the pruning scratch and
+  // the box flags, both rewritten before use)
+  const bool packed_rbf_tc = packed_any && kind == GPIC_KIND_RBF && impl == GPIC_AFFINITY_TC &&
+                             sparse_enabled() && prune_enabled();
+  bool pruned_early = false;
   if (kind == GPIC_KIND_RBF && impl == GPIC_AFFINITY_TC &&
       (storage != GPIC_STORAGE_NONE || may_reorder)) {
     // data-driven engine choice: the spread R^2 from the prepare pass
     double spread2 = 0.0, metric[2] = {0.0, 0.0};
-    GPIC_CUDA_TRY(cudaMemcpyAsync(&spread2, ws.mean + d + 1, 8, cudaMemcpyDeviceToHost, s));
-    if (may_reorder) GPIC_CUDA_TRY(cudaMemcpyAsync(metric, loc.metric, 16, cudaMemcpyDeviceToHost, s));
-    GPIC_CUDA_TRY(cudaStreamSynchronize(s));
+    double* probe = routing_probe();
+    if (probe != nullptr) {
+      GPIC_CUDA_TRY(cudaMemcpyAsync(probe, ws.mean + d + 1, 8, cudaMemcpyDeviceToHost, s));
+      if (may_reorder)
+        GPIC_CUDA_TRY(cudaMemcpyAsync(probe + 1, loc.metric, 16, cudaMemcpyDeviceToHost, s));
+      cudaEvent_t ev;
+      GPIC_CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+      GPIC_CUDA_TRY(cudaEventRecord(ev, s));
+      if (packed_rbf_tc) {
+        const SparseMask sm0 = carve_sparse(ws.sparse, n, d);
+        const PruneMask pm0 = carve_prune(ws.prune, n, dp);
+        GPIC_CUDA_TRY(cudaMemsetAsync(sm0.boxnz, 0, packed_tiles(n) * 16, s));
+        launch_prune(pm0, ws.xlo, ws.colpart, ws.mean, n, d, dp, sigma, tc_mblocks(dp), 0, s);
+        pruned_early = true;
+      }
+      const cudaError_t e = cudaEventSynchronize(ev);
+      cudaEventDestroy(ev);
+      GPIC_CUDA_TRY(e);
+      spread2 = probe[0];
+      if (may_reorder) {
+        metric[0] = probe[1];
+        metric[1] = probe[2];
+      }
+    } else {
+      GPIC_CUDA_TRY(cudaMemcpyAsync(&spread2, ws.mean + d + 1, 8, cudaMemcpyDeviceToHost, s));
+      if (may_reorder)
+        GPIC_CUDA_TRY(cudaMemcpyAsync(metric, loc.metric, 16, cudaMemcpyDeviceToHost, s));
+      GPIC_CUDA_TRY(cudaStreamSynchronize(s));
+    }
     effective_engine(kind, d, &impl, &storage, spread2, sigma);
+    if (impl != GPIC_AFFINITY_TC) pruned_early = false;
     // index neighbours about as far apart as random pairs (E|x_i - x_j|^2 =
     // 2 E|x|^2 for centred data): reorder; cluster-ordered data sit near 0
     if (may_reorder && impl == GPIC_AFFINITY_TC &&
@@ -865,6 +909,7 @@ int cluster_impl(const double* d_x, int64_t n, int32_t d, double sigma, int32_t 
       if (rc2) return rc2;
       x_run = loc.xp;
       reordered = true;
+      pruned_early = false;  // the order changed: prune again below
       static const double one = 1.0;  // recorded for gpic_cluster_permutation
       GPIC_CUDA_TRY(cudaMemcpyAsync(loc.metric + 2, &one, 8, cudaMemcpyHostToDevice, s));
       launch_prepare(x_run, n, d, ws.xhi, ws.xlo, ws.sqn, ws.colpart, ws.mean, ws.ctl, s, kind);
@@ -893,7 +938,7 @@ int cluster_impl(const double* d_x, int64_t n, int32_t d, double sigma, int32_t 
     // not computed at all (prune.cu); their box flags stay 0
     const bool prune = sparse && kind == GPIC_KIND_RBF && prune_enabled();
     const PruneMask pm = carve_prune(ws.prune, n, dp);
-    if (prune) {
+    if (prune && !pruned_early) {
       GPIC_CUDA_TRY(cudaMemsetAsync(sm.boxnz, 0, packed_tiles(n) * 16, s));
       launch_prune(pm, ws.xlo, ws.colpart, ws.mean, n, d, dp, sigma, tc_mblocks(dp), 0, s);
     }
