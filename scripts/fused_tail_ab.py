@@ -54,18 +54,23 @@ if __name__ == "__main__":
         child(sys.argv[1])
         sys.exit(0)
     knob = sys.argv[1] if len(sys.argv) > 1 else "GPIC_FUSED_TAIL"
+    values = sys.argv[2:] or ["0", "1"]
     outs = {}
-    for flag in ("0", "1"):
+    for flag in values:
         out = f"/tmp/tail_ab_{knob}_{flag}.npz"
         env = dict(os.environ, **{knob: flag})
         subprocess.run([sys.executable, __file__, out], check=True, env=env)
         outs[flag] = np.load(out)
-    a, b = outs["0"], outs["1"]
+    a = outs[values[0]]
     ok = True
-    for name in CASES:
-        same = all(np.array_equal(a[f"{name}_{k}"], b[f"{name}_{k}"]) for k in ("labels", "v", "hist"))
-        ok &= same
-        print(f"{name}: bitwise {'equal' if same else 'DIFFERENT'}; iterate "
-              f"{float(a[name + '_iterate_ms']):.3f} ms ({knob}=0) -> "
-              f"{float(b[name + '_iterate_ms']):.3f} ms ({knob}=1), T = {len(b[name + '_hist'])}")
+    for flag in values[1:]:
+        b = outs[flag]
+        for name in CASES:
+            same = all(np.array_equal(a[f"{name}_{k}"], b[f"{name}_{k}"])
+                       for k in ("labels", "v", "hist"))
+            ok &= same
+            print(f"{name}: bitwise {'equal' if same else 'DIFFERENT'}; iterate "
+                  f"{float(a[name + '_iterate_ms']):.3f} ms ({knob}={values[0]}) -> "
+                  f"{float(b[name + '_iterate_ms']):.3f} ms ({knob}={flag}), "
+                  f"T = {len(b[name + '_hist'])}")
     sys.exit(0 if ok else 1)
