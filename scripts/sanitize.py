@@ -31,3 +31,15 @@ if which in ("all", "d128"):
     g = gaussian_blobs(1500, 100, 4, seed=2)
     labels, _, _ = cluster(g, GaussianRbf(5.0), PicParams(k=4), seed=0)
     print("d=100", np.bincount(labels))
+if which in ("all", "isolated"):
+    # a point ~50 from the rest: its fp32 row flushes, the fp64 degree stays
+    # ~1e-60, so the tail computes its y in fp64 every iteration (lowdeg.cuh)
+    rng = np.random.default_rng(1)
+    pts = rng.normal(size=(1200, 16))
+    pts[17] += 12.5
+    from paper_1604_02700_b200 import DataSet  # noqa: E402
+    for storage in ("packed", "dense"):
+        labels, _, tr = cluster(DataSet(pts), GaussianRbf(3.0), PicParams(k=2),
+                                config=KernelConfig(storage=storage), seed=0)
+        print("isolated", storage, "outlier alone" if np.bincount(labels).min() == 1 else "OUTLIER MERGED",
+              tr.iterations_run)
