@@ -188,6 +188,97 @@ __global__ void __launch_bounds__(kScanThreads)
   }
 }
 
+// sb_scan_kernel + sb_list_kernel in one CTA with the weights staged in
+// shared memory (config 3: 19,306 super-blocks, 154 KB): every global
+// access is coalesced and the per-thread segment walks run on shared
+// memory. The same segments, sums and entries: the same integers.
+constexpr int64_t kScanSmemMax = 200 * 1024;
+__global__ void __launch_bounds__(kScanThreads)
+    sb_scan_list_smem_kernel(int64_t nt, int64_t* __restrict__ prefix, int32_t* __restrict__ list,
+                             int64_t* __restrict__ lpre, int64_t* __restrict__ count_out,
+                             int grid, int64_t* __restrict__ ranges) {
+  extern __shared__ int64_t sp[];  // prefix[0 .. total]
+  __shared__ int64_t wsum[kScanThreads / 32];
+  const int64_t ns = (nt + kSB - 1) / kSB;
+  const int64_t total = ns * (ns + 1) / 2;
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  for (int64_t i = t; i <= total; i += kScanThreads) sp[i] = prefix[i];
+  __syncthreads();
+  const int64_t seg = (total + kScanThreads - 1) / kScanThreads;
+  const int64_t a = min(total, t * seg), b = min(total, a + seg);
+  // block-wide exclusive scan of one value per thread (warp shuffles)
+  auto block_excl = [&](int64_t c, int64_t* tot) {
+    int64_t incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane == 31) wsum[w] = incl;
+    __syncthreads();
+    if (w == 0) {
+      int64_t v = lane < kScanThreads / 32 ? wsum[lane] : 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int64_t y = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += y;
+      }
+      if (lane < kScanThreads / 32) wsum[lane] = v;
+    }
+    __syncthreads();
+    const int64_t r = (w > 0 ? wsum[w - 1] : 0) + incl - c;
+    *tot = wsum[kScanThreads / 32 - 1];
+    __syncthreads();  // wsum is reused
+    return r;
+  };
+  // the weight prefix (sb_scan_kernel)
+  int64_t c = 0;
+  for (int64_t i = a; i < b; ++i) c += sp[i + 1];
+  int64_t tot;
+  int64_t run = block_excl(c, &tot);
+  for (int64_t i = a; i < b; ++i) {
+    run += sp[i + 1];
+    sp[i + 1] = run;
+  }
+  __syncthreads();
+  for (int64_t i = t + 1; i <= total; i += kScanThreads) prefix[i] = sp[i];
+  // the non-empty list (sb_list_kernel)
+  int64_t k = 0;
+  for (int64_t q = a; q < b; ++q) k += sp[q + 1] - sp[q] > 1;
+  int64_t cnt;
+  int64_t e = block_excl(k, &cnt);
+  for (int64_t q = a; q < b; ++q)
+    if (sp[q + 1] - sp[q] > 1) {
+      list[e] = (int32_t)q;
+      lpre[e] = sp[q];
+      ++e;
+    }
+  if (t == kScanThreads - 1) {
+    *count_out = cnt;
+    lpre[cnt] = sp[total];
+    unsigned* sched = reinterpret_cast<unsigned*>(reinterpret_cast<uint8_t*>(count_out) + 64);
+    sched[0] = 0u;  // the GEMV's dynamic schedule (sym.cu)
+    sched[1] = 0u;
+  }
+  __syncthreads();
+  const int64_t w0 = lpre[0], W = lpre[cnt] - w0;
+  for (int g = t; g <= grid; g += kScanThreads) {
+    int64_t r;
+    if (g == grid) {
+      r = cnt;
+    } else {
+      const int64_t target = w0 + W * g / grid;
+      int64_t lo = 0, hi = cnt;
+      while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (lpre[mid] >= target) hi = mid; else lo = mid + 1;
+      }
+      r = lo;
+    }
+    ranges[g] = r;
+  }
+}
+
 __global__ void fill_kernel(uint8_t* p, int64_t n, uint8_t v) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) p[i] = v;
@@ -259,8 +350,12 @@ SparseMask carve_sparse(void* base, int64_t n, int32_t /*d*/) {
 void launch_sparse_prefix(const SparseMask& m, cudaStream_t s) {
   sb_weight_kernel<<<(unsigned)ceil_div(m.n_sb, 256), 256, 0, s>>>(
       m.boxnz, m.nt, m.sb_prefix, const_cast<uint16_t*>(sb_bits(m.sb_prefix, m.nt * kT)));
-  sb_scan_kernel<<<1, kScanThreads, 0, s>>>(m.nt, m.sb_prefix);
   const SbList L = sb_list(m.sb_prefix, m.nt * kT);
+  const int64_t smem = (m.n_sb + 1) * 8;
+  // GPIC_SB_SCAN_SMEM=0: the two global-memory kernels (A/B)
+  const char* se = getenv("GPIC_SB_SCAN_SMEM");
+  const bool staged = smem <= kScanSmemMax && (se == nullptr || atoi(se) != 0);
+  if (!staged) sb_scan_kernel<<<1, kScanThreads, 0, s>>>(m.nt, m.sb_prefix);
   static int sms = 0;
   if (sms == 0) {
     int dev = 0;
@@ -270,12 +365,24 @@ void launch_sparse_prefix(const SparseMask& m, cudaStream_t s) {
   const int grid = sms < kMaxGrid ? sms : kMaxGrid;
   int64_t* ranges = const_cast<int64_t*>(L.ranges);
   cudaMemcpyAsync(ranges, &kGridWords[grid], 8, cudaMemcpyHostToDevice, s);
-  sb_list_kernel<<<1, kScanThreads, 0, s>>>(m.nt, m.sb_prefix, const_cast<int32_t*>(L.list),
-                                            const_cast<int64_t*>(L.lpre),
-                                            const_cast<int64_t*>(L.count), grid, ranges + 1);
+  if (staged) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(sb_scan_list_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)kScanSmemMax);
+      attr = true;
+    }
+    sb_scan_list_smem_kernel<<<1, kScanThreads, smem, s>>>(
+        m.nt, m.sb_prefix, const_cast<int32_t*>(L.list), const_cast<int64_t*>(L.lpre),
+        const_cast<int64_t*>(L.count), grid, ranges + 1);
+  } else {
+    sb_list_kernel<<<1, kScanThreads, 0, s>>>(m.nt, m.sb_prefix, const_cast<int32_t*>(L.list),
+                                              const_cast<int64_t*>(L.lpre),
+                                              const_cast<int64_t*>(L.count), grid, ranges + 1);
+  }
   launch_reduce_terms(m.sb_prefix, m.nt, const_cast<int32_t*>(L.tlist),
                       const_cast<int32_t*>(L.tcount), L.tld, s);
-  count_launch(3);
+  count_launch(staged ? 2 : 3);
 }
 
 void launch_box_fill(const SparseMask& m, uint8_t v, cudaStream_t s) {
