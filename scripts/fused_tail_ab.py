@@ -39,12 +39,14 @@ def child(out):
         else:
             d, kind, p, cfg = gaussian_blobs(5000, 24, 4, seed=3), Cosine(), PicParams(k=4), KernelConfig()
         labels, v, tr, ph = gpu.cluster_fused(d, kind, p, cfg, 0, timed=True)
-        ts, ta = [], []
+        ts, ta, trs = [], [], []
         for _ in range(5):
             ph = gpu.cluster_fused(d, kind, p, cfg, 0, timed=True)[3]
             ts.append(ph["iterate"])
             ta.append(ph["affinity"])
+            trs.append(ph["rowsum"])
         res[name + "_affinity_ms"] = np.median(ta) * 1e3
+        res[name + "_rowsum_ms"] = np.median(trs) * 1e3
         res[name + "_labels"] = labels
         res[name + "_v"] = v
         res[name + "_hist"] = tr.delta_history
@@ -76,5 +78,6 @@ if __name__ == "__main__":
                   f"{float(a[name + '_iterate_ms']):.3f} ms ({knob}={values[0]}) -> "
                   f"{float(b[name + '_iterate_ms']):.3f} ms ({knob}={flag}), "
                   f"T = {len(b[name + '_hist'])}; affinity "
-                  f"{float(a[name + '_affinity_ms']):.3f} -> {float(b[name + '_affinity_ms']):.3f} ms")
+                  f"{float(a[name + '_affinity_ms']):.3f} -> {float(b[name + '_affinity_ms']):.3f} ms; "
+                  f"rowsum {float(a[name + '_rowsum_ms']):.3f} -> {float(b[name + '_rowsum_ms']):.3f} ms")
     sys.exit(0 if ok else 1)
